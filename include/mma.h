@@ -1,0 +1,186 @@
+/*
+ * mma.h — C ABI of the B200-native multipath host<->GPU copy engine (MMA, arXiv 2512.16056).
+ *
+ * Citations: P:NNN = line of the paper's text, S:NNN = line of SPEC.md; the
+ * section is named beside each. DESIGN.md §2 maps every entry point to the paper.
+ *
+ * Conventions for every function below
+ *  - Return value: a cudaError_t value as int (0 = cudaSuccess). Validation happens
+ *    before anything is enqueued: a call that returns an error enqueued nothing.
+ *  - Asynchronous failures (a relay kernel whose bounded spin timed out) are sticky: they
+ *    are returned by the next mma_* call and by mma_get_last_error().
+ *  - Thread safety: every call may be made from any thread. Calls for the same target GPU
+ *    serialise at enqueue time. One engine per process (§5.1.2 "each process in MMA
+ *    maintains its own multipath queue").
+ *  - Pointers are plain host or device virtual addresses (UVA). The library never takes
+ *    ownership of caller memory; it owns its streams, events, staging rings and flags,
+ *    all released by mma_finalize().
+ */
+#ifndef MMA_H
+#define MMA_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct CUstream_st* mma_stream_t;   /* == cudaStream_t; NULL = legacy default stream */
+
+#define MMA_MAX_GPUS 16
+#define MMA_MAX_PATHS 16
+
+typedef enum { MMA_H2D = 0, MMA_D2H = 1 } mma_dir_t;
+
+/* How a path moves host bytes (§3.4.3 uses copy-engine DMA only; the SM
+ * zero-copy mode is north_star (d), chosen per path by measurement). */
+typedef enum {
+    MMA_HOP_AUTO = 0,  /* CE for contiguous copies, ZC for scattered segments */
+    MMA_HOP_CE = 1,    /* copy-engine DMA; a relay stages through its HBM ring */
+    MMA_HOP_ZC = 2     /* SM loads/stores of mapped pinned host memory; a relay writes the
+                          target over NVLink directly (one hop, no staging) */
+} mma_hop_t;
+
+typedef enum { MMA_PATH_DIRECT = 0, MMA_PATH_RELAY = 1 } mma_path_kind_t;
+
+/* One scattered segment (north_star (e); paged KV blocks, §2.1). */
+typedef struct {
+    const void* src;
+    void* dst;
+    size_t bytes;
+} mma_segment_t;
+
+typedef struct {
+    /* chunk size per direction in bytes (§3.4.1 "fixed chunk size"; P:902 tuned
+     * optima 2.81 MB H2D / 5.37 MB D2H). 0 = default (4 MiB). Multiple of 4096. */
+    size_t chunk_bytes[2];
+    /* relay staging slots per ring (P:588-594 dual pipeline = 2). 0 = default (4). */
+    unsigned ring_slots;
+    /* fallback threshold per direction (§3.2, §5.1.3): a copy of B < thr
+     * bytes takes the native single path. (size_t)-1 = always native; 0 = never. */
+    size_t fallback_bytes[2];
+    /* relay GPUs in calibration order; npaths = 0 -> every P2P-capable peer, ascending */
+    int path_gpus[MMA_MAX_PATHS];
+    int npaths;
+    /* extra relay paths through the target GPU itself (loopback rings): a diagnostic
+     * mode that exercises the full relay protocol on a single GPU. Default 0. */
+    int loopback_relays;
+    /* 0 = contiguous (each path carries one contiguous range), 1 = interleaved */
+    int plan_mode;
+    /* hop mode per direction for every path (mma_hop_t), refined per path by
+     * mma_set_path_modes() */
+    int hop_mode[2];
+    /* CTAs per relay ring for the relay kernels; 0 = default (8) */
+    int relay_ctas;
+    /* NUMA placement for mma_host_alloc: 0 = off, 1 = local to the target, 2 = spread */
+    int numa_mode;
+    /* record the per-chunk delivery log (debug; off in timed runs) */
+    int debug_log;
+} mma_config_t;
+
+typedef struct {
+    uint64_t calls, fallbacks, bytes;
+    uint64_t path_bytes[MMA_MAX_PATHS];   /* per path of this target, last direction used */
+    uint64_t path_chunks[MMA_MAX_PATHS];
+    uint64_t relay_bytes;                 /* bytes that crossed NVLink (relayed) */
+    uint64_t kernels;                     /* relay / zero-copy kernel launches */
+    double issue_us;                      /* host time spent enqueueing */
+} mma_stats_t;
+
+/* Fill cfg with defaults (then env MMA_* overrides). */
+int mma_default_config(mma_config_t* cfg);
+
+/* Initialise the engine: enable peer access between P2P-capable GPUs, create path streams,
+ * resolve the stream memory-op entry points. cfg = NULL -> defaults + env. Idempotent
+ * (a second call with a different cfg re-applies the tunables). Lazy on first copy. */
+int mma_init(const mma_config_t* cfg);
+int mma_finalize(void);
+
+/*
+ * Multipath copies with cudaMemcpyAsync(dst, src, bytes, kind, stream) semantics
+ * (§3.1 "preserving the semantics of existing transfer APIs"; P:447-448 workflow):
+ * ordered after prior work on `stream`; later work on `stream` sees the bytes; returns
+ * before completion. The GPU is the one owning the device pointer (not the current
+ * device). H2D: dst is device memory, src host memory; D2H the reverse. bytes = 0 is a
+ * no-op. Falls back to the native single-path copy (byte-identical by definition) when
+ * bytes < fallback threshold, host memory is pageable, the stream is capturing, or the
+ * target has a single path (§3.2).
+ * Errors: cudaErrorInvalidValue (null pointer with bytes > 0, wrong memory kinds),
+ * cudaErrorInvalidDevice, or the CUDA error of an enqueue.
+ */
+int mma_memcpy_h2d(void* dst, const void* src, size_t bytes, mma_stream_t stream);
+int mma_memcpy_d2h(void* dst, const void* src, size_t bytes, mma_stream_t stream);
+
+/*
+ * Scattered variant (north_star (e)): segs[k] copies segs[k].bytes from src to dst. The
+ * segments form one virtual stream v (their concatenation in table order) that is chunked
+ * and planned like a contiguous copy. H2D: every src is pinned host memory, every dst is
+ * device memory of dst_device; D2H the reverse with src_device. The table is copied at
+ * call time. Destinations must be pairwise disjoint (cudaErrorInvalidValue otherwise).
+ */
+int mma_memcpy_h2d_segments(const mma_segment_t* segs, size_t nsegs, int dst_device,
+                            mma_stream_t stream);
+int mma_memcpy_d2h_segments(const mma_segment_t* segs, size_t nsegs, int src_device,
+                            mma_stream_t stream);
+
+/* Paths of a target GPU for a direction: path 0 = its own PCIe link (direct), then relays
+ * in calibration order. Arrays of length cap; *npaths receives the count. */
+int mma_get_paths(int device, mma_dir_t dir, int* gpus, int* kinds, uint32_t* mbps,
+                  int* modes, int cap, int* npaths);
+
+/* Pin the bandwidth vector (integer MB/s, index-aligned with mma_get_paths) used by the
+ * planner; bit-exact plan parity runs pin it (SURVEY §7 hard part 7). 0 drops a path. */
+int mma_set_bandwidth(int device, mma_dir_t dir, const uint32_t* mbps, int npaths);
+
+/* Per-path hop mode (mma_hop_t), index-aligned with mma_get_paths. */
+int mma_set_path_modes(int device, mma_dir_t dir, const int* modes, int npaths);
+
+/* Measure each path's bandwidth with all paths active (a copy of `bytes` split by the
+ * current plan), and store the integer MB/s vector (reading R17: llround). */
+int mma_calibrate(int device, mma_dir_t dir, size_t bytes);
+
+/* The plan the engine would use for a copy of `bytes`: path index per chunk. A fallback
+ * plan is reported as nchunks = 1, path_of_chunk[0] = 0, *fallback = 1. */
+int mma_get_plan(int device, mma_dir_t dir, size_t bytes, uint8_t* path_of_chunk,
+                 size_t cap, size_t* nchunks, int* fallback);
+
+/* The planner alone, on the host (no GPU, no engine state): the assignment for a given
+ * path vector. kinds[p] is MMA_PATH_DIRECT (index 0 only) or MMA_PATH_RELAY; backlog may
+ * be NULL (all 0); mode 0 = contiguous, 1 = interleaved; thr = fallback threshold.
+ * Same outputs as mma_get_plan. Returns cudaErrorInvalidValue on bad arguments. */
+int mma_plan_chunks(const uint32_t* mbps, const int* kinds, const uint64_t* backlog, int npaths,
+                    uint64_t bytes, uint64_t chunk_bytes, uint64_t thr, int mode,
+                    uint8_t* path_of_chunk, size_t cap, size_t* nchunks, int* fallback);
+
+/* Debug: the path that delivered each chunk of the most recent multipath copy to/from
+ * `device`, as written on the GPU by the final hop (needs cfg.debug_log; synchronises). */
+int mma_get_delivery_log(int device, uint8_t* path_of_chunk, size_t cap, size_t* nchunks);
+
+/* Pinned, mapped, portable host memory, NUMA-placed per cfg.numa_mode (C8). */
+int mma_host_alloc(void** ptr, size_t bytes, unsigned flags);
+int mma_host_free(void* ptr);
+
+int mma_get_stats(int device, mma_stats_t* out);
+int mma_reset_stats(int device);
+int mma_get_last_error(void);
+const char* mma_error_string(int err);
+
+/* Verification kernels (C4): the seeded offset-unique pattern of SURVEY §8(c) generated on
+ * the device. Word w (8 bytes, little endian) of the stream = splitmix64((seed << 40) ^ w);
+ * `offset` is the stream byte offset of ptr[0].
+ *  - mma_fill_pattern writes bytes [offset, offset+bytes) of the stream to device ptr.
+ *  - mma_verify_pattern counts mismatching bytes of device ptr against the stream and
+ *    adds them to *mismatches (device memory, uint64).
+ *  - mma_verify_segments does the same per segment: dst[k] (device) holds stream bytes
+ *    [offset[k], offset[k] + bytes[k]); tables are host arrays. */
+int mma_fill_pattern(void* ptr, size_t bytes, uint64_t seed, uint64_t offset, mma_stream_t s);
+int mma_verify_pattern(const void* ptr, size_t bytes, uint64_t seed, uint64_t offset,
+                       uint64_t* mismatches, mma_stream_t s);
+int mma_verify_segments(void* const* dst, const uint64_t* offset, const uint64_t* bytes,
+                        size_t nsegs, uint64_t seed, uint64_t* mismatches, mma_stream_t s);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MMA_H */

@@ -1,0 +1,19 @@
+"""B200-native multipath host<->GPU copy engine (MMA, arXiv 2512.16056).
+
+The product is the C-ABI library libmma.so (include/mma.h); `mma` is its thin binding.
+Importing this package loads the library first so that its constructor raises
+CUDA_DEVICE_MAX_CONNECTIONS before any CUDA context exists.
+"""
+from . import mma  # noqa: F401
+from .mma import (  # noqa: F401
+    H2D, D2H, HOP_AUTO, HOP_CE, HOP_ZC, PATH_DIRECT, PATH_RELAY, Config, MMAError,
+    calibrate, default_config, finalize, get_delivery_log, get_last_error, get_paths, get_plan,
+    get_stats, host_alloc, host_array, host_free, init, make_segments, memcpy_d2h,
+    memcpy_d2h_segments, memcpy_h2d, memcpy_h2d_segments, plan_chunks, reset_stats,
+    set_bandwidth, set_path_modes, fill_pattern, verify_pattern, verify_segments,
+)
+
+try:  # load early when built (the build check imports before building otherwise)
+    mma.lib()
+except ImportError:
+    pass

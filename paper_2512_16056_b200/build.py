@@ -1,0 +1,70 @@
+"""Build libmma.so in-tree with nvcc for sm_100a (no torch, no JIT cache).
+
+    python -m paper_2512_16056_b200.build [--force]
+"""
+from __future__ import annotations
+
+import os
+import subprocess
+import sys
+from pathlib import Path
+
+PKG = Path(__file__).resolve().parent
+ROOT = PKG.parent
+CSRC = PKG / "csrc"
+LIB = PKG / "libmma.so"
+NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
+
+SOURCES = [
+    CSRC / "engine.cpp",
+    CSRC / "planner.cpp",
+    CSRC / "hostmem.cpp",
+    CSRC / "kernels" / "relay.cu",
+    CSRC / "kernels" / "zerocopy.cu",
+    CSRC / "kernels" / "verify.cu",
+]
+HEADERS = [ROOT / "include" / "mma.h", CSRC / "engine.h", CSRC / "kargs.h", CSRC / "planner.h",
+           CSRC / "kernels" / "copy.cuh"]
+
+FLAGS = [
+    "-O3", "-std=c++17", "-lineinfo",
+    "-gencode", "arch=compute_100a,code=sm_100a",
+    "-Xcompiler", "-fPIC,-Wall",
+    "-Xptxas", "-v" if os.environ.get("MMA_PTXAS_V") else "-O3",
+    "-I", str(ROOT / "include"),
+    "--expt-relaxed-constexpr", "--extended-lambda",
+]
+
+
+def stale() -> bool:
+    if not LIB.exists():
+        return True
+    t = LIB.stat().st_mtime
+    return any(p.stat().st_mtime > t for p in SOURCES + HEADERS + [Path(__file__)])
+
+
+def build(force: bool = False, verbose: bool = False) -> Path:
+    if not force and not stale():
+        return LIB
+    objdir = PKG / "build"
+    objdir.mkdir(exist_ok=True)
+    objs = []
+    for src in SOURCES:
+        obj = objdir / (src.stem + ".o")
+        cmd = [NVCC, *FLAGS, "-c", str(src), "-o", str(obj)]
+        if src.suffix == ".cpp":
+            cmd = [NVCC, *FLAGS, "-x", "cu", "-c", str(src), "-o", str(obj)]
+        if verbose:
+            print(" ".join(cmd))
+        subprocess.check_call(cmd)
+        objs.append(str(obj))
+    tmp = LIB.with_suffix(".so.tmp")
+    subprocess.check_call([NVCC, "-shared", "-gencode", "arch=compute_100a,code=sm_100a",
+                           "-cudart", "static", "-o", str(tmp), *objs, "-ldl", "-lpthread", "-lrt"])
+    os.replace(tmp, LIB)
+    return LIB
+
+
+if __name__ == "__main__":
+    build(force="--force" in sys.argv, verbose=True)
+    print(LIB)

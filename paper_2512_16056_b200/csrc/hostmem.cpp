@@ -1,0 +1,102 @@
+// hostmem.cpp — C8: NUMA-aware pinned host buffers (layer L1).
+//
+// A multipath copy reads host DRAM through every participating GPU's PCIe link; the paper
+// attributes its 6-path plateau to the cross-NUMA link (§5.1.1). Buffers from
+// mma_host_alloc are anonymous mappings whose pages are bound with mbind(2) (raw syscall:
+// libnuma is absent) to the requested node(s) before first touch, then registered with
+// cudaHostRegister(PORTABLE | MAPPED) so every GPU's copy engine and SMs can reach them.
+// numa_mode: 0 = kernel default placement, 1 = node `node0`, 2 = interleave across nodes.
+#include <cuda_runtime.h>
+#include <sys/mman.h>
+#include <sys/syscall.h>
+#include <unistd.h>
+
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <mutex>
+
+#include "engine.h"
+
+namespace mma {
+
+namespace {
+std::mutex g_mu;
+std::map<void*, size_t> g_allocs;   // base -> mapped length
+
+constexpr int kMpolBind = 2;
+constexpr int kMpolInterleave = 3;
+
+int numa_nodes()
+{
+    int n = 0;
+    for (int i = 0; i < 64; i++) {
+        char path[96];
+        snprintf(path, sizeof path, "/sys/devices/system/node/node%d", i);
+        if (access(path, F_OK) == 0) n = i + 1;
+    }
+    return n < 1 ? 1 : n;
+}
+}  // namespace
+
+int host_alloc(void** ptr, size_t bytes, int numa_mode, int node0)
+{
+    if (!ptr) return cudaErrorInvalidValue;
+    *ptr = nullptr;
+    if (bytes == 0) return cudaSuccess;
+    const size_t align = 2u << 20;
+    const size_t len = (bytes + align - 1) / align * align;
+    void* p = mmap(nullptr, len, PROT_READ | PROT_WRITE, MAP_PRIVATE | MAP_ANONYMOUS, -1, 0);
+    if (p == MAP_FAILED) return cudaErrorMemoryAllocation;
+    madvise(p, len, MADV_HUGEPAGE);
+    const int nodes = numa_nodes();
+    if (numa_mode != 0 && nodes > 1) {
+        unsigned long mask[4] = {0, 0, 0, 0};
+        int mode = kMpolBind;
+        if (numa_mode == 2) {
+            mode = kMpolInterleave;
+            for (int i = 0; i < nodes && i < 256; i++) mask[i / 64] |= 1ul << (i % 64);
+        } else {
+            int nd = node0 < 0 ? 0 : node0 % nodes;
+            mask[nd / 64] |= 1ul << (nd % 64);
+        }
+        syscall(SYS_mbind, p, len, mode, mask, 256ul, 0u);   // best effort
+    }
+    memset(p, 0, len);   // first touch places the pages
+    cudaError_t e = cudaHostRegister(p, len, cudaHostRegisterPortable | cudaHostRegisterMapped);
+    if (e != cudaSuccess) {
+        munmap(p, len);
+        return e;
+    }
+    std::lock_guard<std::mutex> g(g_mu);
+    g_allocs[p] = len;
+    *ptr = p;
+    return cudaSuccess;
+}
+
+int host_free(void* ptr)
+{
+    if (!ptr) return cudaSuccess;
+    size_t len;
+    {
+        std::lock_guard<std::mutex> g(g_mu);
+        auto it = g_allocs.find(ptr);
+        if (it == g_allocs.end()) return cudaErrorInvalidValue;
+        len = it->second;
+        g_allocs.erase(it);
+    }
+    cudaError_t e = cudaHostUnregister(ptr);
+    munmap(ptr, len);
+    return e;
+}
+
+// NUMA node of page `p` (move_pages with nodes = NULL queries), or -1.
+int host_page_node(const void* p)
+{
+    void* pages[1] = {const_cast<void*>(p)};
+    int status[1] = {-1};
+    if (syscall(SYS_move_pages, 0, 1ul, pages, nullptr, status, 0) != 0) return -1;
+    return status[0];
+}
+
+}  // namespace mma

@@ -1,0 +1,43 @@
+// zerocopy.cu — C2/C3: SM zero-copy movement over one path (north_star (d), SURVEY §8(a)
+// rows a7 and a10).
+//
+// The kernel runs on the path's GPU and moves the chunks that path carries directly
+// between mapped pinned host memory and device memory with 16-byte coalesced loads and
+// stores; nothing is staged. Launched on
+//   - the target GPU d: the direct path (H2D host->d HBM, D2H d HBM->host);
+//   - a relay GPU r: a one-hop relay (H2D: loads of host memory cross r's PCIe link,
+//     stores to d's HBM cross NVLink; D2H the reverse), which needs no ring and no flags.
+// For scattered segments (paged KV blocks) it gathers host blocks and scatters them to
+// device blocks in one launch, where the copy engine needs one DMA per block.
+#include <cuda_runtime.h>
+
+#include "copy.cuh"
+
+namespace mma {
+
+__global__ void __launch_bounds__(kThreads) zc_copy_kernel(const __grid_constant__ ZcLaunchArg A)
+{
+    const uint64_t U = A.unit_bytes, C = A.v.C, B = A.v.B;
+    const uint64_t upc = (C + U - 1) / U;
+    const uint64_t nunits = A.chunks.count * upc;
+    for (uint64_t u = blockIdx.x; u < nunits; u += gridDim.x) {
+        const uint64_t j = u / upc, k = u % upc;
+        const uint64_t i = chunk_index(A.chunks, j);
+        const uint64_t off = i * C;
+        const uint64_t len = (B - off < C) ? B - off : C;
+        const uint64_t lo = k * U;
+        if (lo >= len) continue;
+        const uint64_t hi = (lo + U < len) ? lo + U : len;
+        v_copy<V_DIRECT>(A.v, off + lo, off + hi, nullptr);
+        if (A.log && k == 0 && threadIdx.x == 0) A.log[i] = (uint8_t)A.path;
+    }
+}
+
+cudaError_t launch_zc(const ZcLaunchArg& a, unsigned grid, cudaStream_t s)
+{
+    if (grid == 0) return cudaSuccess;
+    zc_copy_kernel<<<grid, kThreads, 0, s>>>(a);
+    return cudaGetLastError();
+}
+
+}  // namespace mma

@@ -1,0 +1,30 @@
+// planner.h — chunk -> path assignment from a measured bandwidth vector (C5, layer L2).
+// Pure C++, no CUDA. Written from SURVEY §8(c) steps 1-3 and DESIGN.md readings R1-R6,
+// independently of oracle/ (the two share no code; tests compare them bit for bit).
+#pragma once
+#include <stdint.h>
+
+#include <vector>
+
+namespace mma {
+
+struct PlanPath {
+    bool direct;        // the target's own link; only legal at index 0
+    uint32_t mbps;      // integer MB/s; 0 drops the path
+    uint64_t backlog;   // bytes already queued on the path
+};
+
+enum PlanMode { PLAN_CONTIGUOUS = 0, PLAN_INTERLEAVED = 1 };
+
+struct Plan {
+    bool fallback = false;          // one piece [0, B) on path 0 (native)
+    uint64_t n = 0;                 // chunks
+    std::vector<uint8_t> path;      // path of each chunk
+    std::vector<uint64_t> count;    // chunks per path
+};
+
+// Returns 0 or a negative errno (-22 invalid arguments / no usable path).
+int make_plan(const PlanPath* paths, int npaths, uint64_t B, uint64_t C, uint64_t thr,
+              int mode, Plan& out);
+
+}  // namespace mma

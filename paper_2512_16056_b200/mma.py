@@ -1,0 +1,299 @@
+"""Python binding of libmma.so (include/mma.h): argument marshalling only.
+
+Every byte of a copy is moved by the library's CUDA path (copy engines + the sm_100a
+kernels in csrc/kernels); nothing here computes. torch is used only to read tensor data
+pointers and CUDA stream handles. If libmma.so is missing the import fails loudly: there
+is no CPU fallback.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from pathlib import Path
+
+PKG = Path(__file__).resolve().parent
+LIB_PATH = PKG / "libmma.so"
+
+H2D, D2H = 0, 1
+HOP_AUTO, HOP_CE, HOP_ZC = 0, 1, 2
+PATH_DIRECT, PATH_RELAY = 0, 1
+MAX_PATHS = 16
+ERR_RELAY_TIMEOUT = 2001
+
+SYMBOLS = [
+    "mma_default_config", "mma_init", "mma_finalize", "mma_memcpy_h2d", "mma_memcpy_d2h",
+    "mma_memcpy_h2d_segments", "mma_memcpy_d2h_segments", "mma_get_paths", "mma_set_bandwidth",
+    "mma_set_path_modes", "mma_calibrate", "mma_get_plan", "mma_plan_chunks",
+    "mma_get_delivery_log", "mma_host_alloc", "mma_host_free", "mma_get_stats",
+    "mma_reset_stats", "mma_get_last_error", "mma_error_string", "mma_fill_pattern",
+    "mma_verify_pattern", "mma_verify_segments",
+]
+
+
+class Config(C.Structure):
+    _fields_ = [
+        ("chunk_bytes", C.c_size_t * 2),
+        ("ring_slots", C.c_uint),
+        ("fallback_bytes", C.c_size_t * 2),
+        ("path_gpus", C.c_int * MAX_PATHS),
+        ("npaths", C.c_int),
+        ("loopback_relays", C.c_int),
+        ("plan_mode", C.c_int),
+        ("hop_mode", C.c_int * 2),
+        ("relay_ctas", C.c_int),
+        ("numa_mode", C.c_int),
+        ("debug_log", C.c_int),
+    ]
+
+
+class Stats(C.Structure):
+    _fields_ = [
+        ("calls", C.c_uint64), ("fallbacks", C.c_uint64), ("bytes", C.c_uint64),
+        ("path_bytes", C.c_uint64 * MAX_PATHS), ("path_chunks", C.c_uint64 * MAX_PATHS),
+        ("relay_bytes", C.c_uint64), ("kernels", C.c_uint64), ("issue_us", C.c_double),
+    ]
+
+
+class Segment(C.Structure):
+    _fields_ = [("src", C.c_void_p), ("dst", C.c_void_p), ("bytes", C.c_size_t)]
+
+
+class MMAError(RuntimeError):
+    def __init__(self, code: int, what: str):
+        super().__init__(f"{what}: {lib().mma_error_string(code).decode()} ({code})")
+        self.code = code
+
+
+_lib = None
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        if not LIB_PATH.exists():
+            raise ImportError(f"{LIB_PATH} is missing: build it with "
+                              "`python -m paper_2512_16056_b200.build` (no CPU fallback exists)")
+        L = C.CDLL(str(LIB_PATH))
+        vp, sz, u64p = C.c_void_p, C.c_size_t, C.POINTER(C.c_uint64)
+        L.mma_default_config.argtypes = [C.POINTER(Config)]
+        L.mma_init.argtypes = [C.POINTER(Config)]
+        L.mma_memcpy_h2d.argtypes = [vp, vp, sz, vp]
+        L.mma_memcpy_d2h.argtypes = [vp, vp, sz, vp]
+        L.mma_memcpy_h2d_segments.argtypes = [C.POINTER(Segment), sz, C.c_int, vp]
+        L.mma_memcpy_d2h_segments.argtypes = [C.POINTER(Segment), sz, C.c_int, vp]
+        L.mma_get_paths.argtypes = [C.c_int, C.c_int, vp, vp, vp, vp, C.c_int, C.POINTER(C.c_int)]
+        L.mma_set_bandwidth.argtypes = [C.c_int, C.c_int, vp, C.c_int]
+        L.mma_set_path_modes.argtypes = [C.c_int, C.c_int, vp, C.c_int]
+        L.mma_calibrate.argtypes = [C.c_int, C.c_int, sz]
+        L.mma_get_plan.argtypes = [C.c_int, C.c_int, sz, vp, sz, C.POINTER(sz), C.POINTER(C.c_int)]
+        L.mma_plan_chunks.argtypes = [vp, vp, vp, C.c_int, C.c_uint64, C.c_uint64, C.c_uint64,
+                                      C.c_int, vp, sz, C.POINTER(sz), C.POINTER(C.c_int)]
+        L.mma_get_delivery_log.argtypes = [C.c_int, vp, sz, C.POINTER(sz)]
+        L.mma_host_alloc.argtypes = [C.POINTER(vp), sz, C.c_uint]
+        L.mma_host_free.argtypes = [vp]
+        L.mma_get_stats.argtypes = [C.c_int, C.POINTER(Stats)]
+        L.mma_reset_stats.argtypes = [C.c_int]
+        L.mma_error_string.restype = C.c_char_p
+        L.mma_error_string.argtypes = [C.c_int]
+        L.mma_fill_pattern.argtypes = [vp, sz, C.c_uint64, C.c_uint64, vp]
+        L.mma_verify_pattern.argtypes = [vp, sz, C.c_uint64, C.c_uint64, vp, vp]
+        L.mma_verify_segments.argtypes = [vp, vp, vp, sz, C.c_uint64, vp, vp]
+        _lib = L
+    return _lib
+
+
+def _check(rc: int, what: str) -> None:
+    if rc != 0:
+        raise MMAError(rc, what)
+
+
+def _ptr(x) -> int:
+    if x is None:
+        return 0
+    if isinstance(x, int):
+        return x
+    if hasattr(x, "data_ptr"):
+        return int(x.data_ptr())
+    if hasattr(x, "ctypes"):
+        return int(x.ctypes.data)
+    raise TypeError(f"cannot take a pointer of {type(x)}")
+
+
+def _nbytes(x) -> int:
+    if hasattr(x, "untyped_storage") and hasattr(x, "element_size"):
+        return x.numel() * x.element_size()
+    if hasattr(x, "nbytes"):
+        return int(x.nbytes)
+    raise TypeError("pass nbytes explicitly")
+
+
+def _stream(stream, device=None) -> int:
+    if stream is None:
+        import torch
+        return int(torch.cuda.current_stream(device).cuda_stream)
+    if isinstance(stream, int):
+        return stream
+    return int(stream.cuda_stream)
+
+
+def default_config() -> Config:
+    c = Config()
+    _check(lib().mma_default_config(C.byref(c)), "mma_default_config")
+    return c
+
+
+def init(cfg: Config | None = None) -> None:
+    _check(lib().mma_init(C.byref(cfg) if cfg is not None else None), "mma_init")
+
+
+def finalize() -> None:
+    _check(lib().mma_finalize(), "mma_finalize")
+
+
+def _dev_of(t):
+    return t.device if hasattr(t, "device") and getattr(t.device, "type", "") == "cuda" else None
+
+
+def memcpy_h2d(dst, src, nbytes: int | None = None, stream=None) -> None:
+    """dst: CUDA tensor or device pointer; src: pinned CPU tensor / ndarray or pointer."""
+    n = _nbytes(src) if nbytes is None else int(nbytes)
+    _check(lib().mma_memcpy_h2d(_ptr(dst), _ptr(src), n, _stream(stream, _dev_of(dst))), "mma_memcpy_h2d")
+
+
+def memcpy_d2h(dst, src, nbytes: int | None = None, stream=None) -> None:
+    n = _nbytes(src) if nbytes is None else int(nbytes)
+    _check(lib().mma_memcpy_d2h(_ptr(dst), _ptr(src), n, _stream(stream, _dev_of(src))), "mma_memcpy_d2h")
+
+
+def make_segments(src_ptrs, dst_ptrs, lens):
+    """Segment table from three integer sequences / numpy arrays."""
+    import numpy as np
+    n = len(lens)
+    arr = (Segment * max(n, 1))()
+    view = np.frombuffer(arr, dtype=np.uint64, count=3 * max(n, 1)).reshape(-1, 3)
+    if n:
+        view[:n, 0] = np.asarray(src_ptrs, dtype=np.uint64)
+        view[:n, 1] = np.asarray(dst_ptrs, dtype=np.uint64)
+        view[:n, 2] = np.asarray(lens, dtype=np.uint64)
+    return arr, n
+
+
+def memcpy_h2d_segments(segs, nsegs: int, dst_device: int, stream=None) -> None:
+    _check(lib().mma_memcpy_h2d_segments(segs, nsegs, dst_device, _stream(stream, dst_device)),
+           "mma_memcpy_h2d_segments")
+
+
+def memcpy_d2h_segments(segs, nsegs: int, src_device: int, stream=None) -> None:
+    _check(lib().mma_memcpy_d2h_segments(segs, nsegs, src_device, _stream(stream, src_device)),
+           "mma_memcpy_d2h_segments")
+
+
+def get_paths(device: int, direction: int):
+    gpus = (C.c_int * MAX_PATHS)()
+    kinds = (C.c_int * MAX_PATHS)()
+    mbps = (C.c_uint32 * MAX_PATHS)()
+    modes = (C.c_int * MAX_PATHS)()
+    n = C.c_int()
+    _check(lib().mma_get_paths(device, direction, gpus, kinds, mbps, modes, MAX_PATHS, C.byref(n)),
+           "mma_get_paths")
+    return [dict(gpu=gpus[i], kind=kinds[i], mbps=mbps[i], mode=modes[i]) for i in range(n.value)]
+
+
+def set_bandwidth(device: int, direction: int, mbps) -> None:
+    arr = (C.c_uint32 * len(mbps))(*[int(x) for x in mbps])
+    _check(lib().mma_set_bandwidth(device, direction, arr, len(mbps)), "mma_set_bandwidth")
+
+
+def set_path_modes(device: int, direction: int, modes) -> None:
+    arr = (C.c_int * len(modes))(*[int(x) for x in modes])
+    _check(lib().mma_set_path_modes(device, direction, arr, len(modes)), "mma_set_path_modes")
+
+
+def calibrate(device: int, direction: int, nbytes: int = 256 << 20) -> None:
+    _check(lib().mma_calibrate(device, direction, nbytes), "mma_calibrate")
+
+
+def get_plan(device: int, direction: int, nbytes: int):
+    """Returns (path_of_chunk bytes, fallback bool)."""
+    n = C.c_size_t()
+    fb = C.c_int()
+    _check(lib().mma_get_plan(device, direction, nbytes, None, 0, C.byref(n), C.byref(fb)), "mma_get_plan")
+    buf = (C.c_uint8 * max(n.value, 1))()
+    _check(lib().mma_get_plan(device, direction, nbytes, buf, n.value, C.byref(n), C.byref(fb)), "mma_get_plan")
+    return bytes(buf[: n.value]), bool(fb.value)
+
+
+def plan_chunks(mbps, kinds, nbytes: int, chunk: int, thr: int = 0, mode: int = 0, backlog=None):
+    """Host-only planner (no GPU): returns (rc, path_of_chunk bytes, fallback)."""
+    P = len(mbps)
+    m = (C.c_uint32 * P)(*[int(x) for x in mbps])
+    k = (C.c_int * P)(*[int(x) for x in kinds])
+    b = (C.c_uint64 * P)(*[int(x) for x in backlog]) if backlog is not None else None
+    n = C.c_size_t()
+    fb = C.c_int()
+    rc = lib().mma_plan_chunks(m, k, b, P, nbytes, chunk, thr, mode, None, 0, C.byref(n), C.byref(fb))
+    if rc:
+        return rc, b"", False
+    buf = (C.c_uint8 * max(n.value, 1))()
+    rc = lib().mma_plan_chunks(m, k, b, P, nbytes, chunk, thr, mode, buf, n.value, C.byref(n), C.byref(fb))
+    return rc, bytes(buf[: n.value]), bool(fb.value)
+
+
+def get_delivery_log(device: int):
+    n = C.c_size_t()
+    _check(lib().mma_get_delivery_log(device, None, 0, C.byref(n)), "mma_get_delivery_log")
+    buf = (C.c_uint8 * max(n.value, 1))()
+    _check(lib().mma_get_delivery_log(device, buf, n.value, C.byref(n)), "mma_get_delivery_log")
+    return bytes(buf[: n.value])
+
+
+def host_alloc(nbytes: int) -> int:
+    p = C.c_void_p()
+    _check(lib().mma_host_alloc(C.byref(p), nbytes, 0), "mma_host_alloc")
+    return int(p.value or 0)
+
+
+def host_free(ptr: int) -> None:
+    _check(lib().mma_host_free(ptr), "mma_host_free")
+
+
+def host_array(ptr: int, nbytes: int):
+    """A numpy uint8 view of library-owned pinned memory (no copy)."""
+    import numpy as np
+    return np.ctypeslib.as_array((C.c_uint8 * nbytes).from_address(ptr))
+
+
+def get_stats(device: int) -> dict:
+    s = Stats()
+    _check(lib().mma_get_stats(device, C.byref(s)), "mma_get_stats")
+    return dict(calls=s.calls, fallbacks=s.fallbacks, bytes=s.bytes,
+                path_bytes=list(s.path_bytes), path_chunks=list(s.path_chunks),
+                relay_bytes=s.relay_bytes, kernels=s.kernels, issue_us=s.issue_us)
+
+
+def reset_stats(device: int) -> None:
+    _check(lib().mma_reset_stats(device), "mma_reset_stats")
+
+
+def get_last_error() -> int:
+    return int(lib().mma_get_last_error())
+
+
+def fill_pattern(dst, nbytes: int, seed: int, offset: int = 0, stream=None) -> None:
+    _check(lib().mma_fill_pattern(_ptr(dst), nbytes, seed, offset, _stream(stream, _dev_of(dst))),
+           "mma_fill_pattern")
+
+
+def verify_pattern(src, nbytes: int, seed: int, offset: int, counter, stream=None) -> None:
+    """Adds the number of mismatching bytes to `counter` (a CUDA uint64/int64 tensor)."""
+    _check(lib().mma_verify_pattern(_ptr(src), nbytes, seed, offset, _ptr(counter),
+                                    _stream(stream, _dev_of(src))), "mma_verify_pattern")
+
+
+def verify_segments(dst_ptrs, offsets, lens, seed: int, counter, stream=None) -> None:
+    import numpy as np
+    d = np.ascontiguousarray(dst_ptrs, dtype=np.uint64)
+    o = np.ascontiguousarray(offsets, dtype=np.uint64)
+    n = np.ascontiguousarray(lens, dtype=np.uint64)
+    _check(lib().mma_verify_segments(d.ctypes.data, o.ctypes.data, n.ctypes.data, d.size, seed,
+                                     _ptr(counter), _stream(stream, _dev_of(counter))),
+           "mma_verify_segments")

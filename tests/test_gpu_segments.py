@@ -1,0 +1,169 @@
+"""GPU parity of the scattered-segment variant (north_star (e)): a paged prefix-cache KV
+fetch (config 3 shape: Llama-3-8B bf16 KV, 16-token blocks, 32 KiB segments scattered in a
+pinned host pool) and its D2H offload mirror, against the oracle moving the same segment
+table, byte for byte including untouched bytes of the pool and cache."""
+import numpy as np
+import pytest
+
+import mma_inputs
+from mma_inputs import workloads as W
+
+from gpu_util import configure
+
+torch = pytest.importorskip("torch")
+pytestmark = [pytest.mark.gpu, pytest.mark.timeout(600)]
+
+MiB = 1 << 20
+
+
+@pytest.fixture(scope="module")
+def mma():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import os
+    os.environ.setdefault("MMA_SPIN_TIMEOUT_MS", "8000")
+    import paper_2512_16056_b200 as m
+    yield m
+    m.finalize()
+
+
+def _kv(tokens, seed=0x4D4D41 + 3):
+    shape = W.scaled_kv(tokens)
+    ho, do, sb, hpool, dbytes = W.kv_segments(shape, seed)
+    return shape, ho, do, sb, hpool, dbytes
+
+
+def _oracle_segments(orc, src_base_np, dst_np, s_off, d_off, lens, C, bw, path, S=2):
+    segs, n = orc.segments_from_arrays(src_base_np.ctypes.data + s_off, dst_np.ctypes.data + d_off, lens)
+    assert orc.move(segs, n, C, bw, path, S=S) == 0
+
+
+CASES = [
+    # tokens, chunk, loopback relays, plan mode, hop
+    (256, MiB, 0, 0, 2),         # direct only, SM gather/scatter (the N=1 bench path)
+    (256, MiB, 0, 0, 1),         # direct only, copy-engine batch
+    (512, MiB, 1, 1, 1),         # ring: batch pack into slots + relay kernel unpack
+    (512, MiB, 2, 0, 2),         # one-hop zero-copy relays
+    (272, 192 << 10, 2, 1, 1),   # chunk not a multiple of the segment: pieces split
+    (272, 192 << 10, 1, 1, 2),
+]
+
+
+@pytest.mark.parametrize("tokens,C,lb,mode,hop", CASES)
+def test_kv_fetch_h2d(mma, orc, tokens, C, lb, mode, hop):
+    configure(mma, loopback=lb, chunk=C, slots=2, plan_mode=mode, hop=(hop, hop))
+    bw = [1] * (1 + lb)
+    mma.set_bandwidth(0, mma.H2D, bw)
+    shape, ho, do, sb, hpool, dbytes = _kv(tokens)
+    host = torch.empty(hpool, dtype=torch.uint8).pin_memory()
+    mma_inputs.fill_pattern(host.numpy(), 21)
+    cache = torch.full((dbytes,), 0xA5, dtype=torch.uint8, device="cuda")
+    lens = np.full(len(ho), sb, dtype=np.int64)
+    segs, n = mma.make_segments(host.data_ptr() + ho, cache.data_ptr() + do, lens)
+    B = int(lens.sum())
+    rc, path, _, fb = orc.plan(bw, B, C, 0, mode)
+    got_path, got_fb = mma.get_plan(0, mma.H2D, B)
+    assert got_path == path.tobytes() and got_fb == fb
+    mma.memcpy_h2d_segments(segs, n, 0)
+    torch.cuda.synchronize()
+    assert mma.get_last_error() == 0
+    exp = np.full(dbytes, 0xA5, dtype=np.uint8)
+    _oracle_segments(orc, host.numpy(), exp, ho, do, lens, C, bw, path)
+    assert np.array_equal(cache.cpu().numpy(), exp)
+    if not fb:
+        assert mma.get_delivery_log(0) == path.tobytes()
+
+
+@pytest.mark.parametrize("tokens,C,lb,mode,hop", CASES)
+def test_kv_offload_d2h(mma, orc, tokens, C, lb, mode, hop):
+    configure(mma, loopback=lb, chunk=C, slots=2, plan_mode=mode, hop=(hop, hop))
+    bw = [1] * (1 + lb)
+    mma.set_bandwidth(0, mma.D2H, bw)
+    shape, ho, do, sb, hpool, dbytes = _kv(tokens, seed=99)
+    cache_host = mma_inputs.pattern_bytes(33, dbytes)
+    cache = torch.from_numpy(cache_host).to("cuda")
+    host = torch.full((hpool,), 0xA5, dtype=torch.uint8).pin_memory()
+    lens = np.full(len(ho), sb, dtype=np.int64)
+    segs, n = mma.make_segments(cache.data_ptr() + do, host.data_ptr() + ho, lens)
+    B = int(lens.sum())
+    rc, path, _, fb = orc.plan(bw, B, C, 0, mode)
+    assert mma.get_plan(0, mma.D2H, B)[0] == path.tobytes()
+    mma.memcpy_d2h_segments(segs, n, 0)
+    torch.cuda.synchronize()
+    exp = np.full(hpool, 0xA5, dtype=np.uint8)
+    _oracle_segments(orc, cache_host, exp, do, ho, lens, C, bw, path)
+    assert np.array_equal(host.numpy(), exp)
+
+
+def test_irregular_segments(mma, orc):
+    """Odd lengths, odd alignments, empty segments, destinations out of order."""
+    rng = np.random.default_rng(8)
+    nseg = 300
+    lens = rng.integers(0, 50000, nseg)
+    lens[::17] = 0
+    pool = torch.empty(int(lens.sum()) * 2 + 1000, dtype=torch.uint8).pin_memory()
+    mma_inputs.fill_pattern(pool.numpy(), 4)
+    s_off = rng.integers(0, pool.numel() - 50000, nseg)
+    order = rng.permutation(nseg)
+    d_off = np.zeros(nseg, np.int64)
+    pos = 3
+    for k in order:
+        d_off[k] = pos
+        pos += int(lens[k]) + int(rng.integers(0, 40))
+    for hop, lb, mode in [(1, 1, 1), (2, 2, 0), (2, 0, 1)]:
+        configure(mma, loopback=lb, chunk=64 << 10, slots=2, plan_mode=mode, hop=(hop, hop))
+        bw = [2] + [1] * lb
+        mma.set_bandwidth(0, mma.H2D, bw)
+        dev = torch.full((pos + 100,), 0xA5, dtype=torch.uint8, device="cuda")
+        segs, n = mma.make_segments(pool.data_ptr() + s_off, dev.data_ptr() + d_off, lens)
+        mma.memcpy_h2d_segments(segs, n, 0)
+        torch.cuda.synchronize()
+        B = int(lens.sum())
+        rc, path, _, _ = orc.plan(bw, B, 64 << 10, 0, mode)
+        exp = np.full(pos + 100, 0xA5, np.uint8)
+        _oracle_segments(orc, pool.numpy(), exp, s_off, d_off, lens, 64 << 10, bw, path)
+        assert np.array_equal(dev.cpu().numpy(), exp), (hop, lb, mode)
+
+
+def test_overlapping_destinations_rejected(mma):
+    configure(mma, loopback=0, chunk=MiB)
+    host = torch.empty(MiB, dtype=torch.uint8).pin_memory()
+    dev = torch.empty(MiB, dtype=torch.uint8, device="cuda")
+    segs, n = mma.make_segments([host.data_ptr()] * 2, [dev.data_ptr(), dev.data_ptr() + 100],
+                                [200, 200])
+    with pytest.raises(mma.MMAError) as e:
+        mma.memcpy_h2d_segments(segs, n, 0)
+    assert e.value.code == 1
+
+
+@pytest.mark.timeout(900)
+def test_full_size_kv_fetch(mma, orc):
+    """BASELINE config 3 at full size (131,072 x 32 KiB = 4 GiB from an 8 GiB pool) in the
+    bench's launch configuration: every byte checked on the device against the seeded
+    pattern, and sampled segments compared with the oracle moving those segments."""
+    configure(mma, loopback=0, chunk=4 * MiB, plan_mode=0, hop=(0, 0), thr=8 * MiB, debug=0)
+    shape, ho, do, sb, hpool, dbytes = _kv(32768)
+    host = torch.empty(hpool, dtype=torch.uint8).pin_memory()
+    seed = 0x4D4D41 + 3
+    hd = torch.empty(hpool, dtype=torch.uint8, device="cuda")
+    mma.fill_pattern(hd, hpool, seed, 0)
+    host.copy_(hd)
+    del hd
+    cache = torch.full((dbytes,), 0xA5, dtype=torch.uint8, device="cuda")
+    lens = np.full(len(ho), sb, dtype=np.int64)
+    segs, n = mma.make_segments(host.data_ptr() + ho, cache.data_ptr() + do, lens)
+    mma.memcpy_h2d_segments(segs, n, 0)
+    torch.cuda.synchronize()
+    cnt = torch.zeros(1, dtype=torch.int64, device="cuda")
+    mma.verify_segments(cache.data_ptr() + do, ho, lens, seed, cnt)
+    torch.cuda.synchronize()
+    assert int(cnt.item()) == 0
+    rng = np.random.default_rng(0)
+    pick = rng.choice(len(ho), 64, replace=False)
+    hnp = host.numpy()
+    for k in pick:
+        exp = np.zeros(sb, np.uint8)
+        segs1, n1 = orc.segments_from_arrays([hnp.ctypes.data + int(ho[k])], [exp.ctypes.data], [sb])
+        assert orc.move(segs1, n1, sb, [1], np.zeros(1, np.uint8)) == 0
+        got = cache[int(do[k]):int(do[k]) + sb].cpu().numpy()
+        assert np.array_equal(got, exp)
