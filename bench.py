@@ -1,0 +1,527 @@
+#!/usr/bin/env python3
+"""bench.py — MMA multipath host<->GPU copy on B200 (BASELINE.json metric: "H2D/D2H GB/s per
+target GPU vs path count (1/2/4/8) and % of roofline").
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl mma|reference]
+                    [--workload kv|contig] [--bytes B]
+
+One step = one pass of the whole hot path over one batch: the prefix-cache KV fetch of
+BASELINE config 3 (131,072 scattered 32 KiB segments = 4 GiB, host pool -> GPU 0 paged
+cache) followed by its offload mirror (GPU 0 cache -> host pool), both through the C ABI
+(mma_memcpy_h2d_segments / mma_memcpy_d2h_segments) with every path of the set active.
+GPU 0 is the target; the k = N path GPUs are GPU 0 (direct) and GPUs 1..N-1 (relays). The
+engine is one process driving all paths (§5.1.2 "each process in MMA maintains its
+own multipath queue"); under torchrun, ranks > 0 only join the CPU (gloo) barriers so
+that no other process time-slices the relay GPUs. Total work is fixed as N grows:
+"scaling": "strong". value = bytes moved per step / device time per step (GB/s, 1e9).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "H2D/D2H GB/s per target GPU vs path count (1/2/4/8) and % of roofline"
+MiB, GiB = 1 << 20, 1 << 30
+SEED = 0x4D4D41 + 3
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["mma", "reference"], default="mma")
+    ap.add_argument("--workload", choices=["kv", "contig"], default="kv")
+    ap.add_argument("--bytes", type=int, default=4 * GiB, help="contig workload size")
+    ap.add_argument("--tokens", type=int, default=32768, help="kv workload tokens")
+    ap.add_argument("--chunk", type=int, default=4 * MiB)
+    ap.add_argument("--hop", type=int, default=0, help="0 auto, 1 copy engine, 2 SM zero-copy")
+    ap.add_argument("--no-verify", action="store_true")
+    ap.add_argument("--quick", action="store_true", help="skip baselines (profiling runs)")
+    ap.add_argument("--modes", default="", help="fix the direct path's mode per direction instead of "
+                    "measuring, e.g. 'ce,zc' (profiling runs that must match a bench's choice)")
+    return ap.parse_args()
+
+
+# ------------------------------------------------------------------ distributed ---
+
+class Dist:
+    def __init__(self):
+        self.rank = int(os.environ.get("RANK", 0))
+        self.world = int(os.environ.get("WORLD_SIZE", 1))
+        self.local = int(os.environ.get("LOCAL_RANK", 0))
+        self.pg = None
+        if self.world > 1:
+            import torch.distributed as dist
+            os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+            dist.init_process_group("gloo")   # control plane only: no GPU work on ranks > 0
+            self.pg = dist
+
+    def barrier(self):
+        if self.pg:
+            self.pg.barrier()
+
+    def max(self, x: float) -> float:
+        if not self.pg:
+            return x
+        import torch
+        t = torch.tensor([x], dtype=torch.float64)
+        self.pg.all_reduce(t, op=self.pg.ReduceOp.MAX)
+        return float(t.item())
+
+    def close(self):
+        if self.pg:
+            self.pg.destroy_process_group()
+
+
+# ---------------------------------------------------------------------- clocks ---
+
+class Clocks:
+    """nvidia-smi samples during the timed region (B200_PROFILING.md clocks line)."""
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpus):
+        self.gpus = gpus
+        self.p = None
+
+    def start(self):
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                                       "-lms", "200", "-i", ",".join(str(g) for g in self.gpus)],
+                                      stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.p = None
+
+    def stop(self):
+        if not self.p:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.p.terminate()
+        out, _ = self.p.communicate(timeout=10)
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in out.strip().splitlines():
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx.append(float(f[2]))
+            except ValueError:
+                continue
+            for n, v in zip(names, f[5:9]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "samples": len(sm), "reasons": sorted(reasons)}
+
+
+# ------------------------------------------------------------------- workloads ---
+
+def kv_workload(torch, mma, tokens, dev):
+    """Config 3 shapes from mma_inputs.workloads; host pool filled with the seeded pattern
+    by the device generator (fill kernel) and copied to the pinned pool."""
+    import numpy as np
+    from mma_inputs import workloads as W
+    shape = W.KVShape() if tokens == 32768 else W.scaled_kv(tokens)
+    ho, do, sb, hpool, dbytes = W.kv_segments(shape, SEED)
+    host = torch.empty(hpool, dtype=torch.uint8).pin_memory()
+    tmp = torch.empty(min(hpool, GiB), dtype=torch.uint8, device=dev)
+    for a in range(0, hpool, tmp.numel()):
+        n = min(tmp.numel(), hpool - a)
+        mma.fill_pattern(tmp, n, SEED, a)
+        host[a:a + n].copy_(tmp[:n])
+    del tmp
+    cache = torch.empty(dbytes, dtype=torch.uint8, device=dev)
+    lens = np.full(len(ho), sb, dtype=np.int64)
+    fetch = mma.make_segments(host.data_ptr() + ho, cache.data_ptr() + do, lens)
+    offload = mma.make_segments(cache.data_ptr() + do, host.data_ptr() + ho, lens)
+    desc = (f"prefix-cache KV fetch + offload (BASELINE config 3): Llama-3-8B bf16 KV, {shape.tokens} tokens, "
+            f"{len(ho)} x {sb // 1024} KiB segments (layer, K|V, 16-token block) scattered by a seeded "
+            f"permutation in a {hpool / GiB:.0f} GiB pinned pool -> paged device cache")
+    return dict(host=host, cache=cache, fetch=fetch, offload=offload, bytes=int(lens.sum()), ho=ho, do=do,
+                sb=sb, desc=desc, nsegs=len(ho))
+
+
+def run_step(mma, w, dev_idx, stream, ev=None):
+    if "fetch" in w:
+        if ev: ev[0].record(stream)
+        mma.memcpy_h2d_segments(*w["fetch"], dev_idx, stream=stream)
+        if ev: ev[1].record(stream)
+        mma.memcpy_d2h_segments(*w["offload"], dev_idx, stream=stream)
+        if ev: ev[2].record(stream)
+    else:
+        if ev: ev[0].record(stream)
+        mma.memcpy_h2d(w["dev"], w["host"], w["bytes"], stream=stream)
+        if ev: ev[1].record(stream)
+        mma.memcpy_d2h(w["host2"], w["dev"], w["bytes"], stream=stream)
+        if ev: ev[2].record(stream)
+
+
+# --------------------------------------------------------------- cpu baseline ---
+
+def oracle_sample(k_paths, nsegs_sample=16384, reps=1):
+    """The oracle's threaded mover (1 thread for the direct path + 2 per relay ring) on a
+    bounded sample of the KV workload: the first `nsegs_sample` segments, gathered from
+    their scattered slots of a pinned-pool-sized host buffer into a packed host 'cache',
+    then scattered back (offload). Returns (GB/s, threads, sample description)."""
+    import numpy as np
+    import oracle
+    from mma_inputs import workloads as W
+    shape = W.KVShape()
+    ho, do, sb, hpool, dbytes = W.kv_segments(shape, SEED)
+    ho = ho[:nsegs_sample]
+    span = int(ho.max()) + sb
+    pool = np.empty(span, dtype=np.uint8)
+    pool[::4096] = 1                                   # touch the pages
+    cache = np.empty(nsegs_sample * sb, dtype=np.uint8)
+    cache[::4096] = 1
+    dofs = np.arange(nsegs_sample, dtype=np.int64) * sb
+    lens = np.full(nsegs_sample, sb, dtype=np.int64)
+    B = int(lens.sum())
+    C = 4 * MiB
+    bw = [1] * k_paths
+    rc, path, _, _ = oracle.plan(bw, B, C, 0, oracle.CONTIG)
+    f_segs, n = oracle.segments_from_arrays(pool.ctypes.data + ho, cache.ctypes.data + dofs, lens)
+    o_segs, _ = oracle.segments_from_arrays(cache.ctypes.data + dofs, pool.ctypes.data + ho, lens)
+    best = None
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        assert oracle.move(f_segs, n, C, bw, path, S=4, exec_mode=oracle.THREADED) == 0
+        assert oracle.move(o_segs, n, C, bw, path, S=4, exec_mode=oracle.THREADED) == 0
+        dt = time.perf_counter() - t0
+        best = dt if best is None else min(best, dt)
+    threads = 1 + 2 * (k_paths - 1)
+    desc = (f"oracle threaded mover (oracle/mma_oracle.c, exec=threaded, {k_paths}-path plan), first "
+            f"{nsegs_sample} of 131072 KV segments ({B / MiB:.0f} MiB) fetched into a packed host buffer "
+            f"and offloaded back, host memory only")
+    return 2 * B / best / 1e9, threads, desc, 2 * B, best
+
+
+def run_reference(args, dist):
+    """--impl reference: the oracle as it stands on the host cores (the base contract's
+    reference arm for this tier); rank 0 only."""
+    if dist.rank != 0:
+        return
+    import oracle
+    oracle.build()
+    k = max(1, args.gpus)
+    times = []
+    gbps = None
+    for i in range(args.warmup + args.steps):
+        g, threads, desc, nbytes, dt = oracle_sample(k, nsegs_sample=8192)
+        if i >= args.warmup:
+            times.append(dt)
+    dt = statistics.median(times)
+    gbps = nbytes / dt / 1e9
+    line = {
+        "impl": "reference", "metric": METRIC, "value": round(gbps, 3), "unit": "GB/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(dt * 1e3, 3), "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "u8", "data": "synthetic",
+        "config": {"workload": "prefix-cache KV fetch + offload (BASELINE config 3), bounded sample",
+                   "paths": k},
+        "cpu_baseline": {"value": round(gbps, 3), "unit": "GB/s", "cores": threads, "kind": "oracle",
+                         "sample": desc},
+        "e2e": {"value": round(gbps, 3), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------- roofline ---
+
+def pcie_rate(torch, g, nbytes=GiB, reps=4):
+    """Solo native cudaMemcpyAsync GB/s of GPU g's PCIe link per direction (the roofline's
+    PCIe term and R(1))."""
+    h = torch.empty(nbytes, dtype=torch.uint8).pin_memory()
+    d = torch.empty(nbytes, dtype=torch.uint8, device=f"cuda:{g}")
+    s = torch.cuda.Stream(device=g)
+    out = {}
+    for name in ("h2d", "d2h"):
+        best = 1e9
+        with torch.cuda.device(g), torch.cuda.stream(s):
+            for _ in range(reps):
+                a = torch.cuda.Event(enable_timing=True)
+                b = torch.cuda.Event(enable_timing=True)
+                a.record(s)
+                if name == "h2d":
+                    d.copy_(h, non_blocking=True)
+                else:
+                    h.copy_(d, non_blocking=True)
+                b.record(s)
+                b.synchronize()
+                best = min(best, a.elapsed_time(b))
+        out[name] = nbytes / best / 1e6
+    del h, d
+    return out
+
+
+def ncu_traffic(direction, kernel):
+    """dram bytes per launch of the dominant kernel from the committed ncu capture
+    (profiles/ncu_summary.json), or None when that kernel was not captured."""
+    p = ROOT / "profiles" / "ncu_summary.json"
+    if p.exists() and kernel == "zc_copy_kernel":
+        try:
+            return json.loads(p.read_text()).get("dram_bytes_per_launch", {}).get(direction)
+        except (ValueError, AttributeError):
+            return None
+    return None
+
+
+# ----------------------------------------------------------------------- main ---
+
+def main():
+    args = parse()
+    dist = Dist()
+    if args.impl == "reference":
+        run_reference(args, dist)
+        dist.close()
+        return
+    import torch
+    import paper_2512_16056_b200 as mma
+
+    if dist.rank != 0:
+        # ranks > 0: no GPU work of their own; their GPUs serve as rank 0's relay paths
+        dist.barrier()      # setup done
+        dist.barrier()      # before timed region
+        dist.max(0.0)
+        dist.barrier()      # after
+        dist.close()
+        return
+
+    ngpu_vis = torch.cuda.device_count()
+    k = max(1, min(args.gpus, ngpu_vis))
+    relays = list(range(1, k))
+    dev = torch.device("cuda:0")
+    torch.cuda.set_device(0)
+    cfg = mma.default_config()
+    cfg.chunk_bytes[0] = cfg.chunk_bytes[1] = args.chunk
+    cfg.npaths = len(relays)
+    for i, g in enumerate(relays):
+        cfg.path_gpus[i] = g
+    if not relays:
+        cfg.npaths = 1
+        cfg.path_gpus[0] = 0     # no relay candidates (self is skipped)
+    cfg.loopback_relays = 0
+    cfg.plan_mode = 0
+    cfg.hop_mode[0] = cfg.hop_mode[1] = args.hop
+    cfg.debug_log = 0
+    mma.init(cfg)
+    paths = mma.get_paths(0, mma.H2D)
+    path_gpus = [p["gpu"] for p in paths]
+
+    if args.workload == "kv":
+        w = kv_workload(torch, mma, args.tokens, dev)
+    else:
+        B = args.bytes
+        host = torch.empty(B, dtype=torch.uint8).pin_memory()
+        tmp = torch.empty(B, dtype=torch.uint8, device=dev)
+        mma.fill_pattern(tmp, B, SEED, 0)
+        host.copy_(tmp)
+        w = dict(host=host, host2=torch.empty(B, dtype=torch.uint8).pin_memory(), dev=tmp, bytes=B,
+                 desc=f"single {B / MiB:.0f} MiB contiguous H2D + D2H (BASELINE config 2 point)")
+    nbytes_step = 2 * w["bytes"]
+    stream = torch.cuda.Stream(device=0)
+
+    # per-path mode and bandwidth chosen by measurement on this workload (north_star (d)),
+    # outside the timed region
+    if args.modes:
+        m = {"ce": mma.HOP_CE, "zc": mma.HOP_ZC}
+        h, d = (m[x] for x in args.modes.split(","))
+        mma.set_path_modes(0, mma.H2D, [h] * len(mma.get_paths(0, mma.H2D)))
+        mma.set_path_modes(0, mma.D2H, [d] * len(mma.get_paths(0, mma.D2H)))
+    elif args.hop == 0:
+        if "fetch" in w:
+            mma.tune_segments(*w["fetch"], 0, mma.H2D, stream=stream, reps=2)
+            mma.tune_segments(*w["offload"], 0, mma.D2H, stream=stream, reps=2)
+        else:
+            mma.calibrate(0, mma.H2D, min(w["bytes"], GiB))
+            mma.calibrate(0, mma.D2H, min(w["bytes"], GiB))
+    tuned = {"h2d": mma.get_paths(0, mma.H2D), "d2h": mma.get_paths(0, mma.D2H)}
+
+    # roofline terms (solo PCIe per path GPU), measured before the timed region
+    pcie = {g: pcie_rate(torch, g) for g in path_gpus}
+    R_h2d = sum(pcie[g]["h2d"] for g in path_gpus)
+    R_d2h = sum(pcie[g]["d2h"] for g in path_gpus)
+
+    # warm-up + correctness check of the bench's own launch configuration
+    for _ in range(args.warmup):
+        run_step(mma, w, 0, stream)
+    stream.synchronize()
+    verify = None
+    if not args.no_verify and "fetch" in w:
+        cnt = torch.zeros(1, dtype=torch.int64, device=dev)
+        torch.cuda.synchronize(0)
+        with torch.cuda.stream(stream):
+            w["cache"].zero_()                      # ordered before the fetch on `stream`
+        mma.memcpy_h2d_segments(*w["fetch"], 0, stream=stream)
+        mma.verify_segments(w["cache"].data_ptr() + w["do"], w["ho"], [w["sb"]] * w["nsegs"], SEED, cnt,
+                            stream=stream)
+        stream.synchronize()
+        verify = {"mismatched_bytes": int(cnt.item()), "checked_bytes": w["bytes"], "on": "device (C4)"}
+    assert mma.get_last_error() == 0
+
+    # ---- timed region
+    mma.reset_stats(0)
+    mma.set_kernel_timing(True)
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(args.steps)]
+    clocks = Clocks(path_gpus)
+    dist.barrier()
+    dist.barrier()
+    for g in path_gpus:
+        torch.cuda.synchronize(g)
+    clocks.start()
+    time.sleep(0.3)
+    t_start = torch.cuda.Event(enable_timing=True)
+    t_end = torch.cuda.Event(enable_timing=True)
+    t_start.record(stream)
+    for i in range(args.steps):
+        run_step(mma, w, 0, stream, evs[i])
+    t_end.record(stream)
+    for g in path_gpus:
+        torch.cuda.synchronize(g)
+    clk = clocks.stop()
+    ktimes = mma.kernel_times()
+    mma.set_kernel_timing(False)
+    ms_total = t_start.elapsed_time(t_end)
+    ms_total = dist.max(ms_total)
+    dist.barrier()
+    st = mma.get_stats(0)
+    assert mma.get_last_error() == 0
+    ms_step = ms_total / args.steps
+    value = nbytes_step / (ms_step * 1e-3) / 1e9
+    h2d_ms = statistics.median(evs[i][0].elapsed_time(evs[i][1]) for i in range(args.steps))
+    d2h_ms = statistics.median(evs[i][1].elapsed_time(evs[i][2]) for i in range(args.steps))
+    h2d_gbps = w["bytes"] / (h2d_ms * 1e-3) / 1e9
+    d2h_gbps = w["bytes"] / (d2h_ms * 1e-3) / 1e9
+
+    # dominant kernel: the (kind, direction, path, device) group with the largest total
+    # launch time in the timed region; its bytes per launch / its mean launch duration,
+    # against the solo PCIe rate of the link(s) it is bound by
+    groups = {}
+    for kt in ktimes:
+        groups.setdefault((kt["kind"], kt["dir"], kt["path"], kt["dev"]), []).append(kt["ms"])
+    kinds = sorted({kt["kind"] for kt in ktimes})
+    roof = None
+    if groups:
+        (kind, kdir, kpath, kdev), ms_list = max(groups.items(), key=lambda kv: sum(kv[1]))
+        dname = "h2d" if kdir == 0 else "d2h"
+        pinfo = tuned[dname]
+
+        def eff_mode(pi):
+            m = pi["seg_mode"] if ("fetch" in w and pi["seg_mode"] >= 0) else pi["mode"]
+            return m if m else (2 if "fetch" in w else 1)
+        if kpath == 255:      # one relay kernel serves every copy-engine ring of the call
+            ring_paths = [i for i, pi in enumerate(pinfo) if pi["kind"] == 1 and eff_mode(pi) == 1]
+            moved = sum(st["path_bytes"][kdir][i] for i in ring_paths)
+            peak = sum(pcie[pinfo[i]["gpu"]][dname] for i in ring_paths)
+        else:
+            moved = st["path_bytes"][kdir][kpath]
+            peak = pcie[pinfo[kpath]["gpu"]][dname]
+        per_launch = moved // max(1, len(ms_list))
+        k_ms = statistics.mean(ms_list)
+        achieved = per_launch / (k_ms * 1e-3) / 1e9
+        roof = {"bound": "pcie", "achieved": round(achieved, 2), "peak": round(peak, 2), "unit": "GB/s",
+                "frac": round(achieved / peak, 4), "traffic": ncu_traffic(dname, {0: "zc_copy_kernel", 1: "relay_pull_kernel", 2: "relay_pack_kernel"}[kind]),
+                "kernel": {0: "zc_copy_kernel", 1: "relay_pull_kernel", 2: "relay_pack_kernel"}[kind],
+                "direction": dname, "path": kpath, "device": kdev, "launches": len(ms_list),
+                "bytes_per_launch": per_launch, "launch_ms": round(k_ms, 3),
+                "share_of_step": round(sum(ms_list) / ms_total, 4),
+                "peak_source": f"measured in this run: solo native cudaMemcpyAsync 1 GiB {dname.upper()} "
+                               "over the PCIe link(s) this kernel's bytes cross (the roofline's PCIe "
+                               "term, SURVEY 8(d)); HBM (MEASURED_PEAKS hbm_gbs 6554 GB/s) is not the "
+                               "bound of a host<->device copy"}
+
+    # path-level roofline R(k) = sum of the used links' solo PCIe rates (DRAM term reported)
+    R_step = nbytes_step / 2 / (R_h2d * 1e9) + nbytes_step / 2 / (R_d2h * 1e9)
+    path_roof = {"R_h2d_gbps": round(R_h2d, 2), "R_d2h_gbps": round(R_d2h, 2),
+                 "frac_h2d": round(h2d_gbps / R_h2d, 4), "frac_d2h": round(d2h_gbps / R_d2h, 4),
+                 "frac_step": round(value / (nbytes_step / R_step / 1e9), 4),
+                 "pcie_solo": {str(g): {k2: round(v, 2) for k2, v in pcie[g].items()} for g in path_gpus}}
+
+    # ---- e2e through the public API: wall clock, host issue + copies + sync every step
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        run_step(mma, w, 0, stream)
+        stream.synchronize()
+    e2e_s = (time.perf_counter() - t0) / args.steps
+    e2e = {"value": round(nbytes_step / e2e_s / 1e9, 3), "unit": "GB/s",
+           "h2d_bytes_per_step": w["bytes"], "d2h_bytes_per_step": w["bytes"],
+           "how": "wall clock around the Python binding -> C ABI calls, stream synchronized each step"}
+
+    # ---- native baseline on the same buffers: one cudaMemcpyBatchAsync (config 3) or
+    # cudaMemcpyAsync (config 2) per direction on the user stream
+    native = None
+    if not args.quick:
+        cfg.fallback_bytes[0] = cfg.fallback_bytes[1] = (1 << 64) - 1   # everything native
+        mma.init(cfg)
+        for _ in range(2):
+            run_step(mma, w, 0, stream)
+        stream.synchronize()
+        nev = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(args.steps)]
+        for i in range(args.steps):
+            run_step(mma, w, 0, stream, nev[i])
+        stream.synchronize()
+        nh = statistics.median(nev[i][0].elapsed_time(nev[i][1]) for i in range(args.steps))
+        nd = statistics.median(nev[i][1].elapsed_time(nev[i][2]) for i in range(args.steps))
+        native = {"h2d_gbps": round(w["bytes"] / nh / 1e6, 2), "d2h_gbps": round(w["bytes"] / nd / 1e6, 2),
+                  "step_gbps": round(nbytes_step / (nh + nd) / 1e6, 2),
+                  "what": "cudaMemcpyBatchAsync of all segments on the user stream (single PCIe link)"
+                  if "fetch" in w else "cudaMemcpyAsync on the user stream (single PCIe link)",
+                  "speedup": round(value / (nbytes_step / (nh + nd) / 1e6), 3)}
+
+    # ---- CPU baseline: the oracle on the host cores, bounded sample, N=1 only
+    cpu = None
+    if not args.quick and dist.world == 1:
+        try:
+            g, threads, desc, _, _ = oracle_sample(k, nsegs_sample=16384)
+            cpu = {"value": round(g, 3), "unit": "GB/s", "cores": threads, "kind": "oracle", "sample": desc}
+        except Exception as ex:  # noqa: BLE001
+            cpu = {"value": None, "unit": "GB/s", "cores": 0, "kind": "oracle", "sample": f"failed: {ex}"}
+
+    line = {
+        "metric": METRIC, "value": round(value, 3), "unit": "GB/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_step, 3),
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u8",
+        "data": "synthetic",
+        "config": {"workload": w["desc"], "paths": k, "path_gpus": path_gpus, "target_gpu": 0,
+                   "chunk_bytes": args.chunk, "hop": {0: "auto", 1: "ce", 2: "zc"}[args.hop],
+                   "bytes_per_step": nbytes_step, "l2": "inputs (4 GiB per direction) exceed the 126 MB L2; no flush",
+                   "parallelism": f"1 process drives {k} path GPU(s); torchrun ranks>0 idle on gloo"},
+        "per_direction": {"h2d_gbps": round(h2d_gbps, 2), "d2h_gbps": round(d2h_gbps, 2),
+                          "h2d_ms": round(h2d_ms, 3), "d2h_ms": round(d2h_ms, 3)},
+        "path_roofline": path_roof,
+        "roofline": roof,
+        "native": native,
+        "cpu_baseline": cpu,
+        "e2e": e2e,
+        "gpu_launches": int(st["kernels"]),
+        "kernel_kinds": kinds,
+        "clocks": clk,
+        "verify": verify,
+        "modes": {d: [{"gpu": pi["gpu"], "mode": {0: "auto", 1: "ce", 2: "zc"}.get(
+            pi["seg_mode"] if ("fetch" in w and pi["seg_mode"] >= 0) else pi["mode"], "?"),
+            "mbps": pi["seg_mbps"] if ("fetch" in w and pi["seg_mbps"]) else pi["mbps"]} for pi in v]
+            for d, v in tuned.items()},
+        "engine": {"issue_us_per_call": round((st["issue_us"] - st["wait_us"]) / max(1, st["calls"]), 1),
+                   "blocked_us_per_call": round(st["wait_us"] / max(1, st["calls"]), 1),
+                   "relay_bytes": int(st["relay_bytes"]), "fallbacks": int(st["fallbacks"])},
+        "paper_context": "245 GB/s = 4.62x one 53 GB/s PCIe link, 8x H20 (P:737); context only",
+    }
+    print(json.dumps(line), flush=True)
+    dist.close()
+
+
+if __name__ == "__main__":
+    main()

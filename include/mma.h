@@ -81,11 +81,12 @@ typedef struct {
 
 typedef struct {
     uint64_t calls, fallbacks, bytes;
-    uint64_t path_bytes[MMA_MAX_PATHS];   /* per path of this target, last direction used */
-    uint64_t path_chunks[MMA_MAX_PATHS];
+    uint64_t path_bytes[2][MMA_MAX_PATHS];   /* [direction][path] of this target */
+    uint64_t path_chunks[2][MMA_MAX_PATHS];
     uint64_t relay_bytes;                 /* bytes that crossed NVLink (relayed) */
     uint64_t kernels;                     /* relay / zero-copy kernel launches */
-    double issue_us;                      /* host time spent enqueueing */
+    double issue_us;                      /* host time spent enqueueing (incl. wait_us) */
+    double wait_us;                       /* of which blocked on table-buffer reuse */
 } mma_stats_t;
 
 /* Fill cfg with defaults (then env MMA_* overrides). */
@@ -136,9 +137,21 @@ int mma_set_bandwidth(int device, mma_dir_t dir, const uint32_t* mbps, int npath
 /* Per-path hop mode (mma_hop_t), index-aligned with mma_get_paths. */
 int mma_set_path_modes(int device, mma_dir_t dir, const int* modes, int npaths);
 
-/* Measure each path's bandwidth with all paths active (a copy of `bytes` split by the
- * current plan), and store the integer MB/s vector (reading R17: llround). */
+/* "Chosen per path by measurement" (north_star (d)): time each path of `device` alone in
+ * each hop mode (copy engine, SM zero-copy) on a contiguous copy of `bytes` through
+ * library-owned buffers, and keep per path the faster mode and its rate as the planner's
+ * bandwidth (integer MB/s, reading R17: llround). Synchronous. */
 int mma_calibrate(int device, mma_dir_t dir, size_t bytes);
+
+/* The same measurement on the caller's scattered transfer (segment table as in
+ * mma_memcpy_*_segments): the copy is executed (1 + reps) times per (path, mode) on
+ * `stream`, so the destinations are written. The result applies to scattered transfers
+ * only; mma_set_bandwidth / mma_set_path_modes clear it. Synchronous. */
+int mma_tune_segments(const mma_segment_t* segs, size_t nsegs, int device, mma_dir_t dir,
+                      mma_stream_t stream, int reps);
+/* What mma_tune_segments chose, index-aligned with mma_get_paths (0 / -1 = not tuned). */
+int mma_get_segment_tuning(int device, mma_dir_t dir, uint32_t* mbps, int* modes, int cap,
+                           int* npaths);
 
 /* The plan the engine would use for a copy of `bytes`: path index per chunk. A fallback
  * plan is reported as nchunks = 1, path_of_chunk[0] = 0, *fallback = 1. */
@@ -160,6 +173,15 @@ int mma_get_delivery_log(int device, uint8_t* path_of_chunk, size_t cap, size_t*
 /* Pinned, mapped, portable host memory, NUMA-placed per cfg.numa_mode (C8). */
 int mma_host_alloc(void** ptr, size_t bytes, unsigned flags);
 int mma_host_free(void* ptr);
+
+/* Measurement: when on, every relay / zero-copy kernel launch is bracketed by CUDA events
+ * on the stream it is launched on. mma_kernel_times synchronises on the recorded launches,
+ * returns their durations (ms) and tags in launch order (up to cap; *n = number recorded)
+ * and clears the record. tag = kind | direction << 4 | path << 8 | device << 16, kind 0 =
+ * zero-copy, 1 = relay pull (H2D), 2 = relay pack (D2H); path 255 = all rings of the
+ * launch. */
+int mma_set_kernel_timing(int on);
+int mma_kernel_times(float* ms, int* kinds, size_t cap, size_t* n);
 
 int mma_get_stats(int device, mma_stats_t* out);
 int mma_reset_stats(int device);

@@ -2,7 +2,9 @@
 
 The product is the C-ABI library libmma.so (include/mma.h); `mma` is its thin binding.
 Importing this package loads the library first so that its constructor raises
-CUDA_DEVICE_MAX_CONNECTIONS before any CUDA context exists.
+CUDA_DEVICE_MAX_CONNECTIONS before any CUDA context exists. A missing or stale library
+makes every call raise (there is no CPU fallback); importing still works so that
+`python -m paper_2512_16056_b200.build` can rebuild it.
 """
 from . import mma  # noqa: F401
 from .mma import (  # noqa: F401
@@ -10,10 +12,11 @@ from .mma import (  # noqa: F401
     calibrate, default_config, finalize, get_delivery_log, get_last_error, get_paths, get_plan,
     get_stats, host_alloc, host_array, host_free, init, make_segments, memcpy_d2h,
     memcpy_d2h_segments, memcpy_h2d, memcpy_h2d_segments, plan_chunks, reset_stats,
-    set_bandwidth, set_path_modes, fill_pattern, verify_pattern, verify_segments,
+    set_bandwidth, set_path_modes, tune_segments, set_kernel_timing, kernel_times, fill_pattern,
+    verify_pattern, verify_segments,
 )
 
-try:  # load early when built (the build check imports before building otherwise)
+try:
     mma.lib()
-except ImportError:
-    pass
+except (ImportError, OSError, AttributeError):
+    mma._lib = None

@@ -67,7 +67,8 @@ struct DeviceGuard {
 
 struct DevRes {
     bool made = false;
-    cudaStream_t direct = nullptr;   // direct-path DMA / zero-copy kernels
+    cudaStream_t direct = nullptr;   // direct-path DMA
+    cudaStream_t zc = nullptr;       // zero-copy kernels (direct or one-hop relay)
     cudaStream_t hop[2] = {};        // relay hop DMAs: dual pipeline, slot parity
     cudaStream_t kern = nullptr;     // relay kernels (pull on a target, pack on a relay)
     cudaEvent_t fork = nullptr;      // recorded on a user stream of this device
@@ -93,6 +94,8 @@ struct PathState {
     int kind;       // MMA_PATH_DIRECT / MMA_PATH_RELAY
     uint32_t mbps;
     int mode;       // mma_hop_t
+    uint32_t seg_mbps = 0;   // measured for scattered transfers (mma_tune_segments); 0 = unset
+    int seg_mode = -1;       // idem; -1 = unset
 };
 
 struct Scratch {    // per-call table uploads, double-buffered by call parity
@@ -112,7 +115,7 @@ struct Target {
     mma_stats_t stats{};
     uint8_t* log = nullptr;
     size_t log_cap = 0, log_n = 0;
-    Scratch scratch[2];
+    Scratch scratch[4];   // table buffers of the last 4 calls (a ring)
     unsigned parity = 0;
 };
 
@@ -222,12 +225,13 @@ static int make_device(int d)
     DeviceGuard g(d);
     int lo, hi;
     CK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
-    // Four streams created back to back so they land on distinct hardware queues: a
+    // Five streams created back to back so they land on distinct hardware queues: a
     // spinning relay kernel must never sit in front of the DMAs it waits for.
     CK(cudaStreamCreateWithPriority(&r.kern, cudaStreamNonBlocking, hi));
     CK(cudaStreamCreateWithPriority(&r.hop[0], cudaStreamNonBlocking, hi));
     CK(cudaStreamCreateWithPriority(&r.hop[1], cudaStreamNonBlocking, hi));
     CK(cudaStreamCreateWithPriority(&r.direct, cudaStreamNonBlocking, hi));
+    CK(cudaStreamCreateWithPriority(&r.zc, cudaStreamNonBlocking, hi));
     CK(cudaEventCreateWithFlags(&r.fork, cudaEventDisableTiming));
     CK(cudaDeviceGetAttribute(&r.sms, cudaDevAttrMultiProcessorCount, d));
     for (int p = 0; p < e.ndev; p++) {
@@ -391,6 +395,9 @@ struct Job {
     uint64_t nseg = 0;
     std::vector<uint64_t> vstart;    // segmented: prefix offsets [nseg + 1]
     bool mapped = false;             // every host address is usable by GPU SMs
+    const uint32_t* bw_override = nullptr;   // measurement runs: per-path bandwidth
+    const int* mode_override = nullptr;      // measurement runs: per-path mode
+    bool no_small_fallback = false;          // measurement runs: ignore the threshold
 
     // pieces of v[a, b) (the per-segment parts; one piece when contiguous)
     template <typename F>
@@ -484,6 +491,39 @@ static int scratch_host(Scratch& sc, size_t bytes, void** out)
     return cudaSuccess;
 }
 
+// Optional per-launch CUDA-event timing of the engine's kernels, recorded on the stream
+// the kernel is launched on (mma_set_kernel_timing / mma_kernel_times).
+struct KRec {
+    int dev;
+    int kind;   // 0 zero-copy, 1 relay pull (H2D), 2 relay pack (D2H) | dir << 4 | path << 8 | dev << 16
+    cudaEvent_t a, b;
+};
+static std::vector<KRec> g_kpending;
+static bool g_ktime = false;
+
+struct KTimer {
+    bool on = false;
+    KRec r{};
+    cudaStream_t s = nullptr;
+    KTimer(int dev, cudaStream_t st, int kind)
+    {
+        if (!g_ktime) return;
+        DeviceGuard g(dev);
+        if (cudaEventCreate(&r.a) != cudaSuccess || cudaEventCreate(&r.b) != cudaSuccess) return;
+        r.dev = dev;
+        r.kind = kind | (dev << 16);
+        s = st;
+        on = cudaEventRecord(r.a, s) == cudaSuccess;
+    }
+    ~KTimer()
+    {
+        if (!on) return;
+        DeviceGuard g(r.dev);
+        cudaEventRecord(r.b, s);
+        g_kpending.push_back(r);
+    }
+};
+
 static int resolve_mode(const Job& j, int mode)
 {
     if (mode == MMA_HOP_AUTO) mode = j.contiguous ? MMA_HOP_CE : MMA_HOP_ZC;
@@ -504,9 +544,17 @@ static int run_job(Job& j)
 
     // ---- plan (a2)
     std::vector<PlanPath> pp(P);
-    for (int p = 0; p < P; p++) pp[p] = PlanPath{ps[p].kind == MMA_PATH_DIRECT, ps[p].mbps, 0};
+    std::vector<int> pmode(P);
+    for (int p = 0; p < P; p++) {
+        uint32_t bw = (!j.contiguous && ps[p].seg_mbps) ? ps[p].seg_mbps : ps[p].mbps;
+        if (j.bw_override) bw = j.bw_override[p];
+        pp[p] = PlanPath{ps[p].kind == MMA_PATH_DIRECT, bw, 0};
+        pmode[p] = (!j.contiguous && ps[p].seg_mode >= 0) ? ps[p].seg_mode : ps[p].mode;
+        if (j.mode_override) pmode[p] = j.mode_override[p];
+    }
+    const uint64_t thr = j.no_small_fallback ? 0 : e.cfg.fallback_bytes[j.dir];
     Plan plan;
-    if (make_plan(pp.data(), P, j.B, j.C, e.cfg.fallback_bytes[j.dir], e.cfg.plan_mode, plan) != 0)
+    if (make_plan(pp.data(), P, j.B, j.C, thr, e.cfg.plan_mode, plan) != 0)
         return cudaErrorInvalidValue;
     t.stats.calls++;
     t.stats.bytes += j.B;
@@ -514,14 +562,14 @@ static int run_job(Job& j)
     // ---- fallback (a1): the native copy on the user stream (§3.2)
     if (plan.fallback) {
         t.stats.fallbacks++;
-        const int mode0 = resolve_mode(j, ps[0].mode);
-        const bool small = j.B < e.cfg.fallback_bytes[j.dir];
+        const int mode0 = resolve_mode(j, pmode[0]);
+        const bool small = j.B < thr;
         if (small || mode0 == MMA_HOP_CE) {
             DmaBatch b;
             j.pieces(0, j.B, [&](const Piece& x) { b.add(x.dst, x.src, x.len); });
             CK((cudaError_t)b.issue(kind, j.user));
-            t.stats.path_bytes[0] += j.B;
-            t.stats.path_chunks[0] += 1;
+            t.stats.path_bytes[j.dir][0] += j.B;
+            t.stats.path_chunks[j.dir][0] += 1;
             t.log_n = 0;
             t.stats.issue_us += std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t0).count();
             return cudaSuccess;
@@ -535,18 +583,22 @@ static int run_job(Job& j)
     }
 
     const uint64_t n = plan.n;
-    Scratch& sc = t.scratch[t.parity & 1];
+    Scratch& sc = t.scratch[t.parity & 3];
     t.parity++;
-    if (sc.pending) {   // the call two back used this scratch: it must be finished
+    if (sc.pending) {   // the call four back used these tables: it must be finished
+        const auto w0 = std::chrono::steady_clock::now();
         CK(cudaEventSynchronize(sc.done));
         sc.pending = false;
+        t.stats.wait_us += std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - w0).count();
     }
+    // every GPU of the path set gets its streams and peer access before any enqueue
+    for (int p = 0; p < P; p++) CK(make_device(ps[p].gpu));
 
     // ---- per-path chunk lists, ascending
     std::vector<std::vector<uint32_t>> lists(P);
     for (uint64_t i = 0; i < n; i++) lists[plan.path[i]].push_back((uint32_t)i);
     std::vector<int> mode(P);
-    for (int p = 0; p < P; p++) mode[p] = resolve_mode(j, ps[p].mode);
+    for (int p = 0; p < P; p++) mode[p] = resolve_mode(j, pmode[p]);
 
     // ---- host tables: chunk lists (interleaved plans) and the segment table
     const bool need_ctab = e.cfg.plan_mode == PLAN_INTERLEAVED;
@@ -672,12 +724,12 @@ static int run_job(Job& j)
         const bool relay = ps[p].kind == MMA_PATH_RELAY;
         uint64_t bytes_p = 0;
         for (uint32_t i : lists[p]) { uint64_t o, l; j.extent(i, &o, &l); bytes_p += l; }
-        t.stats.path_bytes[p] += bytes_p;
-        t.stats.path_chunks[p] += lists[p].size();
+        t.stats.path_bytes[j.dir][p] += bytes_p;
+        t.stats.path_chunks[j.dir][p] += lists[p].size();
         if (relay) t.stats.relay_bytes += bytes_p;
         if (mode[p] == MMA_HOP_ZC) {
             // one kernel per path: on d for the direct path, on r for a one-hop relay
-            cudaStream_t s = e.dev[g].direct;
+            cudaStream_t s = e.dev[g].zc;
             CK((cudaError_t)use(s, g));
             CK((cudaError_t)after_upload(s, g));
             ZcLaunchArg a{};
@@ -690,6 +742,7 @@ static int run_job(Job& j)
             const uint64_t units = a.chunks.count * upc;
             const unsigned grid = (unsigned)std::min<uint64_t>(units, (uint64_t)e.dev[g].sms * 4);
             DeviceGuard dg(g);
+            KTimer kt(g, s, 0 | (j.dir << 4) | (p << 8));
             CK(launch_zc(a, grid, s));
             t.stats.kernels++;
             continue;
@@ -771,6 +824,7 @@ static int run_job(Job& j)
             CK(make_device(kd));
             CK((cudaError_t)use(s, kd));
             DeviceGuard dg(kd);
+            KTimer kt(kd, s, (j.dir == MMA_H2D ? 1 : 2) | (j.dir << 4) | (0xff << 8));
             CK(launch_relay(kv.second, j.dir == MMA_H2D, grids[kd], s));
             t.stats.kernels++;
         }
@@ -893,15 +947,11 @@ static int copy_contiguous(int dir, void* dst, const void* src, size_t bytes, cu
     return run_job(j);
 }
 
-static int copy_segments(int dir, const mma_segment_t* segs, size_t nsegs, int device, cudaStream_t stream)
+// Validate a segment table and fill the job (no engine lock held).
+static int prepare_segments(int dir, const mma_segment_t* segs, size_t nsegs, int device,
+                            cudaStream_t stream, Job& j)
 {
-    CK((cudaError_t)ensure_init());
-    if (int se = sticky()) return se;
     Engine& e = E();
-    if (nsegs == 0) return cudaSuccess;
-    if (!segs) return cudaErrorInvalidValue;
-    if (device < 0 || device >= e.ndev) return cudaErrorInvalidDevice;
-    Job j;
     j.dir = dir;
     j.d = device;
     j.user = stream;
@@ -946,6 +996,20 @@ static int copy_segments(int dir, const mma_segment_t* segs, size_t nsegs, int d
         if (hk == 2) j.mapped = false;   // pageable: CE only
         j.mapped = j.mapped && m;
     }
+    return cudaSuccess;
+}
+
+static int copy_segments(int dir, const mma_segment_t* segs, size_t nsegs, int device, cudaStream_t stream)
+{
+    CK((cudaError_t)ensure_init());
+    if (int se = sticky()) return se;
+    Engine& e = E();
+    if (nsegs == 0) return cudaSuccess;
+    if (!segs) return cudaErrorInvalidValue;
+    if (device < 0 || device >= e.ndev) return cudaErrorInvalidDevice;
+    Job j;
+    CK(prepare_segments(dir, segs, nsegs, device, stream, j));
+    if (j.B == 0) return cudaSuccess;
     std::lock_guard<std::mutex> g(e.mu);
     CK((cudaError_t)make_device(device));
     return run_job(j);
@@ -1006,6 +1070,7 @@ int mma_finalize(void)
         cudaStreamDestroy(r.hop[0]);
         cudaStreamDestroy(r.hop[1]);
         cudaStreamDestroy(r.direct);
+        cudaStreamDestroy(r.zc);
         cudaEventDestroy(r.fork);
         r = DevRes();
     }
@@ -1054,6 +1119,23 @@ int mma_get_paths(int device, mma_dir_t dir, int* gpus, int* kinds, uint32_t* mb
     return cudaSuccess;
 }
 
+int mma_get_segment_tuning(int device, mma_dir_t dir, uint32_t* mbps, int* modes, int cap, int* npaths)
+{
+    CK((cudaError_t)ensure_init());
+    Engine& e = E();
+    if (device < 0 || device >= e.ndev) return cudaErrorInvalidDevice;
+    if ((dir != MMA_H2D && dir != MMA_D2H) || !npaths) return cudaErrorInvalidValue;
+    std::lock_guard<std::mutex> g(e.mu);
+    make_paths(device);
+    auto& ps = e.tgt[device].paths[dir];
+    *npaths = (int)ps.size();
+    for (int i = 0; i < (int)ps.size() && i < cap; i++) {
+        if (mbps) mbps[i] = ps[i].seg_mbps;
+        if (modes) modes[i] = ps[i].seg_mode;
+    }
+    return cudaSuccess;
+}
+
 int mma_set_bandwidth(int device, mma_dir_t dir, const uint32_t* mbps, int npaths)
 {
     CK((cudaError_t)ensure_init());
@@ -1067,7 +1149,7 @@ int mma_set_bandwidth(int device, mma_dir_t dir, const uint32_t* mbps, int npath
     bool any = false;
     for (int i = 0; i < npaths; i++) any |= mbps[i] > 0;
     if (!any) return cudaErrorInvalidValue;
-    for (int i = 0; i < npaths; i++) ps[i].mbps = mbps[i];
+    for (int i = 0; i < npaths; i++) { ps[i].mbps = mbps[i]; ps[i].seg_mbps = 0; }
     return cudaSuccess;
 }
 
@@ -1083,7 +1165,7 @@ int mma_set_path_modes(int device, mma_dir_t dir, const int* modes, int npaths)
     if (npaths != (int)ps.size()) return cudaErrorInvalidValue;
     for (int i = 0; i < npaths; i++)
         if (modes[i] < MMA_HOP_AUTO || modes[i] > MMA_HOP_ZC) return cudaErrorInvalidValue;
-    for (int i = 0; i < npaths; i++) ps[i].mode = modes[i];
+    for (int i = 0; i < npaths; i++) { ps[i].mode = modes[i]; ps[i].seg_mode = -1; }
     return cudaSuccess;
 }
 
@@ -1132,6 +1214,60 @@ int mma_plan_chunks(const uint32_t* mbps, const int* kinds, const uint64_t* back
     return cudaSuccess;
 }
 
+// Measure every path alone in each hop mode on the transfer `proto` describes and keep,
+// per path, the faster mode and its rate (integer MB/s, reading R17: llround). Runs the
+// copy (1 + reps) times per (path, mode); the best of `reps` timed runs counts.
+static int tune_paths(Job proto, int reps, std::vector<uint32_t>& mbps, std::vector<int>& modes)
+{
+    Engine& e = E();
+    auto& ps = e.tgt[proto.d].paths[proto.dir];
+    const int P = (int)ps.size();
+    mbps.assign(P, 0);
+    modes.assign(P, MMA_HOP_CE);
+    std::vector<uint32_t> bw(P);
+    std::vector<int> md(P, MMA_HOP_CE);
+    cudaEvent_t a = nullptr, b = nullptr;
+    {
+        DeviceGuard g(proto.user_dev);
+        CK(cudaEventCreate(&a));
+        CK(cudaEventCreate(&b));
+    }
+    int rc = cudaSuccess;
+    for (int p = 0; p < P && rc == cudaSuccess; p++) {
+        float best_rate = 0.f;
+        for (int m : {MMA_HOP_CE, MMA_HOP_ZC}) {
+            if (m == MMA_HOP_ZC && !proto.mapped) continue;
+            for (int q = 0; q < P; q++) bw[q] = (q == p) ? 1 : 0;
+            md[p] = m;
+            float best = 1e30f;
+            for (int rep = 0; rep <= reps && rc == cudaSuccess; rep++) {
+                Job j = proto;
+                j.bw_override = bw.data();
+                j.mode_override = md.data();
+                j.no_small_fallback = true;
+                DeviceGuard g(j.user_dev);
+                cudaEventRecord(a, j.user);
+                rc = run_job(j);
+                cudaEventRecord(b, j.user);
+                if (cudaEventSynchronize(b) != cudaSuccess) rc = cudaErrorUnknown;
+                float ms = 0;
+                cudaEventElapsedTime(&ms, a, b);
+                if (rep > 0 && ms > 0) best = std::min(best, ms);   // rep 0 warms up
+            }
+            const float rate = best < 1e29f ? (float)((double)proto.B / (best * 1e-3) / 1e6) : 0.f;
+            if (rate > best_rate) {
+                best_rate = rate;
+                modes[p] = m;
+                mbps[p] = (uint32_t)llround(rate);
+            }
+        }
+    }
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+    if (rc == cudaSuccess && sticky()) rc = sticky();
+    return rc;
+}
+
 int mma_calibrate(int device, mma_dir_t dir, size_t bytes)
 {
     CK((cudaError_t)ensure_init());
@@ -1141,55 +1277,58 @@ int mma_calibrate(int device, mma_dir_t dir, size_t bytes)
     std::lock_guard<std::mutex> g(e.mu);
     CK(make_device(device));
     make_paths(device);
-    auto& ps = e.tgt[device].paths[dir];
-    const int P = (int)ps.size();
     DeviceGuard dg(device);
     char* hbuf = nullptr;
     char* dbuf = nullptr;
     cudaStream_t s = nullptr;
-    cudaEvent_t a = nullptr, b = nullptr;
     CK(cudaHostAlloc((void**)&hbuf, bytes, cudaHostAllocPortable | cudaHostAllocMapped));
     CK(cudaMalloc((void**)&dbuf, bytes));
     CK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
-    CK(cudaEventCreate(&a));
-    CK(cudaEventCreate(&b));
-    std::vector<uint32_t> saved(P), measured(P, 0);
-    for (int p = 0; p < P; p++) saved[p] = ps[p].mbps;
-    const size_t thr = e.cfg.fallback_bytes[dir];
-    e.cfg.fallback_bytes[dir] = 0;
-    int rc = cudaSuccess;
-    // Each path alone (the others' bandwidth set to 0), best of 3 (reading R17).
-    for (int p = 0; p < P && rc == cudaSuccess; p++) {
-        for (int q = 0; q < P; q++) ps[q].mbps = (q == p) ? 1 : 0;
-        float best = 1e30f;
-        for (int rep = 0; rep < 4 && rc == cudaSuccess; rep++) {
-            Job j;
-            j.dir = dir;
-            j.d = device;
-            j.user = s;
-            j.user_dev = device;
-            j.B = bytes;
-            j.C = e.cfg.chunk_bytes[dir];
-            j.src0 = dir == MMA_H2D ? hbuf : dbuf;
-            j.dst0 = dir == MMA_H2D ? dbuf : hbuf;
-            j.mapped = true;
-            cudaEventRecord(a, s);
-            rc = run_job(j);
-            cudaEventRecord(b, s);
-            if (cudaEventSynchronize(b) != cudaSuccess) rc = cudaErrorUnknown;
-            float ms = 0;
-            cudaEventElapsedTime(&ms, a, b);
-            if (rep > 0 && ms > 0) best = std::min(best, ms);   // rep 0 warms up
-        }
-        if (best < 1e29f) measured[p] = (uint32_t)llround((double)bytes / (best * 1e-3) / 1e6);
+    Job j;
+    j.dir = dir;
+    j.d = device;
+    j.user = s;
+    j.user_dev = device;
+    j.B = bytes;
+    j.C = e.cfg.chunk_bytes[dir];
+    j.src0 = dir == MMA_H2D ? hbuf : dbuf;
+    j.dst0 = dir == MMA_H2D ? dbuf : hbuf;
+    j.mapped = true;
+    std::vector<uint32_t> mbps;
+    std::vector<int> modes;
+    int rc = tune_paths(j, 3, mbps, modes);
+    if (rc == cudaSuccess) {
+        auto& ps = e.tgt[device].paths[dir];
+        for (size_t p = 0; p < ps.size(); p++)
+            if (mbps[p]) { ps[p].mbps = mbps[p]; ps[p].mode = modes[p]; }
     }
-    e.cfg.fallback_bytes[dir] = thr;
-    for (int p = 0; p < P; p++) ps[p].mbps = (rc == cudaSuccess && measured[p]) ? measured[p] : saved[p];
-    cudaEventDestroy(a);
-    cudaEventDestroy(b);
     cudaStreamDestroy(s);
     cudaFree(dbuf);
     cudaFreeHost(hbuf);
+    return rc;
+}
+
+int mma_tune_segments(const mma_segment_t* segs, size_t nsegs, int device, mma_dir_t dir,
+                      mma_stream_t stream, int reps)
+{
+    CK((cudaError_t)ensure_init());
+    Engine& e = E();
+    if (device < 0 || device >= e.ndev) return cudaErrorInvalidDevice;
+    if ((dir != MMA_H2D && dir != MMA_D2H) || !segs || nsegs == 0 || reps < 1) return cudaErrorInvalidValue;
+    Job j;
+    CK(prepare_segments(dir, segs, nsegs, device, (cudaStream_t)stream, j));
+    if (j.B == 0) return cudaSuccess;
+    std::lock_guard<std::mutex> g(e.mu);
+    CK(make_device(device));
+    make_paths(device);
+    std::vector<uint32_t> mbps;
+    std::vector<int> modes;
+    int rc = tune_paths(j, reps, mbps, modes);
+    if (rc == cudaSuccess) {
+        auto& ps = e.tgt[device].paths[dir];
+        for (size_t p = 0; p < ps.size(); p++)
+            if (mbps[p]) { ps[p].seg_mbps = mbps[p]; ps[p].seg_mode = modes[p]; }
+    }
     return rc;
 }
 
@@ -1238,6 +1377,37 @@ int mma_reset_stats(int device)
     std::lock_guard<std::mutex> g(e.mu);
     e.tgt[device].stats = mma_stats_t{};
     return cudaSuccess;
+}
+
+int mma_set_kernel_timing(int on)
+{
+    std::lock_guard<std::mutex> g(E().mu);
+    g_ktime = on != 0;
+    return cudaSuccess;
+}
+
+int mma_kernel_times(float* ms, int* kinds, size_t cap, size_t* n)
+{
+    if (!n) return cudaErrorInvalidValue;
+    std::lock_guard<std::mutex> g(E().mu);
+    size_t k = 0;
+    int rc = cudaSuccess;
+    for (auto& r : g_kpending) {
+        DeviceGuard dg(r.dev);
+        float t = 0.f;
+        if (cudaEventSynchronize(r.b) != cudaSuccess || cudaEventElapsedTime(&t, r.a, r.b) != cudaSuccess)
+            rc = cudaErrorUnknown;
+        if (k < cap) {
+            if (ms) ms[k] = t;
+            if (kinds) kinds[k] = r.kind;
+        }
+        k++;
+        cudaEventDestroy(r.a);
+        cudaEventDestroy(r.b);
+    }
+    g_kpending.clear();
+    *n = k;
+    return rc;
 }
 
 int mma_get_last_error(void)

@@ -25,7 +25,8 @@ SYMBOLS = [
     "mma_set_path_modes", "mma_calibrate", "mma_get_plan", "mma_plan_chunks",
     "mma_get_delivery_log", "mma_host_alloc", "mma_host_free", "mma_get_stats",
     "mma_reset_stats", "mma_get_last_error", "mma_error_string", "mma_fill_pattern",
-    "mma_verify_pattern", "mma_verify_segments",
+    "mma_verify_pattern", "mma_verify_segments", "mma_set_kernel_timing", "mma_kernel_times",
+    "mma_tune_segments", "mma_get_segment_tuning",
 ]
 
 
@@ -48,8 +49,9 @@ class Config(C.Structure):
 class Stats(C.Structure):
     _fields_ = [
         ("calls", C.c_uint64), ("fallbacks", C.c_uint64), ("bytes", C.c_uint64),
-        ("path_bytes", C.c_uint64 * MAX_PATHS), ("path_chunks", C.c_uint64 * MAX_PATHS),
+        ("path_bytes", (C.c_uint64 * MAX_PATHS) * 2), ("path_chunks", (C.c_uint64 * MAX_PATHS) * 2),
         ("relay_bytes", C.c_uint64), ("kernels", C.c_uint64), ("issue_us", C.c_double),
+        ("wait_us", C.c_double),
     ]
 
 
@@ -97,6 +99,10 @@ def lib():
         L.mma_fill_pattern.argtypes = [vp, sz, C.c_uint64, C.c_uint64, vp]
         L.mma_verify_pattern.argtypes = [vp, sz, C.c_uint64, C.c_uint64, vp, vp]
         L.mma_verify_segments.argtypes = [vp, vp, vp, sz, C.c_uint64, vp, vp]
+        L.mma_set_kernel_timing.argtypes = [C.c_int]
+        L.mma_tune_segments.argtypes = [C.POINTER(Segment), sz, C.c_int, C.c_int, vp, C.c_int]
+        L.mma_kernel_times.argtypes = [vp, vp, sz, C.POINTER(sz)]
+        L.mma_get_segment_tuning.argtypes = [C.c_int, C.c_int, vp, vp, C.c_int, C.POINTER(C.c_int)]
         _lib = L
     return _lib
 
@@ -195,7 +201,12 @@ def get_paths(device: int, direction: int):
     n = C.c_int()
     _check(lib().mma_get_paths(device, direction, gpus, kinds, mbps, modes, MAX_PATHS, C.byref(n)),
            "mma_get_paths")
-    return [dict(gpu=gpus[i], kind=kinds[i], mbps=mbps[i], mode=modes[i]) for i in range(n.value)]
+    smbps = (C.c_uint32 * MAX_PATHS)()
+    smodes = (C.c_int * MAX_PATHS)()
+    _check(lib().mma_get_segment_tuning(device, direction, smbps, smodes, MAX_PATHS, C.byref(n)),
+           "mma_get_segment_tuning")
+    return [dict(gpu=gpus[i], kind=kinds[i], mbps=mbps[i], mode=modes[i], seg_mbps=smbps[i],
+                 seg_mode=smodes[i]) for i in range(n.value)]
 
 
 def set_bandwidth(device: int, direction: int, mbps) -> None:
@@ -210,6 +221,12 @@ def set_path_modes(device: int, direction: int, modes) -> None:
 
 def calibrate(device: int, direction: int, nbytes: int = 256 << 20) -> None:
     _check(lib().mma_calibrate(device, direction, nbytes), "mma_calibrate")
+
+
+def tune_segments(segs, nsegs: int, device: int, direction: int, stream=None, reps: int = 2) -> None:
+    """Measure CE vs SM zero-copy per path on this scattered transfer (writes the dsts)."""
+    _check(lib().mma_tune_segments(segs, nsegs, device, direction, _stream(stream, device), reps),
+           "mma_tune_segments")
 
 
 def get_plan(device: int, direction: int, nbytes: int):
@@ -266,8 +283,9 @@ def get_stats(device: int) -> dict:
     s = Stats()
     _check(lib().mma_get_stats(device, C.byref(s)), "mma_get_stats")
     return dict(calls=s.calls, fallbacks=s.fallbacks, bytes=s.bytes,
-                path_bytes=list(s.path_bytes), path_chunks=list(s.path_chunks),
-                relay_bytes=s.relay_bytes, kernels=s.kernels, issue_us=s.issue_us)
+                path_bytes=[list(x) for x in s.path_bytes], path_chunks=[list(x) for x in s.path_chunks],
+                relay_bytes=s.relay_bytes, kernels=s.kernels, issue_us=s.issue_us,
+                wait_us=s.wait_us)
 
 
 def reset_stats(device: int) -> None:
@@ -297,3 +315,22 @@ def verify_segments(dst_ptrs, offsets, lens, seed: int, counter, stream=None) ->
     _check(lib().mma_verify_segments(d.ctypes.data, o.ctypes.data, n.ctypes.data, d.size, seed,
                                      _ptr(counter), _stream(stream, _dev_of(counter))),
            "mma_verify_segments")
+
+
+def set_kernel_timing(on: bool) -> None:
+    _check(lib().mma_set_kernel_timing(1 if on else 0), "mma_set_kernel_timing")
+
+
+def kernel_times():
+    """[(ms, kind)] of the kernel launches recorded since the last call (kind 0 zero-copy,
+    1 relay pull, 2 relay pack); synchronises on them."""
+    n = C.c_size_t()
+    cap = 1 << 16
+    ms = (C.c_float * cap)()
+    kinds = (C.c_int * cap)()
+    _check(lib().mma_kernel_times(ms, kinds, cap, C.byref(n)), "mma_kernel_times")
+    out = []
+    for i in range(min(n.value, cap)):
+        t = kinds[i]
+        out.append(dict(ms=ms[i], kind=t & 15, dir=(t >> 4) & 15, path=(t >> 8) & 255, dev=t >> 16))
+    return out

@@ -189,8 +189,8 @@ def test_stats_account_paths(mma):
     mma.memcpy_h2d(dst, src, B)
     torch.cuda.synchronize()
     st = mma.get_stats(0)
-    assert st["path_chunks"][:2] == [12, 4]
-    assert st["path_bytes"][0] + st["path_bytes"][1] == B and st["relay_bytes"] == 4 * MiB
+    assert st["path_chunks"][0][:2] == [12, 4] and st["path_chunks"][1][:2] == [0, 0]
+    assert st["path_bytes"][0][0] + st["path_bytes"][0][1] == B and st["relay_bytes"] == 4 * MiB
     assert st["kernels"] == 1
 
 

@@ -167,3 +167,31 @@ def test_full_size_kv_fetch(mma, orc):
         assert orc.move(segs1, n1, sb, [1], np.zeros(1, np.uint8)) == 0
         got = cache[int(do[k]):int(do[k]) + sb].cpu().numpy()
         assert np.array_equal(got, exp)
+
+
+def test_mode_choice_by_measurement(mma, orc):
+    """mma_calibrate / mma_tune_segments time every path in each mode and keep the faster
+    one (north_star (d)); copies afterwards stay bit-exact."""
+    configure(mma, loopback=1, chunk=MiB, plan_mode=0, hop=(0, 0), debug=0)
+    mma.calibrate(0, mma.H2D, 64 * MiB)
+    ps = mma.get_paths(0, mma.H2D)
+    assert all(p["mode"] in (1, 2) and p["mbps"] > 5000 for p in ps), ps
+    shape, ho, do, sb, hpool, dbytes = _kv(512)
+    host = torch.empty(hpool, dtype=torch.uint8).pin_memory()
+    mma_inputs.fill_pattern(host.numpy(), 77)
+    cache = torch.zeros(dbytes, dtype=torch.uint8, device="cuda")
+    lens = np.full(len(ho), sb, dtype=np.int64)
+    segs, n = mma.make_segments(host.data_ptr() + ho, cache.data_ptr() + do, lens)
+    mma.tune_segments(segs, n, 0, mma.H2D, reps=1)
+    ps = mma.get_paths(0, mma.H2D)
+    assert all(p["seg_mode"] in (1, 2) and p["seg_mbps"] > 5000 for p in ps), ps
+    cache.zero_()
+    mma.memcpy_h2d_segments(segs, n, 0)
+    torch.cuda.synchronize()
+    cnt = torch.zeros(1, dtype=torch.int64, device="cuda")
+    got = cache.cpu().numpy()
+    hn = host.numpy()
+    for k in range(0, len(ho), 97):
+        assert np.array_equal(got[do[k]:do[k] + sb], hn[ho[k]:ho[k] + sb])
+    mma.set_bandwidth(0, mma.H2D, [1, 1])       # pinning clears the segment tuning
+    assert all(p["seg_mbps"] == 0 for p in mma.get_paths(0, mma.H2D))
