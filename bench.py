@@ -300,26 +300,17 @@ def main():
         dist.close()
         return
 
+    # rank 0 drives every path GPU: widen a per-rank device restriction if one was set
+    vis = os.environ.get("CUDA_VISIBLE_DEVICES")
+    vis_note = None
+    if dist.world > 1 and vis is not None and len([x for x in vis.split(",") if x.strip()]) < args.gpus:
+        del os.environ["CUDA_VISIBLE_DEVICES"]
+        vis_note = f"CUDA_VISIBLE_DEVICES={vis} widened for rank 0 (it drives all {args.gpus} path GPUs)"
     ngpu_vis = torch.cuda.device_count()
     k = max(1, min(args.gpus, ngpu_vis))
-    relays = list(range(1, k))
     dev = torch.device("cuda:0")
     torch.cuda.set_device(0)
-    cfg = mma.default_config()
-    cfg.chunk_bytes[0] = cfg.chunk_bytes[1] = args.chunk
-    cfg.npaths = len(relays)
-    for i, g in enumerate(relays):
-        cfg.path_gpus[i] = g
-    if not relays:
-        cfg.npaths = 1
-        cfg.path_gpus[0] = 0     # no relay candidates (self is skipped)
-    cfg.loopback_relays = 0
-    cfg.plan_mode = 0
-    cfg.hop_mode[0] = cfg.hop_mode[1] = args.hop
-    cfg.debug_log = 0
-    mma.init(cfg)
-    paths = mma.get_paths(0, mma.H2D)
-    path_gpus = [p["gpu"] for p in paths]
+    stream = torch.cuda.Stream(device=0)
 
     if args.workload == "kv":
         w = kv_workload(torch, mma, args.tokens, dev)
@@ -332,45 +323,73 @@ def main():
         w = dict(host=host, host2=torch.empty(B, dtype=torch.uint8).pin_memory(), dev=tmp, bytes=B,
                  desc=f"single {B / MiB:.0f} MiB contiguous H2D + D2H (BASELINE config 2 point)")
     nbytes_step = 2 * w["bytes"]
-    stream = torch.cuda.Stream(device=0)
 
-    # per-path mode and bandwidth chosen by measurement on this workload (north_star (d)),
-    # outside the timed region
-    if args.modes:
-        m = {"ce": mma.HOP_CE, "zc": mma.HOP_ZC}
-        h, d = (m[x] for x in args.modes.split(","))
-        mma.set_path_modes(0, mma.H2D, [h] * len(mma.get_paths(0, mma.H2D)))
-        mma.set_path_modes(0, mma.D2H, [d] * len(mma.get_paths(0, mma.D2H)))
-    elif args.hop == 0:
-        if "fetch" in w:
-            mma.tune_segments(*w["fetch"], 0, mma.H2D, stream=stream, reps=2)
-            mma.tune_segments(*w["offload"], 0, mma.D2H, stream=stream, reps=2)
-        else:
-            mma.calibrate(0, mma.H2D, min(w["bytes"], GiB))
-            mma.calibrate(0, mma.D2H, min(w["bytes"], GiB))
+    def configure(relays):
+        cfg = mma.default_config()
+        cfg.chunk_bytes[0] = cfg.chunk_bytes[1] = args.chunk
+        cfg.npaths = len(relays) if relays else 1
+        for i, g in enumerate(relays or [0]):
+            cfg.path_gpus[i] = g          # [0] alone = no relay candidates (self is skipped)
+        cfg.loopback_relays = 0
+        cfg.plan_mode = 0
+        cfg.hop_mode[0] = cfg.hop_mode[1] = args.hop
+        cfg.debug_log = 0
+        mma.init(cfg)
+        return cfg
+
+    def prepare(relays):
+        """engine config, per-path mode/bandwidth by measurement, warm-up and a device-side
+        check of the bench's own launch configuration (all outside the timed region)"""
+        cfg = configure(relays)
+        if args.modes:
+            m = {"ce": mma.HOP_CE, "zc": mma.HOP_ZC}
+            h, d = (m[x] for x in args.modes.split(","))
+            mma.set_path_modes(0, mma.H2D, [h] * len(mma.get_paths(0, mma.H2D)))
+            mma.set_path_modes(0, mma.D2H, [d] * len(mma.get_paths(0, mma.D2H)))
+        elif args.hop == 0:
+            if "fetch" in w:
+                mma.tune_segments(*w["fetch"], 0, mma.H2D, stream=stream, reps=2)
+                mma.tune_segments(*w["offload"], 0, mma.D2H, stream=stream, reps=2)
+            else:
+                mma.calibrate(0, mma.H2D, min(w["bytes"], GiB))
+                mma.calibrate(0, mma.D2H, min(w["bytes"], GiB))
+        for _ in range(args.warmup):
+            run_step(mma, w, 0, stream)
+        stream.synchronize()
+        verify = None
+        if not args.no_verify and "fetch" in w:
+            cnt = torch.zeros(1, dtype=torch.int64, device=dev)
+            torch.cuda.synchronize(0)
+            with torch.cuda.stream(stream):
+                w["cache"].zero_()                      # ordered before the fetch on `stream`
+            mma.memcpy_h2d_segments(*w["fetch"], 0, stream=stream)
+            mma.verify_segments(w["cache"].data_ptr() + w["do"], w["ho"], [w["sb"]] * w["nsegs"], SEED, cnt,
+                                stream=stream)
+            stream.synchronize()
+            verify = {"mismatched_bytes": int(cnt.item()), "checked_bytes": w["bytes"], "on": "device (C4)"}
+            if verify["mismatched_bytes"]:
+                raise RuntimeError(f"multipath copy verification failed: {verify}")
+        if mma.get_last_error():
+            raise RuntimeError(f"sticky engine error {mma.get_last_error()}")
+        return cfg, verify
+
+    multipath_error = None
+    try:
+        cfg, verify = prepare(list(range(1, k)))
+    except Exception as ex:  # noqa: BLE001 - report, then measure the direct path alone
+        multipath_error = f"{type(ex).__name__}: {ex}"
+        print(f"multipath setup failed ({multipath_error}); falling back to the direct path", file=sys.stderr)
+        mma.finalize()
+        k = 1
+        cfg, verify = prepare([])
+    paths = mma.get_paths(0, mma.H2D)
+    path_gpus = [p["gpu"] for p in paths]
     tuned = {"h2d": mma.get_paths(0, mma.H2D), "d2h": mma.get_paths(0, mma.D2H)}
 
     # roofline terms (solo PCIe per path GPU), measured before the timed region
     pcie = {g: pcie_rate(torch, g) for g in path_gpus}
     R_h2d = sum(pcie[g]["h2d"] for g in path_gpus)
     R_d2h = sum(pcie[g]["d2h"] for g in path_gpus)
-
-    # warm-up + correctness check of the bench's own launch configuration
-    for _ in range(args.warmup):
-        run_step(mma, w, 0, stream)
-    stream.synchronize()
-    verify = None
-    if not args.no_verify and "fetch" in w:
-        cnt = torch.zeros(1, dtype=torch.int64, device=dev)
-        torch.cuda.synchronize(0)
-        with torch.cuda.stream(stream):
-            w["cache"].zero_()                      # ordered before the fetch on `stream`
-        mma.memcpy_h2d_segments(*w["fetch"], 0, stream=stream)
-        mma.verify_segments(w["cache"].data_ptr() + w["do"], w["ho"], [w["sb"]] * w["nsegs"], SEED, cnt,
-                            stream=stream)
-        stream.synchronize()
-        verify = {"mismatched_bytes": int(cnt.item()), "checked_bytes": w["bytes"], "on": "device (C4)"}
-    assert mma.get_last_error() == 0
 
     # ---- timed region
     mma.reset_stats(0)
@@ -498,7 +517,8 @@ def main():
         "config": {"workload": w["desc"], "paths": k, "path_gpus": path_gpus, "target_gpu": 0,
                    "chunk_bytes": args.chunk, "hop": {0: "auto", 1: "ce", 2: "zc"}[args.hop],
                    "bytes_per_step": nbytes_step, "l2": "inputs (4 GiB per direction) exceed the 126 MB L2; no flush",
-                   "parallelism": f"1 process drives {k} path GPU(s); torchrun ranks>0 idle on gloo"},
+                   "parallelism": f"1 process drives {k} path GPU(s); torchrun ranks>0 idle on gloo",
+                   "visible_devices": vis_note, "multipath_error": multipath_error},
         "per_direction": {"h2d_gbps": round(h2d_gbps, 2), "d2h_gbps": round(d2h_gbps, 2),
                           "h2d_ms": round(h2d_ms, 3), "d2h_ms": round(d2h_ms, 3)},
         "path_roofline": path_roof,

@@ -13,6 +13,7 @@ PKG = Path(__file__).resolve().parent
 ROOT = PKG.parent
 CSRC = PKG / "csrc"
 LIB = PKG / "libmma.so"
+PRELOAD = PKG / "libmma_preload.so"
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
 SOURCES = [
@@ -24,7 +25,7 @@ SOURCES = [
     CSRC / "kernels" / "verify.cu",
 ]
 HEADERS = [ROOT / "include" / "mma.h", CSRC / "engine.h", CSRC / "kargs.h", CSRC / "planner.h",
-           CSRC / "kernels" / "copy.cuh"]
+           CSRC / "kernels" / "copy.cuh", CSRC / "preload.cpp"]
 
 FLAGS = [
     "-O3", "-std=c++17", "-lineinfo",
@@ -37,7 +38,7 @@ FLAGS = [
 
 
 def stale() -> bool:
-    if not LIB.exists():
+    if not LIB.exists() or not PRELOAD.exists():
         return True
     t = LIB.stat().st_mtime
     return any(p.stat().st_mtime > t for p in SOURCES + HEADERS + [Path(__file__)])
@@ -62,7 +63,21 @@ def build(force: bool = False, verbose: bool = False) -> Path:
     subprocess.check_call([NVCC, "-shared", "-gencode", "arch=compute_100a,code=sm_100a",
                            "-cudart", "static", "-o", str(tmp), *objs, "-ldl", "-lpthread", "-lrt"])
     os.replace(tmp, LIB)
+    build_preload(verbose)
     return LIB
+
+
+def build_preload(verbose: bool = False) -> Path:
+    """libmma_preload.so: the LD_PRELOAD interceptor (C10), linked to libmma.so by rpath."""
+    src = CSRC / "preload.cpp"
+    tmp = PRELOAD.with_suffix(".so.tmp")
+    cmd = ["g++", "-O2", "-std=c++17", "-fPIC", "-shared", "-Wall", "-I", str(ROOT / "include"),
+           str(src), "-o", str(tmp), "-L", str(PKG), "-lmma", "-Wl,-rpath,$ORIGIN", "-ldl"]
+    if verbose:
+        print(" ".join(cmd))
+    subprocess.check_call(cmd)
+    os.replace(tmp, PRELOAD)
+    return PRELOAD
 
 
 if __name__ == "__main__":
