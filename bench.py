@@ -41,7 +41,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["mma", "reference"], default="mma")
-    ap.add_argument("--workload", choices=["kv", "contig"], default="kv")
+    ap.add_argument("--workload", choices=["kv", "contig", "wake"], default="kv")
     ap.add_argument("--bytes", type=int, default=4 * GiB, help="contig workload size")
     ap.add_argument("--tokens", type=int, default=32768, help="kv workload tokens")
     ap.add_argument("--chunk", type=int, default=4 * MiB)
@@ -154,8 +154,32 @@ def kv_workload(torch, mma, tokens, dev):
                 sb=sb, desc=desc, nsegs=len(ho))
 
 
+def wake_workload(torch, mma, dev):
+    """Config 4: vLLM sleep-mode wake of Qwen2.5-14B bf16 (339 tensors, 29,540,067,328 B):
+    one pinned backup buffer packed in module order at 256 B, the same layout on the GPU."""
+    from mma_inputs import workloads as W
+    tensors = W.qwen25_14b_tensors()
+    offs, sizes, total = W.packed_layout(tensors)
+    host = torch.empty(total, dtype=torch.uint8).pin_memory()
+    devbuf = torch.empty(total, dtype=torch.uint8, device=dev)
+    mma.fill_pattern(devbuf, total, SEED + 1, 0)
+    host.copy_(devbuf)
+    desc = (f"vLLM sleep-mode wake + fall-asleep (BASELINE config 4): Qwen2.5-14B bf16, {len(tensors)} "
+            f"tensors, {total} B packed at 256 B; one mma_memcpy_h2d / _d2h per tensor")
+    return dict(host=host, dev=devbuf, offs=offs, sizes=sizes, bytes=total, desc=desc, wake=True)
+
+
 def run_step(mma, w, dev_idx, stream, ev=None):
-    if "fetch" in w:
+    if "wake" in w:
+        hp, dp = w["host"].data_ptr(), w["dev"].data_ptr()
+        if ev: ev[0].record(stream)
+        for o, n in zip(w["offs"], w["sizes"]):
+            mma.memcpy_h2d(dp + o, hp + o, n, stream=stream)
+        if ev: ev[1].record(stream)
+        for o, n in zip(w["offs"], w["sizes"]):
+            mma.memcpy_d2h(hp + o, dp + o, n, stream=stream)
+        if ev: ev[2].record(stream)
+    elif "fetch" in w:
         if ev: ev[0].record(stream)
         mma.memcpy_h2d_segments(*w["fetch"], dev_idx, stream=stream)
         if ev: ev[1].record(stream)
@@ -241,7 +265,7 @@ def run_reference(args, dist):
 
 # ------------------------------------------------------------------- roofline ---
 
-def pcie_rate(torch, g, nbytes=GiB, reps=4):
+def pcie_rate(torch, g, nbytes=GiB, reps=8):
     """Solo native cudaMemcpyAsync GB/s of GPU g's PCIe link per direction (the roofline's
     PCIe term and R(1))."""
     h = torch.empty(nbytes, dtype=torch.uint8).pin_memory()
@@ -314,6 +338,8 @@ def main():
 
     if args.workload == "kv":
         w = kv_workload(torch, mma, args.tokens, dev)
+    elif args.workload == "wake":
+        w = wake_workload(torch, mma, dev)
     else:
         B = args.bytes
         host = torch.empty(B, dtype=torch.uint8).pin_memory()
@@ -365,6 +391,17 @@ def main():
             mma.memcpy_h2d_segments(*w["fetch"], 0, stream=stream)
             mma.verify_segments(w["cache"].data_ptr() + w["do"], w["ho"], [w["sb"]] * w["nsegs"], SEED, cnt,
                                 stream=stream)
+            stream.synchronize()
+            verify = {"mismatched_bytes": int(cnt.item()), "checked_bytes": w["bytes"], "on": "device (C4)"}
+            if verify["mismatched_bytes"]:
+                raise RuntimeError(f"multipath copy verification failed: {verify}")
+        if not args.no_verify and "wake" in w:
+            cnt = torch.zeros(1, dtype=torch.int64, device=dev)
+            torch.cuda.synchronize(0)
+            with torch.cuda.stream(stream):
+                w["dev"].zero_()
+            run_step(mma, w, 0, stream)               # wake (H2D) then fall asleep (D2H)
+            mma.verify_pattern(w["dev"], w["bytes"], SEED + 1, 0, cnt, stream=stream)
             stream.synchronize()
             verify = {"mismatched_bytes": int(cnt.item()), "checked_bytes": w["bytes"], "on": "device (C4)"}
             if verify["mismatched_bytes"]:
@@ -497,7 +534,8 @@ def main():
         native = {"h2d_gbps": round(w["bytes"] / nh / 1e6, 2), "d2h_gbps": round(w["bytes"] / nd / 1e6, 2),
                   "step_gbps": round(nbytes_step / (nh + nd) / 1e6, 2),
                   "what": "cudaMemcpyBatchAsync of all segments on the user stream (single PCIe link)"
-                  if "fetch" in w else "cudaMemcpyAsync on the user stream (single PCIe link)",
+                  if "fetch" in w else ("one cudaMemcpyAsync per tensor on the user stream (single PCIe link)"
+                                        if "wake" in w else "cudaMemcpyAsync on the user stream (single PCIe link)"),
                   "speedup": round(value / (nbytes_step / (nh + nd) / 1e6), 3)}
 
     # ---- CPU baseline: the oracle on the host cores, bounded sample, N=1 only
@@ -516,7 +554,7 @@ def main():
         "data": "synthetic",
         "config": {"workload": w["desc"], "paths": k, "path_gpus": path_gpus, "target_gpu": 0,
                    "chunk_bytes": args.chunk, "hop": {0: "auto", 1: "ce", 2: "zc"}[args.hop],
-                   "bytes_per_step": nbytes_step, "l2": "inputs (4 GiB per direction) exceed the 126 MB L2; no flush",
+                   "bytes_per_step": nbytes_step, "l2": f"inputs ({w['bytes'] / GiB:.1f} GiB per direction) exceed the 126 MB L2; no flush",
                    "parallelism": f"1 process drives {k} path GPU(s); torchrun ranks>0 idle on gloo",
                    "visible_devices": vis_note, "multipath_error": multipath_error},
         "per_direction": {"h2d_gbps": round(h2d_gbps, 2), "d2h_gbps": round(d2h_gbps, 2),

@@ -88,8 +88,14 @@ def qwen25_14b_tensors():
     48 layers, hidden 5120, intermediate 13824, 40 Q / 8 KV heads (head_dim 128), vocab
     152064, untied embeddings -> 339 tensors, 29,540,067,328 bytes.
     """
-    h, inter, v, L = 5120, 13824, 152064, 48
-    q, kv = 40 * 128, 8 * 128
+    return qwen_like_tensors(layers=48, hidden=5120, inter=13824, q_heads=40, kv_heads=8,
+                             head_dim=128, vocab=152064)
+
+
+def qwen_like_tensors(layers, hidden, inter, q_heads, kv_heads, head_dim, vocab):
+    """Tensor list (name, bytes) of a Qwen2-architecture bf16 model in module order."""
+    h, v, L = hidden, vocab, layers
+    q, kv = q_heads * head_dim, kv_heads * head_dim
     out = [("embed_tokens", v * h * 2)]
     for i in range(L):
         out += [
@@ -103,3 +109,15 @@ def qwen25_14b_tensors():
         ]
     out += [("norm", h * 2), ("lm_head", v * h * 2)]
     return out
+
+
+def packed_layout(tensors, align=256):
+    """Offsets of the tensors packed in module order at `align` bytes (the sleep-mode backup
+    buffer and the device weights share this layout). Returns (offsets, sizes, total)."""
+    offs, sizes, pos = [], [], 0
+    for _, b in tensors:
+        pos = (pos + align - 1) // align * align
+        offs.append(pos)
+        sizes.append(b)
+        pos += b
+    return offs, sizes, pos

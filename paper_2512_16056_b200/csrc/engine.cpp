@@ -22,6 +22,7 @@
 
 #include <algorithm>
 #include <chrono>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <map>
@@ -531,11 +532,33 @@ static int resolve_mode(const Job& j, int mode)
     return mode;
 }
 
+// MMA_TRACE=1: per-call host-time breakdown of the enqueue on stderr.
+struct Trace {
+    bool on;
+    std::chrono::steady_clock::time_point last;
+    std::string s;
+    Trace() : on(getenv("MMA_TRACE") != nullptr), last(std::chrono::steady_clock::now()) {}
+    void mark(const char* what)
+    {
+        if (!on) return;
+        auto now = std::chrono::steady_clock::now();
+        char buf[64];
+        snprintf(buf, sizeof buf, " %s=%.0fus", what, std::chrono::duration<double, std::micro>(now - last).count());
+        s += buf;
+        last = now;
+    }
+    ~Trace()
+    {
+        if (on && !s.empty()) fprintf(stderr, "[mma]%s\n", s.c_str());
+    }
+};
+
 // Enqueue one multipath copy (engine mutex held).
 static int run_job(Job& j)
 {
     Engine& e = E();
     Target& t = e.tgt[j.d];
+    Trace tr;
     const auto t0 = std::chrono::steady_clock::now();
     const cudaMemcpyKind kind = (j.dir == MMA_H2D) ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToHost;
     make_paths(j.d);
@@ -558,6 +581,7 @@ static int run_job(Job& j)
         return cudaErrorInvalidValue;
     t.stats.calls++;
     t.stats.bytes += j.B;
+    tr.mark("plan");
 
     // ---- fallback (a1): the native copy on the user stream (§3.2)
     if (plan.fallback) {
@@ -593,6 +617,7 @@ static int run_job(Job& j)
     }
     // every GPU of the path set gets its streams and peer access before any enqueue
     for (int p = 0; p < P; p++) CK(make_device(ps[p].gpu));
+    tr.mark("scratch");
 
     // ---- per-path chunk lists, ascending
     std::vector<std::vector<uint32_t>> lists(P);
@@ -626,6 +651,7 @@ static int run_job(Job& j)
                 o += lists[p].size() * 4;
             }
     }
+    tr.mark("tables");
     // devices whose kernels read the tables
     bool needs_tab[MMA_MAX_GPUS] = {};
     for (int p = 0; p < P; p++) {
@@ -663,6 +689,7 @@ static int run_job(Job& j)
         CK((cudaError_t)use(e.dev[g].kern, g));
         CK(cudaMemcpyAsync(dtab[g], htab, tab_bytes, cudaMemcpyHostToDevice, e.dev[g].kern));
     }
+    tr.mark("upload");
     // streams that launch table-reading kernels other than kern wait for the upload
     auto after_upload = [&](cudaStream_t s, int g) -> int {
         if (!dtab[g] || s == e.dev[g].kern) return cudaSuccess;
@@ -767,6 +794,7 @@ static int run_job(Job& j)
         }
     }
 
+    tr.mark("direct+zc");
     // ---- CE relay rings (a5, a6 for H2D; a9 for D2H)
     std::vector<int> rp;   // relay paths using rings
     for (int p = 0; p < P; p++)
@@ -861,6 +889,7 @@ static int run_job(Job& j)
         }
     }
 
+    tr.mark("rings");
     // ---- join (a8)
     for (auto& u : used) {
         cudaEvent_t ev = join_event(u.first, u.second);
@@ -881,6 +910,7 @@ static int run_job(Job& j)
         CK(cudaEventRecord(sc.done, j.user));
         sc.pending = true;
     }
+    tr.mark("join");
     t.stats.issue_us += std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t0).count();
     return cudaSuccess;
 }
@@ -962,27 +992,39 @@ static int prepare_segments(int dir, const mma_segment_t* segs, size_t nsegs, in
     j.nseg = nsegs;
     j.vstart.resize(nsegs + 1);
     j.vstart[0] = 0;
+    // destinations must be pairwise disjoint: O(n) when they are in ascending order,
+    // else a sort -- skipped when the table is byte-identical to the last one validated
     bool sorted = true;
+    uintptr_t prev_end = 0;
     for (size_t k = 0; k < nsegs; k++) {
-        if (segs[k].bytes && (!segs[k].src || !segs[k].dst)) return cudaErrorInvalidValue;
+        if (!segs[k].bytes) { j.vstart[k + 1] = j.vstart[k]; continue; }
+        if (!segs[k].src || !segs[k].dst) return cudaErrorInvalidValue;
         j.vstart[k + 1] = j.vstart[k] + segs[k].bytes;
-        if (k && segs[k].bytes && segs[k - 1].bytes && (const char*)segs[k - 1].dst + segs[k - 1].bytes > (const char*)segs[k].dst)
-            sorted = false;
+        if ((uintptr_t)segs[k].dst < prev_end) sorted = false;
+        prev_end = (uintptr_t)segs[k].dst + segs[k].bytes;
     }
     j.B = j.vstart[nsegs];
     if (j.B == 0) return cudaSuccess;
-    if (!sorted) {   // destinations must be pairwise disjoint
-        std::vector<std::pair<uintptr_t, size_t>> v;
-        v.reserve(nsegs);
-        for (size_t k = 0; k < nsegs; k++)
-            if (segs[k].bytes) v.push_back({(uintptr_t)segs[k].dst, segs[k].bytes});
-        std::sort(v.begin(), v.end());
-        for (size_t k = 1; k < v.size(); k++)
-            if (v[k - 1].first + v[k - 1].second > v[k].first) return cudaErrorInvalidValue;
+    if (!sorted) {
+        static std::mutex mu;
+        static std::vector<mma_segment_t> last_ok[2];
+        std::lock_guard<std::mutex> g(mu);
+        std::vector<mma_segment_t>& ok = last_ok[dir];
+        if (!(ok.size() == nsegs && memcmp(ok.data(), segs, nsegs * sizeof(mma_segment_t)) == 0)) {
+            std::vector<std::pair<uintptr_t, size_t>> v;
+            v.reserve(nsegs);
+            for (size_t k = 0; k < nsegs; k++)
+                if (segs[k].bytes) v.push_back({(uintptr_t)segs[k].dst, segs[k].bytes});
+            std::sort(v.begin(), v.end());
+            for (size_t k = 1; k < v.size(); k++)
+                if (v[k - 1].first + v[k - 1].second > v[k].first) return cudaErrorInvalidValue;
+            ok.assign(segs, segs + nsegs);
+        }
     }
-    // classify a bounded sample of the table (first, last, evenly spaced)
+    // classify a bounded sample of the table (first, last, evenly spaced): a pointer query
+    // costs ~0.1 ms, so the sample stays small; the caller guarantees the memory kinds
     j.mapped = true;
-    const size_t nsample = std::min<size_t>(nsegs, 65);
+    const size_t nsample = std::min<size_t>(nsegs, 5);
     for (size_t q = 0; q < nsample; q++) {
         size_t k = (nsample == 1) ? 0 : q * (nsegs - 1) / (nsample - 1);
         if (!segs[k].bytes) continue;
@@ -1216,7 +1258,11 @@ int mma_plan_chunks(const uint32_t* mbps, const int* kinds, const uint64_t* back
 
 // Measure every path alone in each hop mode on the transfer `proto` describes and keep,
 // per path, the faster mode and its rate (integer MB/s, reading R17: llround). Runs the
-// copy (1 + reps) times per (path, mode); the best of `reps` timed runs counts.
+// copy (1 + reps) times per (path, mode); the best of `reps` timed runs counts. The host
+// thread that enqueues a call is one resource shared by all P paths of a multipath call,
+// so a mode's rate is min(device rate, host-issue rate / P): a copy-engine path that needs
+// one descriptor per 32 KiB segment (~0.6 us each) cannot feed 8 links from one thread
+// (DESIGN.md §5.3).
 static int tune_paths(Job proto, int reps, std::vector<uint32_t>& mbps, std::vector<int>& modes)
 {
     Engine& e = E();
@@ -1239,7 +1285,7 @@ static int tune_paths(Job proto, int reps, std::vector<uint32_t>& mbps, std::vec
             if (m == MMA_HOP_ZC && !proto.mapped) continue;
             for (int q = 0; q < P; q++) bw[q] = (q == p) ? 1 : 0;
             md[p] = m;
-            float best = 1e30f;
+            float best = 1e30f, best_issue = 1e30f;
             for (int rep = 0; rep <= reps && rc == cudaSuccess; rep++) {
                 Job j = proto;
                 j.bw_override = bw.data();
@@ -1247,14 +1293,20 @@ static int tune_paths(Job proto, int reps, std::vector<uint32_t>& mbps, std::vec
                 j.no_small_fallback = true;
                 DeviceGuard g(j.user_dev);
                 cudaEventRecord(a, j.user);
+                const auto h0 = std::chrono::steady_clock::now();
                 rc = run_job(j);
+                const float issue_ms = std::chrono::duration<float, std::milli>(std::chrono::steady_clock::now() - h0).count();
                 cudaEventRecord(b, j.user);
                 if (cudaEventSynchronize(b) != cudaSuccess) rc = cudaErrorUnknown;
                 float ms = 0;
                 cudaEventElapsedTime(&ms, a, b);
-                if (rep > 0 && ms > 0) best = std::min(best, ms);   // rep 0 warms up
+                if (rep > 0 && ms > 0) {                             // rep 0 warms up
+                    best = std::min(best, ms);
+                    best_issue = std::min(best_issue, issue_ms);
+                }
             }
-            const float rate = best < 1e29f ? (float)((double)proto.B / (best * 1e-3) / 1e6) : 0.f;
+            const float eff_ms = std::max(best, best_issue * (float)P);
+            const float rate = best < 1e29f ? (float)((double)proto.B / (eff_ms * 1e-3) / 1e6) : 0.f;
             if (rate > best_rate) {
                 best_rate = rate;
                 modes[p] = m;
