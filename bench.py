@@ -31,6 +31,7 @@ ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
 
 METRIC = "H2D/D2H GB/s per target GPU vs path count (1/2/4/8) and % of roofline"
+KNAMES = {0: "zc_copy_kernel", 1: "relay_pull_kernel", 2: "relay_pack_kernel", 3: "zc_dyn_kernel"}
 MiB, GiB = 1 << 20, 1 << 30
 SEED = 0x4D4D41 + 3
 
@@ -48,6 +49,11 @@ def parse():
     ap.add_argument("--hop", type=int, default=0, help="0 auto, 1 copy engine, 2 SM zero-copy")
     ap.add_argument("--no-verify", action="store_true")
     ap.add_argument("--quick", action="store_true", help="skip baselines (profiling runs)")
+    ap.add_argument("--loopback", type=int, default=0,
+                    help="diagnostic: add loopback relay paths through GPU 0 (exercises the multi-path "
+                         "code of the bench on one GPU; the paths share one link)")
+    ap.add_argument("--plan", choices=["contiguous", "interleaved", "dynamic"], default=None,
+                    help="force the plan mode instead of measuring contiguous vs dynamic")
     ap.add_argument("--modes", default="", help="fix the direct path's mode per direction instead of "
                     "measuring, e.g. 'ce,zc' (profiling runs that must match a bench's choice)")
     return ap.parse_args()
@@ -356,7 +362,7 @@ def main():
         cfg.npaths = len(relays) if relays else 1
         for i, g in enumerate(relays or [0]):
             cfg.path_gpus[i] = g          # [0] alone = no relay candidates (self is skipped)
-        cfg.loopback_relays = 0
+        cfg.loopback_relays = args.loopback
         cfg.plan_mode = 0
         cfg.hop_mode[0] = cfg.hop_mode[1] = args.hop
         cfg.debug_log = 0
@@ -423,6 +429,30 @@ def main():
     path_gpus = [p["gpu"] for p in paths]
     tuned = {"h2d": mma.get_paths(0, mma.H2D), "d2h": mma.get_paths(0, mma.D2H)}
 
+    # planned (contiguous, measured bandwidth split) vs GPU-driven dynamic pull: chosen by
+    # measurement when more than one path exists (dynamic applies to all-zero-copy sets)
+    plan_choice = {"chosen": "contiguous"}
+    if len(path_gpus) > 1 and not args.plan:
+        def step_ms(mode):
+            mma.set_plan_mode(mode)
+            run_step(mma, w, 0, stream)
+            stream.synchronize()
+            a = torch.cuda.Event(enable_timing=True)
+            b = torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            for _ in range(2):
+                run_step(mma, w, 0, stream)
+            b.record(stream)
+            b.synchronize()
+            return a.elapsed_time(b) / 2
+        t_static, t_dyn = step_ms(0), step_ms(2)
+        plan_choice = {"contiguous_ms": round(t_static, 3), "dynamic_ms": round(t_dyn, 3),
+                       "chosen": "dynamic" if t_dyn < t_static else "contiguous"}
+        mma.set_plan_mode(2 if t_dyn < t_static else 0)
+    elif args.plan:
+        mma.set_plan_mode({"contiguous": 0, "interleaved": 1, "dynamic": 2}[args.plan])
+        plan_choice = {"chosen": args.plan, "forced": True}
+
     # roofline terms (solo PCIe per path GPU), measured before the timed region
     pcie = {g: pcie_rate(torch, g) for g in path_gpus}
     R_h2d = sum(pcie[g]["h2d"] for g in path_gpus)
@@ -478,7 +508,11 @@ def main():
         def eff_mode(pi):
             m = pi["seg_mode"] if ("fetch" in w and pi["seg_mode"] >= 0) else pi["mode"]
             return m if m else (2 if "fetch" in w else 1)
-        if kpath == 255:      # one relay kernel serves every copy-engine ring of the call
+        if kind == 3:         # dynamic pull: every path's kernel serves the same call
+            moved = w["bytes"] * args.steps
+            ms_list = [(h2d_ms if kdir == 0 else d2h_ms)] * args.steps
+            peak = sum(pcie[g][dname] for g in path_gpus)
+        elif kpath == 255:    # one relay kernel serves every copy-engine ring of the call
             ring_paths = [i for i, pi in enumerate(pinfo) if pi["kind"] == 1 and eff_mode(pi) == 1]
             moved = sum(st["path_bytes"][kdir][i] for i in ring_paths)
             peak = sum(pcie[pinfo[i]["gpu"]][dname] for i in ring_paths)
@@ -489,8 +523,8 @@ def main():
         k_ms = statistics.mean(ms_list)
         achieved = per_launch / (k_ms * 1e-3) / 1e9
         roof = {"bound": "pcie", "achieved": round(achieved, 2), "peak": round(peak, 2), "unit": "GB/s",
-                "frac": round(achieved / peak, 4), "traffic": ncu_traffic(dname, {0: "zc_copy_kernel", 1: "relay_pull_kernel", 2: "relay_pack_kernel"}[kind]),
-                "kernel": {0: "zc_copy_kernel", 1: "relay_pull_kernel", 2: "relay_pack_kernel"}[kind],
+                "frac": round(achieved / peak, 4), "traffic": ncu_traffic(dname, KNAMES[kind]),
+                "kernel": KNAMES[kind] + (" (all paths of the call; duration = the call's events)" if kind == 3 else ""),
                 "direction": dname, "path": kpath, "device": kdev, "launches": len(ms_list),
                 "bytes_per_launch": per_launch, "launch_ms": round(k_ms, 3),
                 "share_of_step": round(sum(ms_list) / ms_total, 4),
@@ -568,6 +602,7 @@ def main():
         "kernel_kinds": kinds,
         "clocks": clk,
         "verify": verify,
+        "plan": plan_choice,
         "modes": {d: [{"gpu": pi["gpu"], "mode": {0: "auto", 1: "ce", 2: "zc"}.get(
             pi["seg_mode"] if ("fetch" in w and pi["seg_mode"] >= 0) else pi["mode"], "?"),
             "mbps": pi["seg_mbps"] if ("fetch" in w and pi["seg_mbps"]) else pi["mbps"]} for pi in v]

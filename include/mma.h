@@ -66,7 +66,11 @@ typedef struct {
     /* extra relay paths through the target GPU itself (loopback rings): a diagnostic
      * mode that exercises the full relay protocol on a single GPU. Default 0. */
     int loopback_relays;
-    /* 0 = contiguous (each path carries one contiguous range), 1 = interleaved */
+    /* 0 = contiguous (each path carries one contiguous range), 1 = interleaved,
+     * 2 = dynamic: when every usable path is in zero-copy mode, the path kernels claim
+     * chunks from one cursor on the target GPU (the paper's pull scheduler, P:549-557,
+     * run by the GPUs); the assignment is observed (delivery log, mma_get_dynamic_counts)
+     * instead of planned; otherwise the contiguous plan is used */
     int plan_mode;
     /* hop mode per direction for every path (mma_hop_t), refined per path by
      * mma_set_path_modes() */
@@ -87,6 +91,7 @@ typedef struct {
     uint64_t kernels;                     /* relay / zero-copy kernel launches */
     double issue_us;                      /* host time spent enqueueing (incl. wait_us) */
     double wait_us;                       /* of which blocked on table-buffer reuse */
+    uint64_t dynamic_calls;               /* calls moved by GPU-driven dynamic pull */
 } mma_stats_t;
 
 /* Fill cfg with defaults (then env MMA_* overrides). */
@@ -134,6 +139,9 @@ int mma_get_paths(int device, mma_dir_t dir, int* gpus, int* kinds, uint32_t* mb
  * planner; bit-exact plan parity runs pin it (SURVEY §7 hard part 7). 0 drops a path. */
 int mma_set_bandwidth(int device, mma_dir_t dir, const uint32_t* mbps, int npaths);
 
+/* Switch the plan mode (mma_config_t.plan_mode) without re-initialising. */
+int mma_set_plan_mode(int mode);
+
 /* Per-path hop mode (mma_hop_t), index-aligned with mma_get_paths. */
 int mma_set_path_modes(int device, mma_dir_t dir, const int* modes, int npaths);
 
@@ -170,6 +178,10 @@ int mma_plan_chunks(const uint32_t* mbps, const int* kinds, const uint64_t* back
  * `device`, as written on the GPU by the final hop (needs cfg.debug_log; synchronises). */
 int mma_get_delivery_log(int device, uint8_t* path_of_chunk, size_t cap, size_t* nchunks);
 
+/* Chunks each path took in the most recent dynamic-pull call to/from `device`
+ * (synchronises; *npaths = 0 if none). */
+int mma_get_dynamic_counts(int device, uint64_t* chunks, int cap, int* npaths);
+
 /* Pinned, mapped, portable host memory, NUMA-placed per cfg.numa_mode (C8). */
 int mma_host_alloc(void** ptr, size_t bytes, unsigned flags);
 int mma_host_free(void* ptr);
@@ -178,8 +190,8 @@ int mma_host_free(void* ptr);
  * on the stream it is launched on. mma_kernel_times synchronises on the recorded launches,
  * returns their durations (ms) and tags in launch order (up to cap; *n = number recorded)
  * and clears the record. tag = kind | direction << 4 | path << 8 | device << 16, kind 0 =
- * zero-copy, 1 = relay pull (H2D), 2 = relay pack (D2H); path 255 = all rings of the
- * launch. */
+ * zero-copy, 1 = relay pull (H2D), 2 = relay pack (D2H), 3 = dynamic-pull zero-copy;
+ * path 255 = all rings of the launch. */
 int mma_set_kernel_timing(int on);
 int mma_kernel_times(float* ms, int* kinds, size_t cap, size_t* n);
 

@@ -12,7 +12,7 @@ from .mma import (  # noqa: F401
     calibrate, default_config, finalize, get_delivery_log, get_last_error, get_paths, get_plan,
     get_stats, host_alloc, host_array, host_free, init, make_segments, memcpy_d2h,
     memcpy_d2h_segments, memcpy_h2d, memcpy_h2d_segments, plan_chunks, reset_stats,
-    set_bandwidth, set_path_modes, tune_segments, set_kernel_timing, kernel_times, fill_pattern,
+    set_bandwidth, set_path_modes, tune_segments, get_dynamic_counts, set_plan_mode, set_kernel_timing, kernel_times, fill_pattern,
     verify_pattern, verify_segments,
 )
 

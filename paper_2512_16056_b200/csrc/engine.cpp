@@ -52,6 +52,8 @@ constexpr unsigned kDefaultSlots = 4;
 constexpr uint32_t kDefaultMbps = 50000;
 constexpr uint32_t kDefaultUnit = 128u << 10;
 constexpr int kDefaultRelayCtas = 8;
+constexpr unsigned kDynSlots = 64;        // per-call claim slots, rotating
+constexpr unsigned kDynSlotWords = 32;    // cursor + counts[MMA_KMAX_RINGS] (+ padding)
 
 struct DeviceGuard {
     int prev = -1;
@@ -118,6 +120,10 @@ struct Target {
     size_t log_cap = 0, log_n = 0;
     Scratch scratch[4];   // table buffers of the last 4 calls (a ring)
     unsigned parity = 0;
+    unsigned long long* dyn = nullptr;        // dynamic-pull slots: cursor + per-path counts
+    unsigned dyn_next = 0;
+    unsigned long long* last_dyn = nullptr;
+    int last_dyn_paths = 0;
 };
 
 struct Engine {
@@ -210,7 +216,7 @@ static int validate_cfg(const mma_config_t& c)
     if (c.ring_slots < 1 || c.ring_slots > 64) return cudaErrorInvalidValue;
     if (c.npaths < 0 || c.npaths > MMA_MAX_PATHS) return cudaErrorInvalidValue;
     if (c.loopback_relays < 0 || c.loopback_relays > 8) return cudaErrorInvalidValue;
-    if (c.plan_mode != PLAN_CONTIGUOUS && c.plan_mode != PLAN_INTERLEAVED) return cudaErrorInvalidValue;
+    if (c.plan_mode < PLAN_CONTIGUOUS || c.plan_mode > PLAN_DYNAMIC) return cudaErrorInvalidValue;
     for (int d = 0; d < 2; d++)
         if (c.hop_mode[d] < MMA_HOP_AUTO || c.hop_mode[d] > MMA_HOP_ZC) return cudaErrorInvalidValue;
     if (c.relay_ctas < 1 || c.relay_ctas > 64) return cudaErrorInvalidValue;
@@ -316,7 +322,12 @@ static void make_paths(int d)
         if (t.paths[dir].size() == ps.size()) {
             bool same = true;
             for (size_t i = 0; i < ps.size(); i++) same &= ps[i].gpu == t.paths[dir][i].gpu && ps[i].kind == t.paths[dir][i].kind;
-            if (same) for (size_t i = 0; i < ps.size(); i++) ps[i].mbps = t.paths[dir][i].mbps;
+            if (same)
+                for (size_t i = 0; i < ps.size(); i++) {   // measured / pinned values survive
+                    ps[i].mbps = t.paths[dir][i].mbps;
+                    ps[i].seg_mbps = t.paths[dir][i].seg_mbps;
+                    ps[i].seg_mode = t.paths[dir][i].seg_mode;
+                }
         }
         t.paths[dir] = ps;
     }
@@ -577,7 +588,8 @@ static int run_job(Job& j)
     }
     const uint64_t thr = j.no_small_fallback ? 0 : e.cfg.fallback_bytes[j.dir];
     Plan plan;
-    if (make_plan(pp.data(), P, j.B, j.C, thr, e.cfg.plan_mode, plan) != 0)
+    const int pmode_plan = e.cfg.plan_mode == PLAN_DYNAMIC ? PLAN_CONTIGUOUS : e.cfg.plan_mode;
+    if (make_plan(pp.data(), P, j.B, j.C, thr, pmode_plan, plan) != 0)
         return cudaErrorInvalidValue;
     t.stats.calls++;
     t.stats.bytes += j.B;
@@ -624,9 +636,19 @@ static int run_job(Job& j)
     for (uint64_t i = 0; i < n; i++) lists[plan.path[i]].push_back((uint32_t)i);
     std::vector<int> mode(P);
     for (int p = 0; p < P; p++) mode[p] = resolve_mode(j, pmode[p]);
+    // GPU-driven dynamic pull when every usable path moves bytes with SMs:
+    // the assignment is then observed (delivery log, per-path counts), not planned
+    bool dynamic = e.cfg.plan_mode == PLAN_DYNAMIC && !plan.fallback;
+    std::vector<char> active(P, 0);
+    for (int p = 0; p < P; p++) {
+        active[p] = !lists[p].empty();
+        if (dynamic && pp[p].mbps && mode[p] != MMA_HOP_ZC) dynamic = false;
+    }
+    if (dynamic)
+        for (int p = 0; p < P; p++) active[p] = pp[p].mbps > 0;
 
     // ---- host tables: chunk lists (interleaved plans) and the segment table
-    const bool need_ctab = e.cfg.plan_mode == PLAN_INTERLEAVED;
+    const bool need_ctab = e.cfg.plan_mode == PLAN_INTERLEAVED && !dynamic;
     const uint64_t seg_words = j.contiguous ? 0 : (j.nseg + 1) + 2 * j.nseg;
     const size_t tab_bytes = (need_ctab ? n * 4 : 0) + ((need_ctab && (n & 1)) ? 4 : 0) + seg_words * 8;
     std::vector<size_t> ctab_off(P, 0);
@@ -655,7 +677,7 @@ static int run_job(Job& j)
     // devices whose kernels read the tables
     bool needs_tab[MMA_MAX_GPUS] = {};
     for (int p = 0; p < P; p++) {
-        if (lists[p].empty()) continue;
+        if (!active[p]) continue;
         const bool relay = ps[p].kind == MMA_PATH_RELAY;
         if (mode[p] == MMA_HOP_ZC) needs_tab[ps[p].gpu] = true;
         else if (relay) needs_tab[j.dir == MMA_H2D ? j.d : ps[p].gpu] = true;
@@ -743,8 +765,48 @@ static int run_job(Job& j)
         t.log_n = 0;
     }
 
+    // ---- dynamic pull: one claim cursor per call in d's memory, one kernel per path GPU
+    if (dynamic) {
+        if (!t.dyn) {
+            DeviceGuard g(j.d);
+            CK(cudaMalloc(&t.dyn, kDynSlots * kDynSlotWords * sizeof(unsigned long long)));
+        }
+        unsigned long long* slot = t.dyn + (t.dyn_next++ % kDynSlots) * kDynSlotWords;
+        cudaStream_t zs = e.dev[j.d].zc;
+        CK((cudaError_t)use(zs, j.d));
+        cudaEvent_t zeroed = join_event(zs, j.d);
+        {
+            DeviceGuard g(j.d);
+            CK(cudaMemsetAsync(slot, 0, kDynSlotWords * sizeof(unsigned long long), zs));
+            CK(cudaEventRecord(zeroed, zs));
+        }
+        t.last_dyn = slot;
+        t.last_dyn_paths = P;
+        t.stats.dynamic_calls++;
+        for (int p = 0; p < P; p++) {
+            if (!active[p]) continue;
+            const int g = ps[p].gpu;
+            cudaStream_t s = e.dev[g].zc;
+            CK((cudaError_t)use(s, g));
+            CK((cudaError_t)after_upload(s, g));
+            DeviceGuard dg(g);
+            if (s != zs) CK(cudaStreamWaitEvent(s, zeroed, 0));
+            DynLaunchArg a{};
+            a.v = vstream_on(g);
+            a.nchunks = n;
+            a.cursor = slot;
+            a.counts = slot + 1;
+            a.path = (uint32_t)p;
+            a.log = log;
+            const unsigned grid = (unsigned)std::min<uint64_t>(n, (uint64_t)e.dev[g].sms * 4);
+            KTimer kt(g, s, 3 | (j.dir << 4) | (p << 8));
+            CK(launch_zc_dyn(a, grid, s));
+            t.stats.kernels++;
+        }
+    }
+
     // ---- direct path and zero-copy paths (a4, a7)
-    for (int p = 0; p < P; p++) {
+    for (int p = 0; p < P && !dynamic; p++) {
         if (lists[p].empty()) continue;
         const int g = ps[p].gpu;
         CK(make_device(g));
@@ -799,7 +861,7 @@ static int run_job(Job& j)
     std::vector<int> rp;   // relay paths using rings
     for (int p = 0; p < P; p++)
         if (!lists[p].empty() && ps[p].kind == MMA_PATH_RELAY && mode[p] == MMA_HOP_CE) rp.push_back(p);
-    if (!rp.empty()) {
+    if (!rp.empty() && !dynamic) {
         if (!e.wait64 || !e.write64) return MMA_ERR_NO_MEMOPS;
         const uint32_t S = e.cfg.ring_slots;
         const uint64_t upc = (j.C + e.unit_bytes - 1) / e.unit_bytes;
@@ -1094,6 +1156,7 @@ int mma_finalize(void)
         for (int dir = 0; dir < 2; dir++)
             for (int p = 0; p < MMA_MAX_PATHS; p++) free_ring(t.rings[dir][p]);
         if (t.log) { DeviceGuard dg(d); cudaFree(t.log); }
+        if (t.dyn) { DeviceGuard dg(d); cudaFree(t.dyn); }
         for (auto& sc : t.scratch) {
             for (int g2 = 0; g2 < MMA_MAX_GPUS; g2++)
                 if (sc.dev[g2]) { DeviceGuard dg(g2); cudaFree(sc.dev[g2]); }
@@ -1161,6 +1224,15 @@ int mma_get_paths(int device, mma_dir_t dir, int* gpus, int* kinds, uint32_t* mb
     return cudaSuccess;
 }
 
+int mma_set_plan_mode(int mode)
+{
+    CK((cudaError_t)ensure_init());
+    if (mode < PLAN_CONTIGUOUS || mode > PLAN_DYNAMIC) return cudaErrorInvalidValue;
+    std::lock_guard<std::mutex> g(E().mu);
+    E().cfg.plan_mode = mode;
+    return cudaSuccess;
+}
+
 int mma_get_segment_tuning(int device, mma_dir_t dir, uint32_t* mbps, int* modes, int cap, int* npaths)
 {
     CK((cudaError_t)ensure_init());
@@ -1224,7 +1296,8 @@ int mma_get_plan(int device, mma_dir_t dir, size_t bytes, uint8_t* path_of_chunk
     std::vector<PlanPath> pp;
     for (auto& p : ps) pp.push_back(PlanPath{p.kind == MMA_PATH_DIRECT, p.mbps, 0});
     Plan plan;
-    if (make_plan(pp.data(), (int)pp.size(), bytes, e.cfg.chunk_bytes[dir], e.cfg.fallback_bytes[dir], e.cfg.plan_mode, plan))
+    if (make_plan(pp.data(), (int)pp.size(), bytes, e.cfg.chunk_bytes[dir], e.cfg.fallback_bytes[dir],
+                  e.cfg.plan_mode == PLAN_DYNAMIC ? PLAN_CONTIGUOUS : e.cfg.plan_mode, plan))
         return cudaErrorInvalidValue;
     *nchunks = plan.n;
     if (fallback) *fallback = plan.fallback;
@@ -1460,6 +1533,24 @@ int mma_kernel_times(float* ms, int* kinds, size_t cap, size_t* n)
     g_kpending.clear();
     *n = k;
     return rc;
+}
+
+int mma_get_dynamic_counts(int device, uint64_t* chunks, int cap, int* npaths)
+{
+    CK((cudaError_t)ensure_init());
+    Engine& e = E();
+    if (device < 0 || device >= e.ndev) return cudaErrorInvalidDevice;
+    if (!npaths) return cudaErrorInvalidValue;
+    std::lock_guard<std::mutex> g(e.mu);
+    Target& t = e.tgt[device];
+    *npaths = t.last_dyn ? t.last_dyn_paths : 0;
+    if (!t.last_dyn || !chunks) return cudaSuccess;
+    unsigned long long c[MMA_KMAX_RINGS] = {};
+    DeviceGuard dg(device);
+    CK(cudaDeviceSynchronize());
+    CK(cudaMemcpy(c, t.last_dyn + 1, sizeof c, cudaMemcpyDeviceToHost));
+    for (int p = 0; p < t.last_dyn_paths && p < cap; p++) chunks[p] = c[p];
+    return cudaSuccess;
 }
 
 int mma_get_last_error(void)

@@ -15,6 +15,7 @@ namespace mma {
 cudaError_t launch_relay(const RelayLaunchArg& a, bool pull, unsigned grid, cudaStream_t s);
 // kernels/zerocopy.cu
 cudaError_t launch_zc(const ZcLaunchArg& a, unsigned grid, cudaStream_t s);
+cudaError_t launch_zc_dyn(const DynLaunchArg& a, unsigned grid, cudaStream_t s);
 // kernels/verify.cu
 cudaError_t launch_fill(void* p, uint64_t bytes, uint64_t seed, uint64_t offset, cudaStream_t s);
 cudaError_t launch_verify(const void* p, uint64_t bytes, uint64_t seed, uint64_t offset,

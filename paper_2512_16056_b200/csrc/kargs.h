@@ -54,6 +54,18 @@ struct RelayLaunchArg {
     uint64_t timeout_ns;         // bound on every spin
 };
 
+// GPU-driven dynamic pull (the paper's pull scheduler, §3.4.2,
+// moved onto the GPU): every path's kernel claims whole chunks from one cursor in the
+// target's memory until the chunks run out, so faster or less loaded links take more.
+struct DynLaunchArg {
+    VStreamArg v;
+    uint64_t nchunks;
+    unsigned long long* cursor;   // per-call claim cursor (target GPU memory, zeroed per call)
+    unsigned long long* counts;   // [MMA_KMAX_RINGS] chunks taken per path (same slot)
+    uint32_t path;
+    uint8_t* log;
+};
+
 struct ZcLaunchArg {
     VStreamArg v;
     ChunkListArg chunks;

@@ -33,6 +33,39 @@ __global__ void __launch_bounds__(kThreads) zc_copy_kernel(const __grid_constant
     }
 }
 
+// Dynamic pull: a CTA claims the next chunk with a system-scope atomic on the target's
+// cursor (a peer atomic over NVLink for relays), moves it, and claims again. The claim for
+// the next chunk is issued before the current chunk is copied, so the ~2 us NVLink
+// round trip of the atomic overlaps the copy.
+__global__ void __launch_bounds__(kThreads) zc_dyn_kernel(const __grid_constant__ DynLaunchArg A)
+{
+    __shared__ unsigned long long s_next;
+    const uint64_t C = A.v.C, B = A.v.B;
+    if (threadIdx.x == 0) s_next = atomicAdd_system(A.cursor, 1ull);
+    __syncthreads();
+    uint64_t i = s_next;
+    unsigned long long taken = 0;
+    while (i < A.nchunks) {
+        __syncthreads();                                   // everyone has read s_next
+        if (threadIdx.x == 0) s_next = atomicAdd_system(A.cursor, 1ull);
+        const uint64_t off = i * C;
+        const uint64_t len = (B - off < C) ? B - off : C;
+        v_copy<V_DIRECT>(A.v, off, off + len, nullptr);
+        if (threadIdx.x == 0 && A.log) A.log[i] = (uint8_t)A.path;
+        taken++;
+        __syncthreads();
+        i = s_next;
+    }
+    if (threadIdx.x == 0 && taken) atomicAdd_system(&A.counts[A.path], taken);
+}
+
+cudaError_t launch_zc_dyn(const DynLaunchArg& a, unsigned grid, cudaStream_t s)
+{
+    if (grid == 0) return cudaSuccess;
+    zc_dyn_kernel<<<grid, kThreads, 0, s>>>(a);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_zc(const ZcLaunchArg& a, unsigned grid, cudaStream_t s)
 {
     if (grid == 0) return cudaSuccess;

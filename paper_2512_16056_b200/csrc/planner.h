@@ -14,7 +14,7 @@ struct PlanPath {
     uint64_t backlog;   // bytes already queued on the path
 };
 
-enum PlanMode { PLAN_CONTIGUOUS = 0, PLAN_INTERLEAVED = 1 };
+enum PlanMode { PLAN_CONTIGUOUS = 0, PLAN_INTERLEAVED = 1, PLAN_DYNAMIC = 2 /* engine only */ };
 
 struct Plan {
     bool fallback = false;          // one piece [0, B) on path 0 (native)

@@ -26,7 +26,7 @@ SYMBOLS = [
     "mma_get_delivery_log", "mma_host_alloc", "mma_host_free", "mma_get_stats",
     "mma_reset_stats", "mma_get_last_error", "mma_error_string", "mma_fill_pattern",
     "mma_verify_pattern", "mma_verify_segments", "mma_set_kernel_timing", "mma_kernel_times",
-    "mma_tune_segments", "mma_get_segment_tuning",
+    "mma_tune_segments", "mma_get_segment_tuning", "mma_get_dynamic_counts", "mma_set_plan_mode",
 ]
 
 
@@ -51,7 +51,7 @@ class Stats(C.Structure):
         ("calls", C.c_uint64), ("fallbacks", C.c_uint64), ("bytes", C.c_uint64),
         ("path_bytes", (C.c_uint64 * MAX_PATHS) * 2), ("path_chunks", (C.c_uint64 * MAX_PATHS) * 2),
         ("relay_bytes", C.c_uint64), ("kernels", C.c_uint64), ("issue_us", C.c_double),
-        ("wait_us", C.c_double),
+        ("wait_us", C.c_double), ("dynamic_calls", C.c_uint64),
     ]
 
 
@@ -103,6 +103,8 @@ def lib():
         L.mma_tune_segments.argtypes = [C.POINTER(Segment), sz, C.c_int, C.c_int, vp, C.c_int]
         L.mma_kernel_times.argtypes = [vp, vp, sz, C.POINTER(sz)]
         L.mma_get_segment_tuning.argtypes = [C.c_int, C.c_int, vp, vp, C.c_int, C.POINTER(C.c_int)]
+        L.mma_get_dynamic_counts.argtypes = [C.c_int, vp, C.c_int, C.POINTER(C.c_int)]
+        L.mma_set_plan_mode.argtypes = [C.c_int]
         _lib = L
     return _lib
 
@@ -285,7 +287,20 @@ def get_stats(device: int) -> dict:
     return dict(calls=s.calls, fallbacks=s.fallbacks, bytes=s.bytes,
                 path_bytes=[list(x) for x in s.path_bytes], path_chunks=[list(x) for x in s.path_chunks],
                 relay_bytes=s.relay_bytes, kernels=s.kernels, issue_us=s.issue_us,
-                wait_us=s.wait_us)
+                wait_us=s.wait_us, dynamic_calls=s.dynamic_calls)
+
+
+def set_plan_mode(mode: int) -> None:
+    """0 contiguous, 1 interleaved, 2 GPU-driven dynamic pull."""
+    _check(lib().mma_set_plan_mode(mode), "mma_set_plan_mode")
+
+
+def get_dynamic_counts(device: int):
+    """Chunks each path took in the last dynamic-pull call (synchronises)."""
+    buf = (C.c_uint64 * MAX_PATHS)()
+    n = C.c_int()
+    _check(lib().mma_get_dynamic_counts(device, buf, MAX_PATHS, C.byref(n)), "mma_get_dynamic_counts")
+    return [int(buf[i]) for i in range(n.value)]
 
 
 def reset_stats(device: int) -> None:
