@@ -135,6 +135,32 @@ class Clocks:
 
 # ------------------------------------------------------------------- workloads ---
 
+def numa_info(torch, gpus):
+    """Host NUMA nodes and each path GPU's node (sysfs), for the report."""
+    nodes = sorted(p.name for p in Path("/sys/devices/system/node").glob("node[0-9]*"))
+    gmap = {}
+    for g in gpus:
+        try:
+            pr = torch.cuda.get_device_properties(g)
+            bdf = f"{pr.pci_domain_id:04x}:{pr.pci_bus_id:02x}:{pr.pci_device_id:02x}.0"
+            gmap[str(g)] = int(Path(f"/sys/bus/pci/devices/{bdf}/numa_node").read_text().strip())
+        except (OSError, ValueError, AttributeError):
+            gmap[str(g)] = None
+    return {"nodes": len(nodes), "gpu_node": gmap}
+
+
+def host_buffer(torch, mma, nbytes):
+    """Pinned, mapped host buffer from mma_host_alloc (C8): with more than one NUMA node its
+    pages are interleaved across the nodes, so one socket's DRAM does not serve every link.
+    Owned by the engine for the life of the process."""
+    nodes = len(list(Path("/sys/devices/system/node").glob("node[0-9]*")))
+    ptr = mma.host_alloc(nbytes)
+    t = torch.from_numpy(mma.host_array(ptr, nbytes))
+    how = f"mma_host_alloc, pages interleaved over {nodes} NUMA nodes" if nodes > 1 else \
+        "mma_host_alloc (1 NUMA node: default placement)"
+    return t, how
+
+
 def kv_workload(torch, mma, tokens, dev):
     """Config 3 shapes from mma_inputs.workloads; host pool filled with the seeded pattern
     by the device generator (fill kernel) and copied to the pinned pool."""
@@ -142,7 +168,7 @@ def kv_workload(torch, mma, tokens, dev):
     from mma_inputs import workloads as W
     shape = W.KVShape() if tokens == 32768 else W.scaled_kv(tokens)
     ho, do, sb, hpool, dbytes = W.kv_segments(shape, SEED)
-    host = torch.empty(hpool, dtype=torch.uint8).pin_memory()
+    host, how = host_buffer(torch, mma, hpool)
     tmp = torch.empty(min(hpool, GiB), dtype=torch.uint8, device=dev)
     for a in range(0, hpool, tmp.numel()):
         n = min(tmp.numel(), hpool - a)
@@ -157,7 +183,7 @@ def kv_workload(torch, mma, tokens, dev):
             f"{len(ho)} x {sb // 1024} KiB segments (layer, K|V, 16-token block) scattered by a seeded "
             f"permutation in a {hpool / GiB:.0f} GiB pinned pool -> paged device cache")
     return dict(host=host, cache=cache, fetch=fetch, offload=offload, bytes=int(lens.sum()), ho=ho, do=do,
-                sb=sb, desc=desc, nsegs=len(ho))
+                sb=sb, desc=desc + f"; pool: {how}", nsegs=len(ho))
 
 
 def wake_workload(torch, mma, dev):
@@ -341,6 +367,9 @@ def main():
     dev = torch.device("cuda:0")
     torch.cuda.set_device(0)
     stream = torch.cuda.Stream(device=0)
+    early = mma.default_config()
+    early.numa_mode = 2                      # host buffers interleaved when there are nodes
+    mma.init(early)
 
     if args.workload == "kv":
         w = kv_workload(torch, mma, args.tokens, dev)
@@ -366,6 +395,7 @@ def main():
         cfg.plan_mode = 0
         cfg.hop_mode[0] = cfg.hop_mode[1] = args.hop
         cfg.debug_log = 0
+        cfg.numa_mode = 2
         mma.init(cfg)
         return cfg
 
@@ -603,6 +633,7 @@ def main():
         "clocks": clk,
         "verify": verify,
         "plan": plan_choice,
+        "numa": numa_info(torch, sorted(set(path_gpus))),
         "modes": {d: [{"gpu": pi["gpu"], "mode": {0: "auto", 1: "ce", 2: "zc"}.get(
             pi["seg_mode"] if ("fetch" in w and pi["seg_mode"] >= 0) else pi["mode"], "?"),
             "mbps": pi["seg_mbps"] if ("fetch" in w and pi["seg_mbps"]) else pi["mbps"]} for pi in v]

@@ -1,0 +1,46 @@
+"""C8: mma_host_alloc buffers are pinned, mapped and usable by every path mode."""
+import numpy as np
+import pytest
+
+import mma_inputs
+
+from gpu_util import configure
+
+torch = pytest.importorskip("torch")
+pytestmark = [pytest.mark.gpu, pytest.mark.timeout(300)]
+
+MiB = 1 << 20
+
+
+@pytest.fixture(scope="module")
+def mma():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2512_16056_b200 as m
+    yield m
+    m.finalize()
+
+
+@pytest.mark.parametrize("numa", [0, 1, 2])
+@pytest.mark.parametrize("hop", [1, 2])
+def test_host_alloc_roundtrip(mma, numa, hop):
+    cfg = configure(mma, loopback=1, chunk=MiB, hop=(hop, hop), debug=0)
+    cfg.numa_mode = numa
+    mma.init(cfg)
+    B = 24 * MiB + 5
+    ptr = mma.host_alloc(B)
+    assert ptr % (2 << 20) == 0
+    h = mma.host_array(ptr, B)
+    h[:] = mma_inputs.pattern_bytes(3, B)
+    d = torch.empty(B, dtype=torch.uint8, device="cuda")
+    mma.memcpy_h2d(d, ptr, B)
+    back = mma.host_alloc(B)
+    mma.memcpy_d2h(back, d, B)
+    torch.cuda.synchronize()
+    assert np.array_equal(mma.host_array(back, B), h)
+    t = torch.from_numpy(mma.host_array(ptr, B))      # the bench's torch view of the buffer
+    assert torch.equal(d.cpu(), t)
+    mma.host_free(ptr)
+    mma.host_free(back)
+    with pytest.raises(mma.MMAError):
+        mma.host_free(ptr)                             # double free is rejected
