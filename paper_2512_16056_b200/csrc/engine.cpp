@@ -451,6 +451,10 @@ struct DmaBatch {
     {
         if (dst.empty()) return cudaSuccess;
         if (dst.size() == 1) return (int)cudaMemcpyAsync(dst[0], src[0], len[0], kind, s);
+        if (s == nullptr || s == cudaStreamLegacy) {   // the batch API rejects the legacy stream
+            for (size_t i = 0; i < dst.size(); i++) CK(cudaMemcpyAsync(dst[i], src[i], len[i], kind, s));
+            return cudaSuccess;
+        }
         cudaMemcpyAttributes at;
         memset(&at, 0, sizeof(at));
         at.srcAccessOrder = cudaMemcpySrcAccessOrderStream;
@@ -1099,6 +1103,11 @@ static int prepare_segments(int dir, const mma_segment_t* segs, size_t nsegs, in
         if (hk == 1) return cudaErrorInvalidValue;
         if (hk == 2) j.mapped = false;   // pageable: CE only
         j.mapped = j.mapped && m;
+    }
+    if (nsegs == 1) {   // one segment is a contiguous copy (the kernels' nseg == 1 form)
+        j.contiguous = true;
+        j.src0 = (const char*)segs[0].src;
+        j.dst0 = (char*)segs[0].dst;
     }
     return cudaSuccess;
 }

@@ -1,0 +1,100 @@
+"""Randomised GPU parity sweep: seeded random transfers (size, chunk, ring slots, loopback
+relay count, per-path modes, plan mode, direction, contiguous or scattered, pointer
+offsets) through the C ABI, each compared byte for byte with the oracle moving the same
+transfer with the same assignment (the planned one, or the observed one in dynamic mode).
+Rings persist across cases, so sequence bases and slot reuse vary too."""
+import numpy as np
+import pytest
+
+import mma_inputs
+
+from gpu_util import configure
+
+torch = pytest.importorskip("torch")
+pytestmark = [pytest.mark.gpu, pytest.mark.timeout(900)]
+
+KiB, MiB = 1 << 10, 1 << 20
+
+
+@pytest.fixture(scope="module")
+def mma():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import os
+    os.environ.setdefault("MMA_SPIN_TIMEOUT_MS", "8000")
+    import paper_2512_16056_b200 as m
+    yield m
+    m.finalize()
+
+
+def test_random_transfers(mma, orc):
+    rng = np.random.default_rng(20261017)
+    pool_h = torch.empty(48 * MiB, dtype=torch.uint8).pin_memory()
+    mma_inputs.fill_pattern(pool_h.numpy(), 123)
+    pool_d = torch.empty(48 * MiB, dtype=torch.uint8, device="cuda")
+    pool_d.copy_(pool_h)
+    hn = pool_h.numpy()
+    for case in range(200):
+        lb = int(rng.integers(0, 4))
+        P = 1 + lb
+        C = int(rng.choice([4 * KiB, 64 * KiB, 256 * KiB, MiB, 3 * MiB]))
+        S = int(rng.integers(1, 5))
+        plan_mode = int(rng.choice([0, 1, 2]))
+        modes = [int(x) for x in rng.choice([1, 2], P)]
+        if plan_mode == 2 and rng.random() < 0.7:
+            modes = [2] * P
+        bw = [int(x) for x in rng.integers(1, 6, P)]
+        dirn = int(rng.integers(0, 2))
+        scattered = rng.random() < 0.4
+        configure(mma, loopback=lb, chunk=C, slots=S, plan_mode=plan_mode, hop=(1, 1))
+        mma.set_path_modes(0, dirn, modes)
+        mma.set_bandwidth(0, dirn, bw)
+        if scattered:
+            nseg = int(rng.integers(1, 200))
+            lens = rng.integers(1, 96 * KiB, nseg)
+            src_off = rng.integers(0, 40 * MiB, nseg)
+            order = rng.permutation(nseg)
+            dst_off = np.zeros(nseg, np.int64)
+            pos = int(rng.integers(0, 64))
+            for k in order:
+                dst_off[k] = pos
+                pos += int(lens[k]) + int(rng.integers(0, 100))
+            span = pos + 64
+        else:
+            B = int(rng.integers(1, 24 * MiB))
+            lens = np.array([B])
+            src_off = np.array([int(rng.integers(0, 8 * MiB))])
+            dst_off = np.array([int(rng.integers(0, 64))])
+            span = B + 128
+        B = int(lens.sum())
+        print(f"case {case}: lb={lb} C={C} S={S} plan={plan_mode} modes={modes} bw={bw} dir={dirn} "
+              f"scattered={scattered} nseg={len(lens)} B={B}", flush=True)
+        if dirn == 0:      # H2D: host pool -> fresh device buffer
+            dst = torch.full((span,), 0xA5, dtype=torch.uint8, device="cuda")
+            segs, n = mma.make_segments(pool_h.data_ptr() + src_off, dst.data_ptr() + dst_off, lens)
+            src_np = hn
+        else:              # D2H: device pool -> fresh pinned buffer
+            dst = torch.full((span,), 0xA5, dtype=torch.uint8).pin_memory()
+            segs, n = mma.make_segments(pool_d.data_ptr() + src_off, dst.data_ptr() + dst_off, lens)
+            src_np = hn      # pool_d holds the same bytes
+        if scattered or rng.random() < 0.5:
+            (mma.memcpy_h2d_segments if dirn == 0 else mma.memcpy_d2h_segments)(segs, n, 0)
+        elif dirn == 0:
+            mma.memcpy_h2d(dst.data_ptr() + int(dst_off[0]), pool_h.data_ptr() + int(src_off[0]), B)
+        else:
+            mma.memcpy_d2h(dst.data_ptr() + int(dst_off[0]), pool_d.data_ptr() + int(src_off[0]), B)
+        torch.cuda.synchronize()
+        assert mma.get_last_error() == 0, case
+        dynamic = plan_mode == 2 and all(m == 2 for m in modes)
+        if dynamic:
+            path = np.frombuffer(mma.get_delivery_log(0), dtype=np.uint8)
+            assert path.size == (B + C - 1) // C and (path < P).all(), case
+        else:
+            rc, path, _, fb = orc.plan(bw, B, C, 0, 0 if plan_mode == 2 else plan_mode)
+            assert rc == 0
+        exp = np.full(span, 0xA5, dtype=np.uint8)
+        osegs, on = orc.segments_from_arrays(src_np.ctypes.data + src_off, exp.ctypes.data + dst_off, lens)
+        assert orc.move(osegs, on, C, bw, path, S=S) == 0
+        got = dst.cpu().numpy() if dirn == 0 else dst.numpy()
+        assert np.array_equal(got, exp), (case, dict(lb=lb, C=C, S=S, plan=plan_mode, modes=modes, dir=dirn,
+                                                     scattered=scattered, B=B))
