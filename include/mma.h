@@ -81,6 +81,12 @@ typedef struct {
     int numa_mode;
     /* record the per-chunk delivery log (debug; off in timed runs) */
     int debug_log;
+    /* backlog ledger: plan each call against the bytes other in-flight
+     * calls still have queued on every link ("remaining tasks in the buffer provide an
+     * effective proxy for link congestion", §2.3), and never relay through a GPU
+     * whose own link still carries its own target's direct bytes ("direct path first",
+     * P:564-565 §3.4.2). 0 = off, 1 = on (default). */
+    int ledger;
 } mma_config_t;
 
 typedef struct {

@@ -135,6 +135,19 @@ struct Engine {
     DevRes dev[MMA_MAX_GPUS];
     Target tgt[MMA_MAX_GPUS];
     std::map<cudaStream_t, cudaEvent_t> join_ev;   // join event per engine stream
+    // backlog ledger (NEXT-1): bytes in flight per (direction, link GPU), and of those the
+    // link's own target's direct bytes; each call's share is retired when its done event
+    // (recorded on the user stream at the join) has completed
+    struct InFlight {
+        cudaEvent_t done;
+        int dev, dir;
+        uint64_t bytes[MMA_MAX_GPUS];
+        uint64_t own[MMA_MAX_GPUS];
+    };
+    std::vector<InFlight> inflight;
+    std::vector<std::pair<int, cudaEvent_t>> free_events;
+    uint64_t ledger[2][MMA_MAX_GPUS] = {};
+    uint64_t ledger_own[2][MMA_MAX_GPUS] = {};
     int* err = nullptr;              // mapped pinned host word (sticky async error)
     PFN_memop64 wait64 = nullptr, write64 = nullptr;
     uint64_t timeout_ns = 20ull * 1000 * 1000 * 1000;
@@ -184,6 +197,7 @@ static void apply_env(mma_config_t* c)
     c->relay_ctas = env_int("MMA_RELAY_CTAS", c->relay_ctas);
     c->numa_mode = env_int("MMA_NUMA", c->numa_mode);
     c->debug_log = env_int("MMA_DEBUG_LOG", c->debug_log);
+    c->ledger = env_int("MMA_LEDGER", c->ledger);
     if (const char* s = getenv("MMA_PATHS")) {   // comma-separated relay GPU ids
         c->npaths = 0;
         for (const char* p = s; *p && c->npaths < MMA_MAX_PATHS;) {
@@ -207,6 +221,7 @@ static void defaults(mma_config_t* c)
     c->plan_mode = PLAN_CONTIGUOUS;
     c->hop_mode[0] = c->hop_mode[1] = MMA_HOP_AUTO;
     c->relay_ctas = kDefaultRelayCtas;
+    c->ledger = 1;
 }
 
 static int validate_cfg(const mma_config_t& c)
@@ -547,6 +562,65 @@ static int resolve_mode(const Job& j, int mode)
     return mode;
 }
 
+// ---- backlog ledger (NEXT-1) ---------------------------------------------------------
+static void ledger_retire()
+{
+    Engine& e = E();
+    for (size_t i = 0; i < e.inflight.size();) {
+        auto& f = e.inflight[i];
+        if (cudaEventQuery(f.done) == cudaErrorNotReady) { i++; continue; }
+        cudaGetLastError();
+        for (int g = 0; g < MMA_MAX_GPUS; g++) {
+            e.ledger[f.dir][g] -= f.bytes[g];
+            e.ledger_own[f.dir][g] -= f.own[g];
+        }
+        e.free_events.push_back({f.dev, f.done});
+        e.inflight[i] = e.inflight.back();
+        e.inflight.pop_back();
+    }
+}
+
+static int ledger_add(int dir, int user_dev, cudaStream_t user, const uint64_t* bytes, const uint64_t* own)
+{
+    Engine& e = E();
+    Engine::InFlight f{};
+    f.dir = dir;
+    f.dev = user_dev;
+    for (size_t i = 0; i < e.free_events.size(); i++)
+        if (e.free_events[i].first == user_dev) {
+            f.done = e.free_events[i].second;
+            e.free_events.erase(e.free_events.begin() + i);
+            break;
+        }
+    DeviceGuard g(user_dev);
+    if (!f.done) CK(cudaEventCreateWithFlags(&f.done, cudaEventDisableTiming));
+    CK(cudaEventRecord(f.done, user));
+    for (int k = 0; k < MMA_MAX_GPUS; k++) {
+        f.bytes[k] = bytes[k];
+        f.own[k] = own[k];
+        e.ledger[dir][k] += bytes[k];
+        e.ledger_own[dir][k] += own[k];
+    }
+    e.inflight.push_back(f);
+    return cudaSuccess;
+}
+
+// Planner inputs of target d's paths: bandwidth (0 = not usable for this call) and
+// backlog from the ledger.
+static void ledger_inputs(int d, int dir, const std::vector<PathState>& ps, std::vector<PlanPath>& pp)
+{
+    Engine& e = E();
+    if (!e.cfg.ledger) return;
+    ledger_retire();
+    for (size_t p = 0; p < ps.size(); p++) {
+        const int g = ps[p].gpu;
+        pp[p].backlog = e.ledger[dir][g];
+        // direct path first: a GPU whose link still carries its own target's bytes takes
+        // no relay work for another target
+        if (ps[p].kind == MMA_PATH_RELAY && g != d && e.ledger_own[dir][g] > 0) pp[p].mbps = 0;
+    }
+}
+
 // MMA_TRACE=1: per-call host-time breakdown of the enqueue on stderr.
 struct Trace {
     bool on;
@@ -591,6 +665,7 @@ static int run_job(Job& j)
         if (j.mode_override) pmode[p] = j.mode_override[p];
     }
     const uint64_t thr = j.no_small_fallback ? 0 : e.cfg.fallback_bytes[j.dir];
+    if (!j.bw_override) ledger_inputs(j.d, j.dir, ps, pp);
     Plan plan;
     const int pmode_plan = e.cfg.plan_mode == PLAN_DYNAMIC ? PLAN_CONTIGUOUS : e.cfg.plan_mode;
     if (make_plan(pp.data(), P, j.B, j.C, thr, pmode_plan, plan) != 0)
@@ -611,6 +686,11 @@ static int run_job(Job& j)
             t.stats.path_bytes[j.dir][0] += j.B;
             t.stats.path_chunks[j.dir][0] += 1;
             t.log_n = 0;
+            if (e.cfg.ledger) {
+                uint64_t lb[MMA_MAX_GPUS] = {}, lo[MMA_MAX_GPUS] = {};
+                lb[j.d] = lo[j.d] = j.B;
+                CK(ledger_add(j.dir, j.user_dev, j.user, lb, lo));
+            }
             t.stats.issue_us += std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t0).count();
             return cudaSuccess;
         }
@@ -976,6 +1056,16 @@ static int run_job(Job& j)
         CK(cudaEventRecord(sc.done, j.user));
         sc.pending = true;
     }
+    if (e.cfg.ledger && !dynamic) {
+        uint64_t lb[MMA_MAX_GPUS] = {}, lo[MMA_MAX_GPUS] = {};
+        for (int p = 0; p < P; p++) {
+            uint64_t bytes_p = 0;
+            for (uint32_t i : lists[p]) { uint64_t o, l; j.extent(i, &o, &l); bytes_p += l; }
+            lb[ps[p].gpu] += bytes_p;
+            if (ps[p].kind == MMA_PATH_DIRECT) lo[ps[p].gpu] += bytes_p;
+        }
+        CK(ledger_add(j.dir, j.user_dev, j.user, lb, lo));
+    }
     tr.mark("join");
     t.stats.issue_us += std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t0).count();
     return cudaSuccess;
@@ -1176,6 +1266,12 @@ int mma_finalize(void)
     }
     for (auto& kv : e.join_ev) cudaEventDestroy(kv.second);
     e.join_ev.clear();
+    for (auto& f : e.inflight) cudaEventDestroy(f.done);
+    for (auto& f : e.free_events) cudaEventDestroy(f.second);
+    e.inflight.clear();
+    e.free_events.clear();
+    memset(e.ledger, 0, sizeof e.ledger);
+    memset(e.ledger_own, 0, sizeof e.ledger_own);
     for (int d = 0; d < e.ndev; d++) {
         DevRes& r = e.dev[d];
         if (!r.made) continue;
@@ -1304,6 +1400,7 @@ int mma_get_plan(int device, mma_dir_t dir, size_t bytes, uint8_t* path_of_chunk
     auto& ps = e.tgt[device].paths[dir];
     std::vector<PlanPath> pp;
     for (auto& p : ps) pp.push_back(PlanPath{p.kind == MMA_PATH_DIRECT, p.mbps, 0});
+    ledger_inputs(device, dir, ps, pp);
     Plan plan;
     if (make_plan(pp.data(), (int)pp.size(), bytes, e.cfg.chunk_bytes[dir], e.cfg.fallback_bytes[dir],
                   e.cfg.plan_mode == PLAN_DYNAMIC ? PLAN_CONTIGUOUS : e.cfg.plan_mode, plan))

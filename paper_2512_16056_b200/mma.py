@@ -43,6 +43,7 @@ class Config(C.Structure):
         ("relay_ctas", C.c_int),
         ("numa_mode", C.c_int),
         ("debug_log", C.c_int),
+        ("ledger", C.c_int),
     ]
 
 

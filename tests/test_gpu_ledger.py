@@ -1,0 +1,67 @@
+"""Backlog ledger: a call is planned against the bytes that calls still in
+flight have queued on each link. The plan with a pending call must equal the oracle's
+earliest-finish plan with that backlog as input, and return to the unloaded plan once the
+pending call has completed."""
+import numpy as np
+import pytest
+
+from gpu_util import configure, pinned
+
+torch = pytest.importorskip("torch")
+pytestmark = [pytest.mark.gpu, pytest.mark.timeout(300)]
+
+MiB = 1 << 20
+
+
+@pytest.fixture(scope="module")
+def mma():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2512_16056_b200 as m
+    yield m
+    m.finalize()
+
+
+def test_plan_sees_in_flight_backlog(mma, orc):
+    C = MiB
+    configure(mma, loopback=1, chunk=C, plan_mode=1, hop=(1, 1), debug=0)
+    bw = [3, 1]
+    mma.set_bandwidth(0, mma.H2D, bw)
+    B = 8 * C
+    rc, idle_plan, _, _ = orc.plan(bw, B, C, 0, 1)
+    assert mma.get_plan(0, mma.H2D, B)[0] == idle_plan.tobytes()
+    # a call held behind a sleeping kernel stays in flight
+    Ba = 24 * MiB
+    src = pinned(torch, Ba, seed=2)
+    dst = torch.empty(Ba, dtype=torch.uint8, device="cuda")
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        torch.cuda._sleep(3_000_000_000)          # ~1.5 s at 1.9 GHz
+        mma.memcpy_h2d(dst, src, Ba, stream=s)
+    busy_path, _ = mma.get_plan(0, mma.H2D, B)
+    # both paths live on GPU 0's link: each carries the pending call's Ba bytes
+    rc, exp, _, _ = orc.plan(bw, B, C, 0, 1, backlog=[Ba, Ba])
+    assert busy_path == exp.tobytes()
+    assert busy_path != idle_plan.tobytes()
+    s.synchronize()
+    assert torch.equal(dst.cpu(), src[:Ba])
+    assert mma.get_plan(0, mma.H2D, B)[0] == idle_plan.tobytes()
+
+
+def test_ledger_off_ignores_backlog(mma, orc):
+    C = MiB
+    cfg = configure(mma, loopback=1, chunk=C, plan_mode=1, hop=(1, 1), debug=0)
+    cfg.ledger = 0
+    mma.init(cfg)
+    bw = [3, 1]
+    mma.set_bandwidth(0, mma.H2D, bw)
+    B = 8 * C
+    rc, idle_plan, _, _ = orc.plan(bw, B, C, 0, 1)
+    src = pinned(torch, 24 * MiB, seed=2)
+    dst = torch.empty(24 * MiB, dtype=torch.uint8, device="cuda")
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        torch.cuda._sleep(1_000_000_000)
+        mma.memcpy_h2d(dst, src, 24 * MiB, stream=s)
+    assert mma.get_plan(0, mma.H2D, B)[0] == idle_plan.tobytes()
+    s.synchronize()
