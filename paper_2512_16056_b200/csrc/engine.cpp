@@ -152,6 +152,10 @@ struct Engine {
     PFN_memop64 wait64 = nullptr, write64 = nullptr;
     uint64_t timeout_ns = 20ull * 1000 * 1000 * 1000;
     uint32_t unit_bytes = kDefaultUnit;
+    // fault injection (tests only, MMA_FAULT_DROP_PUBLISH=g): the hop-1 publish of global
+    // ring chunk g is never issued, so the relay kernel must time out, record the sticky
+    // error and release the ring instead of hanging (SURVEY §5 failure detection)
+    long long fault_drop_publish = -1;
 };
 
 Engine& E()
@@ -295,6 +299,8 @@ static int do_init(const mma_config_t* cfg)
         memset(e.err, 0, sizeof(int) * 16);
         e.timeout_ns = (uint64_t)env_size("MMA_SPIN_TIMEOUT_MS", 20000) * 1000000ull;
         e.unit_bytes = (uint32_t)env_size("MMA_UNIT_BYTES", kDefaultUnit);
+        const char* f = getenv("MMA_FAULT_DROP_PUBLISH");
+        e.fault_drop_publish = f ? atoll(f) : -1;
         if (e.unit_bytes < 4096) e.unit_bytes = 4096;
     }
     e.cfg = c;
@@ -1023,7 +1029,9 @@ static int run_job(Job& j)
                         return cudaErrorUnknown;
                     j.pieces(off, off + len, [&](const Piece& x) { batch.add(slot + (x.v - off), x.src, x.len); });
                     CK((cudaError_t)batch.issue(kind, hs));
-                    if (e.write64((CUstream)hs, (CUdeviceptr)&r->seq[s], g + 1, 0) != CUDA_SUCCESS) return cudaErrorUnknown;
+                    if ((long long)g != e.fault_drop_publish &&
+                        e.write64((CUstream)hs, (CUdeviceptr)&r->seq[s], g + 1, 0) != CUDA_SUCCESS)
+                        return cudaErrorUnknown;
                 } else {
                     if (e.wait64((CUstream)hs, (CUdeviceptr)&r->seq[s], g + 1, CU_STREAM_WAIT_VALUE_GEQ) != CUDA_SUCCESS)
                         return cudaErrorUnknown;

@@ -5,10 +5,10 @@
 // H2D, on the TARGET GPU d (relay_pull_kernel): for each chunk g of ring r, in order,
 //   poll seq_r[s] (relay-local, ld.acquire.sys over NVLink) until it equals g + 1, then
 //   pull the slot stage_r[s] (peer HBM) with 16-byte coalesced loads and store it to the
-//   destination pieces of v, then st.release.sys credit_r[s] = g + 1.
+//   destination pieces of v, then publishes credit_r[s] = g + 1 (system fence + atomicMax).
 // D2H, on the RELAY GPU r (relay_pack_kernel): for each chunk g, wait credit_r[s] >=
 //   g - S + 1 (the relay's copy engine drained the slot), pull the chunk's source pieces
-//   from d's HBM over NVLink into stage_r[s], then st.release.sys seq_r[s] = g + 1.
+//   from d's HBM over NVLink into stage_r[s], then publishes seq_r[s] = g + 1.
 //
 // "a dependency established between these operations to guarantee the correctness and
 // ordering of data transfer" is the seq flag; the credit flag is the buffer
@@ -28,12 +28,21 @@ namespace mma {
 
 constexpr uint64_t kReleaseAll = 1ull << 62;
 
+// Flags the kernel publishes only ever grow (atomicMax after a system fence = a release
+// that cannot move a flag backwards), so once a ring is aborted every copy-engine wait on
+// it passes even if a CTA still finishing a chunk publishes afterwards.
+__device__ __forceinline__ void publish(uint64_t* flag, uint64_t v)
+{
+    __threadfence_system();
+    atomicMax_system(reinterpret_cast<unsigned long long*>(flag), (unsigned long long)v);
+}
+
 __device__ __forceinline__ void ring_abort(const RelayLaunchArg& A, const RingArg& R)
 {
     if (A.err) atomicExch_system(A.err, 1);
     for (uint32_t s = 0; s < R.S; s++) {
-        st_release_sys(&R.credit[s], kReleaseAll);
-        st_release_sys(&R.seq[s], kReleaseAll);
+        publish(&R.credit[s], kReleaseAll);
+        publish(&R.seq[s], kReleaseAll);
     }
 }
 
@@ -103,9 +112,8 @@ __device__ __forceinline__ void relay_body(const RelayLaunchArg& A)
             if (old == units_j - 1) {                      // last unit of chunk g
                 atomicExch(&R.cnt[s], 0u);
                 if (A.log) A.log[i] = (uint8_t)R.path;
-                __threadfence_system();
-                if (PULL) st_release_sys(&R.credit[s], g + 1);   // slot free for g + S
-                else st_release_sys(&R.seq[s], g + 1);           // chunk g staged
+                if (PULL) publish(&R.credit[s], g + 1);   // slot free for g + S
+                else publish(&R.seq[s], g + 1);           // chunk g staged
             }
         }
     }
