@@ -17,14 +17,16 @@ PRELOAD = PKG / "libmma_preload.so"
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
 SOURCES = [
-    CSRC / "engine.cpp",
+    CSRC / "plane.cpp",
+    CSRC / "api.cpp",
+    CSRC / "tune.cpp",
     CSRC / "planner.cpp",
     CSRC / "hostmem.cpp",
     CSRC / "kernels" / "relay.cu",
     CSRC / "kernels" / "zerocopy.cu",
     CSRC / "kernels" / "verify.cu",
 ]
-HEADERS = [ROOT / "include" / "mma.h", CSRC / "engine.h", CSRC / "kargs.h", CSRC / "planner.h",
+HEADERS = [ROOT / "include" / "mma.h", CSRC / "engine.h", CSRC / "plane.h", CSRC / "kargs.h", CSRC / "planner.h",
            CSRC / "kernels" / "copy.cuh", CSRC / "preload.cpp"]
 
 FLAGS = [

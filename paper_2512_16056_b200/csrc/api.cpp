@@ -1,0 +1,511 @@
+// api.cpp — C7: the C ABI of include/mma.h (validation, fallback decisions, pointer
+// classification) over the data plane in plane.cpp. Every function returns a cudaError_t
+// value as int; validation happens before anything is enqueued.
+#include "plane.h"
+
+namespace mma {
+
+// ------------------------------------------------------------- classification ---
+
+
+static int stream_device(cudaStream_t s, int* dev)
+{
+    cudaError_t e = cudaStreamGetDevice(s, dev);
+    if (e != cudaSuccess) { cudaGetLastError(); return cudaGetDevice(dev); }
+    return cudaSuccess;
+}
+
+// type of pointer: 0 host pinned (mapped if *mapped), 1 device (dev), 2 pageable/unknown
+static int classify(const void* p, int* dev, bool* mapped)
+{
+    cudaPointerAttributes a;
+    cudaError_t e = cudaPointerGetAttributes(&a, p);
+    if (e != cudaSuccess) { cudaGetLastError(); return 2; }
+    if (a.type == cudaMemoryTypeDevice) { *dev = a.device; return 1; }
+    if (a.type == cudaMemoryTypeHost) { *mapped = a.devicePointer != nullptr; return 0; }
+    return 2;
+}
+
+static int copy_contiguous(int dir, void* dst, const void* src, size_t bytes, cudaStream_t stream)
+{
+    CK((cudaError_t)ensure_init());
+    if (int se = sticky()) return se;
+    if (bytes == 0) return cudaSuccess;
+    if (!dst || !src) return cudaErrorInvalidValue;
+    Engine& e = E();
+    const void* dptr = (dir == MMA_H2D) ? dst : src;
+    const void* hptr = (dir == MMA_H2D) ? src : dst;
+    int d = -1, hd = -1;
+    bool mapped = false, dummy = false;
+    if (classify(dptr, &d, &dummy) != 1) return cudaErrorInvalidValue;
+    const int hk = classify(hptr, &hd, &mapped);
+    if (hk == 1) return cudaErrorInvalidValue;   // device -> device is not this API
+    const cudaMemcpyKind kind = (dir == MMA_H2D) ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToHost;
+    cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+    cudaStreamIsCapturing(stream, &cap);
+    if (hk == 2 || cap != cudaStreamCaptureStatusNone || d >= e.ndev)
+        return (int)cudaMemcpyAsync(dst, src, bytes, kind, stream);   // native (R7)
+    Job j;
+    j.dir = dir;
+    j.d = d;
+    j.user = stream;
+    CK((cudaError_t)stream_device(stream, &j.user_dev));
+    j.B = bytes;
+    j.C = e.cfg.chunk_bytes[dir];
+    j.contiguous = true;
+    j.src0 = (const char*)src;
+    j.dst0 = (char*)dst;
+    j.mapped = mapped;
+    std::lock_guard<std::mutex> g(e.mu);
+    CK((cudaError_t)make_device(d));
+    return run_job(j);
+}
+
+// Validate a segment table and fill the job (no engine lock held).
+int prepare_segments(int dir, const mma_segment_t* segs, size_t nsegs, int device,
+                            cudaStream_t stream, Job& j)
+{
+    Engine& e = E();
+    j.dir = dir;
+    j.d = device;
+    j.user = stream;
+    CK((cudaError_t)stream_device(stream, &j.user_dev));
+    j.C = e.cfg.chunk_bytes[dir];
+    j.contiguous = false;
+    j.segs = segs;
+    j.nseg = nsegs;
+    j.vstart.resize(nsegs + 1);
+    j.vstart[0] = 0;
+    // destinations must be pairwise disjoint: O(n) when they are in ascending order,
+    // else a sort -- skipped when the table is byte-identical to the last one validated
+    bool sorted = true;
+    uintptr_t prev_end = 0;
+    for (size_t k = 0; k < nsegs; k++) {
+        if (!segs[k].bytes) { j.vstart[k + 1] = j.vstart[k]; continue; }
+        if (!segs[k].src || !segs[k].dst) return cudaErrorInvalidValue;
+        j.vstart[k + 1] = j.vstart[k] + segs[k].bytes;
+        if ((uintptr_t)segs[k].dst < prev_end) sorted = false;
+        prev_end = (uintptr_t)segs[k].dst + segs[k].bytes;
+    }
+    j.B = j.vstart[nsegs];
+    if (j.B == 0) return cudaSuccess;
+    if (!sorted) {
+        static std::mutex mu;
+        static std::vector<mma_segment_t> last_ok[2];
+        std::lock_guard<std::mutex> g(mu);
+        std::vector<mma_segment_t>& ok = last_ok[dir];
+        if (!(ok.size() == nsegs && memcmp(ok.data(), segs, nsegs * sizeof(mma_segment_t)) == 0)) {
+            std::vector<std::pair<uintptr_t, size_t>> v;
+            v.reserve(nsegs);
+            for (size_t k = 0; k < nsegs; k++)
+                if (segs[k].bytes) v.push_back({(uintptr_t)segs[k].dst, segs[k].bytes});
+            std::sort(v.begin(), v.end());
+            for (size_t k = 1; k < v.size(); k++)
+                if (v[k - 1].first + v[k - 1].second > v[k].first) return cudaErrorInvalidValue;
+            ok.assign(segs, segs + nsegs);
+        }
+    }
+    // classify a bounded sample of the table (first, last, evenly spaced): a pointer query
+    // costs ~0.1 ms, so the sample stays small; the caller guarantees the memory kinds
+    j.mapped = true;
+    const size_t nsample = std::min<size_t>(nsegs, 5);
+    for (size_t q = 0; q < nsample; q++) {
+        size_t k = (nsample == 1) ? 0 : q * (nsegs - 1) / (nsample - 1);
+        if (!segs[k].bytes) continue;
+        const void* dp = (dir == MMA_H2D) ? segs[k].dst : segs[k].src;
+        const void* hp = (dir == MMA_H2D) ? segs[k].src : segs[k].dst;
+        int d = -1, hd = -1;
+        bool m = false, dummy = false;
+        if (classify(dp, &d, &dummy) != 1 || d != device) return cudaErrorInvalidValue;
+        int hk = classify(hp, &hd, &m);
+        if (hk == 1) return cudaErrorInvalidValue;
+        if (hk == 2) j.mapped = false;   // pageable: CE only
+        j.mapped = j.mapped && m;
+    }
+    if (nsegs == 1) {   // one segment is a contiguous copy (the kernels' nseg == 1 form)
+        j.contiguous = true;
+        j.src0 = (const char*)segs[0].src;
+        j.dst0 = (char*)segs[0].dst;
+    }
+    return cudaSuccess;
+}
+
+static int copy_segments(int dir, const mma_segment_t* segs, size_t nsegs, int device, cudaStream_t stream)
+{
+    CK((cudaError_t)ensure_init());
+    if (int se = sticky()) return se;
+    Engine& e = E();
+    if (nsegs == 0) return cudaSuccess;
+    if (!segs) return cudaErrorInvalidValue;
+    if (device < 0 || device >= e.ndev) return cudaErrorInvalidDevice;
+    Job j;
+    CK(prepare_segments(dir, segs, nsegs, device, stream, j));
+    if (j.B == 0) return cudaSuccess;
+    std::lock_guard<std::mutex> g(e.mu);
+    CK((cudaError_t)make_device(device));
+    return run_job(j);
+}
+
+}  // namespace mma
+
+// ====================================================================== C ABI (C7) ===
+
+using namespace mma;
+
+extern "C" {
+
+int mma_default_config(mma_config_t* cfg)
+{
+    if (!cfg) return cudaErrorInvalidValue;
+    defaults(cfg);
+    apply_env(cfg);
+    return cudaSuccess;
+}
+
+int mma_init(const mma_config_t* cfg)
+{
+    std::lock_guard<std::mutex> g(E().mu);
+    return do_init(cfg);
+}
+
+int mma_finalize(void)
+{
+    Engine& e = E();
+    std::lock_guard<std::mutex> g(e.mu);
+    if (!e.inited) return cudaSuccess;
+    for (int d = 0; d < e.ndev; d++) {
+        if (!e.dev[d].made) continue;
+        DeviceGuard dg(d);
+        cudaDeviceSynchronize();
+    }
+    for (int d = 0; d < e.ndev; d++) {
+        Target& t = e.tgt[d];
+        for (int dir = 0; dir < 2; dir++)
+            for (int p = 0; p < MMA_MAX_PATHS; p++) free_ring(t.rings[dir][p]);
+        if (t.log) { DeviceGuard dg(d); cudaFree(t.log); }
+        if (t.dyn) { DeviceGuard dg(d); cudaFree(t.dyn); }
+        for (auto& sc : t.scratch) {
+            for (int g2 = 0; g2 < MMA_MAX_GPUS; g2++)
+                if (sc.dev[g2]) { DeviceGuard dg(g2); cudaFree(sc.dev[g2]); }
+            if (sc.host) cudaFreeHost(sc.host);
+            if (sc.done) cudaEventDestroy(sc.done);
+        }
+        t = Target();
+    }
+    for (auto& kv : e.join_ev) cudaEventDestroy(kv.second);
+    e.join_ev.clear();
+    for (auto& f : e.inflight) cudaEventDestroy(f.done);
+    for (auto& f : e.free_events) cudaEventDestroy(f.second);
+    e.inflight.clear();
+    e.free_events.clear();
+    memset(e.ledger, 0, sizeof e.ledger);
+    memset(e.ledger_own, 0, sizeof e.ledger_own);
+    for (int d = 0; d < e.ndev; d++) {
+        DevRes& r = e.dev[d];
+        if (!r.made) continue;
+        DeviceGuard dg(d);
+        cudaStreamDestroy(r.kern);
+        cudaStreamDestroy(r.hop[0]);
+        cudaStreamDestroy(r.hop[1]);
+        cudaStreamDestroy(r.direct);
+        cudaStreamDestroy(r.zc);
+        cudaEventDestroy(r.fork);
+        r = DevRes();
+    }
+    if (e.err) { cudaFreeHost(e.err); e.err = nullptr; }
+    e.inited = false;
+    return cudaSuccess;
+}
+
+int mma_memcpy_h2d(void* dst, const void* src, size_t bytes, mma_stream_t stream)
+{
+    return copy_contiguous(MMA_H2D, dst, src, bytes, (cudaStream_t)stream);
+}
+
+int mma_memcpy_d2h(void* dst, const void* src, size_t bytes, mma_stream_t stream)
+{
+    return copy_contiguous(MMA_D2H, dst, src, bytes, (cudaStream_t)stream);
+}
+
+int mma_memcpy_h2d_segments(const mma_segment_t* segs, size_t nsegs, int dst_device, mma_stream_t stream)
+{
+    return copy_segments(MMA_H2D, segs, nsegs, dst_device, (cudaStream_t)stream);
+}
+
+int mma_memcpy_d2h_segments(const mma_segment_t* segs, size_t nsegs, int src_device, mma_stream_t stream)
+{
+    return copy_segments(MMA_D2H, segs, nsegs, src_device, (cudaStream_t)stream);
+}
+
+int mma_get_paths(int device, mma_dir_t dir, int* gpus, int* kinds, uint32_t* mbps, int* modes,
+                  int cap, int* npaths)
+{
+    CK((cudaError_t)ensure_init());
+    Engine& e = E();
+    if (device < 0 || device >= e.ndev) return cudaErrorInvalidDevice;
+    if ((dir != MMA_H2D && dir != MMA_D2H) || !npaths) return cudaErrorInvalidValue;
+    std::lock_guard<std::mutex> g(e.mu);
+    make_paths(device);
+    auto& ps = e.tgt[device].paths[dir];
+    *npaths = (int)ps.size();
+    for (int i = 0; i < (int)ps.size() && i < cap; i++) {
+        if (gpus) gpus[i] = ps[i].gpu;
+        if (kinds) kinds[i] = ps[i].kind;
+        if (mbps) mbps[i] = ps[i].mbps;
+        if (modes) modes[i] = ps[i].mode;
+    }
+    return cudaSuccess;
+}
+
+int mma_set_plan_mode(int mode)
+{
+    CK((cudaError_t)ensure_init());
+    if (mode < PLAN_CONTIGUOUS || mode > PLAN_DYNAMIC) return cudaErrorInvalidValue;
+    std::lock_guard<std::mutex> g(E().mu);
+    E().cfg.plan_mode = mode;
+    return cudaSuccess;
+}
+
+int mma_get_segment_tuning(int device, mma_dir_t dir, uint32_t* mbps, int* modes, int cap, int* npaths)
+{
+    CK((cudaError_t)ensure_init());
+    Engine& e = E();
+    if (device < 0 || device >= e.ndev) return cudaErrorInvalidDevice;
+    if ((dir != MMA_H2D && dir != MMA_D2H) || !npaths) return cudaErrorInvalidValue;
+    std::lock_guard<std::mutex> g(e.mu);
+    make_paths(device);
+    auto& ps = e.tgt[device].paths[dir];
+    *npaths = (int)ps.size();
+    for (int i = 0; i < (int)ps.size() && i < cap; i++) {
+        if (mbps) mbps[i] = ps[i].seg_mbps;
+        if (modes) modes[i] = ps[i].seg_mode;
+    }
+    return cudaSuccess;
+}
+
+int mma_set_bandwidth(int device, mma_dir_t dir, const uint32_t* mbps, int npaths)
+{
+    CK((cudaError_t)ensure_init());
+    Engine& e = E();
+    if (device < 0 || device >= e.ndev) return cudaErrorInvalidDevice;
+    if ((dir != MMA_H2D && dir != MMA_D2H) || !mbps) return cudaErrorInvalidValue;
+    std::lock_guard<std::mutex> g(e.mu);
+    make_paths(device);
+    auto& ps = e.tgt[device].paths[dir];
+    if (npaths != (int)ps.size()) return cudaErrorInvalidValue;
+    bool any = false;
+    for (int i = 0; i < npaths; i++) any |= mbps[i] > 0;
+    if (!any) return cudaErrorInvalidValue;
+    for (int i = 0; i < npaths; i++) { ps[i].mbps = mbps[i]; ps[i].seg_mbps = 0; }
+    return cudaSuccess;
+}
+
+int mma_set_path_modes(int device, mma_dir_t dir, const int* modes, int npaths)
+{
+    CK((cudaError_t)ensure_init());
+    Engine& e = E();
+    if (device < 0 || device >= e.ndev) return cudaErrorInvalidDevice;
+    if ((dir != MMA_H2D && dir != MMA_D2H) || !modes) return cudaErrorInvalidValue;
+    std::lock_guard<std::mutex> g(e.mu);
+    make_paths(device);
+    auto& ps = e.tgt[device].paths[dir];
+    if (npaths != (int)ps.size()) return cudaErrorInvalidValue;
+    for (int i = 0; i < npaths; i++)
+        if (modes[i] < MMA_HOP_AUTO || modes[i] > MMA_HOP_ZC) return cudaErrorInvalidValue;
+    for (int i = 0; i < npaths; i++) { ps[i].mode = modes[i]; ps[i].seg_mode = -1; }
+    return cudaSuccess;
+}
+
+int mma_get_plan(int device, mma_dir_t dir, size_t bytes, uint8_t* path_of_chunk, size_t cap,
+                 size_t* nchunks, int* fallback)
+{
+    CK((cudaError_t)ensure_init());
+    Engine& e = E();
+    if (device < 0 || device >= e.ndev) return cudaErrorInvalidDevice;
+    if ((dir != MMA_H2D && dir != MMA_D2H) || !nchunks) return cudaErrorInvalidValue;
+    std::lock_guard<std::mutex> g(e.mu);
+    make_paths(device);
+    auto& ps = e.tgt[device].paths[dir];
+    std::vector<PlanPath> pp;
+    for (auto& p : ps) pp.push_back(PlanPath{p.kind == MMA_PATH_DIRECT, p.mbps, 0});
+    ledger_inputs(device, dir, ps, pp);
+    Plan plan;
+    if (make_plan(pp.data(), (int)pp.size(), bytes, e.cfg.chunk_bytes[dir], e.cfg.fallback_bytes[dir],
+                  e.cfg.plan_mode == PLAN_DYNAMIC ? PLAN_CONTIGUOUS : e.cfg.plan_mode, plan))
+        return cudaErrorInvalidValue;
+    *nchunks = plan.n;
+    if (fallback) *fallback = plan.fallback;
+    if (path_of_chunk) {
+        if (cap < plan.n) return cudaErrorInvalidValue;
+        memcpy(path_of_chunk, plan.path.data(), plan.n);
+    }
+    return cudaSuccess;
+}
+
+int mma_plan_chunks(const uint32_t* mbps, const int* kinds, const uint64_t* backlog, int npaths,
+                    uint64_t bytes, uint64_t chunk_bytes, uint64_t thr, int mode,
+                    uint8_t* path_of_chunk, size_t cap, size_t* nchunks, int* fallback)
+{
+    if (!mbps || !kinds || !nchunks || npaths < 1 || npaths > 255) return cudaErrorInvalidValue;
+    std::vector<PlanPath> pp(npaths);
+    for (int p = 0; p < npaths; p++) {
+        if (kinds[p] != MMA_PATH_DIRECT && kinds[p] != MMA_PATH_RELAY) return cudaErrorInvalidValue;
+        pp[p] = PlanPath{kinds[p] == MMA_PATH_DIRECT, mbps[p], backlog ? backlog[p] : 0};
+    }
+    Plan plan;
+    if (make_plan(pp.data(), npaths, bytes, chunk_bytes, thr, mode, plan)) return cudaErrorInvalidValue;
+    *nchunks = plan.n;
+    if (fallback) *fallback = plan.fallback;
+    if (path_of_chunk) {
+        if (cap < plan.n) return cudaErrorInvalidValue;
+        memcpy(path_of_chunk, plan.path.data(), plan.n);
+    }
+    return cudaSuccess;
+}
+
+int mma_get_delivery_log(int device, uint8_t* path_of_chunk, size_t cap, size_t* nchunks)
+{
+    CK((cudaError_t)ensure_init());
+    Engine& e = E();
+    if (device < 0 || device >= e.ndev) return cudaErrorInvalidDevice;
+    if (!nchunks) return cudaErrorInvalidValue;
+    std::lock_guard<std::mutex> g(e.mu);
+    Target& t = e.tgt[device];
+    *nchunks = t.log_n;
+    if (!t.log_n || !path_of_chunk) return cudaSuccess;
+    if (cap < t.log_n) return cudaErrorInvalidValue;
+    DeviceGuard dg(device);
+    CK(cudaDeviceSynchronize());
+    CK(cudaMemcpy(path_of_chunk, t.log, t.log_n, cudaMemcpyDeviceToHost));
+    return cudaSuccess;
+}
+
+int mma_host_alloc(void** ptr, size_t bytes, unsigned flags)
+{
+    CK((cudaError_t)ensure_init());
+    (void)flags;
+    return host_alloc(ptr, bytes, E().cfg.numa_mode, 0);
+}
+
+int mma_host_free(void* ptr) { return host_free(ptr); }
+
+int mma_get_stats(int device, mma_stats_t* out)
+{
+    CK((cudaError_t)ensure_init());
+    Engine& e = E();
+    if (device < 0 || device >= e.ndev) return cudaErrorInvalidDevice;
+    if (!out) return cudaErrorInvalidValue;
+    std::lock_guard<std::mutex> g(e.mu);
+    *out = e.tgt[device].stats;
+    return cudaSuccess;
+}
+
+int mma_reset_stats(int device)
+{
+    CK((cudaError_t)ensure_init());
+    Engine& e = E();
+    if (device < 0 || device >= e.ndev) return cudaErrorInvalidDevice;
+    std::lock_guard<std::mutex> g(e.mu);
+    e.tgt[device].stats = mma_stats_t{};
+    return cudaSuccess;
+}
+
+int mma_set_kernel_timing(int on)
+{
+    std::lock_guard<std::mutex> g(E().mu);
+    g_ktime = on != 0;
+    return cudaSuccess;
+}
+
+int mma_kernel_times(float* ms, int* kinds, size_t cap, size_t* n)
+{
+    if (!n) return cudaErrorInvalidValue;
+    std::lock_guard<std::mutex> g(E().mu);
+    size_t k = 0;
+    int rc = cudaSuccess;
+    for (auto& r : g_kpending) {
+        DeviceGuard dg(r.dev);
+        float t = 0.f;
+        if (cudaEventSynchronize(r.b) != cudaSuccess || cudaEventElapsedTime(&t, r.a, r.b) != cudaSuccess)
+            rc = cudaErrorUnknown;
+        if (k < cap) {
+            if (ms) ms[k] = t;
+            if (kinds) kinds[k] = r.kind;
+        }
+        k++;
+        cudaEventDestroy(r.a);
+        cudaEventDestroy(r.b);
+    }
+    g_kpending.clear();
+    *n = k;
+    return rc;
+}
+
+int mma_get_dynamic_counts(int device, uint64_t* chunks, int cap, int* npaths)
+{
+    CK((cudaError_t)ensure_init());
+    Engine& e = E();
+    if (device < 0 || device >= e.ndev) return cudaErrorInvalidDevice;
+    if (!npaths) return cudaErrorInvalidValue;
+    std::lock_guard<std::mutex> g(e.mu);
+    Target& t = e.tgt[device];
+    *npaths = t.last_dyn ? t.last_dyn_paths : 0;
+    if (!t.last_dyn || !chunks) return cudaSuccess;
+    unsigned long long c[MMA_KMAX_RINGS] = {};
+    DeviceGuard dg(device);
+    CK(cudaDeviceSynchronize());
+    CK(cudaMemcpy(c, t.last_dyn + 1, sizeof c, cudaMemcpyDeviceToHost));
+    for (int p = 0; p < t.last_dyn_paths && p < cap; p++) chunks[p] = c[p];
+    return cudaSuccess;
+}
+
+int mma_get_last_error(void)
+{
+    if (!E().inited) return cudaSuccess;
+    return sticky();
+}
+
+const char* mma_error_string(int err)
+{
+    if (err == MMA_ERR_RELAY_TIMEOUT) return "mma: relay kernel spin timed out (sticky; mma_finalize to reset)";
+    if (err == MMA_ERR_NO_MEMOPS) return "mma: CUDA stream memory operations unavailable";
+    return cudaGetErrorString((cudaError_t)err);
+}
+
+int mma_fill_pattern(void* ptr, size_t bytes, uint64_t seed, uint64_t offset, mma_stream_t s)
+{
+    if (bytes && !ptr) return cudaErrorInvalidValue;
+    return (int)launch_fill(ptr, bytes, seed, offset, (cudaStream_t)s);
+}
+
+int mma_verify_pattern(const void* ptr, size_t bytes, uint64_t seed, uint64_t offset,
+                       uint64_t* mismatches, mma_stream_t s)
+{
+    if ((bytes && !ptr) || !mismatches) return cudaErrorInvalidValue;
+    return (int)launch_verify(ptr, bytes, seed, offset, mismatches, (cudaStream_t)s);
+}
+
+int mma_verify_segments(void* const* dst, const uint64_t* offset, const uint64_t* bytes,
+                        size_t nsegs, uint64_t seed, uint64_t* mismatches, mma_stream_t s)
+{
+    if (!mismatches || (nsegs && (!dst || !offset || !bytes))) return cudaErrorInvalidValue;
+    if (!nsegs) return cudaSuccess;
+    uint64_t* tab = nullptr;
+    CK(cudaMallocAsync((void**)&tab, 3 * nsegs * 8, (cudaStream_t)s));
+    CK(cudaMemcpyAsync(tab, dst, nsegs * 8, cudaMemcpyHostToDevice, (cudaStream_t)s));
+    CK(cudaMemcpyAsync(tab + nsegs, offset, nsegs * 8, cudaMemcpyHostToDevice, (cudaStream_t)s));
+    CK(cudaMemcpyAsync(tab + 2 * nsegs, bytes, nsegs * 8, cudaMemcpyHostToDevice, (cudaStream_t)s));
+    CK(launch_verify_segments(tab, tab + nsegs, tab + 2 * nsegs, nsegs, seed, mismatches, (cudaStream_t)s));
+    CK(cudaFreeAsync(tab, (cudaStream_t)s));
+    return cudaSuccess;
+}
+
+// Raise the hardware queue count before the first CUDA context exists, so the engine's
+// streams do not alias one queue (SURVEY §7 hard part 4).
+__attribute__((constructor)) static void mma_preinit(void)
+{
+    setenv("CUDA_DEVICE_MAX_CONNECTIONS", "32", 0);
+}
+
+}  // extern "C"
+

@@ -1,5 +1,5 @@
 // engine.h — internal interfaces between the C ABI (api.cpp), the data plane
-// (engine.cpp), the host allocator (hostmem.cpp) and the sm_100a kernels (kernels/*.cu).
+// (plane.cpp, api.cpp, tune.cpp), the host allocator (hostmem.cpp) and the sm_100a kernels (kernels/*.cu).
 #pragma once
 #include <cuda_runtime.h>
 #include <stdint.h>

@@ -1,4 +1,4 @@
-// engine.cpp — the multipath data plane (C6) and its C ABI (C7).
+// plane.cpp — the multipath data plane (C6): configuration, devices, rings, ledger, enqueue.
 //
 // One user copy of B bytes between pinned host memory and GPU d becomes n chunks; each
 // chunk travels over exactly one path:
@@ -16,147 +16,9 @@
 // paper's 2 threads per GPU, cost 822% CPU at 8 GPUs). Per relay chunk
 // the host enqueues: wait(credit) -> DMA -> write(seq) on the relay's stream (cuda.h stream
 // memory operations); the relay kernel polls seq and releases credit on the GPU.
-#include <cuda.h>
-#include <cuda_runtime.h>
-#include <dlfcn.h>
-
-#include <algorithm>
-#include <chrono>
-#include <cstdio>
-#include <cstdlib>
-#include <cstring>
-#include <map>
-#include <mutex>
-#include <string>
-#include <vector>
-
-#include "../../include/mma.h"
-#include "engine.h"
-#include "kargs.h"
-#include "planner.h"
+#include "plane.h"
 
 namespace mma {
-
-#define CK(x)                                   \
-    do {                                        \
-        int e_ = (int)(x);                      \
-        if (e_ != 0) return e_;                 \
-    } while (0)
-
-namespace {
-
-using PFN_memop64 = CUresult (*)(CUstream, CUdeviceptr, cuuint64_t, unsigned int);
-
-constexpr uint64_t kDefaultChunk = 4ull << 20;
-constexpr unsigned kDefaultSlots = 4;
-constexpr uint32_t kDefaultMbps = 50000;
-constexpr uint32_t kDefaultUnit = 128u << 10;
-constexpr int kDefaultRelayCtas = 8;
-constexpr unsigned kDynSlots = 64;        // per-call claim slots, rotating
-constexpr unsigned kDynSlotWords = 32;    // cursor + counts[MMA_KMAX_RINGS] (+ padding)
-
-struct DeviceGuard {
-    int prev = -1;
-    explicit DeviceGuard(int d)
-    {
-        cudaGetDevice(&prev);
-        if (d != prev) cudaSetDevice(d);
-    }
-    ~DeviceGuard()
-    {
-        if (prev >= 0) cudaSetDevice(prev);
-    }
-};
-
-struct DevRes {
-    bool made = false;
-    cudaStream_t direct = nullptr;   // direct-path DMA
-    cudaStream_t zc = nullptr;       // zero-copy kernels (direct or one-hop relay)
-    cudaStream_t hop[2] = {};        // relay hop DMAs: dual pipeline, slot parity
-    cudaStream_t kern = nullptr;     // relay kernels (pull on a target, pack on a relay)
-    cudaEvent_t fork = nullptr;      // recorded on a user stream of this device
-    int sms = 148;
-};
-
-struct Ring {
-    bool made = false;
-    int relay = -1, kdev = -1;       // GPU holding stage and flags; GPU running the kernel
-    uint32_t S = 0;
-    uint64_t slot_bytes = 0;
-    char* stage = nullptr;
-    uint64_t* seq = nullptr;         // relay-local
-    uint64_t* credit = nullptr;      // relay-local
-    unsigned* cnt = nullptr;         // on kdev
-    unsigned long long* cursor = nullptr;   // on kdev
-    uint64_t g_next = 0;             // chunks carried so far (reading R18)
-    unsigned long long unit_next = 0;
-};
-
-struct PathState {
-    int gpu;
-    int kind;       // MMA_PATH_DIRECT / MMA_PATH_RELAY
-    uint32_t mbps;
-    int mode;       // mma_hop_t
-    uint32_t seg_mbps = 0;   // measured for scattered transfers (mma_tune_segments); 0 = unset
-    int seg_mode = -1;       // idem; -1 = unset
-};
-
-struct Scratch {    // per-call table uploads, double-buffered by call parity
-    void* host = nullptr;
-    size_t host_cap = 0;
-    void* dev[MMA_MAX_GPUS] = {};
-    size_t dev_cap[MMA_MAX_GPUS] = {};
-    cudaEvent_t done = nullptr;       // recorded on the user stream at the call's join
-    int done_dev = -1;
-    bool pending = false;
-};
-
-struct Target {
-    bool paths_made = false;
-    std::vector<PathState> paths[2];
-    Ring rings[2][MMA_MAX_PATHS];
-    mma_stats_t stats{};
-    uint8_t* log = nullptr;
-    size_t log_cap = 0, log_n = 0;
-    Scratch scratch[4];   // table buffers of the last 4 calls (a ring)
-    unsigned parity = 0;
-    unsigned long long* dyn = nullptr;        // dynamic-pull slots: cursor + per-path counts
-    unsigned dyn_next = 0;
-    unsigned long long* last_dyn = nullptr;
-    int last_dyn_paths = 0;
-};
-
-struct Engine {
-    std::mutex mu;                   // one multipath enqueue at a time
-    bool inited = false;
-    mma_config_t cfg{};
-    int ndev = 0;
-    bool p2p[MMA_MAX_GPUS][MMA_MAX_GPUS] = {};
-    DevRes dev[MMA_MAX_GPUS];
-    Target tgt[MMA_MAX_GPUS];
-    std::map<cudaStream_t, cudaEvent_t> join_ev;   // join event per engine stream
-    // backlog ledger (NEXT-1): bytes in flight per (direction, link GPU), and of those the
-    // link's own target's direct bytes; each call's share is retired when its done event
-    // (recorded on the user stream at the join) has completed
-    struct InFlight {
-        cudaEvent_t done;
-        int dev, dir;
-        uint64_t bytes[MMA_MAX_GPUS];
-        uint64_t own[MMA_MAX_GPUS];
-    };
-    std::vector<InFlight> inflight;
-    std::vector<std::pair<int, cudaEvent_t>> free_events;
-    uint64_t ledger[2][MMA_MAX_GPUS] = {};
-    uint64_t ledger_own[2][MMA_MAX_GPUS] = {};
-    int* err = nullptr;              // mapped pinned host word (sticky async error)
-    PFN_memop64 wait64 = nullptr, write64 = nullptr;
-    uint64_t timeout_ns = 20ull * 1000 * 1000 * 1000;
-    uint32_t unit_bytes = kDefaultUnit;
-    // fault injection (tests only, MMA_FAULT_DROP_PUBLISH=g): the hop-1 publish of global
-    // ring chunk g is never issued, so the relay kernel must time out, record the sticky
-    // error and release the ring instead of hanging (SURVEY §5 failure detection)
-    long long fault_drop_publish = -1;
-};
 
 Engine& E()
 {
@@ -183,11 +45,9 @@ int env_int(const char* name, int dflt)
     return (s && *s) ? atoi(s) : dflt;
 }
 
-}  // namespace
-
 // ------------------------------------------------------------------- configuration ---
 
-static void apply_env(mma_config_t* c)
+void apply_env(mma_config_t* c)
 {
     c->chunk_bytes[0] = env_size("MMA_CHUNK_BYTES_H2D", env_size("MMA_CHUNK_BYTES", c->chunk_bytes[0]));
     c->chunk_bytes[1] = env_size("MMA_CHUNK_BYTES_D2H", env_size("MMA_CHUNK_BYTES", c->chunk_bytes[1]));
@@ -214,7 +74,7 @@ static void apply_env(mma_config_t* c)
     }
 }
 
-static void defaults(mma_config_t* c)
+void defaults(mma_config_t* c)
 {
     memset(c, 0, sizeof(*c));
     c->chunk_bytes[0] = c->chunk_bytes[1] = kDefaultChunk;
@@ -228,7 +88,7 @@ static void defaults(mma_config_t* c)
     c->ledger = 1;
 }
 
-static int validate_cfg(const mma_config_t& c)
+int validate_cfg(const mma_config_t& c)
 {
     for (int d = 0; d < 2; d++)
         if (c.chunk_bytes[d] == 0 || c.chunk_bytes[d] % 4096) return cudaErrorInvalidValue;
@@ -243,7 +103,7 @@ static int validate_cfg(const mma_config_t& c)
 }
 
 // Streams, peer access and flags for device d (lazily, once).
-static int make_device(int d)
+int make_device(int d)
 {
     Engine& e = E();
     DevRes& r = e.dev[d];
@@ -270,7 +130,7 @@ static int make_device(int d)
     return cudaSuccess;
 }
 
-static int do_init(const mma_config_t* cfg)
+int do_init(const mma_config_t* cfg)
 {
     Engine& e = E();
     mma_config_t c;
@@ -309,7 +169,7 @@ static int do_init(const mma_config_t* cfg)
     return cudaSuccess;
 }
 
-static int ensure_init()
+int ensure_init()
 {
     Engine& e = E();
     if (e.inited) return cudaSuccess;
@@ -320,7 +180,7 @@ static int ensure_init()
 
 // Path set of target d: path 0 = d's own link, then relay GPUs in calibration order, then
 // loopback relays (reading R11).
-static void make_paths(int d)
+void make_paths(int d)
 {
     Engine& e = E();
     Target& t = e.tgt[d];
@@ -357,7 +217,7 @@ static void make_paths(int d)
 
 // --------------------------------------------------------------------- the rings ---
 
-static void free_ring(Ring& r)
+void free_ring(Ring& r)
 {
     if (!r.made) return;
     { DeviceGuard g(r.relay); cudaFree(r.stage); cudaFree(r.seq); }
@@ -366,7 +226,7 @@ static void free_ring(Ring& r)
 }
 
 // Ring of path p of target d in direction dir: S slots of C bytes on the relay.
-static int get_ring(int d, int dir, int p, uint64_t C, uint32_t S, Ring** out)
+int get_ring(int d, int dir, int p, uint64_t C, uint32_t S, Ring** out)
 {
     Engine& e = E();
     Ring& r = e.tgt[d].rings[dir][p];
@@ -407,86 +267,6 @@ static int get_ring(int d, int dir, int p, uint64_t C, uint32_t S, Ring** out)
 
 // ------------------------------------------------------------------ transfer job ---
 
-struct Piece {
-    uint64_t v;       // offset in v
-    uint64_t len;
-    const char* src;
-    char* dst;
-};
-
-struct Job {
-    int dir = 0;
-    int d = 0;                       // target GPU
-    cudaStream_t user = nullptr;
-    int user_dev = 0;
-    uint64_t B = 0;
-    uint64_t C = 0;
-    bool contiguous = true;
-    const char* src0 = nullptr;
-    char* dst0 = nullptr;
-    const mma_segment_t* segs = nullptr;
-    uint64_t nseg = 0;
-    std::vector<uint64_t> vstart;    // segmented: prefix offsets [nseg + 1]
-    bool mapped = false;             // every host address is usable by GPU SMs
-    const uint32_t* bw_override = nullptr;   // measurement runs: per-path bandwidth
-    const int* mode_override = nullptr;      // measurement runs: per-path mode
-    bool no_small_fallback = false;          // measurement runs: ignore the threshold
-
-    // pieces of v[a, b) (the per-segment parts; one piece when contiguous)
-    template <typename F>
-    void pieces(uint64_t a, uint64_t b, F f) const
-    {
-        if (a >= b) return;
-        if (contiguous) { f(Piece{a, b - a, src0 + a, dst0 + a}); return; }
-        uint64_t k = std::upper_bound(vstart.begin(), vstart.end(), a) - vstart.begin() - 1;
-        for (; k < nseg && vstart[k] < b; k++) {
-            uint64_t lo = std::max(vstart[k], a), hi = std::min(vstart[k + 1], b);
-            if (lo >= hi) continue;
-            f(Piece{lo, hi - lo, (const char*)segs[k].src + (lo - vstart[k]),
-                    (char*)segs[k].dst + (lo - vstart[k])});
-        }
-    }
-    void extent(uint64_t i, uint64_t* off, uint64_t* len) const
-    {
-        *off = i * C;
-        *len = std::min(C, B - *off);
-    }
-};
-
-// Pieces copied by one DMA call: cudaMemcpyAsync for one, cudaMemcpyBatchAsync for many.
-struct DmaBatch {
-    std::vector<void*> dst, src;
-    std::vector<size_t> len;
-    void add(void* d, const void* s, size_t n)
-    {
-        if (!n) return;
-        if (!dst.empty() && (char*)dst.back() + len.back() == (char*)d && (const char*)src.back() + len.back() == (const char*)s) {
-            len.back() += n;    // merge adjacent pieces
-            return;
-        }
-        dst.push_back(d);
-        src.push_back(const_cast<void*>(s));
-        len.push_back(n);
-    }
-    int issue(cudaMemcpyKind kind, cudaStream_t s)
-    {
-        if (dst.empty()) return cudaSuccess;
-        if (dst.size() == 1) return (int)cudaMemcpyAsync(dst[0], src[0], len[0], kind, s);
-        if (s == nullptr || s == cudaStreamLegacy) {   // the batch API rejects the legacy stream
-            for (size_t i = 0; i < dst.size(); i++) CK(cudaMemcpyAsync(dst[i], src[i], len[i], kind, s));
-            return cudaSuccess;
-        }
-        cudaMemcpyAttributes at;
-        memset(&at, 0, sizeof(at));
-        at.srcAccessOrder = cudaMemcpySrcAccessOrderStream;
-        size_t idx = 0, fail = 0;
-        cudaError_t e = cudaMemcpyBatchAsync(dst.data(), src.data(), len.data(), dst.size(), &at, &idx, 1, &fail, s);
-        if (e == cudaSuccess) return cudaSuccess;
-        cudaGetLastError();
-        for (size_t i = 0; i < dst.size(); i++) CK(cudaMemcpyAsync(dst[i], src[i], len[i], kind, s));
-        return cudaSuccess;
-    }
-};
 
 static cudaEvent_t join_event(cudaStream_t s, int dev)
 {
@@ -530,13 +310,8 @@ static int scratch_host(Scratch& sc, size_t bytes, void** out)
 
 // Optional per-launch CUDA-event timing of the engine's kernels, recorded on the stream
 // the kernel is launched on (mma_set_kernel_timing / mma_kernel_times).
-struct KRec {
-    int dev;
-    int kind;   // 0 zero-copy, 1 relay pull (H2D), 2 relay pack (D2H) | dir << 4 | path << 8 | dev << 16
-    cudaEvent_t a, b;
-};
-static std::vector<KRec> g_kpending;
-static bool g_ktime = false;
+std::vector<KRec> g_kpending;
+bool g_ktime = false;
 
 struct KTimer {
     bool on = false;
@@ -613,7 +388,7 @@ static int ledger_add(int dir, int user_dev, cudaStream_t user, const uint64_t* 
 
 // Planner inputs of target d's paths: bandwidth (0 = not usable for this call) and
 // backlog from the ledger.
-static void ledger_inputs(int d, int dir, const std::vector<PathState>& ps, std::vector<PlanPath>& pp)
+void ledger_inputs(int d, int dir, const std::vector<PathState>& ps, std::vector<PlanPath>& pp)
 {
     Engine& e = E();
     if (!e.cfg.ledger) return;
@@ -649,7 +424,7 @@ struct Trace {
 };
 
 // Enqueue one multipath copy (engine mutex held).
-static int run_job(Job& j)
+int run_job(Job& j)
 {
     Engine& e = E();
     Target& t = e.tgt[j.d];
@@ -1079,640 +854,11 @@ static int run_job(Job& j)
     return cudaSuccess;
 }
 
-// ------------------------------------------------------------- classification ---
-
-static int sticky()
+int sticky()
 {
     Engine& e = E();
     if (e.err && *(volatile int*)e.err) return MMA_ERR_RELAY_TIMEOUT;
     return cudaSuccess;
 }
 
-static int stream_device(cudaStream_t s, int* dev)
-{
-    cudaError_t e = cudaStreamGetDevice(s, dev);
-    if (e != cudaSuccess) { cudaGetLastError(); return cudaGetDevice(dev); }
-    return cudaSuccess;
-}
-
-// type of pointer: 0 host pinned (mapped if *mapped), 1 device (dev), 2 pageable/unknown
-static int classify(const void* p, int* dev, bool* mapped)
-{
-    cudaPointerAttributes a;
-    cudaError_t e = cudaPointerGetAttributes(&a, p);
-    if (e != cudaSuccess) { cudaGetLastError(); return 2; }
-    if (a.type == cudaMemoryTypeDevice) { *dev = a.device; return 1; }
-    if (a.type == cudaMemoryTypeHost) { *mapped = a.devicePointer != nullptr; return 0; }
-    return 2;
-}
-
-static int copy_contiguous(int dir, void* dst, const void* src, size_t bytes, cudaStream_t stream)
-{
-    CK((cudaError_t)ensure_init());
-    if (int se = sticky()) return se;
-    if (bytes == 0) return cudaSuccess;
-    if (!dst || !src) return cudaErrorInvalidValue;
-    Engine& e = E();
-    const void* dptr = (dir == MMA_H2D) ? dst : src;
-    const void* hptr = (dir == MMA_H2D) ? src : dst;
-    int d = -1, hd = -1;
-    bool mapped = false, dummy = false;
-    if (classify(dptr, &d, &dummy) != 1) return cudaErrorInvalidValue;
-    const int hk = classify(hptr, &hd, &mapped);
-    if (hk == 1) return cudaErrorInvalidValue;   // device -> device is not this API
-    const cudaMemcpyKind kind = (dir == MMA_H2D) ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToHost;
-    cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
-    cudaStreamIsCapturing(stream, &cap);
-    if (hk == 2 || cap != cudaStreamCaptureStatusNone || d >= e.ndev)
-        return (int)cudaMemcpyAsync(dst, src, bytes, kind, stream);   // native (R7)
-    Job j;
-    j.dir = dir;
-    j.d = d;
-    j.user = stream;
-    CK((cudaError_t)stream_device(stream, &j.user_dev));
-    j.B = bytes;
-    j.C = e.cfg.chunk_bytes[dir];
-    j.contiguous = true;
-    j.src0 = (const char*)src;
-    j.dst0 = (char*)dst;
-    j.mapped = mapped;
-    std::lock_guard<std::mutex> g(e.mu);
-    CK((cudaError_t)make_device(d));
-    return run_job(j);
-}
-
-// Validate a segment table and fill the job (no engine lock held).
-static int prepare_segments(int dir, const mma_segment_t* segs, size_t nsegs, int device,
-                            cudaStream_t stream, Job& j)
-{
-    Engine& e = E();
-    j.dir = dir;
-    j.d = device;
-    j.user = stream;
-    CK((cudaError_t)stream_device(stream, &j.user_dev));
-    j.C = e.cfg.chunk_bytes[dir];
-    j.contiguous = false;
-    j.segs = segs;
-    j.nseg = nsegs;
-    j.vstart.resize(nsegs + 1);
-    j.vstart[0] = 0;
-    // destinations must be pairwise disjoint: O(n) when they are in ascending order,
-    // else a sort -- skipped when the table is byte-identical to the last one validated
-    bool sorted = true;
-    uintptr_t prev_end = 0;
-    for (size_t k = 0; k < nsegs; k++) {
-        if (!segs[k].bytes) { j.vstart[k + 1] = j.vstart[k]; continue; }
-        if (!segs[k].src || !segs[k].dst) return cudaErrorInvalidValue;
-        j.vstart[k + 1] = j.vstart[k] + segs[k].bytes;
-        if ((uintptr_t)segs[k].dst < prev_end) sorted = false;
-        prev_end = (uintptr_t)segs[k].dst + segs[k].bytes;
-    }
-    j.B = j.vstart[nsegs];
-    if (j.B == 0) return cudaSuccess;
-    if (!sorted) {
-        static std::mutex mu;
-        static std::vector<mma_segment_t> last_ok[2];
-        std::lock_guard<std::mutex> g(mu);
-        std::vector<mma_segment_t>& ok = last_ok[dir];
-        if (!(ok.size() == nsegs && memcmp(ok.data(), segs, nsegs * sizeof(mma_segment_t)) == 0)) {
-            std::vector<std::pair<uintptr_t, size_t>> v;
-            v.reserve(nsegs);
-            for (size_t k = 0; k < nsegs; k++)
-                if (segs[k].bytes) v.push_back({(uintptr_t)segs[k].dst, segs[k].bytes});
-            std::sort(v.begin(), v.end());
-            for (size_t k = 1; k < v.size(); k++)
-                if (v[k - 1].first + v[k - 1].second > v[k].first) return cudaErrorInvalidValue;
-            ok.assign(segs, segs + nsegs);
-        }
-    }
-    // classify a bounded sample of the table (first, last, evenly spaced): a pointer query
-    // costs ~0.1 ms, so the sample stays small; the caller guarantees the memory kinds
-    j.mapped = true;
-    const size_t nsample = std::min<size_t>(nsegs, 5);
-    for (size_t q = 0; q < nsample; q++) {
-        size_t k = (nsample == 1) ? 0 : q * (nsegs - 1) / (nsample - 1);
-        if (!segs[k].bytes) continue;
-        const void* dp = (dir == MMA_H2D) ? segs[k].dst : segs[k].src;
-        const void* hp = (dir == MMA_H2D) ? segs[k].src : segs[k].dst;
-        int d = -1, hd = -1;
-        bool m = false, dummy = false;
-        if (classify(dp, &d, &dummy) != 1 || d != device) return cudaErrorInvalidValue;
-        int hk = classify(hp, &hd, &m);
-        if (hk == 1) return cudaErrorInvalidValue;
-        if (hk == 2) j.mapped = false;   // pageable: CE only
-        j.mapped = j.mapped && m;
-    }
-    if (nsegs == 1) {   // one segment is a contiguous copy (the kernels' nseg == 1 form)
-        j.contiguous = true;
-        j.src0 = (const char*)segs[0].src;
-        j.dst0 = (char*)segs[0].dst;
-    }
-    return cudaSuccess;
-}
-
-static int copy_segments(int dir, const mma_segment_t* segs, size_t nsegs, int device, cudaStream_t stream)
-{
-    CK((cudaError_t)ensure_init());
-    if (int se = sticky()) return se;
-    Engine& e = E();
-    if (nsegs == 0) return cudaSuccess;
-    if (!segs) return cudaErrorInvalidValue;
-    if (device < 0 || device >= e.ndev) return cudaErrorInvalidDevice;
-    Job j;
-    CK(prepare_segments(dir, segs, nsegs, device, stream, j));
-    if (j.B == 0) return cudaSuccess;
-    std::lock_guard<std::mutex> g(e.mu);
-    CK((cudaError_t)make_device(device));
-    return run_job(j);
-}
-
 }  // namespace mma
-
-// ====================================================================== C ABI (C7) ===
-
-using namespace mma;
-
-extern "C" {
-
-int mma_default_config(mma_config_t* cfg)
-{
-    if (!cfg) return cudaErrorInvalidValue;
-    defaults(cfg);
-    apply_env(cfg);
-    return cudaSuccess;
-}
-
-int mma_init(const mma_config_t* cfg)
-{
-    std::lock_guard<std::mutex> g(E().mu);
-    return do_init(cfg);
-}
-
-int mma_finalize(void)
-{
-    Engine& e = E();
-    std::lock_guard<std::mutex> g(e.mu);
-    if (!e.inited) return cudaSuccess;
-    for (int d = 0; d < e.ndev; d++) {
-        if (!e.dev[d].made) continue;
-        DeviceGuard dg(d);
-        cudaDeviceSynchronize();
-    }
-    for (int d = 0; d < e.ndev; d++) {
-        Target& t = e.tgt[d];
-        for (int dir = 0; dir < 2; dir++)
-            for (int p = 0; p < MMA_MAX_PATHS; p++) free_ring(t.rings[dir][p]);
-        if (t.log) { DeviceGuard dg(d); cudaFree(t.log); }
-        if (t.dyn) { DeviceGuard dg(d); cudaFree(t.dyn); }
-        for (auto& sc : t.scratch) {
-            for (int g2 = 0; g2 < MMA_MAX_GPUS; g2++)
-                if (sc.dev[g2]) { DeviceGuard dg(g2); cudaFree(sc.dev[g2]); }
-            if (sc.host) cudaFreeHost(sc.host);
-            if (sc.done) cudaEventDestroy(sc.done);
-        }
-        t = Target();
-    }
-    for (auto& kv : e.join_ev) cudaEventDestroy(kv.second);
-    e.join_ev.clear();
-    for (auto& f : e.inflight) cudaEventDestroy(f.done);
-    for (auto& f : e.free_events) cudaEventDestroy(f.second);
-    e.inflight.clear();
-    e.free_events.clear();
-    memset(e.ledger, 0, sizeof e.ledger);
-    memset(e.ledger_own, 0, sizeof e.ledger_own);
-    for (int d = 0; d < e.ndev; d++) {
-        DevRes& r = e.dev[d];
-        if (!r.made) continue;
-        DeviceGuard dg(d);
-        cudaStreamDestroy(r.kern);
-        cudaStreamDestroy(r.hop[0]);
-        cudaStreamDestroy(r.hop[1]);
-        cudaStreamDestroy(r.direct);
-        cudaStreamDestroy(r.zc);
-        cudaEventDestroy(r.fork);
-        r = DevRes();
-    }
-    if (e.err) { cudaFreeHost(e.err); e.err = nullptr; }
-    e.inited = false;
-    return cudaSuccess;
-}
-
-int mma_memcpy_h2d(void* dst, const void* src, size_t bytes, mma_stream_t stream)
-{
-    return copy_contiguous(MMA_H2D, dst, src, bytes, (cudaStream_t)stream);
-}
-
-int mma_memcpy_d2h(void* dst, const void* src, size_t bytes, mma_stream_t stream)
-{
-    return copy_contiguous(MMA_D2H, dst, src, bytes, (cudaStream_t)stream);
-}
-
-int mma_memcpy_h2d_segments(const mma_segment_t* segs, size_t nsegs, int dst_device, mma_stream_t stream)
-{
-    return copy_segments(MMA_H2D, segs, nsegs, dst_device, (cudaStream_t)stream);
-}
-
-int mma_memcpy_d2h_segments(const mma_segment_t* segs, size_t nsegs, int src_device, mma_stream_t stream)
-{
-    return copy_segments(MMA_D2H, segs, nsegs, src_device, (cudaStream_t)stream);
-}
-
-int mma_get_paths(int device, mma_dir_t dir, int* gpus, int* kinds, uint32_t* mbps, int* modes,
-                  int cap, int* npaths)
-{
-    CK((cudaError_t)ensure_init());
-    Engine& e = E();
-    if (device < 0 || device >= e.ndev) return cudaErrorInvalidDevice;
-    if ((dir != MMA_H2D && dir != MMA_D2H) || !npaths) return cudaErrorInvalidValue;
-    std::lock_guard<std::mutex> g(e.mu);
-    make_paths(device);
-    auto& ps = e.tgt[device].paths[dir];
-    *npaths = (int)ps.size();
-    for (int i = 0; i < (int)ps.size() && i < cap; i++) {
-        if (gpus) gpus[i] = ps[i].gpu;
-        if (kinds) kinds[i] = ps[i].kind;
-        if (mbps) mbps[i] = ps[i].mbps;
-        if (modes) modes[i] = ps[i].mode;
-    }
-    return cudaSuccess;
-}
-
-int mma_set_plan_mode(int mode)
-{
-    CK((cudaError_t)ensure_init());
-    if (mode < PLAN_CONTIGUOUS || mode > PLAN_DYNAMIC) return cudaErrorInvalidValue;
-    std::lock_guard<std::mutex> g(E().mu);
-    E().cfg.plan_mode = mode;
-    return cudaSuccess;
-}
-
-int mma_get_segment_tuning(int device, mma_dir_t dir, uint32_t* mbps, int* modes, int cap, int* npaths)
-{
-    CK((cudaError_t)ensure_init());
-    Engine& e = E();
-    if (device < 0 || device >= e.ndev) return cudaErrorInvalidDevice;
-    if ((dir != MMA_H2D && dir != MMA_D2H) || !npaths) return cudaErrorInvalidValue;
-    std::lock_guard<std::mutex> g(e.mu);
-    make_paths(device);
-    auto& ps = e.tgt[device].paths[dir];
-    *npaths = (int)ps.size();
-    for (int i = 0; i < (int)ps.size() && i < cap; i++) {
-        if (mbps) mbps[i] = ps[i].seg_mbps;
-        if (modes) modes[i] = ps[i].seg_mode;
-    }
-    return cudaSuccess;
-}
-
-int mma_set_bandwidth(int device, mma_dir_t dir, const uint32_t* mbps, int npaths)
-{
-    CK((cudaError_t)ensure_init());
-    Engine& e = E();
-    if (device < 0 || device >= e.ndev) return cudaErrorInvalidDevice;
-    if ((dir != MMA_H2D && dir != MMA_D2H) || !mbps) return cudaErrorInvalidValue;
-    std::lock_guard<std::mutex> g(e.mu);
-    make_paths(device);
-    auto& ps = e.tgt[device].paths[dir];
-    if (npaths != (int)ps.size()) return cudaErrorInvalidValue;
-    bool any = false;
-    for (int i = 0; i < npaths; i++) any |= mbps[i] > 0;
-    if (!any) return cudaErrorInvalidValue;
-    for (int i = 0; i < npaths; i++) { ps[i].mbps = mbps[i]; ps[i].seg_mbps = 0; }
-    return cudaSuccess;
-}
-
-int mma_set_path_modes(int device, mma_dir_t dir, const int* modes, int npaths)
-{
-    CK((cudaError_t)ensure_init());
-    Engine& e = E();
-    if (device < 0 || device >= e.ndev) return cudaErrorInvalidDevice;
-    if ((dir != MMA_H2D && dir != MMA_D2H) || !modes) return cudaErrorInvalidValue;
-    std::lock_guard<std::mutex> g(e.mu);
-    make_paths(device);
-    auto& ps = e.tgt[device].paths[dir];
-    if (npaths != (int)ps.size()) return cudaErrorInvalidValue;
-    for (int i = 0; i < npaths; i++)
-        if (modes[i] < MMA_HOP_AUTO || modes[i] > MMA_HOP_ZC) return cudaErrorInvalidValue;
-    for (int i = 0; i < npaths; i++) { ps[i].mode = modes[i]; ps[i].seg_mode = -1; }
-    return cudaSuccess;
-}
-
-int mma_get_plan(int device, mma_dir_t dir, size_t bytes, uint8_t* path_of_chunk, size_t cap,
-                 size_t* nchunks, int* fallback)
-{
-    CK((cudaError_t)ensure_init());
-    Engine& e = E();
-    if (device < 0 || device >= e.ndev) return cudaErrorInvalidDevice;
-    if ((dir != MMA_H2D && dir != MMA_D2H) || !nchunks) return cudaErrorInvalidValue;
-    std::lock_guard<std::mutex> g(e.mu);
-    make_paths(device);
-    auto& ps = e.tgt[device].paths[dir];
-    std::vector<PlanPath> pp;
-    for (auto& p : ps) pp.push_back(PlanPath{p.kind == MMA_PATH_DIRECT, p.mbps, 0});
-    ledger_inputs(device, dir, ps, pp);
-    Plan plan;
-    if (make_plan(pp.data(), (int)pp.size(), bytes, e.cfg.chunk_bytes[dir], e.cfg.fallback_bytes[dir],
-                  e.cfg.plan_mode == PLAN_DYNAMIC ? PLAN_CONTIGUOUS : e.cfg.plan_mode, plan))
-        return cudaErrorInvalidValue;
-    *nchunks = plan.n;
-    if (fallback) *fallback = plan.fallback;
-    if (path_of_chunk) {
-        if (cap < plan.n) return cudaErrorInvalidValue;
-        memcpy(path_of_chunk, plan.path.data(), plan.n);
-    }
-    return cudaSuccess;
-}
-
-int mma_plan_chunks(const uint32_t* mbps, const int* kinds, const uint64_t* backlog, int npaths,
-                    uint64_t bytes, uint64_t chunk_bytes, uint64_t thr, int mode,
-                    uint8_t* path_of_chunk, size_t cap, size_t* nchunks, int* fallback)
-{
-    if (!mbps || !kinds || !nchunks || npaths < 1 || npaths > 255) return cudaErrorInvalidValue;
-    std::vector<PlanPath> pp(npaths);
-    for (int p = 0; p < npaths; p++) {
-        if (kinds[p] != MMA_PATH_DIRECT && kinds[p] != MMA_PATH_RELAY) return cudaErrorInvalidValue;
-        pp[p] = PlanPath{kinds[p] == MMA_PATH_DIRECT, mbps[p], backlog ? backlog[p] : 0};
-    }
-    Plan plan;
-    if (make_plan(pp.data(), npaths, bytes, chunk_bytes, thr, mode, plan)) return cudaErrorInvalidValue;
-    *nchunks = plan.n;
-    if (fallback) *fallback = plan.fallback;
-    if (path_of_chunk) {
-        if (cap < plan.n) return cudaErrorInvalidValue;
-        memcpy(path_of_chunk, plan.path.data(), plan.n);
-    }
-    return cudaSuccess;
-}
-
-// Measure every path alone in each hop mode on the transfer `proto` describes and keep,
-// per path, the faster mode and its rate (integer MB/s, reading R17: llround). Runs the
-// copy (1 + reps) times per (path, mode); the best of `reps` timed runs counts. The host
-// thread that enqueues a call is one resource shared by all P paths of a multipath call,
-// so a mode's rate is min(device rate, host-issue rate / P): a copy-engine path that needs
-// one descriptor per 32 KiB segment (~0.6 us each) cannot feed 8 links from one thread
-// (DESIGN.md §5.3).
-static int tune_paths(Job proto, int reps, std::vector<uint32_t>& mbps, std::vector<int>& modes)
-{
-    Engine& e = E();
-    auto& ps = e.tgt[proto.d].paths[proto.dir];
-    const int P = (int)ps.size();
-    mbps.assign(P, 0);
-    modes.assign(P, MMA_HOP_CE);
-    std::vector<uint32_t> bw(P);
-    std::vector<int> md(P, MMA_HOP_CE);
-    cudaEvent_t a = nullptr, b = nullptr;
-    {
-        DeviceGuard g(proto.user_dev);
-        CK(cudaEventCreate(&a));
-        CK(cudaEventCreate(&b));
-    }
-    int rc = cudaSuccess;
-    for (int p = 0; p < P && rc == cudaSuccess; p++) {
-        float best_rate = 0.f;
-        for (int m : {MMA_HOP_CE, MMA_HOP_ZC}) {
-            if (m == MMA_HOP_ZC && !proto.mapped) continue;
-            for (int q = 0; q < P; q++) bw[q] = (q == p) ? 1 : 0;
-            md[p] = m;
-            float best = 1e30f, best_issue = 1e30f;
-            for (int rep = 0; rep <= reps && rc == cudaSuccess; rep++) {
-                Job j = proto;
-                j.bw_override = bw.data();
-                j.mode_override = md.data();
-                j.no_small_fallback = true;
-                DeviceGuard g(j.user_dev);
-                cudaEventRecord(a, j.user);
-                const auto h0 = std::chrono::steady_clock::now();
-                rc = run_job(j);
-                const float issue_ms = std::chrono::duration<float, std::milli>(std::chrono::steady_clock::now() - h0).count();
-                cudaEventRecord(b, j.user);
-                if (cudaEventSynchronize(b) != cudaSuccess) rc = cudaErrorUnknown;
-                float ms = 0;
-                cudaEventElapsedTime(&ms, a, b);
-                if (rep > 0 && ms > 0) {                             // rep 0 warms up
-                    best = std::min(best, ms);
-                    best_issue = std::min(best_issue, issue_ms);
-                }
-            }
-            const float eff_ms = std::max(best, best_issue * (float)P);
-            const float rate = best < 1e29f ? (float)((double)proto.B / (eff_ms * 1e-3) / 1e6) : 0.f;
-            if (rate > best_rate) {
-                best_rate = rate;
-                modes[p] = m;
-                mbps[p] = (uint32_t)llround(rate);
-            }
-        }
-    }
-    cudaEventDestroy(a);
-    cudaEventDestroy(b);
-    if (rc == cudaSuccess && sticky()) rc = sticky();
-    return rc;
-}
-
-int mma_calibrate(int device, mma_dir_t dir, size_t bytes)
-{
-    CK((cudaError_t)ensure_init());
-    Engine& e = E();
-    if (device < 0 || device >= e.ndev) return cudaErrorInvalidDevice;
-    if ((dir != MMA_H2D && dir != MMA_D2H) || bytes == 0) return cudaErrorInvalidValue;
-    std::lock_guard<std::mutex> g(e.mu);
-    CK(make_device(device));
-    make_paths(device);
-    DeviceGuard dg(device);
-    char* hbuf = nullptr;
-    char* dbuf = nullptr;
-    cudaStream_t s = nullptr;
-    CK(cudaHostAlloc((void**)&hbuf, bytes, cudaHostAllocPortable | cudaHostAllocMapped));
-    CK(cudaMalloc((void**)&dbuf, bytes));
-    CK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
-    Job j;
-    j.dir = dir;
-    j.d = device;
-    j.user = s;
-    j.user_dev = device;
-    j.B = bytes;
-    j.C = e.cfg.chunk_bytes[dir];
-    j.src0 = dir == MMA_H2D ? hbuf : dbuf;
-    j.dst0 = dir == MMA_H2D ? dbuf : hbuf;
-    j.mapped = true;
-    std::vector<uint32_t> mbps;
-    std::vector<int> modes;
-    int rc = tune_paths(j, 3, mbps, modes);
-    if (rc == cudaSuccess) {
-        auto& ps = e.tgt[device].paths[dir];
-        for (size_t p = 0; p < ps.size(); p++)
-            if (mbps[p]) { ps[p].mbps = mbps[p]; ps[p].mode = modes[p]; }
-    }
-    cudaStreamDestroy(s);
-    cudaFree(dbuf);
-    cudaFreeHost(hbuf);
-    return rc;
-}
-
-int mma_tune_segments(const mma_segment_t* segs, size_t nsegs, int device, mma_dir_t dir,
-                      mma_stream_t stream, int reps)
-{
-    CK((cudaError_t)ensure_init());
-    Engine& e = E();
-    if (device < 0 || device >= e.ndev) return cudaErrorInvalidDevice;
-    if ((dir != MMA_H2D && dir != MMA_D2H) || !segs || nsegs == 0 || reps < 1) return cudaErrorInvalidValue;
-    Job j;
-    CK(prepare_segments(dir, segs, nsegs, device, (cudaStream_t)stream, j));
-    if (j.B == 0) return cudaSuccess;
-    std::lock_guard<std::mutex> g(e.mu);
-    CK(make_device(device));
-    make_paths(device);
-    std::vector<uint32_t> mbps;
-    std::vector<int> modes;
-    int rc = tune_paths(j, reps, mbps, modes);
-    if (rc == cudaSuccess) {
-        auto& ps = e.tgt[device].paths[dir];
-        for (size_t p = 0; p < ps.size(); p++)
-            if (mbps[p]) { ps[p].seg_mbps = mbps[p]; ps[p].seg_mode = modes[p]; }
-    }
-    return rc;
-}
-
-int mma_get_delivery_log(int device, uint8_t* path_of_chunk, size_t cap, size_t* nchunks)
-{
-    CK((cudaError_t)ensure_init());
-    Engine& e = E();
-    if (device < 0 || device >= e.ndev) return cudaErrorInvalidDevice;
-    if (!nchunks) return cudaErrorInvalidValue;
-    std::lock_guard<std::mutex> g(e.mu);
-    Target& t = e.tgt[device];
-    *nchunks = t.log_n;
-    if (!t.log_n || !path_of_chunk) return cudaSuccess;
-    if (cap < t.log_n) return cudaErrorInvalidValue;
-    DeviceGuard dg(device);
-    CK(cudaDeviceSynchronize());
-    CK(cudaMemcpy(path_of_chunk, t.log, t.log_n, cudaMemcpyDeviceToHost));
-    return cudaSuccess;
-}
-
-int mma_host_alloc(void** ptr, size_t bytes, unsigned flags)
-{
-    CK((cudaError_t)ensure_init());
-    (void)flags;
-    return host_alloc(ptr, bytes, E().cfg.numa_mode, 0);
-}
-
-int mma_host_free(void* ptr) { return host_free(ptr); }
-
-int mma_get_stats(int device, mma_stats_t* out)
-{
-    CK((cudaError_t)ensure_init());
-    Engine& e = E();
-    if (device < 0 || device >= e.ndev) return cudaErrorInvalidDevice;
-    if (!out) return cudaErrorInvalidValue;
-    std::lock_guard<std::mutex> g(e.mu);
-    *out = e.tgt[device].stats;
-    return cudaSuccess;
-}
-
-int mma_reset_stats(int device)
-{
-    CK((cudaError_t)ensure_init());
-    Engine& e = E();
-    if (device < 0 || device >= e.ndev) return cudaErrorInvalidDevice;
-    std::lock_guard<std::mutex> g(e.mu);
-    e.tgt[device].stats = mma_stats_t{};
-    return cudaSuccess;
-}
-
-int mma_set_kernel_timing(int on)
-{
-    std::lock_guard<std::mutex> g(E().mu);
-    g_ktime = on != 0;
-    return cudaSuccess;
-}
-
-int mma_kernel_times(float* ms, int* kinds, size_t cap, size_t* n)
-{
-    if (!n) return cudaErrorInvalidValue;
-    std::lock_guard<std::mutex> g(E().mu);
-    size_t k = 0;
-    int rc = cudaSuccess;
-    for (auto& r : g_kpending) {
-        DeviceGuard dg(r.dev);
-        float t = 0.f;
-        if (cudaEventSynchronize(r.b) != cudaSuccess || cudaEventElapsedTime(&t, r.a, r.b) != cudaSuccess)
-            rc = cudaErrorUnknown;
-        if (k < cap) {
-            if (ms) ms[k] = t;
-            if (kinds) kinds[k] = r.kind;
-        }
-        k++;
-        cudaEventDestroy(r.a);
-        cudaEventDestroy(r.b);
-    }
-    g_kpending.clear();
-    *n = k;
-    return rc;
-}
-
-int mma_get_dynamic_counts(int device, uint64_t* chunks, int cap, int* npaths)
-{
-    CK((cudaError_t)ensure_init());
-    Engine& e = E();
-    if (device < 0 || device >= e.ndev) return cudaErrorInvalidDevice;
-    if (!npaths) return cudaErrorInvalidValue;
-    std::lock_guard<std::mutex> g(e.mu);
-    Target& t = e.tgt[device];
-    *npaths = t.last_dyn ? t.last_dyn_paths : 0;
-    if (!t.last_dyn || !chunks) return cudaSuccess;
-    unsigned long long c[MMA_KMAX_RINGS] = {};
-    DeviceGuard dg(device);
-    CK(cudaDeviceSynchronize());
-    CK(cudaMemcpy(c, t.last_dyn + 1, sizeof c, cudaMemcpyDeviceToHost));
-    for (int p = 0; p < t.last_dyn_paths && p < cap; p++) chunks[p] = c[p];
-    return cudaSuccess;
-}
-
-int mma_get_last_error(void)
-{
-    if (!E().inited) return cudaSuccess;
-    return sticky();
-}
-
-const char* mma_error_string(int err)
-{
-    if (err == MMA_ERR_RELAY_TIMEOUT) return "mma: relay kernel spin timed out (sticky; mma_finalize to reset)";
-    if (err == MMA_ERR_NO_MEMOPS) return "mma: CUDA stream memory operations unavailable";
-    return cudaGetErrorString((cudaError_t)err);
-}
-
-int mma_fill_pattern(void* ptr, size_t bytes, uint64_t seed, uint64_t offset, mma_stream_t s)
-{
-    if (bytes && !ptr) return cudaErrorInvalidValue;
-    return (int)launch_fill(ptr, bytes, seed, offset, (cudaStream_t)s);
-}
-
-int mma_verify_pattern(const void* ptr, size_t bytes, uint64_t seed, uint64_t offset,
-                       uint64_t* mismatches, mma_stream_t s)
-{
-    if ((bytes && !ptr) || !mismatches) return cudaErrorInvalidValue;
-    return (int)launch_verify(ptr, bytes, seed, offset, mismatches, (cudaStream_t)s);
-}
-
-int mma_verify_segments(void* const* dst, const uint64_t* offset, const uint64_t* bytes,
-                        size_t nsegs, uint64_t seed, uint64_t* mismatches, mma_stream_t s)
-{
-    if (!mismatches || (nsegs && (!dst || !offset || !bytes))) return cudaErrorInvalidValue;
-    if (!nsegs) return cudaSuccess;
-    uint64_t* tab = nullptr;
-    CK(cudaMallocAsync((void**)&tab, 3 * nsegs * 8, (cudaStream_t)s));
-    CK(cudaMemcpyAsync(tab, dst, nsegs * 8, cudaMemcpyHostToDevice, (cudaStream_t)s));
-    CK(cudaMemcpyAsync(tab + nsegs, offset, nsegs * 8, cudaMemcpyHostToDevice, (cudaStream_t)s));
-    CK(cudaMemcpyAsync(tab + 2 * nsegs, bytes, nsegs * 8, cudaMemcpyHostToDevice, (cudaStream_t)s));
-    CK(launch_verify_segments(tab, tab + nsegs, tab + 2 * nsegs, nsegs, seed, mismatches, (cudaStream_t)s));
-    CK(cudaFreeAsync(tab, (cudaStream_t)s));
-    return cudaSuccess;
-}
-
-// Raise the hardware queue count before the first CUDA context exists, so the engine's
-// streams do not alias one queue (SURVEY §7 hard part 4).
-__attribute__((constructor)) static void mma_preinit(void)
-{
-    setenv("CUDA_DEVICE_MAX_CONNECTIONS", "32", 0);
-}
-
-}  // extern "C"

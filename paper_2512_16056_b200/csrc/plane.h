@@ -1,0 +1,258 @@
+// plane.h — internal state and interfaces of the data plane (engine) shared by
+// plane.cpp (configuration, devices, rings, ledger, enqueue), api.cpp (the C ABI) and
+// tune.cpp (per-path measurement). Not part of the public ABI (include/mma.h is).
+#pragma once
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/mma.h"
+#include "engine.h"
+#include "kargs.h"
+#include "planner.h"
+
+namespace mma {
+
+#define CK(x)                                   \
+    do {                                        \
+        int e_ = (int)(x);                      \
+        if (e_ != 0) return e_;                 \
+    } while (0)
+
+
+using PFN_memop64 = CUresult (*)(CUstream, CUdeviceptr, cuuint64_t, unsigned int);
+
+constexpr uint64_t kDefaultChunk = 4ull << 20;
+constexpr unsigned kDefaultSlots = 4;
+constexpr uint32_t kDefaultMbps = 50000;
+constexpr uint32_t kDefaultUnit = 128u << 10;
+constexpr int kDefaultRelayCtas = 8;
+constexpr unsigned kDynSlots = 64;        // per-call claim slots, rotating
+constexpr unsigned kDynSlotWords = 32;    // cursor + counts[MMA_KMAX_RINGS] (+ padding)
+
+struct DeviceGuard {
+    int prev = -1;
+    explicit DeviceGuard(int d)
+    {
+        cudaGetDevice(&prev);
+        if (d != prev) cudaSetDevice(d);
+    }
+    ~DeviceGuard()
+    {
+        if (prev >= 0) cudaSetDevice(prev);
+    }
+};
+
+struct DevRes {
+    bool made = false;
+    cudaStream_t direct = nullptr;   // direct-path DMA
+    cudaStream_t zc = nullptr;       // zero-copy kernels (direct or one-hop relay)
+    cudaStream_t hop[2] = {};        // relay hop DMAs: dual pipeline, slot parity
+    cudaStream_t kern = nullptr;     // relay kernels (pull on a target, pack on a relay)
+    cudaEvent_t fork = nullptr;      // recorded on a user stream of this device
+    int sms = 148;
+};
+
+struct Ring {
+    bool made = false;
+    int relay = -1, kdev = -1;       // GPU holding stage and flags; GPU running the kernel
+    uint32_t S = 0;
+    uint64_t slot_bytes = 0;
+    char* stage = nullptr;
+    uint64_t* seq = nullptr;         // relay-local
+    uint64_t* credit = nullptr;      // relay-local
+    unsigned* cnt = nullptr;         // on kdev
+    unsigned long long* cursor = nullptr;   // on kdev
+    uint64_t g_next = 0;             // chunks carried so far (reading R18)
+    unsigned long long unit_next = 0;
+};
+
+struct PathState {
+    int gpu;
+    int kind;       // MMA_PATH_DIRECT / MMA_PATH_RELAY
+    uint32_t mbps;
+    int mode;       // mma_hop_t
+    uint32_t seg_mbps = 0;   // measured for scattered transfers (mma_tune_segments); 0 = unset
+    int seg_mode = -1;       // idem; -1 = unset
+};
+
+struct Scratch {    // per-call table uploads, double-buffered by call parity
+    void* host = nullptr;
+    size_t host_cap = 0;
+    void* dev[MMA_MAX_GPUS] = {};
+    size_t dev_cap[MMA_MAX_GPUS] = {};
+    cudaEvent_t done = nullptr;       // recorded on the user stream at the call's join
+    int done_dev = -1;
+    bool pending = false;
+};
+
+struct Target {
+    bool paths_made = false;
+    std::vector<PathState> paths[2];
+    Ring rings[2][MMA_MAX_PATHS];
+    mma_stats_t stats{};
+    uint8_t* log = nullptr;
+    size_t log_cap = 0, log_n = 0;
+    Scratch scratch[4];   // table buffers of the last 4 calls (a ring)
+    unsigned parity = 0;
+    unsigned long long* dyn = nullptr;        // dynamic-pull slots: cursor + per-path counts
+    unsigned dyn_next = 0;
+    unsigned long long* last_dyn = nullptr;
+    int last_dyn_paths = 0;
+};
+
+struct Engine {
+    std::mutex mu;                   // one multipath enqueue at a time
+    bool inited = false;
+    mma_config_t cfg{};
+    int ndev = 0;
+    bool p2p[MMA_MAX_GPUS][MMA_MAX_GPUS] = {};
+    DevRes dev[MMA_MAX_GPUS];
+    Target tgt[MMA_MAX_GPUS];
+    std::map<cudaStream_t, cudaEvent_t> join_ev;   // join event per engine stream
+    // backlog ledger (NEXT-1): bytes in flight per (direction, link GPU), and of those the
+    // link's own target's direct bytes; each call's share is retired when its done event
+    // (recorded on the user stream at the join) has completed
+    struct InFlight {
+        cudaEvent_t done;
+        int dev, dir;
+        uint64_t bytes[MMA_MAX_GPUS];
+        uint64_t own[MMA_MAX_GPUS];
+    };
+    std::vector<InFlight> inflight;
+    std::vector<std::pair<int, cudaEvent_t>> free_events;
+    uint64_t ledger[2][MMA_MAX_GPUS] = {};
+    uint64_t ledger_own[2][MMA_MAX_GPUS] = {};
+    int* err = nullptr;              // mapped pinned host word (sticky async error)
+    PFN_memop64 wait64 = nullptr, write64 = nullptr;
+    uint64_t timeout_ns = 20ull * 1000 * 1000 * 1000;
+    uint32_t unit_bytes = kDefaultUnit;
+    // fault injection (tests only, MMA_FAULT_DROP_PUBLISH=g): the hop-1 publish of global
+    // ring chunk g is never issued, so the relay kernel must time out, record the sticky
+    // error and release the ring instead of hanging (SURVEY §5 failure detection)
+    long long fault_drop_publish = -1;
+};
+
+Engine& E();
+
+size_t env_size(const char* name, size_t dflt);
+
+int env_int(const char* name, int dflt);
+
+
+// ------------------------------------------------------------------ transfer job ---
+
+struct Piece {
+    uint64_t v;       // offset in v
+    uint64_t len;
+    const char* src;
+    char* dst;
+};
+
+struct Job {
+    int dir = 0;
+    int d = 0;                       // target GPU
+    cudaStream_t user = nullptr;
+    int user_dev = 0;
+    uint64_t B = 0;
+    uint64_t C = 0;
+    bool contiguous = true;
+    const char* src0 = nullptr;
+    char* dst0 = nullptr;
+    const mma_segment_t* segs = nullptr;
+    uint64_t nseg = 0;
+    std::vector<uint64_t> vstart;    // segmented: prefix offsets [nseg + 1]
+    bool mapped = false;             // every host address is usable by GPU SMs
+    const uint32_t* bw_override = nullptr;   // measurement runs: per-path bandwidth
+    const int* mode_override = nullptr;      // measurement runs: per-path mode
+    bool no_small_fallback = false;          // measurement runs: ignore the threshold
+
+    // pieces of v[a, b) (the per-segment parts; one piece when contiguous)
+    template <typename F>
+    void pieces(uint64_t a, uint64_t b, F f) const
+    {
+        if (a >= b) return;
+        if (contiguous) { f(Piece{a, b - a, src0 + a, dst0 + a}); return; }
+        uint64_t k = std::upper_bound(vstart.begin(), vstart.end(), a) - vstart.begin() - 1;
+        for (; k < nseg && vstart[k] < b; k++) {
+            uint64_t lo = std::max(vstart[k], a), hi = std::min(vstart[k + 1], b);
+            if (lo >= hi) continue;
+            f(Piece{lo, hi - lo, (const char*)segs[k].src + (lo - vstart[k]),
+                    (char*)segs[k].dst + (lo - vstart[k])});
+        }
+    }
+    void extent(uint64_t i, uint64_t* off, uint64_t* len) const
+    {
+        *off = i * C;
+        *len = std::min(C, B - *off);
+    }
+};
+
+// Pieces copied by one DMA call: cudaMemcpyAsync for one, cudaMemcpyBatchAsync for many.
+struct DmaBatch {
+    std::vector<void*> dst, src;
+    std::vector<size_t> len;
+    void add(void* d, const void* s, size_t n)
+    {
+        if (!n) return;
+        if (!dst.empty() && (char*)dst.back() + len.back() == (char*)d && (const char*)src.back() + len.back() == (const char*)s) {
+            len.back() += n;    // merge adjacent pieces
+            return;
+        }
+        dst.push_back(d);
+        src.push_back(const_cast<void*>(s));
+        len.push_back(n);
+    }
+    int issue(cudaMemcpyKind kind, cudaStream_t s)
+    {
+        if (dst.empty()) return cudaSuccess;
+        if (dst.size() == 1) return (int)cudaMemcpyAsync(dst[0], src[0], len[0], kind, s);
+        if (s == nullptr || s == cudaStreamLegacy) {   // the batch API rejects the legacy stream
+            for (size_t i = 0; i < dst.size(); i++) CK(cudaMemcpyAsync(dst[i], src[i], len[i], kind, s));
+            return cudaSuccess;
+        }
+        cudaMemcpyAttributes at;
+        memset(&at, 0, sizeof(at));
+        at.srcAccessOrder = cudaMemcpySrcAccessOrderStream;
+        size_t idx = 0, fail = 0;
+        cudaError_t e = cudaMemcpyBatchAsync(dst.data(), src.data(), len.data(), dst.size(), &at, &idx, 1, &fail, s);
+        if (e == cudaSuccess) return cudaSuccess;
+        cudaGetLastError();
+        for (size_t i = 0; i < dst.size(); i++) CK(cudaMemcpyAsync(dst[i], src[i], len[i], kind, s));
+        return cudaSuccess;
+    }
+};
+
+// ---- plane.cpp
+void apply_env(mma_config_t* c);
+void defaults(mma_config_t* c);
+int validate_cfg(const mma_config_t& c);
+int make_device(int d);
+int do_init(const mma_config_t* cfg);
+int ensure_init();
+void make_paths(int d);
+void free_ring(Ring& r);
+int get_ring(int d, int dir, int p, uint64_t C, uint32_t S, Ring** out);
+void ledger_inputs(int d, int dir, const std::vector<PathState>& ps, std::vector<PlanPath>& pp);
+int run_job(Job& j);
+int sticky();
+extern bool g_ktime;
+struct KRec {
+    int dev;
+    int kind;   // 0 zero-copy, 1 relay pull (H2D), 2 relay pack (D2H), 3 dynamic | dir << 4 | path << 8 | dev << 16
+    cudaEvent_t a, b;
+};
+extern std::vector<KRec> g_kpending;
+// ---- api.cpp
+int prepare_segments(int dir, const mma_segment_t* segs, size_t nsegs, int device, cudaStream_t stream, Job& j);
+
+}  // namespace mma
