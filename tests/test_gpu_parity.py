@@ -209,3 +209,43 @@ def test_device_generator_matches_host(mma):
         mma.verify_pattern(d, n, 0x4D4D41, off, cnt)
         torch.cuda.synchronize()
         assert int(cnt.item()) == 1
+
+
+@pytest.mark.timeout(900)
+def test_max_size_16gib(mma):
+    """The sweep's largest size (16 GiB, config 2) through a copy-engine relay ring and the
+    direct path, both directions; every byte checked on the device against the pattern."""
+    B, C = 16 << 30, 4 * MiB
+    configure(mma, loopback=1, chunk=C, slots=4, plan_mode=0, hop=(1, 2), debug=0)
+    mma.set_bandwidth(0, mma.H2D, [1, 1])
+    mma.set_bandwidth(0, mma.D2H, [1, 1])
+    seed = 0x4D4D41 + 2
+    dev = torch.empty(B, dtype=torch.uint8, device="cuda")
+    mma.fill_pattern(dev, B, seed, 0)
+    host = torch.empty(B, dtype=torch.uint8).pin_memory()
+    mma.memcpy_d2h(host, dev, B)                       # D2H: direct ZC + loopback ZC relay
+    dev2 = torch.zeros(B, dtype=torch.uint8, device="cuda")
+    mma.memcpy_h2d(dev2, host, B)                      # H2D: direct CE + loopback CE ring
+    cnt = torch.zeros(1, dtype=torch.int64, device="cuda")
+    mma.verify_pattern(dev2, B, seed, 0, cnt)
+    torch.cuda.synchronize()
+    assert mma.get_last_error() == 0
+    assert int(cnt.item()) == 0
+    st = mma.get_stats(0)
+    assert st["path_bytes"][0][1] > 0 and st["path_bytes"][1][1] > 0
+
+
+def test_degenerate_segment_tables(mma):
+    configure(mma, loopback=1, chunk=MiB, hop=(2, 2))
+    host = torch.empty(MiB, dtype=torch.uint8).pin_memory()
+    dev = torch.empty(MiB, dtype=torch.uint8, device="cuda")
+    segs, n = mma.make_segments([], [], [])
+    mma.memcpy_h2d_segments(segs, 0, 0)                                 # no segments
+    segs, n = mma.make_segments([host.data_ptr()] * 3, [dev.data_ptr()] * 3, [0, 0, 0])
+    mma.memcpy_h2d_segments(segs, n, 0)                                 # only empty ones
+    segs, n = mma.make_segments([host.data_ptr()], [dev.data_ptr()], [1])
+    mma.memcpy_h2d_segments(segs, n, 0)                                 # one byte
+    torch.cuda.synchronize()
+    assert dev[0].item() == host[0].item()
+    with pytest.raises(mma.MMAError):
+        mma.memcpy_h2d_segments(segs, n, 7, stream=torch.cuda.current_stream())  # no such device
