@@ -45,7 +45,7 @@ def parse():
     ap.add_argument("--workload", choices=["kv", "contig", "wake"], default="kv")
     ap.add_argument("--bytes", type=int, default=4 * GiB, help="contig workload size")
     ap.add_argument("--tokens", type=int, default=32768, help="kv workload tokens")
-    ap.add_argument("--chunk", type=int, default=4 * MiB)
+    ap.add_argument("--chunk", type=int, default=0, help="chunk bytes (0 = the engine's default)")
     ap.add_argument("--hop", type=int, default=0, help="0 auto, 1 copy engine, 2 SM zero-copy")
     ap.add_argument("--no-verify", action="store_true")
     ap.add_argument("--quick", action="store_true", help="skip baselines (profiling runs)")
@@ -387,7 +387,8 @@ def main():
 
     def configure(relays):
         cfg = mma.default_config()
-        cfg.chunk_bytes[0] = cfg.chunk_bytes[1] = args.chunk
+        if args.chunk:
+            cfg.chunk_bytes[0] = cfg.chunk_bytes[1] = args.chunk
         cfg.npaths = len(relays) if relays else 1
         for i, g in enumerate(relays or [0]):
             cfg.path_gpus[i] = g          # [0] alone = no relay candidates (self is skipped)
@@ -617,7 +618,7 @@ def main():
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u8",
         "data": "synthetic",
         "config": {"workload": w["desc"], "paths": k, "path_gpus": path_gpus, "target_gpu": 0,
-                   "chunk_bytes": args.chunk, "hop": {0: "auto", 1: "ce", 2: "zc"}[args.hop],
+                   "chunk_bytes": int(cfg.chunk_bytes[0]), "claim_bytes": int(cfg.claim_bytes), "hop": {0: "auto", 1: "ce", 2: "zc"}[args.hop],
                    "bytes_per_step": nbytes_step, "l2": f"inputs ({w['bytes'] / GiB:.1f} GiB per direction) exceed the 126 MB L2; no flush",
                    "parallelism": f"1 process drives {k} path GPU(s); torchrun ranks>0 idle on gloo",
                    "visible_devices": vis_note, "multipath_error": multipath_error},

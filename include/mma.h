@@ -53,7 +53,8 @@ typedef struct {
 
 typedef struct {
     /* chunk size per direction in bytes (§3.4.1 "fixed chunk size"; P:902 tuned
-     * optima 2.81 MB H2D / 5.37 MB D2H). 0 = default (4 MiB). Multiple of 4096. */
+     * optima 2.81 MB H2D / 5.37 MB D2H on H20). Default 8 MiB (B200 DMA setup cost,
+     * DESIGN.md §6). Multiple of 4096. */
     size_t chunk_bytes[2];
     /* relay staging slots per ring (P:588-594 dual pipeline = 2). 0 = default (4). */
     unsigned ring_slots;
@@ -87,6 +88,10 @@ typedef struct {
      * whose own link still carries its own target's direct bytes ("direct path first",
      * P:564-565 §3.4.2). 0 = off, 1 = on (default). */
     int ledger;
+    /* dynamic pull (plan_mode 2): bytes one CTA claims at a time; the delivery log has one
+     * entry per claim. Small claims keep every link's share proportional to its speed
+     * (the paper's outstanding-queue depth). 0 = default (256 KiB). */
+    size_t claim_bytes;
 } mma_config_t;
 
 typedef struct {

@@ -62,6 +62,7 @@ void apply_env(mma_config_t* c)
     c->numa_mode = env_int("MMA_NUMA", c->numa_mode);
     c->debug_log = env_int("MMA_DEBUG_LOG", c->debug_log);
     c->ledger = env_int("MMA_LEDGER", c->ledger);
+    c->claim_bytes = env_size("MMA_CLAIM_BYTES", c->claim_bytes);
     if (const char* s = getenv("MMA_PATHS")) {   // comma-separated relay GPU ids
         c->npaths = 0;
         for (const char* p = s; *p && c->npaths < MMA_MAX_PATHS;) {
@@ -86,6 +87,7 @@ void defaults(mma_config_t* c)
     c->hop_mode[0] = c->hop_mode[1] = MMA_HOP_AUTO;
     c->relay_ctas = kDefaultRelayCtas;
     c->ledger = 1;
+    c->claim_bytes = 256u << 10;
 }
 
 int validate_cfg(const mma_config_t& c)
@@ -99,6 +101,7 @@ int validate_cfg(const mma_config_t& c)
     for (int d = 0; d < 2; d++)
         if (c.hop_mode[d] < MMA_HOP_AUTO || c.hop_mode[d] > MMA_HOP_ZC) return cudaErrorInvalidValue;
     if (c.relay_ctas < 1 || c.relay_ctas > 64) return cudaErrorInvalidValue;
+    if (c.claim_bytes % 16) return cudaErrorInvalidValue;
     return cudaSuccess;
 }
 
@@ -511,6 +514,8 @@ int run_job(Job& j)
     }
     if (dynamic)
         for (int p = 0; p < P; p++) active[p] = pp[p].mbps > 0;
+    const uint64_t claimC = e.cfg.claim_bytes ? e.cfg.claim_bytes : (256u << 10);
+    const uint64_t n_log = dynamic ? (j.B - 1) / claimC + 1 : n;   // log entries
 
     // ---- host tables: chunk lists (interleaved plans) and the segment table
     const bool need_ctab = e.cfg.plan_mode == PLAN_INTERLEAVED && !dynamic;
@@ -615,17 +620,17 @@ int run_job(Job& j)
     // delivery log (debug)
     uint8_t* log = nullptr;
     if (e.cfg.debug_log) {
-        if (t.log_cap < n) {
+        if (t.log_cap < n_log) {
             DeviceGuard g(j.d);
             if (t.log) cudaFree(t.log);
-            CK(cudaMalloc(&t.log, n));
-            t.log_cap = n;
+            CK(cudaMalloc(&t.log, n_log));
+            t.log_cap = n_log;
         }
         log = t.log;
-        t.log_n = n;
+        t.log_n = n_log;
         DeviceGuard g(j.d);
         CK((cudaError_t)use(e.dev[j.d].direct, j.d));
-        CK(cudaMemsetAsync(log, 0xff, n, e.dev[j.d].direct));
+        CK(cudaMemsetAsync(log, 0xff, n_log, e.dev[j.d].direct));
     } else {
         t.log_n = 0;
     }
@@ -658,12 +663,13 @@ int run_job(Job& j)
             if (s != zs) CK(cudaStreamWaitEvent(s, zeroed, 0));
             DynLaunchArg a{};
             a.v = vstream_on(g);
-            a.nchunks = n;
+            a.v.C = claimC;              // the claim unit plays the chunk's role
+            a.nchunks = n_log;
             a.cursor = slot;
             a.counts = slot + 1;
             a.path = (uint32_t)p;
             a.log = log;
-            const unsigned grid = (unsigned)std::min<uint64_t>(n, (uint64_t)e.dev[g].sms * 4);
+            const unsigned grid = (unsigned)std::min<uint64_t>(n_log, (uint64_t)e.dev[g].sms * 4);
             KTimer kt(g, s, 3 | (j.dir << 4) | (p << 8));
             CK(launch_zc_dyn(a, grid, s));
             t.stats.kernels++;

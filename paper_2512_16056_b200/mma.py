@@ -44,6 +44,7 @@ class Config(C.Structure):
         ("numa_mode", C.c_int),
         ("debug_log", C.c_int),
         ("ledger", C.c_int),
+        ("claim_bytes", C.c_size_t),
     ]
 
 

@@ -9,9 +9,10 @@ G = 4096   # guard band bytes on each side of a destination
 
 
 def configure(mma, *, loopback=1, chunk=1 << 20, slots=2, plan_mode=0, hop=(0, 0),
-              thr=0, ctas=8, debug=1, paths=None):
+              thr=0, ctas=8, debug=1, paths=None, claim=None):
     cfg = mma.default_config()
     cfg.chunk_bytes[0] = cfg.chunk_bytes[1] = chunk
+    cfg.claim_bytes = chunk if claim is None else claim   # dynamic pull claims = chunks
     cfg.ring_slots = slots
     cfg.fallback_bytes[0] = cfg.fallback_bytes[1] = thr
     cfg.loopback_relays = loopback
