@@ -227,11 +227,13 @@ def run_step(mma, w, dev_idx, stream, ev=None):
 
 # --------------------------------------------------------------- cpu baseline ---
 
-def oracle_sample(k_paths, nsegs_sample=16384, reps=1):
+def oracle_sample(k_paths, nsegs_sample=16384, reps=1, min_seconds=0.0):
     """The oracle's threaded mover (1 thread for the direct path + 2 per relay ring) on a
     bounded sample of the KV workload: the first `nsegs_sample` segments, gathered from
     their scattered slots of a pinned-pool-sized host buffer into a packed host 'cache',
-    then scattered back (offload). Returns (GB/s, threads, sample description)."""
+    then scattered back (offload); repeated `reps` times or until `min_seconds` of CPU work
+    (at most 30 repetitions). Returns (GB/s of the median repetition, threads, sample
+    description, bytes per repetition, seconds of the median repetition)."""
     import numpy as np
     import oracle
     from mma_inputs import workloads as W
@@ -251,18 +253,18 @@ def oracle_sample(k_paths, nsegs_sample=16384, reps=1):
     rc, path, _, _ = oracle.plan(bw, B, C, 0, oracle.CONTIG)
     f_segs, n = oracle.segments_from_arrays(pool.ctypes.data + ho, cache.ctypes.data + dofs, lens)
     o_segs, _ = oracle.segments_from_arrays(cache.ctypes.data + dofs, pool.ctypes.data + ho, lens)
-    best = None
-    for _ in range(reps):
+    times = []
+    while len(times) < max(reps, 1) or (sum(times) < min_seconds and len(times) < 30):
         t0 = time.perf_counter()
         assert oracle.move(f_segs, n, C, bw, path, S=4, exec_mode=oracle.THREADED) == 0
         assert oracle.move(o_segs, n, C, bw, path, S=4, exec_mode=oracle.THREADED) == 0
-        dt = time.perf_counter() - t0
-        best = dt if best is None else min(best, dt)
+        times.append(time.perf_counter() - t0)
+    med = statistics.median(times)
     threads = 1 + 2 * (k_paths - 1)
     desc = (f"oracle threaded mover (oracle/mma_oracle.c, exec=threaded, {k_paths}-path plan), first "
             f"{nsegs_sample} of 131072 KV segments ({B / MiB:.0f} MiB) fetched into a packed host buffer "
-            f"and offloaded back, host memory only")
-    return 2 * B / best / 1e9, threads, desc, 2 * B, best
+            f"and offloaded back, host memory only; {len(times)} repetitions ({sum(times):.1f} s), median")
+    return 2 * B / med / 1e9, threads, desc, 2 * B, med
 
 
 def run_reference(args, dist):
@@ -607,7 +609,7 @@ def main():
     cpu = None
     if not args.quick and dist.world == 1:
         try:
-            g, threads, desc, _, _ = oracle_sample(k, nsegs_sample=16384)
+            g, threads, desc, _, _ = oracle_sample(k, nsegs_sample=32768, min_seconds=10.0)
             cpu = {"value": round(g, 3), "unit": "GB/s", "cores": threads, "kind": "oracle", "sample": desc}
         except Exception as ex:  # noqa: BLE001
             cpu = {"value": None, "unit": "GB/s", "cores": 0, "kind": "oracle", "sample": f"failed: {ex}"}
