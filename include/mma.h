@@ -9,9 +9,13 @@
  *    before anything is enqueued: a call that returns an error enqueued nothing.
  *  - Asynchronous failures (a relay kernel whose bounded spin timed out) are sticky: they
  *    are returned by the next mma_* call and by mma_get_last_error().
- *  - Thread safety: every call may be made from any thread. Calls for the same target GPU
- *    serialise at enqueue time. One engine per process (§5.1.2 "each process in MMA
- *    maintains its own multipath queue").
+ *  - Thread safety: every call may be made from any thread. Multipath calls serialise at
+ *    enqueue time. One engine per process (§5.1.2 "each process in MMA maintains
+ *    its own multipath queue").
+ *  - Ordering between calls: the engine's path streams are shared, so multipath calls run
+ *    in enqueue order on them. Like any shared resource this adds one rule that plain
+ *    cudaMemcpyAsync does not have: a call must not be made to wait (through stream or
+ *    event dependencies) on a multipath call enqueued after it.
  *  - Pointers are plain host or device virtual addresses (UVA). The library never takes
  *    ownership of caller memory; it owns its streams, events, staging rings and flags,
  *    all released by mma_finalize().
