@@ -167,6 +167,24 @@ def test_full_size_kv_fetch(mma, orc):
         assert orc.move(segs1, n1, sb, [1], np.zeros(1, np.uint8)) == 0
         got = cache[int(do[k]):int(do[k]) + sb].cpu().numpy()
         assert np.array_equal(got, exp)
+    # the bench's measured modes: fetch by the copy engine (batch), offload by the
+    # zero-copy kernel into a fresh pool; the offloaded slots must equal the original pool
+    mma.set_path_modes(0, mma.H2D, [mma.HOP_CE])
+    mma.set_path_modes(0, mma.D2H, [mma.HOP_ZC])
+    cache.fill_(0xA5)
+    mma.memcpy_h2d_segments(segs, n, 0)
+    back = torch.zeros(hpool, dtype=torch.uint8).pin_memory()
+    osegs, on = mma.make_segments(cache.data_ptr() + do, back.data_ptr() + ho, lens)
+    mma.memcpy_d2h_segments(osegs, on, 0)
+    torch.cuda.synchronize()
+    assert mma.get_last_error() == 0
+    bn = back.numpy()
+    for k in rng.choice(len(ho), 256, replace=False):
+        assert np.array_equal(bn[ho[k]:ho[k] + sb], hnp[ho[k]:ho[k] + sb])
+    untouched = np.ones(hpool // sb, bool)
+    untouched[ho // sb] = False
+    free_slot = int(np.flatnonzero(untouched)[0])
+    assert not bn[free_slot * sb:(free_slot + 1) * sb].any()     # slots outside the table stay 0
 
 
 def test_mode_choice_by_measurement(mma, orc):
