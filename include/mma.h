@@ -82,7 +82,8 @@ typedef struct {
     int hop_mode[2];
     /* CTAs per relay ring for the relay kernels; 0 = default (8) */
     int relay_ctas;
-    /* NUMA placement for mma_host_alloc: 0 = off, 1 = local to the target, 2 = spread */
+    /* NUMA placement for mma_host_alloc: 0 = default, 1 = bind to node 0, 2 = interleave
+     * across all nodes (a no-op on a single-node host) */
     int numa_mode;
     /* record the per-chunk delivery log (debug; off in timed runs) */
     int debug_log;
@@ -209,6 +210,38 @@ int mma_host_free(void* ptr);
  * path 255 = all rings of the launch. */
 int mma_set_kernel_timing(int on);
 int mma_kernel_times(float* ms, int* kinds, size_t cap, size_t* n);
+
+/*
+ * Multi-process mode (one process per GPU, as in tensor-parallel serving).
+ * The target's process exports its destination memory; the host buffer is shared memory
+ * registered in every process; each process moves its own share on its own GPU with the
+ * zero-copy kernel. Nothing here is a collective: the processes agree on the plan by
+ * computing it with mma_plan_chunks from the same inputs.
+ *  - mma_shared_host_alloc: `bytes` of pinned, mapped host memory shared by name between
+ *    processes (create = 1 in one process first, 0 in the others); /dev/shm when it has
+ *    room, else MMA_SHM_DIR or /tmp. mma_shared_host_free unmaps (and unlinks `name` if
+ *    given).
+ *  - mma_ipc_export writes a 64-byte CUDA IPC handle of the allocation holding dev_ptr and
+ *    dev_ptr's offset in it; mma_ipc_open maps it on `device` of another process (peer
+ *    access enabled lazily) and returns the matching pointer; mma_ipc_close unmaps.
+ *  - mma_copy_share_segments moves the chunks i of the table with path_of_chunk[i] == path
+ *    (a plan from mma_plan_chunks for the same bytes and chunk size) with a zero-copy kernel
+ *    on `device`; pointers must be valid in this process. Direction follows the pointers.
+ *  - mma_copy_claim_segments is the dynamic-pull form: claim_bytes units are claimed from
+ *    *cursor (device memory, e.g. IPC-mapped from the target, zeroed before the transfer)
+ *    until none is left; counts[path] += units taken.
+ */
+int mma_shared_host_alloc(const char* name, size_t bytes, int create, void** ptr);
+int mma_shared_host_free(void* ptr, const char* unlink_name);
+int mma_ipc_export(const void* dev_ptr, void* handle, uint64_t* offset);
+int mma_ipc_open(const void* handle, uint64_t offset, int device, void** dev_ptr);
+int mma_ipc_close(void* dev_ptr);
+int mma_copy_share_segments(const mma_segment_t* segs, size_t nsegs, size_t chunk_bytes,
+                            const uint8_t* path_of_chunk, size_t nchunks, int path, int device,
+                            mma_stream_t stream);
+int mma_copy_claim_segments(const mma_segment_t* segs, size_t nsegs, size_t claim_bytes,
+                            uint64_t* cursor, uint64_t* counts, int path, int device,
+                            mma_stream_t stream);
 
 int mma_get_stats(int device, mma_stats_t* out);
 int mma_reset_stats(int device);

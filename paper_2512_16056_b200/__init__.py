@@ -13,7 +13,8 @@ from .mma import (  # noqa: F401
     get_stats, host_alloc, host_array, host_free, init, make_segments, memcpy_d2h,
     memcpy_d2h_segments, memcpy_h2d, memcpy_h2d_segments, plan_chunks, reset_stats,
     set_bandwidth, set_path_modes, tune_segments, get_dynamic_counts, set_plan_mode, set_kernel_timing, kernel_times, fill_pattern,
-    verify_pattern, verify_segments,
+    verify_pattern, verify_segments, shared_host_alloc, shared_host_free, ipc_export, ipc_open,
+    ipc_close, copy_share_segments, copy_claim_segments,
 )
 
 try:

@@ -20,6 +20,7 @@ SOURCES = [
     CSRC / "plane.cpp",
     CSRC / "api.cpp",
     CSRC / "tune.cpp",
+    CSRC / "mp.cpp",
     CSRC / "planner.cpp",
     CSRC / "hostmem.cpp",
     CSRC / "kernels" / "relay.cu",

@@ -1,0 +1,249 @@
+// mp.cpp — multi-process mode: one process per GPU, as in vLLM tensor
+// parallel serving. The target's process exports its destination memory (CUDA IPC) and the
+// host buffer lives in shared memory registered by every process; each process then moves
+// its own share of the transfer on its own GPU with the zero-copy kernel -- the chunks the
+// common plan gives its path (planned mode), or the chunks it claims from a cursor in the
+// target's memory (the dynamic pull of plane.cpp, across processes). No process creates a
+// context on another process's GPU, and nothing on the data path is a collective.
+#include <fcntl.h>
+#include <sys/mman.h>
+#include <sys/stat.h>
+#include <sys/statvfs.h>
+#include <unistd.h>
+
+#include "plane.h"
+
+namespace mma {
+
+namespace {
+
+struct SharedMap {
+    size_t len;
+    int fd;
+};
+std::mutex g_mp_mu;
+std::map<void*, SharedMap> g_shared;      // mapping -> length, fd
+std::map<void*, void*> g_ipc_base;        // user pointer -> IPC base to close
+
+using PFN_range = CUresult (*)(CUdeviceptr*, size_t*, CUdeviceptr);
+
+// A directory for the shared buffer: /dev/shm when it has room (tmpfs), else MMA_SHM_DIR or
+// /tmp (a file-backed shared mapping; its pages are locked by cudaHostRegister).
+std::string shared_path(const char* name, size_t bytes)
+{
+    std::string dir = "/dev/shm";
+    struct statvfs v;
+    if (statvfs(dir.c_str(), &v) != 0 || (uint64_t)v.f_bavail * v.f_frsize < bytes + (64u << 20)) {
+        const char* d = getenv("MMA_SHM_DIR");
+        dir = d ? d : "/tmp";
+    }
+    return dir + "/mma_" + name;
+}
+
+// Segment table (and chunk list) on the device for one launch: allocated and freed in
+// stream order.
+int upload(const void* host, size_t bytes, cudaStream_t s, void** dev)
+{
+    *dev = nullptr;
+    if (!bytes) return cudaSuccess;
+    CK(cudaMallocAsync(dev, bytes, s));
+    return (int)cudaMemcpyAsync(*dev, host, bytes, cudaMemcpyHostToDevice, s);
+}
+
+int vstream_from(const mma_segment_t* segs, size_t nsegs, uint64_t C, cudaStream_t s,
+                 VStreamArg& v, void** dtab)
+{
+    v = VStreamArg{};
+    v.C = C;
+    *dtab = nullptr;
+    if (nsegs == 1) {
+        v.nseg = 1;
+        v.B = segs[0].bytes;
+        v.src0 = (uint64_t)segs[0].src;
+        v.dst0 = (uint64_t)segs[0].dst;
+        return cudaSuccess;
+    }
+    std::vector<uint64_t> w(3 * nsegs + 1);
+    w[0] = 0;
+    for (size_t k = 0; k < nsegs; k++) {
+        if (segs[k].bytes && (!segs[k].src || !segs[k].dst)) return cudaErrorInvalidValue;
+        w[k + 1] = w[k] + segs[k].bytes;
+        w[nsegs + 1 + k] = (uint64_t)segs[k].src;
+        w[2 * nsegs + 1 + k] = (uint64_t)segs[k].dst;
+    }
+    v.nseg = nsegs;
+    v.B = w[nsegs];
+    CK(upload(w.data(), w.size() * 8, s, dtab));
+    const uint64_t* d = (const uint64_t*)*dtab;
+    v.start = d;
+    v.src = d + nsegs + 1;
+    v.dst = d + 2 * nsegs + 1;
+    return cudaSuccess;
+}
+
+}  // namespace
+
+}  // namespace mma
+
+using namespace mma;
+
+extern "C" {
+
+int mma_shared_host_alloc(const char* name, size_t bytes, int create, void** ptr)
+{
+    if (!name || !*name || !ptr || bytes == 0) return cudaErrorInvalidValue;
+    CK((cudaError_t)ensure_init());
+    *ptr = nullptr;
+    const std::string path = shared_path(name, bytes);
+    int fd = open(path.c_str(), create ? (O_RDWR | O_CREAT | O_TRUNC) : O_RDWR, 0600);
+    if (fd < 0) return cudaErrorInvalidValue;
+    if (create && ftruncate(fd, (off_t)bytes) != 0) { close(fd); return cudaErrorMemoryAllocation; }
+    struct stat st;
+    if (fstat(fd, &st) != 0 || (size_t)st.st_size < bytes) { close(fd); return cudaErrorInvalidValue; }
+    void* p = mmap(nullptr, bytes, PROT_READ | PROT_WRITE, MAP_SHARED, fd, 0);
+    if (p == MAP_FAILED) { close(fd); return cudaErrorMemoryAllocation; }
+    if (create) memset(p, 0, bytes);           // allocate every page before pinning
+    cudaError_t e = cudaHostRegister(p, bytes, cudaHostRegisterPortable | cudaHostRegisterMapped);
+    if (e != cudaSuccess) { munmap(p, bytes); close(fd); return e; }
+    std::lock_guard<std::mutex> g(g_mp_mu);
+    g_shared[p] = SharedMap{bytes, fd};
+    *ptr = p;
+    return cudaSuccess;
+}
+
+int mma_shared_host_free(void* ptr, const char* unlink_name)
+{
+    SharedMap m;
+    {
+        std::lock_guard<std::mutex> g(g_mp_mu);
+        auto it = g_shared.find(ptr);
+        if (it == g_shared.end()) return cudaErrorInvalidValue;
+        m = it->second;
+        g_shared.erase(it);
+    }
+    cudaError_t e = cudaHostUnregister(ptr);
+    munmap(ptr, m.len);
+    close(m.fd);
+    if (unlink_name && *unlink_name) unlink(shared_path(unlink_name, 0).c_str());
+    return e;
+}
+
+int mma_ipc_export(const void* dev_ptr, void* handle, uint64_t* offset)
+{
+    if (!dev_ptr || !handle || !offset) return cudaErrorInvalidValue;
+    CK((cudaError_t)ensure_init());
+    cudaDriverEntryPointQueryResult q;
+    void* fn = nullptr;
+    if (cudaGetDriverEntryPointByVersion("cuMemGetAddressRange", &fn, 12000, cudaEnableDefault, &q) != cudaSuccess || !fn)
+        return cudaErrorNotSupported;
+    CUdeviceptr base = 0;
+    size_t size = 0;
+    if (((PFN_range)fn)(&base, &size, (CUdeviceptr)dev_ptr) != CUDA_SUCCESS) return cudaErrorInvalidValue;
+    cudaIpcMemHandle_t h;
+    CK(cudaIpcGetMemHandle(&h, (void*)base));
+    memcpy(handle, &h, sizeof h);
+    *offset = (uint64_t)dev_ptr - (uint64_t)base;
+    return cudaSuccess;
+}
+
+int mma_ipc_open(const void* handle, uint64_t offset, int device, void** dev_ptr)
+{
+    if (!handle || !dev_ptr) return cudaErrorInvalidValue;
+    CK((cudaError_t)ensure_init());
+    DeviceGuard g(device);
+    cudaIpcMemHandle_t h;
+    memcpy(&h, handle, sizeof h);
+    void* base = nullptr;
+    CK(cudaIpcOpenMemHandle(&base, h, cudaIpcMemLazyEnablePeerAccess));
+    *dev_ptr = (char*)base + offset;
+    std::lock_guard<std::mutex> lk(g_mp_mu);
+    g_ipc_base[*dev_ptr] = base;
+    return cudaSuccess;
+}
+
+int mma_ipc_close(void* dev_ptr)
+{
+    void* base;
+    {
+        std::lock_guard<std::mutex> lk(g_mp_mu);
+        auto it = g_ipc_base.find(dev_ptr);
+        if (it == g_ipc_base.end()) return cudaErrorInvalidValue;
+        base = it->second;
+        g_ipc_base.erase(it);
+    }
+    return (int)cudaIpcCloseMemHandle(base);
+}
+
+int mma_copy_share_segments(const mma_segment_t* segs, size_t nsegs, size_t chunk_bytes,
+                            const uint8_t* path_of_chunk, size_t nchunks, int path, int device,
+                            mma_stream_t stream)
+{
+    CK((cudaError_t)ensure_init());
+    if (int se = sticky()) return se;
+    if (!nsegs) return cudaSuccess;
+    if (!segs || !path_of_chunk || chunk_bytes == 0 || path < 0) return cudaErrorInvalidValue;
+    Engine& e = E();
+    if (device < 0 || device >= e.ndev) return cudaErrorInvalidDevice;
+    CK(make_device(device));
+    DeviceGuard g(device);
+    cudaStream_t s = (cudaStream_t)stream;
+    VStreamArg v;
+    void* dtab = nullptr;
+    CK(vstream_from(segs, nsegs, chunk_bytes, s, v, &dtab));
+    if ((v.B + chunk_bytes - 1) / chunk_bytes != nchunks && !(nchunks == 1 && v.B > 0))
+        return cudaErrorInvalidValue;
+    if (nchunks == 1) v.C = v.B;             // a one-piece (fallback) plan
+    std::vector<uint32_t> mine;
+    for (size_t i = 0; i < nchunks; i++)
+        if (path_of_chunk[i] == path) mine.push_back((uint32_t)i);
+    int rc = cudaSuccess;
+    if (!mine.empty()) {
+        void* dlist = nullptr;
+        rc = upload(mine.data(), mine.size() * 4, s, &dlist);
+        if (rc == cudaSuccess) {
+            ZcLaunchArg a{};
+            a.v = v;
+            a.chunks.count = mine.size();
+            a.chunks.table = (const uint32_t*)dlist;
+            a.unit_bytes = e.unit_bytes;
+            a.path = (uint32_t)path;
+            const uint64_t upc = (v.C + e.unit_bytes - 1) / e.unit_bytes;
+            const unsigned grid = (unsigned)std::min<uint64_t>(mine.size() * upc, (uint64_t)e.dev[device].sms * 4);
+            rc = launch_zc(a, grid, s);
+            cudaFreeAsync(dlist, s);
+        }
+    }
+    if (dtab) cudaFreeAsync(dtab, s);
+    return rc;
+}
+
+int mma_copy_claim_segments(const mma_segment_t* segs, size_t nsegs, size_t claim_bytes,
+                            uint64_t* cursor, uint64_t* counts, int path, int device,
+                            mma_stream_t stream)
+{
+    CK((cudaError_t)ensure_init());
+    if (int se = sticky()) return se;
+    if (!nsegs) return cudaSuccess;
+    if (!segs || !cursor || !counts || claim_bytes == 0 || path < 0 || path >= MMA_KMAX_RINGS)
+        return cudaErrorInvalidValue;
+    Engine& e = E();
+    if (device < 0 || device >= e.ndev) return cudaErrorInvalidDevice;
+    CK(make_device(device));
+    DeviceGuard g(device);
+    cudaStream_t s = (cudaStream_t)stream;
+    VStreamArg v;
+    void* dtab = nullptr;
+    CK(vstream_from(segs, nsegs, claim_bytes, s, v, &dtab));
+    DynLaunchArg a{};
+    a.v = v;
+    a.nchunks = (v.B + claim_bytes - 1) / claim_bytes;
+    a.cursor = (unsigned long long*)cursor;
+    a.counts = (unsigned long long*)counts;
+    a.path = (uint32_t)path;
+    const unsigned grid = (unsigned)std::min<uint64_t>(a.nchunks, (uint64_t)e.dev[device].sms * 4);
+    int rc = a.nchunks ? launch_zc_dyn(a, grid, s) : cudaSuccess;
+    if (dtab) cudaFreeAsync(dtab, s);
+    return rc;
+}
+
+}  // extern "C"

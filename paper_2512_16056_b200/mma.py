@@ -27,6 +27,8 @@ SYMBOLS = [
     "mma_reset_stats", "mma_get_last_error", "mma_error_string", "mma_fill_pattern",
     "mma_verify_pattern", "mma_verify_segments", "mma_set_kernel_timing", "mma_kernel_times",
     "mma_tune_segments", "mma_get_segment_tuning", "mma_get_dynamic_counts", "mma_set_plan_mode",
+    "mma_shared_host_alloc", "mma_shared_host_free", "mma_ipc_export", "mma_ipc_open", "mma_ipc_close",
+    "mma_copy_share_segments", "mma_copy_claim_segments",
 ]
 
 
@@ -107,6 +109,13 @@ def lib():
         L.mma_get_segment_tuning.argtypes = [C.c_int, C.c_int, vp, vp, C.c_int, C.POINTER(C.c_int)]
         L.mma_get_dynamic_counts.argtypes = [C.c_int, vp, C.c_int, C.POINTER(C.c_int)]
         L.mma_set_plan_mode.argtypes = [C.c_int]
+        L.mma_shared_host_alloc.argtypes = [C.c_char_p, sz, C.c_int, C.POINTER(vp)]
+        L.mma_shared_host_free.argtypes = [vp, C.c_char_p]
+        L.mma_ipc_export.argtypes = [vp, vp, C.POINTER(C.c_uint64)]
+        L.mma_ipc_open.argtypes = [vp, C.c_uint64, C.c_int, C.POINTER(vp)]
+        L.mma_ipc_close.argtypes = [vp]
+        L.mma_copy_share_segments.argtypes = [C.POINTER(Segment), sz, sz, vp, sz, C.c_int, C.c_int, vp]
+        L.mma_copy_claim_segments.argtypes = [C.POINTER(Segment), sz, sz, vp, vp, C.c_int, C.c_int, vp]
         _lib = L
     return _lib
 
@@ -351,3 +360,48 @@ def kernel_times():
         t = kinds[i]
         out.append(dict(ms=ms[i], kind=t & 15, dir=(t >> 4) & 15, path=(t >> 8) & 255, dev=t >> 16))
     return out
+
+
+# ---- multi-process mode (one process per GPU) -------------------------------
+
+def shared_host_alloc(name: str, nbytes: int, create: bool) -> int:
+    p = C.c_void_p()
+    _check(lib().mma_shared_host_alloc(name.encode(), nbytes, 1 if create else 0, C.byref(p)),
+           "mma_shared_host_alloc")
+    return int(p.value)
+
+
+def shared_host_free(ptr: int, unlink_name: str | None = None) -> None:
+    _check(lib().mma_shared_host_free(ptr, unlink_name.encode() if unlink_name else None),
+           "mma_shared_host_free")
+
+
+def ipc_export(dev_ptr) -> tuple[bytes, int]:
+    h = (C.c_uint8 * 64)()
+    off = C.c_uint64()
+    _check(lib().mma_ipc_export(_ptr(dev_ptr), h, C.byref(off)), "mma_ipc_export")
+    return bytes(h), off.value
+
+
+def ipc_open(handle: bytes, offset: int, device: int) -> int:
+    h = (C.c_uint8 * 64).from_buffer_copy(handle)
+    p = C.c_void_p()
+    _check(lib().mma_ipc_open(h, offset, device, C.byref(p)), "mma_ipc_open")
+    return int(p.value)
+
+
+def ipc_close(dev_ptr: int) -> None:
+    _check(lib().mma_ipc_close(dev_ptr), "mma_ipc_close")
+
+
+def copy_share_segments(segs, nsegs: int, chunk_bytes: int, path_of_chunk: bytes, path: int,
+                        device: int, stream=None) -> None:
+    buf = (C.c_uint8 * max(len(path_of_chunk), 1)).from_buffer_copy(path_of_chunk or b"\0")
+    _check(lib().mma_copy_share_segments(segs, nsegs, chunk_bytes, buf, len(path_of_chunk), path, device,
+                                         _stream(stream, device)), "mma_copy_share_segments")
+
+
+def copy_claim_segments(segs, nsegs: int, claim_bytes: int, cursor_ptr: int, counts_ptr: int,
+                        path: int, device: int, stream=None) -> None:
+    _check(lib().mma_copy_claim_segments(segs, nsegs, claim_bytes, cursor_ptr, counts_ptr, path, device,
+                                         _stream(stream, device)), "mma_copy_claim_segments")

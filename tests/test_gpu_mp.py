@@ -1,0 +1,97 @@
+"""Multi-process mode: two processes (gloo world size 2) share one GPU here;
+the target process exports its destination with CUDA IPC, the host pool is shared memory,
+and each process moves its share of a scattered KV fetch -- planned (mma_plan_chunks +
+mma_copy_share_segments) and dynamic (mma_copy_claim_segments on an IPC-shared cursor).
+The target checks every byte on the device against the seeded pattern."""
+import json
+import os
+import socket
+import subprocess
+import sys
+from pathlib import Path
+
+import pytest
+
+ROOT = Path(__file__).resolve().parents[1]
+pytestmark = [pytest.mark.gpu, pytest.mark.timeout(300)]
+
+WORKER = r"""
+import json, os, sys
+sys.path.insert(0, {root!r})
+import numpy as np, torch, torch.distributed as dist
+import paper_2512_16056_b200 as mma
+import mma_inputs
+from mma_inputs import workloads as W
+rank = int(os.environ["RANK"]); dist.init_process_group("gloo")
+torch.cuda.set_device(0)
+shape = W.scaled_kv(1024); ho, do, sb, hpool, dbytes = W.kv_segments(shape)
+name = "mp_test_" + os.environ["MASTER_PORT"]; seed = 91
+if rank == 0:
+    pool = mma.shared_host_alloc(name, hpool, True)
+    mma.host_array(pool, hpool)[:] = mma_inputs.pattern_bytes(seed, hpool)
+    dst = torch.zeros(dbytes, dtype=torch.uint8, device="cuda")
+    ctr = torch.zeros(32, dtype=torch.int64, device="cuda")
+    obj = [(mma.ipc_export(dst), mma.ipc_export(ctr))]
+else:
+    obj = [None]
+dist.barrier()
+dist.broadcast_object_list(obj, src=0)
+(hd, od), (hc, oc) = obj[0]
+if rank == 1:
+    pool = mma.shared_host_alloc(name, hpool, False)
+    dptr = mma.ipc_open(hd, od, 0); cptr = mma.ipc_open(hc, oc, 0)
+else:
+    dptr, cptr = dst.data_ptr(), ctr.data_ptr()
+lens = np.full(len(ho), sb, dtype=np.int64)
+segs, n = mma.make_segments(pool + ho, dptr + do, lens)
+B = int(lens.sum()); C = 1 << 20
+rc, path, fb = mma.plan_chunks([3, 1], [0, 1], B, C, 0, 1)
+s = torch.cuda.Stream()
+mma.copy_share_segments(segs, n, C, path, rank, 0, stream=s)
+s.synchronize(); dist.barrier()
+res = {{}}
+if rank == 0:
+    cnt = torch.zeros(1, dtype=torch.int64, device="cuda")
+    mma.verify_segments(dst.data_ptr() + do, ho, lens, seed, cnt); torch.cuda.synchronize()
+    res["planned_mismatch"] = int(cnt.item())
+    dst.zero_(); ctr.zero_(); torch.cuda.synchronize()
+dist.barrier()
+mma.copy_claim_segments(segs, n, 256 << 10, cptr, cptr + 8, rank, 0, stream=s)
+s.synchronize(); dist.barrier()
+if rank == 0:
+    cnt = torch.zeros(1, dtype=torch.int64, device="cuda")
+    mma.verify_segments(dst.data_ptr() + do, ho, lens, seed, cnt); torch.cuda.synchronize()
+    res["dynamic_mismatch"] = int(cnt.item())
+    counts = ctr.cpu().tolist()
+    res["claims"] = counts[1:3]; res["nclaims"] = (B + (256 << 10) - 1) // (256 << 10)
+    res["err"] = mma.get_last_error()
+    print(json.dumps(res), flush=True)
+dist.barrier()
+if rank == 1:
+    mma.ipc_close(dptr); mma.ipc_close(cptr); mma.shared_host_free(pool)
+dist.barrier()
+if rank == 0:
+    mma.shared_host_free(pool, name)
+dist.destroy_process_group()
+"""
+
+
+def test_two_processes_share_a_transfer(tmp_path):
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    s = socket.socket(); s.bind(("127.0.0.1", 0)); port = s.getsockname()[1]; s.close()
+    script = tmp_path / "w.py"
+    script.write_text(WORKER.format(root=str(ROOT)))
+    procs = []
+    for r in range(2):
+        env = dict(os.environ, RANK=str(r), WORLD_SIZE="2", LOCAL_RANK=str(r),
+                   MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+        procs.append(subprocess.Popen([sys.executable, str(script)], env=env, stdout=subprocess.PIPE,
+                                      stderr=subprocess.PIPE, text=True))
+    outs = [p.communicate(timeout=280) for p in procs]
+    for p, (o, e) in zip(procs, outs):
+        assert p.returncode == 0, e[-3000:]
+    r = json.loads(outs[0][0].strip().splitlines()[-1])
+    assert r["planned_mismatch"] == 0 and r["dynamic_mismatch"] == 0 and r["err"] == 0
+    assert sum(r["claims"]) == r["nclaims"]
