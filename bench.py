@@ -325,6 +325,48 @@ def pcie_rate(torch, g, nbytes=GiB, reps=8):
     return out
 
 
+def dram_read_rate(torch, nbytes=2 * GiB, reps=3):
+    """Host DRAM read GB/s with every core (torch CPU reduction over an int64 buffer)."""
+    t = torch.ones(nbytes // 8, dtype=torch.int64)
+    best = 1e9
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        t.sum()
+        best = min(best, time.perf_counter() - t0)
+    del t
+    return nbytes / best / 1e9
+
+
+def conc_rate(torch, gpus, per_gpu=512 * MiB, reps=3):
+    """R_conc(k): k concurrent plain cudaMemcpyAsync, each path GPU moving its own slice of
+    one pinned buffer: the achievable hop-1 ceiling of this box, exposing
+    shared switch uplinks and the host-memory ceiling."""
+    k = len(gpus)
+    host = torch.empty(k * per_gpu, dtype=torch.uint8).pin_memory()
+    devs = [torch.empty(per_gpu, dtype=torch.uint8, device=f"cuda:{g}") for g in gpus]
+    streams = [torch.cuda.Stream(device=g) for g in gpus]
+    out = {}
+    for name in ("h2d", "d2h"):
+        best = 1e9
+        for _ in range(reps):
+            for g in gpus:
+                torch.cuda.synchronize(g)
+            t0 = time.perf_counter()
+            for i, g in enumerate(gpus):
+                with torch.cuda.device(g), torch.cuda.stream(streams[i]):
+                    sl = host[i * per_gpu:(i + 1) * per_gpu]
+                    if name == "h2d":
+                        devs[i].copy_(sl, non_blocking=True)
+                    else:
+                        sl.copy_(devs[i], non_blocking=True)
+            for s in streams:
+                s.synchronize()
+            best = min(best, time.perf_counter() - t0)
+        out[name] = k * per_gpu / best / 1e9
+    del host, devs
+    return out
+
+
 def ncu_traffic(direction, kernel):
     """dram bytes per launch of the dominant kernel from the committed ncu capture
     (profiles/ncu_summary.json), or None when that kernel was not captured."""
@@ -566,12 +608,27 @@ def main():
                                "term, SURVEY 8(d)); HBM (MEASURED_PEAKS hbm_gbs 6554 GB/s) is not the "
                                "bound of a host<->device copy"}
 
-    # path-level roofline R(k) = sum of the used links' solo PCIe rates (DRAM term reported)
-    R_step = nbytes_step / 2 / (R_h2d * 1e9) + nbytes_step / 2 / (R_d2h * 1e9)
-    path_roof = {"R_h2d_gbps": round(R_h2d, 2), "R_d2h_gbps": round(R_d2h, 2),
-                 "frac_h2d": round(h2d_gbps / R_h2d, 4), "frac_d2h": round(d2h_gbps / R_d2h, 4),
+    # path-level roofline: R(k) = min(sum of the used links' solo PCIe rates,
+    # host DRAM), DRAM taken as the lower bound max(all-core CPU read, R_conc(k)); R_conc(k)
+    # (k plain copies at once) reported beside it. NVLink ingress (900 GB/s per direction)
+    # does not bind at <= 8 links of ~57 GB/s.
+    gset = sorted(set(path_gpus))
+    conc = conc_rate(torch, gset)
+    dram = dram_read_rate(torch)
+    terms = {"h2d": {"pcie_sum": R_h2d, "dram_lb": max(dram, conc["h2d"])},
+             "d2h": {"pcie_sum": R_d2h, "dram_lb": max(dram, conc["d2h"])}}
+    Rh, Rd = min(terms["h2d"].values()), min(terms["d2h"].values())
+    R_step = nbytes_step / 2 / (Rh * 1e9) + nbytes_step / 2 / (Rd * 1e9)
+    path_roof = {"R_h2d_gbps": round(Rh, 2), "R_d2h_gbps": round(Rd, 2),
+                 "binding_h2d": min(terms["h2d"], key=terms["h2d"].get),
+                 "binding_d2h": min(terms["d2h"], key=terms["d2h"].get),
+                 "frac_h2d": round(h2d_gbps / Rh, 4), "frac_d2h": round(d2h_gbps / Rd, 4),
                  "frac_step": round(value / (nbytes_step / R_step / 1e9), 4),
-                 "pcie_solo": {str(g): {k2: round(v, 2) for k2, v in pcie[g].items()} for g in path_gpus}}
+                 "R_conc": {k2: round(v, 2) for k2, v in conc.items()},
+                 "cpu_dram_read_gbps": round(dram, 2),
+                 "pcie_solo": {str(g): {k2: round(v, 2) for k2, v in pcie[g].items()} for g in path_gpus},
+                 "note": "DRAM term is a lower bound (CPU threads in a VM may not saturate DRAM); when it "
+                         "binds, R is a lower bound and the fraction an upper bound"}
 
     # ---- e2e through the public API: wall clock, host issue + copies + sync every step
     t0 = time.perf_counter()
