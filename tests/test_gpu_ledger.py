@@ -2,7 +2,6 @@
 flight have queued on each link. The plan with a pending call must equal the oracle's
 earliest-finish plan with that backlog as input, and return to the unloaded plan once the
 pending call has completed."""
-import numpy as np
 import pytest
 
 from gpu_util import configure, pinned
