@@ -243,6 +243,13 @@ int mma_copy_claim_segments(const mma_segment_t* segs, size_t nsegs, size_t clai
                             uint64_t* cursor, uint64_t* counts, int path, int device,
                             mma_stream_t stream);
 
+/* Timeline tracing: while active, every DMA and kernel the engine enqueues is bracketed by
+ * CUDA events on its stream; mma_trace_end synchronises, writes the spans as a Chrome trace
+ * JSON (one row per GPU and engine stream) to json_path (NULL: discard) and reports their
+ * number. max_spans = 0 -> 100000. */
+int mma_trace_begin(size_t max_spans);
+int mma_trace_end(const char* json_path, size_t* nspans);
+
 int mma_get_stats(int device, mma_stats_t* out);
 int mma_reset_stats(int device);
 int mma_get_last_error(void);

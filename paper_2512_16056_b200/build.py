@@ -21,6 +21,7 @@ SOURCES = [
     CSRC / "api.cpp",
     CSRC / "tune.cpp",
     CSRC / "mp.cpp",
+    CSRC / "trace.cpp",
     CSRC / "planner.cpp",
     CSRC / "hostmem.cpp",
     CSRC / "kernels" / "relay.cu",

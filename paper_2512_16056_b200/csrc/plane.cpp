@@ -466,6 +466,7 @@ int run_job(Job& j)
         if (small || mode0 == MMA_HOP_CE) {
             DmaBatch b;
             j.pieces(0, j.B, [&](const Piece& x) { b.add(x.dst, x.src, x.len); });
+            TSpan ts(j.user_dev, j.user, "DMA native (fallback)", 0, -1, j.B);
             CK((cudaError_t)b.issue(kind, j.user));
             t.stats.path_bytes[j.dir][0] += j.B;
             t.stats.path_chunks[j.dir][0] += 1;
@@ -671,6 +672,7 @@ int run_job(Job& j)
             a.log = log;
             const unsigned grid = (unsigned)std::min<uint64_t>(n_log, (uint64_t)e.dev[g].sms * 4);
             KTimer kt(g, s, 3 | (j.dir << 4) | (p << 8));
+            TSpan ts(g, s, "zero-copy dynamic pull", p, -1, 0);
             CK(launch_zc_dyn(a, grid, s));
             t.stats.kernels++;
         }
@@ -703,6 +705,7 @@ int run_job(Job& j)
             const unsigned grid = (unsigned)std::min<uint64_t>(units, (uint64_t)e.dev[g].sms * 4);
             DeviceGuard dg(g);
             KTimer kt(g, s, 0 | (j.dir << 4) | (p << 8));
+            TSpan ts(g, s, relay ? "zero-copy one-hop relay kernel" : "zero-copy direct kernel", p, -1, bytes_p);
             CK(launch_zc(a, grid, s));
             t.stats.kernels++;
             continue;
@@ -721,6 +724,7 @@ int run_job(Job& j)
             j.extent(lists[p][b - 1], &o1, &l1);
             DmaBatch batch;
             j.pieces(o0, o1 + l1, [&](const Piece& x) { batch.add(x.dst, x.src, x.len); });
+            TSpan ts(g, s, "DMA direct", p, lists[p][a], o1 + l1 - o0);
             CK((cudaError_t)batch.issue(kind, s));
             if (log) CK(cudaMemsetAsync(log + lists[p][a], p, b - a, s));
             a = b;
@@ -786,6 +790,7 @@ int run_job(Job& j)
             CK((cudaError_t)use(s, kd));
             DeviceGuard dg(kd);
             KTimer kt(kd, s, (j.dir == MMA_H2D ? 1 : 2) | (j.dir << 4) | (0xff << 8));
+            TSpan ts(kd, s, j.dir == MMA_H2D ? "relay pull kernel" : "relay pack kernel", -1, -1, 0);
             CK(launch_relay(kv.second, j.dir == MMA_H2D, grids[kd], s));
             t.stats.kernels++;
         }
@@ -809,7 +814,10 @@ int run_job(Job& j)
                     if (g >= S && e.wait64((CUstream)hs, (CUdeviceptr)&r->credit[s], g - S + 1, CU_STREAM_WAIT_VALUE_GEQ) != CUDA_SUCCESS)
                         return cudaErrorUnknown;
                     j.pieces(off, off + len, [&](const Piece& x) { batch.add(slot + (x.v - off), x.src, x.len); });
-                    CK((cudaError_t)batch.issue(kind, hs));
+                    {
+                        TSpan ts(r->relay, hs, "DMA hop 1: host -> relay ring", p, (long long)lists[p][c], len);
+                        CK((cudaError_t)batch.issue(kind, hs));
+                    }
                     if ((long long)g != e.fault_drop_publish &&
                         e.write64((CUstream)hs, (CUdeviceptr)&r->seq[s], g + 1, 0) != CUDA_SUCCESS)
                         return cudaErrorUnknown;
@@ -817,7 +825,10 @@ int run_job(Job& j)
                     if (e.wait64((CUstream)hs, (CUdeviceptr)&r->seq[s], g + 1, CU_STREAM_WAIT_VALUE_GEQ) != CUDA_SUCCESS)
                         return cudaErrorUnknown;
                     j.pieces(off, off + len, [&](const Piece& x) { batch.add(x.dst, slot + (x.v - off), x.len); });
-                    CK((cudaError_t)batch.issue(kind, hs));
+                    {
+                        TSpan ts(r->relay, hs, "DMA hop 2: relay ring -> host", p, (long long)lists[p][c], len);
+                        CK((cudaError_t)batch.issue(kind, hs));
+                    }
                     if (e.write64((CUstream)hs, (CUdeviceptr)&r->credit[s], g + 1, 0) != CUDA_SUCCESS) return cudaErrorUnknown;
                 }
             }

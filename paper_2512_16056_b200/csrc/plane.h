@@ -254,6 +254,13 @@ struct KRec {
     cudaEvent_t a, b;
 };
 extern std::vector<KRec> g_kpending;
+// ---- trace.cpp: a span of stream work bracketed by CUDA events while a trace is active
+struct TSpan {
+    long long idx_ = -1;
+    TSpan(int dev, cudaStream_t s, const char* name, int path, long long chunk, uint64_t bytes);
+    ~TSpan();
+};
+bool trace_on();
 // ---- api.cpp
 int prepare_segments(int dir, const mma_segment_t* segs, size_t nsegs, int device, cudaStream_t stream, Job& j);
 

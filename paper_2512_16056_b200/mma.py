@@ -28,7 +28,7 @@ SYMBOLS = [
     "mma_verify_pattern", "mma_verify_segments", "mma_set_kernel_timing", "mma_kernel_times",
     "mma_tune_segments", "mma_get_segment_tuning", "mma_get_dynamic_counts", "mma_set_plan_mode",
     "mma_shared_host_alloc", "mma_shared_host_free", "mma_ipc_export", "mma_ipc_open", "mma_ipc_close",
-    "mma_copy_share_segments", "mma_copy_claim_segments",
+    "mma_copy_share_segments", "mma_copy_claim_segments", "mma_trace_begin", "mma_trace_end",
 ]
 
 
@@ -109,6 +109,8 @@ def lib():
         L.mma_get_segment_tuning.argtypes = [C.c_int, C.c_int, vp, vp, C.c_int, C.POINTER(C.c_int)]
         L.mma_get_dynamic_counts.argtypes = [C.c_int, vp, C.c_int, C.POINTER(C.c_int)]
         L.mma_set_plan_mode.argtypes = [C.c_int]
+        L.mma_trace_begin.argtypes = [sz]
+        L.mma_trace_end.argtypes = [C.c_char_p, C.POINTER(sz)]
         L.mma_shared_host_alloc.argtypes = [C.c_char_p, sz, C.c_int, C.POINTER(vp)]
         L.mma_shared_host_free.argtypes = [vp, C.c_char_p]
         L.mma_ipc_export.argtypes = [vp, vp, C.POINTER(C.c_uint64)]
@@ -405,3 +407,13 @@ def copy_claim_segments(segs, nsegs: int, claim_bytes: int, cursor_ptr: int, cou
                         path: int, device: int, stream=None) -> None:
     _check(lib().mma_copy_claim_segments(segs, nsegs, claim_bytes, cursor_ptr, counts_ptr, path, device,
                                          _stream(stream, device)), "mma_copy_claim_segments")
+
+
+def trace_begin(max_spans: int = 0) -> None:
+    _check(lib().mma_trace_begin(max_spans), "mma_trace_begin")
+
+
+def trace_end(json_path: str | None) -> int:
+    n = C.c_size_t()
+    _check(lib().mma_trace_end(json_path.encode() if json_path else None, C.byref(n)), "mma_trace_end")
+    return n.value
