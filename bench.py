@@ -366,6 +366,36 @@ def conc_rate(torch, gpus, per_gpu=512 * MiB, reps=3):
     return out
 
 
+def timeline_summary(path):
+    """Per-GPU busy time and GPU concurrency of one traced step (engine Chrome trace)."""
+    ev = json.load(open(path))["traceEvents"]
+    if not ev:
+        return None
+    per_gpu = {}
+    for e in ev:
+        per_gpu.setdefault(e["pid"], []).append((e["ts"], e["ts"] + e["dur"]))
+    t0 = min(s for v in per_gpu.values() for s, _ in v)
+    t1 = max(e for v in per_gpu.values() for _, e in v)
+    pts = sorted({x for v in per_gpu.values() for s in v for x in s})
+    weighted = 0.0
+    for a, b in zip(pts, pts[1:]):
+        m = (a + b) / 2
+        weighted += (b - a) * sum(any(s <= m < e for s, e in v) for v in per_gpu.values())
+    busy = {g: round(sum(e - s for s, e in _merge(v)), 1) for g, v in sorted(per_gpu.items())}
+    return {"span_us": round(t1 - t0, 1), "busy_us": busy, "mean_gpus_busy": round(weighted / max(t1 - t0, 1e-9), 2),
+            "spans": len(ev)}
+
+
+def _merge(iv):
+    out = []
+    for s, e in sorted(iv):
+        if out and s <= out[-1][1]:
+            out[-1][1] = max(out[-1][1], e)
+        else:
+            out.append([s, e])
+    return out
+
+
 def ncu_traffic(direction, kernel):
     """dram bytes per launch of the dominant kernel from the committed ncu capture
     (profiles/ncu_summary.json), or None when that kernel was not captured."""
@@ -629,6 +659,22 @@ def main():
                  "note": "DRAM term is a lower bound (CPU threads in a VM may not saturate DRAM); when it "
                          "binds, R is a lower bound and the fraction an upper bound"}
 
+    # ---- one traced step (engine timeline): which GPUs carried the step, and how
+    # concurrently (outside the timed region)
+    timeline = None
+    try:
+        Path("gpurun_out").mkdir(exist_ok=True)
+        tpath = f"gpurun_out/bench_trace_n{args.gpus}.json"
+        mma.trace_begin()
+        run_step(mma, w, 0, stream)
+        stream.synchronize()
+        mma.trace_end(tpath)
+        timeline = timeline_summary(tpath)
+        if timeline:
+            timeline["file"] = tpath
+    except Exception as ex:  # noqa: BLE001 - evidence only
+        timeline = {"error": str(ex)}
+
     # ---- e2e through the public API: wall clock, host issue + copies + sync every step
     t0 = time.perf_counter()
     for _ in range(args.steps):
@@ -687,6 +733,7 @@ def main():
         "native": native,
         "cpu_baseline": cpu,
         "e2e": e2e,
+        "timeline": timeline,
         "gpu_launches": int(st["kernels"]),
         "kernel_kinds": kinds,
         "clocks": clk,
