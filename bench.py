@@ -676,6 +676,8 @@ def main():
         timeline = {"error": str(ex)}
 
     # ---- e2e through the public API: wall clock, host issue + copies + sync every step
+    run_step(mma, w, 0, stream)                 # one untimed synchronous step first
+    stream.synchronize()
     t0 = time.perf_counter()
     for _ in range(args.steps):
         run_step(mma, w, 0, stream)
