@@ -1,0 +1,65 @@
+"""CPU checks of bench.py's host-side helpers (the round-end runs depend on them): the
+clock sampler's parser, the trace summary, the oracle CPU baseline and the JSON line of the
+reference arm."""
+import json
+import subprocess
+import sys
+from pathlib import Path
+
+import bench
+
+ROOT = Path(__file__).resolve().parents[1]
+
+
+class _FakeProc:
+    def __init__(self, out):
+        self.out = out
+
+    def terminate(self):
+        pass
+
+    def communicate(self, timeout=None):
+        return self.out, ""
+
+
+def test_clock_parser():
+    c = bench.Clocks([0, 1])
+    c.p = _FakeProc("0, 1965, 1965, 250.1, 0x0, Not Active, Not Active, Not Active, Not Active\n"
+                    "1, 1950, 1965, 260.0, 0x4, Not Active, Not Active, Not Active, Active\n"
+                    "garbage line\n")
+    r = c.stop()
+    assert r["sm_mhz"] == 1957.5 and r["sm_max_mhz"] == 1965.0 and r["samples"] == 2
+    assert r["reasons"] == ["sw_power_cap"]
+    c2 = bench.Clocks([0])
+    c2.p = None
+    assert c2.stop()["sm_mhz"] is None
+
+
+def test_timeline_summary(tmp_path):
+    ev = [{"name": "a", "ph": "X", "pid": "GPU 0", "tid": "x", "ts": 0.0, "dur": 10.0, "args": {}},
+          {"name": "b", "ph": "X", "pid": "GPU 0", "tid": "y", "ts": 5.0, "dur": 10.0, "args": {}},
+          {"name": "c", "ph": "X", "pid": "GPU 1", "tid": "x", "ts": 0.0, "dur": 20.0, "args": {}}]
+    p = tmp_path / "t.json"
+    p.write_text(json.dumps({"traceEvents": ev}))
+    s = bench.timeline_summary(str(p))
+    assert s["span_us"] == 20.0 and s["busy_us"] == {"GPU 0": 15.0, "GPU 1": 20.0}
+    assert s["mean_gpus_busy"] == 1.75 and s["spans"] == 3
+    p.write_text(json.dumps({"traceEvents": []}))
+    assert bench.timeline_summary(str(p)) is None
+
+
+def test_oracle_sample_bounded():
+    g, threads, desc, nbytes, dt = bench.oracle_sample(2, nsegs_sample=256, reps=2)
+    assert g > 0 and threads == 3 and nbytes == 2 * 256 * 32768 and dt > 0
+    assert "256 of 131072" in desc
+
+
+def test_reference_arm_line():
+    p = subprocess.run([sys.executable, str(ROOT / "bench.py"), "--impl", "reference", "--steps", "1",
+                        "--warmup", "0"], capture_output=True, text=True, timeout=300, cwd=str(ROOT))
+    assert p.returncode == 0, p.stderr[-2000:]
+    j = json.loads(p.stdout.strip().splitlines()[-1])
+    for key in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better",
+                "scaling", "vs_baseline", "dtype", "data", "config", "cpu_baseline", "e2e"):
+        assert key in j, key
+    assert j["impl"] == "reference" and j["metric"] == bench.METRIC
