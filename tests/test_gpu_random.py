@@ -28,13 +28,14 @@ def mma():
 
 
 def test_random_transfers(mma, orc):
-    rng = np.random.default_rng(20261017)
+    import os
+    rng = np.random.default_rng(int(os.environ.get("MMA_RANDOM_SEED", "20261017")))
     pool_h = torch.empty(48 * MiB, dtype=torch.uint8).pin_memory()
     mma_inputs.fill_pattern(pool_h.numpy(), 123)
     pool_d = torch.empty(48 * MiB, dtype=torch.uint8, device="cuda")
     pool_d.copy_(pool_h)
     hn = pool_h.numpy()
-    for case in range(200):
+    for case in range(int(os.environ.get("MMA_RANDOM_CASES", "200"))):
         lb = int(rng.integers(0, 4))
         P = 1 + lb
         C = int(rng.choice([4 * KiB, 64 * KiB, 256 * KiB, MiB, 3 * MiB]))
