@@ -30,6 +30,15 @@ ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
 
 METRIC = "H2D/D2H GB/s per target GPU vs path count (1/2/4/8) and % of roofline"
+def _hbm_peak():
+    p = ROOT / "MEASURED_PEAKS.json"
+    try:
+        return float(json.loads(p.read_text())["hbm_gbs"]), "MEASURED_PEAKS.json hbm_gbs (measured)"
+    except (OSError, ValueError, KeyError):
+        return 6650.0, "B200_PROFILING.md fallback"
+
+
+HBM_PEAK = _hbm_peak()
 KNAMES = {0: "zc_copy_kernel", 1: "relay_pull_kernel", 2: "relay_pack_kernel", 3: "zc_dyn_kernel"}
 MiB, GiB = 1 << 20, 1 << 30
 SEED = 0x4D4D41 + 3
@@ -634,8 +643,10 @@ def main():
                 "share_of_step": round(sum(ms_list) / ms_total, 4),
                 "peak_source": f"measured in this run: solo native cudaMemcpyAsync 1 GiB {dname.upper()} "
                                "over the PCIe link(s) this kernel's bytes cross (the roofline's PCIe "
-                               "term, SURVEY 8(d)); HBM (MEASURED_PEAKS hbm_gbs 6554 GB/s) is not the "
-                               "bound of a host<->device copy"}
+                               "term, SURVEY 8(d)); HBM is not the bound of a host<->device copy",
+                "hbm_reference": {"peak_gbps": HBM_PEAK[0], "source": HBM_PEAK[1],
+                                  "frac": round(achieved / HBM_PEAK[0], 5) if HBM_PEAK[0] else None,
+                                  "note": "the same bytes against HBM copy bandwidth, for context"}}
 
     # path-level roofline: R(k) = min(sum of the used links' solo PCIe rates,
     # host DRAM), DRAM taken as the lower bound max(all-core CPU read, R_conc(k)); R_conc(k)
