@@ -57,6 +57,9 @@ def parse():
     ap.add_argument("--hop", type=int, default=0, help="0 auto, 1 copy engine, 2 SM zero-copy")
     ap.add_argument("--no-verify", action="store_true")
     ap.add_argument("--quick", action="store_true", help="skip baselines (profiling runs)")
+    ap.add_argument("--mp", action="store_true",
+                    help="multi-process mode (NEXT-4): under torchrun every rank moves its own share of "
+                         "the KV fetch/offload on its own GPU (CUDA IPC + shared host memory)")
     ap.add_argument("--loopback", type=int, default=0,
                     help="diagnostic: add loopback relay paths through GPU 0 (exercises the multi-path "
                          "code of the bench on one GPU; the paths share one link)")
@@ -419,6 +422,124 @@ def ncu_traffic(direction, kernel):
 
 # ----------------------------------------------------------------------- main ---
 
+def run_mp(args, dist, torch, mma):
+    """--mp: one process per GPU. Rank 0 owns the target cache (GPU 0) and
+    exports it by CUDA IPC; the host pool is named shared memory pinned by every rank; each
+    rank moves its share of every fetch and offload with the zero-copy kernel on its own GPU
+    -- the chunks the common contiguous plan gives its path, or the units it claims from a
+    cursor in GPU 0's memory (dynamic), whichever measured faster. Each phase is bracketed by
+    gloo barriers; a phase's time is the max over ranks of the rank's own CUDA-event time."""
+    import numpy as np
+    from mma_inputs import workloads as W
+    rank, world = dist.rank, dist.world
+    ngpu = torch.cuda.device_count()
+    dev = dist.local if ngpu > 1 else 0
+    torch.cuda.set_device(dev)
+    shape = W.KVShape() if args.tokens == 32768 else W.scaled_kv(args.tokens)
+    ho, do, sb, hpool, dbytes = W.kv_segments(shape, SEED)
+    lens = np.full(len(ho), sb, dtype=np.int64)
+    Bytes = int(lens.sum())
+    name = f"bench_{os.environ.get('MASTER_PORT', '0')}"
+    cfg = mma.default_config()
+    cfg.debug_log = 0
+    mma.init(cfg)
+    if rank == 0:
+        pool = mma.shared_host_alloc(name, hpool, True)
+        pt = torch.from_numpy(mma.host_array(pool, hpool))
+        tmp = torch.empty(min(hpool, GiB), dtype=torch.uint8, device="cuda")
+        for a in range(0, hpool, tmp.numel()):
+            n = min(tmp.numel(), hpool - a)
+            mma.fill_pattern(tmp, n, SEED, a)
+            pt[a:a + n].copy_(tmp[:n])
+        del tmp
+        cache = torch.empty(dbytes, dtype=torch.uint8, device="cuda")
+        ctr = torch.zeros(32, dtype=torch.int64, device="cuda")
+        obj = [(mma.ipc_export(cache), mma.ipc_export(ctr))]
+    else:
+        obj = [None]
+    dist.barrier()
+    dist.pg.broadcast_object_list(obj, src=0)
+    (hd, od), (hc, oc) = obj[0]
+    if rank == 0:
+        cptr, kptr = cache.data_ptr(), ctr.data_ptr()
+    else:
+        pool = mma.shared_host_alloc(name, hpool, False)
+        cptr, kptr = mma.ipc_open(hd, od, dev), mma.ipc_open(hc, oc, dev)
+    fetch = mma.make_segments(pool + ho, cptr + do, lens)
+    offload = mma.make_segments(cptr + do, pool + ho, lens)
+    C, claim = 8 * MiB, 256 << 10
+    rc, plan, _ = mma.plan_chunks([1] * world, [0] + [1] * (world - 1), Bytes, C, 0, 0)
+    s = torch.cuda.Stream()
+
+    def phase(segs, dynamic):
+        if dynamic and rank == 0:
+            ctr.zero_()
+            torch.cuda.synchronize()
+        dist.barrier()
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        a.record(s)
+        if dynamic:
+            mma.copy_claim_segments(*segs, claim, kptr, kptr + 8, rank, dev, stream=s)
+        else:
+            mma.copy_share_segments(*segs, C, plan, rank, dev, stream=s)
+        b.record(s)
+        b.synchronize()
+        return dist.max(a.elapsed_time(b))
+
+    def step(dynamic):
+        return phase(fetch, dynamic) + phase(offload, dynamic)
+
+    for _ in range(args.warmup):
+        step(False)
+    t_plan = statistics.median(step(False) for _ in range(2))
+    t_dyn = statistics.median(step(True) for _ in range(2))
+    dynamic = t_dyn < t_plan
+    verify = None
+    if rank == 0:
+        cache.zero_()
+        torch.cuda.synchronize()
+    phase(fetch, dynamic)
+    if rank == 0:
+        cnt = torch.zeros(1, dtype=torch.int64, device="cuda")
+        mma.verify_segments(cache.data_ptr() + do, ho, lens, SEED, cnt)
+        torch.cuda.synchronize()
+        verify = {"mismatched_bytes": int(cnt.item()), "checked_bytes": Bytes, "on": "device (C4)"}
+    mma.set_kernel_timing(True)
+    times = [step(dynamic) for _ in range(args.steps)]
+    kt = mma.kernel_times()
+    mma.set_kernel_timing(False)
+    ms_step = statistics.mean(times)
+    value = 2 * Bytes / (ms_step * 1e-3) / 1e9
+    err = mma.get_last_error()
+    dist.barrier()
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": round(value, 3), "unit": "GB/s", "n_gpus": args.gpus, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(ms_step, 3), "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
+            "config": {"workload": "prefix-cache KV fetch + offload (BASELINE config 3), multi-process mode",
+                       "paths": world, "parallelism": "one process per GPU; rank r moves path r's share on "
+                       "its own GPU (CUDA IPC destination, shared pinned host pool); phase time = max over ranks",
+                       "plan": {"contiguous_ms": round(t_plan, 3), "dynamic_ms": round(t_dyn, 3),
+                                "chosen": "dynamic" if dynamic else "contiguous"},
+                       "gpus_visible_per_rank": ngpu},
+            "gpu_launches": len(kt), "verify": verify, "engine_error": err,
+            "e2e": None, "roofline": None, "cpu_baseline": None,
+            "note": "rank-0 line of the multi-process mode; the default (single-process) bench carries "
+                    "roofline, e2e and cpu_baseline",
+        }
+        print(json.dumps(line), flush=True)
+    dist.barrier()
+    if rank != 0:
+        mma.ipc_close(cptr)
+        mma.ipc_close(kptr)
+        mma.shared_host_free(pool)
+    dist.barrier()
+    if rank == 0:
+        mma.shared_host_free(pool, name)
+
+
 def main():
     args = parse()
     dist = Dist()
@@ -428,6 +549,11 @@ def main():
         return
     import torch
     import paper_2512_16056_b200 as mma
+
+    if args.mp and dist.world > 1:
+        run_mp(args, dist, torch, mma)
+        dist.close()
+        return
 
     if dist.rank != 0:
         # ranks > 0: no GPU work of their own; their GPUs serve as rank 0's relay paths

@@ -421,6 +421,7 @@ int mma_kernel_times(float* ms, int* kinds, size_t cap, size_t* n)
 {
     if (!n) return cudaErrorInvalidValue;
     std::lock_guard<std::mutex> g(E().mu);
+    std::lock_guard<std::mutex> gk(g_kmu);
     size_t k = 0;
     int rc = cudaSuccess;
     for (auto& r : g_kpending) {

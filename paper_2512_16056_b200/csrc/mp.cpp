@@ -190,8 +190,10 @@ int mma_copy_share_segments(const mma_segment_t* segs, size_t nsegs, size_t chun
     VStreamArg v;
     void* dtab = nullptr;
     CK(vstream_from(segs, nsegs, chunk_bytes, s, v, &dtab));
-    if ((v.B + chunk_bytes - 1) / chunk_bytes != nchunks && !(nchunks == 1 && v.B > 0))
+    if ((v.B + chunk_bytes - 1) / chunk_bytes != nchunks && !(nchunks == 1 && v.B > 0)) {
+        if (dtab) cudaFreeAsync(dtab, s);
         return cudaErrorInvalidValue;
+    }
     if (nchunks == 1) v.C = v.B;             // a one-piece (fallback) plan
     std::vector<uint32_t> mine;
     for (size_t i = 0; i < nchunks; i++)
@@ -209,6 +211,7 @@ int mma_copy_share_segments(const mma_segment_t* segs, size_t nsegs, size_t chun
             a.path = (uint32_t)path;
             const uint64_t upc = (v.C + e.unit_bytes - 1) / e.unit_bytes;
             const unsigned grid = (unsigned)std::min<uint64_t>(mine.size() * upc, (uint64_t)e.dev[device].sms * 4);
+            KTimer kt(device, s, 0 | (path << 8));
             rc = launch_zc(a, grid, s);
             cudaFreeAsync(dlist, s);
         }
@@ -241,7 +244,11 @@ int mma_copy_claim_segments(const mma_segment_t* segs, size_t nsegs, size_t clai
     a.counts = (unsigned long long*)counts;
     a.path = (uint32_t)path;
     const unsigned grid = (unsigned)std::min<uint64_t>(a.nchunks, (uint64_t)e.dev[device].sms * 4);
-    int rc = a.nchunks ? launch_zc_dyn(a, grid, s) : cudaSuccess;
+    int rc = cudaSuccess;
+    if (a.nchunks) {
+        KTimer kt(device, s, 3 | (path << 8));
+        rc = launch_zc_dyn(a, grid, s);
+    }
     if (dtab) cudaFreeAsync(dtab, s);
     return rc;
 }

@@ -315,29 +315,7 @@ static int scratch_host(Scratch& sc, size_t bytes, void** out)
 // the kernel is launched on (mma_set_kernel_timing / mma_kernel_times).
 std::vector<KRec> g_kpending;
 bool g_ktime = false;
-
-struct KTimer {
-    bool on = false;
-    KRec r{};
-    cudaStream_t s = nullptr;
-    KTimer(int dev, cudaStream_t st, int kind)
-    {
-        if (!g_ktime) return;
-        DeviceGuard g(dev);
-        if (cudaEventCreate(&r.a) != cudaSuccess || cudaEventCreate(&r.b) != cudaSuccess) return;
-        r.dev = dev;
-        r.kind = kind | (dev << 16);
-        s = st;
-        on = cudaEventRecord(r.a, s) == cudaSuccess;
-    }
-    ~KTimer()
-    {
-        if (!on) return;
-        DeviceGuard g(r.dev);
-        cudaEventRecord(r.b, s);
-        g_kpending.push_back(r);
-    }
-};
+std::mutex g_kmu;
 
 static int resolve_mode(const Job& j, int mode)
 {

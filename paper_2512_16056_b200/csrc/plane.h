@@ -254,6 +254,32 @@ struct KRec {
     cudaEvent_t a, b;
 };
 extern std::vector<KRec> g_kpending;
+extern std::mutex g_kmu;
+// CUDA events around one kernel launch on its stream while kernel timing is on
+struct KTimer {
+    bool on = false;
+    KRec r{};
+    cudaStream_t s = nullptr;
+    KTimer(int dev, cudaStream_t st, int kind)
+    {
+        if (!g_ktime) return;
+        DeviceGuard g(dev);
+        if (cudaEventCreate(&r.a) != cudaSuccess || cudaEventCreate(&r.b) != cudaSuccess) return;
+        r.dev = dev;
+        r.kind = kind | (dev << 16);
+        s = st;
+        on = cudaEventRecord(r.a, s) == cudaSuccess;
+    }
+    ~KTimer()
+    {
+        if (!on) return;
+        DeviceGuard g(r.dev);
+        cudaEventRecord(r.b, s);
+        std::lock_guard<std::mutex> lk(g_kmu);
+        g_kpending.push_back(r);
+    }
+};
+
 // ---- trace.cpp: a span of stream work bracketed by CUDA events while a trace is active
 struct TSpan {
     long long idx_ = -1;
