@@ -35,3 +35,17 @@ def test_explore_rejects_out_of_range(orc):
     assert orc.ring_explore(9, 2)[0] == orc.EINVAL
     assert orc.ring_explore(3, 0)[0] == orc.EINVAL
     assert orc.ring_explore(3, 5)[0] == orc.EINVAL
+
+
+def test_oracle_cli():
+    import json
+    import subprocess
+    import sys
+    run = lambda *a: json.loads(subprocess.run([sys.executable, "-m", "oracle", *a], capture_output=True,
+                                               text=True, check=True).stdout)
+    p = run("plan", "--bw", "50,25", "--bytes", "6", "--chunk", "1", "--mode", "interleaved", "--relay-only")
+    assert p["path"] == [0, 0, 1, 0, 0, 1] and p["counts"] == [4, 2]
+    m = run("move", "--bw", "3,1", "--bytes", "1MiB", "--chunk", "64KiB", "--slots", "2", "--mode", "interleaved")
+    assert m["bytes_equal"] and m["exactly_once"] and m["invariant_violations"] == 0
+    r = run("ring", "--n", "4", "--slots", "2", "--fault", "publish-early")
+    assert r["violations"] > 0
