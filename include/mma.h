@@ -173,6 +173,13 @@ int mma_calibrate(int device, mma_dir_t dir, size_t bytes);
  * only; mma_set_bandwidth / mma_set_path_modes clear it. Synchronous. */
 int mma_tune_segments(const mma_segment_t* segs, size_t nsegs, int device, mma_dir_t dir,
                       mma_stream_t stream, int reps);
+/* Persist / restore what calibration measured (bandwidth and mode per path, contiguous and
+ * scattered), one text line per (device, direction, path). Loading applies a line only
+ * where the current path set has the same GPU and kind at that index; *applied receives the
+ * number of paths updated. MMA_CALIB=<file> loads it at init. */
+int mma_save_calibration(const char* path);
+int mma_load_calibration(const char* path, int* applied);
+
 /* What mma_tune_segments chose, index-aligned with mma_get_paths (0 / -1 = not tuned). */
 int mma_get_segment_tuning(int device, mma_dir_t dir, uint32_t* mbps, int* modes, int cap,
                            int* npaths);

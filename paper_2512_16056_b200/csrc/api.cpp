@@ -146,6 +146,39 @@ static int copy_segments(int dir, const mma_segment_t* segs, size_t nsegs, int d
     return run_job(j);
 }
 
+// (engine mutex held)
+int load_calibration_locked(const char* path, int* applied)
+{
+    if (!path) return cudaErrorInvalidValue;
+    Engine& e = E();
+    FILE* f = fopen(path, "r");
+    if (!f) return cudaErrorInvalidValue;
+    char line[256];
+    int n = 0;
+    while (fgets(line, sizeof line, f)) {
+        if (line[0] == '#') continue;
+        int d, dir, gpu, kind, mode, seg_mode;
+        size_t p;
+        unsigned mbps, seg_mbps;
+        if (sscanf(line, "%d %d %zu %d %d %u %d %u %d", &d, &dir, &p, &gpu, &kind, &mbps, &mode, &seg_mbps, &seg_mode) != 9)
+            continue;
+        if (d < 0 || d >= e.ndev || dir < 0 || dir > 1 || mode < MMA_HOP_AUTO || mode > MMA_HOP_ZC ||
+            seg_mode < -1 || seg_mode > MMA_HOP_ZC)
+            continue;
+        make_paths(d);
+        auto& ps = e.tgt[d].paths[dir];
+        if (p >= ps.size() || ps[p].gpu != gpu || ps[p].kind != kind) continue;
+        ps[p].mbps = mbps ? mbps : ps[p].mbps;
+        ps[p].mode = mode;
+        ps[p].seg_mbps = seg_mbps;
+        ps[p].seg_mode = seg_mode;
+        n++;
+    }
+    fclose(f);
+    if (applied) *applied = n;
+    return cudaSuccess;
+}
+
 }  // namespace mma
 
 // ====================================================================== C ABI (C7) ===
@@ -264,6 +297,39 @@ int mma_set_plan_mode(int mode)
     std::lock_guard<std::mutex> g(E().mu);
     E().cfg.plan_mode = mode;
     return cudaSuccess;
+}
+
+// Calibration file (SURVEY §5 "checkpoint / resume": only the calibration persists): one
+// line per (device, direction, path): device dir path gpu kind mbps mode seg_mbps seg_mode.
+// Loading applies a line only where the current path set has the same (gpu, kind) at that
+// index, so a file from another topology is ignored path by path, never misapplied.
+int mma_save_calibration(const char* path)
+{
+    CK((cudaError_t)ensure_init());
+    if (!path) return cudaErrorInvalidValue;
+    Engine& e = E();
+    std::lock_guard<std::mutex> g(e.mu);
+    FILE* f = fopen(path, "w");
+    if (!f) return cudaErrorInvalidValue;
+    fprintf(f, "# mma calibration v1: device dir path gpu kind mbps mode seg_mbps seg_mode\n");
+    for (int d = 0; d < e.ndev; d++) {
+        make_paths(d);
+        for (int dir = 0; dir < 2; dir++) {
+            const auto& ps = e.tgt[d].paths[dir];
+            for (size_t p = 0; p < ps.size(); p++)
+                fprintf(f, "%d %d %zu %d %d %u %d %u %d\n", d, dir, p, ps[p].gpu, ps[p].kind, ps[p].mbps,
+                        ps[p].mode, ps[p].seg_mbps, ps[p].seg_mode);
+        }
+    }
+    fclose(f);
+    return cudaSuccess;
+}
+
+int mma_load_calibration(const char* path, int* applied)
+{
+    CK((cudaError_t)ensure_init());
+    std::lock_guard<std::mutex> g(E().mu);
+    return load_calibration_locked(path, applied);
 }
 
 int mma_get_segment_tuning(int device, mma_dir_t dir, uint32_t* mbps, int* modes, int cap, int* npaths)

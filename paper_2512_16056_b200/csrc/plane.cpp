@@ -169,6 +169,7 @@ int do_init(const mma_config_t* cfg)
     e.cfg = c;
     for (int d = 0; d < e.ndev; d++) e.tgt[d].paths_made = false;   // re-derive path sets
     e.inited = true;
+    if (const char* cal = getenv("MMA_CALIB")) load_calibration_locked(cal, nullptr);
     return cudaSuccess;
 }
 

@@ -288,6 +288,7 @@ struct TSpan {
 };
 bool trace_on();
 // ---- api.cpp
+int load_calibration_locked(const char* path, int* applied);
 int prepare_segments(int dir, const mma_segment_t* segs, size_t nsegs, int device, cudaStream_t stream, Job& j);
 
 }  // namespace mma

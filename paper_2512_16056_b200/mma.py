@@ -29,6 +29,7 @@ SYMBOLS = [
     "mma_tune_segments", "mma_get_segment_tuning", "mma_get_dynamic_counts", "mma_set_plan_mode",
     "mma_shared_host_alloc", "mma_shared_host_free", "mma_ipc_export", "mma_ipc_open", "mma_ipc_close",
     "mma_copy_share_segments", "mma_copy_claim_segments", "mma_trace_begin", "mma_trace_end",
+    "mma_save_calibration", "mma_load_calibration",
 ]
 
 
@@ -110,6 +111,8 @@ def lib():
         L.mma_get_dynamic_counts.argtypes = [C.c_int, vp, C.c_int, C.POINTER(C.c_int)]
         L.mma_set_plan_mode.argtypes = [C.c_int]
         L.mma_trace_begin.argtypes = [sz]
+        L.mma_save_calibration.argtypes = [C.c_char_p]
+        L.mma_load_calibration.argtypes = [C.c_char_p, C.POINTER(C.c_int)]
         L.mma_trace_end.argtypes = [C.c_char_p, C.POINTER(sz)]
         L.mma_shared_host_alloc.argtypes = [C.c_char_p, sz, C.c_int, C.POINTER(vp)]
         L.mma_shared_host_free.argtypes = [vp, C.c_char_p]
@@ -416,4 +419,14 @@ def trace_begin(max_spans: int = 0) -> None:
 def trace_end(json_path: str | None) -> int:
     n = C.c_size_t()
     _check(lib().mma_trace_end(json_path.encode() if json_path else None, C.byref(n)), "mma_trace_end")
+    return n.value
+
+
+def save_calibration(path: str) -> None:
+    _check(lib().mma_save_calibration(path.encode()), "mma_save_calibration")
+
+
+def load_calibration(path: str) -> int:
+    n = C.c_int()
+    _check(lib().mma_load_calibration(path.encode(), C.byref(n)), "mma_load_calibration")
     return n.value

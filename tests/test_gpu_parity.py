@@ -249,3 +249,21 @@ def test_degenerate_segment_tables(mma):
     assert dev[0].item() == host[0].item()
     with pytest.raises(mma.MMAError):
         mma.memcpy_h2d_segments(segs, n, 7, stream=torch.cuda.current_stream())  # no such device
+
+
+def test_calibration_file_roundtrip(mma, tmp_path):
+    """Only the calibration persists: bandwidth and mode per path survive a
+    save / finalize / load cycle; lines for another path set are ignored."""
+    configure(mma, loopback=2, chunk=MiB, debug=0)
+    mma.set_bandwidth(0, mma.H2D, [7000, 6000, 5000])
+    mma.set_path_modes(0, mma.D2H, [2, 1, 2])
+    f = tmp_path / "cal.txt"
+    mma.save_calibration(str(f))
+    before = (mma.get_paths(0, mma.H2D), mma.get_paths(0, mma.D2H))
+    mma.finalize()
+    configure(mma, loopback=2, chunk=MiB, debug=0)
+    assert mma.get_paths(0, mma.H2D)[0]["mbps"] != 7000
+    assert mma.load_calibration(str(f)) == 6
+    assert (mma.get_paths(0, mma.H2D), mma.get_paths(0, mma.D2H)) == before
+    configure(mma, loopback=1, chunk=MiB, debug=0)      # a different path set
+    assert mma.load_calibration(str(f)) == 4            # paths 0 and 1 still match, path 2 is gone
