@@ -209,6 +209,15 @@ int mma_get_dynamic_counts(int device, uint64_t* chunks, int cap, int* npaths);
 int mma_host_alloc(void** ptr, size_t bytes, unsigned flags);
 int mma_host_free(void* ptr);
 
+/* NUMA "spread" placement (C8): a buffer for a contiguous transfer of `bytes`
+ * to / from `device` whose byte range carried by each path of the current contiguous plan
+ * lives on the NUMA node of that path's GPU, so every link reads node-local memory (the
+ * paper's 6-path plateau came from the cross-socket link). Pinned, mapped, freed with
+ * mma_host_free. mma_host_page_node returns the node holding the page at ptr (-1 if
+ * unknown). */
+int mma_host_alloc_for(void** ptr, size_t bytes, int device, mma_dir_t dir);
+int mma_host_page_node(const void* ptr);
+
 /* Measurement: when on, every relay / zero-copy kernel launch is bracketed by CUDA events
  * on the stream it is launched on. mma_kernel_times synchronises on the recorded launches,
  * returns their durations (ms) and tags in launch order (up to cap; *n = number recorded)

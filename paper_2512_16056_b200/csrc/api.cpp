@@ -455,6 +455,51 @@ int mma_host_alloc(void** ptr, size_t bytes, unsigned flags)
 
 int mma_host_free(void* ptr) { return host_free(ptr); }
 
+// NUMA node of GPU d's PCIe device (sysfs), or -1 when the host does not expose one.
+static int gpu_numa_node(int d)
+{
+    char bdf[32] = {0};
+    if (cudaDeviceGetPCIBusId(bdf, sizeof bdf, d) != cudaSuccess) { cudaGetLastError(); return -1; }
+    for (char* c = bdf; *c; c++) *c = (char)tolower(*c);
+    char path[96];
+    snprintf(path, sizeof path, "/sys/bus/pci/devices/%s/numa_node", bdf);
+    FILE* f = fopen(path, "r");
+    if (!f) return -1;
+    int n = -1;
+    if (fscanf(f, "%d", &n) != 1) n = -1;
+    fclose(f);
+    return n;
+}
+
+int mma_host_alloc_for(void** ptr, size_t bytes, int device, mma_dir_t dir)
+{
+    CK((cudaError_t)ensure_init());
+    Engine& e = E();
+    if (device < 0 || device >= e.ndev) return cudaErrorInvalidDevice;
+    if (!ptr || (dir != MMA_H2D && dir != MMA_D2H)) return cudaErrorInvalidValue;
+    std::vector<uint64_t> ends;
+    std::vector<int> nodes;
+    {
+        std::lock_guard<std::mutex> g(e.mu);
+        make_paths(device);
+        const auto& ps = e.tgt[device].paths[dir];
+        std::vector<PlanPath> pp;
+        for (auto& p : ps) pp.push_back(PlanPath{p.kind == MMA_PATH_DIRECT, p.mbps, 0});
+        Plan plan;
+        const uint64_t C = e.cfg.chunk_bytes[dir];
+        if (make_plan(pp.data(), (int)pp.size(), bytes, C, 0, PLAN_CONTIGUOUS, plan)) return cudaErrorInvalidValue;
+        uint64_t end = 0;
+        for (size_t p = 0; p < ps.size(); p++) {   // contiguous plan: path p's range, in path order
+            end = std::min<uint64_t>(bytes, end + plan.count[p] * C);
+            ends.push_back(end);
+            nodes.push_back(gpu_numa_node(ps[p].gpu));
+        }
+    }
+    return host_alloc_ranges(ptr, bytes, ends.data(), nodes.data(), (int)ends.size());
+}
+
+int mma_host_page_node(const void* ptr) { return host_page_node(ptr); }
+
 int mma_get_stats(int device, mma_stats_t* out)
 {
     CK((cudaError_t)ensure_init());

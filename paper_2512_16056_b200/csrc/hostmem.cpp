@@ -11,6 +11,7 @@
 #include <sys/syscall.h>
 #include <unistd.h>
 
+#include <algorithm>
 #include <cstdio>
 #include <cstring>
 #include <map>
@@ -61,6 +62,42 @@ int host_alloc(void** ptr, size_t bytes, int numa_mode, int node0)
             mask[nd / 64] |= 1ul << (nd % 64);
         }
         syscall(SYS_mbind, p, len, mode, mask, 256ul, 0u);   // best effort
+    }
+    memset(p, 0, len);   // first touch places the pages
+    cudaError_t e = cudaHostRegister(p, len, cudaHostRegisterPortable | cudaHostRegisterMapped);
+    if (e != cudaSuccess) {
+        munmap(p, len);
+        return e;
+    }
+    std::lock_guard<std::mutex> g(g_mu);
+    g_allocs[p] = len;
+    *ptr = p;
+    return cudaSuccess;
+}
+
+// numa_mode 3 ("spread"): bind consecutive byte ranges to given nodes before first
+// touch -- range k = [end[k-1], end[k]) on node[k] (node < 0: default placement). Used for a
+// contiguous transfer whose plan gives path p one range, placed on the node of p's GPU.
+int host_alloc_ranges(void** ptr, size_t bytes, const uint64_t* range_end, const int* node, int nranges)
+{
+    if (!ptr || (nranges && (!range_end || !node))) return cudaErrorInvalidValue;
+    *ptr = nullptr;
+    if (bytes == 0) return cudaSuccess;
+    const size_t align = 2u << 20, page = 4096;
+    const size_t len = (bytes + align - 1) / align * align;
+    void* p = mmap(nullptr, len, PROT_READ | PROT_WRITE, MAP_PRIVATE | MAP_ANONYMOUS, -1, 0);
+    if (p == MAP_FAILED) return cudaErrorMemoryAllocation;
+    const int nodes = numa_nodes();
+    uint64_t a = 0;
+    for (int k = 0; k < nranges && nodes > 1; k++) {
+        const uint64_t b = std::min<uint64_t>(range_end[k], len);
+        const uint64_t pa = a / page * page, pb = (b + page - 1) / page * page;
+        if (node[k] >= 0 && node[k] < nodes && pb > pa) {
+            unsigned long mask[4] = {0, 0, 0, 0};
+            mask[node[k] / 64] |= 1ul << (node[k] % 64);
+            syscall(SYS_mbind, (char*)p + pa, pb - pa, kMpolBind, mask, 256ul, 0u);   // best effort
+        }
+        a = b;
     }
     memset(p, 0, len);   // first touch places the pages
     cudaError_t e = cudaHostRegister(p, len, cudaHostRegisterPortable | cudaHostRegisterMapped);

@@ -29,7 +29,7 @@ SYMBOLS = [
     "mma_tune_segments", "mma_get_segment_tuning", "mma_get_dynamic_counts", "mma_set_plan_mode",
     "mma_shared_host_alloc", "mma_shared_host_free", "mma_ipc_export", "mma_ipc_open", "mma_ipc_close",
     "mma_copy_share_segments", "mma_copy_claim_segments", "mma_trace_begin", "mma_trace_end",
-    "mma_save_calibration", "mma_load_calibration",
+    "mma_save_calibration", "mma_load_calibration", "mma_host_alloc_for", "mma_host_page_node",
 ]
 
 
@@ -112,6 +112,8 @@ def lib():
         L.mma_set_plan_mode.argtypes = [C.c_int]
         L.mma_trace_begin.argtypes = [sz]
         L.mma_save_calibration.argtypes = [C.c_char_p]
+        L.mma_host_alloc_for.argtypes = [C.POINTER(vp), sz, C.c_int, C.c_int]
+        L.mma_host_page_node.argtypes = [vp]
         L.mma_load_calibration.argtypes = [C.c_char_p, C.POINTER(C.c_int)]
         L.mma_trace_end.argtypes = [C.c_char_p, C.POINTER(sz)]
         L.mma_shared_host_alloc.argtypes = [C.c_char_p, sz, C.c_int, C.POINTER(vp)]
@@ -430,3 +432,14 @@ def load_calibration(path: str) -> int:
     n = C.c_int()
     _check(lib().mma_load_calibration(path.encode(), C.byref(n)), "mma_load_calibration")
     return n.value
+
+
+def host_alloc_for(nbytes: int, device: int, direction: int) -> int:
+    """Pinned buffer whose per-path ranges live on each path GPU's NUMA node."""
+    p = C.c_void_p()
+    _check(lib().mma_host_alloc_for(C.byref(p), nbytes, device, direction), "mma_host_alloc_for")
+    return int(p.value or 0)
+
+
+def host_page_node(ptr: int) -> int:
+    return int(lib().mma_host_page_node(ptr))

