@@ -55,8 +55,10 @@ class KVShape:
         return self.nsegs * self.seg_bytes
 
 
-def kv_segments(shape: KVShape, seed: int = SEED_BASE + 3):
-    """Segment table of one prefix-cache fetch (config 3), layer-major.
+def kv_segments(shape: KVShape, seed: int = SEED_BASE + 3, request: int = 0):
+    """Segment table of one prefix-cache fetch (config 3), layer-major. `request` 1 gives a
+    second sequence whose host slots and device blocks are disjoint from request 0's (for
+    overlapping one request's fetch with another's offload).
 
     Returns (host_off, dev_off, seg_bytes, host_pool_bytes, dev_bytes) where host_off[k] /
     dev_off[k] are byte offsets of segment k inside one pinned host pool and one device
@@ -66,8 +68,11 @@ def kv_segments(shape: KVShape, seed: int = SEED_BASE + 3):
     """
     sb = shape.seg_bytes
     nslots = shape.nsegs * shape.host_slot_factor
-    host_slot = permutation(seed, nslots)[: shape.nsegs].astype(np.int64)
-    block_ids = np.sort(permutation(seed + 1, shape.device_blocks)[: shape.nblocks]).astype(np.int64)
+    r0, r1 = request * shape.nsegs, (request + 1) * shape.nsegs
+    b0, b1 = request * shape.nblocks, (request + 1) * shape.nblocks
+    assert r1 <= nslots and b1 <= shape.device_blocks
+    host_slot = permutation(seed, nslots)[r0:r1].astype(np.int64)
+    block_ids = np.sort(permutation(seed + 1, shape.device_blocks)[b0:b1]).astype(np.int64)
     # device layout: [layer][K|V][device_blocks] segments of sb bytes
     k = np.arange(shape.nsegs, dtype=np.int64)
     layer_kv = k // shape.nblocks           # (layer, K|V) index, layer-major

@@ -237,11 +237,13 @@ int mma_finalize(void)
         DevRes& r = e.dev[d];
         if (!r.made) continue;
         DeviceGuard dg(d);
-        cudaStreamDestroy(r.kern);
-        cudaStreamDestroy(r.hop[0]);
-        cudaStreamDestroy(r.hop[1]);
-        cudaStreamDestroy(r.direct);
-        cudaStreamDestroy(r.zc);
+        for (Lanes& l : r.lane) {
+            cudaStreamDestroy(l.kern);
+            cudaStreamDestroy(l.hop[0]);
+            cudaStreamDestroy(l.hop[1]);
+            cudaStreamDestroy(l.direct);
+            cudaStreamDestroy(l.zc);
+        }
         cudaEventDestroy(r.fork);
         r = DevRes();
     }

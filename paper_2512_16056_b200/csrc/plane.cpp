@@ -114,13 +114,15 @@ int make_device(int d)
     DeviceGuard g(d);
     int lo, hi;
     CK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
-    // Five streams created back to back so they land on distinct hardware queues: a
-    // spinning relay kernel must never sit in front of the DMAs it waits for.
-    CK(cudaStreamCreateWithPriority(&r.kern, cudaStreamNonBlocking, hi));
-    CK(cudaStreamCreateWithPriority(&r.hop[0], cudaStreamNonBlocking, hi));
-    CK(cudaStreamCreateWithPriority(&r.hop[1], cudaStreamNonBlocking, hi));
-    CK(cudaStreamCreateWithPriority(&r.direct, cudaStreamNonBlocking, hi));
-    CK(cudaStreamCreateWithPriority(&r.zc, cudaStreamNonBlocking, hi));
+    // Ten streams (five per direction) created back to back so they land on distinct
+    // hardware queues: a spinning relay kernel must never sit in front of the DMAs it waits for.
+    for (Lanes& l : r.lane) {
+        CK(cudaStreamCreateWithPriority(&l.kern, cudaStreamNonBlocking, hi));
+        CK(cudaStreamCreateWithPriority(&l.hop[0], cudaStreamNonBlocking, hi));
+        CK(cudaStreamCreateWithPriority(&l.hop[1], cudaStreamNonBlocking, hi));
+        CK(cudaStreamCreateWithPriority(&l.direct, cudaStreamNonBlocking, hi));
+        CK(cudaStreamCreateWithPriority(&l.zc, cudaStreamNonBlocking, hi));
+    }
     CK(cudaEventCreateWithFlags(&r.fork, cudaEventDisableTiming));
     CK(cudaDeviceGetAttribute(&r.sms, cudaDevAttrMultiProcessorCount, d));
     for (int p = 0; p < e.ndev; p++) {
@@ -558,16 +560,16 @@ int run_job(Job& j)
         // upload on the kernel stream and the direct stream's order: kern first, then
         // the direct stream waits for it through an event-free trick: upload on both
         // streams' common predecessor = kern; the direct stream waits on kern below.
-        CK((cudaError_t)use(e.dev[g].kern, g));
-        CK(cudaMemcpyAsync(dtab[g], htab, tab_bytes, cudaMemcpyHostToDevice, e.dev[g].kern));
+        CK((cudaError_t)use(e.dev[g].lane[j.dir].kern, g));
+        CK(cudaMemcpyAsync(dtab[g], htab, tab_bytes, cudaMemcpyHostToDevice, e.dev[g].lane[j.dir].kern));
     }
     tr.mark("upload");
     // streams that launch table-reading kernels other than kern wait for the upload
     auto after_upload = [&](cudaStream_t s, int g) -> int {
-        if (!dtab[g] || s == e.dev[g].kern) return cudaSuccess;
-        cudaEvent_t ev = join_event(e.dev[g].kern, g);
+        if (!dtab[g] || s == e.dev[g].lane[j.dir].kern) return cudaSuccess;
+        cudaEvent_t ev = join_event(e.dev[g].lane[j.dir].kern, g);
         DeviceGuard dg(g);
-        CK(cudaEventRecord(ev, e.dev[g].kern));
+        CK(cudaEventRecord(ev, e.dev[g].lane[j.dir].kern));
         return (int)cudaStreamWaitEvent(s, ev, 0);
     };
 
@@ -609,8 +611,8 @@ int run_job(Job& j)
         log = t.log;
         t.log_n = n_log;
         DeviceGuard g(j.d);
-        CK((cudaError_t)use(e.dev[j.d].direct, j.d));
-        CK(cudaMemsetAsync(log, 0xff, n_log, e.dev[j.d].direct));
+        CK((cudaError_t)use(e.dev[j.d].lane[j.dir].direct, j.d));
+        CK(cudaMemsetAsync(log, 0xff, n_log, e.dev[j.d].lane[j.dir].direct));
     } else {
         t.log_n = 0;
     }
@@ -622,7 +624,7 @@ int run_job(Job& j)
             CK(cudaMalloc(&t.dyn, kDynSlots * kDynSlotWords * sizeof(unsigned long long)));
         }
         unsigned long long* slot = t.dyn + (t.dyn_next++ % kDynSlots) * kDynSlotWords;
-        cudaStream_t zs = e.dev[j.d].zc;
+        cudaStream_t zs = e.dev[j.d].lane[j.dir].zc;
         CK((cudaError_t)use(zs, j.d));
         cudaEvent_t zeroed = join_event(zs, j.d);
         {
@@ -636,7 +638,7 @@ int run_job(Job& j)
         for (int p = 0; p < P; p++) {
             if (!active[p]) continue;
             const int g = ps[p].gpu;
-            cudaStream_t s = e.dev[g].zc;
+            cudaStream_t s = e.dev[g].lane[j.dir].zc;
             CK((cudaError_t)use(s, g));
             CK((cudaError_t)after_upload(s, g));
             DeviceGuard dg(g);
@@ -670,7 +672,7 @@ int run_job(Job& j)
         if (relay) t.stats.relay_bytes += bytes_p;
         if (mode[p] == MMA_HOP_ZC) {
             // one kernel per path: on d for the direct path, on r for a one-hop relay
-            cudaStream_t s = e.dev[g].zc;
+            cudaStream_t s = e.dev[g].lane[j.dir].zc;
             CK((cudaError_t)use(s, g));
             CK((cudaError_t)after_upload(s, g));
             ZcLaunchArg a{};
@@ -691,7 +693,7 @@ int run_job(Job& j)
         }
         if (relay) continue;                         // CE relays below
         // direct CE: one DMA (or batch) per run of consecutive chunks
-        cudaStream_t s = e.dev[g].direct;
+        cudaStream_t s = e.dev[g].lane[j.dir].direct;
         CK((cudaError_t)use(s, g));
         DeviceGuard dg(g);
         size_t a = 0;
@@ -764,7 +766,7 @@ int run_job(Job& j)
         }
         for (auto& kv : launches) {
             const int kd = kv.first;
-            cudaStream_t s = e.dev[kd].kern;
+            cudaStream_t s = e.dev[kd].lane[j.dir].kern;
             CK(make_device(kd));
             CK((cudaError_t)use(s, kd));
             DeviceGuard dg(kd);
@@ -782,7 +784,7 @@ int run_job(Job& j)
                 Ring* r = rings[p];
                 const uint64_t g = g0[p] + c;
                 const uint32_t s = (uint32_t)(g % S);
-                cudaStream_t hs = e.dev[r->relay].hop[s & 1];
+                cudaStream_t hs = e.dev[r->relay].lane[j.dir].hop[s & 1];
                 CK((cudaError_t)use(hs, r->relay));
                 DeviceGuard dg(r->relay);
                 char* slot = r->stage + (uint64_t)s * r->slot_bytes;

@@ -54,12 +54,18 @@ struct DeviceGuard {
     }
 };
 
-struct DevRes {
-    bool made = false;
+// One set of engine streams per direction, so an H2D call and a D2H call (PCIe is full
+// duplex) never queue behind each other on a shared stream.
+struct Lanes {
     cudaStream_t direct = nullptr;   // direct-path DMA
     cudaStream_t zc = nullptr;       // zero-copy kernels (direct or one-hop relay)
     cudaStream_t hop[2] = {};        // relay hop DMAs: dual pipeline, slot parity
     cudaStream_t kern = nullptr;     // relay kernels (pull on a target, pack on a relay)
+};
+
+struct DevRes {
+    bool made = false;
+    Lanes lane[2];                   // [MMA_H2D], [MMA_D2H]
     cudaEvent_t fork = nullptr;      // recorded on a user stream of this device
     int sms = 148;
 };

@@ -35,11 +35,15 @@ std::string stream_name(cudaStream_t s)
     for (int d = 0; d < e.ndev; d++) {
         const DevRes& r = e.dev[d];
         if (!r.made) continue;
-        if (s == r.direct) return "direct DMA";
-        if (s == r.hop[0]) return "relay hop stream 0";
-        if (s == r.hop[1]) return "relay hop stream 1";
-        if (s == r.kern) return "relay kernels";
-        if (s == r.zc) return "zero-copy kernels";
+        for (int dir = 0; dir < 2; dir++) {
+            const Lanes& l = r.lane[dir];
+            const std::string sfx = dir == MMA_H2D ? " (H2D)" : " (D2H)";
+            if (s == l.direct) return "direct DMA" + sfx;
+            if (s == l.hop[0]) return "relay hop stream 0" + sfx;
+            if (s == l.hop[1]) return "relay hop stream 1" + sfx;
+            if (s == l.kern) return "relay kernels" + sfx;
+            if (s == l.zc) return "zero-copy kernels" + sfx;
+        }
     }
     return "user stream";
 }
