@@ -343,11 +343,14 @@ def pcie_rate(torch, g, nbytes=GiB, reps=8):
 def dram_read_rate(torch, nbytes=2 * GiB, reps=3):
     """Host DRAM read GB/s with every core (torch CPU reduction over an int64 buffer)."""
     t = torch.ones(nbytes // 8, dtype=torch.int64)
+    threads = torch.get_num_threads()
+    torch.set_num_threads(os.cpu_count() or 1)     # torchrun sets OMP_NUM_THREADS=1
     best = 1e9
     for _ in range(reps):
         t0 = time.perf_counter()
         t.sum()
         best = min(best, time.perf_counter() - t0)
+    torch.set_num_threads(threads)
     del t
     return nbytes / best / 1e9
 
