@@ -1014,4 +1014,10 @@ def main():
 
 
 if __name__ == "__main__":
-    main()
+    try:
+        main()
+    except Exception as ex:  # noqa: BLE001 - a failed run still leaves one parseable line
+        if int(os.environ.get("RANK", 0)) == 0:
+            print(json.dumps({"metric": METRIC, "value": None, "unit": "GB/s", "error": f"{type(ex).__name__}: {ex}"}),
+                  flush=True)
+        raise
