@@ -98,6 +98,15 @@ class Dist:
         self.pg.all_reduce(t, op=self.pg.ReduceOp.MAX)
         return float(t.item())
 
+    def gather_visible(self):
+        """Every rank's CUDA_VISIBLE_DEVICES (None = unrestricted), rank order."""
+        v = os.environ.get("CUDA_VISIBLE_DEVICES")
+        if not self.pg:
+            return [v]
+        out = [None] * self.world
+        self.pg.all_gather_object(out, v)
+        return out
+
     def close(self):
         if self.pg:
             self.pg.destroy_process_group()
@@ -549,7 +558,24 @@ def run_mp(args, dist, torch, mma):
         mma.shared_host_free(pool, name)
 
 
-def run_contention(args, dist, torch, mma):
+def widen_visible(dist, visible_sets):
+    """Rank 0 drives every path GPU: if each rank was given only its own device, widen rank
+    0's view to the union of the job's devices (gathered before any CUDA call)."""
+    vis = os.environ.get("CUDA_VISIBLE_DEVICES")
+    if dist.world <= 1 or not visible_sets or any(v is None for v in visible_sets):
+        return None
+    union = []
+    for v in visible_sets:
+        for x in (y.strip() for y in v.split(",")):
+            if x and x not in union:
+                union.append(x)
+    if len(union) > len([x for x in (vis or "").split(",") if x.strip()]):
+        os.environ["CUDA_VISIBLE_DEVICES"] = ",".join(union)
+        return f"CUDA_VISIBLE_DEVICES={vis} widened for rank 0 to the job's devices {','.join(union)}"
+    return None
+
+
+def run_contention(args, dist, torch, mma, visible_sets):
     """BASELINE config 5: every path GPU reloads its Llama-3-70B TP8 weight shard at once
     (one contiguous H2D per GPU, each on its own stream) while GPUs 0 and 1 also fetch a
     prefix-cache KV table -- all through one engine, whose backlog ledger plans each call
@@ -565,6 +591,7 @@ def run_contention(args, dist, torch, mma):
         dist.max(0.0)
         dist.barrier()
         return
+    widen_visible(dist, visible_sets)
     k = max(1, min(args.gpus, torch.cuda.device_count()))
     gpus = list(range(k))
     shard = int(17_640_734_720 * args.contention_scale) // 4096 * 4096
@@ -643,8 +670,9 @@ def main():
         run_mp(args, dist, torch, mma)
         dist.close()
         return
+    visible_sets = dist.gather_visible()
     if args.workload == "contention":
-        run_contention(args, dist, torch, mma)
+        run_contention(args, dist, torch, mma, visible_sets)
         dist.close()
         return
 
@@ -657,12 +685,7 @@ def main():
         dist.close()
         return
 
-    # rank 0 drives every path GPU: widen a per-rank device restriction if one was set
-    vis = os.environ.get("CUDA_VISIBLE_DEVICES")
-    vis_note = None
-    if dist.world > 1 and vis is not None and len([x for x in vis.split(",") if x.strip()]) < args.gpus:
-        del os.environ["CUDA_VISIBLE_DEVICES"]
-        vis_note = f"CUDA_VISIBLE_DEVICES={vis} widened for rank 0 (it drives all {args.gpus} path GPUs)"
+    vis_note = widen_visible(dist, visible_sets)
     ngpu_vis = torch.cuda.device_count()
     k = max(1, min(args.gpus, ngpu_vis))
     dev = torch.device("cuda:0")

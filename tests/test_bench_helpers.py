@@ -63,3 +63,16 @@ def test_reference_arm_line():
                 "scaling", "vs_baseline", "dtype", "data", "config", "cpu_baseline", "e2e"):
         assert key in j, key
     assert j["impl"] == "reference" and j["metric"] == bench.METRIC
+
+
+def test_widen_visible(monkeypatch):
+    class D:
+        world = 4
+    monkeypatch.setenv("CUDA_VISIBLE_DEVICES", "4")
+    note = bench.widen_visible(D(), ["4", "5", "6", "7"])
+    import os
+    assert os.environ["CUDA_VISIBLE_DEVICES"] == "4,5,6,7" and "widened" in note
+    monkeypatch.setenv("CUDA_VISIBLE_DEVICES", "0,1,2,3")
+    assert bench.widen_visible(D(), ["0,1,2,3"] * 4) is None             # already sees the job's GPUs
+    monkeypatch.delenv("CUDA_VISIBLE_DEVICES")
+    assert bench.widen_visible(D(), [None] * 4) is None                  # unrestricted
