@@ -97,6 +97,11 @@ typedef struct {
      * entry per claim. Small claims keep every link's share proportional to its speed
      * (the paper's outstanding-queue depth). 0 = default (256 KiB). */
     size_t claim_bytes;
+    /* CTAs (512 threads each) per zero-copy path kernel, planned or dynamic. A PCIe link
+     * saturates with 4 such CTAs (profiles/r01_probe_grid.txt), so a small grid leaves the
+     * relay GPU's other SMs to its own work (§3.4.3: relaying must not steal the
+     * peer's compute). 0 = default (32); at most 4 x the SM count. */
+    int zc_ctas;
 } mma_config_t;
 
 typedef struct {

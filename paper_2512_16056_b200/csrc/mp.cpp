@@ -210,7 +210,7 @@ int mma_copy_share_segments(const mma_segment_t* segs, size_t nsegs, size_t chun
             a.unit_bytes = e.unit_bytes;
             a.path = (uint32_t)path;
             const uint64_t upc = (v.C + e.unit_bytes - 1) / e.unit_bytes;
-            const unsigned grid = (unsigned)std::min<uint64_t>(mine.size() * upc, (uint64_t)e.dev[device].sms * 4);
+            const unsigned grid = (unsigned)std::min<uint64_t>(mine.size() * upc, zc_grid(device));
             KTimer kt(device, s, 0 | (path << 8));
             rc = launch_zc(a, grid, s);
             cudaFreeAsync(dlist, s);
@@ -243,7 +243,7 @@ int mma_copy_claim_segments(const mma_segment_t* segs, size_t nsegs, size_t clai
     a.cursor = (unsigned long long*)cursor;
     a.counts = (unsigned long long*)counts;
     a.path = (uint32_t)path;
-    const unsigned grid = (unsigned)std::min<uint64_t>(a.nchunks, (uint64_t)e.dev[device].sms * 4);
+    const unsigned grid = (unsigned)std::min<uint64_t>(a.nchunks, zc_grid(device));
     int rc = cudaSuccess;
     if (a.nchunks) {
         KTimer kt(device, s, 3 | (path << 8));

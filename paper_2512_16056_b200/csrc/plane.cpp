@@ -63,6 +63,7 @@ void apply_env(mma_config_t* c)
     c->debug_log = env_int("MMA_DEBUG_LOG", c->debug_log);
     c->ledger = env_int("MMA_LEDGER", c->ledger);
     c->claim_bytes = env_size("MMA_CLAIM_BYTES", c->claim_bytes);
+    c->zc_ctas = env_int("MMA_ZC_CTAS", c->zc_ctas);
     if (const char* s = getenv("MMA_PATHS")) {   // comma-separated relay GPU ids
         c->npaths = 0;
         for (const char* p = s; *p && c->npaths < MMA_MAX_PATHS;) {
@@ -88,6 +89,7 @@ void defaults(mma_config_t* c)
     c->relay_ctas = kDefaultRelayCtas;
     c->ledger = 1;
     c->claim_bytes = 256u << 10;
+    c->zc_ctas = kDefaultZcCtas;
 }
 
 int validate_cfg(const mma_config_t& c)
@@ -102,7 +104,16 @@ int validate_cfg(const mma_config_t& c)
         if (c.hop_mode[d] < MMA_HOP_AUTO || c.hop_mode[d] > MMA_HOP_ZC) return cudaErrorInvalidValue;
     if (c.relay_ctas < 1 || c.relay_ctas > 64) return cudaErrorInvalidValue;
     if (c.claim_bytes % 16) return cudaErrorInvalidValue;
+    if (c.zc_ctas < 0 || c.zc_ctas > 4096) return cudaErrorInvalidValue;
     return cudaSuccess;
+}
+
+uint64_t zc_grid(int d)
+{
+    const Engine& e = E();
+    const uint64_t cap = (uint64_t)e.dev[d].sms * 4;
+    const uint64_t want = e.cfg.zc_ctas > 0 ? (uint64_t)e.cfg.zc_ctas : (uint64_t)kDefaultZcCtas;
+    return std::min(want, cap);
 }
 
 // Streams, peer access and flags for device d (lazily, once).
@@ -651,7 +662,7 @@ int run_job(Job& j)
             a.counts = slot + 1;
             a.path = (uint32_t)p;
             a.log = log;
-            const unsigned grid = (unsigned)std::min<uint64_t>(n_log, (uint64_t)e.dev[g].sms * 4);
+            const unsigned grid = (unsigned)std::min<uint64_t>(n_log, zc_grid(g));
             KTimer kt(g, s, 3 | (j.dir << 4) | (p << 8));
             TSpan ts(g, s, "zero-copy dynamic pull", p, -1, 0);
             CK(launch_zc_dyn(a, grid, s));
@@ -683,7 +694,7 @@ int run_job(Job& j)
             a.log = log;
             const uint64_t upc = (j.C + e.unit_bytes - 1) / e.unit_bytes;
             const uint64_t units = a.chunks.count * upc;
-            const unsigned grid = (unsigned)std::min<uint64_t>(units, (uint64_t)e.dev[g].sms * 4);
+            const unsigned grid = (unsigned)std::min<uint64_t>(units, zc_grid(g));
             DeviceGuard dg(g);
             KTimer kt(g, s, 0 | (j.dir << 4) | (p << 8));
             TSpan ts(g, s, relay ? "zero-copy one-hop relay kernel" : "zero-copy direct kernel", p, -1, bytes_p);

@@ -38,6 +38,7 @@ constexpr unsigned kDefaultSlots = 4;
 constexpr uint32_t kDefaultMbps = 50000;
 constexpr uint32_t kDefaultUnit = 128u << 10;
 constexpr int kDefaultRelayCtas = 8;
+constexpr int kDefaultZcCtas = 32;     // zero-copy kernel grid (mma_config_t::zc_ctas)
 constexpr unsigned kDynSlots = 64;        // per-call claim slots, rotating
 constexpr unsigned kDynSlotWords = 32;    // cursor + counts[MMA_KMAX_RINGS] (+ padding)
 
@@ -245,6 +246,8 @@ void apply_env(mma_config_t* c);
 void defaults(mma_config_t* c);
 int validate_cfg(const mma_config_t& c);
 int make_device(int d);
+// grid of a zero-copy path kernel on device d (cfg.zc_ctas, capped at 4 CTAs per SM)
+uint64_t zc_grid(int d);
 int do_init(const mma_config_t* cfg);
 int ensure_init();
 void make_paths(int d);

@@ -48,6 +48,7 @@ class Config(C.Structure):
         ("debug_log", C.c_int),
         ("ledger", C.c_int),
         ("claim_bytes", C.c_size_t),
+        ("zc_ctas", C.c_int),
     ]
 
 

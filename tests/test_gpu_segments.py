@@ -213,3 +213,40 @@ def test_mode_choice_by_measurement(mma, orc):
         assert np.array_equal(got[do[k]:do[k] + sb], hn[ho[k]:ho[k] + sb])
     mma.set_bandwidth(0, mma.H2D, [1, 1])       # pinning clears the segment tuning
     assert all(p["seg_mbps"] == 0 for p in mma.get_paths(0, mma.H2D))
+
+
+@pytest.mark.parametrize("zc_ctas", [1, 3, 4096])
+@pytest.mark.parametrize("mode", [0, 2])
+def test_zero_copy_grid_sizes(mma, orc, zc_ctas, mode):
+    """mma_config_t::zc_ctas: the zero-copy kernels are grid-stride over units (planned) or
+    claims (dynamic), so any grid -- one CTA, a ragged count, more CTAs than the cap --
+    moves the same bytes. KV fetch and its offload mirror through two ZC paths."""
+    shape, ho, do, sb, hpool, dbytes = _kv(272)
+    cfg = configure(mma, loopback=1, chunk=192 << 10, plan_mode=mode, hop=(2, 2), debug=0)
+    cfg.zc_ctas = zc_ctas
+    mma.init(cfg)
+    bw = [3, 2]
+    for d in (mma.H2D, mma.D2H):
+        mma.set_bandwidth(0, d, bw)
+    pool = torch.empty(hpool, dtype=torch.uint8).pin_memory()
+    mma_inputs.fill_pattern(pool.numpy(), 11)
+    dev = torch.full((dbytes,), 0xA5, dtype=torch.uint8, device="cuda")
+    lens = np.full(len(ho), sb, np.int64)
+    segs, n = mma.make_segments(pool.data_ptr() + ho, dev.data_ptr() + do, lens)
+    mma.memcpy_h2d_segments(segs, n, 0)
+    torch.cuda.synchronize()
+    rc, path, _, _ = orc.plan(bw, int(lens.sum()), 192 << 10, 0, 0)   # bytes do not depend on it
+    exp = np.full(dbytes, 0xA5, np.uint8)
+    _oracle_segments(orc, pool.numpy(), exp, ho, do, lens, 192 << 10, bw, path)
+    assert np.array_equal(dev.cpu().numpy(), exp)
+    back = torch.zeros(hpool, dtype=torch.uint8).pin_memory()
+    segs, n = mma.make_segments(dev.data_ptr() + do, back.data_ptr() + ho, lens)
+    mma.memcpy_d2h_segments(segs, n, 0)
+    torch.cuda.synchronize()
+    exp_h = np.zeros(hpool, np.uint8)
+    _oracle_segments(orc, exp, exp_h, do, ho, lens, 192 << 10, bw, path)
+    assert np.array_equal(back.numpy(), exp_h)
+    bad = mma.default_config()
+    bad.zc_ctas = -1
+    with pytest.raises(mma.MMAError):
+        mma.init(bad)
