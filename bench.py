@@ -23,6 +23,7 @@ import os
 import statistics
 import subprocess
 import sys
+import threading
 import time
 from pathlib import Path
 
@@ -227,28 +228,120 @@ def wake_workload(torch, mma, dev):
     return dict(host=host, dev=devbuf, offs=offs, sizes=sizes, bytes=total, desc=desc, wake=True)
 
 
-def run_step(mma, w, dev_idx, stream, ev=None):
+def run_half(mma, w, dev_idx, stream, half):
+    """half 0 = the step's H2D part (fetch / wake / upload), 1 = its D2H part"""
     if "wake" in w:
         hp, dp = w["host"].data_ptr(), w["dev"].data_ptr()
-        if ev: ev[0].record(stream)
         for o, n in zip(w["offs"], w["sizes"]):
-            mma.memcpy_h2d(dp + o, hp + o, n, stream=stream)
-        if ev: ev[1].record(stream)
-        for o, n in zip(w["offs"], w["sizes"]):
-            mma.memcpy_d2h(hp + o, dp + o, n, stream=stream)
-        if ev: ev[2].record(stream)
+            if half == 0:
+                mma.memcpy_h2d(dp + o, hp + o, n, stream=stream)
+            else:
+                mma.memcpy_d2h(hp + o, dp + o, n, stream=stream)
     elif "fetch" in w:
-        if ev: ev[0].record(stream)
-        mma.memcpy_h2d_segments(*w["fetch"], dev_idx, stream=stream)
-        if ev: ev[1].record(stream)
-        mma.memcpy_d2h_segments(*w["offload"], dev_idx, stream=stream)
-        if ev: ev[2].record(stream)
-    else:
-        if ev: ev[0].record(stream)
+        if half == 0:
+            mma.memcpy_h2d_segments(*w["fetch"], dev_idx, stream=stream)
+        else:
+            mma.memcpy_d2h_segments(*w["offload"], dev_idx, stream=stream)
+    elif half == 0:
         mma.memcpy_h2d(w["dev"], w["host"], w["bytes"], stream=stream)
-        if ev: ev[1].record(stream)
+    else:
         mma.memcpy_d2h(w["host2"], w["dev"], w["bytes"], stream=stream)
-        if ev: ev[2].record(stream)
+
+
+def run_step(mma, w, dev_idx, stream, ev=None):
+    if ev: ev[0].record(stream)
+    run_half(mma, w, dev_idx, stream, 0)
+    if ev: ev[1].record(stream)
+    run_half(mma, w, dev_idx, stream, 1)
+    if ev: ev[2].record(stream)
+
+
+# ------------------------------------------------------- hardware byte counters ---
+
+class PcieCounters:
+    """NVML's cumulative PCIe byte counters per GPU (RX = into the GPU, TX = out of it;
+    SURVEY 8(d): "PCIe bytes per GPU should match the planned bytes per path"). On B200 they
+    are 32-bit and wrap every 4 GiB (~75 ms at link rate) and one read takes ~1.3 ms
+    (profiles/r01_probe_nvml.json), so a thread samples every GPU continuously and unwraps;
+    mark() returns the unwrapped totals after a fresh sample. Used outside the timed region."""
+
+    def __init__(self, torch, gpus):
+        import pynvml as N
+        N.nvmlInit()
+        self.N, self.gpus = N, list(gpus)
+        self.h = []
+        for g in self.gpus:
+            pr = torch.cuda.get_device_properties(g)
+            bdf = f"{pr.pci_domain_id:08x}:{pr.pci_bus_id:02x}:{pr.pci_device_id:02x}.0"
+            self.h.append(N.nvmlDeviceGetHandleByPciBusId(bdf))
+        self.fields = [N.NVML_FI_DEV_PCIE_COUNT_RX_BYTES, N.NVML_FI_DEV_PCIE_COUNT_TX_BYTES]
+        self.last = [self._read(h) for h in self.h]
+        self.tot = [[0, 0] for _ in self.h]
+        self.lock = threading.Lock()
+        self.stop_ev = threading.Event()
+        self.th = threading.Thread(target=self._loop, daemon=True)
+        self.th.start()
+
+    def _read(self, h):
+        v = self.N.nvmlDeviceGetFieldValues(h, self.fields)
+        if v[0].nvmlReturn or v[1].nvmlReturn:
+            raise RuntimeError(f"NVML PCIe counters unsupported ({v[0].nvmlReturn}, {v[1].nvmlReturn})")
+        return [int(v[0].value.ullVal), int(v[1].value.ullVal)]
+
+    def _pass(self):
+        with self.lock:
+            for i, h in enumerate(self.h):
+                cur = self._read(h)
+                for c in range(2):
+                    self.tot[i][c] += (cur[c] - self.last[i][c]) % (1 << 32)
+                self.last[i] = cur
+
+    def _loop(self):
+        while not self.stop_ev.is_set():
+            self._pass()
+            time.sleep(0.001)
+
+    def mark(self):
+        self._pass()
+        with self.lock:
+            return [list(t) for t in self.tot]
+
+    def close(self):
+        self.stop_ev.set()
+        self.th.join()
+
+
+def pcie_hw_check(torch, mma, w, stream, path_gpus, dynamic):
+    """One untimed step with the hardware counters running: bytes that entered (H2D) / left
+    (D2H) each path GPU over its PCIe link vs the bytes the plan gave that GPU's path."""
+    gset = sorted(set(path_gpus))
+    cnt = PcieCounters(torch, gset)
+    try:
+        for g in gset:
+            torch.cuda.synchronize(g)
+        out = {"source": "NVML_FI_DEV_PCIE_COUNT_{RX,TX}_BYTES (32-bit, unwrapped by a sampler thread)",
+               "note": "counters include TLP/DLLP protocol overhead (~8% H2D, ~9.5% D2H on one B200 link) "
+                       "and idle background traffic (~16 KB/ms)"}
+        for half, (dname, col) in enumerate((("h2d", 0), ("d2h", 1))):
+            mma.reset_stats(0)
+            a = cnt.mark()
+            run_half(mma, w, 0, stream, half)
+            for g in gset:
+                torch.cuda.synchronize(g)
+            b = cnt.mark()
+            st = mma.get_stats(0)
+            paths = mma.get_paths(0, mma.H2D if half == 0 else mma.D2H)
+            rows = []
+            for i, g in enumerate(gset):
+                hw = b[i][col] - a[i][col]
+                planned = None if dynamic else sum(int(st["path_bytes"][half][p]) for p, pi in enumerate(paths)
+                                                   if pi["gpu"] == g)
+                rows.append({"gpu": g, "planned_bytes": planned, ("rx_bytes" if col == 0 else "tx_bytes"): hw,
+                             "ratio": round(hw / planned, 4) if planned else None})
+            out[dname] = rows
+        return out
+    finally:
+        cnt.close()
 
 
 # --------------------------------------------------------------- cpu baseline ---
@@ -908,6 +1001,8 @@ def main():
                  "frac_step": round(value / (nbytes_step / R_step / 1e9), 4),
                  "R_conc": {k2: round(v, 2) for k2, v in conc.items()},
                  "cpu_dram_read_gbps": round(dram, 2),
+                 # SURVEY 8(c) bound: a rate above 1.02 x R is a timing bug, not a result
+                 "above_roofline_flag": bool(h2d_gbps > 1.02 * Rh or d2h_gbps > 1.02 * Rd),
                  "pcie_solo": {str(g): {k2: round(v, 2) for k2, v in pcie[g].items()} for g in path_gpus},
                  "note": "DRAM term is a lower bound (CPU threads in a VM may not saturate DRAM); when it "
                          "binds, R is a lower bound and the fraction an upper bound"}
@@ -954,6 +1049,12 @@ def main():
             timeline["file"] = tpath
     except Exception as ex:  # noqa: BLE001 - evidence only
         timeline = {"error": str(ex)}
+
+    # ---- hardware check of the chunk -> path assignment: PCIe bytes per path GPU (NVML)
+    try:
+        pcie_hw = pcie_hw_check(torch, mma, w, stream, path_gpus, plan_choice.get("chosen") == "dynamic")
+    except Exception as ex:  # noqa: BLE001 - evidence only
+        pcie_hw = {"error": f"{type(ex).__name__}: {ex}"}
 
     # ---- e2e through the public API: wall clock, host issue + copies + sync every step
     run_step(mma, w, 0, stream)                 # one untimed synchronous step first
@@ -1017,6 +1118,7 @@ def main():
         "e2e": e2e,
         "timeline": timeline,
         "duplex": duplex,
+        "pcie_hw": pcie_hw,
         "gpu_launches": int(st["kernels"]),
         "kernel_kinds": kinds,
         "clocks": clk,

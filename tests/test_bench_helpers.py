@@ -76,3 +76,18 @@ def test_widen_visible(monkeypatch):
     assert bench.widen_visible(D(), ["0,1,2,3"] * 4) is None             # already sees the job's GPUs
     monkeypatch.delenv("CUDA_VISIBLE_DEVICES")
     assert bench.widen_visible(D(), [None] * 4) is None                  # unrestricted
+
+
+def test_pcie_counter_unwrap():
+    """The NVML PCIe counters are 32-bit: the sampler adds deltas modulo 2^32."""
+    import threading
+    c = bench.PcieCounters.__new__(bench.PcieCounters)
+    seq = iter([[4_000_000_000, 10], [100, 20], [4_294_967_000, 30]])
+    c._read = lambda h: next(seq)
+    c.h = [object()]
+    c.last = [[3_000_000_000, 0]]
+    c.tot = [[0, 0]]
+    c.lock = threading.Lock()
+    assert c.mark() == [[1_000_000_000, 10]]
+    assert c.mark() == [[1_000_000_000 + 294_967_396, 20]]
+    assert c.mark() == [[1_000_000_000 + 294_967_396 + 4_294_966_900, 30]]
