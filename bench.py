@@ -1034,6 +1034,36 @@ def main():
                           "offloaded (D2H) on another; both through the engine"}
         assert mma.get_last_error() == 0
 
+    # ---- pre-enqueued (secondary): the stream is held by a gate kernel while two
+    # steps are enqueued, then released -- the data-plane rate without host issue in the way
+    preenq = None
+    try:
+        nst = 2                                       # 4 calls: within the 4 rotating table buffers
+        ga = torch.cuda.Event(enable_timing=True)
+        gb = torch.cuda.Event(enable_timing=True)
+        best = None
+        for _ in range(2):
+            torch.cuda.synchronize(0)
+            with torch.cuda.stream(stream):
+                torch.cuda._sleep(int(2.0e9))          # ~1 s at ~2 GHz: longer than the issue
+            ga.record(stream)
+            t_issue = time.perf_counter()
+            for _ in range(nst):
+                run_step(mma, w, 0, stream)
+            t_issue = time.perf_counter() - t_issue
+            gb.record(stream)
+            gb.synchronize()
+            ms = ga.elapsed_time(gb)
+            best = ms if best is None else min(best, ms)
+        preenq = {"gbps": round(nst * nbytes_step / (best * 1e-3) / 1e9, 3), "steps": nst,
+                  "host_enqueue_ms_per_step": round(t_issue * 1e3 / nst, 3),
+                  "what": "stream gated by a sleep kernel while the steps are enqueued; device time after the "
+                          "gate. The enqueue time includes blocking once the GPU's command queue is full "
+                          "(a copy-engine batch of 131,072 descriptors does not fit while gated)"}
+        assert mma.get_last_error() == 0
+    except Exception as ex:  # noqa: BLE001 - evidence only
+        preenq = {"error": f"{type(ex).__name__}: {ex}"}
+
     # ---- one traced step (engine timeline): which GPUs carried the step, and how
     # concurrently (outside the timed region)
     timeline = None
@@ -1119,6 +1149,7 @@ def main():
         "timeline": timeline,
         "duplex": duplex,
         "pcie_hw": pcie_hw,
+        "preenqueued": preenq,
         "gpu_launches": int(st["kernels"]),
         "kernel_kinds": kinds,
         "clocks": clk,
