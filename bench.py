@@ -876,6 +876,9 @@ def main():
     paths = mma.get_paths(0, mma.H2D)
     path_gpus = [p["gpu"] for p in paths]
     tuned = {"h2d": mma.get_paths(0, mma.H2D), "d2h": mma.get_paths(0, mma.D2H)}
+    # each path's rate alone (mode choice) and with every path active (planner)
+    calib = {d: mma.get_calibration(0, dv, scattered="fetch" in w)
+             for d, dv in (("h2d", mma.H2D), ("d2h", mma.D2H))}
 
     # planned (contiguous, measured bandwidth split) vs GPU-driven dynamic pull: chosen by
     # measurement when more than one path exists (dynamic applies to all-zero-copy sets)
@@ -1160,6 +1163,9 @@ def main():
             pi["seg_mode"] if ("fetch" in w and pi["seg_mode"] >= 0) else pi["mode"], "?"),
             "mbps": pi["seg_mbps"] if ("fetch" in w and pi["seg_mbps"]) else pi["mbps"]} for pi in v]
             for d, v in tuned.items()},
+        "calibration": {"per_path_mbps": calib, "rounds": int(cfg.calib_rounds),
+                        "what": "solo = the path alone in its chosen mode; conc = with every path of the set "
+                                "active (0: single path, not refined)"},
         "engine": {"issue_us_per_call": round((st["issue_us"] - st["wait_us"]) / max(1, st["calls"]), 1),
                    "blocked_us_per_call": round(st["wait_us"] / max(1, st["calls"]), 1),
                    "relay_bytes": int(st["relay_bytes"]), "fallbacks": int(st["fallbacks"])},

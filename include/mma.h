@@ -102,6 +102,14 @@ typedef struct {
      * relay GPU's other SMs to its own work (§3.4.3: relaying must not steal the
      * peer's compute). 0 = default (32); at most 4 x the SM count. */
     int zc_ctas;
+    /* Concurrent calibration rounds (the bandwidth vector is "measured with
+     * all paths of the set active"). After mma_calibrate / mma_tune_segments pick each
+     * path's mode and solo rate, the transfer is run this many more times with every path
+     * active, planned from the current vector; each path's rate becomes the bytes it carried
+     * over the time its own streams took (events on those streams), quantised as in R17.
+     * Shared host DRAM, switch uplinks or socket links then show up in the vector the
+     * planner uses. 0 = solo rates only; default 2. */
+    int calib_rounds;
 } mma_config_t;
 
 typedef struct {
@@ -188,6 +196,14 @@ int mma_load_calibration(const char* path, int* applied);
 /* What mma_tune_segments chose, index-aligned with mma_get_paths (0 / -1 = not tuned). */
 int mma_get_segment_tuning(int device, mma_dir_t dir, uint32_t* mbps, int* modes, int cap,
                            int* npaths);
+
+/* Evidence of the last calibration of (device, dir): per path, the solo rate of the chosen
+ * mode and the rate measured with all paths active (integer MB/s; 0 = not measured: the
+ * path carried no bytes, or calib_rounds = 0 / a single path). scattered = 0 reads
+ * mma_calibrate's result, 1 mma_tune_segments'. Arrays of length cap (either may be NULL);
+ * *npaths receives the path count. */
+int mma_get_calibration(int device, mma_dir_t dir, int scattered, uint32_t* solo_mbps,
+                        uint32_t* conc_mbps, int cap, int* npaths);
 
 /* The plan the engine would use for a copy of `bytes`: path index per chunk. A fallback
  * plan is reported as nchunks = 1, path_of_chunk[0] = 0, *fallback = 1. */

@@ -64,6 +64,7 @@ void apply_env(mma_config_t* c)
     c->ledger = env_int("MMA_LEDGER", c->ledger);
     c->claim_bytes = env_size("MMA_CLAIM_BYTES", c->claim_bytes);
     c->zc_ctas = env_int("MMA_ZC_CTAS", c->zc_ctas);
+    c->calib_rounds = env_int("MMA_CALIB_ROUNDS", c->calib_rounds);
     if (const char* s = getenv("MMA_PATHS")) {   // comma-separated relay GPU ids
         c->npaths = 0;
         for (const char* p = s; *p && c->npaths < MMA_MAX_PATHS;) {
@@ -90,6 +91,7 @@ void defaults(mma_config_t* c)
     c->ledger = 1;
     c->claim_bytes = 256u << 10;
     c->zc_ctas = kDefaultZcCtas;
+    c->calib_rounds = 2;
 }
 
 int validate_cfg(const mma_config_t& c)
@@ -105,6 +107,7 @@ int validate_cfg(const mma_config_t& c)
     if (c.relay_ctas < 1 || c.relay_ctas > 64) return cudaErrorInvalidValue;
     if (c.claim_bytes % 16) return cudaErrorInvalidValue;
     if (c.zc_ctas < 0 || c.zc_ctas > 4096) return cudaErrorInvalidValue;
+    if (c.calib_rounds < 0 || c.calib_rounds > 16) return cudaErrorInvalidValue;
     return cudaSuccess;
 }
 
@@ -225,6 +228,10 @@ void make_paths(int d)
                     ps[i].mbps = t.paths[dir][i].mbps;
                     ps[i].seg_mbps = t.paths[dir][i].seg_mbps;
                     ps[i].seg_mode = t.paths[dir][i].seg_mode;
+                    for (int k = 0; k < 2; k++) {
+                        ps[i].solo_mbps[k] = t.paths[dir][i].solo_mbps[k];
+                        ps[i].conc_mbps[k] = t.paths[dir][i].conc_mbps[k];
+                    }
                 }
         }
         t.paths[dir] = ps;
@@ -322,6 +329,32 @@ static int scratch_host(Scratch& sc, size_t bytes, void** out)
         sc.host_cap = cap;
     }
     *out = sc.host;
+    return cudaSuccess;
+}
+
+// Measurement runs: grow every rotating table buffer of target d (host and each path GPU)
+// to what a call of j's shape can need, so no timed call pays a first-use allocation.
+int reserve_tables(const Job& j)
+{
+    Engine& e = E();
+    Target& t = e.tgt[j.d];
+    make_paths(j.d);
+    const uint64_t n = j.B ? (j.B - 1) / j.C + 1 : 0;
+    const uint64_t seg_words = j.contiguous ? 0 : (j.nseg + 1) + 2 * j.nseg;
+    const size_t bytes = n * 4 + 4 + seg_words * 8;
+    for (Scratch& sc : t.scratch) {
+        if (sc.pending) {
+            CK(cudaEventSynchronize(sc.done));
+            sc.pending = false;
+        }
+        void* p = nullptr;
+        CK((cudaError_t)scratch_host(sc, bytes, &p));
+        for (const PathState& ps : t.paths[j.dir]) {
+            CK(make_device(ps.gpu));
+            CK((cudaError_t)scratch_dev(sc, ps.gpu, bytes, &p));
+        }
+        CK((cudaError_t)scratch_dev(sc, j.d, bytes, &p));
+    }
     return cudaSuccess;
 }
 
@@ -499,7 +532,7 @@ int run_job(Job& j)
     for (int p = 0; p < P; p++) mode[p] = resolve_mode(j, pmode[p]);
     // GPU-driven dynamic pull when every usable path moves bytes with SMs:
     // the assignment is then observed (delivery log, per-path counts), not planned
-    bool dynamic = e.cfg.plan_mode == PLAN_DYNAMIC && !plan.fallback;
+    bool dynamic = e.cfg.plan_mode == PLAN_DYNAMIC && !plan.fallback && !j.timing;
     std::vector<char> active(P, 0);
     for (int p = 0; p < P; p++) {
         active[p] = !lists[p].empty();
@@ -628,6 +661,31 @@ int run_job(Job& j)
         t.log_n = 0;
     }
 
+    // ---- measurement runs: every path's spans open at the fork, before any path's work is
+    // enqueued, so a path's time counts from the start of the call even where paths share a
+    // stream (loopback relays share their GPU's streams)
+    if (j.timing)
+        for (int p = 0; p < P; p++) {
+            if (lists[p].empty()) continue;
+            const int g = ps[p].gpu;
+            CK(make_device(g));
+            Lanes& L = e.dev[g].lane[j.dir];
+            if (mode[p] == MMA_HOP_ZC || ps[p].kind == MMA_PATH_DIRECT) {
+                cudaStream_t s = mode[p] == MMA_HOP_ZC ? L.zc : L.direct;
+                CK((cudaError_t)use(s, g));
+                j.timing->start(p, g, s);
+                continue;
+            }
+            if (!e.wait64 || !e.write64) return MMA_ERR_NO_MEMOPS;
+            Ring* r = nullptr;      // the ring section below gets the same ring and base
+            CK((cudaError_t)get_ring(j.d, j.dir, p, j.C, e.cfg.ring_slots, &r));
+            for (size_t c = 0; c < lists[p].size() && c < 2 * (size_t)r->S; c++) {
+                cudaStream_t hs = L.hop[((r->g_next + c) % r->S) & 1];
+                CK((cudaError_t)use(hs, g));
+                j.timing->start(p, g, hs);
+            }
+        }
+
     // ---- dynamic pull: one claim cursor per call in d's memory, one kernel per path GPU
     if (dynamic) {
         if (!t.dyn) {
@@ -681,6 +739,7 @@ int run_job(Job& j)
         t.stats.path_bytes[j.dir][p] += bytes_p;
         t.stats.path_chunks[j.dir][p] += lists[p].size();
         if (relay) t.stats.relay_bytes += bytes_p;
+        if (j.timing) j.timing->bytes[p] = bytes_p;
         if (mode[p] == MMA_HOP_ZC) {
             // one kernel per path: on d for the direct path, on r for a one-hop relay
             cudaStream_t s = e.dev[g].lane[j.dir].zc;
@@ -700,6 +759,7 @@ int run_job(Job& j)
             TSpan ts(g, s, relay ? "zero-copy one-hop relay kernel" : "zero-copy direct kernel", p, -1, bytes_p);
             CK(launch_zc(a, grid, s));
             t.stats.kernels++;
+            if (j.timing) j.timing->end(p);
             continue;
         }
         if (relay) continue;                         // CE relays below
@@ -721,6 +781,7 @@ int run_job(Job& j)
             if (log) CK(cudaMemsetAsync(log + lists[p][a], p, b - a, s));
             a = b;
         }
+        if (j.timing) j.timing->end(p);
     }
 
     tr.mark("direct+zc");
@@ -823,6 +884,9 @@ int run_job(Job& j)
                     }
                     if (e.write64((CUstream)hs, (CUdeviceptr)&r->credit[s], g + 1, 0) != CUDA_SUCCESS) return cudaErrorUnknown;
                 }
+                // the path's last hop-1 (H2D) / last hop-2 (D2H) DMA closes its spans; the
+                // H2D forward of that chunk (one chunk over NVLink) is not attributed
+                if (j.timing && c + 1 == lists[p].size()) j.timing->end(p);
             }
         }
     }

@@ -92,6 +92,9 @@ struct PathState {
     int mode;       // mma_hop_t
     uint32_t seg_mbps = 0;   // measured for scattered transfers (mma_tune_segments); 0 = unset
     int seg_mode = -1;       // idem; -1 = unset
+    // calibration evidence (mma_get_calibration): [0] contiguous, [1] scattered
+    uint32_t solo_mbps[2] = {0, 0};   // solo rate of the chosen mode
+    uint32_t conc_mbps[2] = {0, 0};   // rate with every path of the set active (0 = not measured)
 };
 
 struct Scratch {    // per-call table uploads, double-buffered by call parity
@@ -167,6 +170,25 @@ struct Piece {
     char* dst;
 };
 
+// Measurement runs (concurrent calibration): per path, timing events
+// bracketing the work each engine stream does for that path, recorded on that stream. A
+// path's time is the longest of its spans; every span starts when its stream passes the
+// call's fork, so the spans of one call share an origin.
+struct PathTiming {
+    struct Span {
+        int dev;
+        cudaStream_t s;
+        cudaEvent_t a, b;
+    };
+    std::vector<std::vector<Span>> path;
+    std::vector<uint64_t> bytes;      // bytes the plan gave each path
+    explicit PathTiming(int P) : path(P), bytes(P, 0) {}
+    ~PathTiming();
+    void start(int p, int dev, cudaStream_t s);   // once per (path, stream)
+    void end(int p);                              // closes every open span of p
+    int collect(std::vector<float>& ms);          // synchronises; 0 ms = no span
+};
+
 struct Job {
     int dir = 0;
     int d = 0;                       // target GPU
@@ -184,6 +206,7 @@ struct Job {
     const uint32_t* bw_override = nullptr;   // measurement runs: per-path bandwidth
     const int* mode_override = nullptr;      // measurement runs: per-path mode
     bool no_small_fallback = false;          // measurement runs: ignore the threshold
+    PathTiming* timing = nullptr;            // measurement runs: per-path events (planned plans only)
 
     // pieces of v[a, b) (the per-segment parts; one piece when contiguous)
     template <typename F>
@@ -255,6 +278,7 @@ void free_ring(Ring& r);
 int get_ring(int d, int dir, int p, uint64_t C, uint32_t S, Ring** out);
 void ledger_inputs(int d, int dir, const std::vector<PathState>& ps, std::vector<PlanPath>& pp);
 int run_job(Job& j);
+int reserve_tables(const Job& j);
 int sticky();
 extern bool g_ktime;
 struct KRec {

@@ -1,8 +1,57 @@
 // tune.cpp — "chosen per path by measurement" (north_star (d)): time
-// every path alone in each hop mode and keep the faster mode and its rate for the planner.
+// every path alone in each hop mode and keep the faster mode; then measure every path's rate
+// with all paths of the set active (a0) and keep that rate for the planner.
 #include "plane.h"
 
 namespace mma {
+
+// ---- per-path timing spans (Job::timing) ---------------------------------------------
+
+PathTiming::~PathTiming()
+{
+    for (auto& v : path)
+        for (auto& sp : v) {
+            DeviceGuard g(sp.dev);
+            if (sp.a) cudaEventDestroy(sp.a);
+            if (sp.b) cudaEventDestroy(sp.b);
+        }
+}
+
+void PathTiming::start(int p, int dev, cudaStream_t s)
+{
+    for (auto& sp : path[p])
+        if (sp.s == s) return;
+    Span sp{dev, s, nullptr, nullptr};
+    DeviceGuard g(dev);
+    if (cudaEventCreate(&sp.a) != cudaSuccess) { cudaGetLastError(); return; }
+    cudaEventRecord(sp.a, s);
+    path[p].push_back(sp);
+}
+
+void PathTiming::end(int p)
+{
+    for (auto& sp : path[p]) {
+        if (sp.b) continue;
+        DeviceGuard g(sp.dev);
+        if (cudaEventCreate(&sp.b) != cudaSuccess) { cudaGetLastError(); continue; }
+        cudaEventRecord(sp.b, sp.s);
+    }
+}
+
+int PathTiming::collect(std::vector<float>& ms)
+{
+    ms.assign(path.size(), 0.f);
+    for (size_t p = 0; p < path.size(); p++)
+        for (auto& sp : path[p]) {
+            if (!sp.a || !sp.b) continue;
+            DeviceGuard g(sp.dev);
+            CK(cudaEventSynchronize(sp.b));
+            float t = 0.f;
+            CK(cudaEventElapsedTime(&t, sp.a, sp.b));
+            ms[p] = std::max(ms[p], t);
+        }
+    return cudaSuccess;
+}
 
 // Measure every path alone in each hop mode on the transfer `proto` describes and keep,
 // per path, the faster mode and its rate (integer MB/s, reading R17: llround). Runs the
@@ -20,6 +69,7 @@ static int tune_paths(Job proto, int reps, std::vector<uint32_t>& mbps, std::vec
     modes.assign(P, MMA_HOP_CE);
     std::vector<uint32_t> bw(P);
     std::vector<int> md(P, MMA_HOP_CE);
+    CK(reserve_tables(proto));
     cudaEvent_t a = nullptr, b = nullptr;
     {
         DeviceGuard g(proto.user_dev);
@@ -68,6 +118,82 @@ static int tune_paths(Job proto, int reps, std::vector<uint32_t>& mbps, std::vec
     return rc;
 }
 
+// Concurrent refinement (bw[p] "measured with all paths of the set
+// active"). Starting from the solo vector, run the transfer `rounds` times with every path
+// active, planned from the current vector (same modes); a path's new rate is the bytes the
+// plan gave it over the longest of its own stream spans (best of `reps`). Paths that get no
+// chunk keep their rate (conc = 0 in the evidence). A link that shares DRAM, a switch uplink
+// or a socket link with others thus enters the planner at the rate it actually gets. The
+// iteration moves toward equal finish times, where every path is busy for the whole call
+// and the measured rates are the concurrent ones.
+static int refine_concurrent(Job proto, int rounds, int reps, std::vector<uint32_t>& mbps,
+                             const std::vector<int>& modes, std::vector<uint32_t>& conc)
+{
+    const int P = (int)mbps.size();
+    conc.assign(P, 0);
+    int active = 0;
+    for (int p = 0; p < P; p++) active += mbps[p] > 0;
+    if (active < 2 || rounds <= 0) return cudaSuccess;
+    int rc = cudaSuccess;
+    for (int r = 0; r < rounds && rc == cudaSuccess; r++) {
+        std::vector<float> best(P, 0.f);
+        std::vector<uint64_t> bytes(P, 0);
+        for (int rep = 0; rep <= reps && rc == cudaSuccess; rep++) {
+            Job j = proto;
+            j.bw_override = mbps.data();
+            j.mode_override = modes.data();
+            j.no_small_fallback = true;
+            PathTiming pt(P);
+            j.timing = &pt;
+            {
+                DeviceGuard g(j.user_dev);
+                rc = run_job(j);
+            }
+            if (rc != cudaSuccess) break;
+            std::vector<float> ms;
+            rc = pt.collect(ms);
+            if (rc != cudaSuccess || rep == 0) continue;   // rep 0 warms up
+            for (int p = 0; p < P; p++)
+                if (ms[p] > 0.f && (best[p] == 0.f || ms[p] < best[p])) best[p] = ms[p];
+            bytes = pt.bytes;
+        }
+        if (rc != cudaSuccess) break;
+        for (int p = 0; p < P; p++) {
+            if (!bytes[p] || best[p] <= 0.f) { conc[p] = 0; continue; }
+            const long long v = llround((double)bytes[p] / ((double)best[p] * 1e-3) / 1e6);
+            conc[p] = (uint32_t)std::max(1ll, v);
+            mbps[p] = conc[p];
+        }
+    }
+    {
+        DeviceGuard g(proto.user_dev);
+        if (rc == cudaSuccess && cudaStreamSynchronize(proto.user) != cudaSuccess) rc = cudaErrorUnknown;
+    }
+    if (rc == cudaSuccess && sticky()) rc = sticky();
+    return rc;
+}
+
+// Solo mode choice, then the concurrent refinement; results stored for contiguous (k = 0)
+// or scattered (k = 1) transfers.
+static int calibrate_job(Job& j, int reps, int k)
+{
+    Engine& e = E();
+    std::vector<uint32_t> mbps, conc;
+    std::vector<int> modes;
+    CK(tune_paths(j, reps, mbps, modes));
+    std::vector<uint32_t> solo = mbps;
+    CK(refine_concurrent(j, e.cfg.calib_rounds, reps, mbps, modes, conc));
+    auto& ps = e.tgt[j.d].paths[j.dir];
+    for (size_t p = 0; p < ps.size(); p++) {
+        if (!mbps[p]) continue;
+        if (k == 0) { ps[p].mbps = mbps[p]; ps[p].mode = modes[p]; }
+        else { ps[p].seg_mbps = mbps[p]; ps[p].seg_mode = modes[p]; }
+        ps[p].solo_mbps[k] = solo[p];
+        ps[p].conc_mbps[k] = conc[p];
+    }
+    return cudaSuccess;
+}
+
 }  // namespace mma
 
 using namespace mma;
@@ -100,14 +226,7 @@ int mma_calibrate(int device, mma_dir_t dir, size_t bytes)
     j.src0 = dir == MMA_H2D ? hbuf : dbuf;
     j.dst0 = dir == MMA_H2D ? dbuf : hbuf;
     j.mapped = true;
-    std::vector<uint32_t> mbps;
-    std::vector<int> modes;
-    int rc = tune_paths(j, 3, mbps, modes);
-    if (rc == cudaSuccess) {
-        auto& ps = e.tgt[device].paths[dir];
-        for (size_t p = 0; p < ps.size(); p++)
-            if (mbps[p]) { ps[p].mbps = mbps[p]; ps[p].mode = modes[p]; }
-    }
+    int rc = calibrate_job(j, 3, 0);
     cudaStreamDestroy(s);
     cudaFree(dbuf);
     cudaFreeHost(hbuf);
@@ -127,15 +246,26 @@ int mma_tune_segments(const mma_segment_t* segs, size_t nsegs, int device, mma_d
     std::lock_guard<std::mutex> g(e.mu);
     CK(make_device(device));
     make_paths(device);
-    std::vector<uint32_t> mbps;
-    std::vector<int> modes;
-    int rc = tune_paths(j, reps, mbps, modes);
-    if (rc == cudaSuccess) {
-        auto& ps = e.tgt[device].paths[dir];
-        for (size_t p = 0; p < ps.size(); p++)
-            if (mbps[p]) { ps[p].seg_mbps = mbps[p]; ps[p].seg_mode = modes[p]; }
+    return calibrate_job(j, reps, 1);
+}
+
+int mma_get_calibration(int device, mma_dir_t dir, int scattered, uint32_t* solo_mbps,
+                        uint32_t* conc_mbps, int cap, int* npaths)
+{
+    CK((cudaError_t)ensure_init());
+    Engine& e = E();
+    if (device < 0 || device >= e.ndev) return cudaErrorInvalidDevice;
+    if ((dir != MMA_H2D && dir != MMA_D2H) || !npaths || cap < 0) return cudaErrorInvalidValue;
+    const int k = scattered ? 1 : 0;
+    std::lock_guard<std::mutex> g(e.mu);
+    make_paths(device);
+    auto& ps = e.tgt[device].paths[dir];
+    *npaths = (int)ps.size();
+    for (int i = 0; i < (int)ps.size() && i < cap; i++) {
+        if (solo_mbps) solo_mbps[i] = ps[i].solo_mbps[k];
+        if (conc_mbps) conc_mbps[i] = ps[i].conc_mbps[k];
     }
-    return rc;
+    return cudaSuccess;
 }
 
 }  // extern "C"

@@ -30,6 +30,7 @@ SYMBOLS = [
     "mma_shared_host_alloc", "mma_shared_host_free", "mma_ipc_export", "mma_ipc_open", "mma_ipc_close",
     "mma_copy_share_segments", "mma_copy_claim_segments", "mma_trace_begin", "mma_trace_end",
     "mma_save_calibration", "mma_load_calibration", "mma_host_alloc_for", "mma_host_page_node",
+    "mma_get_calibration",
 ]
 
 
@@ -49,6 +50,7 @@ class Config(C.Structure):
         ("ledger", C.c_int),
         ("claim_bytes", C.c_size_t),
         ("zc_ctas", C.c_int),
+        ("calib_rounds", C.c_int),
     ]
 
 
@@ -109,6 +111,7 @@ def lib():
         L.mma_tune_segments.argtypes = [C.POINTER(Segment), sz, C.c_int, C.c_int, vp, C.c_int]
         L.mma_kernel_times.argtypes = [vp, vp, sz, C.POINTER(sz)]
         L.mma_get_segment_tuning.argtypes = [C.c_int, C.c_int, vp, vp, C.c_int, C.POINTER(C.c_int)]
+        L.mma_get_calibration.argtypes = [C.c_int, C.c_int, C.c_int, vp, vp, C.c_int, C.POINTER(C.c_int)]
         L.mma_get_dynamic_counts.argtypes = [C.c_int, vp, C.c_int, C.POINTER(C.c_int)]
         L.mma_set_plan_mode.argtypes = [C.c_int]
         L.mma_trace_begin.argtypes = [sz]
@@ -248,6 +251,16 @@ def tune_segments(segs, nsegs: int, device: int, direction: int, stream=None, re
     """Measure CE vs SM zero-copy per path on this scattered transfer (writes the dsts)."""
     _check(lib().mma_tune_segments(segs, nsegs, device, direction, _stream(stream, device), reps),
            "mma_tune_segments")
+
+
+def get_calibration(device: int, direction: int, scattered: bool = False):
+    """Per path: {"solo": MB/s alone, "conc": MB/s with every path active (0 = not measured)}."""
+    solo = (C.c_uint32 * MAX_PATHS)()
+    conc = (C.c_uint32 * MAX_PATHS)()
+    n = C.c_int()
+    _check(lib().mma_get_calibration(device, direction, int(scattered), solo, conc, MAX_PATHS, C.byref(n)),
+           "mma_get_calibration")
+    return [{"solo": int(solo[i]), "conc": int(conc[i])} for i in range(n.value)]
 
 
 def get_plan(device: int, direction: int, nbytes: int):
