@@ -245,6 +245,7 @@ int mma_finalize(void)
             cudaStreamDestroy(l.zc);
         }
         cudaEventDestroy(r.fork);
+        cudaStreamDestroy(r.setup);
         r = DevRes();
     }
     if (e.err) { cudaFreeHost(e.err); e.err = nullptr; }

@@ -77,6 +77,10 @@ __device__ __forceinline__ void relay_body(const RelayLaunchArg& A)
     const uint64_t nunits = R.chunks.count * upc;
     __shared__ unsigned long long s_u;
     __shared__ int s_ok;
+    // thread 0: the last chunk whose flag this CTA saw satisfied. Its flag cannot move on
+    // while this CTA still holds one of its units (the slot is released only when every unit
+    // of the chunk is done), so a later unit of the same chunk skips the poll.
+    uint64_t seen = ~0ull;
     for (;;) {
         if (threadIdx.x == 0) s_u = atomicAdd(R.cursor, 1ull) - R.unit0;
         __syncthreads();
@@ -95,9 +99,11 @@ __device__ __forceinline__ void relay_body(const RelayLaunchArg& A)
         char* slot = R.stage + (uint64_t)s * R.slot_bytes;
         if (threadIdx.x == 0) {
             bool ok;
-            if (PULL) ok = spin_until(A, &R.seq[s], [g](uint64_t v) { return v == g + 1; });
+            if (g == seen) ok = true;
+            else if (PULL) ok = spin_until(A, &R.seq[s], [g](uint64_t v) { return v == g + 1; });
             else ok = (g < R.S) || spin_until(A, &R.credit[s], [g, &R](uint64_t v) { return v >= g - R.S + 1; });
             if (!ok) ring_abort(A, R);
+            else seen = g;
             s_ok = ok;
         }
         __syncthreads();

@@ -138,6 +138,7 @@ int make_device(int d)
         CK(cudaStreamCreateWithPriority(&l.zc, cudaStreamNonBlocking, hi));
     }
     CK(cudaEventCreateWithFlags(&r.fork, cudaEventDisableTiming));
+    CK(cudaStreamCreateWithFlags(&r.setup, cudaStreamNonBlocking));
     CK(cudaDeviceGetAttribute(&r.sms, cudaDevAttrMultiProcessorCount, d));
     for (int p = 0; p < e.ndev; p++) {
         if (p == d || !e.p2p[d][p]) continue;
@@ -263,24 +264,29 @@ int get_ring(int d, int dir, int p, uint64_t C, uint32_t S, Ring** out)
         free_ring(r);
     }
     if (!r.made) {
+        CK(make_device(relay));
+        CK(make_device(kdev));
         r.relay = relay;
         r.kdev = kdev;
         r.S = S;
         r.slot_bytes = C;
+        // flags are zeroed on each device's setup stream and waited for there alone: a new
+        // ring never waits on (possibly long) user work already queued on the device
         {
             DeviceGuard g(relay);
             CK(cudaMalloc(&r.stage, (size_t)S * C));
             CK(cudaMalloc(&r.seq, 2 * 64 * sizeof(uint64_t)));
-            CK(cudaMemset(r.seq, 0, 2 * 64 * sizeof(uint64_t)));
+            CK(cudaMemsetAsync(r.seq, 0, 2 * 64 * sizeof(uint64_t), e.dev[relay].setup));
             r.credit = r.seq + 64;
         }
         {
             DeviceGuard g(kdev);
             CK(cudaMalloc(&r.cnt, 64 * sizeof(unsigned) + 64));
-            CK(cudaMemset(r.cnt, 0, 64 * sizeof(unsigned) + 64));
+            CK(cudaMemsetAsync(r.cnt, 0, 64 * sizeof(unsigned) + 64, e.dev[kdev].setup));
             r.cursor = (unsigned long long*)((char*)r.cnt + 64 * sizeof(unsigned));
         }
-        CK(cudaDeviceSynchronize());
+        CK(cudaStreamSynchronize(e.dev[relay].setup));
+        CK(cudaStreamSynchronize(e.dev[kdev].setup));
         r.g_next = 0;
         r.unit_next = 0;
         r.made = true;

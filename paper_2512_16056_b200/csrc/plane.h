@@ -36,7 +36,11 @@ using PFN_memop64 = CUresult (*)(CUstream, CUdeviceptr, cuuint64_t, unsigned int
 constexpr uint64_t kDefaultChunk = 8ull << 20;
 constexpr unsigned kDefaultSlots = 4;
 constexpr uint32_t kDefaultMbps = 50000;
-constexpr uint32_t kDefaultUnit = 128u << 10;
+// Claim unit of the relay and zero-copy kernels: a CTA claims, checks the flag, copies and
+// releases per unit, so small units pay that bookkeeping often. Relay kernel alone, 8 CTAs,
+// local HBM: 23 GB/s per CTA at 128 KiB, 38 at 512 KiB, 41 at 1 MiB
+// (profiles/r01_probe_relay_unroll.txt)
+constexpr uint32_t kDefaultUnit = 512u << 10;
 constexpr int kDefaultRelayCtas = 8;
 constexpr int kDefaultZcCtas = 32;     // zero-copy kernel grid (mma_config_t::zc_ctas)
 constexpr unsigned kDynSlots = 64;        // per-call claim slots, rotating
@@ -68,6 +72,7 @@ struct DevRes {
     bool made = false;
     Lanes lane[2];                   // [MMA_H2D], [MMA_D2H]
     cudaEvent_t fork = nullptr;      // recorded on a user stream of this device
+    cudaStream_t setup = nullptr;    // ring initialisation (never waits on user work)
     int sms = 148;
 };
 

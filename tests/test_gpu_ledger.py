@@ -34,6 +34,9 @@ def test_plan_sees_in_flight_backlog(mma, orc):
     src = pinned(torch, Ba, seed=2)
     dst = torch.empty(Ba, dtype=torch.uint8, device="cuda")
     s = torch.cuda.Stream()
+    mma.memcpy_h2d(dst, src, Ba, stream=s)        # rings and table buffers exist from here on
+    s.synchronize()
+    assert mma.get_plan(0, mma.H2D, B)[0] == idle_plan.tobytes()
     with torch.cuda.stream(s):
         torch.cuda._sleep(3_000_000_000)          # ~1.5 s at 1.9 GHz
         mma.memcpy_h2d(dst, src, Ba, stream=s)
@@ -64,3 +67,26 @@ def test_ledger_off_ignores_backlog(mma, orc):
         mma.memcpy_h2d(dst, src, 24 * MiB, stream=s)
     assert mma.get_plan(0, mma.H2D, B)[0] == idle_plan.tobytes()
     s.synchronize()
+
+
+def test_new_ring_does_not_wait_on_user_work(mma):
+    """Creating a relay ring zeroes its flags on a private setup stream: the first multipath
+    call returns (is enqueued) while unrelated user work still runs on the device."""
+    import time
+    mma.finalize()
+    configure(mma, loopback=1, chunk=MiB, plan_mode=0, hop=(1, 1), debug=0)
+    mma.set_bandwidth(0, mma.H2D, [1, 1])
+    B = 16 * MiB
+    src = pinned(torch, B, seed=3)
+    dst = torch.empty(B, dtype=torch.uint8, device="cuda")
+    busy, s = torch.cuda.Stream(), torch.cuda.Stream()
+    with torch.cuda.stream(busy):
+        torch.cuda._sleep(2_000_000_000)          # ~1 s of unrelated work
+    t0 = time.perf_counter()
+    mma.memcpy_h2d(dst, src, B, stream=s)         # creates the ring
+    enqueue_s = time.perf_counter() - t0
+    s.synchronize()
+    torch.cuda.synchronize()
+    assert enqueue_s < 0.4, enqueue_s
+    assert torch.equal(dst.cpu(), src[:B])
+    assert mma.get_stats(0)["relay_bytes"] > 0
