@@ -1,0 +1,25 @@
+#!/bin/bash
+# ncu evidence for the current code on one B200 (run under gpurun); reports land in gpurun_out/.
+# Read them here with scripts/ncu_summarize.py, which writes profiles/ncu_summary.json and the
+# per-kernel CSVs under profiles/.
+#   1. launch list of the bench (per-launch gpu__time_duration, cold, serialised)
+#   2. --set full of the zero-copy gather (config-3 KV fetch, H2D), one launch
+#   3. DRAM / PCIe counters of the zero-copy scatter (config-3 KV offload, D2H); host-writing
+#      kernels return nan under kernel replay, so application replay with a metric list
+#   4. --set full of the relay pull / pack kernels alone (scripts/probe/probe_relay ncu:
+#      7 rings x 8 CTAs, hop 1 complete, slots in local HBM)
+mkdir -p gpurun_out
+NCU="ncu --clock-control none"
+timeout 900 $NCU --metrics gpu__time_duration.sum -c 400 --csv --log-file gpurun_out/launches_bench.csv \
+    python bench.py --steps 2 --warmup 1 --quick --no-verify --modes ce,zc > gpurun_out/ncu_launch_bench.log 2>&1
+echo "launch list rc=$?"
+timeout 900 $NCU --set full --import-source on -k regex:zc_copy -c 1 -f -o gpurun_out/prof_zc_h2d \
+    python scripts/ncu_one_kernel.py --dir h2d > gpurun_out/ncu_zc_h2d.log 2>&1
+echo "zc h2d rc=$?"
+timeout 900 $NCU --replay-mode application -k regex:zc_copy -c 1 -f -o gpurun_out/prof_zc_d2h \
+    --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,pcie__read_bytes.sum,pcie__write_bytes.sum,lts__t_bytes.sum \
+    python scripts/ncu_one_kernel.py --dir d2h > gpurun_out/ncu_zc_d2h.log 2>&1
+echo "zc d2h rc=$?"
+timeout 600 $NCU --set full --import-source on -k regex:relay -c 2 -f -o gpurun_out/prof_relay \
+    ./scripts/probe/probe_relay ncu > gpurun_out/ncu_relay.log 2>&1
+echo "relay rc=$?"
