@@ -817,6 +817,8 @@ def main():
         mma.init(cfg)
         return cfg
 
+    thresholds = {}
+
     def prepare(relays):
         """engine config, per-path mode/bandwidth by measurement, warm-up and a device-side
         check of the bench's own launch configuration (all outside the timed region)"""
@@ -833,6 +835,15 @@ def main():
             else:
                 mma.calibrate(0, mma.H2D, min(w["bytes"], GiB))
                 mma.calibrate(0, mma.D2H, min(w["bytes"], GiB))
+            if len(mma.get_paths(0, mma.H2D)) > 1:
+                # the fallback threshold is the measured native/multipath break-even
+                # (for a contiguous copy; a single path needs none)
+                if "fetch" in w:
+                    mma.calibrate(0, mma.H2D, 256 * MiB)
+                    mma.calibrate(0, mma.D2H, 256 * MiB)
+                for name, dv in (("h2d", mma.H2D), ("d2h", mma.D2H)):
+                    thr, found = mma.tune_threshold(0, dv, 256 * MiB)
+                    thresholds[name] = thr if found else f"no break-even up to 256 MiB (kept {thr})"
         for _ in range(args.warmup):
             run_step(mma, w, 0, stream)
         stream.synchronize()
@@ -1139,7 +1150,9 @@ def main():
         "data": "synthetic",
         "config": {"workload": w["desc"], "paths": k, "path_gpus": path_gpus, "target_gpu": 0,
                    "chunk_bytes": int(cfg.chunk_bytes[0]), "claim_bytes": int(cfg.claim_bytes), "hop": {0: "auto", 1: "ce", 2: "zc"}[args.hop],
-                   "bytes_per_step": nbytes_step, "l2": f"inputs ({w['bytes'] / GiB:.1f} GiB per direction) exceed the 126 MB L2; no flush",
+                   "bytes_per_step": nbytes_step,
+                   "fallback_bytes": thresholds or {"h2d": int(cfg.fallback_bytes[0]), "d2h": int(cfg.fallback_bytes[1])},
+                   "fallback_how": "measured break-even (mma_tune_threshold)" if thresholds else "default (2 chunks)", "l2": f"inputs ({w['bytes'] / GiB:.1f} GiB per direction) exceed the 126 MB L2; no flush",
                    "parallelism": f"1 process drives {k} path GPU(s); torchrun ranks>0 idle on gloo",
                    "visible_devices": vis_note, "multipath_error": multipath_error},
         "per_direction": {"h2d_gbps": round(h2d_gbps, 2), "d2h_gbps": round(d2h_gbps, 2),

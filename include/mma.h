@@ -180,6 +180,16 @@ int mma_set_path_modes(int device, mma_dir_t dir, const int* modes, int npaths);
  * bandwidth (integer MB/s, reading R17: llround). Synchronous. */
 int mma_calibrate(int device, mma_dir_t dir, size_t bytes);
 
+/* Fallback threshold by measurement (§3.2, §5.1.3: below a break-even size
+ * the native single-path copy wins). Times the native copy and the multipath copy (current
+ * bandwidth vector and modes) at sizes chunk, 2*chunk, 4*chunk, ... <= max_bytes through
+ * library-owned buffers, and sets cfg.fallback_bytes[dir] to the smallest swept size from
+ * which every larger swept size is >= 3% faster by multipath. If even max_bytes is not
+ * (a single-path set, or relays that share the target's link), there is no break-even:
+ * the threshold is left unchanged and *found = 0. *thr_out receives the threshold in effect.
+ * Either pointer may be NULL. Synchronous. */
+int mma_tune_threshold(int device, mma_dir_t dir, size_t max_bytes, size_t* thr_out, int* found);
+
 /* The same measurement on the caller's scattered transfer (segment table as in
  * mma_memcpy_*_segments): the copy is executed (1 + reps) times per (path, mode) on
  * `stream`, so the destinations are written. The result applies to scattered transfers

@@ -15,7 +15,7 @@ from .mma import (  # noqa: F401
     set_bandwidth, set_path_modes, tune_segments, get_dynamic_counts, set_plan_mode, set_kernel_timing, kernel_times, fill_pattern,
     verify_pattern, verify_segments, shared_host_alloc, shared_host_free, ipc_export, ipc_open,
     ipc_close, copy_share_segments, copy_claim_segments, trace_begin, trace_end,
-    save_calibration, load_calibration, host_alloc_for, host_page_node, get_calibration,
+    save_calibration, load_calibration, host_alloc_for, host_page_node, get_calibration, tune_threshold,
 )
 
 try:

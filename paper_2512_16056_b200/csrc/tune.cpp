@@ -194,6 +194,44 @@ static int calibrate_job(Job& j, int reps, int k)
     return cudaSuccess;
 }
 
+// Library-owned buffers for a contiguous measurement transfer of `bytes` to/from `device`:
+// pinned mapped host memory, device memory and a private stream; freed on scope exit.
+struct CalBuffers {
+    int dev;
+    char* h = nullptr;
+    char* d = nullptr;
+    cudaStream_t s = nullptr;
+    int rc = cudaSuccess;
+    CalBuffers(int device, size_t bytes) : dev(device)
+    {
+        DeviceGuard g(dev);
+        if ((rc = cudaHostAlloc((void**)&h, bytes, cudaHostAllocPortable | cudaHostAllocMapped))) return;
+        if ((rc = cudaMalloc((void**)&d, bytes))) return;
+        rc = cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking);
+    }
+    ~CalBuffers()
+    {
+        DeviceGuard g(dev);
+        if (s) cudaStreamDestroy(s);
+        if (d) cudaFree(d);
+        if (h) cudaFreeHost(h);
+    }
+    Job job(int dir, size_t bytes) const
+    {
+        Job j;
+        j.dir = dir;
+        j.d = dev;
+        j.user = s;
+        j.user_dev = dev;
+        j.B = bytes;
+        j.C = E().cfg.chunk_bytes[dir];
+        j.src0 = dir == MMA_H2D ? h : d;
+        j.dst0 = dir == MMA_H2D ? d : h;
+        j.mapped = true;
+        return j;
+    }
+};
+
 }  // namespace mma
 
 using namespace mma;
@@ -210,27 +248,78 @@ int mma_calibrate(int device, mma_dir_t dir, size_t bytes)
     CK(make_device(device));
     make_paths(device);
     DeviceGuard dg(device);
-    char* hbuf = nullptr;
-    char* dbuf = nullptr;
-    cudaStream_t s = nullptr;
-    CK(cudaHostAlloc((void**)&hbuf, bytes, cudaHostAllocPortable | cudaHostAllocMapped));
-    CK(cudaMalloc((void**)&dbuf, bytes));
-    CK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
-    Job j;
-    j.dir = dir;
-    j.d = device;
-    j.user = s;
-    j.user_dev = device;
-    j.B = bytes;
-    j.C = e.cfg.chunk_bytes[dir];
-    j.src0 = dir == MMA_H2D ? hbuf : dbuf;
-    j.dst0 = dir == MMA_H2D ? dbuf : hbuf;
-    j.mapped = true;
-    int rc = calibrate_job(j, 3, 0);
-    cudaStreamDestroy(s);
-    cudaFree(dbuf);
-    cudaFreeHost(hbuf);
-    return rc;
+    CalBuffers cb(device, bytes);
+    CK(cb.rc);
+    Job j = cb.job(dir, bytes);
+    return calibrate_job(j, 3, 0);
+}
+
+// Break-even ("thr defaults to the measured B200 break-even"; the paper's
+// 11.3 MB H2D / 13 MB D2H on H20, §5.1.3). Sizes C, 2C, 4C, ... up to max_bytes: each
+// is timed as the native copy on one stream and as the multipath copy with the current
+// vector and modes (best of 5 after a warm-up, CUDA events). The threshold becomes the
+// smallest swept size from which every larger swept size is at least 3% faster by
+// multipath. When even the largest is not, no break-even exists up to max_bytes and the
+// threshold is left as it was (*found = 0): the path set, not the size, is the problem then,
+// and a direct path in zero-copy mode must still serve large scattered copies.
+int mma_tune_threshold(int device, mma_dir_t dir, size_t max_bytes, size_t* thr_out, int* found)
+{
+    CK((cudaError_t)ensure_init());
+    Engine& e = E();
+    if (device < 0 || device >= e.ndev) return cudaErrorInvalidDevice;
+    if ((dir != MMA_H2D && dir != MMA_D2H) || max_bytes == 0) return cudaErrorInvalidValue;
+    std::lock_guard<std::mutex> g(e.mu);
+    CK(make_device(device));
+    make_paths(device);
+    DeviceGuard dg(device);
+    const uint64_t C = e.cfg.chunk_bytes[dir];
+    if (max_bytes < C) max_bytes = C;
+    CalBuffers cb(device, max_bytes);
+    CK(cb.rc);
+    CK(reserve_tables(cb.job(dir, max_bytes)));
+    cudaEvent_t a = nullptr, b = nullptr;
+    CK(cudaEventCreate(&a));
+    CK(cudaEventCreate(&b));
+    const cudaMemcpyKind kind = dir == MMA_H2D ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToHost;
+    std::vector<uint64_t> sizes;
+    std::vector<char> faster;
+    int rc = cudaSuccess;
+    for (uint64_t B = C; B <= max_bytes && rc == cudaSuccess; B *= 2) {
+        float best[2] = {1e30f, 1e30f};
+        for (int how = 0; how < 2 && rc == cudaSuccess; how++)
+            for (int rep = 0; rep <= 5 && rc == cudaSuccess; rep++) {
+                cudaEventRecord(a, cb.s);
+                if (how == 0) {
+                    rc = cudaMemcpyAsync(dir == MMA_H2D ? cb.d : cb.h, dir == MMA_H2D ? cb.h : cb.d, B, kind, cb.s);
+                } else {
+                    Job j = cb.job(dir, B);
+                    j.no_small_fallback = true;
+                    rc = run_job(j);
+                }
+                cudaEventRecord(b, cb.s);
+                if (rc == cudaSuccess && cudaEventSynchronize(b) != cudaSuccess) rc = cudaErrorUnknown;
+                float ms = 0;
+                cudaEventElapsedTime(&ms, a, b);
+                if (rep > 0 && ms > 0) best[how] = std::min(best[how], ms);
+            }
+        sizes.push_back(B);
+        faster.push_back(best[1] < 0.97f * best[0]);
+    }
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+    if (rc == cudaSuccess && sticky()) rc = sticky();
+    if (rc != cudaSuccess) return rc;
+    size_t thr = 0;
+    bool any = false;
+    for (size_t k = sizes.size(); k-- > 0;) {
+        if (!faster[k]) break;
+        thr = sizes[k];
+        any = true;
+    }
+    if (any) e.cfg.fallback_bytes[dir] = thr;
+    if (thr_out) *thr_out = e.cfg.fallback_bytes[dir];
+    if (found) *found = any ? 1 : 0;
+    return cudaSuccess;
 }
 
 int mma_tune_segments(const mma_segment_t* segs, size_t nsegs, int device, mma_dir_t dir,

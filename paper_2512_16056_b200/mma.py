@@ -30,7 +30,7 @@ SYMBOLS = [
     "mma_shared_host_alloc", "mma_shared_host_free", "mma_ipc_export", "mma_ipc_open", "mma_ipc_close",
     "mma_copy_share_segments", "mma_copy_claim_segments", "mma_trace_begin", "mma_trace_end",
     "mma_save_calibration", "mma_load_calibration", "mma_host_alloc_for", "mma_host_page_node",
-    "mma_get_calibration",
+    "mma_get_calibration", "mma_tune_threshold",
 ]
 
 
@@ -111,6 +111,7 @@ def lib():
         L.mma_tune_segments.argtypes = [C.POINTER(Segment), sz, C.c_int, C.c_int, vp, C.c_int]
         L.mma_kernel_times.argtypes = [vp, vp, sz, C.POINTER(sz)]
         L.mma_get_segment_tuning.argtypes = [C.c_int, C.c_int, vp, vp, C.c_int, C.POINTER(C.c_int)]
+        L.mma_tune_threshold.argtypes = [C.c_int, C.c_int, sz, C.POINTER(sz), C.POINTER(C.c_int)]
         L.mma_get_calibration.argtypes = [C.c_int, C.c_int, C.c_int, vp, vp, C.c_int, C.POINTER(C.c_int)]
         L.mma_get_dynamic_counts.argtypes = [C.c_int, vp, C.c_int, C.POINTER(C.c_int)]
         L.mma_set_plan_mode.argtypes = [C.c_int]
@@ -251,6 +252,17 @@ def tune_segments(segs, nsegs: int, device: int, direction: int, stream=None, re
     """Measure CE vs SM zero-copy per path on this scattered transfer (writes the dsts)."""
     _check(lib().mma_tune_segments(segs, nsegs, device, direction, _stream(stream, device), reps),
            "mma_tune_segments")
+
+
+def tune_threshold(device: int, direction: int, max_bytes: int = 256 << 20):
+    """Measure the native/multipath break-even and set it as the fallback threshold.
+    Returns (threshold in effect, found): found is False when multipath did not win even at
+    max_bytes (threshold unchanged)."""
+    thr = C.c_size_t()
+    found = C.c_int()
+    _check(lib().mma_tune_threshold(device, direction, max_bytes, C.byref(thr), C.byref(found)),
+           "mma_tune_threshold")
+    return int(thr.value), bool(found.value)
 
 
 def get_calibration(device: int, direction: int, scattered: bool = False):

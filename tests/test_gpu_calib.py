@@ -118,3 +118,21 @@ def test_scattered_tuning_is_refined(mma, orc):
     assert np.array_equal(blocks[dperm], pool.numpy()[:2 * nseg * sb].reshape(2 * nseg, sb)[slots])
     assert not got[:G].any() and not got[G + nseg * sb:].any()
     assert mma.get_last_error() == 0
+
+
+@pytest.mark.parametrize("dirn", [0, 1], ids=["h2d", "d2h"])
+def test_threshold_by_measurement(mma, dirn):
+    """mma_tune_threshold (SURVEY a1, P:910 break-even): on one B200 a loopback relay shares
+    the target's own link, so multipath never beats the native copy at any size: no
+    break-even is found and the configured threshold stays. A direct-only set gives the same
+    answer (nothing to gain)."""
+    cfg = configure(mma, loopback=1, chunk=4 * MiB, slots=4, debug=0, thr=12 * MiB)
+    mma.set_bandwidth(0, dirn, [1, 1])
+    assert mma.get_plan(0, dirn, 8 * MiB)[1] is True               # below the threshold
+    assert mma.get_plan(0, dirn, 64 * MiB)[1] is False
+    thr, found = mma.tune_threshold(0, dirn, 128 * MiB)
+    assert (thr, found) == (12 * MiB, False)
+    assert mma.get_plan(0, dirn, 64 * MiB)[1] is False
+    configure(mma, loopback=0, chunk=4 * MiB, debug=0, thr=0)
+    assert mma.tune_threshold(0, dirn, 32 * MiB) == (0, False)
+    assert mma.get_last_error() == 0
