@@ -310,6 +310,11 @@ static cudaEvent_t join_event(cudaStream_t s, int dev)
     return ev;
 }
 
+// Table buffers start at 4 MiB (a 131,072-segment table is 3 MiB) and grow by 1.5x: an
+// allocation of pinned or device memory while copies are in flight can stall the enqueueing
+// thread for tens of ms (scripts/probe_e2e.py with MMA_TRACE=1), so it should happen rarely.
+constexpr size_t kScratchMin = 4u << 20;
+
 // Grow-only device scratch on device `dev` for this call's tables.
 static int scratch_dev(Scratch& sc, int dev, size_t bytes, void** out)
 {
@@ -317,7 +322,7 @@ static int scratch_dev(Scratch& sc, int dev, size_t bytes, void** out)
         DeviceGuard g(dev);
         if (sc.dev[dev]) cudaFree(sc.dev[dev]);
         sc.dev[dev] = nullptr;
-        size_t cap = std::max(bytes, (size_t)1 << 20);
+        size_t cap = std::max(bytes + bytes / 2, kScratchMin);
         CK(cudaMalloc(&sc.dev[dev], cap));
         sc.dev_cap[dev] = cap;
     }
@@ -330,7 +335,7 @@ static int scratch_host(Scratch& sc, size_t bytes, void** out)
     if (sc.host_cap < bytes) {
         if (sc.host) cudaFreeHost(sc.host);
         sc.host = nullptr;
-        size_t cap = std::max(bytes, (size_t)1 << 20);
+        size_t cap = std::max(bytes + bytes / 2, kScratchMin);
         CK(cudaHostAlloc(&sc.host, cap, cudaHostAllocPortable));
         sc.host_cap = cap;
     }
@@ -549,10 +554,20 @@ int run_job(Job& j)
     const uint64_t claimC = e.cfg.claim_bytes ? e.cfg.claim_bytes : (256u << 10);
     const uint64_t n_log = dynamic ? (j.B - 1) / claimC + 1 : n;   // log entries
 
+    // devices whose kernels read the tables (copy-engine-only calls build none)
+    bool needs_tab[MMA_MAX_GPUS] = {};
+    bool any_tab = false;
+    for (int p = 0; p < P; p++) {
+        if (!active[p]) continue;
+        const bool relay = ps[p].kind == MMA_PATH_RELAY;
+        if (mode[p] == MMA_HOP_ZC) needs_tab[ps[p].gpu] = any_tab = true;
+        else if (relay) needs_tab[j.dir == MMA_H2D ? j.d : ps[p].gpu] = any_tab = true;
+    }
+
     // ---- host tables: chunk lists (interleaved plans) and the segment table
     const bool need_ctab = e.cfg.plan_mode == PLAN_INTERLEAVED && !dynamic;
     const uint64_t seg_words = j.contiguous ? 0 : (j.nseg + 1) + 2 * j.nseg;
-    const size_t tab_bytes = (need_ctab ? n * 4 : 0) + ((need_ctab && (n & 1)) ? 4 : 0) + seg_words * 8;
+    const size_t tab_bytes = !any_tab ? 0 : (need_ctab ? n * 4 : 0) + ((need_ctab && (n & 1)) ? 4 : 0) + seg_words * 8;
     std::vector<size_t> ctab_off(P, 0);
     void* htab = nullptr;
     if (tab_bytes) {
@@ -576,14 +591,6 @@ int run_job(Job& j)
             }
     }
     tr.mark("tables");
-    // devices whose kernels read the tables
-    bool needs_tab[MMA_MAX_GPUS] = {};
-    for (int p = 0; p < P; p++) {
-        if (!active[p]) continue;
-        const bool relay = ps[p].kind == MMA_PATH_RELAY;
-        if (mode[p] == MMA_HOP_ZC) needs_tab[ps[p].gpu] = true;
-        else if (relay) needs_tab[j.dir == MMA_H2D ? j.d : ps[p].gpu] = true;
-    }
 
     // ---- fork (a3)
     {

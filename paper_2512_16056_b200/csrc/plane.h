@@ -6,6 +6,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <chrono>
 #include <cstdio>
 #include <cstdlib>
@@ -129,7 +130,7 @@ struct Target {
 
 struct Engine {
     std::mutex mu;                   // one multipath enqueue at a time
-    bool inited = false;
+    std::atomic<bool> inited{false};   // read without the mutex by ensure_init's fast path
     mma_config_t cfg{};
     int ndev = 0;
     bool p2p[MMA_MAX_GPUS][MMA_MAX_GPUS] = {};
