@@ -462,357 +462,472 @@ struct Trace {
     }
 };
 
-// Enqueue one multipath copy (engine mutex held).
-int run_job(Job& j)
-{
-    Engine& e = E();
-    Target& t = e.tgt[j.d];
-    Trace tr;
-    const auto t0 = std::chrono::steady_clock::now();
-    const cudaMemcpyKind kind = (j.dir == MMA_H2D) ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToHost;
-    make_paths(j.d);
-    std::vector<PathState>& ps = t.paths[j.dir];
-    const int P = (int)ps.size();
-
-    // ---- plan (a2)
-    std::vector<PlanPath> pp(P);
-    std::vector<int> pmode(P);
-    for (int p = 0; p < P; p++) {
-        uint32_t bw = (!j.contiguous && ps[p].seg_mbps) ? ps[p].seg_mbps : ps[p].mbps;
-        if (j.bw_override) bw = j.bw_override[p];
-        pp[p] = PlanPath{ps[p].kind == MMA_PATH_DIRECT, bw, 0};
-        pmode[p] = (!j.contiguous && ps[p].seg_mode >= 0) ? ps[p].seg_mode : ps[p].mode;
-        if (j.mode_override) pmode[p] = j.mode_override[p];
+// One multipath call being enqueued (engine mutex held). The stages run in this order:
+// plan (a2) -> native fallback (a1) -> chunk lists and modes -> host tables -> fork (a3) ->
+// table uploads -> delivery log -> measurement spans -> dynamic pull | direct and zero-copy
+// paths (a4, a7) -> copy-engine relay rings (a5, a6, a9) -> join (a8).
+class Call {
+public:
+    explicit Call(Job& j)
+        : j_(j), eng_(E()), t_(eng_.tgt[j.d]),
+          kind_(j.dir == MMA_H2D ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToHost)
+    {
     }
-    const uint64_t thr = j.no_small_fallback ? 0 : e.cfg.fallback_bytes[j.dir];
-    if (!j.bw_override) ledger_inputs(j.d, j.dir, ps, pp);
-    Plan plan;
-    const int pmode_plan = e.cfg.plan_mode == PLAN_DYNAMIC ? PLAN_CONTIGUOUS : e.cfg.plan_mode;
-    if (make_plan(pp.data(), P, j.B, j.C, thr, pmode_plan, plan) != 0)
-        return cudaErrorInvalidValue;
-    t.stats.calls++;
-    t.stats.bytes += j.B;
-    tr.mark("plan");
 
-    // ---- fallback (a1): the native copy on the user stream (§3.2)
-    if (plan.fallback) {
-        t.stats.fallbacks++;
-        const int mode0 = resolve_mode(j, pmode[0]);
-        const bool small = j.B < thr;
-        if (small || mode0 == MMA_HOP_CE) {
+    int run()
+    {
+        t0_ = std::chrono::steady_clock::now();
+        make_paths(j_.d);
+        ps_ = &t_.paths[j_.dir];
+        P_ = (int)ps_->size();
+        CK(plan());
+        if (plan_.fallback) {
+            bool done = false;
+            CK(native_fallback(&done));
+            if (done) return finish();
+        }
+        CK(prepare());
+        CK(build_tables());
+        CK(fork());
+        CK(upload_tables());
+        CK(delivery_log());
+        CK(open_timing());
+        if (dynamic_) CK(enqueue_dynamic());
+        else {
+            CK(enqueue_paths());
+            CK(enqueue_rings());
+        }
+        CK(join());
+        return finish();
+    }
+
+private:
+    Job& j_;
+    Engine& eng_;
+    Target& t_;
+    const cudaMemcpyKind kind_;
+    Trace tr_;
+    std::chrono::steady_clock::time_point t0_;
+    std::vector<PathState>* ps_ = nullptr;
+    int P_ = 0;
+    std::vector<PlanPath> pp_;
+    std::vector<int> pmode_, mode_;
+    uint64_t thr_ = 0;
+    Plan plan_;
+    uint64_t n_ = 0, n_log_ = 0, claimC_ = 0;
+    Scratch* sc_ = nullptr;
+    std::vector<std::vector<uint32_t>> lists_;
+    std::vector<char> active_;
+    bool dynamic_ = false;
+    bool needs_tab_[MMA_MAX_GPUS] = {};
+    bool need_ctab_ = false;
+    size_t tab_bytes_ = 0;
+    std::vector<size_t> ctab_off_;
+    void* htab_ = nullptr;
+    void* dtab_[MMA_MAX_GPUS] = {};
+    cudaEvent_t fork_ = nullptr;
+    std::vector<std::pair<cudaStream_t, int>> used_;   // engine streams this call enqueued on
+    uint8_t* log_ = nullptr;
+
+    PathState& path(int p) { return (*ps_)[p]; }
+    Lanes& lanes(int g) { return eng_.dev[g].lane[j_.dir]; }
+
+    int finish()
+    {
+        t_.stats.issue_us += std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t0_).count();
+        return cudaSuccess;
+    }
+
+    uint64_t path_bytes(int p) const
+    {
+        uint64_t b = 0;
+        for (uint32_t i : lists_[p]) {
+            uint64_t o, l;
+            j_.extent(i, &o, &l);
+            b += l;
+        }
+        return b;
+    }
+
+    // ---- plan (a2): bandwidth and mode per path (scattered tuning, measurement overrides),
+    // backlog from the ledger, then the integer earliest-finish plan
+    int plan()
+    {
+        pp_.resize(P_);
+        pmode_.resize(P_);
+        for (int p = 0; p < P_; p++) {
+            const PathState& q = path(p);
+            uint32_t bw = (!j_.contiguous && q.seg_mbps) ? q.seg_mbps : q.mbps;
+            if (j_.bw_override) bw = j_.bw_override[p];
+            pp_[p] = PlanPath{q.kind == MMA_PATH_DIRECT, bw, 0};
+            pmode_[p] = (!j_.contiguous && q.seg_mode >= 0) ? q.seg_mode : q.mode;
+            if (j_.mode_override) pmode_[p] = j_.mode_override[p];
+        }
+        thr_ = j_.no_small_fallback ? 0 : eng_.cfg.fallback_bytes[j_.dir];
+        if (!j_.bw_override) ledger_inputs(j_.d, j_.dir, *ps_, pp_);
+        const int pm = eng_.cfg.plan_mode == PLAN_DYNAMIC ? PLAN_CONTIGUOUS : eng_.cfg.plan_mode;
+        if (make_plan(pp_.data(), P_, j_.B, j_.C, thr_, pm, plan_) != 0) return cudaErrorInvalidValue;
+        t_.stats.calls++;
+        t_.stats.bytes += j_.B;
+        tr_.mark("plan");
+        return cudaSuccess;
+    }
+
+    // ---- fallback (a1): the native copy on the user stream (§3.2). A single direct
+    // path in zero-copy mode is not native: it continues as a one-path plan.
+    int native_fallback(bool* done)
+    {
+        t_.stats.fallbacks++;
+        const bool small = j_.B < thr_;
+        if (small || resolve_mode(j_, pmode_[0]) == MMA_HOP_CE) {
             DmaBatch b;
-            j.pieces(0, j.B, [&](const Piece& x) { b.add(x.dst, x.src, x.len); });
-            TSpan ts(j.user_dev, j.user, "DMA native (fallback)", 0, -1, j.B);
-            CK((cudaError_t)b.issue(kind, j.user));
-            t.stats.path_bytes[j.dir][0] += j.B;
-            t.stats.path_chunks[j.dir][0] += 1;
-            t.log_n = 0;
-            if (e.cfg.ledger) {
+            j_.pieces(0, j_.B, [&](const Piece& x) { b.add(x.dst, x.src, x.len); });
+            TSpan ts(j_.user_dev, j_.user, "DMA native (fallback)", 0, -1, j_.B);
+            CK((cudaError_t)b.issue(kind_, j_.user));
+            t_.stats.path_bytes[j_.dir][0] += j_.B;
+            t_.stats.path_chunks[j_.dir][0] += 1;
+            t_.log_n = 0;
+            if (eng_.cfg.ledger) {
                 uint64_t lb[MMA_MAX_GPUS] = {}, lo[MMA_MAX_GPUS] = {};
-                lb[j.d] = lo[j.d] = j.B;
-                CK(ledger_add(j.dir, j.user_dev, j.user, lb, lo));
+                lb[j_.d] = lo[j_.d] = j_.B;
+                CK(ledger_add(j_.dir, j_.user_dev, j_.user, lb, lo));
             }
-            t.stats.issue_us += std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t0).count();
+            *done = true;
             return cudaSuccess;
         }
-        // single direct path moved by SM zero-copy: fall through with a one-path plan
-        plan.fallback = false;
-        plan.n = (j.B - 1) / j.C + 1;
-        plan.path.assign(plan.n, 0);
-        plan.count.assign(P, 0);
-        plan.count[0] = plan.n;
+        plan_.fallback = false;
+        plan_.n = (j_.B - 1) / j_.C + 1;
+        plan_.path.assign(plan_.n, 0);
+        plan_.count.assign(P_, 0);
+        plan_.count[0] = plan_.n;
+        return cudaSuccess;
     }
 
-    const uint64_t n = plan.n;
-    Scratch& sc = t.scratch[t.parity & 3];
-    t.parity++;
-    if (sc.pending) {   // the call four back used these tables: it must be finished
-        const auto w0 = std::chrono::steady_clock::now();
-        CK(cudaEventSynchronize(sc.done));
-        sc.pending = false;
-        t.stats.wait_us += std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - w0).count();
-    }
-    // every GPU of the path set gets its streams and peer access before any enqueue
-    for (int p = 0; p < P; p++) CK(make_device(ps[p].gpu));
-    tr.mark("scratch");
-
-    // ---- per-path chunk lists, ascending
-    std::vector<std::vector<uint32_t>> lists(P);
-    for (uint64_t i = 0; i < n; i++) lists[plan.path[i]].push_back((uint32_t)i);
-    std::vector<int> mode(P);
-    for (int p = 0; p < P; p++) mode[p] = resolve_mode(j, pmode[p]);
-    // GPU-driven dynamic pull when every usable path moves bytes with SMs:
-    // the assignment is then observed (delivery log, per-path counts), not planned
-    bool dynamic = e.cfg.plan_mode == PLAN_DYNAMIC && !plan.fallback && !j.timing;
-    std::vector<char> active(P, 0);
-    for (int p = 0; p < P; p++) {
-        active[p] = !lists[p].empty();
-        if (dynamic && pp[p].mbps && mode[p] != MMA_HOP_ZC) dynamic = false;
-    }
-    if (dynamic)
-        for (int p = 0; p < P; p++) active[p] = pp[p].mbps > 0;
-    const uint64_t claimC = e.cfg.claim_bytes ? e.cfg.claim_bytes : (256u << 10);
-    const uint64_t n_log = dynamic ? (j.B - 1) / claimC + 1 : n;   // log entries
-
-    // devices whose kernels read the tables (copy-engine-only calls build none)
-    bool needs_tab[MMA_MAX_GPUS] = {};
-    bool any_tab = false;
-    for (int p = 0; p < P; p++) {
-        if (!active[p]) continue;
-        const bool relay = ps[p].kind == MMA_PATH_RELAY;
-        if (mode[p] == MMA_HOP_ZC) needs_tab[ps[p].gpu] = any_tab = true;
-        else if (relay) needs_tab[j.dir == MMA_H2D ? j.d : ps[p].gpu] = any_tab = true;
-    }
-
-    // ---- host tables: chunk lists (interleaved plans) and the segment table
-    const bool need_ctab = e.cfg.plan_mode == PLAN_INTERLEAVED && !dynamic;
-    const uint64_t seg_words = j.contiguous ? 0 : (j.nseg + 1) + 2 * j.nseg;
-    const size_t tab_bytes = !any_tab ? 0 : (need_ctab ? n * 4 : 0) + ((need_ctab && (n & 1)) ? 4 : 0) + seg_words * 8;
-    std::vector<size_t> ctab_off(P, 0);
-    void* htab = nullptr;
-    if (tab_bytes) {
-        CK((cudaError_t)scratch_host(sc, tab_bytes, &htab));
-        char* h = (char*)htab;
-        size_t o = 0;
-        if (!j.contiguous) {
-            uint64_t* w = (uint64_t*)h;
-            memcpy(w, j.vstart.data(), (j.nseg + 1) * 8);
-            for (uint64_t k = 0; k < j.nseg; k++) {
-                w[j.nseg + 1 + k] = (uint64_t)j.segs[k].src;
-                w[2 * j.nseg + 1 + k] = (uint64_t)j.segs[k].dst;
-            }
-            o = seg_words * 8;
-        }
-        if (need_ctab)
-            for (int p = 0; p < P; p++) {
-                ctab_off[p] = o;
-                memcpy(h + o, lists[p].data(), lists[p].size() * 4);
-                o += lists[p].size() * 4;
-            }
-    }
-    tr.mark("tables");
-
-    // ---- fork (a3)
+    // ---- table buffers, devices, per-path chunk lists and modes
+    int prepare()
     {
-        DeviceGuard g(j.user_dev);
-        CK(make_device(j.user_dev));
-        CK(cudaEventRecord(e.dev[j.user_dev].fork, j.user));
+        n_ = plan_.n;
+        sc_ = &t_.scratch[t_.parity & 3];
+        t_.parity++;
+        if (sc_->pending) {   // the call four back used these tables: it must be finished
+            const auto w0 = std::chrono::steady_clock::now();
+            CK(cudaEventSynchronize(sc_->done));
+            sc_->pending = false;
+            t_.stats.wait_us += std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - w0).count();
+        }
+        // every GPU of the path set gets its streams and peer access before any enqueue
+        for (int p = 0; p < P_; p++) CK(make_device(path(p).gpu));
+        tr_.mark("scratch");
+        lists_.assign(P_, {});
+        for (uint64_t i = 0; i < n_; i++) lists_[plan_.path[i]].push_back((uint32_t)i);
+        mode_.resize(P_);
+        for (int p = 0; p < P_; p++) mode_[p] = resolve_mode(j_, pmode_[p]);
+        // GPU-driven dynamic pull when every usable path moves bytes with SMs:
+        // the assignment is then observed (delivery log, per-path counts), not planned
+        dynamic_ = eng_.cfg.plan_mode == PLAN_DYNAMIC && !j_.timing;
+        active_.assign(P_, 0);
+        for (int p = 0; p < P_; p++) {
+            active_[p] = !lists_[p].empty();
+            if (dynamic_ && pp_[p].mbps && mode_[p] != MMA_HOP_ZC) dynamic_ = false;
+        }
+        if (dynamic_)
+            for (int p = 0; p < P_; p++) active_[p] = pp_[p].mbps > 0;
+        claimC_ = eng_.cfg.claim_bytes ? eng_.cfg.claim_bytes : (256u << 10);
+        n_log_ = dynamic_ ? (j_.B - 1) / claimC_ + 1 : n_;
+        return cudaSuccess;
     }
-    const cudaEvent_t fork = e.dev[j.user_dev].fork;
-    std::vector<std::pair<cudaStream_t, int>> used;
-    auto use = [&](cudaStream_t s, int dev) -> int {
-        for (auto& u : used) if (u.first == s) return cudaSuccess;
-        used.push_back({s, dev});
+
+    // ---- host tables: the segment table and (interleaved plans) the chunk lists, built
+    // only when some kernel reads them (copy-engine-only calls build none)
+    int build_tables()
+    {
+        bool any = false;
+        for (int p = 0; p < P_; p++) {
+            if (!active_[p]) continue;
+            if (mode_[p] == MMA_HOP_ZC) needs_tab_[path(p).gpu] = any = true;
+            else if (path(p).kind == MMA_PATH_RELAY) needs_tab_[j_.dir == MMA_H2D ? j_.d : path(p).gpu] = any = true;
+        }
+        need_ctab_ = eng_.cfg.plan_mode == PLAN_INTERLEAVED && !dynamic_;
+        const uint64_t seg_words = j_.contiguous ? 0 : (j_.nseg + 1) + 2 * j_.nseg;
+        tab_bytes_ = !any ? 0 : (need_ctab_ ? n_ * 4 : 0) + ((need_ctab_ && (n_ & 1)) ? 4 : 0) + seg_words * 8;
+        ctab_off_.assign(P_, 0);
+        if (tab_bytes_) {
+            CK((cudaError_t)scratch_host(*sc_, tab_bytes_, &htab_));
+            char* h = (char*)htab_;
+            size_t o = 0;
+            if (!j_.contiguous) {
+                uint64_t* w = (uint64_t*)h;
+                memcpy(w, j_.vstart.data(), (j_.nseg + 1) * 8);
+                for (uint64_t k = 0; k < j_.nseg; k++) {
+                    w[j_.nseg + 1 + k] = (uint64_t)j_.segs[k].src;
+                    w[2 * j_.nseg + 1 + k] = (uint64_t)j_.segs[k].dst;
+                }
+                o = seg_words * 8;
+            }
+            if (need_ctab_)
+                for (int p = 0; p < P_; p++) {
+                    ctab_off_[p] = o;
+                    memcpy(h + o, lists_[p].data(), lists_[p].size() * 4);
+                    o += lists_[p].size() * 4;
+                }
+        }
+        tr_.mark("tables");
+        return cudaSuccess;
+    }
+
+    // ---- fork (a3): an event on the user stream gates every engine stream the call uses
+    int fork()
+    {
+        DeviceGuard g(j_.user_dev);
+        CK(make_device(j_.user_dev));
+        CK(cudaEventRecord(eng_.dev[j_.user_dev].fork, j_.user));
+        fork_ = eng_.dev[j_.user_dev].fork;
+        return cudaSuccess;
+    }
+
+    int use(cudaStream_t s, int dev)
+    {
+        for (auto& u : used_)
+            if (u.first == s) return cudaSuccess;
+        used_.push_back({s, dev});
         DeviceGuard g(dev);
-        return (int)cudaStreamWaitEvent(s, fork, 0);
-    };
-
-    // table uploads, one per device that runs a kernel (before its kernels, same streams)
-    void* dtab[MMA_MAX_GPUS] = {};
-    for (int g = 0; g < e.ndev; g++) {
-        if (!needs_tab[g] || !tab_bytes) continue;
-        CK(make_device(g));
-        CK((cudaError_t)scratch_dev(sc, g, tab_bytes, &dtab[g]));
-        DeviceGuard dg(g);
-        // upload on the kernel stream and the direct stream's order: kern first, then
-        // the direct stream waits for it through an event-free trick: upload on both
-        // streams' common predecessor = kern; the direct stream waits on kern below.
-        CK((cudaError_t)use(e.dev[g].lane[j.dir].kern, g));
-        CK(cudaMemcpyAsync(dtab[g], htab, tab_bytes, cudaMemcpyHostToDevice, e.dev[g].lane[j.dir].kern));
+        return (int)cudaStreamWaitEvent(s, fork_, 0);
     }
-    tr.mark("upload");
-    // streams that launch table-reading kernels other than kern wait for the upload
-    auto after_upload = [&](cudaStream_t s, int g) -> int {
-        if (!dtab[g] || s == e.dev[g].lane[j.dir].kern) return cudaSuccess;
-        cudaEvent_t ev = join_event(e.dev[g].lane[j.dir].kern, g);
-        DeviceGuard dg(g);
-        CK(cudaEventRecord(ev, e.dev[g].lane[j.dir].kern));
-        return (int)cudaStreamWaitEvent(s, ev, 0);
-    };
 
-    auto vstream_on = [&](int g) {
+    // table uploads, one per device that runs a kernel, on that device's kernel stream
+    int upload_tables()
+    {
+        for (int g = 0; g < eng_.ndev; g++) {
+            if (!needs_tab_[g] || !tab_bytes_) continue;
+            CK(make_device(g));
+            CK((cudaError_t)scratch_dev(*sc_, g, tab_bytes_, &dtab_[g]));
+            DeviceGuard dg(g);
+            CK((cudaError_t)use(lanes(g).kern, g));
+            CK(cudaMemcpyAsync(dtab_[g], htab_, tab_bytes_, cudaMemcpyHostToDevice, lanes(g).kern));
+        }
+        tr_.mark("upload");
+        return cudaSuccess;
+    }
+
+    // streams other than kern that launch table-reading kernels wait for the upload
+    int after_upload(cudaStream_t s, int g)
+    {
+        if (!dtab_[g] || s == lanes(g).kern) return cudaSuccess;
+        cudaEvent_t ev = join_event(lanes(g).kern, g);
+        DeviceGuard dg(g);
+        CK(cudaEventRecord(ev, lanes(g).kern));
+        return (int)cudaStreamWaitEvent(s, ev, 0);
+    }
+
+    VStreamArg vstream_on(int g) const
+    {
         VStreamArg v{};
-        v.B = j.B;
-        v.C = j.C;
-        if (j.contiguous) {
+        v.B = j_.B;
+        v.C = j_.C;
+        if (j_.contiguous) {
             v.nseg = 1;
-            v.src0 = (uint64_t)j.src0;
-            v.dst0 = (uint64_t)j.dst0;
+            v.src0 = (uint64_t)j_.src0;
+            v.dst0 = (uint64_t)j_.dst0;
         } else {
-            v.nseg = j.nseg;
-            const uint64_t* w = (const uint64_t*)dtab[g];
+            v.nseg = j_.nseg;
+            const uint64_t* w = (const uint64_t*)dtab_[g];
             v.start = w;
-            v.src = w + j.nseg + 1;
-            v.dst = w + 2 * j.nseg + 1;
+            v.src = w + j_.nseg + 1;
+            v.dst = w + 2 * j_.nseg + 1;
         }
         return v;
-    };
-    auto chunks_on = [&](int p, int g) {
-        ChunkListArg c{};
-        c.count = lists[p].size();
-        if (c.count == 0) return c;
-        if (need_ctab) c.table = (const uint32_t*)((const char*)dtab[g] + ctab_off[p]);
-        else c.first = lists[p][0];
-        return c;
-    };
+    }
 
-    // delivery log (debug)
-    uint8_t* log = nullptr;
-    if (e.cfg.debug_log) {
-        if (t.log_cap < n_log) {
-            DeviceGuard g(j.d);
-            if (t.log) cudaFree(t.log);
-            CK(cudaMalloc(&t.log, n_log));
-            t.log_cap = n_log;
+    ChunkListArg chunks_on(int p, int g) const
+    {
+        ChunkListArg c{};
+        c.count = lists_[p].size();
+        if (c.count == 0) return c;
+        if (need_ctab_) c.table = (const uint32_t*)((const char*)dtab_[g] + ctab_off_[p]);
+        else c.first = lists_[p][0];
+        return c;
+    }
+
+    // delivery log (debug): one byte per chunk (per claim in dynamic pull), 0xff = unwritten
+    int delivery_log()
+    {
+        if (!eng_.cfg.debug_log) {
+            t_.log_n = 0;
+            return cudaSuccess;
         }
-        log = t.log;
-        t.log_n = n_log;
-        DeviceGuard g(j.d);
-        CK((cudaError_t)use(e.dev[j.d].lane[j.dir].direct, j.d));
-        CK(cudaMemsetAsync(log, 0xff, n_log, e.dev[j.d].lane[j.dir].direct));
-    } else {
-        t.log_n = 0;
+        DeviceGuard g(j_.d);
+        if (t_.log_cap < n_log_) {
+            if (t_.log) cudaFree(t_.log);
+            CK(cudaMalloc(&t_.log, n_log_));
+            t_.log_cap = n_log_;
+        }
+        log_ = t_.log;
+        t_.log_n = n_log_;
+        CK((cudaError_t)use(lanes(j_.d).direct, j_.d));
+        return (int)cudaMemsetAsync(log_, 0xff, n_log_, lanes(j_.d).direct);
     }
 
     // ---- measurement runs: every path's spans open at the fork, before any path's work is
     // enqueued, so a path's time counts from the start of the call even where paths share a
     // stream (loopback relays share their GPU's streams)
-    if (j.timing)
-        for (int p = 0; p < P; p++) {
-            if (lists[p].empty()) continue;
-            const int g = ps[p].gpu;
+    int open_timing()
+    {
+        if (!j_.timing) return cudaSuccess;
+        for (int p = 0; p < P_; p++) {
+            if (lists_[p].empty()) continue;
+            const int g = path(p).gpu;
             CK(make_device(g));
-            Lanes& L = e.dev[g].lane[j.dir];
-            if (mode[p] == MMA_HOP_ZC || ps[p].kind == MMA_PATH_DIRECT) {
-                cudaStream_t s = mode[p] == MMA_HOP_ZC ? L.zc : L.direct;
+            Lanes& L = lanes(g);
+            if (mode_[p] == MMA_HOP_ZC || path(p).kind == MMA_PATH_DIRECT) {
+                cudaStream_t s = mode_[p] == MMA_HOP_ZC ? L.zc : L.direct;
                 CK((cudaError_t)use(s, g));
-                j.timing->start(p, g, s);
+                j_.timing->start(p, g, s);
                 continue;
             }
-            if (!e.wait64 || !e.write64) return MMA_ERR_NO_MEMOPS;
-            Ring* r = nullptr;      // the ring section below gets the same ring and base
-            CK((cudaError_t)get_ring(j.d, j.dir, p, j.C, e.cfg.ring_slots, &r));
-            for (size_t c = 0; c < lists[p].size() && c < 2 * (size_t)r->S; c++) {
+            if (!eng_.wait64 || !eng_.write64) return MMA_ERR_NO_MEMOPS;
+            Ring* r = nullptr;   // enqueue_rings gets the same ring and base
+            CK((cudaError_t)get_ring(j_.d, j_.dir, p, j_.C, eng_.cfg.ring_slots, &r));
+            for (size_t c = 0; c < lists_[p].size() && c < 2 * (size_t)r->S; c++) {
                 cudaStream_t hs = L.hop[((r->g_next + c) % r->S) & 1];
                 CK((cudaError_t)use(hs, g));
-                j.timing->start(p, g, hs);
+                j_.timing->start(p, g, hs);
             }
         }
+        return cudaSuccess;
+    }
 
     // ---- dynamic pull: one claim cursor per call in d's memory, one kernel per path GPU
-    if (dynamic) {
-        if (!t.dyn) {
-            DeviceGuard g(j.d);
-            CK(cudaMalloc(&t.dyn, kDynSlots * kDynSlotWords * sizeof(unsigned long long)));
+    int enqueue_dynamic()
+    {
+        if (!t_.dyn) {
+            DeviceGuard g(j_.d);
+            CK(cudaMalloc(&t_.dyn, kDynSlots * kDynSlotWords * sizeof(unsigned long long)));
         }
-        unsigned long long* slot = t.dyn + (t.dyn_next++ % kDynSlots) * kDynSlotWords;
-        cudaStream_t zs = e.dev[j.d].lane[j.dir].zc;
-        CK((cudaError_t)use(zs, j.d));
-        cudaEvent_t zeroed = join_event(zs, j.d);
+        unsigned long long* slot = t_.dyn + (t_.dyn_next++ % kDynSlots) * kDynSlotWords;
+        cudaStream_t zs = lanes(j_.d).zc;
+        CK((cudaError_t)use(zs, j_.d));
+        cudaEvent_t zeroed = join_event(zs, j_.d);
         {
-            DeviceGuard g(j.d);
+            DeviceGuard g(j_.d);
             CK(cudaMemsetAsync(slot, 0, kDynSlotWords * sizeof(unsigned long long), zs));
             CK(cudaEventRecord(zeroed, zs));
         }
-        t.last_dyn = slot;
-        t.last_dyn_paths = P;
-        t.stats.dynamic_calls++;
-        for (int p = 0; p < P; p++) {
-            if (!active[p]) continue;
-            const int g = ps[p].gpu;
-            cudaStream_t s = e.dev[g].lane[j.dir].zc;
+        t_.last_dyn = slot;
+        t_.last_dyn_paths = P_;
+        t_.stats.dynamic_calls++;
+        for (int p = 0; p < P_; p++) {
+            if (!active_[p]) continue;
+            const int g = path(p).gpu;
+            cudaStream_t s = lanes(g).zc;
             CK((cudaError_t)use(s, g));
             CK((cudaError_t)after_upload(s, g));
             DeviceGuard dg(g);
             if (s != zs) CK(cudaStreamWaitEvent(s, zeroed, 0));
             DynLaunchArg a{};
             a.v = vstream_on(g);
-            a.v.C = claimC;              // the claim unit plays the chunk's role
-            a.nchunks = n_log;
+            a.v.C = claimC_;   // the claim unit plays the chunk's role
+            a.nchunks = n_log_;
             a.cursor = slot;
             a.counts = slot + 1;
             a.path = (uint32_t)p;
-            a.log = log;
-            const unsigned grid = (unsigned)std::min<uint64_t>(n_log, zc_grid(g));
-            KTimer kt(g, s, 3 | (j.dir << 4) | (p << 8));
+            a.log = log_;
+            const unsigned grid = (unsigned)std::min<uint64_t>(n_log_, zc_grid(g));
+            KTimer kt(g, s, 3 | (j_.dir << 4) | (p << 8));
             TSpan ts(g, s, "zero-copy dynamic pull", p, -1, 0);
             CK(launch_zc_dyn(a, grid, s));
-            t.stats.kernels++;
+            t_.stats.kernels++;
         }
+        return cudaSuccess;
     }
 
-    // ---- direct path and zero-copy paths (a4, a7)
-    for (int p = 0; p < P && !dynamic; p++) {
-        if (lists[p].empty()) continue;
-        const int g = ps[p].gpu;
-        CK(make_device(g));
-        const bool relay = ps[p].kind == MMA_PATH_RELAY;
-        uint64_t bytes_p = 0;
-        for (uint32_t i : lists[p]) { uint64_t o, l; j.extent(i, &o, &l); bytes_p += l; }
-        t.stats.path_bytes[j.dir][p] += bytes_p;
-        t.stats.path_chunks[j.dir][p] += lists[p].size();
-        if (relay) t.stats.relay_bytes += bytes_p;
-        if (j.timing) j.timing->bytes[p] = bytes_p;
-        if (mode[p] == MMA_HOP_ZC) {
-            // one kernel per path: on d for the direct path, on r for a one-hop relay
-            cudaStream_t s = e.dev[g].lane[j.dir].zc;
-            CK((cudaError_t)use(s, g));
-            CK((cudaError_t)after_upload(s, g));
-            ZcLaunchArg a{};
-            a.v = vstream_on(g);
-            a.chunks = chunks_on(p, g);
-            a.unit_bytes = e.unit_bytes;
-            a.path = (uint32_t)p;
-            a.log = log;
-            const uint64_t upc = (j.C + e.unit_bytes - 1) / e.unit_bytes;
-            const uint64_t units = a.chunks.count * upc;
-            const unsigned grid = (unsigned)std::min<uint64_t>(units, zc_grid(g));
-            DeviceGuard dg(g);
-            KTimer kt(g, s, 0 | (j.dir << 4) | (p << 8));
+    // ---- direct path and zero-copy paths (a4, a7); copy-engine relays are enqueue_rings'
+    int enqueue_paths()
+    {
+        for (int p = 0; p < P_; p++) {
+            if (lists_[p].empty()) continue;
+            const int g = path(p).gpu;
+            CK(make_device(g));
+            const bool relay = path(p).kind == MMA_PATH_RELAY;
+            const uint64_t bytes_p = path_bytes(p);
+            t_.stats.path_bytes[j_.dir][p] += bytes_p;
+            t_.stats.path_chunks[j_.dir][p] += lists_[p].size();
+            if (relay) t_.stats.relay_bytes += bytes_p;
+            if (j_.timing) j_.timing->bytes[p] = bytes_p;
+            if (mode_[p] == MMA_HOP_ZC) CK(enqueue_zero_copy(p, g, relay, bytes_p));
+            else if (!relay) CK(enqueue_direct_ce(p, g));
+        }
+        tr_.mark("direct+zc");
+        return cudaSuccess;
+    }
+
+    // one kernel per path: on d for the direct path, on r for a one-hop relay
+    int enqueue_zero_copy(int p, int g, bool relay, uint64_t bytes_p)
+    {
+        cudaStream_t s = lanes(g).zc;
+        CK((cudaError_t)use(s, g));
+        CK((cudaError_t)after_upload(s, g));
+        ZcLaunchArg a{};
+        a.v = vstream_on(g);
+        a.chunks = chunks_on(p, g);
+        a.unit_bytes = eng_.unit_bytes;
+        a.path = (uint32_t)p;
+        a.log = log_;
+        const uint64_t upc = (j_.C + eng_.unit_bytes - 1) / eng_.unit_bytes;
+        const unsigned grid = (unsigned)std::min<uint64_t>(a.chunks.count * upc, zc_grid(g));
+        DeviceGuard dg(g);
+        {
+            KTimer kt(g, s, 0 | (j_.dir << 4) | (p << 8));
             TSpan ts(g, s, relay ? "zero-copy one-hop relay kernel" : "zero-copy direct kernel", p, -1, bytes_p);
             CK(launch_zc(a, grid, s));
-            t.stats.kernels++;
-            if (j.timing) j.timing->end(p);
-            continue;
         }
-        if (relay) continue;                         // CE relays below
-        // direct CE: one DMA (or batch) per run of consecutive chunks
-        cudaStream_t s = e.dev[g].lane[j.dir].direct;
-        CK((cudaError_t)use(s, g));
-        DeviceGuard dg(g);
-        size_t a = 0;
-        while (a < lists[p].size()) {
-            size_t b = a + 1;
-            while (b < lists[p].size() && lists[p][b] == lists[p][b - 1] + 1) b++;
-            uint64_t o0, l0, o1, l1;
-            j.extent(lists[p][a], &o0, &l0);
-            j.extent(lists[p][b - 1], &o1, &l1);
-            DmaBatch batch;
-            j.pieces(o0, o1 + l1, [&](const Piece& x) { batch.add(x.dst, x.src, x.len); });
-            TSpan ts(g, s, "DMA direct", p, lists[p][a], o1 + l1 - o0);
-            CK((cudaError_t)batch.issue(kind, s));
-            if (log) CK(cudaMemsetAsync(log + lists[p][a], p, b - a, s));
-            a = b;
-        }
-        if (j.timing) j.timing->end(p);
+        t_.stats.kernels++;
+        if (j_.timing) j_.timing->end(p);
+        return cudaSuccess;
     }
 
-    tr.mark("direct+zc");
-    // ---- CE relay rings (a5, a6 for H2D; a9 for D2H)
-    std::vector<int> rp;   // relay paths using rings
-    for (int p = 0; p < P; p++)
-        if (!lists[p].empty() && ps[p].kind == MMA_PATH_RELAY && mode[p] == MMA_HOP_CE) rp.push_back(p);
-    if (!rp.empty() && !dynamic) {
-        if (!e.wait64 || !e.write64) return MMA_ERR_NO_MEMOPS;
-        const uint32_t S = e.cfg.ring_slots;
-        const uint64_t upc = (j.C + e.unit_bytes - 1) / e.unit_bytes;
-        std::vector<Ring*> rings(P, nullptr);
-        std::vector<uint64_t> g0(P, 0);
+    // direct copy engine: one DMA (or batch) per run of consecutive chunks
+    int enqueue_direct_ce(int p, int g)
+    {
+        cudaStream_t s = lanes(g).direct;
+        CK((cudaError_t)use(s, g));
+        DeviceGuard dg(g);
+        const auto& L = lists_[p];
+        for (size_t a = 0; a < L.size();) {
+            size_t b = a + 1;
+            while (b < L.size() && L[b] == L[b - 1] + 1) b++;
+            uint64_t o0, l0, o1, l1;
+            j_.extent(L[a], &o0, &l0);
+            j_.extent(L[b - 1], &o1, &l1);
+            DmaBatch batch;
+            j_.pieces(o0, o1 + l1, [&](const Piece& x) { batch.add(x.dst, x.src, x.len); });
+            {
+                TSpan ts(g, s, "DMA direct", p, L[a], o1 + l1 - o0);
+                CK((cudaError_t)batch.issue(kind_, s));
+            }
+            if (log_) CK(cudaMemsetAsync(log_ + L[a], p, b - a, s));
+            a = b;
+        }
+        if (j_.timing) j_.timing->end(p);
+        return cudaSuccess;
+    }
+
+    // ---- copy-engine relay rings (a5, a6 for H2D; a9 for D2H): one relay kernel launch per
+    // kernel GPU covering all of its rings, then the copy-engine hops chunk by chunk
+    int enqueue_rings()
+    {
+        std::vector<int> rp;   // relay paths using rings
+        for (int p = 0; p < P_; p++)
+            if (!lists_[p].empty() && path(p).kind == MMA_PATH_RELAY && mode_[p] == MMA_HOP_CE) rp.push_back(p);
+        if (rp.empty()) return cudaSuccess;
+        if (!eng_.wait64 || !eng_.write64) return MMA_ERR_NO_MEMOPS;
+        const uint32_t S = eng_.cfg.ring_slots;
+        const uint64_t upc = (j_.C + eng_.unit_bytes - 1) / eng_.unit_bytes;
+        std::vector<Ring*> rings(P_, nullptr);
+        std::vector<uint64_t> g0(P_, 0);
         for (int p : rp) {
-            CK((cudaError_t)get_ring(j.d, j.dir, p, j.C, S, &rings[p]));
+            CK((cudaError_t)get_ring(j_.d, j_.dir, p, j_.C, S, &rings[p]));
             g0[p] = rings[p]->g_next;
         }
-        // relay kernels: one launch per kernel GPU covering all of its rings
         std::map<int, RelayLaunchArg> launches;
         std::map<int, unsigned> grids;
         for (int p : rp) {
@@ -822,10 +937,10 @@ int run_job(Job& j)
             if (grids.find(kd) == grids.end()) {
                 memset(&A, 0, sizeof(A));
                 A.v = vstream_on(kd);
-                A.unit_bytes = e.unit_bytes;
-                A.log = log;
-                A.err = e.err;
-                A.timeout_ns = e.timeout_ns;
+                A.unit_bytes = eng_.unit_bytes;
+                A.log = log_;
+                A.err = eng_.err;
+                A.timeout_ns = eng_.timeout_ns;
                 grids[kd] = 0;
             }
             if (A.nrings >= MMA_KMAX_RINGS) return cudaErrorInvalidValue;
@@ -842,102 +957,120 @@ int run_job(Job& j)
             R.S = S;
             R.path = (uint32_t)p;
             R.cta_begin = grids[kd];
-            grids[kd] += (unsigned)e.cfg.relay_ctas;
+            grids[kd] += (unsigned)eng_.cfg.relay_ctas;
             R.cta_end = grids[kd];
-            r->g_next += lists[p].size();
+            r->g_next += lists_[p].size();
             // every CTA of the ring claims until it draws one unit past the end, so the
             // cursor advances by the units plus one claim per CTA
-            r->unit_next += (unsigned long long)lists[p].size() * upc + (unsigned)e.cfg.relay_ctas;
+            r->unit_next += (unsigned long long)lists_[p].size() * upc + (unsigned)eng_.cfg.relay_ctas;
         }
         for (auto& kv : launches) {
             const int kd = kv.first;
-            cudaStream_t s = e.dev[kd].lane[j.dir].kern;
+            cudaStream_t s = lanes(kd).kern;
             CK(make_device(kd));
             CK((cudaError_t)use(s, kd));
             DeviceGuard dg(kd);
-            KTimer kt(kd, s, (j.dir == MMA_H2D ? 1 : 2) | (j.dir << 4) | (0xff << 8));
-            TSpan ts(kd, s, j.dir == MMA_H2D ? "relay pull kernel" : "relay pack kernel", -1, -1, 0);
-            CK(launch_relay(kv.second, j.dir == MMA_H2D, grids[kd], s));
-            t.stats.kernels++;
+            KTimer kt(kd, s, (j_.dir == MMA_H2D ? 1 : 2) | (j_.dir << 4) | (0xff << 8));
+            TSpan ts(kd, s, j_.dir == MMA_H2D ? "relay pull kernel" : "relay pack kernel", -1, -1, 0);
+            CK(launch_relay(kv.second, j_.dir == MMA_H2D, grids[kd], s));
+            t_.stats.kernels++;
         }
         // host issue of the copy-engine hops, round-robin across rings chunk by chunk
         size_t maxc = 0;
-        for (int p : rp) maxc = std::max(maxc, lists[p].size());
-        for (size_t c = 0; c < maxc; c++) {
+        for (int p : rp) maxc = std::max(maxc, lists_[p].size());
+        for (size_t c = 0; c < maxc; c++)
             for (int p : rp) {
-                if (c >= lists[p].size()) continue;
-                Ring* r = rings[p];
-                const uint64_t g = g0[p] + c;
-                const uint32_t s = (uint32_t)(g % S);
-                cudaStream_t hs = e.dev[r->relay].lane[j.dir].hop[s & 1];
-                CK((cudaError_t)use(hs, r->relay));
-                DeviceGuard dg(r->relay);
-                char* slot = r->stage + (uint64_t)s * r->slot_bytes;
-                uint64_t off, len;
-                j.extent(lists[p][c], &off, &len);
-                DmaBatch batch;
-                if (j.dir == MMA_H2D) {
-                    if (g >= S && e.wait64((CUstream)hs, (CUdeviceptr)&r->credit[s], g - S + 1, CU_STREAM_WAIT_VALUE_GEQ) != CUDA_SUCCESS)
-                        return cudaErrorUnknown;
-                    j.pieces(off, off + len, [&](const Piece& x) { batch.add(slot + (x.v - off), x.src, x.len); });
-                    {
-                        TSpan ts(r->relay, hs, "DMA hop 1: host -> relay ring", p, (long long)lists[p][c], len);
-                        CK((cudaError_t)batch.issue(kind, hs));
-                    }
-                    if ((long long)g != e.fault_drop_publish &&
-                        e.write64((CUstream)hs, (CUdeviceptr)&r->seq[s], g + 1, 0) != CUDA_SUCCESS)
-                        return cudaErrorUnknown;
-                } else {
-                    if (e.wait64((CUstream)hs, (CUdeviceptr)&r->seq[s], g + 1, CU_STREAM_WAIT_VALUE_GEQ) != CUDA_SUCCESS)
-                        return cudaErrorUnknown;
-                    j.pieces(off, off + len, [&](const Piece& x) { batch.add(x.dst, slot + (x.v - off), x.len); });
-                    {
-                        TSpan ts(r->relay, hs, "DMA hop 2: relay ring -> host", p, (long long)lists[p][c], len);
-                        CK((cudaError_t)batch.issue(kind, hs));
-                    }
-                    if (e.write64((CUstream)hs, (CUdeviceptr)&r->credit[s], g + 1, 0) != CUDA_SUCCESS) return cudaErrorUnknown;
-                }
+                if (c >= lists_[p].size()) continue;
+                CK(ring_hop(p, rings[p], g0[p] + c, lists_[p][c], S));
                 // the path's last hop-1 (H2D) / last hop-2 (D2H) DMA closes its spans; the
                 // H2D forward of that chunk (one chunk over NVLink) is not attributed
-                if (j.timing && c + 1 == lists[p].size()) j.timing->end(p);
+                if (j_.timing && c + 1 == lists_[p].size()) j_.timing->end(p);
             }
-        }
+        tr_.mark("rings");
+        return cudaSuccess;
     }
 
-    tr.mark("rings");
-    // ---- join (a8)
-    for (auto& u : used) {
-        cudaEvent_t ev = join_event(u.first, u.second);
-        {
-            DeviceGuard g(u.second);
-            CK(cudaEventRecord(ev, u.first));
+    // the copy-engine side of ring chunk g (chunk index i of v) on the relay's hop stream.
+    // H2D: wait credit[s] >= g-S+1 (slot drained) -> DMA host -> slot -> publish seq[s] = g+1.
+    // D2H: wait seq[s] >= g+1 (slot packed by the relay kernel) -> DMA slot -> host ->
+    // release credit[s] = g+1.
+    int ring_hop(int p, Ring* r, uint64_t g, uint32_t i, uint32_t S)
+    {
+        const uint32_t s = (uint32_t)(g % S);
+        cudaStream_t hs = lanes(r->relay).hop[s & 1];
+        CK((cudaError_t)use(hs, r->relay));
+        DeviceGuard dg(r->relay);
+        char* slot = r->stage + (uint64_t)s * r->slot_bytes;
+        uint64_t off, len;
+        j_.extent(i, &off, &len);
+        DmaBatch batch;
+        if (j_.dir == MMA_H2D) {
+            if (g >= S && eng_.wait64((CUstream)hs, (CUdeviceptr)&r->credit[s], g - S + 1, CU_STREAM_WAIT_VALUE_GEQ) !=
+                              CUDA_SUCCESS)
+                return cudaErrorUnknown;
+            j_.pieces(off, off + len, [&](const Piece& x) { batch.add(slot + (x.v - off), x.src, x.len); });
+            {
+                TSpan ts(r->relay, hs, "DMA hop 1: host -> relay ring", p, (long long)i, len);
+                CK((cudaError_t)batch.issue(kind_, hs));
+            }
+            if ((long long)g != eng_.fault_drop_publish &&
+                eng_.write64((CUstream)hs, (CUdeviceptr)&r->seq[s], g + 1, 0) != CUDA_SUCCESS)
+                return cudaErrorUnknown;
+        } else {
+            if (eng_.wait64((CUstream)hs, (CUdeviceptr)&r->seq[s], g + 1, CU_STREAM_WAIT_VALUE_GEQ) != CUDA_SUCCESS)
+                return cudaErrorUnknown;
+            j_.pieces(off, off + len, [&](const Piece& x) { batch.add(x.dst, slot + (x.v - off), x.len); });
+            {
+                TSpan ts(r->relay, hs, "DMA hop 2: relay ring -> host", p, (long long)i, len);
+                CK((cudaError_t)batch.issue(kind_, hs));
+            }
+            if (eng_.write64((CUstream)hs, (CUdeviceptr)&r->credit[s], g + 1, 0) != CUDA_SUCCESS) return cudaErrorUnknown;
         }
-        DeviceGuard g(j.user_dev);
-        CK(cudaStreamWaitEvent(j.user, ev, 0));
+        return cudaSuccess;
     }
-    if (tab_bytes) {
-        DeviceGuard g(j.user_dev);
-        if (!sc.done || sc.done_dev != j.user_dev) {
-            if (sc.done) cudaEventDestroy(sc.done);
-            CK(cudaEventCreateWithFlags(&sc.done, cudaEventDisableTiming));
-            sc.done_dev = j.user_dev;
+
+    // ---- join (a8): the user stream waits on every engine stream used; table buffers and
+    // ledger entries are released by events on the user stream
+    int join()
+    {
+        for (auto& u : used_) {
+            cudaEvent_t ev = join_event(u.first, u.second);
+            {
+                DeviceGuard g(u.second);
+                CK(cudaEventRecord(ev, u.first));
+            }
+            DeviceGuard g(j_.user_dev);
+            CK(cudaStreamWaitEvent(j_.user, ev, 0));
         }
-        CK(cudaEventRecord(sc.done, j.user));
-        sc.pending = true;
-    }
-    if (e.cfg.ledger && !dynamic) {
-        uint64_t lb[MMA_MAX_GPUS] = {}, lo[MMA_MAX_GPUS] = {};
-        for (int p = 0; p < P; p++) {
-            uint64_t bytes_p = 0;
-            for (uint32_t i : lists[p]) { uint64_t o, l; j.extent(i, &o, &l); bytes_p += l; }
-            lb[ps[p].gpu] += bytes_p;
-            if (ps[p].kind == MMA_PATH_DIRECT) lo[ps[p].gpu] += bytes_p;
+        if (tab_bytes_) {
+            DeviceGuard g(j_.user_dev);
+            if (!sc_->done || sc_->done_dev != j_.user_dev) {
+                if (sc_->done) cudaEventDestroy(sc_->done);
+                CK(cudaEventCreateWithFlags(&sc_->done, cudaEventDisableTiming));
+                sc_->done_dev = j_.user_dev;
+            }
+            CK(cudaEventRecord(sc_->done, j_.user));
+            sc_->pending = true;
         }
-        CK(ledger_add(j.dir, j.user_dev, j.user, lb, lo));
+        if (eng_.cfg.ledger && !dynamic_) {
+            uint64_t lb[MMA_MAX_GPUS] = {}, lo[MMA_MAX_GPUS] = {};
+            for (int p = 0; p < P_; p++) {
+                const uint64_t bytes_p = path_bytes(p);
+                lb[path(p).gpu] += bytes_p;
+                if (path(p).kind == MMA_PATH_DIRECT) lo[path(p).gpu] += bytes_p;
+            }
+            CK(ledger_add(j_.dir, j_.user_dev, j_.user, lb, lo));
+        }
+        tr_.mark("join");
+        return cudaSuccess;
     }
-    tr.mark("join");
-    t.stats.issue_us += std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t0).count();
-    return cudaSuccess;
+};
+
+// Enqueue one multipath copy (engine mutex held).
+int run_job(Job& j)
+{
+    Call c(j);
+    return c.run();
 }
 
 int sticky()
