@@ -59,6 +59,8 @@ def parse():
     ap.add_argument("--chunk", type=int, default=0, help="chunk bytes (0 = the engine's default)")
     ap.add_argument("--hop", type=int, default=0, help="0 auto, 1 copy engine, 2 SM zero-copy")
     ap.add_argument("--no-verify", action="store_true")
+    ap.add_argument("--engine-modes", action="store_true",
+                    help="N=1: keep the engine's measured mode for the offload (default pins the SM scatter)")
     ap.add_argument("--quick", action="store_true", help="skip baselines (profiling runs)")
     ap.add_argument("--mp", action="store_true",
                     help="multi-process mode (NEXT-4): under torchrun every rank moves its own share of "
@@ -818,6 +820,21 @@ def main():
         return cfg
 
     thresholds = {}
+    policy = {}
+
+    def offload_rate(mode, calls=3):
+        """D2H rate of the workload's offload with the single path pinned to `mode`: `calls`
+        offloads enqueued back to back after a warm-up call (as the timed region runs them)"""
+        mma.set_path_modes(0, mma.D2H, [mode])
+        mma.memcpy_d2h_segments(*w["offload"], 0, stream=stream)
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        for _ in range(calls):
+            mma.memcpy_d2h_segments(*w["offload"], 0, stream=stream)
+        b.record(stream)
+        b.synchronize()
+        return round(calls * w["bytes"] / (a.elapsed_time(b) * 1e-3) / 1e9, 2)
 
     def prepare(relays):
         """engine config, per-path mode/bandwidth by measurement, warm-up and a device-side
@@ -835,6 +852,17 @@ def main():
             else:
                 mma.calibrate(0, mma.H2D, min(w["bytes"], GiB))
                 mma.calibrate(0, mma.D2H, min(w["bytes"], GiB))
+            if len(mma.get_paths(0, mma.D2H)) == 1 and "fetch" in w and not args.engine_modes:
+                # N = 1 policy (DESIGN 6.1): with one path the copy engine in host-address order
+                # can beat the SM scatter on the offload; the line times the repo's kernel path
+                # (a7/a10) and reports both rates from this run
+                tuned_d2h = mma.get_paths(0, mma.D2H)
+                ce, zc = offload_rate(mma.HOP_CE), offload_rate(mma.HOP_ZC)
+                policy.update({"d2h_single_path": "SM zero-copy scatter (pinned for the line)",
+                               "measured_choice": {1: "ce", 2: "zc"}.get(tuned_d2h[0]["seg_mode"], "?"),
+                               "d2h_ce_host_order_gbps": ce, "d2h_zc_gbps": zc,
+                               "note": "copy-engine batches run in host-address order (cfg.host_order); "
+                                       "--engine-modes times the engine's own measured choice"})
             if len(mma.get_paths(0, mma.H2D)) > 1:
                 # the fallback threshold is the measured native/multipath break-even
                 # (for a contiguous copy; a single path needs none)
@@ -1171,6 +1199,7 @@ def main():
         "clocks": clk,
         "verify": verify,
         "plan": plan_choice,
+        "mode_policy": policy or None,
         "numa": numa_info(torch, sorted(set(path_gpus))),
         "modes": {d: [{"gpu": pi["gpu"], "mode": {0: "auto", 1: "ce", 2: "zc"}.get(
             pi["seg_mode"] if ("fetch" in w and pi["seg_mode"] >= 0) else pi["mode"], "?"),

@@ -110,6 +110,13 @@ typedef struct {
      * Shared host DRAM, switch uplinks or socket links then show up in the vector the
      * planner uses. 0 = solo rates only; default 2. */
     int calib_rounds;
+    /* Host-address order for scattered transfers: each path moves its pieces in ascending
+     * host address instead of table order (the bytes and the chunk -> path plan are
+     * unchanged; only the order of work inside a path's share). Random 32 KiB host writes
+     * cost the copy engine 7% on B200 and, on some hosts, the SM scatter 12%
+     * (profiles/r01_probe_sort.jsonl). 0 = table order, 1 = D2H (default), 2 = both
+     * directions. */
+    int host_order;
 } mma_config_t;
 
 typedef struct {

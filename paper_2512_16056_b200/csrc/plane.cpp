@@ -65,6 +65,7 @@ void apply_env(mma_config_t* c)
     c->claim_bytes = env_size("MMA_CLAIM_BYTES", c->claim_bytes);
     c->zc_ctas = env_int("MMA_ZC_CTAS", c->zc_ctas);
     c->calib_rounds = env_int("MMA_CALIB_ROUNDS", c->calib_rounds);
+    c->host_order = env_int("MMA_HOST_ORDER", c->host_order);
     if (const char* s = getenv("MMA_PATHS")) {   // comma-separated relay GPU ids
         c->npaths = 0;
         for (const char* p = s; *p && c->npaths < MMA_MAX_PATHS;) {
@@ -92,6 +93,7 @@ void defaults(mma_config_t* c)
     c->claim_bytes = 256u << 10;
     c->zc_ctas = kDefaultZcCtas;
     c->calib_rounds = 2;
+    c->host_order = 1;
 }
 
 int validate_cfg(const mma_config_t& c)
@@ -108,7 +110,46 @@ int validate_cfg(const mma_config_t& c)
     if (c.claim_bytes % 16) return cudaErrorInvalidValue;
     if (c.zc_ctas < 0 || c.zc_ctas > 4096) return cudaErrorInvalidValue;
     if (c.calib_rounds < 0 || c.calib_rounds > 16) return cudaErrorInvalidValue;
+    if (c.host_order < 0 || c.host_order > 2) return cudaErrorInvalidValue;
     return cudaSuccess;
+}
+
+// Permutation that orders n keys ascending (stable): LSD radix sort on (key - min) >> 12
+// (4 KiB pages) in 11-bit digits, std::sort below 4096 keys. O(n) per digit; the digit count
+// follows the key range (a few passes for one host pool).
+void order_by_key(const uint64_t* key, size_t n, std::vector<uint32_t>& perm)
+{
+    perm.resize(n);
+    for (size_t i = 0; i < n; i++) perm[i] = (uint32_t)i;
+    if (n < 2) return;
+    if (n < 4096) {
+        std::stable_sort(perm.begin(), perm.end(), [&](uint32_t a, uint32_t b) { return key[a] < key[b]; });
+        return;
+    }
+    uint64_t lo = key[0], hi = key[0];
+    for (size_t i = 1; i < n; i++) {
+        lo = std::min(lo, key[i]);
+        hi = std::max(hi, key[i]);
+    }
+    const uint64_t range = (hi - lo) >> 12;
+    std::vector<uint32_t> tmp(n);
+    std::vector<size_t> cnt(1u << 11);
+    for (int shift = 0; shift < 64 && (range >> shift); shift += 11) {
+        std::fill(cnt.begin(), cnt.end(), 0);
+        for (size_t i = 0; i < n; i++) cnt[(((key[perm[i]] - lo) >> 12) >> shift) & 2047]++;
+        size_t sum = 0;
+        for (auto& c : cnt) { const size_t t = c; c = sum; sum += t; }
+        for (size_t i = 0; i < n; i++) tmp[cnt[(((key[perm[i]] - lo) >> 12) >> shift) & 2047]++] = perm[i];
+        perm.swap(tmp);
+    }
+    // within one 4 KiB page keep ascending addresses too (pieces of a page are few)
+    for (size_t a = 0; a < n;) {
+        size_t b = a + 1;
+        while (b < n && ((key[perm[b]] - lo) >> 12) == ((key[perm[a]] - lo) >> 12)) b++;
+        if (b - a > 1)
+            std::stable_sort(perm.begin() + a, perm.begin() + b, [&](uint32_t x, uint32_t y) { return key[x] < key[y]; });
+        a = b;
+    }
 }
 
 uint64_t zc_grid(int d)
@@ -480,6 +521,7 @@ public:
         make_paths(j_.d);
         ps_ = &t_.paths[j_.dir];
         P_ = (int)ps_->size();
+        host_order_ = !j_.contiguous && (eng_.cfg.host_order == 2 || (eng_.cfg.host_order == 1 && j_.dir == MMA_D2H));
         CK(plan());
         if (plan_.fallback) {
             bool done = false;
@@ -528,6 +570,16 @@ private:
     cudaEvent_t fork_ = nullptr;
     std::vector<std::pair<cudaStream_t, int>> used_;   // engine streams this call enqueued on
     uint8_t* log_ = nullptr;
+    // host-address order (config host_order): a zero-copy path of a scattered transfer gets a
+    // private table of its own pieces sorted by host address, copy-engine batches are sorted
+    bool host_order_ = false;
+    struct Priv {
+        bool on = false;
+        size_t off = 0;          // byte offset of its table in the upload
+        uint64_t npieces = 0, B = 0;
+        std::vector<uint64_t> src, dst, len;
+    };
+    std::vector<Priv> priv_;
 
     PathState& path(int p) { return (*ps_)[p]; }
     Lanes& lanes(int g) { return eng_.dev[g].lane[j_.dir]; }
@@ -582,6 +634,7 @@ private:
         if (small || resolve_mode(j_, pmode_[0]) == MMA_HOP_CE) {
             DmaBatch b;
             j_.pieces(0, j_.B, [&](const Piece& x) { b.add(x.dst, x.src, x.len); });
+            if (!small && host_order_) b.sort_by_host(kind_);   // a one-path plan, not a small copy
             TSpan ts(j_.user_dev, j_.user, "DMA native (fallback)", 0, -1, j_.B);
             CK((cudaError_t)b.issue(kind_, j_.user));
             t_.stats.path_bytes[j_.dir][0] += j_.B;
@@ -637,25 +690,38 @@ private:
         return cudaSuccess;
     }
 
-    // ---- host tables: the segment table and (interleaved plans) the chunk lists, built
-    // only when some kernel reads them (copy-engine-only calls build none)
+    // ---- host tables: the shared segment table and (interleaved plans) the chunk lists,
+    // built only when some kernel reads them (copy-engine-only calls build none), then the
+    // private host-ordered tables of zero-copy paths
     int build_tables()
     {
-        bool any = false;
+        bool shared = false;
+        priv_.assign(P_, Priv());
         for (int p = 0; p < P_; p++) {
             if (!active_[p]) continue;
-            if (mode_[p] == MMA_HOP_ZC) needs_tab_[path(p).gpu] = any = true;
-            else if (path(p).kind == MMA_PATH_RELAY) needs_tab_[j_.dir == MMA_H2D ? j_.d : path(p).gpu] = any = true;
+            if (mode_[p] == MMA_HOP_ZC) {
+                needs_tab_[path(p).gpu] = true;
+                if (host_order_ && !dynamic_) build_private(p);
+                else shared = true;
+            } else if (path(p).kind == MMA_PATH_RELAY) {
+                needs_tab_[j_.dir == MMA_H2D ? j_.d : path(p).gpu] = shared = true;
+            }
         }
-        need_ctab_ = eng_.cfg.plan_mode == PLAN_INTERLEAVED && !dynamic_;
-        const uint64_t seg_words = j_.contiguous ? 0 : (j_.nseg + 1) + 2 * j_.nseg;
-        tab_bytes_ = !any ? 0 : (need_ctab_ ? n_ * 4 : 0) + ((need_ctab_ && (n_ & 1)) ? 4 : 0) + seg_words * 8;
+        need_ctab_ = shared && e_plan_interleaved() && !dynamic_;
+        const uint64_t seg_words = (shared && !j_.contiguous) ? (j_.nseg + 1) + 2 * j_.nseg : 0;
+        size_t bytes = seg_words * 8 + (need_ctab_ ? n_ * 4 + (n_ & 1) * 4 : 0);
+        for (auto& q : priv_)
+            if (q.on) {
+                q.off = bytes;
+                bytes += (3 * q.npieces + 1) * 8;
+            }
+        tab_bytes_ = bytes;
         ctab_off_.assign(P_, 0);
         if (tab_bytes_) {
             CK((cudaError_t)scratch_host(*sc_, tab_bytes_, &htab_));
             char* h = (char*)htab_;
             size_t o = 0;
-            if (!j_.contiguous) {
+            if (seg_words) {
                 uint64_t* w = (uint64_t*)h;
                 memcpy(w, j_.vstart.data(), (j_.nseg + 1) * 8);
                 for (uint64_t k = 0; k < j_.nseg; k++) {
@@ -670,9 +736,55 @@ private:
                     memcpy(h + o, lists_[p].data(), lists_[p].size() * 4);
                     o += lists_[p].size() * 4;
                 }
+            for (auto& q : priv_) {
+                if (!q.on) continue;
+                uint64_t* w = (uint64_t*)(h + q.off);
+                w[0] = 0;
+                for (uint64_t k = 0; k < q.npieces; k++) w[k + 1] = w[k] + q.len[k];
+                memcpy(w + q.npieces + 1, q.src.data(), q.npieces * 8);
+                memcpy(w + 2 * q.npieces + 1, q.dst.data(), q.npieces * 8);
+            }
         }
         tr_.mark("tables");
         return cudaSuccess;
+    }
+
+    bool e_plan_interleaved() const { return eng_.cfg.plan_mode == PLAN_INTERLEAVED; }
+
+    // path p's pieces (the parts of its chunks, in chunk order) reordered by host address:
+    // a private virtual stream of B_p bytes that the path's zero-copy kernel moves alone
+    void build_private(int p)
+    {
+        Priv& q = priv_[p];
+        std::vector<uint64_t> src, dst, len;
+        const auto& L = lists_[p];
+        for (size_t a = 0; a < L.size();) {
+            size_t b = a + 1;
+            while (b < L.size() && L[b] == L[b - 1] + 1) b++;
+            uint64_t o0, l0, o1, l1;
+            j_.extent(L[a], &o0, &l0);
+            j_.extent(L[b - 1], &o1, &l1);
+            j_.pieces(o0, o1 + l1, [&](const Piece& x) {
+                src.push_back((uint64_t)x.src);
+                dst.push_back((uint64_t)x.dst);
+                len.push_back(x.len);
+            });
+            a = b;
+        }
+        std::vector<uint32_t> perm;
+        order_by_key(j_.dir == MMA_D2H ? dst.data() : src.data(), src.size(), perm);
+        q.on = true;
+        q.npieces = src.size();
+        q.src.resize(q.npieces);
+        q.dst.resize(q.npieces);
+        q.len.resize(q.npieces);
+        q.B = 0;
+        for (size_t k = 0; k < perm.size(); k++) {
+            q.src[k] = src[perm[k]];
+            q.dst[k] = dst[perm[k]];
+            q.len[k] = len[perm[k]];
+            q.B += q.len[k];
+        }
     }
 
     // ---- fork (a3): an event on the user stream gates every engine stream the call uses
@@ -734,6 +846,27 @@ private:
             v.start = w;
             v.src = w + j_.nseg + 1;
             v.dst = w + 2 * j_.nseg + 1;
+        }
+        return v;
+    }
+
+    // the private stream of zero-copy path p (build_private) on device g, and its chunks
+    VStreamArg private_stream_on(int p, int g) const
+    {
+        const Priv& q = priv_[p];
+        VStreamArg v{};
+        v.B = q.B;
+        v.C = j_.C;
+        if (q.npieces == 1) {
+            v.nseg = 1;
+            v.src0 = q.src[0];
+            v.dst0 = q.dst[0];
+        } else {
+            const uint64_t* w = (const uint64_t*)((const char*)dtab_[g] + q.off);
+            v.nseg = q.npieces;
+            v.start = w;
+            v.src = w + q.npieces + 1;
+            v.dst = w + 2 * q.npieces + 1;
         }
         return v;
     }
@@ -867,11 +1000,18 @@ private:
         CK((cudaError_t)use(s, g));
         CK((cudaError_t)after_upload(s, g));
         ZcLaunchArg a{};
-        a.v = vstream_on(g);
-        a.chunks = chunks_on(p, g);
+        const bool own = priv_[p].on;
+        if (own) {   // its own host-ordered stream: chunks 0..ceil(B_p/C)-1 of it
+            a.v = private_stream_on(p, g);
+            a.chunks.count = (priv_[p].B + j_.C - 1) / j_.C;
+            a.chunks.first = 0;
+        } else {
+            a.v = vstream_on(g);
+            a.chunks = chunks_on(p, g);
+        }
         a.unit_bytes = eng_.unit_bytes;
         a.path = (uint32_t)p;
-        a.log = log_;
+        a.log = own ? nullptr : log_;
         const uint64_t upc = (j_.C + eng_.unit_bytes - 1) / eng_.unit_bytes;
         const unsigned grid = (unsigned)std::min<uint64_t>(a.chunks.count * upc, zc_grid(g));
         DeviceGuard dg(g);
@@ -881,7 +1021,22 @@ private:
             CK(launch_zc(a, grid, s));
         }
         t_.stats.kernels++;
+        // a private stream's chunks are not v's: the log entries of p's chunks are written
+        // behind the kernel on its stream, as for a copy-engine path
+        if (own && log_) CK(log_runs(p, s));
         if (j_.timing) j_.timing->end(p);
+        return cudaSuccess;
+    }
+
+    int log_runs(int p, cudaStream_t s)
+    {
+        const auto& L = lists_[p];
+        for (size_t a = 0; a < L.size();) {
+            size_t b = a + 1;
+            while (b < L.size() && L[b] == L[b - 1] + 1) b++;
+            CK(cudaMemsetAsync(log_ + L[a], p, b - a, s));
+            a = b;
+        }
         return cudaSuccess;
     }
 
@@ -900,6 +1055,7 @@ private:
             j_.extent(L[b - 1], &o1, &l1);
             DmaBatch batch;
             j_.pieces(o0, o1 + l1, [&](const Piece& x) { batch.add(x.dst, x.src, x.len); });
+            if (host_order_) batch.sort_by_host(kind_);
             {
                 TSpan ts(g, s, "DMA direct", p, L[a], o1 + l1 - o0);
                 CK((cudaError_t)batch.issue(kind_, s));
@@ -1009,6 +1165,7 @@ private:
                               CUDA_SUCCESS)
                 return cudaErrorUnknown;
             j_.pieces(off, off + len, [&](const Piece& x) { batch.add(slot + (x.v - off), x.src, x.len); });
+            if (host_order_) batch.sort_by_host(kind_);
             {
                 TSpan ts(r->relay, hs, "DMA hop 1: host -> relay ring", p, (long long)i, len);
                 CK((cudaError_t)batch.issue(kind_, hs));
@@ -1020,6 +1177,7 @@ private:
             if (eng_.wait64((CUstream)hs, (CUdeviceptr)&r->seq[s], g + 1, CU_STREAM_WAIT_VALUE_GEQ) != CUDA_SUCCESS)
                 return cudaErrorUnknown;
             j_.pieces(off, off + len, [&](const Piece& x) { batch.add(x.dst, slot + (x.v - off), x.len); });
+            if (host_order_) batch.sort_by_host(kind_);
             {
                 TSpan ts(r->relay, hs, "DMA hop 2: relay ring -> host", p, (long long)i, len);
                 CK((cudaError_t)batch.issue(kind_, hs));

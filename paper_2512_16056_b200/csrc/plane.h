@@ -235,6 +235,8 @@ struct Job {
     }
 };
 
+void order_by_key(const uint64_t* key, size_t n, std::vector<uint32_t>& perm);
+
 // Pieces copied by one DMA call: cudaMemcpyAsync for one, cudaMemcpyBatchAsync for many.
 struct DmaBatch {
     std::vector<void*> dst, src;
@@ -249,6 +251,26 @@ struct DmaBatch {
         dst.push_back(d);
         src.push_back(const_cast<void*>(s));
         len.push_back(n);
+    }
+    // issue order = ascending host address (the copies are independent; config host_order)
+    void sort_by_host(cudaMemcpyKind kind)
+    {
+        if (dst.size() < 2) return;
+        const std::vector<void*>& h = kind == cudaMemcpyDeviceToHost ? dst : src;
+        std::vector<uint64_t> key(h.size());
+        for (size_t i = 0; i < h.size(); i++) key[i] = (uint64_t)h[i];
+        std::vector<uint32_t> perm;
+        order_by_key(key.data(), key.size(), perm);
+        std::vector<void*> d2(dst.size()), s2(src.size());
+        std::vector<size_t> l2(len.size());
+        for (size_t i = 0; i < perm.size(); i++) {
+            d2[i] = dst[perm[i]];
+            s2[i] = src[perm[i]];
+            l2[i] = len[perm[i]];
+        }
+        dst.swap(d2);
+        src.swap(s2);
+        len.swap(l2);
     }
     int issue(cudaMemcpyKind kind, cudaStream_t s)
     {

@@ -51,6 +51,7 @@ class Config(C.Structure):
         ("claim_bytes", C.c_size_t),
         ("zc_ctas", C.c_int),
         ("calib_rounds", C.c_int),
+        ("host_order", C.c_int),
     ]
 
 

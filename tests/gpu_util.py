@@ -9,7 +9,7 @@ G = 4096   # guard band bytes on each side of a destination
 
 
 def configure(mma, *, loopback=1, chunk=1 << 20, slots=2, plan_mode=0, hop=(0, 0),
-              thr=0, ctas=8, debug=1, paths=None, claim=None):
+              thr=0, ctas=8, debug=1, paths=None, claim=None, host_order=None):
     cfg = mma.default_config()
     cfg.chunk_bytes[0] = cfg.chunk_bytes[1] = chunk
     cfg.claim_bytes = chunk if claim is None else claim   # dynamic pull claims = chunks
@@ -20,6 +20,8 @@ def configure(mma, *, loopback=1, chunk=1 << 20, slots=2, plan_mode=0, hop=(0, 0
     cfg.hop_mode[0], cfg.hop_mode[1] = hop
     cfg.relay_ctas = ctas
     cfg.debug_log = debug
+    if host_order is not None:
+        cfg.host_order = host_order
     if paths is not None:
         cfg.npaths = len(paths)
         for i, g in enumerate(paths):

@@ -46,12 +46,14 @@ CASES = [
     (512, MiB, 2, 0, 2),         # one-hop zero-copy relays
     (272, 192 << 10, 2, 1, 1),   # chunk not a multiple of the segment: pieces split
     (272, 192 << 10, 1, 1, 2),
+    (2048, MiB, 1, 0, 2),        # 8192 segments: the radix path of the host-order sort
 ]
 
 
+@pytest.mark.parametrize("order", [0, 2], ids=["table_order", "host_order"])
 @pytest.mark.parametrize("tokens,C,lb,mode,hop", CASES)
-def test_kv_fetch_h2d(mma, orc, tokens, C, lb, mode, hop):
-    configure(mma, loopback=lb, chunk=C, slots=2, plan_mode=mode, hop=(hop, hop))
+def test_kv_fetch_h2d(mma, orc, tokens, C, lb, mode, hop, order):
+    configure(mma, loopback=lb, chunk=C, slots=2, plan_mode=mode, hop=(hop, hop), host_order=order)
     bw = [1] * (1 + lb)
     mma.set_bandwidth(0, mma.H2D, bw)
     shape, ho, do, sb, hpool, dbytes = _kv(tokens)
@@ -74,9 +76,12 @@ def test_kv_fetch_h2d(mma, orc, tokens, C, lb, mode, hop):
         assert mma.get_delivery_log(0) == path.tobytes()
 
 
+@pytest.mark.parametrize("order", [0, 1], ids=["table_order", "host_order"])
 @pytest.mark.parametrize("tokens,C,lb,mode,hop", CASES)
-def test_kv_offload_d2h(mma, orc, tokens, C, lb, mode, hop):
-    configure(mma, loopback=lb, chunk=C, slots=2, plan_mode=mode, hop=(hop, hop))
+def test_kv_offload_d2h(mma, orc, tokens, C, lb, mode, hop, order):
+    """host_order 1 (the default) moves each path's pieces in ascending host address: the
+    plan, the bytes and the delivery log must not change."""
+    configure(mma, loopback=lb, chunk=C, slots=2, plan_mode=mode, hop=(hop, hop), host_order=order)
     bw = [1] * (1 + lb)
     mma.set_bandwidth(0, mma.D2H, bw)
     shape, ho, do, sb, hpool, dbytes = _kv(tokens, seed=99)
@@ -93,6 +98,9 @@ def test_kv_offload_d2h(mma, orc, tokens, C, lb, mode, hop):
     exp = np.full(hpool, 0xA5, dtype=np.uint8)
     _oracle_segments(orc, cache_host, exp, do, ho, lens, C, bw, path)
     assert np.array_equal(host.numpy(), exp)
+    if not fb:
+        assert mma.get_delivery_log(0) == path.tobytes()
+    assert mma.get_last_error() == 0
 
 
 def test_irregular_segments(mma, orc):
