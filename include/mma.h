@@ -297,6 +297,26 @@ int mma_copy_claim_segments(const mma_segment_t* segs, size_t nsegs, size_t clai
                             uint64_t* cursor, uint64_t* counts, int path, int device,
                             mma_stream_t stream);
 
+/*
+ * Cross-process backlog ledger (SURVEY NEXT-4 "a shared-memory path ledger"; §5.1.2:
+ * one multipath queue per process). mma_ledger_attach(name) maps the POSIX shared-memory
+ * object /mma_ledger_<name> (created on first use, all-zero = empty); from then on every call
+ * of this process adds its per-link bytes to it until the call completes, and every plan uses
+ * the bytes all attached processes have queued on each link as the backlog (and skips a relay
+ * whose own target's direct bytes are in flight). Attach before the first copy.
+ * name = NULL or "" detaches. MMA_LEDGER_SHM=<name> attaches at init. Links are keyed by PCI
+ * bus id, so processes with different CUDA_VISIBLE_DEVICES agree. A process that dies with
+ * calls in flight leaves its bytes counted: mma_ledger_unlink removes the object.
+ * mma_ledger_shared_add / _get read or adjust one link's counters directly (bus id as from
+ * cudaDeviceGetPCIBusId), for schedulers outside the engine and for tests. Host-only.
+ */
+int mma_ledger_attach(const char* name);
+int mma_ledger_unlink(const char* name);
+int mma_ledger_shared_add(const char* bus_id, int dir, int64_t bytes, int64_t own);
+int mma_ledger_shared_get(const char* bus_id, int dir, uint64_t* bytes, uint64_t* own);
+/* PCI bus id of a device ("dddd:bb:dd.f", as cudaDeviceGetPCIBusId) for the calls above. */
+int mma_device_bus_id(int device, char* buf, int len);
+
 /* Timeline tracing: while active, every DMA and kernel the engine enqueues is bracketed by
  * CUDA events on its stream; mma_trace_end synchronises, writes the spans as a Chrome trace
  * JSON (one row per GPU and engine stream) to json_path (NULL: discard) and reports their

@@ -24,6 +24,7 @@ SOURCES = [
     CSRC / "trace.cpp",
     CSRC / "planner.cpp",
     CSRC / "hostmem.cpp",
+    CSRC / "ledger_shm.cpp",
     CSRC / "kernels" / "relay.cu",
     CSRC / "kernels" / "zerocopy.cu",
     CSRC / "kernels" / "verify.cu",

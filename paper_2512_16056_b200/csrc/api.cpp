@@ -227,6 +227,7 @@ int mma_finalize(void)
     }
     for (auto& kv : e.join_ev) cudaEventDestroy(kv.second);
     e.join_ev.clear();
+    ledger_retire();   // every call has completed: their bytes leave the (shared) ledger
     for (auto& f : e.inflight) cudaEventDestroy(f.done);
     for (auto& f : e.free_events) cudaEventDestroy(f.second);
     e.inflight.clear();

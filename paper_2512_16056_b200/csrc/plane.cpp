@@ -228,6 +228,7 @@ int do_init(const mma_config_t* cfg)
     for (int d = 0; d < e.ndev; d++) e.tgt[d].paths_made = false;   // re-derive path sets
     e.inited = true;
     if (const char* cal = getenv("MMA_CALIB")) load_calibration_locked(cal, nullptr);
+    if (const char* led = getenv("MMA_LEDGER_SHM")) mma_ledger_attach(led);
     return cudaSuccess;
 }
 
@@ -424,7 +425,7 @@ static int resolve_mode(const Job& j, int mode)
 }
 
 // ---- backlog ledger (NEXT-1) ---------------------------------------------------------
-static void ledger_retire()
+void ledger_retire()
 {
     Engine& e = E();
     for (size_t i = 0; i < e.inflight.size();) {
@@ -434,6 +435,8 @@ static void ledger_retire()
         for (int g = 0; g < MMA_MAX_GPUS; g++) {
             e.ledger[f.dir][g] -= f.bytes[g];
             e.ledger_own[f.dir][g] -= f.own[g];
+            if (f.shared && (f.bytes[g] || f.own[g]))
+                shm_ledger_add(f.dir, g, -(int64_t)f.bytes[g], -(int64_t)f.own[g]);
         }
         e.free_events.push_back({f.dev, f.done});
         e.inflight[i] = e.inflight.back();
@@ -462,6 +465,11 @@ static int ledger_add(int dir, int user_dev, cudaStream_t user, const uint64_t* 
         e.ledger[dir][k] += bytes[k];
         e.ledger_own[dir][k] += own[k];
     }
+    // with a cross-process ledger attached, every process plans against every process's bytes
+    f.shared = shm_ledger_on();
+    if (f.shared)
+        for (int k = 0; k < MMA_MAX_GPUS; k++)
+            if (bytes[k] || own[k]) shm_ledger_add(dir, k, (int64_t)bytes[k], (int64_t)own[k]);
     e.inflight.push_back(f);
     return cudaSuccess;
 }
@@ -473,12 +481,15 @@ void ledger_inputs(int d, int dir, const std::vector<PathState>& ps, std::vector
     Engine& e = E();
     if (!e.cfg.ledger) return;
     ledger_retire();
+    const bool shared = shm_ledger_on();
     for (size_t p = 0; p < ps.size(); p++) {
         const int g = ps[p].gpu;
-        pp[p].backlog = e.ledger[dir][g];
+        uint64_t bytes = e.ledger[dir][g], own = e.ledger_own[dir][g];
+        if (shared) shm_ledger_get(dir, g, &bytes, &own);   // includes this process's bytes
+        pp[p].backlog = bytes;
         // direct path first: a GPU whose link still carries its own target's bytes takes
         // no relay work for another target
-        if (ps[p].kind == MMA_PATH_RELAY && g != d && e.ledger_own[dir][g] > 0) pp[p].mbps = 0;
+        if (ps[p].kind == MMA_PATH_RELAY && g != d && own > 0) pp[p].mbps = 0;
     }
 }
 

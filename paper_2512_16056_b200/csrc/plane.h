@@ -145,6 +145,7 @@ struct Engine {
         int dev, dir;
         uint64_t bytes[MMA_MAX_GPUS];
         uint64_t own[MMA_MAX_GPUS];
+        bool shared;                 // also entered in the cross-process ledger
     };
     std::vector<InFlight> inflight;
     std::vector<std::pair<int, cudaEvent_t>> free_events;
@@ -305,6 +306,11 @@ void make_paths(int d);
 void free_ring(Ring& r);
 int get_ring(int d, int dir, int p, uint64_t C, uint32_t S, Ring** out);
 void ledger_inputs(int d, int dir, const std::vector<PathState>& ps, std::vector<PlanPath>& pp);
+void ledger_retire();
+// ---- ledger_shm.cpp: the cross-process ledger (mma_ledger_attach)
+bool shm_ledger_on();
+void shm_ledger_add(int dir, int dev, int64_t bytes, int64_t own);
+void shm_ledger_get(int dir, int dev, uint64_t* bytes, uint64_t* own);
 int run_job(Job& j);
 int reserve_tables(const Job& j);
 int sticky();

@@ -30,7 +30,8 @@ SYMBOLS = [
     "mma_shared_host_alloc", "mma_shared_host_free", "mma_ipc_export", "mma_ipc_open", "mma_ipc_close",
     "mma_copy_share_segments", "mma_copy_claim_segments", "mma_trace_begin", "mma_trace_end",
     "mma_save_calibration", "mma_load_calibration", "mma_host_alloc_for", "mma_host_page_node",
-    "mma_get_calibration", "mma_tune_threshold",
+    "mma_get_calibration", "mma_tune_threshold", "mma_ledger_attach", "mma_ledger_unlink",
+    "mma_ledger_shared_add", "mma_ledger_shared_get", "mma_device_bus_id",
 ]
 
 
@@ -112,6 +113,11 @@ def lib():
         L.mma_tune_segments.argtypes = [C.POINTER(Segment), sz, C.c_int, C.c_int, vp, C.c_int]
         L.mma_kernel_times.argtypes = [vp, vp, sz, C.POINTER(sz)]
         L.mma_get_segment_tuning.argtypes = [C.c_int, C.c_int, vp, vp, C.c_int, C.POINTER(C.c_int)]
+        L.mma_ledger_attach.argtypes = [C.c_char_p]
+        L.mma_device_bus_id.argtypes = [C.c_int, C.c_char_p, C.c_int]
+        L.mma_ledger_unlink.argtypes = [C.c_char_p]
+        L.mma_ledger_shared_add.argtypes = [C.c_char_p, C.c_int, C.c_int64, C.c_int64]
+        L.mma_ledger_shared_get.argtypes = [C.c_char_p, C.c_int, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]
         L.mma_tune_threshold.argtypes = [C.c_int, C.c_int, sz, C.POINTER(sz), C.POINTER(C.c_int)]
         L.mma_get_calibration.argtypes = [C.c_int, C.c_int, C.c_int, vp, vp, C.c_int, C.POINTER(C.c_int)]
         L.mma_get_dynamic_counts.argtypes = [C.c_int, vp, C.c_int, C.POINTER(C.c_int)]
@@ -264,6 +270,33 @@ def tune_threshold(device: int, direction: int, max_bytes: int = 256 << 20):
     _check(lib().mma_tune_threshold(device, direction, max_bytes, C.byref(thr), C.byref(found)),
            "mma_tune_threshold")
     return int(thr.value), bool(found.value)
+
+
+def ledger_attach(name: str | None) -> None:
+    """Attach this process's engine to the cross-process ledger `name` (None detaches)."""
+    _check(lib().mma_ledger_attach(name.encode() if name else None), "mma_ledger_attach")
+
+
+def device_bus_id(device: int) -> str:
+    buf = C.create_string_buffer(64)
+    _check(lib().mma_device_bus_id(device, buf, 64), "mma_device_bus_id")
+    return buf.value.decode()
+
+
+def ledger_unlink(name: str) -> None:
+    _check(lib().mma_ledger_unlink(name.encode()), "mma_ledger_unlink")
+
+
+def ledger_shared_add(bus_id: str, direction: int, nbytes: int, own: int = 0) -> None:
+    _check(lib().mma_ledger_shared_add(bus_id.encode(), direction, nbytes, own), "mma_ledger_shared_add")
+
+
+def ledger_shared_get(bus_id: str, direction: int):
+    """(bytes, own) queued on the link of the GPU with this PCI bus id, all processes."""
+    b, o = C.c_uint64(), C.c_uint64()
+    _check(lib().mma_ledger_shared_get(bus_id.encode(), direction, C.byref(b), C.byref(o)),
+           "mma_ledger_shared_get")
+    return int(b.value), int(o.value)
 
 
 def get_calibration(device: int, direction: int, scattered: bool = False):

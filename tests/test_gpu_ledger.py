@@ -90,3 +90,67 @@ def test_new_ring_does_not_wait_on_user_work(mma):
     assert enqueue_s < 0.4, enqueue_s
     assert torch.equal(dst.cpu(), src[:B])
     assert mma.get_stats(0)["relay_bytes"] > 0
+
+
+def test_shared_ledger_backlog_from_another_process(mma, orc):
+    """Cross-process ledger (NEXT-4): bytes another process has queued on a link (entered
+    here through mma_ledger_shared_add, as that process's engine would) become the backlog
+    of this process's plan; removing them restores the idle plan."""
+    import os
+    name = f"gpu{os.getpid()}"
+    mma.finalize()
+    mma.ledger_attach(name)
+    try:
+        C = MiB
+        configure(mma, loopback=1, chunk=C, plan_mode=1, hop=(1, 1), debug=0)
+        bw = [3, 1]
+        mma.set_bandwidth(0, mma.H2D, bw)
+        B = 8 * C
+        rc, idle_plan, _, _ = orc.plan(bw, B, C, 0, 1)
+        assert mma.get_plan(0, mma.H2D, B)[0] == idle_plan.tobytes()
+        bus = mma.device_bus_id(0)
+        Ba = 24 * MiB
+        mma.ledger_shared_add(bus, mma.H2D, Ba, 0)
+        rc, exp, _, _ = orc.plan(bw, B, C, 0, 1, backlog=[Ba, Ba])    # both paths are GPU 0's link
+        assert mma.get_plan(0, mma.H2D, B)[0] == exp.tobytes() != idle_plan.tobytes()
+        mma.ledger_shared_add(bus, mma.H2D, -Ba, 0)
+        assert mma.get_plan(0, mma.H2D, B)[0] == idle_plan.tobytes()
+    finally:
+        mma.finalize()
+        mma.ledger_attach(None)
+        mma.ledger_unlink(name)
+
+
+def test_engine_calls_enter_the_shared_ledger(mma):
+    """A call in flight is visible in the shared ledger with its per-link bytes (all of it on
+    GPU 0's link here, the direct share as `own`) and leaves it once it has completed."""
+    import os
+    name = f"gpu{os.getpid()}b"
+    mma.finalize()
+    mma.ledger_attach(name)
+    try:
+        C = MiB
+        configure(mma, loopback=1, chunk=C, plan_mode=1, hop=(1, 1), debug=0)
+        mma.set_bandwidth(0, mma.H2D, [3, 1])
+        bus = mma.device_bus_id(0)
+        Ba = 24 * MiB
+        src = pinned(torch, Ba, seed=5)
+        dst = torch.empty(Ba, dtype=torch.uint8, device="cuda")
+        s = torch.cuda.Stream()
+        mma.memcpy_h2d(dst, src, Ba, stream=s)      # rings and tables exist from here on
+        s.synchronize()
+        mma.get_plan(0, mma.H2D, Ba)                # retires the completed call
+        assert mma.ledger_shared_get(bus, mma.H2D) == (0, 0)
+        with torch.cuda.stream(s):
+            torch.cuda._sleep(2_000_000_000)
+            mma.memcpy_h2d(dst, src, Ba, stream=s)
+        got = mma.ledger_shared_get(bus, mma.H2D)
+        assert got == (Ba, 18 * MiB), got          # plan 3:1 -> 18 MiB on the direct path
+        s.synchronize()
+        mma.get_plan(0, mma.H2D, Ba)
+        assert mma.ledger_shared_get(bus, mma.H2D) == (0, 0)
+        assert torch.equal(dst.cpu(), src[:Ba])
+    finally:
+        mma.finalize()
+        mma.ledger_attach(None)
+        mma.ledger_unlink(name)
