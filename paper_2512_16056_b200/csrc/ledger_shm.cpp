@@ -90,6 +90,20 @@ void shm_ledger_add(int dir, int dev, int64_t bytes, int64_t own)
     g_shm->own[dir][s].fetch_add((uint64_t)own, std::memory_order_relaxed);
 }
 
+int shm_ledger_slot(int dev)
+{
+    std::lock_guard<std::mutex> g(g_mu);
+    return g_shm ? slot_of_device(dev) : -1;
+}
+
+void shm_ledger_add_slot(int dir, int slot, int64_t bytes, int64_t own)
+{
+    std::lock_guard<std::mutex> g(g_mu);
+    if (!g_shm || slot < 0 || slot >= MMA_MAX_GPUS) return;
+    g_shm->bytes[dir][slot].fetch_add((uint64_t)bytes, std::memory_order_relaxed);
+    g_shm->own[dir][slot].fetch_add((uint64_t)own, std::memory_order_relaxed);
+}
+
 void shm_ledger_get(int dir, int dev, uint64_t* bytes, uint64_t* own)
 {
     std::lock_guard<std::mutex> g(g_mu);

@@ -81,6 +81,36 @@ int vstream_from(const mma_segment_t* segs, size_t nsegs, uint64_t C, cudaStream
     return cudaSuccess;
 }
 
+// Multi-process shares enter the cross-process ledger (mma_ledger_attach) while queued: the
+// bytes are added at enqueue and removed by a host function on the stream once the kernel
+// has run (the function makes no CUDA call: the ledger slot is resolved here).
+struct LedgerRelease {
+    int dir, slot;
+    int64_t bytes, own;
+};
+
+void CUDART_CB release_share(void* p)
+{
+    LedgerRelease* r = (LedgerRelease*)p;
+    shm_ledger_add_slot(r->dir, r->slot, -r->bytes, -r->own);
+    delete r;
+}
+
+int ledger_share(const mma_segment_t* segs, int device, uint64_t bytes, bool own, cudaStream_t s)
+{
+    const int slot = shm_ledger_slot(device);
+    if (slot < 0 || !bytes) return cudaSuccess;
+    cudaPointerAttributes a;
+    int dir = MMA_H2D;
+    if (cudaPointerGetAttributes(&a, segs[0].src) == cudaSuccess && a.type == cudaMemoryTypeDevice) dir = MMA_D2H;
+    cudaGetLastError();
+    LedgerRelease* r = new LedgerRelease{dir, slot, (int64_t)bytes, own ? (int64_t)bytes : 0};
+    shm_ledger_add_slot(dir, slot, r->bytes, r->own);
+    const cudaError_t e = cudaLaunchHostFunc(s, release_share, r);
+    if (e != cudaSuccess) release_share(r);
+    return (int)e;
+}
+
 }  // namespace
 
 }  // namespace mma
@@ -214,6 +244,11 @@ int mma_copy_share_segments(const mma_segment_t* segs, size_t nsegs, size_t chun
             KTimer kt(device, s, 0 | (path << 8));
             rc = launch_zc(a, grid, s);
             cudaFreeAsync(dlist, s);
+        }
+        if (rc == cudaSuccess) {   // this share's bytes, queued on this GPU's link
+            uint64_t mine_bytes = 0;
+            for (uint32_t i : mine) mine_bytes += std::min<uint64_t>(v.C, v.B - (uint64_t)i * v.C);
+            rc = ledger_share(segs, device, mine_bytes, path == 0, s);
         }
     }
     if (dtab) cudaFreeAsync(dtab, s);

@@ -311,6 +311,8 @@ void ledger_retire();
 bool shm_ledger_on();
 void shm_ledger_add(int dir, int dev, int64_t bytes, int64_t own);
 void shm_ledger_get(int dir, int dev, uint64_t* bytes, uint64_t* own);
+int shm_ledger_slot(int dev);   // -1 when detached; resolves the bus id (a CUDA call)
+void shm_ledger_add_slot(int dir, int slot, int64_t bytes, int64_t own);   // no CUDA calls
 int run_job(Job& j);
 int reserve_tables(const Job& j);
 int sticky();

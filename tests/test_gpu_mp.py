@@ -65,7 +65,28 @@ if rank == 0:
     counts = ctr.cpu().tolist()
     res["claims"] = counts[1:3]; res["nclaims"] = (B + (256 << 10) - 1) // (256 << 10)
     res["err"] = mma.get_last_error()
+dist.barrier()
+# cross-process ledger: rank 1's share, held behind a sleeping kernel, is visible to rank 0
+led = "mpled_" + os.environ["MASTER_PORT"]
+mma.ledger_attach(led)
+bus = mma.device_bus_id(0)
+if rank == 1:
+    with torch.cuda.stream(s):
+        torch.cuda._sleep(1_500_000_000)
+    mma.copy_share_segments(segs, n, C, path, 1, 0, stream=s)
+dist.barrier()
+if rank == 0:
+    res["ledger_in_flight"] = list(mma.ledger_shared_get(bus, mma.H2D))
+    res["share1_bytes"] = sum(min(C, B - i * C) for i in range(len(path)) if path[i] == 1)
+dist.barrier()
+s.synchronize(); dist.barrier()
+if rank == 0:
+    res["ledger_after"] = list(mma.ledger_shared_get(bus, mma.H2D))
     print(json.dumps(res), flush=True)
+dist.barrier()
+mma.ledger_attach(None)
+if rank == 0:
+    mma.ledger_unlink(led)
 dist.barrier()
 if rank == 1:
     mma.ipc_close(dptr); mma.ipc_close(cptr); mma.shared_host_free(pool)
@@ -95,3 +116,5 @@ def test_two_processes_share_a_transfer(tmp_path):
     r = json.loads(outs[0][0].strip().splitlines()[-1])
     assert r["planned_mismatch"] == 0 and r["dynamic_mismatch"] == 0 and r["err"] == 0
     assert sum(r["claims"]) == r["nclaims"]
+    assert r["ledger_in_flight"] == [r["share1_bytes"], 0] and r["share1_bytes"] > 0   # a relay share: not own
+    assert r["ledger_after"] == [0, 0]
