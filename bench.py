@@ -914,6 +914,7 @@ def main():
         cfg, verify = prepare([])
     paths = mma.get_paths(0, mma.H2D)
     path_gpus = [p["gpu"] for p in paths]
+    fallback_cfg = {"h2d": int(cfg.fallback_bytes[0]), "d2h": int(cfg.fallback_bytes[1])}
     tuned = {"h2d": mma.get_paths(0, mma.H2D), "d2h": mma.get_paths(0, mma.D2H)}
     # each path's rate alone (mode choice) and with every path active (planner)
     calib = {d: mma.get_calibration(0, dv, scattered="fetch" in w)
@@ -1179,7 +1180,7 @@ def main():
         "config": {"workload": w["desc"], "paths": k, "path_gpus": path_gpus, "target_gpu": 0,
                    "chunk_bytes": int(cfg.chunk_bytes[0]), "claim_bytes": int(cfg.claim_bytes), "hop": {0: "auto", 1: "ce", 2: "zc"}[args.hop],
                    "bytes_per_step": nbytes_step,
-                   "fallback_bytes": thresholds or {"h2d": int(cfg.fallback_bytes[0]), "d2h": int(cfg.fallback_bytes[1])},
+                   "fallback_bytes": thresholds or fallback_cfg,
                    "fallback_how": "measured break-even (mma_tune_threshold)" if thresholds else "default (2 chunks)", "l2": f"inputs ({w['bytes'] / GiB:.1f} GiB per direction) exceed the 126 MB L2; no flush",
                    "parallelism": f"1 process drives {k} path GPU(s); torchrun ranks>0 idle on gloo",
                    "visible_devices": vis_note, "multipath_error": multipath_error},

@@ -105,7 +105,9 @@ static int tune_paths(Job proto, int reps, std::vector<uint32_t>& mbps, std::vec
             }
             const float eff_ms = std::max(best, best_issue * (float)P);
             const float rate = best < 1e29f ? (float)((double)proto.B / (eff_ms * 1e-3) / 1e6) : 0.f;
-            if (rate > best_rate) {
+            // SM zero-copy must beat the copy engine by 2%: on a near-tie the path keeps its SMs
+            // free (§3.4.3) and the run-to-run noise of one timed call cannot flip it
+            if (rate > best_rate * (m == MMA_HOP_ZC ? 1.02f : 1.0f)) {
                 best_rate = rate;
                 modes[p] = m;
                 mbps[p] = (uint32_t)llround(rate);
