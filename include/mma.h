@@ -146,8 +146,17 @@ int mma_finalize(void);
  * before completion. The GPU is the one owning the device pointer (not the current
  * device). H2D: dst is device memory, src host memory; D2H the reverse. bytes = 0 is a
  * no-op. Falls back to the native single-path copy (byte-identical by definition) when
- * bytes < fallback threshold, host memory is pageable, the stream is capturing, or the
- * target has a single path (§3.2).
+ * bytes < fallback threshold, host memory is pageable, or the target has a single path
+ * (§3.2).
+ * Graph capture: a call on a stream being captured is recorded as a replayable multipath
+ * copy -- zero-copy paths and the direct copy engine (relay rings and the backlog ledger
+ * stay out: ring sequence numbers advance per call), tables in a pinned arena made at init
+ * (MMA_GRAPH_ARENA bytes, default 16 MiB; when full, the native copy is captured) and on the
+ * device as graph allocations. The engine must have made a copy on that device before the
+ * capture (nothing may be allocated while capturing); else the native copy is captured.
+ * While such a capture is open, other threads must not make multipath calls (the engine's
+ * streams are part of it). Graphs holding captured copies must not be replayed after
+ * mma_finalize.
  * Errors: cudaErrorInvalidValue (null pointer with bytes > 0, wrong memory kinds),
  * cudaErrorInvalidDevice, or the CUDA error of an enqueue.
  */

@@ -10,6 +10,12 @@ namespace mma {
 
 static int stream_device(cudaStream_t s, int* dev)
 {
+    // cudaStreamGetDevice invalidates a capture in progress on s (either capture mode,
+    // profiles/r01_probe_capture_calls.txt): a capturing stream is taken to be on the
+    // current device, where torch.cuda.graph and cudaStreamBeginCapture users create it
+    cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+    if (cudaStreamIsCapturing(s, &cap) == cudaSuccess && cap != cudaStreamCaptureStatusNone) return cudaGetDevice(dev);
+    cudaGetLastError();
     cudaError_t e = cudaStreamGetDevice(s, dev);
     if (e != cudaSuccess) { cudaGetLastError(); return cudaGetDevice(dev); }
     return cudaSuccess;
@@ -26,8 +32,37 @@ static int classify(const void* p, int* dev, bool* mapped)
     return 2;
 }
 
+// Capture status of the user stream. A captured call may not initialise anything (the
+// engine, a device's streams, the graph arena): those are made by an uncaptured call first,
+// else the copy is the native one. Returns 1 = capture the multipath copy, 0 = not
+// capturing, -1 = capturing but not ready (native copy).
+static int capture_state(cudaStream_t stream, int d)
+{
+    cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+    if (cudaStreamIsCapturing(stream, &cap) != cudaSuccess) {
+        cudaGetLastError();
+        return -1;
+    }
+    if (cap == cudaStreamCaptureStatusNone) return 0;
+    if (cap != cudaStreamCaptureStatusActive) return -1;
+    Engine& e = E();
+    if (!e.inited || !e.arena || d < 0 || d >= e.ndev) return -1;
+    make_paths(d);
+    for (int dir = 0; dir < 2; dir++)
+        for (const PathState& p : e.tgt[d].paths[dir])
+            if (!e.dev[p.gpu].made) return -1;
+    return 1;
+}
+
 static int copy_contiguous(int dir, void* dst, const void* src, size_t bytes, cudaStream_t stream)
 {
+    {   // the first call of a process must not initialise inside a capture
+        cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+        if (!E().inited && cudaStreamIsCapturing(stream, &cap) == cudaSuccess && cap != cudaStreamCaptureStatusNone)
+            return (int)cudaMemcpyAsync(dst, src, bytes, dir == MMA_H2D ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToHost,
+                                        stream);
+        cudaGetLastError();
+    }
     CK((cudaError_t)ensure_init());
     if (int se = sticky()) return se;
     if (bytes == 0) return cudaSuccess;
@@ -41,11 +76,12 @@ static int copy_contiguous(int dir, void* dst, const void* src, size_t bytes, cu
     const int hk = classify(hptr, &hd, &mapped);
     if (hk == 1) return cudaErrorInvalidValue;   // device -> device is not this API
     const cudaMemcpyKind kind = (dir == MMA_H2D) ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToHost;
-    cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
-    cudaStreamIsCapturing(stream, &cap);
-    if (hk == 2 || cap != cudaStreamCaptureStatusNone || d >= e.ndev)
-        return (int)cudaMemcpyAsync(dst, src, bytes, kind, stream);   // native (R7)
+    if (hk == 2 || d >= e.ndev) return (int)cudaMemcpyAsync(dst, src, bytes, kind, stream);   // native (R7)
+    std::lock_guard<std::mutex> g(e.mu);
+    const int cs = capture_state(stream, d);
+    if (cs < 0) return (int)cudaMemcpyAsync(dst, src, bytes, kind, stream);   // native (R7)
     Job j;
+    j.capturing = cs == 1;
     j.dir = dir;
     j.d = d;
     j.user = stream;
@@ -56,8 +92,7 @@ static int copy_contiguous(int dir, void* dst, const void* src, size_t bytes, cu
     j.src0 = (const char*)src;
     j.dst0 = (char*)dst;
     j.mapped = mapped;
-    std::lock_guard<std::mutex> g(e.mu);
-    CK((cudaError_t)make_device(d));
+    if (!j.capturing) CK((cudaError_t)make_device(d));
     return run_job(j);
 }
 
@@ -130,8 +165,23 @@ int prepare_segments(int dir, const mma_segment_t* segs, size_t nsegs, int devic
     return cudaSuccess;
 }
 
+// the native form of a segment table: one cudaMemcpyAsync per segment (capturable)
+static int native_segments(int dir, const mma_segment_t* segs, size_t nsegs, cudaStream_t stream)
+{
+    const cudaMemcpyKind kind = dir == MMA_H2D ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToHost;
+    for (size_t k = 0; k < nsegs; k++)
+        if (segs[k].bytes) CK(cudaMemcpyAsync(segs[k].dst, segs[k].src, segs[k].bytes, kind, stream));
+    return cudaSuccess;
+}
+
 static int copy_segments(int dir, const mma_segment_t* segs, size_t nsegs, int device, cudaStream_t stream)
 {
+    {   // the first call of a process must not initialise inside a capture
+        cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+        if (!E().inited && cudaStreamIsCapturing(stream, &cap) == cudaSuccess && cap != cudaStreamCaptureStatusNone)
+            return (nsegs && !segs) ? cudaErrorInvalidValue : native_segments(dir, segs, nsegs, stream);
+        cudaGetLastError();
+    }
     CK((cudaError_t)ensure_init());
     if (int se = sticky()) return se;
     Engine& e = E();
@@ -142,7 +192,10 @@ static int copy_segments(int dir, const mma_segment_t* segs, size_t nsegs, int d
     CK(prepare_segments(dir, segs, nsegs, device, stream, j));
     if (j.B == 0) return cudaSuccess;
     std::lock_guard<std::mutex> g(e.mu);
-    CK((cudaError_t)make_device(device));
+    const int cs = capture_state(stream, device);
+    if (cs < 0) return native_segments(dir, segs, nsegs, stream);
+    j.capturing = cs == 1;
+    if (!j.capturing) CK((cudaError_t)make_device(device));
     return run_job(j);
 }
 
@@ -246,10 +299,13 @@ int mma_finalize(void)
             cudaStreamDestroy(l.zc);
         }
         cudaEventDestroy(r.fork);
+        cudaEventDestroy(r.cap_ev);
         cudaStreamDestroy(r.setup);
         r = DevRes();
     }
     if (e.err) { cudaFreeHost(e.err); e.err = nullptr; }
+    if (e.arena) { cudaFreeHost(e.arena); e.arena = nullptr; }   // graphs with captured copies die with it
+    e.arena_used = e.arena_cap = 0;
     e.inited = false;
     return cudaSuccess;
 }

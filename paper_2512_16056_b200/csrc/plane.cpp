@@ -160,6 +160,8 @@ uint64_t zc_grid(int d)
     return std::min(want, cap);
 }
 
+static cudaEvent_t join_event(cudaStream_t s, int dev);
+
 // Streams, peer access and flags for device d (lazily, once).
 int make_device(int d)
 {
@@ -179,7 +181,12 @@ int make_device(int d)
         CK(cudaStreamCreateWithPriority(&l.zc, cudaStreamNonBlocking, hi));
     }
     CK(cudaEventCreateWithFlags(&r.fork, cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&r.cap_ev, cudaEventDisableTiming));
     CK(cudaStreamCreateWithFlags(&r.setup, cudaStreamNonBlocking));
+    // join events exist before any call: a captured call may not create one
+    for (Lanes& l : r.lane)
+        for (cudaStream_t s : {l.kern, l.hop[0], l.hop[1], l.direct, l.zc})
+            if (!join_event(s, d)) return cudaErrorMemoryAllocation;
     CK(cudaDeviceGetAttribute(&r.sms, cudaDevAttrMultiProcessorCount, d));
     for (int p = 0; p < e.ndev; p++) {
         if (p == d || !e.p2p[d][p]) continue;
@@ -218,6 +225,9 @@ int do_init(const mma_config_t* cfg)
             e.write64 = (PFN_memop64)fn;
         CK(cudaHostAlloc((void**)&e.err, sizeof(int) * 16, cudaHostAllocPortable | cudaHostAllocMapped));
         memset(e.err, 0, sizeof(int) * 16);
+        e.arena_cap = env_size("MMA_GRAPH_ARENA", 16u << 20);
+        e.arena_used = 0;
+        if (e.arena_cap) CK(cudaHostAlloc((void**)&e.arena, e.arena_cap, cudaHostAllocPortable));
         e.timeout_ns = (uint64_t)env_size("MMA_SPIN_TIMEOUT_MS", 20000) * 1000000ull;
         e.unit_bytes = (uint32_t)env_size("MMA_UNIT_BYTES", kDefaultUnit);
         const char* f = getenv("MMA_FAULT_DROP_PUBLISH");
@@ -415,6 +425,7 @@ int reserve_tables(const Job& j)
 // the kernel is launched on (mma_set_kernel_timing / mma_kernel_times).
 std::vector<KRec> g_kpending;
 bool g_ktime = false;
+thread_local bool tl_capturing = false;
 std::mutex g_kmu;
 
 static int resolve_mode(const Job& j, int mode)
@@ -498,9 +509,16 @@ struct Trace {
     bool on;
     std::chrono::steady_clock::time_point last;
     std::string s;
+    bool cap_debug = getenv("MMA_CAPTURE_DEBUG") != nullptr;
+    cudaStream_t cap_stream = nullptr;
     Trace() : on(getenv("MMA_TRACE") != nullptr), last(std::chrono::steady_clock::now()) {}
     void mark(const char* what)
     {
+        if (cap_debug) {   // MMA_CAPTURE_DEBUG: the capture status of the user stream per stage
+            cudaStreamCaptureStatus st = cudaStreamCaptureStatusNone;
+            cudaStreamIsCapturing(cap_stream, &st);
+            fprintf(stderr, "[mma capture] after %s: status %d\n", what, (int)st);
+        }
         if (!on) return;
         auto now = std::chrono::steady_clock::now();
         char buf[64];
@@ -529,6 +547,12 @@ public:
     int run()
     {
         t0_ = std::chrono::steady_clock::now();
+        struct CaptureFlag {   // no timing / trace events inside a capture
+            explicit CaptureFlag(bool on) { tl_capturing = on; }
+            ~CaptureFlag() { tl_capturing = false; }
+        } cflag(j_.capturing);
+        tr_.cap_stream = j_.user;
+        tr_.mark("start");
         make_paths(j_.d);
         ps_ = &t_.paths[j_.dir];
         P_ = (int)ps_->size();
@@ -540,7 +564,14 @@ public:
             if (done) return finish();
         }
         CK(prepare());
-        CK(build_tables());
+        const int tb = build_tables();
+        if (tb == kArenaFull) {   // a captured call whose tables do not fit: the native copy
+            bool done = false;
+            thr_ = ~0ull;
+            CK(native_fallback(&done));
+            return finish();
+        }
+        CK(tb);
         CK(fork());
         CK(upload_tables());
         CK(delivery_log());
@@ -591,6 +622,7 @@ private:
         std::vector<uint64_t> src, dst, len;
     };
     std::vector<Priv> priv_;
+    static constexpr int kArenaFull = -1000;
 
     PathState& path(int p) { return (*ps_)[p]; }
     Lanes& lanes(int g) { return eng_.dev[g].lane[j_.dir]; }
@@ -627,7 +659,15 @@ private:
             if (j_.mode_override) pmode_[p] = j_.mode_override[p];
         }
         thr_ = j_.no_small_fallback ? 0 : eng_.cfg.fallback_bytes[j_.dir];
-        if (!j_.bw_override) ledger_inputs(j_.d, j_.dir, *ps_, pp_);
+        if (j_.capturing) {
+            // a graph replays this call any number of times: relay rings (whose sequence
+            // numbers advance per call) and the ledger (which retires calls by events) stay
+            // out; zero-copy paths and the direct copy engine replay as they are
+            for (int p = 0; p < P_; p++)
+                if (path(p).kind == MMA_PATH_RELAY && resolve_mode(j_, pmode_[p]) == MMA_HOP_CE) pp_[p].mbps = 0;
+        } else if (!j_.bw_override) {
+            ledger_inputs(j_.d, j_.dir, *ps_, pp_);
+        }
         const int pm = eng_.cfg.plan_mode == PLAN_DYNAMIC ? PLAN_CONTIGUOUS : eng_.cfg.plan_mode;
         if (make_plan(pp_.data(), P_, j_.B, j_.C, thr_, pm, plan_) != 0) return cudaErrorInvalidValue;
         t_.stats.calls++;
@@ -647,11 +687,11 @@ private:
             j_.pieces(0, j_.B, [&](const Piece& x) { b.add(x.dst, x.src, x.len); });
             if (!small && host_order_) b.sort_by_host(kind_);   // a one-path plan, not a small copy
             TSpan ts(j_.user_dev, j_.user, "DMA native (fallback)", 0, -1, j_.B);
-            CK((cudaError_t)b.issue(kind_, j_.user));
+            CK((cudaError_t)b.issue(kind_, j_.user, !j_.capturing));
             t_.stats.path_bytes[j_.dir][0] += j_.B;
             t_.stats.path_chunks[j_.dir][0] += 1;
             t_.log_n = 0;
-            if (eng_.cfg.ledger) {
+            if (eng_.cfg.ledger && !j_.capturing) {
                 uint64_t lb[MMA_MAX_GPUS] = {}, lo[MMA_MAX_GPUS] = {};
                 lb[j_.d] = lo[j_.d] = j_.B;
                 CK(ledger_add(j_.dir, j_.user_dev, j_.user, lb, lo));
@@ -672,8 +712,8 @@ private:
     {
         n_ = plan_.n;
         sc_ = &t_.scratch[t_.parity & 3];
-        t_.parity++;
-        if (sc_->pending) {   // the call four back used these tables: it must be finished
+        if (!j_.capturing) t_.parity++;
+        if (!j_.capturing && sc_->pending) {   // the call four back used these tables: it must be finished
             const auto w0 = std::chrono::steady_clock::now();
             CK(cudaEventSynchronize(sc_->done));
             sc_->pending = false;
@@ -688,7 +728,7 @@ private:
         for (int p = 0; p < P_; p++) mode_[p] = resolve_mode(j_, pmode_[p]);
         // GPU-driven dynamic pull when every usable path moves bytes with SMs:
         // the assignment is then observed (delivery log, per-path counts), not planned
-        dynamic_ = eng_.cfg.plan_mode == PLAN_DYNAMIC && !j_.timing;
+        dynamic_ = eng_.cfg.plan_mode == PLAN_DYNAMIC && !j_.timing && !j_.capturing;
         active_.assign(P_, 0);
         for (int p = 0; p < P_; p++) {
             active_[p] = !lists_[p].empty();
@@ -728,8 +768,15 @@ private:
             }
         tab_bytes_ = bytes;
         ctab_off_.assign(P_, 0);
-        if (tab_bytes_) {
+        if (tab_bytes_ && j_.capturing) {   // replays read the tables: they live in the arena
+            const size_t need = (tab_bytes_ + 255) & ~(size_t)255;
+            if (!eng_.arena || eng_.arena_used + need > eng_.arena_cap) return kArenaFull;
+            htab_ = eng_.arena + eng_.arena_used;
+            eng_.arena_used += need;
+        } else if (tab_bytes_) {
             CK((cudaError_t)scratch_host(*sc_, tab_bytes_, &htab_));
+        }
+        if (tab_bytes_) {
             char* h = (char*)htab_;
             size_t o = 0;
             if (seg_words) {
@@ -823,9 +870,10 @@ private:
         for (int g = 0; g < eng_.ndev; g++) {
             if (!needs_tab_[g] || !tab_bytes_) continue;
             CK(make_device(g));
-            CK((cudaError_t)scratch_dev(*sc_, g, tab_bytes_, &dtab_[g]));
             DeviceGuard dg(g);
             CK((cudaError_t)use(lanes(g).kern, g));
+            if (j_.capturing) CK(cudaMallocAsync(&dtab_[g], tab_bytes_, lanes(g).kern));   // a graph allocation
+            else CK((cudaError_t)scratch_dev(*sc_, g, tab_bytes_, &dtab_[g]));
             CK(cudaMemcpyAsync(dtab_[g], htab_, tab_bytes_, cudaMemcpyHostToDevice, lanes(g).kern));
         }
         tr_.mark("upload");
@@ -895,7 +943,7 @@ private:
     // delivery log (debug): one byte per chunk (per claim in dynamic pull), 0xff = unwritten
     int delivery_log()
     {
-        if (!eng_.cfg.debug_log) {
+        if (!eng_.cfg.debug_log || j_.capturing) {
             t_.log_n = 0;
             return cudaSuccess;
         }
@@ -1069,7 +1117,7 @@ private:
             if (host_order_) batch.sort_by_host(kind_);
             {
                 TSpan ts(g, s, "DMA direct", p, L[a], o1 + l1 - o0);
-                CK((cudaError_t)batch.issue(kind_, s));
+                CK((cudaError_t)batch.issue(kind_, s, !j_.capturing));
             }
             if (log_) CK(cudaMemsetAsync(log_ + L[a], p, b - a, s));
             a = b;
@@ -1211,6 +1259,11 @@ private:
             DeviceGuard g(j_.user_dev);
             CK(cudaStreamWaitEvent(j_.user, ev, 0));
         }
+        if (j_.capturing) {
+            CK(free_captured_tables());
+            tr_.mark("join");
+            return cudaSuccess;
+        }
         if (tab_bytes_) {
             DeviceGuard g(j_.user_dev);
             if (!sc_->done || sc_->done_dev != j_.user_dev) {
@@ -1231,6 +1284,29 @@ private:
             CK(ledger_add(j_.dir, j_.user_dev, j_.user, lb, lo));
         }
         tr_.mark("join");
+        return cudaSuccess;
+    }
+
+    // captured call: each device's graph-allocated tables are freed on its kernel stream once
+    // the user stream has joined every path (fork -> free -> join, all inside the capture)
+    int free_captured_tables()
+    {
+        cudaEvent_t done = eng_.dev[j_.user_dev].cap_ev;
+        {
+            DeviceGuard g(j_.user_dev);
+            CK(cudaEventRecord(done, j_.user));
+        }
+        for (int g = 0; g < eng_.ndev; g++) {
+            if (!dtab_[g]) continue;
+            cudaStream_t k = lanes(g).kern;
+            DeviceGuard dg(g);
+            CK(cudaStreamWaitEvent(k, done, 0));
+            CK(cudaFreeAsync(dtab_[g], k));
+            cudaEvent_t ev = join_event(k, g);
+            CK(cudaEventRecord(ev, k));
+            DeviceGuard ug(j_.user_dev);
+            CK(cudaStreamWaitEvent(j_.user, ev, 0));
+        }
         return cudaSuccess;
     }
 };

@@ -74,6 +74,7 @@ struct DevRes {
     Lanes lane[2];                   // [MMA_H2D], [MMA_D2H]
     cudaEvent_t fork = nullptr;      // recorded on a user stream of this device
     cudaStream_t setup = nullptr;    // ring initialisation (never waits on user work)
+    cudaEvent_t cap_ev = nullptr;    // captured calls: orders the table frees after the join
     int sms = 148;
 };
 
@@ -152,6 +153,10 @@ struct Engine {
     uint64_t ledger[2][MMA_MAX_GPUS] = {};
     uint64_t ledger_own[2][MMA_MAX_GPUS] = {};
     int* err = nullptr;              // mapped pinned host word (sticky async error)
+    // tables of captured calls (graph replays read them): an append-only pinned arena made at
+    // init, since nothing may be allocated while a stream is captured
+    char* arena = nullptr;
+    size_t arena_cap = 0, arena_used = 0;
     PFN_memop64 wait64 = nullptr, write64 = nullptr;
     uint64_t timeout_ns = 20ull * 1000 * 1000 * 1000;
     uint32_t unit_bytes = kDefaultUnit;
@@ -214,6 +219,7 @@ struct Job {
     const int* mode_override = nullptr;      // measurement runs: per-path mode
     bool no_small_fallback = false;          // measurement runs: ignore the threshold
     PathTiming* timing = nullptr;            // measurement runs: per-path events (planned plans only)
+    bool capturing = false;                  // the user stream is being captured into a graph
 
     // pieces of v[a, b) (the per-segment parts; one piece when contiguous)
     template <typename F>
@@ -273,11 +279,12 @@ struct DmaBatch {
         src.swap(s2);
         len.swap(l2);
     }
-    int issue(cudaMemcpyKind kind, cudaStream_t s)
+    // batch = false: one cudaMemcpyAsync per piece (graph capture records memcpy nodes)
+    int issue(cudaMemcpyKind kind, cudaStream_t s, bool batch = true)
     {
         if (dst.empty()) return cudaSuccess;
         if (dst.size() == 1) return (int)cudaMemcpyAsync(dst[0], src[0], len[0], kind, s);
-        if (s == nullptr || s == cudaStreamLegacy) {   // the batch API rejects the legacy stream
+        if (!batch || s == nullptr || s == cudaStreamLegacy) {   // the batch API rejects the legacy stream
             for (size_t i = 0; i < dst.size(); i++) CK(cudaMemcpyAsync(dst[i], src[i], len[i], kind, s));
             return cudaSuccess;
         }
@@ -317,6 +324,7 @@ int run_job(Job& j);
 int reserve_tables(const Job& j);
 int sticky();
 extern bool g_ktime;
+extern thread_local bool tl_capturing;   // no timing / trace events inside a capture
 struct KRec {
     int dev;
     int kind;   // 0 zero-copy, 1 relay pull (H2D), 2 relay pack (D2H), 3 dynamic | dir << 4 | path << 8 | dev << 16
@@ -331,7 +339,7 @@ struct KTimer {
     cudaStream_t s = nullptr;
     KTimer(int dev, cudaStream_t st, int kind)
     {
-        if (!g_ktime) return;
+        if (!g_ktime || tl_capturing) return;
         DeviceGuard g(dev);
         if (cudaEventCreate(&r.a) != cudaSuccess || cudaEventCreate(&r.b) != cudaSuccess) return;
         r.dev = dev;

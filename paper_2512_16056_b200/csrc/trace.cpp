@@ -54,7 +54,7 @@ bool trace_on() { return g_on; }
 
 TSpan::TSpan(int dev, cudaStream_t s, const char* name, int path, long long chunk, uint64_t bytes)
 {
-    if (!g_on) return;
+    if (!g_on || tl_capturing) return;
     std::lock_guard<std::mutex> g(g_tmu);
     if (g_spans.size() >= g_cap) return;
     DeviceGuard dg(dev);

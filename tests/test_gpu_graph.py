@@ -1,0 +1,136 @@
+"""Graph capture: a multipath copy on a stream being captured (torch.cuda.graph) is recorded
+as a replayable copy -- zero-copy paths and the direct copy engine, tables in the engine's
+pinned arena and graph allocations. Each replay must move the CURRENT bytes of the source,
+bit-exact, in both directions and for scattered tables; a capture that cannot be served
+(engine not yet initialised, arena full) records the native copy instead, still correct."""
+import os
+
+import numpy as np
+import pytest
+
+import mma_inputs
+
+from gpu_util import configure, pinned
+
+torch = pytest.importorskip("torch")
+pytestmark = [pytest.mark.gpu, pytest.mark.timeout(300)]
+
+MiB = 1 << 20
+
+
+@pytest.fixture(scope="module")
+def mma():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    os.environ.setdefault("MMA_SPIN_TIMEOUT_MS", "8000")
+    import paper_2512_16056_b200 as m
+    torch.cuda.init()
+    yield m
+    m.finalize()
+
+
+def _two_paths(mma, dirn):
+    """direct path by copy engine + one loopback path by SM zero-copy, split 1:1"""
+    mma.set_path_modes(0, dirn, [mma.HOP_CE, mma.HOP_ZC])
+    mma.set_bandwidth(0, dirn, [1, 1])
+
+
+def test_captured_h2d_replays_current_bytes(mma):
+    configure(mma, loopback=1, chunk=MiB, debug=0)
+    _two_paths(mma, mma.H2D)
+    B = 24 * MiB + 4096 + 16
+    src = pinned(torch, B, seed=1)
+    dst = torch.zeros(B, dtype=torch.uint8, device="cuda")
+    mma.memcpy_h2d(dst, src, B)                       # uncaptured first: device state exists
+    torch.cuda.synchronize()
+    k0 = mma.get_stats(0)["kernels"]
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        mma.memcpy_h2d(dst, src, B)
+    assert mma.get_stats(0)["kernels"] == k0 + 1      # the zero-copy path was captured
+    for seed in (11, 12, 13):
+        mma_inputs.fill_pattern(src.numpy()[:B], seed)
+        g.replay()
+        torch.cuda.synchronize()
+        assert torch.equal(dst.cpu(), src[:B]), seed
+    mma.memcpy_h2d(dst, src, B)                       # the engine keeps working uncaptured
+    torch.cuda.synchronize()
+    assert torch.equal(dst.cpu(), src[:B]) and mma.get_last_error() == 0
+
+
+@pytest.mark.parametrize("order", [0, 1], ids=["table_order", "host_order"])
+def test_captured_kv_offload_replays(mma, order):
+    """scattered D2H (the KV offload shape), with and without host-ordered private tables"""
+    configure(mma, loopback=1, chunk=MiB, debug=0, host_order=order)
+    _two_paths(mma, mma.D2H)
+    nseg, sb = 1024, 32 << 10
+    rng = np.random.default_rng(3)
+    slots = rng.permutation(2 * nseg)[:nseg]
+    blocks = rng.permutation(nseg)
+    cache = torch.empty(nseg * sb, dtype=torch.uint8, device="cuda")
+    pool = torch.zeros(2 * nseg * sb, dtype=torch.uint8).pin_memory()
+    segs, n = mma.make_segments([cache.data_ptr() + int(b) * sb for b in blocks],
+                                [pool.data_ptr() + int(s) * sb for s in slots], [sb] * nseg)
+    mma.memcpy_d2h_segments(segs, n, 0)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        mma.memcpy_d2h_segments(segs, n, 0)
+    for seed in (21, 22):
+        mma.fill_pattern(cache, nseg * sb, seed, 0)
+        torch.cuda.synchronize()
+        pool.zero_()
+        g.replay()
+        torch.cuda.synchronize()
+        got = pool.numpy().reshape(2 * nseg, sb)[slots]
+        exp = cache.cpu().numpy().reshape(nseg, sb)[blocks]
+        assert np.array_equal(got, exp), seed
+        free = np.setdiff1d(np.arange(2 * nseg), slots)
+        assert not pool.numpy().reshape(2 * nseg, sb)[free].any()
+    assert mma.get_last_error() == 0
+
+
+def test_capture_as_first_call_is_native(mma):
+    """nothing may be initialised inside a capture: the first call of a fresh engine records
+    the native copy, which replays correctly"""
+    mma.finalize()
+    B = 8 * MiB
+    src = pinned(torch, B, seed=4)
+    dst = torch.zeros(B, dtype=torch.uint8, device="cuda")
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        mma.memcpy_h2d(dst, src, B)
+    mma_inputs.fill_pattern(src.numpy()[:B], 5)
+    g.replay()
+    torch.cuda.synchronize()
+    assert torch.equal(dst.cpu(), src[:B])
+
+
+def test_arena_full_captures_native(mma):
+    mma.finalize()
+    os.environ["MMA_GRAPH_ARENA"] = "4096"            # too small for the table below
+    try:
+        configure(mma, loopback=1, chunk=MiB, debug=0)
+        _two_paths(mma, mma.H2D)
+        nseg, sb = 512, 16 << 10
+        pool = pinned(torch, nseg * sb, seed=6)
+        cache = torch.zeros(nseg * sb, dtype=torch.uint8, device="cuda")
+        perm = np.random.default_rng(9).permutation(nseg)
+        segs, n = mma.make_segments([pool.data_ptr() + int(k) * sb for k in range(nseg)],
+                                    [cache.data_ptr() + int(p) * sb for p in perm], [sb] * nseg)
+        mma.memcpy_h2d_segments(segs, n, 0)
+        torch.cuda.synchronize()
+        k0 = mma.get_stats(0)["kernels"]
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            mma.memcpy_h2d_segments(segs, n, 0)
+        assert mma.get_stats(0)["kernels"] == k0       # native: no kernel captured
+        mma_inputs.fill_pattern(pool.numpy(), 7)
+        cache.zero_()
+        g.replay()
+        torch.cuda.synchronize()
+        got = cache.cpu().numpy().reshape(nseg, sb)[perm]
+        assert np.array_equal(got, pool.numpy().reshape(nseg, sb))
+    finally:
+        del os.environ["MMA_GRAPH_ARENA"]
+        mma.finalize()
