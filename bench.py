@@ -915,6 +915,10 @@ def main():
     paths = mma.get_paths(0, mma.H2D)
     path_gpus = [p["gpu"] for p in paths]
     fallback_cfg = {"h2d": int(cfg.fallback_bytes[0]), "d2h": int(cfg.fallback_bytes[1])}
+    try:
+        topology = mma.get_topology()   # P2P matrix, NUMA node, copy engines per GPU
+    except Exception as ex:  # noqa: BLE001 - evidence only
+        topology = {"error": str(ex)}
     tuned = {"h2d": mma.get_paths(0, mma.H2D), "d2h": mma.get_paths(0, mma.D2H)}
     # each path's rate alone (mode choice) and with every path active (planner)
     calib = {d: mma.get_calibration(0, dv, scattered="fetch" in w)
@@ -1202,6 +1206,7 @@ def main():
         "plan": plan_choice,
         "mode_policy": policy or None,
         "numa": numa_info(torch, sorted(set(path_gpus))),
+        "topology": topology,
         "modes": {d: [{"gpu": pi["gpu"], "mode": {0: "auto", 1: "ce", 2: "zc"}.get(
             pi["seg_mode"] if ("fetch" in w and pi["seg_mode"] >= 0) else pi["mode"], "?"),
             "mbps": pi["seg_mbps"] if ("fetch" in w and pi["seg_mbps"]) else pi["mbps"]} for pi in v]

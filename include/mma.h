@@ -333,6 +333,21 @@ int mma_device_bus_id(int device, char* buf, int len);
 int mma_trace_begin(size_t max_spans);
 int mma_trace_end(const char* json_path, size_t* nspans);
 
+/* Topology probe ("P2P matrix, NUMA node per GPU, CE count"), as the
+ * engine sees it: peer access is what cudaDeviceCanAccessPeer reports (and what the engine
+ * enabled), the NUMA node comes from sysfs for the GPU's PCI device (-1 = unknown), copy
+ * engines from cudaDevAttrAsyncEngineCount. */
+typedef struct {
+    int ngpu;
+    int p2p[MMA_MAX_GPUS][MMA_MAX_GPUS];  /* 1 = device i can access device j's memory */
+    int numa_node[MMA_MAX_GPUS];
+    int copy_engines[MMA_MAX_GPUS];
+    int sms[MMA_MAX_GPUS];
+    char bus_id[MMA_MAX_GPUS][16];        /* "dddd:bb:dd.f" */
+    int host_numa_nodes;                  /* NUMA nodes the host exposes */
+} mma_topology_t;
+int mma_get_topology(mma_topology_t* out);
+
 int mma_get_stats(int device, mma_stats_t* out);
 int mma_reset_stats(int device);
 int mma_get_last_error(void);

@@ -16,7 +16,7 @@ from .mma import (  # noqa: F401
     verify_pattern, verify_segments, shared_host_alloc, shared_host_free, ipc_export, ipc_open,
     ipc_close, copy_share_segments, copy_claim_segments, trace_begin, trace_end,
     save_calibration, load_calibration, host_alloc_for, host_page_node, get_calibration, tune_threshold,
-    ledger_attach, ledger_unlink, ledger_shared_add, ledger_shared_get, device_bus_id,
+    ledger_attach, ledger_unlink, ledger_shared_add, ledger_shared_get, device_bus_id, get_topology,
 )
 
 try:

@@ -1,6 +1,11 @@
 // api.cpp — C7: the C ABI of include/mma.h (validation, fallback decisions, pointer
 // classification) over the data plane in plane.cpp. Every function returns a cudaError_t
 // value as int; validation happens before anything is enqueued.
+#include <unistd.h>
+
+#include <cctype>
+#include <string>
+
 #include "plane.h"
 
 namespace mma {
@@ -307,6 +312,34 @@ int mma_finalize(void)
     if (e.arena) { cudaFreeHost(e.arena); e.arena = nullptr; }   // graphs with captured copies die with it
     e.arena_used = e.arena_cap = 0;
     e.inited = false;
+    return cudaSuccess;
+}
+
+int mma_get_topology(mma_topology_t* out)
+{
+    if (!out) return cudaErrorInvalidValue;
+    CK((cudaError_t)ensure_init());
+    Engine& e = E();
+    memset(out, 0, sizeof(*out));
+    out->ngpu = e.ndev;
+    for (int a = 0; a < e.ndev; a++) {
+        for (int b = 0; b < e.ndev; b++) out->p2p[a][b] = e.p2p[a][b] ? 1 : 0;
+        CK(cudaDeviceGetAttribute(&out->copy_engines[a], cudaDevAttrAsyncEngineCount, a));
+        CK(cudaDeviceGetAttribute(&out->sms[a], cudaDevAttrMultiProcessorCount, a));
+        CK(cudaDeviceGetPCIBusId(out->bus_id[a], sizeof out->bus_id[a], a));
+        std::string bus = out->bus_id[a];
+        for (char& c : bus) c = (char)tolower((unsigned char)c);
+        out->numa_node[a] = -1;
+        if (FILE* f = fopen(("/sys/bus/pci/devices/" + bus + "/numa_node").c_str(), "r")) {
+            if (fscanf(f, "%d", &out->numa_node[a]) != 1) out->numa_node[a] = -1;
+            fclose(f);
+        }
+    }
+    for (int i = 0; i < 256; i++) {
+        char p[96];
+        snprintf(p, sizeof p, "/sys/devices/system/node/node%d", i);
+        if (access(p, F_OK) == 0) out->host_numa_nodes = i + 1;
+    }
     return cudaSuccess;
 }
 

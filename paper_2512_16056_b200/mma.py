@@ -17,6 +17,7 @@ H2D, D2H = 0, 1
 HOP_AUTO, HOP_CE, HOP_ZC = 0, 1, 2
 PATH_DIRECT, PATH_RELAY = 0, 1
 MAX_PATHS = 16
+MAX_GPUS = 16
 ERR_RELAY_TIMEOUT = 2001
 
 SYMBOLS = [
@@ -31,7 +32,7 @@ SYMBOLS = [
     "mma_copy_share_segments", "mma_copy_claim_segments", "mma_trace_begin", "mma_trace_end",
     "mma_save_calibration", "mma_load_calibration", "mma_host_alloc_for", "mma_host_page_node",
     "mma_get_calibration", "mma_tune_threshold", "mma_ledger_attach", "mma_ledger_unlink",
-    "mma_ledger_shared_add", "mma_ledger_shared_get", "mma_device_bus_id",
+    "mma_ledger_shared_add", "mma_ledger_shared_get", "mma_device_bus_id", "mma_get_topology",
 ]
 
 
@@ -53,6 +54,18 @@ class Config(C.Structure):
         ("zc_ctas", C.c_int),
         ("calib_rounds", C.c_int),
         ("host_order", C.c_int),
+    ]
+
+
+class Topology(C.Structure):
+    _fields_ = [
+        ("ngpu", C.c_int),
+        ("p2p", (C.c_int * MAX_GPUS) * MAX_GPUS),
+        ("numa_node", C.c_int * MAX_GPUS),
+        ("copy_engines", C.c_int * MAX_GPUS),
+        ("sms", C.c_int * MAX_GPUS),
+        ("bus_id", (C.c_char * 16) * MAX_GPUS),
+        ("host_numa_nodes", C.c_int),
     ]
 
 
@@ -115,6 +128,7 @@ def lib():
         L.mma_get_segment_tuning.argtypes = [C.c_int, C.c_int, vp, vp, C.c_int, C.POINTER(C.c_int)]
         L.mma_ledger_attach.argtypes = [C.c_char_p]
         L.mma_device_bus_id.argtypes = [C.c_int, C.c_char_p, C.c_int]
+        L.mma_get_topology.argtypes = [C.POINTER(Topology)]
         L.mma_ledger_unlink.argtypes = [C.c_char_p]
         L.mma_ledger_shared_add.argtypes = [C.c_char_p, C.c_int, C.c_int64, C.c_int64]
         L.mma_ledger_shared_get.argtypes = [C.c_char_p, C.c_int, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]
@@ -275,6 +289,19 @@ def tune_threshold(device: int, direction: int, max_bytes: int = 256 << 20):
 def ledger_attach(name: str | None) -> None:
     """Attach this process's engine to the cross-process ledger `name` (None detaches)."""
     _check(lib().mma_ledger_attach(name.encode() if name else None), "mma_ledger_attach")
+
+
+def get_topology() -> dict:
+    """P2P matrix, NUMA node, copy engines, SMs and PCI bus id per GPU (SURVEY a0 probe)."""
+    t = Topology()
+    _check(lib().mma_get_topology(C.byref(t)), "mma_get_topology")
+    n = t.ngpu
+    return {"ngpu": n, "p2p": [[int(t.p2p[a][b]) for b in range(n)] for a in range(n)],
+            "numa_node": [int(t.numa_node[a]) for a in range(n)],
+            "copy_engines": [int(t.copy_engines[a]) for a in range(n)],
+            "sms": [int(t.sms[a]) for a in range(n)],
+            "bus_id": [t.bus_id[a].value.decode() for a in range(n)],
+            "host_numa_nodes": int(t.host_numa_nodes)}
 
 
 def device_bus_id(device: int) -> str:
