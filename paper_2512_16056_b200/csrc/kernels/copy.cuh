@@ -53,16 +53,27 @@ __device__ __forceinline__ void cta_copy(char* __restrict__ dst, const char* __r
         const uint64_t nvec = (len - head) >> 4;
         uint4* __restrict__ d4 = reinterpret_cast<uint4*>(dst + head);
         const uint4* __restrict__ s4 = reinterpret_cast<const uint4*>(src + head);
-        uint64_t i = tid;
+        // rounds of kThreads x kUnroll vectors; a partial last round is predicated rather than
+        // run one vector at a time, so a 32 KiB paged-KV segment (2048 vectors) is ONE round of
+        // loads in flight, not four dependent ones (probe_relay "seg" rows)
         constexpr uint64_t step = (uint64_t)kThreads * kUnroll;
-        for (; i + (kUnroll - 1) * kThreads < nvec; i += step) {
+        for (uint64_t base = 0; base < nvec; base += step) {
+            const uint64_t i = base + tid;
             uint4 r[kUnroll];
+            if (base + step <= nvec) {
 #pragma unroll
-            for (int u = 0; u < kUnroll; u++) r[u] = __ldcg(s4 + i + u * kThreads);
+                for (int u = 0; u < kUnroll; u++) r[u] = __ldcg(s4 + i + u * kThreads);
 #pragma unroll
-            for (int u = 0; u < kUnroll; u++) __stcg(d4 + i + u * kThreads, r[u]);
+                for (int u = 0; u < kUnroll; u++) __stcg(d4 + i + u * kThreads, r[u]);
+            } else {
+#pragma unroll
+                for (int u = 0; u < kUnroll; u++)
+                    if (i + u * kThreads < nvec) r[u] = __ldcg(s4 + i + u * kThreads);
+#pragma unroll
+                for (int u = 0; u < kUnroll; u++)
+                    if (i + u * kThreads < nvec) __stcg(d4 + i + u * kThreads, r[u]);
+            }
         }
-        for (; i < nvec; i += kThreads) __stcg(d4 + i, __ldcg(s4 + i));
         const uint64_t done = head + (nvec << 4);
         const uint64_t tail = len - done;
         if (tid < tail) dst[done + tid] = src[done + tid];

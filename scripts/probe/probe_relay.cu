@@ -8,6 +8,9 @@
 //   nvcc -O3 -std=c++17 -gencode arch=compute_100a,code=sm_100a -lineinfo \
 //        -I include scripts/probe/probe_relay.cu -o scripts/probe/probe_relay
 //   ./scripts/probe/probe_relay [ncu]      (ncu: one launch of the 7 x 8 configuration only)
+// "seg" rows (C3): the destination is a table of 32 KiB segments at a seeded
+// permutation of block slots (the paged-KV layout), so the pull scatters every slot into 256
+// blocks and the pack gathers them.
 #include <cuda_runtime.h>
 #include <cstdio>
 #include <cstring>
@@ -53,12 +56,43 @@ int main(int argc, char** argv)
     std::vector<uint64_t> seqs(128, 0);
     for (uint32_t s = 0; s < S; s++) seqs[s] = s + 1;   // chunk g = s staged (g0 = 0)
 
-    auto run = [&](int rings, int ctas, bool pull, uint32_t unit, float* ms_out) -> int {
+    // segment table of the scattered form: segment k (32 KiB) of v lives at block perm[k]
+    const uint64_t SB = 32 << 10, nseg_max = per_ring * max_rings / SB;
+    std::vector<uint64_t> tab(3 * nseg_max + 1);
+    {
+        std::vector<uint64_t> perm(nseg_max);
+        for (uint64_t k = 0; k < nseg_max; k++) perm[k] = k;
+        uint64_t x = 0x4D4D41;
+        for (uint64_t k = nseg_max - 1; k > 0; k--) {   // seeded Fisher-Yates (splitmix64)
+            x += 0x9e3779b97f4a7c15ull;
+            uint64_t z = x;
+            z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+            z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+            z ^= z >> 31;
+            std::swap(perm[k], perm[z % (k + 1)]);
+        }
+        for (uint64_t k = 0; k <= nseg_max; k++) tab[k] = k * SB;
+        for (uint64_t k = 0; k < nseg_max; k++) {
+            tab[nseg_max + 1 + k] = (uint64_t)dst + perm[k] * SB;       // src (pack reads it)
+            tab[2 * nseg_max + 1 + k] = (uint64_t)dst + perm[k] * SB;   // dst (pull writes it)
+        }
+    }
+    uint64_t* dtab;
+    CK(cudaMalloc(&dtab, tab.size() * 8));
+    CK(cudaMemcpy(dtab, tab.data(), tab.size() * 8, cudaMemcpyHostToDevice));
+
+    auto run = [&](int rings, int ctas, bool pull, uint32_t unit, float* ms_out, bool seg = false) -> int {
         RelayLaunchArg A;
         memset(&A, 0, sizeof(A));
         A.v.nseg = 1;
         A.v.B = per_ring * rings;
         A.v.C = C;
+        if (seg) {   // v = the first B / 32 KiB segments of the table
+            A.v.nseg = A.v.B / SB;
+            A.v.start = dtab;
+            A.v.src = dtab + nseg_max + 1;
+            A.v.dst = dtab + 2 * nseg_max + 1;
+        }
         A.unit_bytes = unit;
         A.err = err;
         A.timeout_ns = 5ull * 1000 * 1000 * 1000;
@@ -100,6 +134,8 @@ int main(int argc, char** argv)
         float ms;
         CK((cudaError_t)run(7, 8, true, 128u << 10, &ms));
         CK((cudaError_t)run(7, 8, false, 128u << 10, &ms));
+        CK((cudaError_t)run(7, 8, true, 512u << 10, &ms, true));
+        CK((cudaError_t)run(7, 8, false, 512u << 10, &ms, true));
         printf("ncu launches done\n");
         return 0;
     }
@@ -123,5 +159,20 @@ int main(int argc, char** argv)
                     printf("%-5s %-6d %-5d %-8u %10.1f %10.1f %12.1f\n", pull ? "pull" : "pack", rings, ctas,
                            unit >> 10, gbs, gbs / (rings * ctas), 2 * gbs);
                 }
+    printf("# C3 scattered form: v = 32 KiB segments at permuted blocks (the pull scatters, the pack gathers)\n");
+    for (int pull = 1; pull >= 0; pull--)
+        for (int rings : {1, 7})
+            for (int ctas : {8, 32}) {
+                float best = 1e30f;
+                for (int rep = 0; rep < 6; rep++) {
+                    float ms = 0;
+                    int rc = run(rings, ctas, pull, 512u << 10, &ms, true);
+                    if (rc) { printf("ERR run rc=%d\n", rc); return 1; }
+                    if (rep) best = std::min(best, ms);
+                }
+                const double gbs = (double)per_ring * rings / (best * 1e-3) / 1e9;
+                printf("%-5s %-6d %-5d %-8s %10.1f %10.1f %12.1f\n", pull ? "pull" : "pack", rings, ctas, "512seg",
+                       gbs, gbs / (rings * ctas), 2 * gbs);
+            }
     return 0;
 }
