@@ -2,7 +2,9 @@
 relay count, per-path modes, plan mode, direction, contiguous or scattered, pointer
 offsets) through the C ABI, each compared byte for byte with the oracle moving the same
 transfer with the same assignment (the planned one, or the observed one in dynamic mode).
-Rings persist across cases, so sequence bases and slot reuse vary too."""
+Rings persist across cases, so sequence bases and slot reuse vary too. The work order inside
+a path (host_order) and CUDA graph capture + replay are drawn at random as well; neither may
+change a byte."""
 import numpy as np
 import pytest
 
@@ -47,7 +49,9 @@ def test_random_transfers(mma, orc):
         bw = [int(x) for x in rng.integers(1, 6, P)]
         dirn = int(rng.integers(0, 2))
         scattered = rng.random() < 0.4
-        configure(mma, loopback=lb, chunk=C, slots=S, plan_mode=plan_mode, hop=(1, 1))
+        host_order = int(rng.integers(0, 3))
+        capture = plan_mode != 2 and rng.random() < 0.15
+        configure(mma, loopback=lb, chunk=C, slots=S, plan_mode=plan_mode, hop=(1, 1), host_order=host_order)
         mma.set_path_modes(0, dirn, modes)
         mma.set_bandwidth(0, dirn, bw)
         if scattered:
@@ -69,7 +73,7 @@ def test_random_transfers(mma, orc):
             span = B + 128
         B = int(lens.sum())
         print(f"case {case}: lb={lb} C={C} S={S} plan={plan_mode} modes={modes} bw={bw} dir={dirn} "
-              f"scattered={scattered} nseg={len(lens)} B={B}", flush=True)
+              f"scattered={scattered} nseg={len(lens)} B={B} order={host_order} capture={capture}", flush=True)
         if dirn == 0:      # H2D: host pool -> fresh device buffer
             dst = torch.full((span,), 0xA5, dtype=torch.uint8, device="cuda")
             segs, n = mma.make_segments(pool_h.data_ptr() + src_off, dst.data_ptr() + dst_off, lens)
@@ -78,16 +82,29 @@ def test_random_transfers(mma, orc):
             dst = torch.full((span,), 0xA5, dtype=torch.uint8).pin_memory()
             segs, n = mma.make_segments(pool_d.data_ptr() + src_off, dst.data_ptr() + dst_off, lens)
             src_np = hn      # pool_d holds the same bytes
-        if scattered or rng.random() < 0.5:
-            (mma.memcpy_h2d_segments if dirn == 0 else mma.memcpy_d2h_segments)(segs, n, 0)
-        elif dirn == 0:
-            mma.memcpy_h2d(dst.data_ptr() + int(dst_off[0]), pool_h.data_ptr() + int(src_off[0]), B)
+        as_segments = scattered or rng.random() < 0.5
+
+        def copy():
+            if as_segments:
+                (mma.memcpy_h2d_segments if dirn == 0 else mma.memcpy_d2h_segments)(segs, n, 0)
+            elif dirn == 0:
+                mma.memcpy_h2d(dst.data_ptr() + int(dst_off[0]), pool_h.data_ptr() + int(src_off[0]), B)
+            else:
+                mma.memcpy_d2h(dst.data_ptr() + int(dst_off[0]), pool_d.data_ptr() + int(src_off[0]), B)
+        if capture:      # recorded into a graph (rings stay out), then replayed once
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                copy()
+            g.replay()
         else:
-            mma.memcpy_d2h(dst.data_ptr() + int(dst_off[0]), pool_d.data_ptr() + int(src_off[0]), B)
+            copy()
         torch.cuda.synchronize()
         assert mma.get_last_error() == 0, case
         dynamic = plan_mode == 2 and all(m == 2 for m in modes)
-        if dynamic:
+        if capture:      # the bytes are dst == src whatever the captured plan; check with the planned one
+            rc, path, _, fb = orc.plan(bw, B, C, 0, plan_mode)
+            assert rc == 0
+        elif dynamic:
             path = np.frombuffer(mma.get_delivery_log(0), dtype=np.uint8)
             assert path.size == (B + C - 1) // C and (path < P).all(), case
         else:
