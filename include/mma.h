@@ -100,7 +100,7 @@ typedef struct {
     /* CTAs (512 threads each) per zero-copy path kernel, planned or dynamic. A PCIe link
      * saturates with 4 such CTAs (profiles/r01_probe_grid.txt), so a small grid leaves the
      * relay GPU's other SMs to its own work (§3.4.3: relaying must not steal the
-     * peer's compute). 0 = default (32); at most 4 x the SM count. */
+     * peer's compute). 0 = default (16); at most 4 x the SM count. */
     int zc_ctas;
     /* Concurrent calibration rounds (the bandwidth vector is "measured with
      * all paths of the set active"). After mma_calibrate / mma_tune_segments pick each

@@ -43,7 +43,7 @@ constexpr uint32_t kDefaultMbps = 50000;
 // (profiles/r01_probe_relay_unroll.txt)
 constexpr uint32_t kDefaultUnit = 512u << 10;
 constexpr int kDefaultRelayCtas = 8;
-constexpr int kDefaultZcCtas = 32;     // zero-copy kernel grid (mma_config_t::zc_ctas)
+constexpr int kDefaultZcCtas = 16;     // zero-copy kernel grid (mma_config_t::zc_ctas): the link saturates from 4-8
 constexpr unsigned kDynSlots = 64;        // per-call claim slots, rotating
 constexpr unsigned kDynSlotWords = 32;    // cursor + counts[MMA_KMAX_RINGS] (+ padding)
 
