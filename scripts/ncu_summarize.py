@@ -110,6 +110,18 @@ def main():
             if e["gpu_time_ms"]:
                 e["payload_gbps"] = round(RELAY_BYTES / (e["gpu_time_ms"] * 1e-3) / 1e9, 1)
             summary["kernels"][name] = e
+    rel = OUT / "prof_relay_seg.ncu-rep"
+    if rel.exists():
+        (PROF / f"{TAG}_ncu_relay_seg_details.csv").write_text(ncu_csv(rel, "details"))
+        for d in raw_rows(rel):
+            name = d["Kernel Name"][0].split("(")[0].split("::")[-1] + "/scattered"
+            e = kernel_entry(d, f"{name} alone, C3 scattered form: v = 32 KiB segments at permuted blocks, "
+                                "7 rings x 8 CTAs, hop 1 complete, local HBM", RELAY_BYTES,
+                             f"profiles/{TAG}_ncu_relay_seg_details.csv")
+            e["algorithmic_hbm_bytes_per_launch"] = 2 * RELAY_BYTES
+            if e["gpu_time_ms"]:
+                e["payload_gbps"] = round(RELAY_BYTES / (e["gpu_time_ms"] * 1e-3) / 1e9, 1)
+            summary["kernels"][name] = e
     lst = OUT / "launches_bench.csv"
     if lst.exists():
         shutil.copy(lst, PROF / f"{TAG}_launches_bench.csv")

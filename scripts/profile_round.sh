@@ -23,3 +23,6 @@ echo "zc d2h rc=$?"
 timeout 600 $NCU --set full --import-source on -k regex:relay -c 2 -f -o gpurun_out/prof_relay \
     ./scripts/probe/probe_relay ncu > gpurun_out/ncu_relay.log 2>&1
 echo "relay rc=$?"
+timeout 600 $NCU --set full --import-source on -k regex:relay -s 2 -c 2 -f -o gpurun_out/prof_relay_seg \
+    ./scripts/probe/probe_relay ncu > gpurun_out/ncu_relay_seg.log 2>&1
+echo "relay seg rc=$?"
