@@ -863,12 +863,9 @@ def main():
                                "d2h_ce_host_order_gbps": ce, "d2h_zc_gbps": zc,
                                "note": "copy-engine batches run in host-address order (cfg.host_order); "
                                        "--engine-modes times the engine's own measured choice"})
-            if len(mma.get_paths(0, mma.H2D)) > 1:
-                # the fallback threshold is the measured native/multipath break-even
-                # (for a contiguous copy; a single path needs none)
-                if "fetch" in w:
-                    mma.calibrate(0, mma.H2D, 256 * MiB)
-                    mma.calibrate(0, mma.D2H, 256 * MiB)
+            if len(mma.get_paths(0, mma.H2D)) > 1 and "fetch" not in w:
+                # the fallback threshold is the measured native/multipath break-even of
+                # a contiguous copy (a single path needs none; the 4 GiB KV calls are far above it)
                 for name, dv in (("h2d", mma.H2D), ("d2h", mma.D2H)):
                     thr, found = mma.tune_threshold(0, dv, 256 * MiB)
                     thresholds[name] = thr if found else f"no break-even up to 256 MiB (kept {thr})"
