@@ -323,6 +323,11 @@ int mma_ledger_attach(const char* name);
 int mma_ledger_unlink(const char* name);
 int mma_ledger_shared_add(const char* bus_id, int dir, int64_t bytes, int64_t own);
 int mma_ledger_shared_get(const char* bus_id, int dir, uint64_t* bytes, uint64_t* own);
+/* The order the engine issues a path's pieces in under cfg.host_order (reading R22): perm
+ * receives the stable ascending order of the n addresses (radix sort on 4 KiB page numbers,
+ * then by address inside a page). Host-only; exposed for tests and external schedulers. */
+int mma_order_by_address(const uint64_t* addr, size_t n, uint32_t* perm);
+
 /* PCI bus id of a device ("dddd:bb:dd.f", as cudaDeviceGetPCIBusId) for the calls above. */
 int mma_device_bus_id(int device, char* buf, int len);
 

@@ -315,6 +315,15 @@ int mma_finalize(void)
     return cudaSuccess;
 }
 
+int mma_order_by_address(const uint64_t* addr, size_t n, uint32_t* perm)
+{
+    if ((n && (!addr || !perm)) || n > 0xffffffffull) return cudaErrorInvalidValue;
+    std::vector<uint32_t> p;
+    order_by_key(addr, n, p);
+    if (n) memcpy(perm, p.data(), n * sizeof(uint32_t));
+    return cudaSuccess;
+}
+
 int mma_get_topology(mma_topology_t* out)
 {
     if (!out) return cudaErrorInvalidValue;

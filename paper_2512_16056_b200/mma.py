@@ -32,7 +32,7 @@ SYMBOLS = [
     "mma_copy_share_segments", "mma_copy_claim_segments", "mma_trace_begin", "mma_trace_end",
     "mma_save_calibration", "mma_load_calibration", "mma_host_alloc_for", "mma_host_page_node",
     "mma_get_calibration", "mma_tune_threshold", "mma_ledger_attach", "mma_ledger_unlink",
-    "mma_ledger_shared_add", "mma_ledger_shared_get", "mma_device_bus_id", "mma_get_topology",
+    "mma_ledger_shared_add", "mma_ledger_shared_get", "mma_device_bus_id", "mma_get_topology", "mma_order_by_address",
 ]
 
 
@@ -129,6 +129,7 @@ def lib():
         L.mma_ledger_attach.argtypes = [C.c_char_p]
         L.mma_device_bus_id.argtypes = [C.c_int, C.c_char_p, C.c_int]
         L.mma_get_topology.argtypes = [C.POINTER(Topology)]
+        L.mma_order_by_address.argtypes = [vp, sz, vp]
         L.mma_ledger_unlink.argtypes = [C.c_char_p]
         L.mma_ledger_shared_add.argtypes = [C.c_char_p, C.c_int, C.c_int64, C.c_int64]
         L.mma_ledger_shared_get.argtypes = [C.c_char_p, C.c_int, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]
@@ -289,6 +290,15 @@ def tune_threshold(device: int, direction: int, max_bytes: int = 256 << 20):
 def ledger_attach(name: str | None) -> None:
     """Attach this process's engine to the cross-process ledger `name` (None detaches)."""
     _check(lib().mma_ledger_attach(name.encode() if name else None), "mma_ledger_attach")
+
+
+def order_by_address(addr):
+    """The engine's host-address issue order (R22): stable ascending permutation of addr."""
+    import numpy as np
+    a = np.ascontiguousarray(addr, dtype=np.uint64)
+    perm = np.empty(a.size, dtype=np.uint32)
+    _check(lib().mma_order_by_address(a.ctypes.data, a.size, perm.ctypes.data), "mma_order_by_address")
+    return perm
 
 
 def get_topology() -> dict:
