@@ -1164,6 +1164,32 @@ def main():
                                         if "wake" in w else "cudaMemcpyAsync on the user stream (single PCIe link)"),
                   "speedup": round(value / (nbytes_step / (nh + nd) / 1e6), 3)}
 
+    # ---- the metric's path-count axis inside one run (GB/s vs k = 1/2/4/8): the
+    # same step with the target plus the first k-1 relays, each set tuned as above
+    per_k = None
+    if k > 1 and not args.quick and multipath_error is None:
+        per_k = {}
+        saved = (dict(policy), dict(thresholds))     # the line reports the headline run's choices
+        for kk in (1, 2, 4, 8):
+            if kk >= k:
+                continue
+            try:
+                prepare(list(range(1, kk)))
+                a = torch.cuda.Event(enable_timing=True)
+                b = torch.cuda.Event(enable_timing=True)
+                a.record(stream)
+                for _ in range(args.steps):
+                    run_step(mma, w, 0, stream)
+                b.record(stream)
+                b.synchronize()
+                ms = a.elapsed_time(b) / args.steps
+                per_k[str(kk)] = {"value": round(nbytes_step / (ms * 1e-3) / 1e9, 3), "ms_per_step": round(ms, 3)}
+            except Exception as ex:  # noqa: BLE001 - evidence only
+                per_k[str(kk)] = {"error": f"{type(ex).__name__}: {ex}"}
+        per_k[str(k)] = {"value": round(value, 3), "ms_per_step": round(ms_step, 3), "headline": True}
+        policy.clear(); policy.update(saved[0])
+        thresholds.clear(); thresholds.update(saved[1])
+
     # ---- CPU baseline: the oracle on the host cores, bounded sample, N=1 only
     cpu = None
     if not args.quick and dist.world == 1:
@@ -1202,6 +1228,7 @@ def main():
         "verify": verify,
         "plan": plan_choice,
         "mode_policy": policy or None,
+        "per_path_count": per_k,
         "numa": numa_info(torch, sorted(set(path_gpus))),
         "topology": topology,
         "modes": {d: [{"gpu": pi["gpu"], "mode": {0: "auto", 1: "ce", 2: "zc"}.get(
