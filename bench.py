@@ -42,6 +42,9 @@ def _hbm_peak():
 HBM_PEAK = _hbm_peak()
 KNAMES = {0: "zc_copy_kernel", 1: "relay_pull_kernel", 2: "relay_pack_kernel", 3: "zc_dyn_kernel"}
 MiB, GiB = 1 << 20, 1 << 30
+# PCIe bytes per payload byte of a native copy-engine 4 GiB copy on one B200 link (NVML
+# counters, profiles/r01_probe_nvml.json): 256-byte TLPs + DLLPs
+CE_PCIE_OVERHEAD = {"h2d": 1.080, "d2h": 1.095}
 SEED = 0x4D4D41 + 3
 
 
@@ -1129,6 +1132,25 @@ def main():
         pcie_hw = pcie_hw_check(torch, mma, w, stream, path_gpus, plan_choice.get("chosen") == "dynamic")
     except Exception as ex:  # noqa: BLE001 - evidence only
         pcie_hw = {"error": f"{type(ex).__name__}: {ex}"}
+
+    # the dominant kernel against the ceiling of SM-initiated host traffic on this link: the link's
+    # raw byte rate (the native copy's rate x its measured protocol overhead) over the kernel's own
+    # measured overhead (SM writes / read completions travel as 128-byte TLPs; the copy engine's as
+    # 256-byte ones). A second denominator beside the link peak, derived from two counters.
+    try:
+        if roof and roof["kernel"] == "zc_copy_kernel" and roof["path"] == 0 and isinstance(pcie_hw, dict):
+            rows = pcie_hw.get(roof["direction"]) or []
+            kern_ratio = next((r["ratio"] for r in rows if r["gpu"] == roof["device"] and r["ratio"]), None)
+            ce_ratio = CE_PCIE_OVERHEAD[roof["direction"]]
+            if kern_ratio:
+                ceil = roof["peak"] * ce_ratio / kern_ratio
+                roof["sm_tlp_ceiling"] = {
+                    "gbps": round(ceil, 2), "frac": round(roof["achieved"] / ceil, 4),
+                    "kernel_pcie_over_payload": kern_ratio, "copy_engine_pcie_over_payload": ce_ratio,
+                    "how": "peak x copy-engine overhead (profiles/r01_probe_nvml.json, native 4 GiB copy) / "
+                           "this kernel's overhead (pcie_hw, this run)"}
+    except (KeyError, TypeError, ZeroDivisionError, StopIteration):
+        pass
 
     # ---- e2e through the public API: wall clock, host issue + copies + sync every step
     run_step(mma, w, 0, stream)                 # one untimed synchronous step first
