@@ -16,6 +16,8 @@
 // paper's 2 threads per GPU, cost 822% CPU at 8 GPUs). Per relay chunk
 // the host enqueues: wait(credit) -> DMA -> write(seq) on the relay's stream (cuda.h stream
 // memory operations); the relay kernel polls seq and releases credit on the GPU.
+#include <nvtx3/nvToolsExt.h>   // header-only: ranges are free unless a tool (nsys) attaches
+
 #include "plane.h"
 
 namespace mma {
@@ -551,6 +553,17 @@ public:
             explicit CaptureFlag(bool on) { tl_capturing = on; }
             ~CaptureFlag() { tl_capturing = false; }
         } cflag(j_.capturing);
+        struct Range {         // one NVTX range per call (SURVEY §5 tracing) around the enqueue
+            explicit Range(const Job& j)
+            {
+                char m[96];
+                snprintf(m, sizeof m, "mma %s %s %.1f MiB -> gpu %d%s", j.dir == MMA_H2D ? "h2d" : "d2h",
+                         j.contiguous ? "contig" : "segments", (double)j.B / (1 << 20), j.d,
+                         j.capturing ? " (captured)" : "");
+                nvtxRangePushA(m);
+            }
+            ~Range() { nvtxRangePop(); }
+        } nvtx(j_);
         tr_.cap_stream = j_.user;
         tr_.mark("start");
         make_paths(j_.d);
