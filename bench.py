@@ -60,7 +60,8 @@ def parse():
     ap.add_argument("--bytes", type=int, default=4 * GiB, help="contig workload size")
     ap.add_argument("--tokens", type=int, default=32768, help="kv workload tokens")
     ap.add_argument("--chunk", type=int, default=0, help="chunk bytes (0 = the engine's default)")
-    ap.add_argument("--hop", type=int, default=0, help="0 auto, 1 copy engine, 2 SM zero-copy")
+    ap.add_argument("--hop", type=int, default=0, help="0 auto, 1 copy engine, 2 SM zero-copy, "
+                    "3 copy engine for both relay hops")
     ap.add_argument("--no-verify", action="store_true")
     ap.add_argument("--engine-modes", action="store_true",
                     help="N=1: keep the engine's measured mode for the offload (default pins the SM scatter)")
@@ -844,7 +845,7 @@ def main():
         check of the bench's own launch configuration (all outside the timed region)"""
         cfg = configure(relays)
         if args.modes:
-            m = {"ce": mma.HOP_CE, "zc": mma.HOP_ZC}
+            m = {"ce": mma.HOP_CE, "zc": mma.HOP_ZC, "ce_p2p": mma.HOP_CE_P2P}
             h, d = (m[x] for x in args.modes.split(","))
             mma.set_path_modes(0, mma.H2D, [h] * len(mma.get_paths(0, mma.H2D)))
             mma.set_path_modes(0, mma.D2H, [d] * len(mma.get_paths(0, mma.D2H)))
@@ -1227,7 +1228,7 @@ def main():
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u8",
         "data": "synthetic",
         "config": {"workload": w["desc"], "paths": k, "path_gpus": path_gpus, "target_gpu": 0,
-                   "chunk_bytes": int(cfg.chunk_bytes[0]), "claim_bytes": int(cfg.claim_bytes), "hop": {0: "auto", 1: "ce", 2: "zc"}[args.hop],
+                   "chunk_bytes": int(cfg.chunk_bytes[0]), "claim_bytes": int(cfg.claim_bytes), "hop": {0: "auto", 1: "ce", 2: "zc", 3: "ce_p2p"}[args.hop],
                    "bytes_per_step": nbytes_step,
                    "fallback_bytes": thresholds or fallback_cfg,
                    "fallback_how": "measured break-even (mma_tune_threshold)" if thresholds else "default (2 chunks)", "l2": f"inputs ({w['bytes'] / GiB:.1f} GiB per direction) exceed the 126 MB L2; no flush",
@@ -1253,7 +1254,7 @@ def main():
         "per_path_count": per_k,
         "numa": numa_info(torch, sorted(set(path_gpus))),
         "topology": topology,
-        "modes": {d: [{"gpu": pi["gpu"], "mode": {0: "auto", 1: "ce", 2: "zc"}.get(
+        "modes": {d: [{"gpu": pi["gpu"], "mode": {0: "auto", 1: "ce", 2: "zc", 3: "ce_p2p"}.get(
             pi["seg_mode"] if ("fetch" in w and pi["seg_mode"] >= 0) else pi["mode"], "?"),
             "mbps": pi["seg_mbps"] if ("fetch" in w and pi["seg_mbps"]) else pi["mbps"]} for pi in v]
             for d, v in tuned.items()},

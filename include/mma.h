@@ -42,8 +42,13 @@ typedef enum { MMA_H2D = 0, MMA_D2H = 1 } mma_dir_t;
 typedef enum {
     MMA_HOP_AUTO = 0,  /* CE for contiguous copies, ZC for scattered segments */
     MMA_HOP_CE = 1,    /* copy-engine DMA; a relay stages through its HBM ring */
-    MMA_HOP_ZC = 2     /* SM loads/stores of mapped pinned host memory; a relay writes the
+    MMA_HOP_ZC = 2,    /* SM loads/stores of mapped pinned host memory; a relay writes the
                           target over NVLink directly (one hop, no staging) */
+    MMA_HOP_CE_P2P = 3 /* relays only: the copy engine for both hops, the paper's own design
+                          ("an H2D operation and a P2P operation"): host <-> the relay's
+                          ring slot, then a peer DMA slot <-> the target, on the same relay
+                          stream, under the ring's seq/credit flags -- no SM work anywhere.
+                          A direct path given this mode uses MMA_HOP_CE. */
 } mma_hop_t;
 
 typedef enum { MMA_PATH_DIRECT = 0, MMA_PATH_RELAY = 1 } mma_path_kind_t;

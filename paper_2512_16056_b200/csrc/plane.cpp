@@ -107,7 +107,7 @@ int validate_cfg(const mma_config_t& c)
     if (c.loopback_relays < 0 || c.loopback_relays > 8) return cudaErrorInvalidValue;
     if (c.plan_mode < PLAN_CONTIGUOUS || c.plan_mode > PLAN_DYNAMIC) return cudaErrorInvalidValue;
     for (int d = 0; d < 2; d++)
-        if (c.hop_mode[d] < MMA_HOP_AUTO || c.hop_mode[d] > MMA_HOP_ZC) return cudaErrorInvalidValue;
+        if (c.hop_mode[d] < MMA_HOP_AUTO || c.hop_mode[d] > MMA_HOP_CE_P2P) return cudaErrorInvalidValue;
     if (c.relay_ctas < 1 || c.relay_ctas > 64) return cudaErrorInvalidValue;
     if (c.claim_bytes % 16) return cudaErrorInvalidValue;
     if (c.zc_ctas < 0 || c.zc_ctas > 4096) return cudaErrorInvalidValue;
@@ -677,7 +677,7 @@ private:
             // numbers advance per call) and the ledger (which retires calls by events) stay
             // out; zero-copy paths and the direct copy engine replay as they are
             for (int p = 0; p < P_; p++)
-                if (path(p).kind == MMA_PATH_RELAY && resolve_mode(j_, pmode_[p]) == MMA_HOP_CE) pp_[p].mbps = 0;
+                if (path(p).kind == MMA_PATH_RELAY && resolve_mode(j_, pmode_[p]) != MMA_HOP_ZC) pp_[p].mbps = 0;
         } else if (!j_.bw_override) {
             ledger_inputs(j_.d, j_.dir, *ps_, pp_);
         }
@@ -695,7 +695,7 @@ private:
     {
         t_.stats.fallbacks++;
         const bool small = j_.B < thr_;
-        if (small || resolve_mode(j_, pmode_[0]) == MMA_HOP_CE) {
+        if (small || resolve_mode(j_, pmode_[0]) != MMA_HOP_ZC) {
             DmaBatch b;
             j_.pieces(0, j_.B, [&](const Piece& x) { b.add(x.dst, x.src, x.len); });
             if (!small && host_order_) b.sort_by_host(kind_);   // a one-path plan, not a small copy
@@ -738,7 +738,10 @@ private:
         lists_.assign(P_, {});
         for (uint64_t i = 0; i < n_; i++) lists_[plan_.path[i]].push_back((uint32_t)i);
         mode_.resize(P_);
-        for (int p = 0; p < P_; p++) mode_[p] = resolve_mode(j_, pmode_[p]);
+        for (int p = 0; p < P_; p++) {
+            mode_[p] = resolve_mode(j_, pmode_[p]);
+            if (mode_[p] == MMA_HOP_CE_P2P && path(p).kind == MMA_PATH_DIRECT) mode_[p] = MMA_HOP_CE;
+        }
         // GPU-driven dynamic pull when every usable path moves bytes with SMs:
         // the assignment is then observed (delivery log, per-path counts), not planned
         dynamic_ = eng_.cfg.plan_mode == PLAN_DYNAMIC && !j_.timing && !j_.capturing;
@@ -767,7 +770,7 @@ private:
                 needs_tab_[path(p).gpu] = true;
                 if (host_order_ && !dynamic_) build_private(p);
                 else shared = true;
-            } else if (path(p).kind == MMA_PATH_RELAY) {
+            } else if (path(p).kind == MMA_PATH_RELAY && mode_[p] == MMA_HOP_CE) {   // the relay kernel
                 needs_tab_[j_.dir == MMA_H2D ? j_.d : path(p).gpu] = shared = true;
             }
         }
@@ -1145,7 +1148,9 @@ private:
     {
         std::vector<int> rp;   // relay paths using rings
         for (int p = 0; p < P_; p++)
-            if (!lists_[p].empty() && path(p).kind == MMA_PATH_RELAY && mode_[p] == MMA_HOP_CE) rp.push_back(p);
+            if (!lists_[p].empty() && path(p).kind == MMA_PATH_RELAY &&
+                (mode_[p] == MMA_HOP_CE || mode_[p] == MMA_HOP_CE_P2P))
+                rp.push_back(p);
         if (rp.empty()) return cudaSuccess;
         if (!eng_.wait64 || !eng_.write64) return MMA_ERR_NO_MEMOPS;
         const uint32_t S = eng_.cfg.ring_slots;
@@ -1160,6 +1165,10 @@ private:
         std::map<int, unsigned> grids;
         for (int p : rp) {
             Ring* r = rings[p];
+            if (mode_[p] == MMA_HOP_CE_P2P) {   // no kernel: the relay stream does both hops
+                r->g_next += lists_[p].size();
+                continue;
+            }
             const int kd = r->kdev;
             auto& A = launches[kd];
             if (grids.find(kd) == grids.end()) {
@@ -1209,7 +1218,7 @@ private:
         for (size_t c = 0; c < maxc; c++)
             for (int p : rp) {
                 if (c >= lists_[p].size()) continue;
-                CK(ring_hop(p, rings[p], g0[p] + c, lists_[p][c], S));
+                CK(ring_hop(p, rings[p], g0[p] + c, lists_[p][c], S, mode_[p] == MMA_HOP_CE_P2P));
                 // the path's last hop-1 (H2D) / last hop-2 (D2H) DMA closes its spans; the
                 // H2D forward of that chunk (one chunk over NVLink) is not attributed
                 if (j_.timing && c + 1 == lists_[p].size()) j_.timing->end(p);
@@ -1222,7 +1231,13 @@ private:
     // H2D: wait credit[s] >= g-S+1 (slot drained) -> DMA host -> slot -> publish seq[s] = g+1.
     // D2H: wait seq[s] >= g+1 (slot packed by the relay kernel) -> DMA slot -> host ->
     // release credit[s] = g+1.
-    int ring_hop(int p, Ring* r, uint64_t g, uint32_t i, uint32_t S)
+    // p2p (MMA_HOP_CE_P2P): the same stream also does the other hop with a peer DMA, so the
+    // slot protocol (slot g mod S on stream s & 1, seq / credit) is the kernel ring's and the
+    // two kinds of ring may follow each other on one ring. H2D: ... publish seq -> DMA slot ->
+    // target pieces -> release credit. D2H: wait credit -> DMA source pieces -> slot -> publish
+    // seq -> DMA slot -> host -> release credit. The delivery log is written behind the final
+    // DMA on the stream.
+    int ring_hop(int p, Ring* r, uint64_t g, uint32_t i, uint32_t S, bool p2p)
     {
         const uint32_t s = (uint32_t)(g % S);
         cudaStream_t hs = lanes(r->relay).hop[s & 1];
@@ -1231,31 +1246,42 @@ private:
         char* slot = r->stage + (uint64_t)s * r->slot_bytes;
         uint64_t off, len;
         j_.extent(i, &off, &len);
-        DmaBatch batch;
+        auto wait = [&](uint64_t* flag, uint64_t v) -> int {
+            return eng_.wait64((CUstream)hs, (CUdeviceptr)flag, v, CU_STREAM_WAIT_VALUE_GEQ) == CUDA_SUCCESS
+                       ? cudaSuccess : cudaErrorUnknown;
+        };
+        auto write = [&](uint64_t* flag, uint64_t v) -> int {
+            return eng_.write64((CUstream)hs, (CUdeviceptr)flag, v, 0) == CUDA_SUCCESS ? cudaSuccess
+                                                                                         : cudaErrorUnknown;
+        };
+        auto dma = [&](bool to_slot, cudaMemcpyKind kind, bool host_side, const char* name) -> int {
+            DmaBatch batch;
+            if (to_slot) j_.pieces(off, off + len, [&](const Piece& x) { batch.add(slot + (x.v - off), x.src, x.len); });
+            else j_.pieces(off, off + len, [&](const Piece& x) { batch.add(x.dst, slot + (x.v - off), x.len); });
+            if (host_side && host_order_) batch.sort_by_host(kind);
+            TSpan ts(r->relay, hs, name, p, (long long)i, len);
+            return batch.issue(kind, hs);
+        };
         if (j_.dir == MMA_H2D) {
-            if (g >= S && eng_.wait64((CUstream)hs, (CUdeviceptr)&r->credit[s], g - S + 1, CU_STREAM_WAIT_VALUE_GEQ) !=
-                              CUDA_SUCCESS)
-                return cudaErrorUnknown;
-            j_.pieces(off, off + len, [&](const Piece& x) { batch.add(slot + (x.v - off), x.src, x.len); });
-            if (host_order_) batch.sort_by_host(kind_);
-            {
-                TSpan ts(r->relay, hs, "DMA hop 1: host -> relay ring", p, (long long)i, len);
-                CK((cudaError_t)batch.issue(kind_, hs));
+            if (g >= S) CK(wait(&r->credit[s], g - S + 1));
+            CK(dma(true, cudaMemcpyHostToDevice, true, "DMA hop 1: host -> relay ring"));
+            if ((long long)g != eng_.fault_drop_publish) CK(write(&r->seq[s], g + 1));
+            if (p2p) {
+                CK(dma(false, cudaMemcpyDeviceToDevice, false, "DMA hop 2: relay ring -> target (peer)"));
+                CK(write(&r->credit[s], g + 1));
             }
-            if ((long long)g != eng_.fault_drop_publish &&
-                eng_.write64((CUstream)hs, (CUdeviceptr)&r->seq[s], g + 1, 0) != CUDA_SUCCESS)
-                return cudaErrorUnknown;
         } else {
-            if (eng_.wait64((CUstream)hs, (CUdeviceptr)&r->seq[s], g + 1, CU_STREAM_WAIT_VALUE_GEQ) != CUDA_SUCCESS)
-                return cudaErrorUnknown;
-            j_.pieces(off, off + len, [&](const Piece& x) { batch.add(x.dst, slot + (x.v - off), x.len); });
-            if (host_order_) batch.sort_by_host(kind_);
-            {
-                TSpan ts(r->relay, hs, "DMA hop 2: relay ring -> host", p, (long long)i, len);
-                CK((cudaError_t)batch.issue(kind_, hs));
+            if (p2p) {
+                if (g >= S) CK(wait(&r->credit[s], g - S + 1));
+                CK(dma(true, cudaMemcpyDeviceToDevice, false, "DMA hop 1: source (peer) -> relay ring"));
+                CK(write(&r->seq[s], g + 1));
+            } else {
+                CK(wait(&r->seq[s], g + 1));
             }
-            if (eng_.write64((CUstream)hs, (CUdeviceptr)&r->credit[s], g + 1, 0) != CUDA_SUCCESS) return cudaErrorUnknown;
+            CK(dma(false, cudaMemcpyDeviceToHost, true, "DMA hop 2: relay ring -> host"));
+            CK(write(&r->credit[s], g + 1));
         }
+        if (p2p && log_) CK(cudaMemsetAsync(log_ + i, p, 1, hs));
         return cudaSuccess;
     }
 

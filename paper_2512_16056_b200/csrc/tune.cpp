@@ -79,7 +79,14 @@ static int tune_paths(Job proto, int reps, std::vector<uint32_t>& mbps, std::vec
     int rc = cudaSuccess;
     for (int p = 0; p < P && rc == cudaSuccess; p++) {
         float best_rate = 0.f;
-        for (int m : {MMA_HOP_CE, MMA_HOP_ZC}) {
+        // candidates in order of SM use: a relay's all-copy-engine ring uses none, the kernel
+        // ring the relay kernel, zero-copy its own grid; a later candidate must win by 2%
+        const bool relay = ps[p].kind == MMA_PATH_RELAY;
+        std::vector<int> cands;
+        if (relay) cands.push_back(MMA_HOP_CE_P2P);
+        cands.push_back(MMA_HOP_CE);
+        cands.push_back(MMA_HOP_ZC);
+        for (int m : cands) {
             if (m == MMA_HOP_ZC && !proto.mapped) continue;
             for (int q = 0; q < P; q++) bw[q] = (q == p) ? 1 : 0;
             md[p] = m;
@@ -105,9 +112,9 @@ static int tune_paths(Job proto, int reps, std::vector<uint32_t>& mbps, std::vec
             }
             const float eff_ms = std::max(best, best_issue * (float)P);
             const float rate = best < 1e29f ? (float)((double)proto.B / (eff_ms * 1e-3) / 1e6) : 0.f;
-            // SM zero-copy must beat the copy engine by 2%: on a near-tie the path keeps its SMs
+            // a candidate that uses more SMs must win by 2%: on a near-tie the path keeps its SMs
             // free (§3.4.3) and the run-to-run noise of one timed call cannot flip it
-            if (rate > best_rate * (m == MMA_HOP_ZC ? 1.02f : 1.0f)) {
+            if (rate > best_rate * (best_rate > 0.f ? 1.02f : 1.0f)) {
                 best_rate = rate;
                 modes[p] = m;
                 mbps[p] = (uint32_t)llround(rate);

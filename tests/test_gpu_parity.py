@@ -57,7 +57,7 @@ H2D_CASES = [
 
 
 @pytest.mark.parametrize("B,C,lb,S,mode", H2D_CASES)
-@pytest.mark.parametrize("hop", [1, 2], ids=["ce", "zc"])
+@pytest.mark.parametrize("hop", [1, 2, 3], ids=["ce", "zc", "ce_p2p"])
 def test_h2d_contiguous(mma, orc, B, C, lb, S, mode, hop):
     configure(mma, loopback=lb, chunk=C, slots=S, plan_mode=mode, hop=(hop, hop))
     bw = [1] * (1 + lb)
@@ -76,7 +76,7 @@ def test_h2d_contiguous(mma, orc, B, C, lb, S, mode, hop):
 
 
 @pytest.mark.parametrize("B,C,lb,S,mode", H2D_CASES)
-@pytest.mark.parametrize("hop", [1, 2], ids=["ce", "zc"])
+@pytest.mark.parametrize("hop", [1, 2, 3], ids=["ce", "zc", "ce_p2p"])
 def test_d2h_contiguous(mma, orc, B, C, lb, S, mode, hop):
     configure(mma, loopback=lb, chunk=C, slots=S, plan_mode=mode, hop=(hop, hop))
     bw = [1] * (1 + lb)
@@ -267,3 +267,39 @@ def test_calibration_file_roundtrip(mma, tmp_path):
     assert (mma.get_paths(0, mma.H2D), mma.get_paths(0, mma.D2H)) == before
     configure(mma, loopback=1, chunk=MiB, debug=0)      # a different path set
     assert mma.load_calibration(str(f)) == 4            # paths 0 and 1 still match, path 2 is gone
+
+
+@pytest.mark.parametrize("dirn", [0, 1], ids=["h2d", "d2h"])
+def test_ring_kinds_alternate_on_one_ring(mma, orc, dirn):
+    """A relay ring driven by its kernel and the same ring driven by the copy engine alone
+    (MMA_HOP_CE_P2P) share one slot protocol, so calls may alternate between them -- with an
+    odd slot count, so slots change stream parity from one lap to the next."""
+    C, S = 1 << 20, 3
+    configure(mma, loopback=1, chunk=C, slots=S, plan_mode=1, hop=(1, 1), debug=1)
+    bw = [1, 2]
+    mma.set_bandwidth(0, dirn, bw)
+    B = 11 * C + 777
+    for k, relay_mode in enumerate([1, 3, 3, 1, 3, 1]):
+        mma.set_path_modes(0, dirn, [1, relay_mode])
+        mma.set_bandwidth(0, dirn, bw)
+        seed = 0x4D4D41 + k
+        rc, path, _, fb = orc.plan(bw, B, C, 0, 1)
+        if dirn == 0:
+            src = pinned(torch, B, seed=seed)
+            dst = guarded_device(torch, B)
+            mma.memcpy_h2d(dst[G:G + B], src, B)
+            torch.cuda.synchronize()
+            got = dst.cpu().numpy()
+        else:
+            dsrc = torch.empty(B, dtype=torch.uint8, device="cuda")
+            mma.fill_pattern(dsrc, B, seed, 0)
+            host = pinned(torch, B + 2 * G)
+            host.numpy()[:] = 0xA5
+            mma.memcpy_d2h(host[G:G + B], dsrc, B)
+            torch.cuda.synchronize()
+            got = host.numpy()
+        exp = guarded_host(B)
+        exp[G:G + B] = mma_inputs.pattern_bytes(seed, B, 0)
+        assert np.array_equal(got, exp), (k, relay_mode)
+        assert mma.get_delivery_log(0) == path.tobytes(), (k, relay_mode)
+        assert mma.get_last_error() == 0

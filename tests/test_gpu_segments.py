@@ -47,6 +47,8 @@ CASES = [
     (272, 192 << 10, 2, 1, 1),   # chunk not a multiple of the segment: pieces split
     (272, 192 << 10, 1, 1, 2),
     (2048, MiB, 1, 0, 2),        # 8192 segments: the radix path of the host-order sort
+    (512, MiB, 2, 1, 3),         # all-copy-engine rings: batch into slots, peer batch out
+    (272, 192 << 10, 1, 0, 3),
 ]
 
 
