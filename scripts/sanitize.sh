@@ -3,7 +3,7 @@
 # logs in gpurun_out/
 mkdir -p gpurun_out
 export MMA_SPIN_TIMEOUT_MS=60000 MMA_RANDOM_CASES=${MMA_RANDOM_CASES:-40}
-SEL='test_h2d_contiguous and (3158073 or 2101248) or test_d2h_contiguous and 3158073 or test_misaligned or test_dynamic or test_kv_fetch_h2d and 272 or test_kv_offload_d2h and 272 or test_random or test_two_processes'
+SEL='test_h2d_contiguous and (3158073 or 2101248) or test_d2h_contiguous and 3158073 or test_misaligned or test_dynamic or test_kv_fetch_h2d and 272 or test_kv_offload_d2h and 272 or test_random or test_two_processes or test_ring_kinds'
 for tool in memcheck synccheck racecheck; do
   timeout 1500 compute-sanitizer --tool $tool --target-processes all --print-limit 20 \
     python -m pytest tests/test_gpu_parity.py tests/test_gpu_dynamic.py tests/test_gpu_segments.py \
