@@ -154,8 +154,9 @@ int mma_finalize(void);
  * bytes < fallback threshold, host memory is pageable, or the target has a single path
  * (§3.2).
  * Graph capture: a call on a stream being captured is recorded as a replayable multipath
- * copy -- zero-copy paths and the direct copy engine (relay rings and the backlog ledger
- * stay out: ring sequence numbers advance per call), tables in a pinned arena made at init
+ * copy -- zero-copy paths, the direct copy engine and MMA_HOP_CE_P2P relays on two staging
+ * slots of their own (graph allocations); kernel-driven relay rings and the backlog ledger
+ * stay out (ring sequence numbers advance per call) -- tables in a pinned arena made at init
  * (MMA_GRAPH_ARENA bytes, default 16 MiB; when full, the native copy is captured) and on the
  * device as graph allocations. The engine must have made a copy on that device before the
  * capture (nothing may be allocated while capturing); else the native copy is captured.

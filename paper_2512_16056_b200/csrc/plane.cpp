@@ -636,6 +636,12 @@ private:
     };
     std::vector<Priv> priv_;
     static constexpr int kArenaFull = -1000;
+    struct CapturedAlloc {
+        int dev;
+        cudaStream_t s;
+        void* p;
+    };
+    std::vector<CapturedAlloc> captured_;   // captured relay staging, freed behind the join
 
     PathState& path(int p) { return (*ps_)[p]; }
     Lanes& lanes(int g) { return eng_.dev[g].lane[j_.dir]; }
@@ -673,11 +679,12 @@ private:
         }
         thr_ = j_.no_small_fallback ? 0 : eng_.cfg.fallback_bytes[j_.dir];
         if (j_.capturing) {
-            // a graph replays this call any number of times: relay rings (whose sequence
+            // a graph replays this call any number of times: kernel rings (whose sequence
             // numbers advance per call) and the ledger (which retires calls by events) stay
-            // out; zero-copy paths and the direct copy engine replay as they are
+            // out; zero-copy paths, the direct copy engine and all-copy-engine relays (on
+            // staging of their own, enqueue_captured_p2p) replay as they are
             for (int p = 0; p < P_; p++)
-                if (path(p).kind == MMA_PATH_RELAY && resolve_mode(j_, pmode_[p]) != MMA_HOP_ZC) pp_[p].mbps = 0;
+                if (path(p).kind == MMA_PATH_RELAY && resolve_mode(j_, pmode_[p]) == MMA_HOP_CE) pp_[p].mbps = 0;
         } else if (!j_.bw_override) {
             ledger_inputs(j_.d, j_.dir, *ps_, pp_);
         }
@@ -1152,6 +1159,11 @@ private:
                 (mode_[p] == MMA_HOP_CE || mode_[p] == MMA_HOP_CE_P2P))
                 rp.push_back(p);
         if (rp.empty()) return cudaSuccess;
+        if (j_.capturing) {
+            for (int p : rp) CK(enqueue_captured_p2p(p));   // plan() left only CE_P2P relays
+            tr_.mark("rings");
+            return cudaSuccess;
+        }
         if (!eng_.wait64 || !eng_.write64) return MMA_ERR_NO_MEMOPS;
         const uint32_t S = eng_.cfg.ring_slots;
         const uint64_t upc = (j_.C + eng_.unit_bytes - 1) / eng_.unit_bytes;
@@ -1224,6 +1236,46 @@ private:
                 if (j_.timing && c + 1 == lists_[p].size()) j_.timing->end(p);
             }
         tr_.mark("rings");
+        return cudaSuccess;
+    }
+
+    // captured all-copy-engine relay: two staging slots of its own (graph allocations on the
+    // relay, freed at the end of each replay), chunk c on hop stream c & 1 with slot c & 1, so
+    // stream order alone keeps a slot's two uses apart -- no flags, nothing shared with live
+    // rings, and every replay moves the same chunks again
+    int enqueue_captured_p2p(int p)
+    {
+        const int r = path(p).gpu;
+        Lanes& L = lanes(r);
+        const uint64_t C = j_.C;
+        char* slots[2] = {nullptr, nullptr};
+        DeviceGuard dg(r);
+        for (int k = 0; k < 2 && k < (int)lists_[p].size(); k++) {
+            CK((cudaError_t)use(L.hop[k], r));
+            CK(cudaMallocAsync((void**)&slots[k], C, L.hop[k]));
+            captured_.push_back({r, L.hop[k], slots[k]});
+        }
+        for (size_t c = 0; c < lists_[p].size(); c++) {
+            const int k = (int)(c & 1);
+            cudaStream_t hs = L.hop[k];
+            char* slot = slots[k];
+            uint64_t off, len;
+            j_.extent(lists_[p][c], &off, &len);
+            DmaBatch in, out;
+            if (j_.dir == MMA_H2D) {
+                j_.pieces(off, off + len, [&](const Piece& x) { in.add(slot + (x.v - off), x.src, x.len); });
+                j_.pieces(off, off + len, [&](const Piece& x) { out.add(x.dst, slot + (x.v - off), x.len); });
+                if (host_order_) in.sort_by_host(cudaMemcpyHostToDevice);
+                CK((cudaError_t)in.issue(cudaMemcpyHostToDevice, hs, false));
+                CK((cudaError_t)out.issue(cudaMemcpyDeviceToDevice, hs, false));
+            } else {
+                j_.pieces(off, off + len, [&](const Piece& x) { in.add(slot + (x.v - off), x.src, x.len); });
+                j_.pieces(off, off + len, [&](const Piece& x) { out.add(x.dst, slot + (x.v - off), x.len); });
+                if (host_order_) out.sort_by_host(cudaMemcpyDeviceToHost);
+                CK((cudaError_t)in.issue(cudaMemcpyDeviceToDevice, hs, false));
+                CK((cudaError_t)out.issue(cudaMemcpyDeviceToHost, hs, false));
+            }
+        }
         return cudaSuccess;
     }
 
@@ -1334,6 +1386,15 @@ private:
         {
             DeviceGuard g(j_.user_dev);
             CK(cudaEventRecord(done, j_.user));
+        }
+        for (const CapturedAlloc& c : captured_) {   // staging slots, on the stream that made them
+            DeviceGuard dg(c.dev);
+            CK(cudaStreamWaitEvent(c.s, done, 0));
+            CK(cudaFreeAsync(c.p, c.s));
+            cudaEvent_t ev = join_event(c.s, c.dev);
+            CK(cudaEventRecord(ev, c.s));
+            DeviceGuard ug(j_.user_dev);
+            CK(cudaStreamWaitEvent(j_.user, ev, 0));
         }
         for (int g = 0; g < eng_.ndev; g++) {
             if (!dtab_[g]) continue;

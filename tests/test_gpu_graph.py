@@ -1,6 +1,6 @@
 """Graph capture: a multipath copy on a stream being captured (torch.cuda.graph) is recorded
-as a replayable copy -- zero-copy paths and the direct copy engine, tables in the engine's
-pinned arena and graph allocations. Each replay must move the CURRENT bytes of the source,
+as a replayable copy -- zero-copy paths, the direct copy engine and all-copy-engine relays
+(on staging of their own), tables in the engine's pinned arena and graph allocations. Each replay must move the CURRENT bytes of the source,
 bit-exact, in both directions and for scattered tables; a capture that cannot be served
 (engine not yet initialised, arena full) records the native copy instead, still correct."""
 import os
@@ -134,3 +134,52 @@ def test_arena_full_captures_native(mma):
     finally:
         del os.environ["MMA_GRAPH_ARENA"]
         mma.finalize()
+
+
+@pytest.mark.parametrize("dirn", [0, 1], ids=["h2d", "d2h"])
+@pytest.mark.parametrize("scattered", [False, True], ids=["contig", "segments"])
+def test_captured_all_copy_engine_relay(mma, dirn, scattered):
+    """an all-copy-engine relay (MMA_HOP_CE_P2P) is captured on staging of its own: replays
+    move the current bytes through it (the relay's bytes counted at capture prove it took part)"""
+    configure(mma, loopback=1, chunk=MiB, slots=4, debug=0)
+    mma.set_path_modes(0, dirn, [mma.HOP_CE, mma.HOP_CE_P2P])
+    mma.set_bandwidth(0, dirn, [1, 1])
+    nseg, sb = 256, 48 << 10
+    B = nseg * sb
+    rng = np.random.default_rng(12)
+    perm = rng.permutation(nseg) if scattered else np.arange(nseg)
+    host = pinned(torch, B)
+    dev = torch.zeros(B, dtype=torch.uint8, device="cuda")
+    if dirn == 0:
+        segs = ([host.data_ptr() + k * sb for k in range(nseg)], [dev.data_ptr() + int(p) * sb for p in perm])
+    else:
+        segs = ([dev.data_ptr() + int(p) * sb for p in perm], [host.data_ptr() + k * sb for k in range(nseg)])
+    table, n = mma.make_segments(*segs, [sb] * nseg)
+
+    def copy():
+        if scattered:
+            (mma.memcpy_h2d_segments if dirn == 0 else mma.memcpy_d2h_segments)(table, n, 0)
+        elif dirn == 0:
+            mma.memcpy_h2d(dev, host, B)
+        else:
+            mma.memcpy_d2h(host, dev, B)
+    copy()
+    torch.cuda.synchronize()
+    r0 = mma.get_stats(0)["relay_bytes"]
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        copy()
+    assert mma.get_stats(0)["relay_bytes"] > r0
+    for seed in (31, 32):
+        if dirn == 0:
+            mma_inputs.fill_pattern(host.numpy()[:B], seed)
+        else:
+            mma.fill_pattern(dev, B, seed, 0)
+            torch.cuda.synchronize()
+            host.numpy()[:] = 0
+        g.replay()
+        torch.cuda.synchronize()
+        h = host.numpy()[:B].reshape(nseg, sb)
+        d = dev.cpu().numpy().reshape(nseg, sb)
+        assert np.array_equal(d[perm], h), seed
+    assert mma.get_last_error() == 0
