@@ -51,7 +51,7 @@ static int capture_state(cudaStream_t stream, int d)
     if (cap == cudaStreamCaptureStatusNone) return 0;
     if (cap != cudaStreamCaptureStatusActive) return -1;
     Engine& e = E();
-    if (!e.inited || !e.arena || d < 0 || d >= e.ndev) return -1;
+    if (!e.inited || !e.arena || d < 0 || d >= e.ndev || !e.tgt[d].paths_made) return -1;
     make_paths(d);
     for (int dir = 0; dir < 2; dir++)
         for (const PathState& p : e.tgt[d].paths[dir])

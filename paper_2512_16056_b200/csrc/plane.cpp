@@ -266,8 +266,12 @@ void make_paths(int d)
         std::vector<int> cand;
         if (e.cfg.npaths > 0) cand.assign(e.cfg.path_gpus, e.cfg.path_gpus + e.cfg.npaths);
         else for (int g = 0; g < e.ndev; g++) cand.push_back(g);
+        // peer access is enabled (make_device) before a relay is admitted: a pair whose
+        // cudaDeviceEnablePeerAccess failed is marked non-P2P there and never becomes a path
+        const bool dev_ok = make_device(d) == cudaSuccess;
         for (int g : cand) {
-            if (g < 0 || g >= e.ndev || g == d || !e.p2p[d][g] || !e.p2p[g][d]) continue;
+            if (g < 0 || g >= e.ndev || g == d || !dev_ok || !e.p2p[d][g] || !e.p2p[g][d]) continue;
+            if (make_device(g) != cudaSuccess || !e.p2p[d][g] || !e.p2p[g][d]) continue;
             bool dup = false;
             for (auto& p : ps) dup |= (p.gpu == g);
             if (!dup && ps.size() < MMA_MAX_PATHS) ps.push_back({g, MMA_PATH_RELAY, kDefaultMbps, e.cfg.hop_mode[dir]});
