@@ -110,6 +110,22 @@ def predict(bw, B, C_, path_of_chunk, kinds=None, backlog=None):
     return T.value, g.value
 
 
+def direct_rate(C_, depth, B, t0):
+    """Steady-state rate (bytes/s) of a direct path with `depth` outstanding DMAs (model)."""
+    f = lib().orc_direct_rate
+    f.restype = C.c_double
+    f.argtypes = [C.c_double, C.c_uint, C.c_double, C.c_double]
+    return f(C_, depth, B, t0)
+
+
+def relay_rate(C_, streams, Bp, Bn, t0):
+    """Steady-state rate (bytes/s) of a relay path with `streams` relay pipelines (model)."""
+    f = lib().orc_relay_rate
+    f.restype = C.c_double
+    f.argtypes = [C.c_double, C.c_uint, C.c_double, C.c_double, C.c_double]
+    return f(C_, streams, Bp, Bn, t0)
+
+
 def segments_from_arrays(src_ptrs, dst_ptrs, lens):
     n = len(lens)
     arr = (Segment * max(n, 1))()

@@ -703,3 +703,21 @@ int orc_ring_explore(int n, int S, uint64_t base, int fault, uint64_t* states,
     free(set.used);
     return 0;
 }
+
+
+/* ---- steady-state path throughput model (performance; header comment) ------------------ */
+
+double orc_direct_rate(double C, unsigned depth, double B, double t0)
+{
+    if (C <= 0 || B <= 0 || depth == 0) return 0.0;
+    const double per_slot = depth * C / (t0 + C / B);   /* each slot: setup then transfer */
+    return per_slot < B ? per_slot : B;                  /* the link cannot exceed B */
+}
+
+double orc_relay_rate(double C, unsigned streams, double Bp, double Bn, double t0)
+{
+    if (C <= 0 || Bp <= 0 || Bn <= 0 || streams == 0) return 0.0;
+    const double hop1 = t0 + C / Bp, hop2 = C / Bn;
+    if (streams == 1) return C / (hop1 + hop2);         /* Fig 6a: the hops serialise */
+    return C / (hop1 > hop2 ? hop1 : hop2);             /* Fig 6b: hop 2 of i under hop 1 of i+1 */
+}

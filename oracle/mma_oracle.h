@@ -83,6 +83,21 @@ void orc_predict(const orc_path* paths, int P, uint64_t B, uint64_t C,
                  const uint8_t* path_of_chunk, uint64_t n, double* T_s, double* agg_gbps);
 
 /*
+ * Steady-state throughput model of one path (performance, not bytes; §3.4.3,
+ * Fig 6; SPEC S:462-486 launch_direct / launch_relay). Rates in bytes/s, C in bytes, t0 =
+ * the DMA setup time in seconds of one chunk.
+ *   orc_direct_rate: `depth` outstanding DMAs on a link of rate B. A chunk occupies its
+ *     slot for t0 + C/B; the link is busy whenever another slot is in setup, so
+ *     rate = min(B, depth * C / (t0 + C/B)).
+ *   orc_relay_rate: a relay with `streams` relay pipelines: hop 1 (t0 + C/Bp on the relay's
+ *     PCIe link) then hop 2 (C/Bn over NVLink). One pipeline serialises the hops:
+ *     rate = C / (t0 + C/Bp + C/Bn); two or more overlap hop 2 of chunk i with hop 1 of
+ *     chunk i+1: rate = C / max(t0 + C/Bp, C/Bn).
+ */
+double orc_direct_rate(double C, unsigned depth, double B, double t0);
+double orc_relay_rate(double C, unsigned streams, double Bp, double Bn, double t0);
+
+/*
  * Move a transfer according to a plan. The host buffers stand in for both host memory and
  * device memory (D2H is the same program with the roles of src and dst swapped).
  *   segs/nsegs  the transfer as a list of segments; the contiguous case is one segment
