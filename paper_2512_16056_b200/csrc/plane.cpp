@@ -278,6 +278,20 @@ void make_paths(int d)
         }
         for (int k = 0; k < e.cfg.loopback_relays && ps.size() < MMA_MAX_PATHS; k++)
             ps.push_back({d, MMA_PATH_RELAY, kDefaultMbps, e.cfg.hop_mode[dir]});
+        // MMA_BW="mbps0,mbps1,...": a pinned vector for parity runs (SURVEY §7 hard part 7),
+        // applied when it names exactly this set's paths
+        if (const char* bwenv = getenv("MMA_BW")) {
+            std::vector<uint32_t> v;
+            for (const char* q = bwenv; *q;) {
+                char* end;
+                const unsigned long x = strtoul(q, &end, 10);
+                if (end == q) break;
+                v.push_back((uint32_t)x);
+                q = (*end == ',') ? end + 1 : end;
+            }
+            if (v.size() == ps.size())
+                for (size_t i = 0; i < ps.size(); i++) ps[i].mbps = v[i];
+        }
         // keep a previously pinned vector when the set is unchanged
         if (t.paths[dir].size() == ps.size()) {
             bool same = true;

@@ -35,3 +35,18 @@ def test_cli_show_calibrate_plan(tmp_path):
     plan = _run(["plan", "--device", "0", "--bytes", str(1 << 30)], dict(env, MMA_CALIB=str(cal)))
     assert [p["mbps"] for p in plan["paths"]] == [p["mbps"] for p in out["calibration"]["0"]["h2d"]["paths"]]
     assert sum(plan["chunks_per_path"].values()) == plan["nchunks"]
+
+
+def test_env_pinned_bandwidth():
+    """MMA_BW pins the planner's vector from the environment (parity runs): the
+    plan a fresh process reports is the oracle's plan for that vector"""
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import oracle
+    env = {"MMA_LOOPBACK": "2", "MMA_BW": "3000,2000,1000", "MMA_PLAN_MODE": "1", "MMA_FALLBACK_BYTES": "0",
+           "MMA_CHUNK_BYTES": str(1 << 20)}
+    out = _run(["plan", "--device", "0", "--bytes", str(37 << 20)], env)
+    assert [p["mbps"] for p in out["paths"]] == [3000, 2000, 1000]
+    rc, path, counts, fb = oracle.plan([3000, 2000, 1000], 37 << 20, 1 << 20, 0, 1)
+    assert out["chunks_per_path"] == {str(p): int(c) for p, c in enumerate(counts) if c}
