@@ -202,6 +202,13 @@ int mma_set_path_modes(int device, mma_dir_t dir, const int* modes, int npaths);
  * bandwidth (integer MB/s, reading R17: llround). Synchronous. */
 int mma_calibrate(int device, mma_dir_t dir, size_t bytes);
 
+/* Chunk size by measurement (§3.4.1 "dynamically adjusts"; reading R3): times
+ * a contiguous copy of `bytes` (>= 2 MiB) through library-owned buffers at chunk sizes
+ * 32, 16, 8, 4, 2, 1 MiB (those <= bytes / 2) with the current bandwidth vector and modes,
+ * and sets cfg.chunk_bytes[dir] to the fastest (a smaller chunk must be >= 1% faster).
+ * *chunk_out (may be NULL) receives it. Synchronous; rings are re-made for the new size. */
+int mma_tune_chunk(int device, mma_dir_t dir, size_t bytes, size_t* chunk_out);
+
 /* Fallback threshold by measurement (§3.2, §5.1.3: below a break-even size
  * the native single-path copy wins). Times the native copy and the multipath copy (current
  * bandwidth vector and modes) at sizes chunk, 2*chunk, 4*chunk, ... <= max_bytes through

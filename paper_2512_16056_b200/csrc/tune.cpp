@@ -263,6 +263,60 @@ int mma_calibrate(int device, mma_dir_t dir, size_t bytes)
     return calibrate_job(j, 3, 0);
 }
 
+// Chunk size by measurement (§3.4.1: the Task Manager "dynamically adjusts" the chunk
+// size; P:902 tuned optima 2.81 / 5.37 MB on H20; reading R3). Each candidate C in
+// {1, 2, 4, 8, 16, 32} MiB not above bytes / 2 is timed on a contiguous copy of `bytes` with
+// the current vector and modes (best of 3 after a warm-up); the fastest is kept, a smaller
+// chunk only when it is >= 1% faster (fewer DMAs, memops and flags per byte otherwise).
+int mma_tune_chunk(int device, mma_dir_t dir, size_t bytes, size_t* chunk_out)
+{
+    CK((cudaError_t)ensure_init());
+    Engine& e = E();
+    if (device < 0 || device >= e.ndev) return cudaErrorInvalidDevice;
+    if ((dir != MMA_H2D && dir != MMA_D2H) || bytes < (2u << 20)) return cudaErrorInvalidValue;
+    std::lock_guard<std::mutex> g(e.mu);
+    CK(make_device(device));
+    make_paths(device);
+    DeviceGuard dg(device);
+    CalBuffers cb(device, bytes);
+    CK(cb.rc);
+    cudaEvent_t a = nullptr, b = nullptr;
+    CK(cudaEventCreate(&a));
+    CK(cudaEventCreate(&b));
+    const size_t keep = e.cfg.chunk_bytes[dir];
+    size_t best_c = keep;
+    float best_ms = 1e30f;
+    int rc = cudaSuccess;
+    for (size_t C = 32u << 20; C >= (1u << 20) && rc == cudaSuccess; C >>= 1) {   // large first
+        if (C > bytes / 2) continue;
+        e.cfg.chunk_bytes[dir] = C;
+        Job proto = cb.job(dir, bytes);
+        if ((rc = reserve_tables(proto)) != cudaSuccess) break;
+        float best = 1e30f;
+        for (int rep = 0; rep <= 3 && rc == cudaSuccess; rep++) {
+            Job j = cb.job(dir, bytes);
+            j.no_small_fallback = true;
+            cudaEventRecord(a, cb.s);
+            rc = run_job(j);
+            cudaEventRecord(b, cb.s);
+            if (rc == cudaSuccess && cudaEventSynchronize(b) != cudaSuccess) rc = cudaErrorUnknown;
+            float ms = 0;
+            cudaEventElapsedTime(&ms, a, b);
+            if (rep > 0 && ms > 0) best = std::min(best, ms);
+        }
+        if (best < best_ms * 0.99f) {
+            best_ms = best;
+            best_c = C;
+        }
+    }
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+    if (rc == cudaSuccess && sticky()) rc = sticky();
+    e.cfg.chunk_bytes[dir] = rc == cudaSuccess ? best_c : keep;
+    if (chunk_out) *chunk_out = e.cfg.chunk_bytes[dir];
+    return rc;
+}
+
 // Break-even ("thr defaults to the measured B200 break-even"; the paper's
 // 11.3 MB H2D / 13 MB D2H on H20, §5.1.3). Sizes C, 2C, 4C, ... up to max_bytes: each
 // is timed as the native copy on one stream and as the multipath copy with the current

@@ -32,7 +32,7 @@ SYMBOLS = [
     "mma_copy_share_segments", "mma_copy_claim_segments", "mma_trace_begin", "mma_trace_end",
     "mma_save_calibration", "mma_load_calibration", "mma_host_alloc_for", "mma_host_page_node",
     "mma_get_calibration", "mma_tune_threshold", "mma_ledger_attach", "mma_ledger_unlink",
-    "mma_ledger_shared_add", "mma_ledger_shared_get", "mma_device_bus_id", "mma_get_topology", "mma_order_by_address",
+    "mma_ledger_shared_add", "mma_ledger_shared_get", "mma_device_bus_id", "mma_get_topology", "mma_order_by_address", "mma_tune_chunk",
 ]
 
 
@@ -133,6 +133,7 @@ def lib():
         L.mma_ledger_unlink.argtypes = [C.c_char_p]
         L.mma_ledger_shared_add.argtypes = [C.c_char_p, C.c_int, C.c_int64, C.c_int64]
         L.mma_ledger_shared_get.argtypes = [C.c_char_p, C.c_int, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]
+        L.mma_tune_chunk.argtypes = [C.c_int, C.c_int, sz, C.POINTER(sz)]
         L.mma_tune_threshold.argtypes = [C.c_int, C.c_int, sz, C.POINTER(sz), C.POINTER(C.c_int)]
         L.mma_get_calibration.argtypes = [C.c_int, C.c_int, C.c_int, vp, vp, C.c_int, C.POINTER(C.c_int)]
         L.mma_get_dynamic_counts.argtypes = [C.c_int, vp, C.c_int, C.POINTER(C.c_int)]
@@ -274,6 +275,13 @@ def tune_segments(segs, nsegs: int, device: int, direction: int, stream=None, re
     """Measure CE vs SM zero-copy per path on this scattered transfer (writes the dsts)."""
     _check(lib().mma_tune_segments(segs, nsegs, device, direction, _stream(stream, device), reps),
            "mma_tune_segments")
+
+
+def tune_chunk(device: int, direction: int, nbytes: int = 512 << 20) -> int:
+    """Pick the chunk size by measurement (returns the size now in effect)."""
+    c = C.c_size_t()
+    _check(lib().mma_tune_chunk(device, direction, nbytes, C.byref(c)), "mma_tune_chunk")
+    return int(c.value)
 
 
 def tune_threshold(device: int, direction: int, max_bytes: int = 256 << 20):

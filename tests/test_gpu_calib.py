@@ -136,3 +136,25 @@ def test_threshold_by_measurement(mma, dirn):
     configure(mma, loopback=0, chunk=4 * MiB, debug=0, thr=0)
     assert mma.tune_threshold(0, dirn, 32 * MiB) == (0, False)
     assert mma.get_last_error() == 0
+
+
+def test_chunk_size_by_measurement(mma, orc):
+    """mma_tune_chunk (P:526 'dynamically adjusts', reading R3): the chosen size is one of the
+    candidates, becomes the planner's chunk, and copies stay byte- and plan-exact with it"""
+    configure(mma, loopback=1, chunk=4 * MiB, slots=4, debug=1)
+    mma.set_path_modes(0, mma.H2D, [mma.HOP_CE, mma.HOP_CE_P2P])
+    mma.set_bandwidth(0, mma.H2D, [1, 1])
+    C = mma.tune_chunk(0, mma.H2D, 256 * MiB)
+    assert C in [k * MiB for k in (1, 2, 4, 8, 16, 32)], C
+    B = 3 * C + 12345
+    path, fb = mma.get_plan(0, mma.H2D, B)
+    assert not fb and len(path) == 4
+    rc, exp_path, _, _ = orc.plan([1, 1], B, C, 0, 0)
+    assert path == exp_path.tobytes()
+    src = pinned(torch, B, seed=8)
+    dst = torch.zeros(B, dtype=torch.uint8, device="cuda")
+    mma.memcpy_h2d(dst, src, B)
+    torch.cuda.synchronize()
+    assert torch.equal(dst.cpu(), src[:B])
+    assert mma.get_delivery_log(0) == exp_path.tobytes()
+    assert mma.get_last_error() == 0
