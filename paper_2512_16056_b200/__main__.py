@@ -55,6 +55,8 @@ def main(argv=None) -> int:
             for name, dv in (("h2d", mma.H2D), ("d2h", mma.D2H)):
                 mma.calibrate(d, dv, a.bytes)
                 r = {"paths": mma.get_paths(d, dv), "rates": mma.get_calibration(d, dv)}
+                if len(r["paths"]) > 1 and a.bytes >= (2 << 20):
+                    r["chunk_bytes"] = mma.tune_chunk(d, dv, a.bytes)   # set MMA_CHUNK_BYTES_H2D/_D2H
                 if not a.no_threshold and len(r["paths"]) > 1:
                     thr, found = mma.tune_threshold(d, dv, a.bytes)
                     r["fallback_bytes"] = thr if found else None
