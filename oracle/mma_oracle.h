@@ -21,6 +21,9 @@
  *   - the paper's invariants (north_star): every byte delivered exactly once; a chunk is
  *     forwarded only after its staging write completes; a slot is reused only after its
  *     forward completes.
+ *   - a steady-state throughput model of one path (performance, not bytes): direct path
+ *     with `depth` outstanding DMAs, relay with one or two pipelines (Fig 6;
+ *     SPEC S:462-486), pinned by SPEC's worked numbers and a discrete-event schedule.
  * Every function is pinned by tests/test_oracle_*.py against closed forms, worked
  * examples (tests/golden/) or brute force; see DESIGN.md §3 "Pins".
  */
