@@ -294,6 +294,18 @@ class PcieCounters:
             raise RuntimeError(f"NVML PCIe counters unsupported ({v[0].nvmlReturn}, {v[1].nvmlReturn})")
         return [int(v[0].value.ullVal), int(v[1].value.ullVal)]
 
+    def nvlink_kib(self):
+        """NVML cumulative NVLink data counters per GPU (KiB: [rx, tx]) or None if unsupported
+        (relay bytes cross NVLink)."""
+        N, out = self.N, []
+        for h in self.h:
+            v = N.nvmlDeviceGetFieldValues(h, [N.NVML_FI_DEV_NVLINK_THROUGHPUT_DATA_RX,
+                                               N.NVML_FI_DEV_NVLINK_THROUGHPUT_DATA_TX])
+            if v[0].nvmlReturn or v[1].nvmlReturn:
+                return None
+            out.append([int(v[0].value.ullVal), int(v[1].value.ullVal)])
+        return out
+
     def _pass(self):
         with self.lock:
             for i, h in enumerate(self.h):
@@ -331,10 +343,12 @@ def pcie_hw_check(torch, mma, w, stream, path_gpus, dynamic):
         for half, (dname, col) in enumerate((("h2d", 0), ("d2h", 1))):
             mma.reset_stats(0)
             a = cnt.mark()
+            na = cnt.nvlink_kib()
             run_half(mma, w, 0, stream, half)
             for g in gset:
                 torch.cuda.synchronize(g)
             b = cnt.mark()
+            nb = cnt.nvlink_kib()
             st = mma.get_stats(0)
             paths = mma.get_paths(0, mma.H2D if half == 0 else mma.D2H)
             rows = []
@@ -342,8 +356,12 @@ def pcie_hw_check(torch, mma, w, stream, path_gpus, dynamic):
                 hw = b[i][col] - a[i][col]
                 planned = None if dynamic else sum(int(st["path_bytes"][half][p]) for p, pi in enumerate(paths)
                                                    if pi["gpu"] == g)
-                rows.append({"gpu": g, "planned_bytes": planned, ("rx_bytes" if col == 0 else "tx_bytes"): hw,
-                             "ratio": round(hw / planned, 4) if planned else None})
+                row = {"gpu": g, "planned_bytes": planned, ("rx_bytes" if col == 0 else "tx_bytes"): hw,
+                       "ratio": round(hw / planned, 4) if planned else None}
+                if na is not None and nb is not None:   # relayed bytes crossing NVLink (KiB counters)
+                    row["nvlink_rx_kib"] = nb[i][0] - na[i][0]
+                    row["nvlink_tx_kib"] = nb[i][1] - na[i][1]
+                rows.append(row)
             out[dname] = rows
         return out
     finally:
