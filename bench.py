@@ -513,6 +513,36 @@ def conc_rate(torch, gpus, per_gpu=512 * MiB, reps=3):
     return out
 
 
+def nvlink_rate(torch, target, relays, per_gpu=512 * MiB, reps=3):
+    """NVLink ingress into / egress out of the target from every relay at once (SURVEY 8(d):
+    the roofline term PCIe[d] + NVLinkIn[d]): each relay's copy engine moves its own buffer
+    to (from) the target concurrently; wall time around the whole set, best of reps."""
+    if not relays:
+        return None
+    tgt = [torch.empty(per_gpu, dtype=torch.uint8, device=f"cuda:{target}") for _ in relays]
+    src = [torch.empty(per_gpu, dtype=torch.uint8, device=f"cuda:{g}") for g in relays]
+    streams = [torch.cuda.Stream(device=g) for g in relays]
+    out = {}
+    for name in ("ingress", "egress"):
+        best = 1e9
+        for _ in range(reps):
+            for g in [target] + list(relays):
+                torch.cuda.synchronize(g)
+            t0 = time.perf_counter()
+            for i, g in enumerate(relays):
+                with torch.cuda.device(g), torch.cuda.stream(streams[i]):
+                    if name == "ingress":
+                        tgt[i].copy_(src[i], non_blocking=True)
+                    else:
+                        src[i].copy_(tgt[i], non_blocking=True)
+            for st in streams:
+                st.synchronize()
+            best = min(best, time.perf_counter() - t0)
+        out[name] = len(relays) * per_gpu / best / 1e9
+    del tgt, src
+    return out
+
+
 def timeline_summary(path):
     """Per-GPU busy time and GPU concurrency of one traced step (engine Chrome trace)."""
     ev = json.load(open(path))["traceEvents"]
@@ -1058,6 +1088,15 @@ def main():
     dram = dram_read_rate(torch)
     terms = {"h2d": {"pcie_sum": R_h2d, "dram_lb": max(dram, conc["h2d"])},
              "d2h": {"pcie_sum": R_d2h, "dram_lb": max(dram, conc["d2h"])}}
+    nvl = None
+    relay_gpus = [g for g in gset if g != 0]
+    if relay_gpus:        # the target's own link plus everything NVLink brings in / takes out
+        try:
+            nvl = nvlink_rate(torch, 0, relay_gpus)
+            terms["h2d"]["ingress"] = pcie[0]["h2d"] + nvl["ingress"]
+            terms["d2h"]["ingress"] = pcie[0]["d2h"] + nvl["egress"]
+        except Exception as ex:  # noqa: BLE001 - evidence only
+            nvl = {"error": f"{type(ex).__name__}: {ex}"}
     Rh, Rd = min(terms["h2d"].values()), min(terms["d2h"].values())
     R_step = nbytes_step / 2 / (Rh * 1e9) + nbytes_step / 2 / (Rd * 1e9)
     path_roof = {"R_h2d_gbps": round(Rh, 2), "R_d2h_gbps": round(Rd, 2),
@@ -1067,6 +1106,7 @@ def main():
                  "frac_step": round(value / (nbytes_step / R_step / 1e9), 4),
                  "R_conc": {k2: round(v, 2) for k2, v in conc.items()},
                  "cpu_dram_read_gbps": round(dram, 2),
+                 "nvlink_gbps": {k2: round(v, 1) for k2, v in nvl.items()} if nvl and "error" not in nvl else nvl,
                  # SURVEY 8(c) bound: a rate above 1.02 x R is a timing bug, not a result
                  "above_roofline_flag": bool(h2d_gbps > 1.02 * Rh or d2h_gbps > 1.02 * Rd),
                  "pcie_solo": {str(g): {k2: round(v, 2) for k2, v in pcie[g].items()} for g in path_gpus},
