@@ -1321,7 +1321,9 @@ def main():
                                 "active (0: single path, not refined)"},
         "engine": {"issue_us_per_call": round((st["issue_us"] - st["wait_us"]) / max(1, st["calls"]), 1),
                    "blocked_us_per_call": round(st["wait_us"] / max(1, st["calls"]), 1),
-                   "relay_bytes": int(st["relay_bytes"]), "fallbacks": int(st["fallbacks"])},
+                   "relay_bytes": int(st["relay_bytes"]), "fallbacks": int(st["fallbacks"]),
+                   "numa_local_of_known_bytes": [int(st["numa_local_bytes"][0]), int(st["numa_known_bytes"][0]),
+                                                 int(st["numa_local_bytes"][1]), int(st["numa_known_bytes"][1])]},
         "paper_context": "245 GB/s = 4.62x one 53 GB/s PCIe link, 8x H20 (P:737); context only",
     }
     print(json.dumps(line), flush=True)

@@ -122,6 +122,13 @@ typedef struct {
      * (profiles/r01_probe_sort.jsonl). 0 = table order, 1 = D2H (default), 2 = both
      * directions. */
     int host_order;
+    /* NUMA-affine planning of scattered transfers (north_star (b); reading R23): when the
+     * path GPUs sit on more than one NUMA node, a scattered table is planned as the stable
+     * regrouping of its segments by host node, groups in path order, and relays are ordered
+     * with the target's node first, so the contiguous plan gives each path (mostly) the
+     * bytes on its own GPU's node. Bytes are unchanged; mma_get_stats reports local bytes.
+     * 0 = off, 1 = auto (default; inert on a one-node host). */
+    int numa_plan;
 } mma_config_t;
 
 typedef struct {
@@ -133,6 +140,8 @@ typedef struct {
     double issue_us;                      /* host time spent enqueueing (incl. wait_us) */
     double wait_us;                       /* of which blocked on table-buffer reuse */
     uint64_t dynamic_calls;               /* calls moved by GPU-driven dynamic pull */
+    uint64_t numa_known_bytes[2];         /* [direction] bytes whose host NUMA node is known */
+    uint64_t numa_local_bytes[2];         /* of those, carried by a path on the same node */
 } mma_stats_t;
 
 /* Fill cfg with defaults (then env MMA_* overrides). */

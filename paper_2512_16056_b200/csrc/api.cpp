@@ -336,13 +336,7 @@ int mma_get_topology(mma_topology_t* out)
         CK(cudaDeviceGetAttribute(&out->copy_engines[a], cudaDevAttrAsyncEngineCount, a));
         CK(cudaDeviceGetAttribute(&out->sms[a], cudaDevAttrMultiProcessorCount, a));
         CK(cudaDeviceGetPCIBusId(out->bus_id[a], sizeof out->bus_id[a], a));
-        std::string bus = out->bus_id[a];
-        for (char& c : bus) c = (char)tolower((unsigned char)c);
-        out->numa_node[a] = -1;
-        if (FILE* f = fopen(("/sys/bus/pci/devices/" + bus + "/numa_node").c_str(), "r")) {
-            if (fscanf(f, "%d", &out->numa_node[a]) != 1) out->numa_node[a] = -1;
-            fclose(f);
-        }
+        out->numa_node[a] = gpu_numa_node(a);
     }
     for (int i = 0; i < 256; i++) {
         char p[96];
@@ -556,22 +550,6 @@ int mma_host_alloc(void** ptr, size_t bytes, unsigned flags)
 }
 
 int mma_host_free(void* ptr) { return host_free(ptr); }
-
-// NUMA node of GPU d's PCIe device (sysfs), or -1 when the host does not expose one.
-static int gpu_numa_node(int d)
-{
-    char bdf[32] = {0};
-    if (cudaDeviceGetPCIBusId(bdf, sizeof bdf, d) != cudaSuccess) { cudaGetLastError(); return -1; }
-    for (char* c = bdf; *c; c++) *c = (char)tolower(*c);
-    char path[96];
-    snprintf(path, sizeof path, "/sys/bus/pci/devices/%s/numa_node", bdf);
-    FILE* f = fopen(path, "r");
-    if (!f) return -1;
-    int n = -1;
-    if (fscanf(f, "%d", &n) != 1) n = -1;
-    fclose(f);
-    return n;
-}
 
 int mma_host_alloc_for(void** ptr, size_t bytes, int device, mma_dir_t dir)
 {

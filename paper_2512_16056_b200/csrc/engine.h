@@ -29,5 +29,11 @@ int host_alloc(void** ptr, size_t bytes, int numa_mode, int node0);
 int host_free(void* ptr);
 int host_alloc_ranges(void** ptr, size_t bytes, const uint64_t* range_end, const int* node, int nranges);
 int host_page_node(const void* p);
+// NUMA node of each host address (2 MiB regions cached; MMA_FAKE_HOST_NODES=K (tests): node =
+// (address >> 21) mod K); -1 = unknown
+void host_nodes(const void* const* p, size_t n, int* nodes);
+int host_numa_count();
+// NUMA node of a GPU's PCI device from sysfs (-1 = unknown)
+int gpu_numa_node(int dev);
 
 }  // namespace mma

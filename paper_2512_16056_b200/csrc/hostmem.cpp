@@ -12,10 +12,14 @@
 #include <unistd.h>
 
 #include <algorithm>
+#include <cctype>
 #include <cstdio>
 #include <cstring>
 #include <map>
 #include <mutex>
+#include <string>
+#include <unordered_map>
+#include <vector>
 
 #include "engine.h"
 
@@ -134,6 +138,61 @@ int host_page_node(const void* p)
     int status[1] = {-1};
     if (syscall(SYS_move_pages, 0, 1ul, pages, nullptr, status, 0) != 0) return -1;
     return status[0];
+}
+
+int host_numa_count() { return numa_nodes(); }
+
+void host_nodes(const void* const* p, size_t n, int* nodes)
+{
+    if (const char* fk = getenv("MMA_FAKE_HOST_NODES")) {   // test hook: 2 MiB regions round-robin
+        const long k = atol(fk);
+        for (size_t i = 0; i < n; i++) nodes[i] = k > 0 ? (int)((reinterpret_cast<uintptr_t>(p[i]) >> 21) % k) : -1;
+        return;
+    }
+    if (numa_nodes() < 2) {
+        for (size_t i = 0; i < n; i++) nodes[i] = 0;
+        return;
+    }
+    static std::mutex mu;
+    static std::unordered_map<uintptr_t, int> cache;   // 2 MiB region -> node (pinned pages stay)
+    std::lock_guard<std::mutex> g(mu);
+    std::vector<void*> ask;
+    std::vector<size_t> who;
+    for (size_t i = 0; i < n; i++) {
+        const uintptr_t r = reinterpret_cast<uintptr_t>(p[i]) >> 21;
+        auto it = cache.find(r);
+        if (it != cache.end()) nodes[i] = it->second;
+        else { nodes[i] = -2; ask.push_back(const_cast<void*>(p[i])); who.push_back(i); }
+    }
+    if (!ask.empty()) {   // one move_pages query (nodes = NULL: report) for every unknown region
+        std::vector<int> st(ask.size(), -1);
+        if (syscall(SYS_move_pages, 0, (unsigned long)ask.size(), ask.data(), nullptr, st.data(), 0) != 0)
+            std::fill(st.begin(), st.end(), -1);
+        for (size_t q = 0; q < ask.size(); q++) {
+            const int nd = st[q] >= 0 ? st[q] : -1;
+            cache[reinterpret_cast<uintptr_t>(ask[q]) >> 21] = nd;
+            nodes[who[q]] = nd;
+        }
+        for (size_t i = 0; i < n; i++)   // repeats of a region asked in this call
+            if (nodes[i] == -2) nodes[i] = cache[reinterpret_cast<uintptr_t>(p[i]) >> 21];
+    }
+}
+
+int gpu_numa_node(int dev)
+{
+    char bus[32] = {0};
+    if (cudaDeviceGetPCIBusId(bus, sizeof bus - 1, dev) != cudaSuccess) {
+        cudaGetLastError();
+        return -1;
+    }
+    std::string b = bus;
+    for (char& c : b) c = (char)tolower((unsigned char)c);
+    int node = -1;
+    if (FILE* f = fopen(("/sys/bus/pci/devices/" + b + "/numa_node").c_str(), "r")) {
+        if (fscanf(f, "%d", &node) != 1) node = -1;
+        fclose(f);
+    }
+    return node;
 }
 
 }  // namespace mma

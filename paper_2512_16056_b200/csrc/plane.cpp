@@ -68,6 +68,7 @@ void apply_env(mma_config_t* c)
     c->zc_ctas = env_int("MMA_ZC_CTAS", c->zc_ctas);
     c->calib_rounds = env_int("MMA_CALIB_ROUNDS", c->calib_rounds);
     c->host_order = env_int("MMA_HOST_ORDER", c->host_order);
+    c->numa_plan = env_int("MMA_NUMA_PLAN", c->numa_plan);
     if (const char* s = getenv("MMA_PATHS")) {   // comma-separated relay GPU ids
         c->npaths = 0;
         for (const char* p = s; *p && c->npaths < MMA_MAX_PATHS;) {
@@ -96,6 +97,7 @@ void defaults(mma_config_t* c)
     c->zc_ctas = kDefaultZcCtas;
     c->calib_rounds = 2;
     c->host_order = 1;
+    c->numa_plan = 1;
 }
 
 int validate_cfg(const mma_config_t& c)
@@ -113,6 +115,7 @@ int validate_cfg(const mma_config_t& c)
     if (c.zc_ctas < 0 || c.zc_ctas > 4096) return cudaErrorInvalidValue;
     if (c.calib_rounds < 0 || c.calib_rounds > 16) return cudaErrorInvalidValue;
     if (c.host_order < 0 || c.host_order > 2) return cudaErrorInvalidValue;
+    if (c.numa_plan < 0 || c.numa_plan > 1) return cudaErrorInvalidValue;
     return cudaSuccess;
 }
 
@@ -278,6 +281,25 @@ void make_paths(int d)
         }
         for (int k = 0; k < e.cfg.loopback_relays && ps.size() < MMA_MAX_PATHS; k++)
             ps.push_back({d, MMA_PATH_RELAY, kDefaultMbps, e.cfg.hop_mode[dir]});
+        // NUMA (reading R23): each path's GPU node; relays on the target's node first (stable),
+        // so the first group of a node-grouped table meets the target's own link
+        for (auto& p : ps) p.node = gpu_numa_node(p.gpu);
+        if (e.cfg.numa_plan) {
+            const int nd = ps[0].node;
+            std::stable_sort(ps.begin() + 1, ps.end(), [nd](const PathState& a, const PathState& b) {
+                return (a.node != nd) < (b.node != nd);
+            });
+        }
+        if (const char* fk = getenv("MMA_FAKE_PATH_NODES")) {   // test hook: node per path index
+            size_t i = 0;
+            for (const char* q = fk; *q && i < ps.size(); i++) {
+                char* end;
+                const long x = strtol(q, &end, 10);
+                if (end == q) break;
+                ps[i].node = (int)x;
+                q = (*end == ',') ? end + 1 : end;
+            }
+        }
         // MMA_BW="mbps0,mbps1,...": a pinned vector for parity runs (SURVEY §7 hard part 7),
         // applied when it names exactly this set's paths
         if (const char* bwenv = getenv("MMA_BW")) {
@@ -660,6 +682,10 @@ private:
         void* p;
     };
     std::vector<CapturedAlloc> captured_;   // captured relay staging, freed behind the join
+    // NUMA (R23): the host node of every segment (when the path set spans two or more nodes)
+    // and, with numa_plan, the table regrouped by node in path order
+    std::vector<int> seg_node_;
+    std::vector<mma_segment_t> reseg_;
 
     PathState& path(int p) { return (*ps_)[p]; }
     Lanes& lanes(int g) { return eng_.dev[g].lane[j_.dir]; }
@@ -745,9 +771,75 @@ private:
         return cudaSuccess;
     }
 
+    // ---- NUMA-affine regrouping (reading R23): segments stably grouped by the NUMA node of
+    // their host memory, groups in the order of the usable paths' nodes (the target's first),
+    // then other nodes, unknown last. The virtual stream is the regrouped table, so the
+    // contiguous plan gives each path the bytes of its own node except at group boundaries.
+    int numa_regroup()
+    {
+        if (j_.contiguous || j_.nseg < 2) return cudaSuccess;
+        std::vector<int> order;   // distinct known nodes of the paths that may carry bytes
+        for (int p = 0; p < P_; p++) {
+            const int nd = path(p).node;
+            if (pp_[p].mbps == 0 || nd < 0) continue;
+            if (std::find(order.begin(), order.end(), nd) == order.end()) order.push_back(nd);
+        }
+        if (order.size() < 2) return cudaSuccess;
+        const uint64_t n = j_.nseg;
+        std::vector<const void*> hp(n);
+        for (uint64_t k = 0; k < n; k++) hp[k] = j_.dir == MMA_H2D ? j_.segs[k].src : j_.segs[k].dst;
+        seg_node_.resize(n);
+        host_nodes(hp.data(), n, seg_node_.data());
+        if (!eng_.cfg.numa_plan) return cudaSuccess;   // nodes kept for the statistics only
+        auto rank = [&](int nd) -> int {
+            if (nd < 0) return 1 << 30;
+            for (size_t r = 0; r < order.size(); r++)
+                if (order[r] == nd) return (int)r;
+            return (int)order.size() + nd;
+        };
+        std::vector<uint32_t> idx(n);
+        for (uint64_t k = 0; k < n; k++) idx[k] = (uint32_t)k;
+        std::stable_sort(idx.begin(), idx.end(), [&](uint32_t a, uint32_t b) {
+            return rank(seg_node_[a]) < rank(seg_node_[b]);
+        });
+        reseg_.resize(n);
+        std::vector<int> nodes(n);
+        for (uint64_t k = 0; k < n; k++) {
+            reseg_[k] = j_.segs[idx[k]];
+            nodes[k] = seg_node_[idx[k]];
+        }
+        seg_node_.swap(nodes);
+        j_.segs = reseg_.data();
+        for (uint64_t k = 0; k < n; k++) j_.vstart[k + 1] = j_.vstart[k] + j_.segs[k].bytes;
+        return cudaSuccess;
+    }
+
+    // bytes whose host node is known, and of those the bytes carried by a path on that node
+    void numa_stats()
+    {
+        if (seg_node_.empty() || dynamic_) return;
+        uint64_t known = 0, local = 0;
+        for (uint64_t i = 0; i < n_; i++) {
+            const int pn = path(plan_.path[i]).node;
+            uint64_t a, len;
+            j_.extent(i, &a, &len);
+            const uint64_t b = a + len;
+            uint64_t k = std::upper_bound(j_.vstart.begin(), j_.vstart.end(), a) - j_.vstart.begin() - 1;
+            for (; k < j_.nseg && j_.vstart[k] < b; k++) {
+                const uint64_t lo = std::max(j_.vstart[k], a), hi = std::min(j_.vstart[k + 1], b);
+                if (lo >= hi || seg_node_[k] < 0) continue;
+                known += hi - lo;
+                if (seg_node_[k] == pn) local += hi - lo;
+            }
+        }
+        t_.stats.numa_known_bytes[j_.dir] += known;
+        t_.stats.numa_local_bytes[j_.dir] += local;
+    }
+
     // ---- table buffers, devices, per-path chunk lists and modes
     int prepare()
     {
+        CK(numa_regroup());
         n_ = plan_.n;
         sc_ = &t_.scratch[t_.parity & 3];
         if (!j_.capturing) t_.parity++;
@@ -779,6 +871,7 @@ private:
             for (int p = 0; p < P_; p++) active_[p] = pp_[p].mbps > 0;
         claimC_ = eng_.cfg.claim_bytes ? eng_.cfg.claim_bytes : (256u << 10);
         n_log_ = dynamic_ ? (j_.B - 1) / claimC_ + 1 : n_;
+        numa_stats();
         return cudaSuccess;
     }
 

@@ -102,6 +102,7 @@ struct PathState {
     // calibration evidence (mma_get_calibration): [0] contiguous, [1] scattered
     uint32_t solo_mbps[2] = {0, 0};   // solo rate of the chosen mode
     uint32_t conc_mbps[2] = {0, 0};   // rate with every path of the set active (0 = not measured)
+    int node = -1;                    // NUMA node of the path's GPU (R23; -1 = unknown)
 };
 
 struct Scratch {    // per-call table uploads, double-buffered by call parity

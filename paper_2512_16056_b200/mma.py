@@ -54,6 +54,7 @@ class Config(C.Structure):
         ("zc_ctas", C.c_int),
         ("calib_rounds", C.c_int),
         ("host_order", C.c_int),
+        ("numa_plan", C.c_int),
     ]
 
 
@@ -75,6 +76,7 @@ class Stats(C.Structure):
         ("path_bytes", (C.c_uint64 * MAX_PATHS) * 2), ("path_chunks", (C.c_uint64 * MAX_PATHS) * 2),
         ("relay_bytes", C.c_uint64), ("kernels", C.c_uint64), ("issue_us", C.c_double),
         ("wait_us", C.c_double), ("dynamic_calls", C.c_uint64),
+        ("numa_known_bytes", C.c_uint64 * 2), ("numa_local_bytes", C.c_uint64 * 2),
     ]
 
 
@@ -410,7 +412,8 @@ def get_stats(device: int) -> dict:
     return dict(calls=s.calls, fallbacks=s.fallbacks, bytes=s.bytes,
                 path_bytes=[list(x) for x in s.path_bytes], path_chunks=[list(x) for x in s.path_chunks],
                 relay_bytes=s.relay_bytes, kernels=s.kernels, issue_us=s.issue_us,
-                wait_us=s.wait_us, dynamic_calls=s.dynamic_calls)
+                wait_us=s.wait_us, dynamic_calls=s.dynamic_calls,
+                numa_known_bytes=list(s.numa_known_bytes), numa_local_bytes=list(s.numa_local_bytes))
 
 
 def set_plan_mode(mode: int) -> None:
