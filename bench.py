@@ -185,7 +185,7 @@ def host_buffer(torch, mma, nbytes):
     nodes = len(list(Path("/sys/devices/system/node").glob("node[0-9]*")))
     ptr = mma.host_alloc(nbytes)
     t = torch.from_numpy(mma.host_array(ptr, nbytes))
-    how = f"mma_host_alloc, pages interleaved over {nodes} NUMA nodes" if nodes > 1 else \
+    how = f"mma_host_alloc, 2 MiB blocks round-robin over {nodes} NUMA nodes" if nodes > 1 else \
         "mma_host_alloc (1 NUMA node: default placement)"
     return t, how
 
@@ -839,7 +839,7 @@ def main():
     torch.cuda.set_device(0)
     stream = torch.cuda.Stream(device=0)
     early = mma.default_config()
-    early.numa_mode = 2                      # host buffers interleaved when there are nodes
+    early.numa_mode = 3                      # host buffers in 2 MiB blocks round-robin over the nodes
     mma.init(early)
 
     if args.workload == "kv":
@@ -867,7 +867,7 @@ def main():
         cfg.plan_mode = 0
         cfg.hop_mode[0] = cfg.hop_mode[1] = args.hop
         cfg.debug_log = 0
-        cfg.numa_mode = 2
+        cfg.numa_mode = 3
         mma.init(cfg)
         return cfg
 

@@ -88,7 +88,9 @@ typedef struct {
     /* CTAs per relay ring for the relay kernels; 0 = default (8) */
     int relay_ctas;
     /* NUMA placement for mma_host_alloc: 0 = default, 1 = bind to node 0, 2 = interleave
-     * across all nodes (a no-op on a single-node host) */
+     * across all nodes page by page, 3 = 2 MiB blocks round-robin over the nodes (a paged-KV
+     * block then never straddles nodes, for the planner's regrouping, numa_plan) -- all a
+     * no-op on a single-node host */
     int numa_mode;
     /* record the per-chunk delivery log (debug; off in timed runs) */
     int debug_log;

@@ -5,7 +5,9 @@
 // mma_host_alloc are anonymous mappings whose pages are bound with mbind(2) (raw syscall:
 // libnuma is absent) to the requested node(s) before first touch, then registered with
 // cudaHostRegister(PORTABLE | MAPPED) so every GPU's copy engine and SMs can reach them.
-// numa_mode: 0 = kernel default placement, 1 = node `node0`, 2 = interleave across nodes.
+// numa_mode: 0 = kernel default placement, 1 = node `node0`, 2 = interleave across nodes
+// (page by page), 3 = 2 MiB blocks round-robin over the nodes (every block on one node, so a
+// paged-KV block never straddles nodes and the planner's regrouping, R23, sees whole blocks).
 #include <cuda_runtime.h>
 #include <sys/mman.h>
 #include <sys/syscall.h>
@@ -55,7 +57,14 @@ int host_alloc(void** ptr, size_t bytes, int numa_mode, int node0)
     if (p == MAP_FAILED) return cudaErrorMemoryAllocation;
     madvise(p, len, MADV_HUGEPAGE);
     const int nodes = numa_nodes();
-    if (numa_mode != 0 && nodes > 1) {
+    if (numa_mode == 3 && nodes > 1) {
+        for (size_t off = 0; off < len; off += align) {
+            unsigned long mask[4] = {0, 0, 0, 0};
+            const int nd = (int)((off / align) % nodes);
+            mask[nd / 64] |= 1ul << (nd % 64);
+            syscall(SYS_mbind, (char*)p + off, align, kMpolBind, mask, 256ul, 0u);   // best effort
+        }
+    } else if (numa_mode != 0 && nodes > 1) {
         unsigned long mask[4] = {0, 0, 0, 0};
         int mode = kMpolBind;
         if (numa_mode == 2) {
