@@ -224,8 +224,9 @@ int mma_tune_chunk(int device, mma_dir_t dir, size_t bytes, size_t* chunk_out);
  * the native single-path copy wins). Times the native copy and the multipath copy (current
  * bandwidth vector and modes) at sizes chunk, 2*chunk, 4*chunk, ... <= max_bytes through
  * library-owned buffers, and sets cfg.fallback_bytes[dir] to the smallest swept size from
- * which every larger swept size is >= 3% faster by multipath. If even max_bytes is not
- * (a single-path set, or relays that share the target's link), there is no break-even:
+ * which every larger swept size is >= 3% faster by multipath (at least two such sizes when
+ * two or more are swept). If even max_bytes is not (a single-path set, or relays that share
+ * the target's link), there is no break-even:
  * the threshold is left unchanged and *found = 0. *thr_out receives the threshold in effect.
  * Either pointer may be NULL. Synchronous. */
 int mma_tune_threshold(int device, mma_dir_t dir, size_t max_bytes, size_t* thr_out, int* found);

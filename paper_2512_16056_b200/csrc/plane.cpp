@@ -235,6 +235,7 @@ int do_init(const mma_config_t* cfg)
         if (e.arena_cap) CK(cudaHostAlloc((void**)&e.arena, e.arena_cap, cudaHostAllocPortable));
         e.timeout_ns = (uint64_t)env_size("MMA_SPIN_TIMEOUT_MS", 20000) * 1000000ull;
         e.unit_bytes = (uint32_t)env_size("MMA_UNIT_BYTES", kDefaultUnit);
+        if (const char* u = getenv("MMA_UPLOAD")) e.upload_by_kernel = strcmp(u, "ce") != 0;
         const char* f = getenv("MMA_FAULT_DROP_PUBLISH");
         e.fault_drop_publish = f ? atoll(f) : -1;
         if (e.unit_bytes < 4096) e.unit_bytes = 4096;
@@ -430,7 +431,7 @@ static int scratch_host(Scratch& sc, size_t bytes, void** out)
         if (sc.host) cudaFreeHost(sc.host);
         sc.host = nullptr;
         size_t cap = std::max(bytes + bytes / 2, kScratchMin);
-        CK(cudaHostAlloc(&sc.host, cap, cudaHostAllocPortable));
+        CK(cudaHostAlloc(&sc.host, cap, cudaHostAllocPortable | cudaHostAllocMapped));   // kernels read it
         sc.host_cap = cap;
     }
     *out = sc.host;
@@ -1008,7 +1009,24 @@ private:
             CK((cudaError_t)use(lanes(g).kern, g));
             if (j_.capturing) CK(cudaMallocAsync(&dtab_[g], tab_bytes_, lanes(g).kern));   // a graph allocation
             else CK((cudaError_t)scratch_dev(*sc_, g, tab_bytes_, &dtab_[g]));
-            CK(cudaMemcpyAsync(dtab_[g], htab_, tab_bytes_, cudaMemcpyHostToDevice, lanes(g).kern));
+            if (!j_.capturing && tab_bytes_ >= (64u << 10) && eng_.upload_by_kernel) {
+                // a large table is fetched by the zero-copy kernel from the mapped staging
+                // buffer: a copy-engine upload would queue behind whatever DMAs the copy
+                // engines hold (a 131,072-descriptor batch of another call), and its enqueue
+                // blocks the host once the engine's queue is full
+                ZcLaunchArg a{};
+                a.v.nseg = 1;
+                a.v.B = a.v.C = tab_bytes_;
+                a.v.src0 = (uint64_t)htab_;
+                a.v.dst0 = (uint64_t)dtab_[g];
+                a.chunks.count = 1;
+                a.unit_bytes = eng_.unit_bytes;
+                const unsigned grid = (unsigned)std::min<uint64_t>((tab_bytes_ + eng_.unit_bytes - 1) / eng_.unit_bytes, 8);
+                CK(launch_zc(a, grid, lanes(g).kern));
+                t_.stats.kernels++;
+            } else {
+                CK(cudaMemcpyAsync(dtab_[g], htab_, tab_bytes_, cudaMemcpyHostToDevice, lanes(g).kern));
+            }
         }
         tr_.mark("upload");
         return cudaSuccess;

@@ -161,6 +161,7 @@ struct Engine {
     PFN_memop64 wait64 = nullptr, write64 = nullptr;
     uint64_t timeout_ns = 20ull * 1000 * 1000 * 1000;
     uint32_t unit_bytes = kDefaultUnit;
+    bool upload_by_kernel = true;    // MMA_UPLOAD=ce: table uploads by the copy engine
     // fault injection (tests only, MMA_FAULT_DROP_PUBLISH=g): the hop-1 publish of global
     // ring chunk g is never issued, so the relay kernel must time out, record the sticky
     // error and release the ring instead of hanging (SURVEY §5 failure detection)

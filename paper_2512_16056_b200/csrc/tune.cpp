@@ -337,6 +337,16 @@ int mma_tune_threshold(int device, mma_dir_t dir, size_t max_bytes, size_t* thr_
     DeviceGuard dg(device);
     const uint64_t C = e.cfg.chunk_bytes[dir];
     if (max_bytes < C) max_bytes = C;
+    {   // a set whose only usable path is the direct one has nothing to gain: no break-even
+        const auto& ps = e.tgt[device].paths[dir];
+        int usable = 0;
+        for (const PathState& q : ps) usable += q.mbps > 0;
+        if (usable < 2) {
+            if (thr_out) *thr_out = e.cfg.fallback_bytes[dir];
+            if (found) *found = 0;
+            return cudaSuccess;
+        }
+    }
     CalBuffers cb(device, max_bytes);
     CK(cb.rc);
     CK(reserve_tables(cb.job(dir, max_bytes)));
@@ -372,13 +382,16 @@ int mma_tune_threshold(int device, mma_dir_t dir, size_t max_bytes, size_t* thr_
     cudaEventDestroy(b);
     if (rc == cudaSuccess && sticky()) rc = sticky();
     if (rc != cudaSuccess) return rc;
+    // the smallest size from which every larger swept size wins; at least two winning sizes
+    // (one timed point alone cannot tell a break-even from noise)
     size_t thr = 0;
-    bool any = false;
+    int wins = 0;
     for (size_t k = sizes.size(); k-- > 0;) {
         if (!faster[k]) break;
         thr = sizes[k];
-        any = true;
+        wins++;
     }
+    const bool any = wins >= 2 || (wins == 1 && sizes.size() == 1);
     if (any) e.cfg.fallback_bytes[dir] = thr;
     if (thr_out) *thr_out = e.cfg.fallback_bytes[dir];
     if (found) *found = any ? 1 : 0;
