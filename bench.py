@@ -1207,7 +1207,8 @@ def main():
                     "gbps": round(ceil, 2), "frac": round(roof["achieved"] / ceil, 4),
                     "kernel_pcie_over_payload": kern_ratio, "copy_engine_pcie_over_payload": ce_ratio,
                     "how": "peak x copy-engine overhead (profiles/r01_probe_nvml.json, native 4 GiB copy) / "
-                           "this kernel's overhead (pcie_hw, this run)"}
+                           "this kernel's overhead (pcie_hw, this run); the two overhead factors come from "
+                           "different runs, so the ceiling is good to about +-2%"}
     except (KeyError, TypeError, ZeroDivisionError, StopIteration):
         pass
 
