@@ -203,7 +203,8 @@ def test_mode_choice_by_measurement(mma, orc):
     configure(mma, loopback=1, chunk=MiB, plan_mode=0, hop=(0, 0), debug=0)
     mma.calibrate(0, mma.H2D, 64 * MiB)
     ps = mma.get_paths(0, mma.H2D)
-    assert all(p["mode"] in (1, 2) and p["mbps"] > 5000 for p in ps), ps
+    # the direct path is copy engine or zero-copy; a relay may also be the all-copy-engine ring
+    assert all(p["mode"] in ((1, 2) if p["kind"] == 0 else (1, 2, 3)) and p["mbps"] > 5000 for p in ps), ps
     shape, ho, do, sb, hpool, dbytes = _kv(512)
     host = torch.empty(hpool, dtype=torch.uint8).pin_memory()
     mma_inputs.fill_pattern(host.numpy(), 77)
@@ -212,7 +213,7 @@ def test_mode_choice_by_measurement(mma, orc):
     segs, n = mma.make_segments(host.data_ptr() + ho, cache.data_ptr() + do, lens)
     mma.tune_segments(segs, n, 0, mma.H2D, reps=1)
     ps = mma.get_paths(0, mma.H2D)
-    assert all(p["seg_mode"] in (1, 2) and p["seg_mbps"] > 5000 for p in ps), ps
+    assert all(p["seg_mode"] in ((1, 2) if p["kind"] == 0 else (1, 2, 3)) and p["seg_mbps"] > 5000 for p in ps), ps
     cache.zero_()
     mma.memcpy_h2d_segments(segs, n, 0)
     torch.cuda.synchronize()
