@@ -1,7 +1,9 @@
 #!/usr/bin/env python3
 """Engine timeline (Chrome trace) of a loopback multipath copy on one GPU, plus an overlap
 summary: the direct DMA stream, two relay hop streams and the relay kernel run at once.
-Writes gpurun_out/trace_loopback_{h2d,d2h}.json."""
+Writes gpurun_out/trace_loopback_{h2d,d2h}.json; with `p2p` as argument the relays are
+all-copy-engine rings (hop 1 and the peer hop 2 on the same relay stream, the two streams
+overlapping: the paper's dual pipeline, Fig 6b) -> trace_loopback_p2p_{h2d,d2h}.json."""
 import json, sys
 from pathlib import Path
 sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
@@ -33,7 +35,11 @@ cfg = mma.default_config()
 cfg.fallback_bytes[0] = cfg.fallback_bytes[1] = 0
 cfg.loopback_relays = 2
 cfg.hop_mode[0] = cfg.hop_mode[1] = mma.HOP_CE
+p2p = len(sys.argv) > 1 and sys.argv[1] == "p2p"
 mma.init(cfg)
+if p2p:
+    for d in (mma.H2D, mma.D2H):
+        mma.set_path_modes(0, d, [mma.HOP_CE, mma.HOP_CE_P2P, mma.HOP_CE_P2P])
 for d in (mma.H2D, mma.D2H):
     mma.set_bandwidth(0, d, [2, 1, 1])
 mma.memcpy_h2d(dev, host, B, stream=s); mma.memcpy_d2h(host, dev, B, stream=s); s.synchronize()
@@ -43,7 +49,7 @@ for name, fn in (("h2d", lambda: mma.memcpy_h2d(dev, host, B, stream=s)),
     mma.trace_begin()
     fn()
     s.synchronize()
-    p = out / f"trace_loopback_{name}.json"
+    p = out / (f"trace_loopback_p2p_{name}.json" if p2p else f"trace_loopback_{name}.json")
     n = mma.trace_end(str(p))
     print(json.dumps({"dir": name, "spans": n, **overlap(p)}), flush=True)
 assert mma.get_last_error() == 0
