@@ -92,3 +92,18 @@ def test_planner_rejects_bad_input():
     assert mma.plan_chunks([1], [0], 100, 0)[0] != 0               # zero chunk
     rc, path, fb = mma.plan_chunks([1, 1], [0, 1], 0, 10)
     assert rc == 0 and path == b""
+
+
+def test_header_is_plain_c(tmp_path):
+    """include/mma.h is a C ABI: it compiles as strict C11 (no C++ types in the signatures)"""
+    import shutil
+    import subprocess
+    gcc = shutil.which("gcc")
+    if not gcc:
+        pytest.skip("no gcc")
+    src = tmp_path / "t.c"
+    src.write_text('#include "mma.h"\nint main(void) { mma_config_t c; mma_stats_t s; mma_topology_t t;'
+                   ' (void)c; (void)s; (void)t; return 0; }\n')
+    r = subprocess.run([gcc, "-std=c11", "-Wall", "-Wextra", "-pedantic", "-Werror", "-I", str(ROOT / "include"),
+                        "-c", str(src), "-o", str(tmp_path / "t.o")], capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
