@@ -183,3 +183,34 @@ def test_captured_all_copy_engine_relay(mma, dirn, scattered):
         d = dev.cpu().numpy().reshape(nseg, sb)
         assert np.array_equal(d[perm], h), seed
     assert mma.get_last_error() == 0
+
+
+def test_replays_concurrent_with_live_ring_calls(mma):
+    """a replayed graph (all-copy-engine relay on its own staging) and live calls through the
+    kernel-driven ring of the same relay path, on two streams at once: both stay exact"""
+    configure(mma, loopback=1, chunk=MiB, slots=2, debug=0)
+    mma.set_path_modes(0, mma.H2D, [mma.HOP_CE, mma.HOP_CE_P2P])
+    mma.set_bandwidth(0, mma.H2D, [1, 1])
+    B = 16 * MiB + 4096
+    gsrc = pinned(torch, B, seed=41)
+    gdst = torch.zeros(B, dtype=torch.uint8, device="cuda")
+    mma.memcpy_h2d(gdst, gsrc, B)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        mma.memcpy_h2d(gdst, gsrc, B)
+    mma.set_path_modes(0, mma.H2D, [mma.HOP_CE, mma.HOP_CE])     # live calls: the kernel ring
+    mma.set_bandwidth(0, mma.H2D, [1, 1])
+    lsrc = pinned(torch, B, seed=42)
+    ldst = torch.zeros(B, dtype=torch.uint8, device="cuda")
+    s_graph, s_live = torch.cuda.Stream(), torch.cuda.Stream()
+    for it in range(4):
+        mma_inputs.fill_pattern(gsrc.numpy()[:B], 50 + it)
+        mma_inputs.fill_pattern(lsrc.numpy()[:B], 60 + it)
+        with torch.cuda.stream(s_graph):
+            g.replay()
+        mma.memcpy_h2d(ldst, lsrc, B, stream=s_live)
+        torch.cuda.synchronize()
+        assert torch.equal(gdst.cpu(), gsrc[:B]), it
+        assert torch.equal(ldst.cpu(), lsrc[:B]), it
+    assert mma.get_last_error() == 0
