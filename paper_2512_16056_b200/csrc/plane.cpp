@@ -4,11 +4,15 @@
 // chunk travels over exactly one path:
 //   direct   d's own PCIe link: copy-engine DMA ("a single H2D transfer operation")
 //            or SM zero-copy (north_star (d));
-//   relay r  r's PCIe link into r's HBM staging ring, then NVLink r -> d pulled by the
-//            relay kernel on d ("an H2D operation and a P2P operation ... with a
-//            dependency"; dual pipeline generalised to S slots); D2H mirrors it. In
-//            zero-copy mode a relay is one hop: a kernel on r reads host memory over r's
-//            PCIe and stores into d's HBM over NVLink.
+//   relay r  r's PCIe link into r's HBM staging ring, then NVLink r -> d, pulled by the
+//            relay kernel on d or pushed by a peer DMA on r's own stream (MMA_HOP_CE_P2P)
+//            ("an H2D operation and a P2P operation ... with a dependency"; dual
+//            pipeline generalised to S slots); D2H mirrors it. In zero-copy mode a relay is
+//            one hop: a kernel on r reads host memory over r's PCIe and stores into d's HBM
+//            over NVLink.
+// A call on a stream being captured is recorded as a replayable graph (class Call, capture
+// mode); scattered tables may be regrouped by host NUMA node (R23) and moved in host-address
+// order inside a path (R22).
 // The paper's Dummy Task + callback + spin kernel (§3.3, §4) is
 // replaced by GPU-ordered fork/join: an event recorded on the user stream gates every path
 // stream and every path stream's completion event gates the user stream, so the copy is
