@@ -51,6 +51,13 @@ def test_random_transfers(mma, orc):
         scattered = rng.random() < 0.4
         host_order = int(rng.integers(0, 3))
         capture = plan_mode != 2 and rng.random() < 0.15
+        fake_numa = rng.random() < 0.25      # R23 regrouping with faked host / path nodes
+        if fake_numa:
+            os.environ["MMA_FAKE_HOST_NODES"] = str(int(rng.integers(2, 4)))
+            os.environ["MMA_FAKE_PATH_NODES"] = ",".join(str(int(x)) for x in rng.integers(0, 3, P))
+        else:
+            os.environ.pop("MMA_FAKE_HOST_NODES", None)
+            os.environ.pop("MMA_FAKE_PATH_NODES", None)
         configure(mma, loopback=lb, chunk=C, slots=S, plan_mode=plan_mode, hop=(1, 1), host_order=host_order)
         mma.set_path_modes(0, dirn, modes)
         mma.set_bandwidth(0, dirn, bw)
@@ -73,7 +80,8 @@ def test_random_transfers(mma, orc):
             span = B + 128
         B = int(lens.sum())
         print(f"case {case}: lb={lb} C={C} S={S} plan={plan_mode} modes={modes} bw={bw} dir={dirn} "
-              f"scattered={scattered} nseg={len(lens)} B={B} order={host_order} capture={capture}", flush=True)
+              f"scattered={scattered} nseg={len(lens)} B={B} order={host_order} capture={capture} "
+              f"numa={fake_numa}", flush=True)
         if dirn == 0:      # H2D: host pool -> fresh device buffer
             dst = torch.full((span,), 0xA5, dtype=torch.uint8, device="cuda")
             segs, n = mma.make_segments(pool_h.data_ptr() + src_off, dst.data_ptr() + dst_off, lens)
@@ -115,4 +123,6 @@ def test_random_transfers(mma, orc):
         assert orc.move(osegs, on, C, bw, path, S=S) == 0
         got = dst.cpu().numpy() if dirn == 0 else dst.numpy()
         assert np.array_equal(got, exp), (case, dict(lb=lb, C=C, S=S, plan=plan_mode, modes=modes, dir=dirn,
-                                                     scattered=scattered, B=B))
+                                                     scattered=scattered, B=B, numa=fake_numa))
+    os.environ.pop("MMA_FAKE_HOST_NODES", None)
+    os.environ.pop("MMA_FAKE_PATH_NODES", None)
