@@ -51,6 +51,7 @@ def main():
     variants = [("native", None), ("mma", dict(loopback=0, modes=None, bw=None))]
     if ngpu == 1:
         variants += [("loopback-ring 1:1", dict(loopback=1, modes=[1, 1], bw=[1, 1])),
+                     ("loopback-ce-p2p-ring 1:1", dict(loopback=1, modes=[1, 3], bw=[1, 1])),
                      ("loopback-zc 1:1", dict(loopback=1, modes=[1, 2], bw=[1, 1]))]
     for name, v in variants:
         cfg = mma.default_config()
