@@ -6,7 +6,9 @@
  *
  * Conventions for every function below
  *  - Return value: a cudaError_t value as int (0 = cudaSuccess). Validation happens
- *    before anything is enqueued: a call that returns an error enqueued nothing.
+ *    before anything is enqueued: a call that fails validation enqueued nothing. A CUDA
+ *    error while enqueueing (after validation) is returned after the user stream has been
+ *    made to wait for whatever part of the copy was already enqueued.
  *  - Asynchronous failures (a relay kernel whose bounded spin timed out) are sticky: they
  *    are returned by the next mma_* call and by mma_get_last_error().
  *  - Thread safety: every call may be made from any thread. Multipath calls serialise at

@@ -631,13 +631,21 @@ public:
         }
         CK(tb);
         CK(fork());
-        CK(upload_tables());
-        CK(delivery_log());
-        CK(open_timing());
-        if (dynamic_) CK(enqueue_dynamic());
-        else {
-            CK(enqueue_paths());
-            CK(enqueue_rings());
+        // after the fork, a failing stage still joins every stream it enqueued on, so the
+        // user stream never runs ahead of partial engine work; the error is returned
+        int rc = upload_tables();
+        if (rc == cudaSuccess) rc = delivery_log();
+        if (rc == cudaSuccess) rc = open_timing();
+        if (rc == cudaSuccess) {
+            if (dynamic_) rc = enqueue_dynamic();
+            else {
+                rc = enqueue_paths();
+                if (rc == cudaSuccess) rc = enqueue_rings();
+            }
+        }
+        if (rc != cudaSuccess) {
+            join_streams();
+            return rc;
         }
         CK(join());
         return finish();
@@ -1472,7 +1480,7 @@ private:
 
     // ---- join (a8): the user stream waits on every engine stream used; table buffers and
     // ledger entries are released by events on the user stream
-    int join()
+    int join_streams()
     {
         for (auto& u : used_) {
             cudaEvent_t ev = join_event(u.first, u.second);
@@ -1483,6 +1491,12 @@ private:
             DeviceGuard g(j_.user_dev);
             CK(cudaStreamWaitEvent(j_.user, ev, 0));
         }
+        return cudaSuccess;
+    }
+
+    int join()
+    {
+        CK(join_streams());
         if (j_.capturing) {
             CK(free_captured_tables());
             tr_.mark("join");
