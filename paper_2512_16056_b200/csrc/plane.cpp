@@ -242,6 +242,7 @@ int do_init(const mma_config_t* cfg)
         if (const char* u = getenv("MMA_UPLOAD")) e.upload_by_kernel = strcmp(u, "ce") != 0;
         const char* f = getenv("MMA_FAULT_DROP_PUBLISH");
         e.fault_drop_publish = f ? atoll(f) : -1;
+        e.fault_fail_rings = getenv("MMA_FAULT_FAIL_RINGS") != nullptr;
         if (e.unit_bytes < 4096) e.unit_bytes = 4096;
     }
     e.cfg = c;
@@ -1300,6 +1301,7 @@ private:
                 (mode_[p] == MMA_HOP_CE || mode_[p] == MMA_HOP_CE_P2P))
                 rp.push_back(p);
         if (rp.empty()) return cudaSuccess;
+        if (eng_.fault_fail_rings) return cudaErrorUnknown;   // test hook (plane.h)
         if (j_.capturing) {
             for (int p : rp) CK(enqueue_captured_p2p(p));   // plan() left only CE_P2P relays
             tr_.mark("rings");

@@ -166,6 +166,9 @@ struct Engine {
     // ring chunk g is never issued, so the relay kernel must time out, record the sticky
     // error and release the ring instead of hanging (SURVEY §5 failure detection)
     long long fault_drop_publish = -1;
+    // fault injection (tests only, MMA_FAULT_FAIL_RINGS=1): the ring stage of every call fails
+    // after the direct path was enqueued, to check that a failed call still joins its streams
+    bool fault_fail_rings = false;
 };
 
 Engine& E();

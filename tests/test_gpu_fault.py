@@ -61,3 +61,46 @@ def test_dropped_publish_times_out_cleanly(tmp_path):
     r = json.loads(p.stdout.strip().splitlines()[-1])
     assert r["err"] == 2001 and r["refused"]
     assert r["ok"] and r["err2"] == 0
+
+
+FAIL_PROG = r"""
+import json, sys, torch
+sys.path.insert(0, {root!r})
+import paper_2512_16056_b200 as m
+cfg = m.default_config()
+cfg.chunk_bytes[0] = cfg.chunk_bytes[1] = 1 << 20
+cfg.fallback_bytes[0] = cfg.fallback_bytes[1] = 0
+cfg.loopback_relays = 1
+cfg.hop_mode[0] = cfg.hop_mode[1] = m.HOP_CE
+m.init(cfg)
+m.set_bandwidth(0, m.H2D, [1, 1])          # the direct half is enqueued, then the ring stage fails
+n = 512 << 20
+src = torch.full((n,), 7, dtype=torch.uint8).pin_memory()
+dst = torch.zeros(n, dtype=torch.uint8, device="cuda")
+probe = torch.zeros(1 << 20, dtype=torch.uint8, device="cuda")
+s = torch.cuda.Stream()
+try:
+    m.memcpy_h2d(dst, src, n, stream=s)
+    failed = False
+except m.MMAError:
+    failed = True
+with torch.cuda.stream(s):
+    probe.copy_(dst[(n // 2) - (1 << 20):n // 2])   # the tail of the direct half, right after the call
+torch.cuda.synchronize()
+print(json.dumps(dict(failed=failed, probe_done=bool((probe == 7).all().item()))))
+"""
+
+
+def test_failed_enqueue_still_orders_the_user_stream(tmp_path):
+    """a CUDA error while enqueueing (injected after the direct path's DMA was enqueued) is
+    returned, and work the user enqueues next on its stream still runs after that DMA"""
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    script = tmp_path / "f.py"
+    script.write_text(FAIL_PROG.format(root=str(ROOT)))
+    env = dict(os.environ, MMA_FAULT_FAIL_RINGS="1")
+    p = subprocess.run([sys.executable, str(script)], env=env, capture_output=True, text=True, timeout=240)
+    assert p.returncode == 0, p.stderr[-3000:]
+    r = json.loads(p.stdout.strip().splitlines()[-1])
+    assert r["failed"] and r["probe_done"], r
