@@ -91,3 +91,32 @@ def test_pcie_counter_unwrap():
     assert c.mark() == [[1_000_000_000, 10]]
     assert c.mark() == [[1_000_000_000 + 294_967_396, 20]]
     assert c.mark() == [[1_000_000_000 + 294_967_396 + 4_294_966_900, 30]]
+
+
+def test_committed_bench_line_has_the_contract_keys():
+    """the committed bench line (profiles/r01_bench.json) carries every key the driver's
+    contract names, with the types it expects"""
+    import json
+    from pathlib import Path
+    d = json.loads((Path(__file__).resolve().parents[1] / "profiles" / "r01_bench.json").read_text())
+    for k in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better",
+              "scaling", "vs_baseline", "dtype", "data", "config", "roofline", "cpu_baseline", "e2e",
+              "gpu_launches", "clocks"):
+        assert k in d, k
+    assert d["value"] > 0 and d["steps"] >= 1 and d["warmup"] >= 3 and d["higher_is_better"] is True
+    assert "workload" in d["config"]
+    r = d["roofline"]
+    for k in ("bound", "achieved", "peak", "unit", "frac", "traffic"):
+        assert k in r, k
+    assert abs(r["frac"] - r["achieved"] / r["peak"]) < 1e-3
+    c = d["cpu_baseline"]
+    for k in ("value", "unit", "cores", "kind", "sample"):
+        assert k in c, k
+    assert c["kind"] == "oracle" and c["cores"] >= 1
+    e = d["e2e"]
+    for k in ("value", "unit", "h2d_bytes_per_step", "d2h_bytes_per_step"):
+        assert k in e, k
+    assert e["h2d_bytes_per_step"] > 0 and e["d2h_bytes_per_step"] > 0
+    assert d["gpu_launches"] > 0
+    for k in ("sm_mhz", "sm_max_mhz", "reasons"):
+        assert k in d["clocks"], k
