@@ -1323,6 +1323,8 @@ def main():
         "engine": {"issue_us_per_call": round((st["issue_us"] - st["wait_us"]) / max(1, st["calls"]), 1),
                    "blocked_us_per_call": round(st["wait_us"] / max(1, st["calls"]), 1),
                    "relay_bytes": int(st["relay_bytes"]), "fallbacks": int(st["fallbacks"]),
+                   "single_path_calls": int(st["single_path_calls"]),
+                   "validate_us_per_call": round(st["validate_us"] / max(1, st["calls"]), 1),
                    "numa_local_of_known_bytes": [int(st["numa_local_bytes"][0]), int(st["numa_known_bytes"][0]),
                                                  int(st["numa_local_bytes"][1]), int(st["numa_known_bytes"][1])]},
         "paper_context": "245 GB/s = 4.62x one 53 GB/s PCIe link, 8x H20 (P:737); context only",

@@ -146,6 +146,12 @@ typedef struct {
     uint64_t dynamic_calls;               /* calls moved by GPU-driven dynamic pull */
     uint64_t numa_known_bytes[2];         /* [direction] bytes whose host NUMA node is known */
     uint64_t numa_local_bytes[2];         /* of those, carried by a path on the same node */
+    /* fallbacks counts calls moved by the NATIVE copy (below the threshold, pageable, or a
+     * one-path plan on the copy engine); a one-path plan that runs the engine's zero-copy
+     * kernel is counted here instead */
+    uint64_t single_path_calls;
+    double validate_us;                   /* host time classifying segment memory kinds */
+    uint64_t ptr_queries;                 /* driver pointer queries made for it */
 } mma_stats_t;
 
 /* Fill cfg with defaults (then env MMA_* overrides). */
@@ -188,6 +194,13 @@ int mma_memcpy_d2h(void* dst, const void* src, size_t bytes, mma_stream_t stream
  * and planned like a contiguous copy. H2D: every src is pinned host memory, every dst is
  * device memory of dst_device; D2H the reverse with src_device. The table is copied at
  * call time. Destinations must be pairwise disjoint (cudaErrorInvalidValue otherwise).
+ * Every segment's memory is classified before anything is enqueued (a per-call cache of
+ * the driver's allocation ranges, mma_stats_t.validate_us / ptr_queries): a device-side
+ * piece that is not device memory of that GPU, a host-side piece that is device memory, or
+ * a piece that spans two kinds of memory -> cudaErrorInvalidValue, nothing enqueued. A
+ * host-side piece that is pageable (not page-locked) -> the whole table is copied by the
+ * native cudaMemcpyAsync per segment on `stream` (byte-identical; its errors are that
+ * call's), as for a contiguous copy (reading R7).
  */
 int mma_memcpy_h2d_segments(const mma_segment_t* segs, size_t nsegs, int dst_device,
                             mma_stream_t stream);

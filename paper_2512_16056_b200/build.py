@@ -30,7 +30,7 @@ SOURCES = [
     CSRC / "kernels" / "verify.cu",
 ]
 HEADERS = [ROOT / "include" / "mma.h", CSRC / "engine.h", CSRC / "plane.h", CSRC / "kargs.h", CSRC / "planner.h",
-           CSRC / "kernels" / "copy.cuh", CSRC / "preload.cpp"]
+           CSRC / "kernels" / "copy.cuh", CSRC / "preload.cpp", CSRC / "ranges.h"]
 
 FLAGS = [
     "-O3", "-std=c++17", "-lineinfo",
@@ -39,7 +39,7 @@ FLAGS = [
     "-Xptxas", "-v" if os.environ.get("MMA_PTXAS_V") else "-O3",
     "-I", str(ROOT / "include"),
     "--expt-relaxed-constexpr", "--extended-lambda",
-]
+] + (["-g"] if os.environ.get("MMA_HOST_DEBUG") else [])
 
 
 def stale() -> bool:

@@ -7,6 +7,7 @@
 #include <string>
 
 #include "plane.h"
+#include "ranges.h"
 
 namespace mma {
 
@@ -37,6 +38,49 @@ static int classify(const void* p, int* dev, bool* mapped)
     return 2;
 }
 
+// Memory-kind query behind the per-call range cache (ranges.h): cudaPointerGetAttributes for
+// the kind, the driver's RANGE_START_ADDR / RANGE_SIZE for the allocation's bounds.
+using PFN_ptrattrs = CUresult (*)(unsigned, CUpointer_attribute*, void**, CUdeviceptr);
+
+static PFN_ptrattrs ptr_attrs()
+{
+    static PFN_ptrattrs fn = [] {
+        void* f = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPointByVersion("cuPointerGetAttributes", &f, 12000, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess) {
+            cudaGetLastError();
+            f = nullptr;
+        }
+        return (PFN_ptrattrs)f;
+    }();
+    return fn;
+}
+
+static MemRange query_range(uintptr_t p, uintptr_t end, void*)
+{
+    MemRange r{p, end, MK_PAGEABLE, -1, false};
+    r.kind = classify((const void*)p, &r.dev, &r.mapped);
+    CUdeviceptr start = 0;
+    size_t size = 0;
+    CUpointer_attribute at[2] = {CU_POINTER_ATTRIBUTE_RANGE_START_ADDR, CU_POINTER_ATTRIBUTE_RANGE_SIZE};
+    void* data[2] = {&start, &size};
+    if (PFN_ptrattrs f = ptr_attrs(); f && r.kind != MK_PAGEABLE)
+        if (f(2, at, data, (CUdeviceptr)p) == CUDA_SUCCESS && size && start <= p && p < start + size) {
+            r.lo = (uintptr_t)start;
+            r.hi = (uintptr_t)start + size;
+            return r;
+        }
+    if (end - p > 1) {   // no bounds (pageable, or none reported): both ends of the piece must agree
+        int dev2 = -1;
+        bool m2 = false;
+        const int k2 = classify((const void*)(end - 1), &dev2, &m2);
+        if (k2 != r.kind || dev2 != r.dev) r.kind = MK_MIXED;
+        r.mapped = r.mapped && m2;
+    }
+    return r;
+}
+
 // Capture status of the user stream. A captured call may not initialise anything (the
 // engine, a device's streams, the graph arena): those are made by an uncaptured call first,
 // else the copy is the native one. Returns 1 = capture the multipath copy, 0 = not
@@ -54,8 +98,21 @@ static int capture_state(cudaStream_t stream, int d)
     if (!e.inited || !e.arena || d < 0 || d >= e.ndev || !e.tgt[d].paths_made) return -1;
     make_paths(d);
     for (int dir = 0; dir < 2; dir++)
-        for (const PathState& p : e.tgt[d].paths[dir])
-            if (!e.dev[p.gpu].made) return -1;
+        for (const PathState& p : e.tgt[d].paths[dir]) {
+            const DevRes& r = e.dev[p.gpu];
+            if (!r.made) return -1;
+            // another capture still holds the capture lanes (its user has not ended it yet):
+            // joining them would tie the two graphs together
+            for (const Lanes& l : r.cap_lane)
+                for (cudaStream_t s : {l.kern, l.hop[0], l.hop[1], l.direct, l.zc}) {
+                    cudaStreamCaptureStatus st = cudaStreamCaptureStatusNone;
+                    if (cudaStreamIsCapturing(s, &st) != cudaSuccess) {
+                        cudaGetLastError();
+                        return -1;
+                    }
+                    if (st != cudaStreamCaptureStatusNone) return -1;
+                }
+        }
     return 1;
 }
 
@@ -145,23 +202,29 @@ int prepare_segments(int dir, const mma_segment_t* segs, size_t nsegs, int devic
             ok.assign(segs, segs + nsegs);
         }
     }
-    // classify a bounded sample of the table (first, last, evenly spaced): a pointer query
-    // costs ~0.1 ms, so the sample stays small; the caller guarantees the memory kinds
+    // every segment's memory kind, through a per-call cache of the allocations seen so far
+    // (a few driver queries per call; one per segment only for memory CUDA does not know)
+    const auto v0 = std::chrono::steady_clock::now();
+    RangeCache hc(query_range, nullptr), dc(query_range, nullptr);
     j.mapped = true;
-    const size_t nsample = std::min<size_t>(nsegs, 5);
-    for (size_t q = 0; q < nsample; q++) {
-        size_t k = (nsample == 1) ? 0 : q * (nsegs - 1) / (nsample - 1);
+    j.pageable = false;
+    for (size_t k = 0; k < nsegs; k++) {
         if (!segs[k].bytes) continue;
         const void* dp = (dir == MMA_H2D) ? segs[k].dst : segs[k].src;
         const void* hp = (dir == MMA_H2D) ? segs[k].src : segs[k].dst;
-        int d = -1, hd = -1;
-        bool m = false, dummy = false;
-        if (classify(dp, &d, &dummy) != 1 || d != device) return cudaErrorInvalidValue;
-        int hk = classify(hp, &hd, &m);
-        if (hk == 1) return cudaErrorInvalidValue;
-        if (hk == 2) j.mapped = false;   // pageable: CE only
+        int d = -1;
+        bool m = false;
+        if (dc.kind((uintptr_t)dp, segs[k].bytes, &d, &m) != MK_DEVICE || d != device) return cudaErrorInvalidValue;
+        const int hk = hc.kind((uintptr_t)hp, segs[k].bytes, &d, &m);
+        if (hk == MK_DEVICE || hk == MK_MIXED) return cudaErrorInvalidValue;
+        if (hk == MK_PAGEABLE) {   // pageable or unregistered: the whole table goes native (R7)
+            j.pageable = true;
+            break;
+        }
         j.mapped = j.mapped && m;
     }
+    j.validate_us = std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - v0).count();
+    j.ptr_queries = hc.queries() + dc.queries();
     if (nsegs == 1) {   // one segment is a contiguous copy (the kernels' nseg == 1 form)
         j.contiguous = true;
         j.src0 = (const char*)segs[0].src;
@@ -196,6 +259,15 @@ static int copy_segments(int dir, const mma_segment_t* segs, size_t nsegs, int d
     Job j;
     CK(prepare_segments(dir, segs, nsegs, device, stream, j));
     if (j.B == 0) return cudaSuccess;
+    if (j.pageable) {   // some host segment is not page-locked: the native copy (R7)
+        std::lock_guard<std::mutex> g(e.mu);
+        e.tgt[device].stats.fallbacks++;
+        e.tgt[device].stats.calls++;
+        e.tgt[device].stats.bytes += j.B;
+        e.tgt[device].stats.validate_us += j.validate_us;
+        e.tgt[device].stats.ptr_queries += j.ptr_queries;
+        return native_segments(dir, segs, nsegs, stream);
+    }
     std::lock_guard<std::mutex> g(e.mu);
     const int cs = capture_state(stream, device);
     if (cs < 0) return native_segments(dir, segs, nsegs, stream);
@@ -296,14 +368,16 @@ int mma_finalize(void)
         DevRes& r = e.dev[d];
         if (!r.made) continue;
         DeviceGuard dg(d);
-        for (Lanes& l : r.lane) {
-            cudaStreamDestroy(l.kern);
-            cudaStreamDestroy(l.hop[0]);
-            cudaStreamDestroy(l.hop[1]);
-            cudaStreamDestroy(l.direct);
-            cudaStreamDestroy(l.zc);
-        }
+        for (Lanes* ls : {r.lane, r.cap_lane})
+            for (int k = 0; k < 2; k++) {
+                cudaStreamDestroy(ls[k].kern);
+                cudaStreamDestroy(ls[k].hop[0]);
+                cudaStreamDestroy(ls[k].hop[1]);
+                cudaStreamDestroy(ls[k].direct);
+                cudaStreamDestroy(ls[k].zc);
+            }
         cudaEventDestroy(r.fork);
+        cudaEventDestroy(r.cap_fork);
         cudaEventDestroy(r.cap_ev);
         cudaStreamDestroy(r.setup);
         r = DevRes();

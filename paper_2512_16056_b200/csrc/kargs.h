@@ -72,6 +72,10 @@ struct ZcLaunchArg {
     uint32_t unit_bytes;
     uint32_t path;
     uint8_t* log;
+    // a private (host-ordered) stream: piece k belongs to chunk piece_chunk[k] of the call's
+    // virtual stream; the kernel logs that chunk for every piece it moves. nullptr: v is the
+    // call's own stream and chunk i is logged directly.
+    const uint32_t* piece_chunk;
 };
 
 }  // namespace mma

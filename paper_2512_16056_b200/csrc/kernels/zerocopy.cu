@@ -29,7 +29,15 @@ __global__ void __launch_bounds__(kThreads) zc_copy_kernel(const __grid_constant
         if (lo >= len) continue;
         const uint64_t hi = (lo + U < len) ? lo + U : len;
         v_copy<V_DIRECT>(A.v, off + lo, off + hi, nullptr);
-        if (A.log && k == 0 && threadIdx.x == 0) A.log[i] = (uint8_t)A.path;
+        if (!A.log) continue;
+        if (!A.piece_chunk) {
+            if (k == 0 && threadIdx.x == 0) A.log[i] = (uint8_t)A.path;
+        } else if (A.v.nseg == 1) {
+            if (threadIdx.x == 0) A.log[A.piece_chunk[0]] = (uint8_t)A.path;
+        } else {   // every piece this unit touched: its chunk was carried by this path
+            for (uint64_t q = v_find(A.v, off + lo) + threadIdx.x; q < A.v.nseg && A.v.start[q] < off + hi; q += blockDim.x)
+                A.log[A.piece_chunk[q]] = (uint8_t)A.path;
+        }
     }
 }
 

@@ -189,13 +189,22 @@ int make_device(int d)
         CK(cudaStreamCreateWithPriority(&l.direct, cudaStreamNonBlocking, hi));
         CK(cudaStreamCreateWithPriority(&l.zc, cudaStreamNonBlocking, hi));
     }
+    for (Lanes& l : r.cap_lane) {
+        CK(cudaStreamCreateWithPriority(&l.kern, cudaStreamNonBlocking, hi));
+        CK(cudaStreamCreateWithPriority(&l.hop[0], cudaStreamNonBlocking, hi));
+        CK(cudaStreamCreateWithPriority(&l.hop[1], cudaStreamNonBlocking, hi));
+        CK(cudaStreamCreateWithPriority(&l.direct, cudaStreamNonBlocking, hi));
+        CK(cudaStreamCreateWithPriority(&l.zc, cudaStreamNonBlocking, hi));
+    }
     CK(cudaEventCreateWithFlags(&r.fork, cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&r.cap_fork, cudaEventDisableTiming));
     CK(cudaEventCreateWithFlags(&r.cap_ev, cudaEventDisableTiming));
     CK(cudaStreamCreateWithFlags(&r.setup, cudaStreamNonBlocking));
     // join events exist before any call: a captured call may not create one
-    for (Lanes& l : r.lane)
-        for (cudaStream_t s : {l.kern, l.hop[0], l.hop[1], l.direct, l.zc})
-            if (!join_event(s, d)) return cudaErrorMemoryAllocation;
+    for (Lanes* ls : {r.lane, r.cap_lane})
+        for (int k = 0; k < 2; k++)
+            for (cudaStream_t s : {ls[k].kern, ls[k].hop[0], ls[k].hop[1], ls[k].direct, ls[k].zc})
+                if (!join_event(s, d)) return cudaErrorMemoryAllocation;
     CK(cudaDeviceGetAttribute(&r.sms, cudaDevAttrMultiProcessorCount, d));
     for (int p = 0; p < e.ndev; p++) {
         if (p == d || !e.p2p[d][p]) continue;
@@ -232,6 +241,10 @@ int do_init(const mma_config_t* cfg)
         if (cudaGetDriverEntryPointByVersion("cuStreamWriteValue64", &fn, 12000, cudaEnableDefault, &q) == cudaSuccess &&
             q == cudaDriverEntryPointSuccess)
             e.write64 = (PFN_memop64)fn;
+        fn = nullptr;
+        if (cudaGetDriverEntryPointByVersion("cuStreamBatchMemOp", &fn, 12000, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess && !getenv("MMA_NO_BATCH_MEMOP"))
+            e.batch_memop = (PFN_batch_memop)fn;
         CK(cudaHostAlloc((void**)&e.err, sizeof(int) * 16, cudaHostAllocPortable | cudaHostAllocMapped));
         memset(e.err, 0, sizeof(int) * 16);
         e.arena_cap = env_size("MMA_GRAPH_ARENA", 16u << 20);
@@ -239,10 +252,15 @@ int do_init(const mma_config_t* cfg)
         if (e.arena_cap) CK(cudaHostAlloc((void**)&e.arena, e.arena_cap, cudaHostAllocPortable));
         e.timeout_ns = (uint64_t)env_size("MMA_SPIN_TIMEOUT_MS", 20000) * 1000000ull;
         e.unit_bytes = (uint32_t)env_size("MMA_UNIT_BYTES", kDefaultUnit);
+        e.group_bytes = env_size("MMA_GROUP_BYTES", kDefaultGroupBytes);
         if (const char* u = getenv("MMA_UPLOAD")) e.upload_by_kernel = strcmp(u, "ce") != 0;
         const char* f = getenv("MMA_FAULT_DROP_PUBLISH");
         e.fault_drop_publish = f ? atoll(f) : -1;
         e.fault_fail_rings = getenv("MMA_FAULT_FAIL_RINGS") != nullptr;
+        const char* fh = getenv("MMA_FAULT_FAIL_HOP");
+        e.fault_fail_hop = fh ? atoll(fh) : -1;
+        e.hops_issued = 0;
+        e.fault_misroute = getenv("MMA_FAULT_MISROUTE") != nullptr;
         if (e.unit_bytes < 4096) e.unit_bytes = 4096;
     }
     e.cfg = c;
@@ -357,8 +375,9 @@ int get_ring(int d, int dir, int p, uint64_t C, uint32_t S, Ring** out)
     Ring& r = e.tgt[d].rings[dir][p];
     const int relay = e.tgt[d].paths[dir][p].gpu;
     const int kdev = (dir == MMA_H2D) ? d : relay;
-    if (r.made && (r.slot_bytes < C || r.S != S || r.relay != relay)) {
-        // tunables changed: drain everything that may still use the old ring
+    if (r.made && (r.broken || r.slot_bytes < C || r.S != S || r.relay != relay)) {
+        // tunables changed, or a failed call left the ring out of step: drain everything
+        // that may still use the old ring
         { DeviceGuard g(r.relay); cudaDeviceSynchronize(); }
         { DeviceGuard g(r.kdev); cudaDeviceSynchronize(); }
         free_ring(r);
@@ -646,6 +665,7 @@ public:
         }
         if (rc != cudaSuccess) {
             join_streams();
+            if (!j_.capturing) mark_tables_busy();   // partial work may still read the tables
             return rc;
         }
         CK(join());
@@ -687,6 +707,7 @@ private:
         size_t off = 0;          // byte offset of its table in the upload
         uint64_t npieces = 0, B = 0;
         std::vector<uint64_t> src, dst, len;
+        std::vector<uint32_t> chunk;   // chunk of v each piece belongs to (the kernel logs it)
     };
     std::vector<Priv> priv_;
     static constexpr int kArenaFull = -1000;
@@ -702,7 +723,7 @@ private:
     std::vector<mma_segment_t> reseg_;
 
     PathState& path(int p) { return (*ps_)[p]; }
-    Lanes& lanes(int g) { return eng_.dev[g].lane[j_.dir]; }
+    Lanes& lanes(int g) { return j_.capturing ? eng_.dev[g].cap_lane[j_.dir] : eng_.dev[g].lane[j_.dir]; }
 
     int finish()
     {
@@ -750,6 +771,8 @@ private:
         if (make_plan(pp_.data(), P_, j_.B, j_.C, thr_, pm, plan_) != 0) return cudaErrorInvalidValue;
         t_.stats.calls++;
         t_.stats.bytes += j_.B;
+        t_.stats.validate_us += j_.validate_us;
+        t_.stats.ptr_queries += j_.ptr_queries;
         tr_.mark("plan");
         return cudaSuccess;
     }
@@ -758,9 +781,9 @@ private:
     // path in zero-copy mode is not native: it continues as a one-path plan.
     int native_fallback(bool* done)
     {
-        t_.stats.fallbacks++;
         const bool small = j_.B < thr_;
         if (small || resolve_mode(j_, pmode_[0]) != MMA_HOP_ZC) {
+            t_.stats.fallbacks++;
             DmaBatch b;
             j_.pieces(0, j_.B, [&](const Piece& x) { b.add(x.dst, x.src, x.len); });
             if (!small && host_order_) b.sort_by_host(kind_);   // a one-path plan, not a small copy
@@ -777,6 +800,7 @@ private:
             *done = true;
             return cudaSuccess;
         }
+        t_.stats.single_path_calls++;
         plan_.fallback = false;
         plan_.n = (j_.B - 1) / j_.C + 1;
         plan_.path.assign(plan_.n, 0);
@@ -868,6 +892,11 @@ private:
         tr_.mark("scratch");
         lists_.assign(P_, {});
         for (uint64_t i = 0; i < n_; i++) lists_[plan_.path[i]].push_back((uint32_t)i);
+        if (eng_.fault_misroute && P_ >= 2 && !lists_[0].empty() && !lists_[1].empty()) {   // test hook
+            const uint32_t c = lists_[0].back();
+            lists_[0].pop_back();
+            lists_[1].insert(std::lower_bound(lists_[1].begin(), lists_[1].end(), c), c);
+        }
         mode_.resize(P_);
         for (int p = 0; p < P_; p++) {
             mode_[p] = resolve_mode(j_, pmode_[p]);
@@ -912,7 +941,7 @@ private:
         for (auto& q : priv_)
             if (q.on) {
                 q.off = bytes;
-                bytes += (3 * q.npieces + 1) * 8;
+                bytes += (3 * q.npieces + 1) * 8 + ((q.npieces * 4 + 7) & ~(uint64_t)7);
             }
         tab_bytes_ = bytes;
         ctab_off_.assign(P_, 0);
@@ -949,6 +978,7 @@ private:
                 for (uint64_t k = 0; k < q.npieces; k++) w[k + 1] = w[k] + q.len[k];
                 memcpy(w + q.npieces + 1, q.src.data(), q.npieces * 8);
                 memcpy(w + 2 * q.npieces + 1, q.dst.data(), q.npieces * 8);
+                memcpy(w + 3 * q.npieces + 1, q.chunk.data(), q.npieces * 4);
             }
         }
         tr_.mark("tables");
@@ -957,25 +987,23 @@ private:
 
     bool e_plan_interleaved() const { return eng_.cfg.plan_mode == PLAN_INTERLEAVED; }
 
-    // path p's pieces (the parts of its chunks, in chunk order) reordered by host address:
-    // a private virtual stream of B_p bytes that the path's zero-copy kernel moves alone
+    // path p's pieces (the parts of its chunks, chunk by chunk) reordered by host address: a
+    // private virtual stream of B_p bytes that the path's zero-copy kernel moves alone. Each
+    // piece keeps the index of its chunk in v, which the kernel writes to the delivery log.
     void build_private(int p)
     {
         Priv& q = priv_[p];
         std::vector<uint64_t> src, dst, len;
-        const auto& L = lists_[p];
-        for (size_t a = 0; a < L.size();) {
-            size_t b = a + 1;
-            while (b < L.size() && L[b] == L[b - 1] + 1) b++;
-            uint64_t o0, l0, o1, l1;
-            j_.extent(L[a], &o0, &l0);
-            j_.extent(L[b - 1], &o1, &l1);
-            j_.pieces(o0, o1 + l1, [&](const Piece& x) {
+        std::vector<uint32_t> chunk;
+        for (uint32_t i : lists_[p]) {
+            uint64_t o, l;
+            j_.extent(i, &o, &l);
+            j_.pieces(o, o + l, [&](const Piece& x) {
                 src.push_back((uint64_t)x.src);
                 dst.push_back((uint64_t)x.dst);
                 len.push_back(x.len);
+                chunk.push_back(i);
             });
-            a = b;
         }
         std::vector<uint32_t> perm;
         order_by_key(j_.dir == MMA_D2H ? dst.data() : src.data(), src.size(), perm);
@@ -984,11 +1012,13 @@ private:
         q.src.resize(q.npieces);
         q.dst.resize(q.npieces);
         q.len.resize(q.npieces);
+        q.chunk.resize(q.npieces);
         q.B = 0;
         for (size_t k = 0; k < perm.size(); k++) {
             q.src[k] = src[perm[k]];
             q.dst[k] = dst[perm[k]];
             q.len[k] = len[perm[k]];
+            q.chunk[k] = chunk[perm[k]];
             q.B += q.len[k];
         }
     }
@@ -998,8 +1028,8 @@ private:
     {
         DeviceGuard g(j_.user_dev);
         CK(make_device(j_.user_dev));
-        CK(cudaEventRecord(eng_.dev[j_.user_dev].fork, j_.user));
-        fork_ = eng_.dev[j_.user_dev].fork;
+        fork_ = j_.capturing ? eng_.dev[j_.user_dev].cap_fork : eng_.dev[j_.user_dev].fork;
+        CK(cudaEventRecord(fork_, j_.user));
         return cudaSuccess;
     }
 
@@ -1075,6 +1105,12 @@ private:
     }
 
     // the private stream of zero-copy path p (build_private) on device g, and its chunks
+    const uint32_t* private_chunks_on(int p, int g) const
+    {
+        const Priv& q = priv_[p];
+        return (const uint32_t*)((const char*)dtab_[g] + q.off + (3 * q.npieces + 1) * 8);
+    }
+
     VStreamArg private_stream_on(int p, int g) const
     {
         const Priv& q = priv_[p];
@@ -1235,7 +1271,8 @@ private:
         }
         a.unit_bytes = eng_.unit_bytes;
         a.path = (uint32_t)p;
-        a.log = own ? nullptr : log_;
+        a.log = log_;
+        if (own) a.piece_chunk = private_chunks_on(p, g);   // the kernel logs each piece's chunk
         const uint64_t upc = (j_.C + eng_.unit_bytes - 1) / eng_.unit_bytes;
         const unsigned grid = (unsigned)std::min<uint64_t>(a.chunks.count * upc, zc_grid(g));
         DeviceGuard dg(g);
@@ -1245,22 +1282,7 @@ private:
             CK(launch_zc(a, grid, s));
         }
         t_.stats.kernels++;
-        // a private stream's chunks are not v's: the log entries of p's chunks are written
-        // behind the kernel on its stream, as for a copy-engine path
-        if (own && log_) CK(log_runs(p, s));
         if (j_.timing) j_.timing->end(p);
-        return cudaSuccess;
-    }
-
-    int log_runs(int p, cudaStream_t s)
-    {
-        const auto& L = lists_[p];
-        for (size_t a = 0; a < L.size();) {
-            size_t b = a + 1;
-            while (b < L.size() && L[b] == L[b - 1] + 1) b++;
-            CK(cudaMemsetAsync(log_ + L[a], p, b - a, s));
-            a = b;
-        }
         return cudaSuccess;
     }
 
@@ -1291,8 +1313,17 @@ private:
         return cudaSuccess;
     }
 
-    // ---- copy-engine relay rings (a5, a6 for H2D; a9 for D2H): one relay kernel launch per
-    // kernel GPU covering all of its rings, then the copy-engine hops chunk by chunk
+    // ---- copy-engine relay rings (a5, a6 for H2D; a9 for D2H), enqueued in WAVES of at most
+    // S chunks per ring, so that every wait the call enqueues depends only on work enqueued
+    // before it:
+    //   H2D wave w: the hops of w first (hop 1 of chunk c waits for the credit of chunk c - S,
+    //     which the pull kernel of an earlier wave releases), then the pull kernel of w;
+    //   D2H wave w: the pack kernel of w first (its credit waits name chunks of earlier waves,
+    //     whose hops are already enqueued), then the hops of w (they wait for its seq flags).
+    // The copy therefore completes when launches are serialised (CUDA_LAUNCH_BLOCKING, a
+    // profiler that runs each kernel alone), and a call that fails part-way leaves nothing
+    // waiting on work that was never issued. A wave holds at most S chunks of a ring because
+    // chunk c's slot last held chunk c - S, which must belong to an earlier wave.
     int enqueue_rings()
     {
         std::vector<int> rp;   // relay paths using rings
@@ -1309,21 +1340,85 @@ private:
         }
         if (!eng_.wait64 || !eng_.write64) return MMA_ERR_NO_MEMOPS;
         const uint32_t S = eng_.cfg.ring_slots;
-        const uint64_t upc = (j_.C + eng_.unit_bytes - 1) / eng_.unit_bytes;
         std::vector<Ring*> rings(P_, nullptr);
         std::vector<uint64_t> g0(P_, 0);
         for (int p : rp) {
             CK((cudaError_t)get_ring(j_.d, j_.dir, p, j_.C, S, &rings[p]));
             g0[p] = rings[p]->g_next;
         }
+        size_t maxc = 0;
+        for (int p : rp) maxc = std::max(maxc, lists_[p].size());
+        int rc = cudaSuccess;
+        for (size_t w0 = 0; w0 < maxc && rc == cudaSuccess; w0 += S) {
+            const size_t w1 = std::min<size_t>(maxc, w0 + S);
+            if (j_.dir == MMA_H2D) {
+                rc = wave_hops(rp, rings, g0, S, w0, w1);
+                if (rc == cudaSuccess) rc = wave_kernels(rp, rings, g0, S, w0, w1);
+            } else {
+                rc = wave_kernels(rp, rings, g0, S, w0, w1);
+                if (rc == cudaSuccess) rc = wave_hops(rp, rings, g0, S, w0, w1);
+            }
+        }
+        if (rc != cudaSuccess) {   // flags and counters may now be out of step with g_next
+            for (int p : rp) rings[p]->broken = true;
+            return rc;
+        }
+        for (int p : rp) rings[p]->g_next = g0[p] + lists_[p].size();
+        tr_.mark("rings");
+        return cudaSuccess;
+    }
+
+    // chunks per hop group: small chunks are grouped up to eng_.group_bytes (at most S/2, so a
+    // wave still holds two groups, one per hop stream: the dual pipeline); a chunk
+    // of group_bytes or more goes alone. A group's chunks are published together when its DMA
+    // ends, so large groups delay the relay's pull and the slots' reuse (measured: grouping
+    // 8 MiB chunks in pairs cut a loopback kernel ring from 0.93 to 0.90 of native).
+    size_t group_chunks(uint32_t S) const
+    {
+        const uint64_t k = eng_.group_bytes / std::max<uint64_t>(1, j_.C);
+        return (size_t)std::max<uint64_t>(1, std::min<uint64_t>(k, S / 2));
+    }
+
+    // the copy-engine side of ring chunks [w0, w1) of every ring. A ring's chunks go in groups
+    // (group_chunks) of consecutive chunks on consecutive slots: one DMA (or batch) and one
+    // batched flag operation per group instead of per chunk -- a stream memory operation and
+    // a DMA each cost microseconds of setup, which 1 MiB chunks feel. Groups are
+    // issued round-robin across rings.
+    int wave_hops(const std::vector<int>& rp, std::vector<Ring*>& rings, const std::vector<uint64_t>& g0,
+                  uint32_t S, size_t w0, size_t w1)
+    {
+        const size_t k = group_chunks(S);
+        std::vector<size_t> next(P_, w0);
+        for (bool any = true; any;) {
+            any = false;
+            for (int p : rp) {
+                const size_t end = std::min(lists_[p].size(), w1);
+                const size_t c0 = next[p];
+                if (c0 >= end) continue;
+                const uint32_t s0 = (uint32_t)((g0[p] + c0) % S);
+                const size_t c1 = c0 + std::min<size_t>({k, S - s0, end - c0});
+                CK(ring_hops(p, rings[p], g0[p], c0, c1, S, (s0 / k) & 1, mode_[p] == MMA_HOP_CE_P2P));
+                next[p] = c1;
+                // the path's last hop-1 (H2D) / last hop-2 (D2H) DMA closes its spans; the
+                // H2D forward of that chunk (one chunk over NVLink) is not attributed
+                if (j_.timing && c1 == lists_[p].size()) j_.timing->end(p);
+                any = true;
+            }
+        }
+        return cudaSuccess;
+    }
+
+    // one relay kernel launch per kernel GPU for ring chunks [w0, w1) of its kernel rings
+    int wave_kernels(const std::vector<int>& rp, std::vector<Ring*>& rings, const std::vector<uint64_t>& g0,
+                     uint32_t S, size_t w0, size_t w1)
+    {
+        const uint64_t upc = (j_.C + eng_.unit_bytes - 1) / eng_.unit_bytes;
         std::map<int, RelayLaunchArg> launches;
         std::map<int, unsigned> grids;
         for (int p : rp) {
+            if (mode_[p] == MMA_HOP_CE_P2P || lists_[p].size() <= w0) continue;   // no kernel
             Ring* r = rings[p];
-            if (mode_[p] == MMA_HOP_CE_P2P) {   // no kernel: the relay stream does both hops
-                r->g_next += lists_[p].size();
-                continue;
-            }
+            const size_t c1 = std::min(lists_[p].size(), w1);
             const int kd = r->kdev;
             auto& A = launches[kd];
             if (grids.find(kd) == grids.end()) {
@@ -1343,18 +1438,21 @@ private:
             R.credit = r->credit;
             R.cnt = r->cnt;
             R.cursor = r->cursor;
-            R.g0 = g0[p];
+            R.g0 = g0[p] + w0;
             R.unit0 = r->unit_next;
             R.chunks = chunks_on(p, kd);
+            R.chunks.count = c1 - w0;
+            if (R.chunks.table) R.chunks.table += w0;
+            else R.chunks.first += w0;
             R.S = S;
             R.path = (uint32_t)p;
             R.cta_begin = grids[kd];
-            grids[kd] += (unsigned)eng_.cfg.relay_ctas;
+            const unsigned ctas = (unsigned)std::min<uint64_t>((uint64_t)eng_.cfg.relay_ctas, R.chunks.count * upc);
+            grids[kd] += ctas;
             R.cta_end = grids[kd];
-            r->g_next += lists_[p].size();
             // every CTA of the ring claims until it draws one unit past the end, so the
             // cursor advances by the units plus one claim per CTA
-            r->unit_next += (unsigned long long)lists_[p].size() * upc + (unsigned)eng_.cfg.relay_ctas;
+            r->unit_next += (unsigned long long)R.chunks.count * upc + ctas;
         }
         for (auto& kv : launches) {
             const int kd = kv.first;
@@ -1363,22 +1461,10 @@ private:
             CK((cudaError_t)use(s, kd));
             DeviceGuard dg(kd);
             KTimer kt(kd, s, (j_.dir == MMA_H2D ? 1 : 2) | (j_.dir << 4) | (0xff << 8));
-            TSpan ts(kd, s, j_.dir == MMA_H2D ? "relay pull kernel" : "relay pack kernel", -1, -1, 0);
+            TSpan ts(kd, s, j_.dir == MMA_H2D ? "relay pull kernel" : "relay pack kernel", -1, (long long)w0, 0);
             CK(launch_relay(kv.second, j_.dir == MMA_H2D, grids[kd], s));
             t_.stats.kernels++;
         }
-        // host issue of the copy-engine hops, round-robin across rings chunk by chunk
-        size_t maxc = 0;
-        for (int p : rp) maxc = std::max(maxc, lists_[p].size());
-        for (size_t c = 0; c < maxc; c++)
-            for (int p : rp) {
-                if (c >= lists_[p].size()) continue;
-                CK(ring_hop(p, rings[p], g0[p] + c, lists_[p][c], S, mode_[p] == MMA_HOP_CE_P2P));
-                // the path's last hop-1 (H2D) / last hop-2 (D2H) DMA closes its spans; the
-                // H2D forward of that chunk (one chunk over NVLink) is not attributed
-                if (j_.timing && c + 1 == lists_[p].size()) j_.timing->end(p);
-            }
-        tr_.mark("rings");
         return cudaSuccess;
     }
 
@@ -1422,61 +1508,91 @@ private:
         return cudaSuccess;
     }
 
-    // the copy-engine side of ring chunk g (chunk index i of v) on the relay's hop stream.
-    // H2D: wait credit[s] >= g-S+1 (slot drained) -> DMA host -> slot -> publish seq[s] = g+1.
-    // D2H: wait seq[s] >= g+1 (slot packed by the relay kernel) -> DMA slot -> host ->
+    // the copy-engine side of ring chunks c0..c1-1 of path p (ring index g = gbase + c, slot
+    // g mod S, consecutive slots) on the relay's hop stream `lane`.
+    // H2D: wait credit[s] >= g-S+1 (slot drained) -> DMA host -> slots -> publish seq[s] = g+1.
+    // D2H: wait seq[s] >= g+1 (slot packed by the relay kernel) -> DMA slots -> host ->
     // release credit[s] = g+1.
     // p2p (MMA_HOP_CE_P2P): the same stream also does the other hop with a peer DMA, so the
-    // slot protocol (slot g mod S on stream s & 1, seq / credit) is the kernel ring's and the
-    // two kinds of ring may follow each other on one ring. H2D: ... publish seq -> DMA slot ->
-    // target pieces -> release credit. D2H: wait credit -> DMA source pieces -> slot -> publish
-    // seq -> DMA slot -> host -> release credit. The delivery log is written behind the final
-    // DMA on the stream.
-    int ring_hop(int p, Ring* r, uint64_t g, uint32_t i, uint32_t S, bool p2p)
+    // slot protocol (seq / credit per slot) is the kernel ring's and the two kinds of ring may
+    // follow each other on one ring. H2D: ... publish seq -> DMA slots -> target pieces ->
+    // release credit. D2H: wait credit -> DMA source pieces -> slots -> publish seq -> DMA
+    // slots -> host -> release credit. The delivery log is written behind the final DMA.
+    int ring_hops(int p, Ring* r, uint64_t gbase, size_t c0, size_t c1, uint32_t S, int lane, bool p2p)
     {
-        const uint32_t s = (uint32_t)(g % S);
-        cudaStream_t hs = lanes(r->relay).hop[s & 1];
+        if (eng_.fault_fail_hop >= 0 && eng_.hops_issued++ == eng_.fault_fail_hop) return cudaErrorUnknown;   // test hook
+        cudaStream_t hs = lanes(r->relay).hop[lane];
         CK((cudaError_t)use(hs, r->relay));
         DeviceGuard dg(r->relay);
-        char* slot = r->stage + (uint64_t)s * r->slot_bytes;
-        uint64_t off, len;
-        j_.extent(i, &off, &len);
-        auto wait = [&](uint64_t* flag, uint64_t v) -> int {
-            return eng_.wait64((CUstream)hs, (CUdeviceptr)flag, v, CU_STREAM_WAIT_VALUE_GEQ) == CUDA_SUCCESS
-                       ? cudaSuccess : cudaErrorUnknown;
-        };
-        auto write = [&](uint64_t* flag, uint64_t v) -> int {
-            return eng_.write64((CUstream)hs, (CUdeviceptr)flag, v, 0) == CUDA_SUCCESS ? cudaSuccess
-                                                                                         : cudaErrorUnknown;
+        auto slot_of = [&](size_t c) { return (uint32_t)((gbase + c) % S); };
+        // one batched stream memory operation: wait (GEQ) or write each listed flag
+        auto flags = [&](bool wait, uint64_t* base, uint64_t delta, bool credit_wait) -> int {
+            CUstreamBatchMemOpParams op[64];
+            unsigned n = 0;
+            for (size_t c = c0; c < c1; c++) {
+                const uint64_t g = gbase + c;
+                if (credit_wait && g < S) continue;                        // slot never used yet
+                if (!wait && base == r->seq && (long long)g == eng_.fault_drop_publish) continue;   // test hook
+                const uint64_t v = credit_wait ? g - S + 1 : g + delta;
+                uint64_t* addr = base + slot_of(c);
+                if (!eng_.batch_memop) {
+                    const CUresult e = wait ? eng_.wait64((CUstream)hs, (CUdeviceptr)addr, v, CU_STREAM_WAIT_VALUE_GEQ)
+                                            : eng_.write64((CUstream)hs, (CUdeviceptr)addr, v, 0);
+                    if (e != CUDA_SUCCESS) return cudaErrorUnknown;
+                    continue;
+                }
+                memset(&op[n], 0, sizeof(op[n]));
+                if (wait) {
+                    op[n].waitValue.operation = CU_STREAM_MEM_OP_WAIT_VALUE_64;
+                    op[n].waitValue.address = (CUdeviceptr)addr;
+                    op[n].waitValue.value64 = v;
+                    op[n].waitValue.flags = CU_STREAM_WAIT_VALUE_GEQ;
+                } else {
+                    op[n].writeValue.operation = CU_STREAM_MEM_OP_WRITE_VALUE_64;
+                    op[n].writeValue.address = (CUdeviceptr)addr;
+                    op[n].writeValue.value64 = v;
+                }
+                n++;
+            }
+            if (n && eng_.batch_memop((CUstream)hs, n, op, 0) != CUDA_SUCCESS) return cudaErrorUnknown;
+            return cudaSuccess;
         };
         auto dma = [&](bool to_slot, cudaMemcpyKind kind, bool host_side, const char* name) -> int {
             DmaBatch batch;
-            if (to_slot) j_.pieces(off, off + len, [&](const Piece& x) { batch.add(slot + (x.v - off), x.src, x.len); });
-            else j_.pieces(off, off + len, [&](const Piece& x) { batch.add(x.dst, slot + (x.v - off), x.len); });
+            uint64_t bytes = 0;
+            for (size_t c = c0; c < c1; c++) {
+                uint64_t off, len;
+                j_.extent(lists_[p][c], &off, &len);
+                char* slot = r->stage + (uint64_t)slot_of(c) * r->slot_bytes;
+                bytes += len;
+                if (to_slot) j_.pieces(off, off + len, [&](const Piece& x) { batch.add(slot + (x.v - off), x.src, x.len); });
+                else j_.pieces(off, off + len, [&](const Piece& x) { batch.add(x.dst, slot + (x.v - off), x.len); });
+            }
             if (host_side && host_order_) batch.sort_by_host(kind);
-            TSpan ts(r->relay, hs, name, p, (long long)i, len);
+            TSpan ts(r->relay, hs, name, p, (long long)lists_[p][c0], bytes);
             return batch.issue(kind, hs);
         };
         if (j_.dir == MMA_H2D) {
-            if (g >= S) CK(wait(&r->credit[s], g - S + 1));
+            CK(flags(true, r->credit, 0, true));
             CK(dma(true, cudaMemcpyHostToDevice, true, "DMA hop 1: host -> relay ring"));
-            if ((long long)g != eng_.fault_drop_publish) CK(write(&r->seq[s], g + 1));
+            CK(flags(false, r->seq, 1, false));
             if (p2p) {
                 CK(dma(false, cudaMemcpyDeviceToDevice, false, "DMA hop 2: relay ring -> target (peer)"));
-                CK(write(&r->credit[s], g + 1));
+                CK(flags(false, r->credit, 1, false));
             }
         } else {
             if (p2p) {
-                if (g >= S) CK(wait(&r->credit[s], g - S + 1));
+                CK(flags(true, r->credit, 0, true));
                 CK(dma(true, cudaMemcpyDeviceToDevice, false, "DMA hop 1: source (peer) -> relay ring"));
-                CK(write(&r->seq[s], g + 1));
+                CK(flags(false, r->seq, 1, false));
             } else {
-                CK(wait(&r->seq[s], g + 1));
+                CK(flags(true, r->seq, 1, false));
             }
             CK(dma(false, cudaMemcpyDeviceToHost, true, "DMA hop 2: relay ring -> host"));
-            CK(write(&r->credit[s], g + 1));
+            CK(flags(false, r->credit, 1, false));
         }
-        if (p2p && log_) CK(cudaMemsetAsync(log_ + i, p, 1, hs));
+        if (p2p && log_)
+            for (size_t c = c0; c < c1; c++) CK(cudaMemsetAsync(log_ + lists_[p][c], p, 1, hs));
         return cudaSuccess;
     }
 
@@ -1496,6 +1612,21 @@ private:
         return cudaSuccess;
     }
 
+    // this call's table buffers stay in use until the user stream passes the join
+    int mark_tables_busy()
+    {
+        if (!tab_bytes_ || !sc_) return cudaSuccess;
+        DeviceGuard g(j_.user_dev);
+        if (!sc_->done || sc_->done_dev != j_.user_dev) {
+            if (sc_->done) cudaEventDestroy(sc_->done);
+            CK(cudaEventCreateWithFlags(&sc_->done, cudaEventDisableTiming));
+            sc_->done_dev = j_.user_dev;
+        }
+        CK(cudaEventRecord(sc_->done, j_.user));
+        sc_->pending = true;
+        return cudaSuccess;
+    }
+
     int join()
     {
         CK(join_streams());
@@ -1504,16 +1635,7 @@ private:
             tr_.mark("join");
             return cudaSuccess;
         }
-        if (tab_bytes_) {
-            DeviceGuard g(j_.user_dev);
-            if (!sc_->done || sc_->done_dev != j_.user_dev) {
-                if (sc_->done) cudaEventDestroy(sc_->done);
-                CK(cudaEventCreateWithFlags(&sc_->done, cudaEventDisableTiming));
-                sc_->done_dev = j_.user_dev;
-            }
-            CK(cudaEventRecord(sc_->done, j_.user));
-            sc_->pending = true;
-        }
+        CK(mark_tables_busy());
         if (eng_.cfg.ledger && !dynamic_) {
             uint64_t lb[MMA_MAX_GPUS] = {}, lo[MMA_MAX_GPUS] = {};
             for (int p = 0; p < P_; p++) {

@@ -31,6 +31,7 @@ namespace mma {
 
 
 using PFN_memop64 = CUresult (*)(CUstream, CUdeviceptr, cuuint64_t, unsigned int);
+using PFN_batch_memop = CUresult (*)(CUstream, unsigned int, CUstreamBatchMemOpParams*, unsigned int);
 
 // 8 MiB: a copy-engine DMA costs ~4 us of setup on B200, so 1 MiB chunks reach 46 GB/s,
 // 4 MiB 52.6, 16 MiB 54.8 of the link's 55.6 (scripts/probe/probe_chunks.cu)
@@ -43,6 +44,7 @@ constexpr uint32_t kDefaultMbps = 50000;
 // (profiles/r01_probe_relay_unroll.txt)
 constexpr uint32_t kDefaultUnit = 512u << 10;
 constexpr int kDefaultRelayCtas = 8;
+constexpr uint64_t kDefaultGroupBytes = 2ull << 20;   // MMA_GROUP_BYTES
 constexpr int kDefaultZcCtas = 16;     // zero-copy kernel grid (mma_config_t::zc_ctas): the link saturates from 4-8
 constexpr unsigned kDynSlots = 64;        // per-call claim slots, rotating
 constexpr unsigned kDynSlotWords = 32;    // cursor + counts[MMA_KMAX_RINGS] (+ padding)
@@ -72,7 +74,13 @@ struct Lanes {
 struct DevRes {
     bool made = false;
     Lanes lane[2];                   // [MMA_H2D], [MMA_D2H]
+    // streams of captured calls only: a call on a capturing stream pulls every engine stream
+    // it uses into that capture until the user ends it, so captured calls never touch the
+    // live lanes (a live call on another stream may run in that window), and a second
+    // capture while these are still capturing is recorded as the native copy (api.cpp)
+    Lanes cap_lane[2];
     cudaEvent_t fork = nullptr;      // recorded on a user stream of this device
+    cudaEvent_t cap_fork = nullptr;  // idem, captured calls
     cudaStream_t setup = nullptr;    // ring initialisation (never waits on user work)
     cudaEvent_t cap_ev = nullptr;    // captured calls: orders the table frees after the join
     int sms = 148;
@@ -90,6 +98,10 @@ struct Ring {
     unsigned long long* cursor = nullptr;   // on kdev
     uint64_t g_next = 0;             // chunks carried so far (reading R18)
     unsigned long long unit_next = 0;
+    // a call failed part-way through this ring's enqueue: its flags and counters may be out
+    // of step with g_next / unit_next. get_ring drains both devices (every wait already
+    // enqueued is satisfiable, DESIGN §5 item 8) and makes the ring afresh.
+    bool broken = false;
 };
 
 struct PathState {
@@ -159,8 +171,10 @@ struct Engine {
     char* arena = nullptr;
     size_t arena_cap = 0, arena_used = 0;
     PFN_memop64 wait64 = nullptr, write64 = nullptr;
+    PFN_batch_memop batch_memop = nullptr;   // several flag waits / writes in one stream operation
     uint64_t timeout_ns = 20ull * 1000 * 1000 * 1000;
     uint32_t unit_bytes = kDefaultUnit;
+    uint64_t group_bytes = kDefaultGroupBytes;   // ring hop groups (plane.cpp group_chunks)
     bool upload_by_kernel = true;    // MMA_UPLOAD=ce: table uploads by the copy engine
     // fault injection (tests only, MMA_FAULT_DROP_PUBLISH=g): the hop-1 publish of global
     // ring chunk g is never issued, so the relay kernel must time out, record the sticky
@@ -169,6 +183,15 @@ struct Engine {
     // fault injection (tests only, MMA_FAULT_FAIL_RINGS=1): the ring stage of every call fails
     // after the direct path was enqueued, to check that a failed call still joins its streams
     bool fault_fail_rings = false;
+    // fault injection (tests only, MMA_FAULT_FAIL_HOP=k): the k-th copy-engine ring hop the
+    // engine enqueues (counted from init, 0-based) fails once, in the middle of a call whose
+    // rings have already advanced, to check ring poisoning and the join of a failed call
+    long long fault_fail_hop = -1;
+    // fault injection (tests only, MMA_FAULT_MISROUTE=1): after planning, path 0's last chunk
+    // is moved to path 1's work list, so the engine carries a plan other than the one it
+    // reports; the delivery log (written by the hop that moves each chunk) must show it
+    bool fault_misroute = false;
+    long long hops_issued = 0;
 };
 
 Engine& E();
@@ -220,6 +243,9 @@ struct Job {
     uint64_t nseg = 0;
     std::vector<uint64_t> vstart;    // segmented: prefix offsets [nseg + 1]
     bool mapped = false;             // every host address is usable by GPU SMs
+    bool pageable = false;           // segmented: some host segment is pageable (native copy)
+    double validate_us = 0;          // segmented: host time classifying the table
+    uint64_t ptr_queries = 0;
     const uint32_t* bw_override = nullptr;   // measurement runs: per-path bandwidth
     const int* mode_override = nullptr;      // measurement runs: per-path mode
     bool no_small_fallback = false;          // measurement runs: ignore the threshold

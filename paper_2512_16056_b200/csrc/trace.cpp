@@ -35,9 +35,10 @@ std::string stream_name(cudaStream_t s)
     for (int d = 0; d < e.ndev; d++) {
         const DevRes& r = e.dev[d];
         if (!r.made) continue;
-        for (int dir = 0; dir < 2; dir++) {
-            const Lanes& l = r.lane[dir];
-            const std::string sfx = dir == MMA_H2D ? " (H2D)" : " (D2H)";
+        for (int k = 0; k < 4; k++) {
+            const int dir = k & 1;
+            const Lanes& l = k < 2 ? r.lane[dir] : r.cap_lane[dir];
+            const std::string sfx = std::string(dir == MMA_H2D ? " (H2D" : " (D2H") + (k < 2 ? ")" : ", captured)");
             if (s == l.direct) return "direct DMA" + sfx;
             if (s == l.hop[0]) return "relay hop stream 0" + sfx;
             if (s == l.hop[1]) return "relay hop stream 1" + sfx;

@@ -408,6 +408,7 @@ int mma_tune_segments(const mma_segment_t* segs, size_t nsegs, int device, mma_d
     Job j;
     CK(prepare_segments(dir, segs, nsegs, device, (cudaStream_t)stream, j));
     if (j.B == 0) return cudaSuccess;
+    if (j.pageable) return cudaErrorInvalidValue;   // tuning measures pinned transfers only
     std::lock_guard<std::mutex> g(e.mu);
     CK(make_device(device));
     make_paths(device);

@@ -77,6 +77,7 @@ class Stats(C.Structure):
         ("relay_bytes", C.c_uint64), ("kernels", C.c_uint64), ("issue_us", C.c_double),
         ("wait_us", C.c_double), ("dynamic_calls", C.c_uint64),
         ("numa_known_bytes", C.c_uint64 * 2), ("numa_local_bytes", C.c_uint64 * 2),
+        ("single_path_calls", C.c_uint64), ("validate_us", C.c_double), ("ptr_queries", C.c_uint64),
     ]
 
 
@@ -413,7 +414,8 @@ def get_stats(device: int) -> dict:
                 path_bytes=[list(x) for x in s.path_bytes], path_chunks=[list(x) for x in s.path_chunks],
                 relay_bytes=s.relay_bytes, kernels=s.kernels, issue_us=s.issue_us,
                 wait_us=s.wait_us, dynamic_calls=s.dynamic_calls,
-                numa_known_bytes=list(s.numa_known_bytes), numa_local_bytes=list(s.numa_local_bytes))
+                numa_known_bytes=list(s.numa_known_bytes), numa_local_bytes=list(s.numa_local_bytes),
+                single_path_calls=s.single_path_calls, validate_us=s.validate_us, ptr_queries=s.ptr_queries)
 
 
 def set_plan_mode(mode: int) -> None:

@@ -214,3 +214,72 @@ def test_replays_concurrent_with_live_ring_calls(mma):
         assert torch.equal(gdst.cpu(), gsrc[:B]), it
         assert torch.equal(ldst.cpu(), lsrc[:B]), it
     assert mma.get_last_error() == 0
+
+
+def test_live_call_while_a_capture_is_open(mma):
+    """a captured call must not pull the streams live calls use into its capture.
+    Between a captured mma call and the end of that capture, a live call on another stream
+    runs at once (its bytes are there when its stream is synchronised, still inside the
+    capture window), and the graph replays correctly afterwards."""
+    configure(mma, loopback=1, chunk=MiB, debug=0)
+    _two_paths(mma, mma.H2D)
+    B = 12 * MiB + 4096
+    gsrc, lsrc = pinned(torch, B, seed=71), pinned(torch, B, seed=72)
+    gdst = torch.zeros(B, dtype=torch.uint8, device="cuda")
+    ldst = torch.zeros(B, dtype=torch.uint8, device="cuda")
+    mma.memcpy_h2d(gdst, gsrc, B)                     # uncaptured first: device state exists
+    torch.cuda.synchronize()
+    gdst.zero_()
+    torch.cuda.synchronize()
+    live = torch.cuda.Stream()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, capture_error_mode="relaxed"):
+        mma.memcpy_h2d(gdst, gsrc, B)                 # captured
+        with torch.cuda.stream(live):                 # live, same paths, capture still open
+            mma.memcpy_h2d(ldst, lsrc, B, stream=live)
+            live_ok = torch.equal(ldst.cpu(), lsrc[:B])
+    assert live_ok
+    assert not gdst.any().item()                      # nothing ran at capture time
+    mma_inputs.fill_pattern(gsrc.numpy()[:B], 73)
+    g.replay()
+    torch.cuda.synchronize()
+    assert torch.equal(gdst.cpu(), gsrc[:B])
+    assert mma.get_last_error() == 0
+
+
+def test_second_open_capture_records_native(mma):
+    """two captures open at once: the second finds the capture lanes still capturing and
+    records the native copy (no edge ties the two graphs); both replay correctly"""
+    configure(mma, loopback=1, chunk=MiB, debug=0)
+    _two_paths(mma, mma.H2D)
+    B = 8 * MiB
+    s1, s2 = pinned(torch, B, seed=81), pinned(torch, B, seed=82)
+    d1 = torch.zeros(B, dtype=torch.uint8, device="cuda")
+    d2 = torch.zeros(B, dtype=torch.uint8, device="cuda")
+    mma.memcpy_h2d(d1, s1, B)
+    torch.cuda.synchronize()
+    st1, st2 = torch.cuda.Stream(), torch.cuda.Stream()
+    g1, g2 = torch.cuda.CUDAGraph(), torch.cuda.CUDAGraph()
+    k0 = mma.get_stats(0)["kernels"]
+    # raw capture API through torch streams: begin both, record one call into each, end both
+    with torch.cuda.stream(st1):
+        g1.capture_begin(capture_error_mode="relaxed")
+        mma.memcpy_h2d(d1, s1, B, stream=st1)
+    k1 = mma.get_stats(0)["kernels"]
+    with torch.cuda.stream(st2):
+        g2.capture_begin(capture_error_mode="relaxed")
+        mma.memcpy_h2d(d2, s2, B, stream=st2)
+    k2 = mma.get_stats(0)["kernels"]
+    with torch.cuda.stream(st2):
+        g2.capture_end()
+    with torch.cuda.stream(st1):
+        g1.capture_end()
+    assert k1 == k0 + 1 and k2 == k1                  # the second call is the native copy
+    for seed in (83, 84):
+        mma_inputs.fill_pattern(s1.numpy()[:B], seed)
+        mma_inputs.fill_pattern(s2.numpy()[:B], seed + 10)
+        g1.replay()
+        g2.replay()
+        torch.cuda.synchronize()
+        assert torch.equal(d1.cpu(), s1[:B]) and torch.equal(d2.cpu(), s2[:B]), seed
+    assert mma.get_last_error() == 0

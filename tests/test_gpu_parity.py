@@ -191,7 +191,7 @@ def test_stats_account_paths(mma):
     st = mma.get_stats(0)
     assert st["path_chunks"][0][:2] == [12, 4] and st["path_chunks"][1][:2] == [0, 0]
     assert st["path_bytes"][0][0] + st["path_bytes"][0][1] == B and st["relay_bytes"] == 4 * MiB
-    assert st["kernels"] == 1
+    assert st["kernels"] == 2                 # relay pull kernels: one per wave of S = 2 ring chunks
 
 
 def test_device_generator_matches_host(mma):

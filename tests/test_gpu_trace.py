@@ -27,7 +27,8 @@ def test_trace_spans(tmp_path):
     p = tmp_path / "t.json"
     n = mma.trace_end(str(p))
     ev = json.load(open(p))["traceEvents"]
-    assert n == len(ev) == 1 + 8 + 1          # one direct run, 8 relay chunks, one relay kernel
+    # one direct run, 8 relay chunks, one relay kernel per wave of S = 2 ring chunks
+    assert n == len(ev) == 1 + 8 + 4
     names = {e["name"] for e in ev}
     assert {"DMA direct", "DMA hop 1: host -> relay ring", "relay pull kernel"} <= names
     assert all(e["dur"] > 0 for e in ev)
