@@ -288,6 +288,13 @@ int mma_plan_chunks(const uint32_t* mbps, const int* kinds, const uint64_t* back
  * `device`, as written on the GPU by the final hop (needs cfg.debug_log; synchronises). */
 int mma_get_delivery_log(int device, uint8_t* path_of_chunk, size_t cap, size_t* nchunks);
 
+/* Debug (cfg.debug_log): the order of the segments in the virtual stream v of the last
+ * scattered call to `device` -- order[k] = table index of v's k-th segment. It is the table
+ * order unless the call was regrouped by host NUMA node (reading R23, §5.1.1; the
+ * oracle's orc_numa_order). With mma_get_delivery_log it gives the path that carried every
+ * byte. *nsegs = 0 after a contiguous or native call. cap < *nsegs -> cudaErrorInvalidValue. */
+int mma_get_segment_order(int device, uint32_t* order, size_t cap, size_t* nsegs);
+
 /* Chunks each path took in the most recent dynamic-pull call to/from `device`
  * (synchronises; *npaths = 0 if none). */
 int mma_get_dynamic_counts(int device, uint64_t* chunks, int cap, int* npaths);

@@ -64,6 +64,7 @@ def lib():
         L.orc_check_events.argtypes = [C.c_void_p, p(Path_), C.c_int, C.c_void_p, u64,
                                        C.c_uint32, C.c_void_p]
         L.orc_ring_explore.argtypes = [C.c_int, C.c_int, u64, C.c_int, p(u64), p(u64)]
+        L.orc_numa_order.argtypes = [C.c_void_p, u64, p(Path_), C.c_void_p, C.c_int, C.c_void_p]
         _lib = L
     return _lib
 
@@ -76,6 +77,15 @@ def make_paths(bw, kinds=None, backlog=None):
         arr[i].bw_mbps = int(bw[i])
         arr[i].backlog = int(backlog[i]) if backlog is not None else 0
     return arr
+
+
+def numa_order(seg_node, bw, path_node, kinds=None):
+    """Reading R23: the table order of v's segments, regrouped by host node."""
+    sn = np.ascontiguousarray(seg_node, dtype=np.int32)
+    pn = np.ascontiguousarray(path_node, dtype=np.int32)
+    out = np.zeros(max(1, sn.size), dtype=np.uint32)
+    lib().orc_numa_order(sn.ctypes.data, sn.size, make_paths(bw, kinds), pn.ctypes.data, len(bw), out.ctypes.data)
+    return out[: sn.size]
 
 
 def nchunks(B: int, C_: int) -> int:

@@ -185,6 +185,45 @@ static void vs_copy(const vstream* vs, uint64_t a, uint64_t b, int what, unsigne
     }
 }
 
+/* ---------------------------------------------------- NUMA-affine order (R23) --- */
+
+/* Bucket pass, one group at a time, written for the eye rather than for speed: collect the
+ * groups' nodes in the reading's order, then for each group append its segments in table
+ * order; the unknown group last. */
+void orc_numa_order(const int32_t* seg_node, uint64_t nsegs, const orc_path* paths,
+                    const int32_t* path_node, int P, uint32_t* order)
+{
+    int32_t groups[256];
+    int ng = 0, npath_nodes;
+    for (int p = 0; p < P; p++) {                       /* path nodes, in path order */
+        if (paths[p].bw_mbps == 0 || path_node[p] < 0) continue;
+        int seen = 0;
+        for (int g = 0; g < ng; g++) seen |= groups[g] == path_node[p];
+        if (!seen && ng < 256) groups[ng++] = path_node[p];
+    }
+    npath_nodes = ng;
+    for (uint64_t k = 0; k < nsegs; k++) order[k] = (uint32_t)k;
+    if (npath_nodes < 2 || nsegs < 2) return;           /* as given */
+    for (;;) {                                          /* other known nodes, ascending */
+        int32_t next = -1;
+        for (uint64_t k = 0; k < nsegs; k++) {
+            int32_t nd = seg_node[k], listed = 0;
+            if (nd < 0) continue;
+            for (int g = 0; g < ng; g++) listed |= groups[g] == nd;
+            if (!listed && (next < 0 || nd < next)) next = nd;
+        }
+        if (next < 0 || ng >= 255) break;
+        groups[ng++] = next;
+    }
+    groups[ng++] = -1;                                  /* unknown last */
+    uint64_t o = 0;
+    for (int g = 0; g < ng; g++)
+        for (uint64_t k = 0; k < nsegs; k++) {
+            int32_t nd = seg_node[k] < 0 ? -1 : seg_node[k];
+            if (nd == groups[g]) order[o++] = (uint32_t)k;
+        }
+}
+
 static int cmp_dst(const void* x, const void* y)
 {
     const orc_segment* a = (const orc_segment*)x;

@@ -119,6 +119,21 @@ int orc_move(const orc_segment* segs, uint64_t nsegs, uint64_t C,
              uint32_t S, const uint64_t* base, int exec, uint64_t* events,
              uint32_t* write_count, int fault);
 
+/*
+ * NUMA-affine order of a scattered transfer's segments (reading R23): the
+ * paper's bandwidth saturates at six GPUs because "typically four GPUs reside within a
+ * single NUMA node, while cross-NUMA H2D transfers rely on the UPI link" (§5.1.1),
+ * so the virtual stream v is the segment table regrouped by the host node of each segment:
+ *   groups, in this order: each distinct node of the paths that may carry bytes (bw > 0,
+ *   path_node >= 0), in path order; then every other known node, ascending; then unknown
+ *   nodes (-1). Inside a group, table order.
+ * With fewer than two distinct path nodes (or fewer than two segments) v is the table as
+ * given. order[k] = table index of the k-th segment of v. The planner then runs on v
+ * unchanged (§8(c) step 6).
+ */
+void orc_numa_order(const int32_t* seg_node, uint64_t nsegs, const orc_path* paths,
+                    const int32_t* path_node, int P, uint32_t* order);
+
 /* 1 if the segment destinations are pairwise disjoint, else 0. */
 int orc_segments_disjoint(const orc_segment* segs, uint64_t nsegs);
 

@@ -616,6 +616,21 @@ int mma_get_delivery_log(int device, uint8_t* path_of_chunk, size_t cap, size_t*
     return cudaSuccess;
 }
 
+int mma_get_segment_order(int device, uint32_t* order, size_t cap, size_t* nsegs)
+{
+    CK((cudaError_t)ensure_init());
+    Engine& e = E();
+    if (device < 0 || device >= e.ndev) return cudaErrorInvalidDevice;
+    if (!nsegs) return cudaErrorInvalidValue;
+    std::lock_guard<std::mutex> g(e.mu);
+    const auto& o = e.tgt[device].last_order;
+    *nsegs = o.size();
+    if (!order || o.empty()) return cudaSuccess;
+    if (cap < o.size()) return cudaErrorInvalidValue;
+    memcpy(order, o.data(), o.size() * sizeof(uint32_t));
+    return cudaSuccess;
+}
+
 int mma_host_alloc(void** ptr, size_t bytes, unsigned flags)
 {
     CK((cudaError_t)ensure_init());

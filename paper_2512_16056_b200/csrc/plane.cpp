@@ -253,6 +253,7 @@ int do_init(const mma_config_t* cfg)
         e.timeout_ns = (uint64_t)env_size("MMA_SPIN_TIMEOUT_MS", 20000) * 1000000ull;
         e.unit_bytes = (uint32_t)env_size("MMA_UNIT_BYTES", kDefaultUnit);
         e.group_bytes = env_size("MMA_GROUP_BYTES", kDefaultGroupBytes);
+        e.hop_lanes = env_int("MMA_HOP_LANES", 2) == 1 ? 1 : 2;
         if (const char* u = getenv("MMA_UPLOAD")) e.upload_by_kernel = strcmp(u, "ce") != 0;
         const char* f = getenv("MMA_FAULT_DROP_PUBLISH");
         e.fault_drop_publish = f ? atoll(f) : -1;
@@ -772,6 +773,7 @@ private:
         t_.stats.calls++;
         t_.stats.bytes += j_.B;
         t_.stats.validate_us += j_.validate_us;
+        t_.last_order.clear();
         t_.stats.ptr_queries += j_.ptr_queries;
         tr_.mark("plan");
         return cudaSuccess;
@@ -816,6 +818,10 @@ private:
     int numa_regroup()
     {
         if (j_.contiguous || j_.nseg < 2) return cudaSuccess;
+        if (eng_.cfg.debug_log) {   // identity unless regrouped below
+            t_.last_order.resize(j_.nseg);
+            for (uint64_t k = 0; k < j_.nseg; k++) t_.last_order[k] = (uint32_t)k;
+        }
         std::vector<int> order;   // distinct known nodes of the paths that may carry bytes
         for (int p = 0; p < P_; p++) {
             const int nd = path(p).node;
@@ -840,6 +846,7 @@ private:
         std::stable_sort(idx.begin(), idx.end(), [&](uint32_t a, uint32_t b) {
             return rank(seg_node_[a]) < rank(seg_node_[b]);
         });
+        if (eng_.cfg.debug_log) t_.last_order = idx;
         reseg_.resize(n);
         std::vector<int> nodes(n);
         for (uint64_t k = 0; k < n; k++) {
@@ -1397,7 +1404,8 @@ private:
                 if (c0 >= end) continue;
                 const uint32_t s0 = (uint32_t)((g0[p] + c0) % S);
                 const size_t c1 = c0 + std::min<size_t>({k, S - s0, end - c0});
-                CK(ring_hops(p, rings[p], g0[p], c0, c1, S, (s0 / k) & 1, mode_[p] == MMA_HOP_CE_P2P));
+                CK(ring_hops(p, rings[p], g0[p], c0, c1, S, eng_.hop_lanes > 1 ? (int)((s0 / k) & 1) : 0,
+                             mode_[p] == MMA_HOP_CE_P2P));
                 next[p] = c1;
                 // the path's last hop-1 (H2D) / last hop-2 (D2H) DMA closes its spans; the
                 // H2D forward of that chunk (one chunk over NVLink) is not attributed

@@ -44,7 +44,7 @@ constexpr uint32_t kDefaultMbps = 50000;
 // (profiles/r01_probe_relay_unroll.txt)
 constexpr uint32_t kDefaultUnit = 512u << 10;
 constexpr int kDefaultRelayCtas = 8;
-constexpr uint64_t kDefaultGroupBytes = 2ull << 20;   // MMA_GROUP_BYTES
+constexpr uint64_t kDefaultGroupBytes = 8ull << 20;   // MMA_GROUP_BYTES (profiles/r02_sweep_group_lanes.jsonl)
 constexpr int kDefaultZcCtas = 16;     // zero-copy kernel grid (mma_config_t::zc_ctas): the link saturates from 4-8
 constexpr unsigned kDynSlots = 64;        // per-call claim slots, rotating
 constexpr unsigned kDynSlotWords = 32;    // cursor + counts[MMA_KMAX_RINGS] (+ padding)
@@ -134,6 +134,9 @@ struct Target {
     mma_stats_t stats{};
     uint8_t* log = nullptr;
     size_t log_cap = 0, log_n = 0;
+    // debug_log: the table order of the last scattered call's virtual stream (R23 regrouping;
+    // identity when not regrouped): last_order[k] = table index of v's k-th segment
+    std::vector<uint32_t> last_order;
     Scratch scratch[4];   // table buffers of the last 4 calls (a ring)
     unsigned parity = 0;
     unsigned long long* dyn = nullptr;        // dynamic-pull slots: cursor + per-path counts
@@ -175,6 +178,7 @@ struct Engine {
     uint64_t timeout_ns = 20ull * 1000 * 1000 * 1000;
     uint32_t unit_bytes = kDefaultUnit;
     uint64_t group_bytes = kDefaultGroupBytes;   // ring hop groups (plane.cpp group_chunks)
+    int hop_lanes = 2;                           // relay hop streams per direction used (1 or 2)
     bool upload_by_kernel = true;    // MMA_UPLOAD=ce: table uploads by the copy engine
     // fault injection (tests only, MMA_FAULT_DROP_PUBLISH=g): the hop-1 publish of global
     // ring chunk g is never issued, so the relay kernel must time out, record the sticky

@@ -24,7 +24,7 @@ SYMBOLS = [
     "mma_default_config", "mma_init", "mma_finalize", "mma_memcpy_h2d", "mma_memcpy_d2h",
     "mma_memcpy_h2d_segments", "mma_memcpy_d2h_segments", "mma_get_paths", "mma_set_bandwidth",
     "mma_set_path_modes", "mma_calibrate", "mma_get_plan", "mma_plan_chunks",
-    "mma_get_delivery_log", "mma_host_alloc", "mma_host_free", "mma_get_stats",
+    "mma_get_delivery_log", "mma_get_segment_order", "mma_host_alloc", "mma_host_free", "mma_get_stats",
     "mma_reset_stats", "mma_get_last_error", "mma_error_string", "mma_fill_pattern",
     "mma_verify_pattern", "mma_verify_segments", "mma_set_kernel_timing", "mma_kernel_times",
     "mma_tune_segments", "mma_get_segment_tuning", "mma_get_dynamic_counts", "mma_set_plan_mode",
@@ -116,6 +116,7 @@ def lib():
         L.mma_plan_chunks.argtypes = [vp, vp, vp, C.c_int, C.c_uint64, C.c_uint64, C.c_uint64,
                                       C.c_int, vp, sz, C.POINTER(sz), C.POINTER(C.c_int)]
         L.mma_get_delivery_log.argtypes = [C.c_int, vp, sz, C.POINTER(sz)]
+        L.mma_get_segment_order.argtypes = [C.c_int, vp, sz, C.POINTER(sz)]
         L.mma_host_alloc.argtypes = [C.POINTER(vp), sz, C.c_uint]
         L.mma_host_free.argtypes = [vp]
         L.mma_get_stats.argtypes = [C.c_int, C.POINTER(Stats)]
@@ -389,6 +390,17 @@ def get_delivery_log(device: int):
     buf = (C.c_uint8 * max(n.value, 1))()
     _check(lib().mma_get_delivery_log(device, buf, n.value, C.byref(n)), "mma_get_delivery_log")
     return bytes(buf[: n.value])
+
+
+def get_segment_order(device: int):
+    """Debug: table index of each segment of the last scattered call's virtual stream."""
+    import numpy as np
+    n = C.c_size_t()
+    _check(lib().mma_get_segment_order(device, None, 0, C.byref(n)), "mma_get_segment_order")
+    out = np.zeros(max(1, n.value), dtype=np.uint32)
+    _check(lib().mma_get_segment_order(device, out.ctypes.data, n.value, C.byref(n)),
+           "mma_get_segment_order")
+    return out[: n.value]
 
 
 def host_alloc(nbytes: int) -> int:

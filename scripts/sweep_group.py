@@ -8,7 +8,7 @@ from pathlib import Path
 
 ROOT = Path(__file__).resolve().parents[1]
 CHILD = r'''
-import json, statistics, sys
+import json, os, statistics, sys
 sys.path.insert(0, %r)
 import torch
 import paper_2512_16056_b200 as mma
@@ -40,10 +40,11 @@ for kind, hop in (("kernel", mma.HOP_CE), ("ce_p2p", mma.HOP_CE_P2P)):
             mma.set_bandwidth(0, d, [0, 1])
         h = B / timed(lambda: mma.memcpy_h2d(dev, host, B, stream=s)) / 1e6
         d2 = B / timed(lambda: mma.memcpy_d2h(host, dev, B, stream=s)) / 1e6
-        print(json.dumps({"group_bytes": %d, "kind": kind, "C": C, "S": S, "h2d_frac": round(h / nat["h2d"], 3),
+        print(json.dumps({"group_bytes": %d, "lanes": os.environ.get("MMA_HOP_LANES", "2"), "kind": kind, "C": C, "S": S, "h2d_frac": round(h / nat["h2d"], 3),
                           "d2h_frac": round(d2 / nat["d2h"], 3), "native": {k: round(v, 2) for k, v in nat.items()}}), flush=True)
         assert mma.get_last_error() == 0
 '''
+# argv: group-bytes values; MMA_HOP_LANES from the environment is passed through
 for gb in [int(x) for x in (sys.argv[1:] or ["0", str(2 << 20), str(4 << 20)])]:
     env = dict(os.environ, MMA_GROUP_BYTES=str(gb))
     subprocess.run([sys.executable, "-c", CHILD % (str(ROOT), gb)], env=env, check=False)

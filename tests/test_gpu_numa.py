@@ -2,12 +2,19 @@
 the test hooks MMA_FAKE_HOST_NODES (host node = 2 MiB region index mod K) and
 MMA_FAKE_PATH_NODES (node per path index): the direct path on node 0, a loopback relay on
 node 1. Regrouping the table by node must make (almost) every byte travel on a path of its own
-node, against about half without it -- and the bytes must stay exactly the oracle's."""
+node, against about half without it -- and the bytes must stay exactly the oracle's.
+
+Parity covers WHICH path carried every byte, not only the chunk indices: the engine's
+virtual-stream order (mma_get_segment_order) and delivery log give a per-byte path map,
+compared with the oracle's: orc_numa_order (the regrouping step, pinned by
+tests/test_oracle_numa.py) on the same per-segment nodes, then orc_plan on the regrouped
+stream (VERDICT r1 weak #1)."""
 import os
 import subprocess
 import sys
 from pathlib import Path
 
+import numpy as np
 import pytest
 
 ROOT = Path(__file__).resolve().parents[1]
@@ -45,7 +52,8 @@ if dirn == 0:
 else:
     ok = bool(np.array_equal(pool.numpy().reshape(2 * nseg, sb)[slots], src_host.reshape(nseg, sb)))
 print(json.dumps(dict(ok=ok, known=st["numa_known_bytes"][dirn], local=st["numa_local_bytes"][dirn],
-                      log=list(mma.get_delivery_log(0)), err=mma.get_last_error())))
+                      log=list(mma.get_delivery_log(0)), err=mma.get_last_error(),
+                      order=mma.get_segment_order(0).tolist(), host=[int(x) for x in hs])))
 """
 
 
@@ -74,3 +82,31 @@ def test_node_affine_plan(tmp_path, dirn):
         assert bytes(r["log"]) == path.tobytes()          # the plan is the oracle's either way
     assert on["local"] / B > 0.9, on["local"] / B        # regrouped: bytes travel on their node
     assert 0.35 < off["local"] / B < 0.65, off["local"] / B   # table order: about half
+    # per-byte path maps: engine (its v order + its log) vs oracle (orc_numa_order + orc_plan)
+    nseg, sb = 2048, 64 << 10
+    seg_node = (np.array(on["host"], dtype=np.uint64) >> np.uint64(21)) % np.uint64(2)
+    exp_order = oracle.numa_order(seg_node.astype(np.int32), [1, 1], [0, 1])
+    assert on["order"] == exp_order.tolist()
+    assert off["order"] == list(range(nseg))              # numa_plan = 0: table order
+    for r, order in ((on, exp_order), (off, np.arange(nseg))):
+        got = per_byte_paths(np.array(r["order"]), [sb] * nseg, bytes(r["log"]), 1 << 20)
+        exp = per_byte_paths(order, [sb] * nseg, path.tobytes(), 1 << 20)
+        assert np.array_equal(got, exp)
+    # the oracle's map itself: regrouped, > 90% of bytes on a path of their own node
+    pmap = per_byte_paths(exp_order, [sb] * nseg, path.tobytes(), 1 << 20).reshape(nseg, sb)
+    local = (np.array([0, 1])[pmap] == seg_node.astype(np.int64)[:, None]).mean()
+    assert local > 0.9, local
+
+
+def per_byte_paths(order, lens, log, C):
+    """path of every byte of the transfer, in TABLE order: v holds the table's segments in
+    `order`, and byte y of v rides log[y // C]"""
+    lens = np.asarray(lens, dtype=np.int64)
+    vlen = lens[order]
+    vstart = np.concatenate([[0], np.cumsum(vlen)])
+    pbv = np.repeat(np.frombuffer(log, dtype=np.uint8), C)[: vstart[-1]]
+    tstart = np.concatenate([[0], np.cumsum(lens)])
+    out = np.empty(int(tstart[-1]), dtype=np.uint8)
+    for k, t in enumerate(order):
+        out[tstart[t]:tstart[t + 1]] = pbv[vstart[k]:vstart[k + 1]]
+    return out

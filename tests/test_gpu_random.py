@@ -4,7 +4,9 @@ offsets) through the C ABI, each compared byte for byte with the oracle moving t
 transfer with the same assignment (the planned one, or the observed one in dynamic mode).
 Rings persist across cases, so sequence bases and slot reuse vary too. The work order inside
 a path (host_order) and CUDA graph capture + replay are drawn at random as well; neither may
-change a byte."""
+change a byte. In planned mode the delivery log must equal the oracle's plan and, for
+scattered tables (with faked NUMA nodes a quarter of the time), the engine's virtual-stream
+order must equal the oracle's orc_numa_order: together the path of every byte."""
 import numpy as np
 import pytest
 
@@ -53,8 +55,10 @@ def test_random_transfers(mma, orc):
         capture = plan_mode != 2 and rng.random() < 0.15
         fake_numa = rng.random() < 0.25      # R23 regrouping with faked host / path nodes
         if fake_numa:
-            os.environ["MMA_FAKE_HOST_NODES"] = str(int(rng.integers(2, 4)))
-            os.environ["MMA_FAKE_PATH_NODES"] = ",".join(str(int(x)) for x in rng.integers(0, 3, P))
+            K = int(rng.integers(2, 4))
+            path_node = [int(x) for x in rng.integers(0, 3, P)]
+            os.environ["MMA_FAKE_HOST_NODES"] = str(K)
+            os.environ["MMA_FAKE_PATH_NODES"] = ",".join(str(x) for x in path_node)
         else:
             os.environ.pop("MMA_FAKE_HOST_NODES", None)
             os.environ.pop("MMA_FAKE_PATH_NODES", None)
@@ -113,13 +117,26 @@ def test_random_transfers(mma, orc):
             rc, path, _, fb = orc.plan(bw, B, C, 0, plan_mode)
             assert rc == 0
         elif dynamic:
+            fb = False
             path = np.frombuffer(mma.get_delivery_log(0), dtype=np.uint8)
             assert path.size == (B + C - 1) // C and (path < P).all(), case
         else:
             rc, path, _, fb = orc.plan(bw, B, C, 0, 0 if plan_mode == 2 else plan_mode)
             assert rc == 0
+        # the virtual stream's segment order: the oracle's NUMA-affine order (R23) of the same
+        # per-segment host nodes (the fake hook: 2 MiB region index mod K), else table order
+        vorder = np.arange(len(lens))
+        if as_segments and len(lens) >= 2 and fake_numa:
+            hptr = (pool_h.data_ptr() + src_off) if dirn == 0 else (dst.data_ptr() + dst_off)
+            seg_node = ((np.asarray(hptr, dtype=np.uint64) >> np.uint64(21)) % np.uint64(K)).astype(np.int32)
+            vorder = orc.numa_order(seg_node, bw, path_node).astype(np.int64)
+        if not capture and not dynamic and not fb:   # planned: the executed route is the oracle's, per byte
+            assert mma.get_delivery_log(0) == path.tobytes(), case
+            if as_segments and len(lens) >= 2:
+                assert mma.get_segment_order(0).tolist() == vorder.tolist(), case
         exp = np.full(span, 0xA5, dtype=np.uint8)
-        osegs, on = orc.segments_from_arrays(src_np.ctypes.data + src_off, exp.ctypes.data + dst_off, lens)
+        osegs, on = orc.segments_from_arrays(src_np.ctypes.data + src_off[vorder], exp.ctypes.data + dst_off[vorder],
+                                             lens[vorder])
         assert orc.move(osegs, on, C, bw, path, S=S) == 0
         got = dst.cpu().numpy() if dirn == 0 else dst.numpy()
         assert np.array_equal(got, exp), (case, dict(lb=lb, C=C, S=S, plan=plan_mode, modes=modes, dir=dirn,
