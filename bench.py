@@ -410,6 +410,30 @@ def oracle_sample(k_paths, nsegs_sample=16384, reps=1, min_seconds=0.0):
     return 2 * B / med / 1e9, threads, desc, 2 * B, med
 
 
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
+
+
+def cpu_baseline(k_paths, nsegs_sample=32768, seconds_per_leg=6.0):
+    """the cpu_baseline object: the oracle mover at T = the k-path thread set and at T ~ nproc"""
+    nproc = os.cpu_count() or 1
+    legs = []
+    for kk in dict.fromkeys([k_paths, max(1, (nproc + 1) // 2)]):
+        g, threads, desc, _, _ = oracle_sample(kk, nsegs_sample=nsegs_sample, reps=5, min_seconds=seconds_per_leg)
+        legs.append({"paths": kk, "threads": threads, "gbps": round(g, 3), "sample": desc})
+    head = legs[0]
+    return {"value": head["gbps"], "unit": "GB/s", "cores": head["threads"], "kind": "oracle",
+            "sample": head["sample"], "legs": legs, "nproc": nproc, "cpu_model": cpu_model(),
+            "note": "value/cores = the leg with the bench's own path count; the other leg runs the same oracle "
+                    "with (nproc + 1) // 2 paths so its threads (1 + 2 per relay) fill the host's cores"}
+
+
 def run_reference(args, dist):
     """--impl reference: the oracle as it stands on the host cores (the base contract's
     reference arm for this tier); rank 0 only."""
@@ -1272,12 +1296,13 @@ def main():
         policy.clear(); policy.update(saved[0])
         thresholds.clear(); thresholds.update(saved[1])
 
-    # ---- CPU baseline: the oracle on the host cores, bounded sample, N=1 only
+    # ---- CPU baseline: the oracle on the host cores, bounded sample, N=1 only. Two legs
+    # (SURVEY 8(d) "Oracle timing alongside"): T = the path set's threads (1 + 2 per relay)
+    # and T ~ nproc (a plan over (nproc + 1) // 2 paths), each the median of >= 5 repetitions
     cpu = None
     if not args.quick and dist.world == 1:
         try:
-            g, threads, desc, _, _ = oracle_sample(k, nsegs_sample=32768, min_seconds=10.0)
-            cpu = {"value": round(g, 3), "unit": "GB/s", "cores": threads, "kind": "oracle", "sample": desc}
+            cpu = cpu_baseline(k)
         except Exception as ex:  # noqa: BLE001
             cpu = {"value": None, "unit": "GB/s", "cores": 0, "kind": "oracle", "sample": f"failed: {ex}"}
 

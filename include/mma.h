@@ -207,6 +207,27 @@ int mma_memcpy_h2d_segments(const mma_segment_t* segs, size_t nsegs, int dst_dev
 int mma_memcpy_d2h_segments(const mma_segment_t* segs, size_t nsegs, int src_device,
                             mma_stream_t stream);
 
+/* Concurrent transfers under ONE joint plan (config 5: every GPU reloading
+ * its weights while some also fetch KV): the paper's Path Selector, §3.4.2. Per
+ * direction, one micro-task queue per target GPU (its transfers' chunks, FIFO in array
+ * order); the link that is free first takes its own GPU's next chunk ("direct path first"),
+ * else the next chunk of the longest queue it may relay for; link rates are each GPU's
+ * direct-path rate (mma_set_bandwidth on that GPU, path 0). The plan is mma_plan_multi's.
+ * Each transfer is then enqueued like mma_memcpy_*_segments on its own stream with that
+ * plan: first every transfer's direct part, then every relay part, the relay work on a GPU
+ * waiting for that GPU's own direct work of the batch. Semantics per transfer are
+ * cudaMemcpyAsync's on x.stream. A transfer that is pageable, below the direction's fallback
+ * threshold, or on a capturing stream is copied on its own instead. Every transfer is
+ * validated before anything is enqueued (errors as mma_memcpy_*_segments). */
+typedef struct {
+    int dir;                     /* MMA_H2D or MMA_D2H */
+    int device;                  /* H2D: the destination GPU; D2H: the source GPU */
+    const mma_segment_t* segs;   /* the transfer; one segment = a contiguous copy */
+    size_t nsegs;
+    mma_stream_t stream;
+} mma_transfer_t;
+int mma_memcpy_multi(const mma_transfer_t* xfers, size_t n);
+
 /* Paths of a target GPU for a direction: path 0 = its own PCIe link (direct), then relays
  * in calibration order. Arrays of length cap; *npaths receives the count. */
 int mma_get_paths(int device, mma_dir_t dir, int* gpus, int* kinds, uint32_t* mbps,
@@ -283,6 +304,24 @@ int mma_get_plan(int device, mma_dir_t dir, size_t bytes, uint8_t* path_of_chunk
 int mma_plan_chunks(const uint32_t* mbps, const int* kinds, const uint64_t* backlog, int npaths,
                     uint64_t bytes, uint64_t chunk_bytes, uint64_t thr, int mode,
                     uint8_t* path_of_chunk, size_t cap, size_t* nchunks, int* fallback);
+
+/* The joint planner alone (no GPU, no engine state): the plan of concurrent transfers that
+ * mma_memcpy_multi uses (the paper's Path Selector under constant link rates,
+ * P:549-574 §3.4.2, reading R24 in DESIGN.md). One micro-task queue per endpoint holds the
+ * chunks of every transfer to it, FIFO in array order; the link that is free first (chunks
+ * pulled x chunk_bytes / link_mbps, exact; ties to the lower id) takes its own endpoint's
+ * head ("direct path first"), else the head of the longest queue it may carry
+ * (ties to the lower endpoint id).
+ *   nlinks, link_mbps[nlinks]     link rates (0 = absent); a GPU's own link has its id
+ *   carry[d * nlinks + l]         1 if link l may carry chunks for endpoint d
+ *   target[t], nchunks[t]         transfers
+ *   mode                          MMA plan mode: 0 contiguous (per transfer, own link's range
+ *                                 first, then the other links by id), 1 interleaved (as pulled)
+ *   link_of_chunk                 out: sum(nchunks) link ids, transfer after transfer
+ * cudaErrorInvalidValue: bad arguments, or a transfer no link may carry. */
+int mma_plan_multi(int nlinks, const uint32_t* link_mbps, const uint8_t* carry, int ntransfers,
+                   const int* target, const uint64_t* nchunks, uint64_t chunk_bytes, int mode,
+                   int32_t* link_of_chunk);
 
 /* Debug: the path that delivered each chunk of the most recent multipath copy to/from
  * `device`, as written on the GPU by the final hop (needs cfg.debug_log; synchronises). */

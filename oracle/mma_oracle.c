@@ -113,6 +113,95 @@ int orc_plan(const orc_path* paths, int P, uint64_t B, uint64_t C, uint64_t thr,
     return 0;
 }
 
+/* ------------------------------------ joint plan of concurrent transfers --- */
+
+/* May link l take chunks of endpoint GPU d? Its own GPU's queue always; others by relay_ok. */
+static int may_carry(int L, const uint8_t* relay_ok, int d, int l)
+{
+    return l == d || relay_ok[(size_t)d * L + l];
+}
+
+int orc_plan_multi(int L, const uint32_t* link_bw, const uint8_t* relay_ok, int T,
+                   const int32_t* target, const uint64_t* nchunks, uint64_t C, int mode,
+                   int32_t* link_of_chunk)
+{
+    if (L < 1 || L > 128 || T < 0 || !link_bw || !relay_ok || (T && (!target || !nchunks)) || C == 0)
+        return ORC_EINVAL;
+    if (mode != ORC_INTERLEAVED && mode != ORC_CONTIG) return ORC_EINVAL;
+    uint64_t total = 0;
+    for (int t = 0; t < T; t++) {
+        if (target[t] < 0 || target[t] >= L) return ORC_EINVAL;
+        int any = 0;
+        for (int l = 0; l < L; l++) any |= link_bw[l] > 0 && may_carry(L, relay_ok, target[t], l);
+        if (!any && nchunks[t]) return ORC_EINVAL;
+        total += nchunks[t];
+    }
+    /* the queue of GPU d: transfers to d in order, each transfer's chunks in order */
+    uint64_t* first = calloc((size_t)T + 1, sizeof(uint64_t));   /* transfer t's first out index */
+    uint64_t* left = calloc((size_t)L, sizeof(uint64_t));        /* chunks waiting per queue */
+    int* cur_t = calloc((size_t)L, sizeof(int));                 /* head: transfer, chunk */
+    uint64_t* cur_c = calloc((size_t)L, sizeof(uint64_t));
+    uint64_t* taken = calloc((size_t)L, sizeof(uint64_t));       /* chunks pulled per link */
+    int* live = calloc((size_t)L, sizeof(int));
+    uint64_t* cnt = calloc((size_t)T * L + 1, sizeof(uint64_t)); /* per transfer, per link */
+    if (!first || !left || !cur_t || !cur_c || !taken || !live || !cnt) {
+        free(first); free(left); free(cur_t); free(cur_c); free(taken); free(live); free(cnt);
+        return ORC_EINVAL;
+    }
+    for (int t = 0; t < T; t++) first[t + 1] = first[t] + nchunks[t];
+    for (int d = 0; d < L; d++) {
+        cur_t[d] = -1;
+        for (int t = 0; t < T; t++)
+            if (target[t] == d) {
+                left[d] += nchunks[t];
+                if (cur_t[d] < 0 && nchunks[t]) cur_t[d] = t;
+            }
+    }
+    for (int l = 0; l < L; l++) live[l] = link_bw[l] > 0;
+    for (uint64_t step = 0; step < total; step++) {
+        /* the live link that is free first: taken_l * C / bw_l smallest, ties -> lower id */
+        int best = -1;
+        for (int l = 0; l < L; l++) {
+            if (!live[l]) continue;
+            if (best < 0) { best = l; continue; }
+            u128 a = (u128)taken[l] * C * link_bw[best], b = (u128)taken[best] * C * link_bw[l];
+            if (a < b) best = l;
+        }
+        if (best < 0) break;
+        /* what it takes: its own queue first, else the longest queue it may relay for */
+        int q = -1;
+        if (left[best] > 0) q = best;
+        else
+            for (int d = 0; d < L; d++)
+                if (d != best && left[d] > 0 && may_carry(L, relay_ok, d, best) && (q < 0 || left[d] > left[q])) q = d;
+        if (q < 0) { live[best] = 0; step--; continue; }   /* nothing to take, ever again */
+        int t = cur_t[q];
+        uint64_t c = cur_c[q];
+        link_of_chunk[first[t] + c] = best;
+        cnt[(size_t)t * L + best]++;
+        taken[best]++;
+        left[q]--;
+        if (++cur_c[q] == nchunks[t]) {                      /* next transfer of this queue */
+            cur_c[q] = 0;
+            int nt = -1;
+            for (int u = t + 1; u < T; u++)
+                if (target[u] == q && nchunks[u]) { nt = u; break; }
+            cur_t[q] = nt;
+        }
+    }
+    if (mode == ORC_CONTIG)                                  /* own link first, then by id */
+        for (int t = 0; t < T; t++) {
+            uint64_t i = first[t];
+            int d = target[t];
+            for (uint64_t c = 0; c < cnt[(size_t)t * L + d]; c++) link_of_chunk[i++] = d;
+            for (int l = 0; l < L; l++)
+                if (l != d)
+                    for (uint64_t c = 0; c < cnt[(size_t)t * L + l]; c++) link_of_chunk[i++] = l;
+        }
+    free(first); free(left); free(cur_t); free(cur_c); free(taken); free(live); free(cnt);
+    return 0;
+}
+
 void orc_predict(const orc_path* paths, int P, uint64_t B, uint64_t C,
                  const uint8_t* path_of_chunk, uint64_t n, double* T_s, double* agg_gbps)
 {

@@ -120,6 +120,32 @@ int orc_move(const orc_segment* segs, uint64_t nsegs, uint64_t C,
              uint32_t* write_count, int fault);
 
 /*
+ * Joint plan of concurrent transfers: the paper's Path Selector under
+ * constant link rates (§3.4.2). One micro-task queue per endpoint GPU holds the
+ * chunks of every transfer to that GPU, FIFO in transfer order; every link
+ * has an outstanding queue that pulls. The link that becomes free first -- free time =
+ * chunks taken x C / link_bw, compared exactly; ties -> lower link id -- takes
+ *   the head of its own GPU's queue when that is non-empty ("the Outstanding queue
+ *   corresponding to each GPU always has priority in fetching transfer tasks from the
+ *   associated Mico-task Queue"), else
+ *   the head of the longest queue it may relay for ("prioritizing tasks from the longest
+ *   micro-task queue"; ties -> lower GPU id),
+ * and a link with nothing it may take drops out (queues only shrink).
+ *   L                  links (ids 0..L-1; a GPU's own link has the GPU's id), L <= 128
+ *   link_bw[l]         MB/s; 0 = absent
+ *   relay_ok[d*L + l]  1 if link l may carry chunks for endpoint GPU d (d's own link always may)
+ *   T, target[t], nchunks[t]   the transfers (target[t] < L)
+ *   mode  ORC_INTERLEAVED: chunks numbered in FIFO order as pulled; ORC_CONTIG: per
+ *         transfer, the same per-link counts laid out as contiguous ranges, the target's own
+ *         link first, then the other links by id (reading R1's contiguous form)
+ *   link_of_chunk      out: sum(nchunks) entries, transfer after transfer
+ * Returns 0 or ORC_EINVAL (a transfer no link may carry, bad arguments).
+ */
+int orc_plan_multi(int L, const uint32_t* link_bw, const uint8_t* relay_ok, int T,
+                   const int32_t* target, const uint64_t* nchunks, uint64_t C, int mode,
+                   int32_t* link_of_chunk);
+
+/*
  * NUMA-affine order of a scattered transfer's segments (reading R23): the
  * paper's bandwidth saturates at six GPUs because "typically four GPUs reside within a
  * single NUMA node, while cross-NUMA H2D transfers rely on the UPI link" (§5.1.1),

@@ -378,6 +378,8 @@ int mma_finalize(void)
             }
         cudaEventDestroy(r.fork);
         cudaEventDestroy(r.cap_fork);
+        for (auto& gd : r.gate_ev)
+            for (cudaEvent_t ev : gd) cudaEventDestroy(ev);
         cudaEventDestroy(r.cap_ev);
         cudaStreamDestroy(r.setup);
         r = DevRes();
@@ -438,6 +440,43 @@ int mma_memcpy_h2d_segments(const mma_segment_t* segs, size_t nsegs, int dst_dev
 int mma_memcpy_d2h_segments(const mma_segment_t* segs, size_t nsegs, int src_device, mma_stream_t stream)
 {
     return copy_segments(MMA_D2H, segs, nsegs, src_device, (cudaStream_t)stream);
+}
+
+int mma_memcpy_multi(const mma_transfer_t* xf, size_t n)
+{
+    CK((cudaError_t)ensure_init());
+    if (int se = sticky()) return se;
+    if (n == 0) return cudaSuccess;
+    if (!xf) return cudaErrorInvalidValue;
+    Engine& e = E();
+    std::vector<Job> jobs;
+    jobs.reserve(n);
+    std::vector<size_t> single;   // copied on their own: native (pageable, small) or capturing
+    for (size_t k = 0; k < n; k++) {   // validate everything before anything is enqueued
+        const mma_transfer_t& x = xf[k];
+        if (x.dir != MMA_H2D && x.dir != MMA_D2H) return cudaErrorInvalidValue;
+        if (x.device < 0 || x.device >= e.ndev) return cudaErrorInvalidDevice;
+        if (x.nsegs && !x.segs) return cudaErrorInvalidValue;
+        if (!x.nsegs) continue;
+        cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+        if (cudaStreamIsCapturing((cudaStream_t)x.stream, &cap) != cudaSuccess) cudaGetLastError();
+        Job j;
+        CK(prepare_segments(x.dir, x.segs, x.nsegs, x.device, (cudaStream_t)x.stream, j));
+        if (j.B == 0) continue;
+        if (cap != cudaStreamCaptureStatusNone || j.pageable || j.B < e.cfg.fallback_bytes[x.dir]) {
+            single.push_back(k);
+            continue;
+        }
+        jobs.push_back(std::move(j));
+    }
+    for (size_t k : single) {   // the ordinary single-transfer path (it takes the engine lock)
+        const mma_transfer_t& x = xf[k];
+        CK(copy_segments(x.dir, x.segs, x.nsegs, x.device, (cudaStream_t)x.stream));
+    }
+    if (jobs.empty()) return cudaSuccess;
+    std::lock_guard<std::mutex> g(e.mu);
+    for (Job& j : jobs) CK((cudaError_t)make_device(j.d));
+    return run_multi(jobs);
 }
 
 int mma_get_paths(int device, mma_dir_t dir, int* gpus, int* kinds, uint32_t* mbps, int* modes,
@@ -596,6 +635,28 @@ int mma_plan_chunks(const uint32_t* mbps, const int* kinds, const uint64_t* back
         if (cap < plan.n) return cudaErrorInvalidValue;
         memcpy(path_of_chunk, plan.path.data(), plan.n);
     }
+    return cudaSuccess;
+}
+
+int mma_plan_multi(int nlinks, const uint32_t* link_mbps, const uint8_t* carry, int ntransfers,
+                   const int* target, const uint64_t* nchunks, uint64_t chunk_bytes, int mode,
+                   int32_t* link_of_chunk)
+{
+    if (nlinks < 1 || nlinks > 128 || ntransfers < 0 || !link_mbps || !carry ||
+        (ntransfers && (!target || !nchunks || !link_of_chunk)))
+        return cudaErrorInvalidValue;
+    std::vector<MultiLink> links(nlinks);
+    std::vector<std::vector<uint8_t>> ok(nlinks, std::vector<uint8_t>(nlinks));
+    for (int l = 0; l < nlinks; l++) links[l].mbps = link_mbps[l];
+    for (int d = 0; d < nlinks; d++)
+        for (int l = 0; l < nlinks; l++) ok[d][l] = carry[(size_t)d * nlinks + l];
+    std::vector<int> tg(target, target + ntransfers);
+    std::vector<uint64_t> nc(nchunks, nchunks + ntransfers);
+    std::vector<std::vector<int>> out;
+    if (make_plan_multi(links, ok, tg, nc, chunk_bytes, mode, out)) return cudaErrorInvalidValue;
+    size_t i = 0;
+    for (const auto& v : out)
+        for (int l : v) link_of_chunk[i++] = l;
     return cudaSuccess;
 }
 

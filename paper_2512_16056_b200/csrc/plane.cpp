@@ -22,6 +22,8 @@
 // memory operations); the relay kernel polls seq and releases credit on the GPU.
 #include <nvtx3/nvToolsExt.h>   // header-only: ranges are free unless a tool (nsys) attaches
 
+#include <memory>
+
 #include "plane.h"
 
 namespace mma {
@@ -171,6 +173,24 @@ uint64_t zc_grid(int d)
 
 static cudaEvent_t join_event(cudaStream_t s, int dev);
 
+// test hook (MMA_DENY_PEER="a,b;c,d"): cudaDeviceEnablePeerAccess is taken to fail for these
+// ordered pairs, so the refused-peer branch below runs on a box where every pair works
+static bool peer_denied(int a, int b)
+{
+    const char* s = getenv("MMA_DENY_PEER");
+    if (!s) return false;
+    for (const char* q = s; *q;) {
+        char* end;
+        const long x = strtol(q, &end, 10);
+        if (end == q || *end != ',') break;
+        const long y = strtol(end + 1, &end, 10);
+        if (x == a && y == b) return true;
+        while (*end && *end != ';') end++;
+        q = *end ? end + 1 : end;
+    }
+    return false;
+}
+
 // Streams, peer access and flags for device d (lazily, once).
 int make_device(int d)
 {
@@ -199,6 +219,8 @@ int make_device(int d)
     CK(cudaEventCreateWithFlags(&r.fork, cudaEventDisableTiming));
     CK(cudaEventCreateWithFlags(&r.cap_fork, cudaEventDisableTiming));
     CK(cudaEventCreateWithFlags(&r.cap_ev, cudaEventDisableTiming));
+    for (auto& gd : r.gate_ev)
+        for (cudaEvent_t& ev : gd) CK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
     CK(cudaStreamCreateWithFlags(&r.setup, cudaStreamNonBlocking));
     // join events exist before any call: a captured call may not create one
     for (Lanes* ls : {r.lane, r.cap_lane})
@@ -208,9 +230,9 @@ int make_device(int d)
     CK(cudaDeviceGetAttribute(&r.sms, cudaDevAttrMultiProcessorCount, d));
     for (int p = 0; p < e.ndev; p++) {
         if (p == d || !e.p2p[d][p]) continue;
-        cudaError_t pe = cudaDeviceEnablePeerAccess(p, 0);
+        cudaError_t pe = peer_denied(d, p) ? cudaErrorPeerAccessUnsupported : cudaDeviceEnablePeerAccess(p, 0);
         if (pe == cudaErrorPeerAccessAlreadyEnabled) cudaGetLastError();
-        else if (pe != cudaSuccess) { cudaGetLastError(); e.p2p[d][p] = false; }
+        else if (pe != cudaSuccess) { cudaGetLastError(); e.p2p[d][p] = false; }   // never a path
     }
     r.made = true;
     return cudaSuccess;
@@ -553,9 +575,14 @@ static int ledger_add(int dir, int user_dev, cudaStream_t user, const uint64_t* 
     return cudaSuccess;
 }
 
-// Planner inputs of target d's paths: bandwidth (0 = not usable for this call) and
-// backlog from the ledger.
-void ledger_inputs(int d, int dir, const std::vector<PathState>& ps, std::vector<PlanPath>& pp)
+// Planner inputs of target d's paths: backlog from the ledger (bytes in flight on each
+// link, the link's own target's direct bytes included), so a relay's chunks are planned
+// behind whatever its link still carries. "Direct path first" (§3.4.2): a relay
+// GPU whose own direct work is in flight in this process is returned in `gate`, and the
+// call's relay work on it waits for that work (Call::gate); own direct work of ANOTHER process
+// (cross-process ledger) cannot be waited for, so such a relay is not used (bandwidth 0).
+void ledger_inputs(int d, int dir, const std::vector<PathState>& ps, std::vector<PlanPath>& pp,
+                   std::vector<int>* gate)
 {
     Engine& e = E();
     if (!e.cfg.ledger) return;
@@ -563,13 +590,26 @@ void ledger_inputs(int d, int dir, const std::vector<PathState>& ps, std::vector
     const bool shared = shm_ledger_on();
     for (size_t p = 0; p < ps.size(); p++) {
         const int g = ps[p].gpu;
-        uint64_t bytes = e.ledger[dir][g], own = e.ledger_own[dir][g];
+        const uint64_t local_own = e.ledger_own[dir][g];
+        uint64_t bytes = e.ledger[dir][g], own = local_own;
         if (shared) shm_ledger_get(dir, g, &bytes, &own);   // includes this process's bytes
         pp[p].backlog = bytes;
-        // direct path first: a GPU whose link still carries its own target's bytes takes
-        // no relay work for another target
-        if (ps[p].kind == MMA_PATH_RELAY && g != d && own > 0) pp[p].mbps = 0;
+        if (ps[p].kind != MMA_PATH_RELAY || g == d) continue;
+        if (own > local_own) pp[p].mbps = 0;
+        else if (local_own > 0 && gate && std::find(gate->begin(), gate->end(), g) == gate->end())
+            gate->push_back(g);
     }
+}
+
+int record_gates(int g, int dir)
+{
+    Engine& e = E();
+    DevRes& r = e.dev[g];
+    if (!r.made) return cudaSuccess;
+    DeviceGuard dg(g);
+    CK(cudaEventRecord(r.gate_ev[dir][0], r.lane[dir].direct));
+    CK(cudaEventRecord(r.gate_ev[dir][1], r.lane[dir].zc));
+    return cudaSuccess;
 }
 
 // MMA_TRACE=1: per-call host-time breakdown of the enqueue on stderr.
@@ -614,22 +654,31 @@ public:
 
     int run()
     {
-        t0_ = std::chrono::steady_clock::now();
         struct CaptureFlag {   // no timing / trace events inside a capture
             explicit CaptureFlag(bool on) { tl_capturing = on; }
             ~CaptureFlag() { tl_capturing = false; }
         } cflag(j_.capturing);
-        struct Range {         // one NVTX range per call (SURVEY §5 tracing) around the enqueue
-            explicit Range(const Job& j)
-            {
-                char m[96];
-                snprintf(m, sizeof m, "mma %s %s %.1f MiB -> gpu %d%s", j.dir == MMA_H2D ? "h2d" : "d2h",
-                         j.contiguous ? "contig" : "segments", (double)j.B / (1 << 20), j.d,
-                         j.capturing ? " (captured)" : "");
-                nvtxRangePushA(m);
-            }
-            ~Range() { nvtxRangePop(); }
-        } nvtx(j_);
+        int rc = begin();
+        if (rc != cudaSuccess || done_) return rc;
+        rc = enqueue_side(false);
+        if (rc == cudaSuccess) rc = enqueue_side(true);
+        return end(rc);
+    }
+
+    // ---- the phases run() strings together; run_multi interleaves them across the calls of
+    // one joint plan (every call's direct side, then every call's relay side, gated)
+
+    // plan .. fork .. uploads: everything before a byte moves. done() after it: the call was
+    // completed by a native copy. An error after the fork must still go through end().
+    int begin()
+    {
+        t0_ = std::chrono::steady_clock::now();
+        char m[96];
+        snprintf(m, sizeof m, "mma %s %s %.1f MiB -> gpu %d%s", j_.dir == MMA_H2D ? "h2d" : "d2h",
+                 j_.contiguous ? "contig" : "segments", (double)j_.B / (1 << 20), j_.d,
+                 j_.capturing ? " (captured)" : "");
+        nvtxRangePushA(m);   // one NVTX range per call (SURVEY §5 tracing) around the enqueue
+        nvtx_open_ = true;
         tr_.cap_stream = j_.user;
         tr_.mark("start");
         make_paths(j_.d);
@@ -640,7 +689,7 @@ public:
         if (plan_.fallback) {
             bool done = false;
             CK(native_fallback(&done));
-            if (done) return finish();
+            if (done) { done_ = true; return finish(); }
         }
         CK(prepare());
         const int tb = build_tables();
@@ -648,32 +697,80 @@ public:
             bool done = false;
             thr_ = ~0ull;
             CK(native_fallback(&done));
+            done_ = true;
             return finish();
         }
         CK(tb);
         CK(fork());
+        forked_ = true;
         // after the fork, a failing stage still joins every stream it enqueued on, so the
         // user stream never runs ahead of partial engine work; the error is returned
         int rc = upload_tables();
         if (rc == cudaSuccess) rc = delivery_log();
         if (rc == cudaSuccess) rc = open_timing();
-        if (rc == cudaSuccess) {
-            if (dynamic_) rc = enqueue_dynamic();
-            else {
-                rc = enqueue_paths();
-                if (rc == cudaSuccess) rc = enqueue_rings();
-            }
-        }
+        return rc;
+    }
+
+    bool done() const { return done_; }
+    bool forked() const { return forked_; }
+
+    // the direct side (relay = false: the target's own link, or a dynamic pull launch) or the
+    // relay side (zero-copy relays and relay rings) of the call
+    int enqueue_side(bool relay)
+    {
+        if (dynamic_) return relay ? cudaSuccess : enqueue_dynamic();
+        CK(enqueue_paths(relay));
+        return relay ? enqueue_rings() : cudaSuccess;
+    }
+
+    // relay work that crosses GPU g's PCIe link first waits for `ev` (recorded behind g's own
+    // direct work): "the outstanding queue prioritizes completing direct tasks before
+    // processing micro-tasks from other queues" (§3.4.2)
+    void gate(int g, cudaEvent_t ev)
+    {
+        if (g >= 0 && g < MMA_MAX_GPUS && g != j_.d) gates_[g].push_back(ev);
+    }
+
+    int end(int rc)
+    {
         if (rc != cudaSuccess) {
-            join_streams();
-            if (!j_.capturing) mark_tables_busy();   // partial work may still read the tables
+            if (forked_) {
+                join_streams();
+                if (!j_.capturing) mark_tables_busy();   // partial work may still read the tables
+            }
+            close_range();
             return rc;
         }
-        CK(join());
+        rc = join();
+        close_range();
+        if (rc != cudaSuccess) return rc;
         return finish();
     }
 
+    ~Call() { close_range(); }
+
 private:
+    bool done_ = false, forked_ = false, nvtx_open_ = false;
+    std::vector<cudaEvent_t> gates_[MMA_MAX_GPUS];
+    std::vector<cudaStream_t> gated_;   // streams already made to wait on their GPU's gates
+
+    void close_range()
+    {
+        if (nvtx_open_) nvtxRangePop();
+        nvtx_open_ = false;
+    }
+
+    // a relay stream on GPU g waits for g's gates once per call
+    int apply_gates(cudaStream_t s, int g)
+    {
+        if (g < 0 || g >= MMA_MAX_GPUS || gates_[g].empty()) return cudaSuccess;
+        if (std::find(gated_.begin(), gated_.end(), s) != gated_.end()) return cudaSuccess;
+        gated_.push_back(s);
+        DeviceGuard dg(g);
+        for (cudaEvent_t ev : gates_[g]) CK(cudaStreamWaitEvent(s, ev, 0));
+        return cudaSuccess;
+    }
+
     Job& j_;
     Engine& eng_;
     Target& t_;
@@ -765,11 +862,28 @@ private:
             // staging of their own, enqueue_captured_p2p) replay as they are
             for (int p = 0; p < P_; p++)
                 if (path(p).kind == MMA_PATH_RELAY && resolve_mode(j_, pmode_[p]) == MMA_HOP_CE) pp_[p].mbps = 0;
-        } else if (!j_.bw_override) {
-            ledger_inputs(j_.d, j_.dir, *ps_, pp_);
+        } else if (!j_.bw_override && !j_.plan_override) {
+            std::vector<int> gate;
+            ledger_inputs(j_.d, j_.dir, *ps_, pp_, &gate);
+            for (int g : gate) {   // relays behind their own links' direct work
+                CK(record_gates(g, j_.dir));
+                for (cudaEvent_t ev : eng_.dev[g].gate_ev[j_.dir]) this->gate(g, ev);
+            }
         }
         const int pm = eng_.cfg.plan_mode == PLAN_DYNAMIC ? PLAN_CONTIGUOUS : eng_.cfg.plan_mode;
-        if (make_plan(pp_.data(), P_, j_.B, j_.C, thr_, pm, plan_) != 0) return cudaErrorInvalidValue;
+        if (j_.plan_override) {   // a joint plan (run_multi): the chunk -> path map is given
+            plan_ = Plan();
+            plan_.n = j_.plan_override->size();
+            plan_.path = *j_.plan_override;
+            plan_.count.assign(P_, 0);
+            for (uint8_t p : plan_.path) {
+                if (p >= P_) return cudaErrorInvalidValue;
+                plan_.count[p]++;
+            }
+            if (plan_.n != (j_.B ? (j_.B - 1) / j_.C + 1 : 0)) return cudaErrorInvalidValue;
+        } else if (make_plan(pp_.data(), P_, j_.B, j_.C, thr_, pm, plan_) != 0) {
+            return cudaErrorInvalidValue;
+        }
         t_.stats.calls++;
         t_.stats.bytes += j_.B;
         t_.stats.validate_us += j_.validate_us;
@@ -992,7 +1106,7 @@ private:
         return cudaSuccess;
     }
 
-    bool e_plan_interleaved() const { return eng_.cfg.plan_mode == PLAN_INTERLEAVED; }
+    bool e_plan_interleaved() const { return eng_.cfg.plan_mode == PLAN_INTERLEAVED || j_.interleaved_plan; }
 
     // path p's pieces (the parts of its chunks, chunk by chunk) reordered by host address: a
     // private virtual stream of B_p bytes that the path's zero-copy kernel moves alone. Each
@@ -1151,6 +1265,7 @@ private:
     // delivery log (debug): one byte per chunk (per claim in dynamic pull), 0xff = unwritten
     int delivery_log()
     {
+        if (j_.no_log) return cudaSuccess;   // log_ stays null; the target's log is another call's
         if (!eng_.cfg.debug_log || j_.capturing) {
             t_.log_n = 0;
             return cudaSuccess;
@@ -1240,14 +1355,16 @@ private:
         return cudaSuccess;
     }
 
-    // ---- direct path and zero-copy paths (a4, a7); copy-engine relays are enqueue_rings'
-    int enqueue_paths()
+    // ---- direct path (a4, a7) when relay = false; zero-copy relays (a7) when relay = true;
+    // copy-engine relays are enqueue_rings'
+    int enqueue_paths(bool relay_side)
     {
         for (int p = 0; p < P_; p++) {
             if (lists_[p].empty()) continue;
+            const bool relay = path(p).kind == MMA_PATH_RELAY;
+            if (relay != relay_side) continue;
             const int g = path(p).gpu;
             CK(make_device(g));
-            const bool relay = path(p).kind == MMA_PATH_RELAY;
             const uint64_t bytes_p = path_bytes(p);
             t_.stats.path_bytes[j_.dir][p] += bytes_p;
             t_.stats.path_chunks[j_.dir][p] += lists_[p].size();
@@ -1255,8 +1372,9 @@ private:
             if (j_.timing) j_.timing->bytes[p] = bytes_p;
             if (mode_[p] == MMA_HOP_ZC) CK(enqueue_zero_copy(p, g, relay, bytes_p));
             else if (!relay) CK(enqueue_direct_ce(p, g));
+            // (copy-engine relays: their bytes are counted here, moved by enqueue_rings)
         }
-        tr_.mark("direct+zc");
+        tr_.mark(relay_side ? "zc relays" : "direct");
         return cudaSuccess;
     }
 
@@ -1265,6 +1383,7 @@ private:
     {
         cudaStream_t s = lanes(g).zc;
         CK((cudaError_t)use(s, g));
+        if (relay) CK(apply_gates(s, g));
         CK((cudaError_t)after_upload(s, g));
         ZcLaunchArg a{};
         const bool own = priv_[p].on;
@@ -1531,6 +1650,7 @@ private:
         if (eng_.fault_fail_hop >= 0 && eng_.hops_issued++ == eng_.fault_fail_hop) return cudaErrorUnknown;   // test hook
         cudaStream_t hs = lanes(r->relay).hop[lane];
         CK((cudaError_t)use(hs, r->relay));
+        CK(apply_gates(hs, r->relay));
         DeviceGuard dg(r->relay);
         auto slot_of = [&](size_t c) { return (uint32_t)((gbase + c) % S); };
         // one batched stream memory operation: wait (GEQ) or write each listed flag
@@ -1695,6 +1815,102 @@ int run_job(Job& j)
 {
     Call c(j);
     return c.run();
+}
+
+// Link id of path p of target d in a joint plan: the path GPU's own link, or for a loopback
+// relay (relay GPU == target, one-GPU test mode) a virtual link MMA_MAX_GPUS + its ordinal.
+static int link_of_path(const std::vector<PathState>& ps, int d, size_t p)
+{
+    if (ps[p].kind == MMA_PATH_DIRECT || ps[p].gpu != d) return ps[p].gpu;
+    int k = 0;
+    for (size_t q = 1; q < p; q++) k += ps[q].kind == MMA_PATH_RELAY && ps[q].gpu == d;
+    return MMA_MAX_GPUS + k;
+}
+
+// Enqueue concurrent transfers under one joint plan (engine mutex held): per
+// direction, make_plan_multi over the links of every transfer's path set (a link's rate is
+// its own GPU's direct-path rate; a loopback relay's is its path's), then every call's direct
+// side, then -- behind gates recorded on the direct lanes of every target GPU of the batch --
+// every call's relay side, so a link finishes its own target's work before it relays
+// ("direct path first", §3.4.2), as the joint plan assumed.
+int run_multi(std::vector<Job>& jobs)
+{
+    Engine& e = E();
+    const int L = MMA_MAX_GPUS + 8;
+    std::vector<std::vector<uint8_t>> plans(jobs.size());
+    for (int dir = 0; dir < 2; dir++) {
+        std::vector<MultiLink> links(L, MultiLink{0});
+        std::vector<std::vector<uint8_t>> carry(L, std::vector<uint8_t>(L, 0));
+        std::vector<int> target;
+        std::vector<uint64_t> nchunks;
+        std::vector<size_t> idx;
+        for (size_t t = 0; t < jobs.size(); t++) {
+            if (jobs[t].dir != dir) continue;
+            const int d = jobs[t].d;
+            make_paths(d);
+            const auto& ps = e.tgt[d].paths[dir];
+            for (size_t p = 0; p < ps.size(); p++) {
+                const int l = link_of_path(ps, d, p);
+                if (l >= L || !ps[p].mbps) continue;
+                if (l < MMA_MAX_GPUS) {
+                    make_paths(l);
+                    links[l].mbps = e.tgt[l].paths[dir][0].mbps;
+                } else if (!links[l].mbps) {
+                    links[l].mbps = ps[p].mbps;
+                }
+                carry[d][l] = 1;
+            }
+            target.push_back(d);
+            nchunks.push_back(jobs[t].B ? (jobs[t].B - 1) / jobs[t].C + 1 : 0);
+            idx.push_back(t);
+        }
+        if (idx.empty()) continue;
+        const int mode = e.cfg.plan_mode == PLAN_INTERLEAVED ? PLAN_INTERLEAVED : PLAN_CONTIGUOUS;
+        std::vector<std::vector<int>> lk;
+        if (make_plan_multi(links, carry, target, nchunks, jobs[idx[0]].C, mode, lk)) return cudaErrorInvalidValue;
+        for (size_t k = 0; k < idx.size(); k++) {
+            Job& j = jobs[idx[k]];
+            const auto& ps = e.tgt[j.d].paths[dir];
+            auto& pl = plans[idx[k]];
+            pl.resize(lk[k].size());
+            for (size_t c = 0; c < lk[k].size(); c++) {
+                size_t p = 0;
+                while (p < ps.size() && link_of_path(ps, j.d, p) != lk[k][c]) p++;
+                if (p == ps.size()) return cudaErrorInvalidValue;
+                pl[c] = (uint8_t)p;
+            }
+            j.plan_override = &pl;
+            j.interleaved_plan = mode == PLAN_INTERLEAVED;
+        }
+    }
+    for (size_t t = 0; t < jobs.size(); t++)   // one delivery log per GPU: the last transfer's
+        for (size_t u = t + 1; u < jobs.size(); u++) jobs[t].no_log |= jobs[u].d == jobs[t].d;
+    std::vector<std::unique_ptr<Call>> calls;
+    for (Job& j : jobs) calls.emplace_back(new Call(j));
+    std::vector<int> rc(jobs.size(), cudaSuccess);
+    for (size_t t = 0; t < calls.size(); t++) {
+        rc[t] = calls[t]->begin();
+        if (rc[t] == cudaSuccess && !calls[t]->done()) rc[t] = calls[t]->enqueue_side(false);
+    }
+    for (size_t t = 0; t < jobs.size(); t++)   // every target's own work, per direction
+        if (rc[t] == cudaSuccess && !calls[t]->done()) {
+            const int r = record_gates(jobs[t].d, jobs[t].dir);
+            if (r != cudaSuccess) rc[t] = r;
+        }
+    for (size_t t = 0; t < calls.size(); t++) {
+        if (calls[t]->done()) continue;
+        if (rc[t] == cudaSuccess) {
+            for (size_t u = 0; u < jobs.size(); u++)
+                if (jobs[u].dir == jobs[t].dir)
+                    for (cudaEvent_t ev : e.dev[jobs[u].d].gate_ev[jobs[u].dir]) calls[t]->gate(jobs[u].d, ev);
+            rc[t] = calls[t]->enqueue_side(true);
+        }
+        if (rc[t] != cudaSuccess && !calls[t]->forked()) continue;
+        rc[t] = calls[t]->end(rc[t]);
+    }
+    for (int r : rc)
+        if (r != cudaSuccess) return r;
+    return cudaSuccess;
 }
 
 int sticky()

@@ -81,6 +81,9 @@ struct DevRes {
     Lanes cap_lane[2];
     cudaEvent_t fork = nullptr;      // recorded on a user stream of this device
     cudaEvent_t cap_fork = nullptr;  // idem, captured calls
+    // [dir][0 direct lane, 1 zero-copy lane]: recorded behind this GPU's own direct work when
+    // a relay through this GPU must wait for it (direct path first, plane.cpp Call::gate)
+    cudaEvent_t gate_ev[2][2] = {};
     cudaStream_t setup = nullptr;    // ring initialisation (never waits on user work)
     cudaEvent_t cap_ev = nullptr;    // captured calls: orders the table frees after the join
     int sms = 148;
@@ -252,6 +255,9 @@ struct Job {
     uint64_t ptr_queries = 0;
     const uint32_t* bw_override = nullptr;   // measurement runs: per-path bandwidth
     const int* mode_override = nullptr;      // measurement runs: per-path mode
+    const std::vector<uint8_t>* plan_override = nullptr;   // joint plans: path of each chunk
+    bool interleaved_plan = false;           // the given plan is not contiguous per path
+    bool no_log = false;                     // joint plans: another transfer to this GPU keeps the log
     bool no_small_fallback = false;          // measurement runs: ignore the threshold
     PathTiming* timing = nullptr;            // measurement runs: per-path events (planned plans only)
     bool capturing = false;                  // the user stream is being captured into a graph
@@ -347,7 +353,12 @@ int ensure_init();
 void make_paths(int d);
 void free_ring(Ring& r);
 int get_ring(int d, int dir, int p, uint64_t C, uint32_t S, Ring** out);
-void ledger_inputs(int d, int dir, const std::vector<PathState>& ps, std::vector<PlanPath>& pp);
+// gate (optional): GPUs whose own direct work is in flight in this process; a relay through
+// one of them is planned behind that backlog and waits for it (direct path first)
+void ledger_inputs(int d, int dir, const std::vector<PathState>& ps, std::vector<PlanPath>& pp,
+                   std::vector<int>* gate = nullptr);
+// record gate_ev of GPU g for direction dir behind its direct and zero-copy lanes
+int record_gates(int g, int dir);
 void ledger_retire();
 // ---- ledger_shm.cpp: the cross-process ledger (mma_ledger_attach)
 bool shm_ledger_on();
@@ -356,6 +367,7 @@ void shm_ledger_get(int dir, int dev, uint64_t* bytes, uint64_t* own);
 int shm_ledger_slot(int dev);   // -1 when detached; resolves the bus id (a CUDA call)
 void shm_ledger_add_slot(int dir, int slot, int64_t bytes, int64_t own);   // no CUDA calls
 int run_job(Job& j);
+int run_multi(std::vector<Job>& jobs);   // a joint plan of concurrent transfers (NEXT-1)
 int reserve_tables(const Job& j);
 int sticky();
 extern bool g_ktime;

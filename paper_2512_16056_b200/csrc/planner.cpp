@@ -85,4 +85,76 @@ int make_plan(const PlanPath* paths, int npaths, uint64_t B, uint64_t C, uint64_
     return 0;
 }
 
+// ---- joint plan (NEXT-1). Links wait in a heap keyed by the time they become free (chunks
+// pulled x C / rate, compared exactly); each endpoint's queue is a FIFO cursor over its
+// transfers. Queue lengths are few (<= the link count), so the longest is found by a scan.
+int make_plan_multi(const std::vector<MultiLink>& links, const std::vector<std::vector<uint8_t>>& carry,
+                    const std::vector<int>& target, const std::vector<uint64_t>& nchunks, uint64_t C, int mode,
+                    std::vector<std::vector<int>>& link_of_chunk)
+{
+    const int L = (int)links.size(), T = (int)target.size();
+    if (L < 1 || L > 128 || C == 0 || (int)nchunks.size() != T || (int)carry.size() != L) return -22;
+    if (mode != PLAN_CONTIGUOUS && mode != PLAN_INTERLEAVED) return -22;
+    auto may = [&](int d, int l) { return l == d || carry[d][l] != 0; };
+    struct Queue {
+        uint64_t left = 0;
+        std::vector<int> transfers;   // to this endpoint, in call order
+        size_t ti = 0;                // current transfer (index into transfers)
+        uint64_t next = 0;            // next chunk of it
+    };
+    std::vector<Queue> q(L);
+    link_of_chunk.assign(T, {});
+    for (int t = 0; t < T; t++) {
+        if (target[t] < 0 || target[t] >= L) return -22;
+        link_of_chunk[t].assign(nchunks[t], -1);
+        if (!nchunks[t]) continue;
+        bool any = false;
+        for (int l = 0; l < L && !any; l++) any = links[l].mbps && may(target[t], l);
+        if (!any) return -22;
+        q[target[t]].left += nchunks[t];
+        q[target[t]].transfers.push_back(t);
+    }
+    std::vector<Key> heap;   // num = chunks pulled * C, den = rate, idx = link
+    for (int l = 0; l < L; l++)
+        if (links[l].mbps) heap.push_back(Key{0, links[l].mbps, l});
+    std::make_heap(heap.begin(), heap.end(), HeapCmp());
+    std::vector<std::vector<uint64_t>> cnt(T, std::vector<uint64_t>(L, 0));
+    uint64_t remaining = 0;
+    for (const Queue& x : q) remaining += x.left;
+    while (remaining && !heap.empty()) {
+        std::pop_heap(heap.begin(), heap.end(), HeapCmp());
+        Key k = heap.back();
+        heap.pop_back();
+        const int l = k.idx;
+        int d = -1;
+        if (q[l].left) d = l;   // direct path first
+        else
+            for (int e = 0; e < L; e++)   // longest queue it may relay for; ties: lower id
+                if (e != l && q[e].left && may(e, l) && (d < 0 || q[e].left > q[d].left)) d = e;
+        if (d < 0) continue;   // nothing this link may take, now or later: it leaves the heap
+        Queue& Q = q[d];
+        while (Q.next >= nchunks[Q.transfers[Q.ti]]) { Q.ti++; Q.next = 0; }
+        const int t = Q.transfers[Q.ti];
+        link_of_chunk[t][Q.next++] = l;
+        cnt[t][l]++;
+        Q.left--;
+        remaining--;
+        k.num += C;
+        heap.push_back(k);
+        std::push_heap(heap.begin(), heap.end(), HeapCmp());
+    }
+    if (remaining) return -22;
+    if (mode == PLAN_CONTIGUOUS)
+        for (int t = 0; t < T; t++) {
+            auto& v = link_of_chunk[t];
+            size_t i = 0;
+            const int d = target[t];
+            for (uint64_t c = 0; c < cnt[t][d]; c++) v[i++] = d;
+            for (int l = 0; l < L; l++)
+                if (l != d)
+                    for (uint64_t c = 0; c < cnt[t][l]; c++) v[i++] = l;
+        }
+    return 0;
+}
+
 }  // namespace mma

@@ -27,4 +27,18 @@ struct Plan {
 int make_plan(const PlanPath* paths, int npaths, uint64_t B, uint64_t C, uint64_t thr,
               int mode, Plan& out);
 
+// Joint plan of concurrent transfers (the paper's Path Selector under constant
+// link rates, §3.4.2): one micro-task queue per endpoint, FIFO over the transfers
+// to it; the link free first pulls its own endpoint's queue head ("direct path first",
+// P:564-565), else the head of the longest queue it may relay for (ties to the lower
+// id). links: rate per link id (0 = absent); carry(d, l): may link l carry chunks of endpoint d
+// (its own queue always). Output: for each transfer, the link id of each chunk; contiguous
+// mode lays each transfer's per-link counts out as ranges, own link first, then by link id.
+struct MultiLink {
+    uint32_t mbps;
+};
+int make_plan_multi(const std::vector<MultiLink>& links, const std::vector<std::vector<uint8_t>>& carry,
+                    const std::vector<int>& target, const std::vector<uint64_t>& nchunks, uint64_t C, int mode,
+                    std::vector<std::vector<int>>& link_of_chunk);
+
 }  // namespace mma

@@ -24,7 +24,7 @@ SYMBOLS = [
     "mma_default_config", "mma_init", "mma_finalize", "mma_memcpy_h2d", "mma_memcpy_d2h",
     "mma_memcpy_h2d_segments", "mma_memcpy_d2h_segments", "mma_get_paths", "mma_set_bandwidth",
     "mma_set_path_modes", "mma_calibrate", "mma_get_plan", "mma_plan_chunks",
-    "mma_get_delivery_log", "mma_get_segment_order", "mma_host_alloc", "mma_host_free", "mma_get_stats",
+    "mma_get_delivery_log", "mma_get_segment_order", "mma_plan_multi", "mma_memcpy_multi", "mma_host_alloc", "mma_host_free", "mma_get_stats",
     "mma_reset_stats", "mma_get_last_error", "mma_error_string", "mma_fill_pattern",
     "mma_verify_pattern", "mma_verify_segments", "mma_set_kernel_timing", "mma_kernel_times",
     "mma_tune_segments", "mma_get_segment_tuning", "mma_get_dynamic_counts", "mma_set_plan_mode",
@@ -85,6 +85,11 @@ class Segment(C.Structure):
     _fields_ = [("src", C.c_void_p), ("dst", C.c_void_p), ("bytes", C.c_size_t)]
 
 
+class Transfer(C.Structure):
+    _fields_ = [("dir", C.c_int), ("device", C.c_int), ("segs", C.POINTER(Segment)), ("nsegs", C.c_size_t),
+                ("stream", C.c_void_p)]
+
+
 class MMAError(RuntimeError):
     def __init__(self, code: int, what: str):
         super().__init__(f"{what}: {lib().mma_error_string(code).decode()} ({code})")
@@ -117,6 +122,8 @@ def lib():
                                       C.c_int, vp, sz, C.POINTER(sz), C.POINTER(C.c_int)]
         L.mma_get_delivery_log.argtypes = [C.c_int, vp, sz, C.POINTER(sz)]
         L.mma_get_segment_order.argtypes = [C.c_int, vp, sz, C.POINTER(sz)]
+        L.mma_memcpy_multi.argtypes = [C.POINTER(Transfer), sz]
+        L.mma_plan_multi.argtypes = [C.c_int, vp, vp, C.c_int, vp, vp, C.c_uint64, C.c_int, vp]
         L.mma_host_alloc.argtypes = [C.POINTER(vp), sz, C.c_uint]
         L.mma_host_free.argtypes = [vp]
         L.mma_get_stats.argtypes = [C.c_int, C.POINTER(Stats)]
@@ -243,6 +250,20 @@ def memcpy_h2d_segments(segs, nsegs: int, dst_device: int, stream=None) -> None:
 def memcpy_d2h_segments(segs, nsegs: int, src_device: int, stream=None) -> None:
     _check(lib().mma_memcpy_d2h_segments(segs, nsegs, src_device, _stream(stream, src_device)),
            "mma_memcpy_d2h_segments")
+
+
+def memcpy_multi(transfers) -> None:
+    """Concurrent transfers under one joint plan (mma_memcpy_multi). `transfers`: sequence of
+    (direction, device, (segs, nsegs) from make_segments, stream or None)."""
+    arr = (Transfer * max(1, len(transfers)))()
+    keep = []
+    for i, (d, dev, (segs, n), stream) in enumerate(transfers):
+        keep.append(segs)
+        arr[i].dir, arr[i].device = d, dev
+        arr[i].segs = C.cast(segs, C.POINTER(Segment))
+        arr[i].nsegs = n
+        arr[i].stream = _stream(stream, dev)
+    _check(lib().mma_memcpy_multi(arr, len(transfers)), "mma_memcpy_multi")
 
 
 def get_paths(device: int, direction: int):
@@ -390,6 +411,21 @@ def get_delivery_log(device: int):
     buf = (C.c_uint8 * max(n.value, 1))()
     _check(lib().mma_get_delivery_log(device, buf, n.value, C.byref(n)), "mma_get_delivery_log")
     return bytes(buf[: n.value])
+
+
+def plan_multi(link_mbps, carry, targets, nchunks, chunk: int, mode: int = 0):
+    """The joint planner alone (mma_plan_multi): per transfer, the link id of each chunk."""
+    import numpy as np
+    L = len(link_mbps)
+    bw = np.ascontiguousarray(link_mbps, dtype=np.uint32)
+    ok = np.ascontiguousarray(carry, dtype=np.uint8).reshape(L, L)
+    tg = np.ascontiguousarray(targets, dtype=np.int32)
+    nc = np.ascontiguousarray(nchunks, dtype=np.uint64)
+    out = np.full(max(1, int(nc.sum())), -1, dtype=np.int32)
+    rc = lib().mma_plan_multi(L, bw.ctypes.data, ok.ctypes.data, len(tg), tg.ctypes.data, nc.ctypes.data, chunk,
+                              mode, out.ctypes.data)
+    offs = np.concatenate([[0], np.cumsum(nc)]).astype(np.int64)
+    return rc, [out[offs[t]:offs[t + 1]].copy() for t in range(len(tg))]
 
 
 def get_segment_order(device: int):

@@ -107,3 +107,27 @@ def test_header_is_plain_c(tmp_path):
     r = subprocess.run([gcc, "-std=c11", "-Wall", "-Wextra", "-pedantic", "-Werror", "-I", str(ROOT / "include"),
                         "-c", str(src), "-o", str(tmp_path / "t.o")], capture_output=True, text=True)
     assert r.returncode == 0, r.stderr
+
+
+@pytest.mark.parametrize("mode", [0, 1], ids=["contiguous", "interleaved"])
+def test_multi_planner_parity_random(orc, mode):
+    """the engine's joint planner (mma_plan_multi, heap-based) vs the oracle's
+    orc_plan_multi (linear scans), bit for bit on random link sets, carry matrices and
+    transfer lists (NEXT-1)"""
+    rng = np.random.default_rng(77 + mode)
+    for case in range(3000):
+        L = int(rng.integers(1, 10))
+        bw = [int(x) for x in rng.integers(0, 60001, L)]
+        if rng.random() < 0.4:
+            bw = [int(x) for x in rng.choice([0, 1, 2, 3, 55000], L)]
+        ok = (rng.random((L, L)) < rng.random()).astype(np.uint8)
+        T = int(rng.integers(0, 7))
+        targets = [int(x) for x in rng.integers(0, L, T)]
+        nch = [int(x) for x in rng.integers(0, 300, T)]
+        C = int(rng.choice([4096, 1 << 20, 8 << 20]))
+        orc_rc, orc_plans = orc.plan_multi(bw, ok, targets, nch, C, mode)
+        rc, plans = mma.plan_multi(bw, ok, targets, nch, C, mode)
+        assert (rc == 0) == (orc_rc == 0), (case, bw, ok.tolist(), targets, nch)
+        if rc == 0:
+            for a, b in zip(plans, orc_plans):
+                assert a.tolist() == b.tolist(), (case, bw, ok.tolist(), targets, nch)
