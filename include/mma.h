@@ -341,6 +341,10 @@ int mma_get_dynamic_counts(int device, uint64_t* chunks, int cap, int* npaths);
 /* Pinned, mapped, portable host memory, NUMA-placed per cfg.numa_mode (C8). */
 int mma_host_alloc(void** ptr, size_t bytes, unsigned flags);
 int mma_host_free(void* ptr);
+/* Whether ptr is the base of a live mma_host_alloc buffer (C8): cudaSuccess and its mapped
+ * length (a 2 MiB multiple) in *bytes, else cudaErrorInvalidValue. The LD_PRELOAD shim uses
+ * it to route cudaFreeHost of buffers it allocated through the engine. */
+int mma_host_alloc_size(const void* ptr, size_t* bytes);
 
 /* NUMA "spread" placement (C8): a buffer for a contiguous transfer of `bytes`
  * to / from `device` whose byte range carried by each path of the current contiguous plan

@@ -701,6 +701,8 @@ int mma_host_alloc(void** ptr, size_t bytes, unsigned flags)
 
 int mma_host_free(void* ptr) { return host_free(ptr); }
 
+int mma_host_alloc_size(const void* ptr, size_t* bytes) { return host_alloc_size(ptr, bytes); }
+
 int mma_host_alloc_for(void** ptr, size_t bytes, int device, mma_dir_t dir)
 {
     CK((cudaError_t)ensure_init());

@@ -27,6 +27,7 @@ cudaError_t launch_verify_segments(const uint64_t* dst, const uint64_t* off, con
 // hostmem.cpp
 int host_alloc(void** ptr, size_t bytes, int numa_mode, int node0);
 int host_free(void* ptr);
+int host_alloc_size(const void* ptr, size_t* bytes);   // cudaErrorInvalidValue: not a host_alloc base
 int host_alloc_ranges(void** ptr, size_t bytes, const uint64_t* range_end, const int* node, int nranges);
 int host_page_node(const void* p);
 // NUMA node of each host address (2 MiB regions cached; MMA_FAKE_HOST_NODES=K (tests): node =

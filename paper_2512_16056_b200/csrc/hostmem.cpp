@@ -30,6 +30,12 @@ namespace mma {
 namespace {
 std::mutex g_mu;
 std::map<void*, size_t> g_allocs;   // base -> mapped length
+std::map<void*, bool> g_interleaved;   // bases placed page by page (numa_mode 2): never cached
+
+// host_nodes' cache: 2 MiB region -> node. Pinned pages do not move, but a freed range can be
+// mapped again on another node, so host_free drops its regions.
+std::mutex g_node_mu;
+std::unordered_map<uintptr_t, int> g_node_cache;
 
 constexpr int kMpolBind = 2;
 constexpr int kMpolInterleave = 3;
@@ -84,6 +90,7 @@ int host_alloc(void** ptr, size_t bytes, int numa_mode, int node0)
     }
     std::lock_guard<std::mutex> g(g_mu);
     g_allocs[p] = len;
+    if (numa_mode == 2 && nodes > 1) g_interleaved[p] = true;
     *ptr = p;
     return cudaSuccess;
 }
@@ -124,6 +131,15 @@ int host_alloc_ranges(void** ptr, size_t bytes, const uint64_t* range_end, const
     return cudaSuccess;
 }
 
+int host_alloc_size(const void* ptr, size_t* bytes)
+{
+    std::lock_guard<std::mutex> g(g_mu);
+    auto it = g_allocs.find(const_cast<void*>(ptr));
+    if (it == g_allocs.end()) return cudaErrorInvalidValue;
+    if (bytes) *bytes = it->second;
+    return cudaSuccess;
+}
+
 int host_free(void* ptr)
 {
     if (!ptr) return cudaSuccess;
@@ -134,6 +150,12 @@ int host_free(void* ptr)
         if (it == g_allocs.end()) return cudaErrorInvalidValue;
         len = it->second;
         g_allocs.erase(it);
+        g_interleaved.erase(ptr);
+    }
+    {
+        std::lock_guard<std::mutex> g(g_node_mu);
+        const uintptr_t a = reinterpret_cast<uintptr_t>(ptr) >> 21, b = (reinterpret_cast<uintptr_t>(ptr) + len - 1) >> 21;
+        for (uintptr_t r = a; r <= b; r++) g_node_cache.erase(r);
     }
     cudaError_t e = cudaHostUnregister(ptr);
     munmap(ptr, len);
@@ -162,14 +184,25 @@ void host_nodes(const void* const* p, size_t n, int* nodes)
         for (size_t i = 0; i < n; i++) nodes[i] = 0;
         return;
     }
-    static std::mutex mu;
-    static std::unordered_map<uintptr_t, int> cache;   // 2 MiB region -> node (pinned pages stay)
-    std::lock_guard<std::mutex> g(mu);
+    // regions inside page-interleaved allocations are asked page by page, never cached
+    std::vector<char> nocache(n, 0);
+    {
+        std::lock_guard<std::mutex> g(g_mu);
+        if (!g_interleaved.empty())
+            for (size_t i = 0; i < n; i++) {
+                auto it = g_allocs.upper_bound(const_cast<void*>(p[i]));
+                if (it == g_allocs.begin()) continue;
+                --it;
+                if ((const char*)p[i] < (const char*)it->first + it->second && g_interleaved.count(it->first)) nocache[i] = 1;
+            }
+    }
+    std::unordered_map<uintptr_t, int>& cache = g_node_cache;
+    std::lock_guard<std::mutex> g(g_node_mu);
     std::vector<void*> ask;
     std::vector<size_t> who;
     for (size_t i = 0; i < n; i++) {
         const uintptr_t r = reinterpret_cast<uintptr_t>(p[i]) >> 21;
-        auto it = cache.find(r);
+        auto it = nocache[i] ? cache.end() : cache.find(r);
         if (it != cache.end()) nodes[i] = it->second;
         else { nodes[i] = -2; ask.push_back(const_cast<void*>(p[i])); who.push_back(i); }
     }
@@ -179,7 +212,7 @@ void host_nodes(const void* const* p, size_t n, int* nodes)
             std::fill(st.begin(), st.end(), -1);
         for (size_t q = 0; q < ask.size(); q++) {
             const int nd = st[q] >= 0 ? st[q] : -1;
-            cache[reinterpret_cast<uintptr_t>(ask[q]) >> 21] = nd;
+            if (!nocache[who[q]]) cache[reinterpret_cast<uintptr_t>(ask[q]) >> 21] = nd;
             nodes[who[q]] = nd;
         }
         for (size_t i = 0; i < n; i++)   // repeats of a region asked in this call

@@ -10,6 +10,12 @@
 // dlsym(RTLD_NEXT). A thread-local guard keeps the engine's own copies native. The shim
 // links no CUDA runtime: every runtime function it needs is looked up with RTLD_NEXT.
 //
+// Pinned allocations: cudaHostAlloc / cudaMallocHost of at least
+// MMA_PRELOAD_ALLOC_MIN_BYTES (default 2 MiB; 0 = off) become mma_host_alloc (C8: NUMA-placed
+// per the engine's numa_mode, page-locked, mapped into every GPU), so a torch pin_memory()
+// buffer is the engine's own and usable by its zero-copy kernels; cudaFreeHost of such a
+// buffer is mma_host_free. Write-combined requests and every failure go to the runtime.
+//
 // It also exports cudaMemcpyBatchAsync (+ _ptsz), the batch API paged KV caches use for
 // block swaps: a batch of at least MMA_PRELOAD_MIN_BYTES whose every entry is pinned host
 // -> device memory of one GPU (or the reverse) becomes one scattered multipath copy
@@ -138,6 +144,30 @@ int engine_batch(void** dsts, void** srcs, const size_t* sizes, size_t count, in
 }
 
 typedef int (*batch_fn)(void**, void**, size_t*, size_t, void*, size_t*, size_t, size_t*, void*);
+typedef int (*host_alloc_fn)(void**, size_t, unsigned);
+typedef int (*malloc_host_fn)(void**, size_t);
+typedef int (*free_host_fn)(void*);
+
+constexpr unsigned kWriteCombined = 0x04;   // cudaHostAllocWriteCombined
+
+size_t alloc_min_bytes()
+{
+    static size_t v = [] {
+        const char* s = getenv("MMA_PRELOAD_ALLOC_MIN_BYTES");
+        return s ? (size_t)strtoull(s, nullptr, 10) : (size_t)(2u << 20);
+    }();
+    return v;
+}
+
+// 0 if the engine allocated it (C8), else nonzero
+int engine_alloc(void** p, size_t n, unsigned flags)
+{
+    if (g_inside || !p || alloc_min_bytes() == 0 || n < alloc_min_bytes() || (flags & kWriteCombined)) return 1;
+    g_inside = 1;
+    const int rc = mma_host_alloc(p, n, 0);
+    g_inside = 0;
+    return rc;
+}
 
 }  // namespace
 
@@ -184,6 +214,28 @@ __attribute__((visibility("default"))) int cudaMemcpyBatchAsync_ptsz(void** dsts
         if (engine_batch(dsts, srcs, sizes, count, k, dev, stream ? stream : (void*)0x2) == 0) return 0;
     }
     return real ? real(dsts, srcs, sizes, count, attrs, attrs_idx, nattrs, fail_idx, stream) : 1;
+}
+
+__attribute__((visibility("default"))) int cudaHostAlloc(void** p, size_t n, unsigned flags)
+{
+    static host_alloc_fn real = next<host_alloc_fn>("cudaHostAlloc");
+    if (engine_alloc(p, n, flags) == 0) return 0;
+    return real(p, n, flags);
+}
+
+__attribute__((visibility("default"))) int cudaMallocHost(void** p, size_t n)
+{
+    static malloc_host_fn real = next<malloc_host_fn>("cudaMallocHost");
+    if (engine_alloc(p, n, 0) == 0) return 0;
+    return real(p, n);
+}
+
+__attribute__((visibility("default"))) int cudaFreeHost(void* p)
+{
+    static free_host_fn real = next<free_host_fn>("cudaFreeHost");
+    size_t n = 0;
+    if (p && mma_host_alloc_size(p, &n) == 0) return mma_host_free(p);   // the engine's (C8)
+    return real(p);
 }
 
 __attribute__((visibility("default"))) int cudaMemcpy(void* dst, const void* src, size_t n, int kind)

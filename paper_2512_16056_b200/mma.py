@@ -24,7 +24,8 @@ SYMBOLS = [
     "mma_default_config", "mma_init", "mma_finalize", "mma_memcpy_h2d", "mma_memcpy_d2h",
     "mma_memcpy_h2d_segments", "mma_memcpy_d2h_segments", "mma_get_paths", "mma_set_bandwidth",
     "mma_set_path_modes", "mma_calibrate", "mma_get_plan", "mma_plan_chunks",
-    "mma_get_delivery_log", "mma_get_segment_order", "mma_plan_multi", "mma_memcpy_multi", "mma_host_alloc", "mma_host_free", "mma_get_stats",
+    "mma_get_delivery_log", "mma_get_segment_order", "mma_plan_multi", "mma_memcpy_multi",
+    "mma_host_alloc_size", "mma_host_alloc", "mma_host_free", "mma_get_stats",
     "mma_reset_stats", "mma_get_last_error", "mma_error_string", "mma_fill_pattern",
     "mma_verify_pattern", "mma_verify_segments", "mma_set_kernel_timing", "mma_kernel_times",
     "mma_tune_segments", "mma_get_segment_tuning", "mma_get_dynamic_counts", "mma_set_plan_mode",
@@ -123,6 +124,7 @@ def lib():
         L.mma_get_delivery_log.argtypes = [C.c_int, vp, sz, C.POINTER(sz)]
         L.mma_get_segment_order.argtypes = [C.c_int, vp, sz, C.POINTER(sz)]
         L.mma_memcpy_multi.argtypes = [C.POINTER(Transfer), sz]
+        L.mma_host_alloc_size.argtypes = [vp, C.POINTER(sz)]
         L.mma_plan_multi.argtypes = [C.c_int, vp, vp, C.c_int, vp, vp, C.c_uint64, C.c_int, vp]
         L.mma_host_alloc.argtypes = [C.POINTER(vp), sz, C.c_uint]
         L.mma_host_free.argtypes = [vp]
@@ -597,6 +599,12 @@ def host_alloc_for(nbytes: int, device: int, direction: int) -> int:
     p = C.c_void_p()
     _check(lib().mma_host_alloc_for(C.byref(p), nbytes, device, direction), "mma_host_alloc_for")
     return int(p.value or 0)
+
+
+def host_alloc_size(ptr: int):
+    """Mapped length of an mma_host_alloc buffer based at ptr, or None if it is not one."""
+    n = C.c_size_t()
+    return int(n.value) if lib().mma_host_alloc_size(ptr, C.byref(n)) == 0 else None
 
 
 def host_page_node(ptr: int) -> int:
