@@ -380,6 +380,13 @@ int mma_kernel_times(float* ms, int* kinds, size_t cap, size_t* n);
  *  - mma_copy_share_segments moves the chunks i of the table with path_of_chunk[i] == path
  *    (a plan from mma_plan_chunks for the same bytes and chunk size) with a zero-copy kernel
  *    on `device`; pointers must be valid in this process. Direction follows the pointers.
+ *  - mma_copy_share_segments_ring moves the same share through this process's own
+ *    copy-engine relay ring on `device` (`slots` slots of chunk_bytes in its HBM, the dual
+ *    relay pipeline of P:588-590): per chunk, hop 1 into a slot -- host -> this GPU (H2D) or
+ *    the source GPU -> this GPU over NVLink (D2H, source IPC-mapped) -- then hop 2 out of it
+ *    to the destination (the target GPU over NVLink, or host memory), both DMAs on this
+ *    process's streams; slot s always uses stream s & 1, so stream order reuses slots and no
+ *    flag crosses a process. Ordered on `stream` like mma_copy_share_segments.
  *  - mma_copy_claim_segments is the dynamic-pull form: claim_bytes units are claimed from
  *    *cursor (device memory, e.g. IPC-mapped from the target, zeroed before the transfer)
  *    until none is left; counts[path] += units taken.
@@ -392,6 +399,9 @@ int mma_ipc_close(void* dev_ptr);
 int mma_copy_share_segments(const mma_segment_t* segs, size_t nsegs, size_t chunk_bytes,
                             const uint8_t* path_of_chunk, size_t nchunks, int path, int device,
                             mma_stream_t stream);
+int mma_copy_share_segments_ring(const mma_segment_t* segs, size_t nsegs, size_t chunk_bytes,
+                                 const uint8_t* path_of_chunk, size_t nchunks, int path, int device,
+                                 unsigned slots, mma_stream_t stream);
 int mma_copy_claim_segments(const mma_segment_t* segs, size_t nsegs, size_t claim_bytes,
                             uint64_t* cursor, uint64_t* counts, int path, int device,
                             mma_stream_t stream);
@@ -412,6 +422,11 @@ int mma_copy_claim_segments(const mma_segment_t* segs, size_t nsegs, size_t clai
 int mma_ledger_attach(const char* name);
 int mma_ledger_unlink(const char* name);
 int mma_ledger_shared_add(const char* bus_id, int dir, int64_t bytes, int64_t own);
+/* Adds to THIS process's entry of the attached ledger, as the engine's own calls do (they
+ * are removed when the call completes, or with the entry when the process detaches or dies:
+ * readers skip entries whose process is gone, and the next attacher reclaims them).
+ * mma_ledger_shared_add instead adds to a hand-entered entry that no process owns. */
+int mma_ledger_process_add(const char* bus_id, int dir, int64_t bytes, int64_t own);
 int mma_ledger_shared_get(const char* bus_id, int dir, uint64_t* bytes, uint64_t* own);
 /* The order the engine issues a path's pieces in under cfg.host_order (reading R22): perm
  * receives the stable ascending order of the n addresses (radix sort on 4 KiB page numbers,

@@ -3,14 +3,17 @@
 // its own multipath queue, so without a shared view two flows relay through each other's
 // links blindly -- Fig 9b's two MMA flows).
 //
-// One POSIX shared-memory object per name holds, per (direction, GPU), the bytes that calls
-// of every attached process still have queued on that GPU's link, and of those the bytes of
-// the GPU's own (direct) transfers. GPUs are keyed by PCI bus id, so processes with different
+// One POSIX shared-memory object per name holds, per attached process and per (direction,
+// GPU), the bytes that the process's calls still have queued on that GPU's link, and of those
+// the bytes of the GPU's own (direct) transfers; a reader sums the live processes' entries. GPUs are keyed by PCI bus id, so processes with different
 // CUDA_VISIBLE_DEVICES agree on them. An all-zero object is a valid empty ledger, so creation
 // needs no initialisation protocol. Counters are lock-free 64-bit atomics in the mapping.
 #include <fcntl.h>
+#include <signal.h>
 #include <sys/mman.h>
 #include <unistd.h>
+
+#include <cerrno>
 
 #include <atomic>
 
@@ -20,28 +23,47 @@ namespace mma {
 
 namespace {
 
-struct ShmLedger {
-    std::atomic<uint32_t> lock;                    // guards the slot table
+// One entry per attached process, written only by its owner: a process that dies with
+// calls in flight leaves counters that readers then ignore (its pid is gone) and the next
+// attacher reclaims. Entry 0 holds bytes entered by hand (mma_ledger_shared_add).
+constexpr int kEntries = 64;
+struct Entry {
+    std::atomic<int32_t> pid;                      // 0 = free; entry 0: always live
     uint32_t pad;
-    char bus[MMA_MAX_GPUS][32];                    // PCI bus id per slot ("" = free)
     std::atomic<uint64_t> bytes[2][MMA_MAX_GPUS];  // queued on the slot's link
     std::atomic<uint64_t> own[2][MMA_MAX_GPUS];    // of which the slot's own target's direct bytes
+};
+struct ShmLedger {
+    std::atomic<uint32_t> lock;                    // guards the slot and entry tables
+    uint32_t pad;
+    char bus[MMA_MAX_GPUS][32];                    // PCI bus id per slot ("" = free)
+    Entry entry[kEntries];
 };
 static_assert(std::atomic<uint64_t>::is_always_lock_free, "cross-process atomics must be lock-free");
 
 std::mutex g_mu;
 ShmLedger* g_shm = nullptr;
-int g_slot_cache[MMA_MAX_GPUS];   // local device -> slot (-2 = not looked up); reset on attach
+int g_entry = -1;                  // this process's entry
+uint64_t g_gen = 0;                // attach generation (InFlight records it)
+int g_slot_cache[MMA_MAX_GPUS];    // local device -> slot (-2 = not looked up); reset on attach
 bool g_cache_init = false;
 
-std::string shm_name(const char* name) { return std::string("/mma_ledger_") + name; }
+std::string shm_name(const char* name) { return std::string("/mma_ledger2_") + name; }
+
+void lock_table()
+{
+    while (g_shm->lock.exchange(1, std::memory_order_acquire)) {
+    }
+}
+void unlock_table() { g_shm->lock.store(0, std::memory_order_release); }
+
+bool alive(int32_t pid) { return pid > 0 && (kill(pid, 0) == 0 || errno == EPERM); }
 
 // slot of a bus id (claimed on first use); -1 when the table is full
 int slot_of(const char* bus)
 {
     if (!g_shm || !bus || !*bus) return -1;
-    while (g_shm->lock.exchange(1, std::memory_order_acquire)) {
-    }
+    lock_table();
     int found = -1, free_slot = -1;
     for (int s = 0; s < MMA_MAX_GPUS; s++) {
         if (!strncmp(g_shm->bus[s], bus, sizeof g_shm->bus[s])) { found = s; break; }
@@ -51,7 +73,7 @@ int slot_of(const char* bus)
         strncpy(g_shm->bus[free_slot], bus, sizeof g_shm->bus[free_slot] - 1);
         found = free_slot;
     }
-    g_shm->lock.store(0, std::memory_order_release);
+    unlock_table();
     return found;
 }
 
@@ -73,6 +95,46 @@ int slot_of_device(int dev)
     }
     return g_slot_cache[dev];
 }
+
+void clear_entry(Entry& e)
+{
+    for (int d = 0; d < 2; d++)
+        for (int s = 0; s < MMA_MAX_GPUS; s++) {
+            e.bytes[d][s].store(0, std::memory_order_relaxed);
+            e.own[d][s].store(0, std::memory_order_relaxed);
+        }
+}
+
+void add(Entry& e, int dir, int slot, int64_t bytes, int64_t own)
+{
+    e.bytes[dir][slot].fetch_add((uint64_t)bytes, std::memory_order_relaxed);
+    e.own[dir][slot].fetch_add((uint64_t)own, std::memory_order_relaxed);
+}
+
+// sum over the live entries
+void sum(int dir, int slot, uint64_t* bytes, uint64_t* own)
+{
+    *bytes = *own = 0;
+    for (int k = 0; k < kEntries; k++) {
+        Entry& e = g_shm->entry[k];
+        if (k != 0 && !alive(e.pid.load(std::memory_order_relaxed))) continue;
+        *bytes += e.bytes[dir][slot].load(std::memory_order_relaxed);
+        *own += e.own[dir][slot].load(std::memory_order_relaxed);
+    }
+}
+
+// give this process's entry back (its in-flight bytes leave the ledger with it)
+void detach_locked()
+{
+    if (!g_shm) return;
+    if (g_entry > 0) {
+        clear_entry(g_shm->entry[g_entry]);
+        g_shm->entry[g_entry].pid.store(0, std::memory_order_release);
+    }
+    munmap(g_shm, sizeof(ShmLedger));
+    g_shm = nullptr;
+    g_entry = -1;
+}
 }  // namespace
 
 bool shm_ledger_on()
@@ -81,13 +143,19 @@ bool shm_ledger_on()
     return g_shm != nullptr;
 }
 
-void shm_ledger_add(int dir, int dev, int64_t bytes, int64_t own)
+uint64_t shm_ledger_gen()
 {
     std::lock_guard<std::mutex> g(g_mu);
+    return g_shm ? g_gen : 0;
+}
+
+void shm_ledger_add(int dir, int dev, int64_t bytes, int64_t own, uint64_t gen)
+{
+    std::lock_guard<std::mutex> g(g_mu);
+    if (!g_shm || g_entry < 0 || gen != g_gen) return;   // entered under another attach: gone with it
     const int s = slot_of_device(dev);
     if (s < 0) return;
-    g_shm->bytes[dir][s].fetch_add((uint64_t)bytes, std::memory_order_relaxed);
-    g_shm->own[dir][s].fetch_add((uint64_t)own, std::memory_order_relaxed);
+    add(g_shm->entry[g_entry], dir, s, bytes, own);
 }
 
 int shm_ledger_slot(int dev)
@@ -96,12 +164,11 @@ int shm_ledger_slot(int dev)
     return g_shm ? slot_of_device(dev) : -1;
 }
 
-void shm_ledger_add_slot(int dir, int slot, int64_t bytes, int64_t own)
+void shm_ledger_add_slot(int dir, int slot, int64_t bytes, int64_t own, uint64_t gen)
 {
     std::lock_guard<std::mutex> g(g_mu);
-    if (!g_shm || slot < 0 || slot >= MMA_MAX_GPUS) return;
-    g_shm->bytes[dir][slot].fetch_add((uint64_t)bytes, std::memory_order_relaxed);
-    g_shm->own[dir][slot].fetch_add((uint64_t)own, std::memory_order_relaxed);
+    if (!g_shm || g_entry < 0 || gen != g_gen || slot < 0 || slot >= MMA_MAX_GPUS) return;
+    add(g_shm->entry[g_entry], dir, slot, bytes, own);
 }
 
 void shm_ledger_get(int dir, int dev, uint64_t* bytes, uint64_t* own)
@@ -110,8 +177,7 @@ void shm_ledger_get(int dir, int dev, uint64_t* bytes, uint64_t* own)
     *bytes = *own = 0;
     const int s = slot_of_device(dev);
     if (s < 0) return;
-    *bytes = g_shm->bytes[dir][s].load(std::memory_order_relaxed);
-    *own = g_shm->own[dir][s].load(std::memory_order_relaxed);
+    sum(dir, s, bytes, own);
 }
 
 }  // namespace mma
@@ -123,11 +189,9 @@ extern "C" {
 int mma_ledger_attach(const char* name)
 {
     std::lock_guard<std::mutex> g(g_mu);
-    if (g_shm) {
-        munmap(g_shm, sizeof(ShmLedger));
-        g_shm = nullptr;
-    }
+    detach_locked();
     g_cache_init = false;
+    g_gen++;
     if (!name || !*name) return cudaSuccess;
     if (strchr(name, '/') || strlen(name) > 200) return cudaErrorInvalidValue;
     const int fd = shm_open(shm_name(name).c_str(), O_CREAT | O_RDWR, 0600);
@@ -140,6 +204,25 @@ int mma_ledger_attach(const char* name)
     close(fd);
     if (p == MAP_FAILED) return cudaErrorMemoryAllocation;
     g_shm = (ShmLedger*)p;
+    // claim an entry: our own (re-attach), a dead process's, or a free one
+    const int32_t me = (int32_t)getpid();
+    lock_table();
+    int pick = -1;
+    for (int k = 1; k < kEntries && pick < 0; k++)
+        if (g_shm->entry[k].pid.load(std::memory_order_relaxed) == me) pick = k;
+    for (int k = 1; k < kEntries && pick < 0; k++)
+        if (!alive(g_shm->entry[k].pid.load(std::memory_order_relaxed))) pick = k;
+    if (pick > 0) {
+        clear_entry(g_shm->entry[pick]);
+        g_shm->entry[pick].pid.store(me, std::memory_order_release);
+    }
+    unlock_table();
+    if (pick < 0) {   // 63 live processes already: no room
+        munmap(g_shm, sizeof(ShmLedger));
+        g_shm = nullptr;
+        return cudaErrorMemoryAllocation;
+    }
+    g_entry = pick;
     return cudaSuccess;
 }
 
@@ -163,8 +246,18 @@ int mma_ledger_shared_add(const char* bus_id, int dir, int64_t bytes, int64_t ow
     if (dir != MMA_H2D && dir != MMA_D2H) return cudaErrorInvalidValue;
     const int s = slot_of(bus_id);
     if (s < 0) return cudaErrorInvalidValue;
-    g_shm->bytes[dir][s].fetch_add((uint64_t)bytes, std::memory_order_relaxed);
-    g_shm->own[dir][s].fetch_add((uint64_t)own, std::memory_order_relaxed);
+    add(g_shm->entry[0], dir, s, bytes, own);   // the hand-entered entry (always live)
+    return cudaSuccess;
+}
+
+int mma_ledger_process_add(const char* bus_id, int dir, int64_t bytes, int64_t own)
+{
+    std::lock_guard<std::mutex> g(g_mu);
+    if (!g_shm || g_entry < 0) return cudaErrorInvalidValue;
+    if (dir != MMA_H2D && dir != MMA_D2H) return cudaErrorInvalidValue;
+    const int s = slot_of(bus_id);
+    if (s < 0) return cudaErrorInvalidValue;
+    add(g_shm->entry[g_entry], dir, s, bytes, own);   // this process's entry, as its calls do
     return cudaSuccess;
 }
 
@@ -175,8 +268,7 @@ int mma_ledger_shared_get(const char* bus_id, int dir, uint64_t* bytes, uint64_t
     if (dir != MMA_H2D && dir != MMA_D2H) return cudaErrorInvalidValue;
     const int s = slot_of(bus_id);
     if (s < 0) return cudaErrorInvalidValue;
-    *bytes = g_shm->bytes[dir][s].load(std::memory_order_relaxed);
-    *own = g_shm->own[dir][s].load(std::memory_order_relaxed);
+    sum(dir, s, bytes, own);
     return cudaSuccess;
 }
 

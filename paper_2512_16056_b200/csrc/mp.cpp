@@ -87,12 +87,13 @@ int vstream_from(const mma_segment_t* segs, size_t nsegs, uint64_t C, cudaStream
 struct LedgerRelease {
     int dir, slot;
     int64_t bytes, own;
+    uint64_t gen;   // the attach it entered (a re-attach drops it)
 };
 
 void CUDART_CB release_share(void* p)
 {
     LedgerRelease* r = (LedgerRelease*)p;
-    shm_ledger_add_slot(r->dir, r->slot, -r->bytes, -r->own);
+    shm_ledger_add_slot(r->dir, r->slot, -r->bytes, -r->own, r->gen);
     delete r;
 }
 
@@ -104,11 +105,52 @@ int ledger_share(const mma_segment_t* segs, int device, uint64_t bytes, bool own
     int dir = MMA_H2D;
     if (cudaPointerGetAttributes(&a, segs[0].src) == cudaSuccess && a.type == cudaMemoryTypeDevice) dir = MMA_D2H;
     cudaGetLastError();
-    LedgerRelease* r = new LedgerRelease{dir, slot, (int64_t)bytes, own ? (int64_t)bytes : 0};
-    shm_ledger_add_slot(dir, slot, r->bytes, r->own);
+    LedgerRelease* r = new LedgerRelease{dir, slot, (int64_t)bytes, own ? (int64_t)bytes : 0, shm_ledger_gen()};
+    shm_ledger_add_slot(dir, slot, r->bytes, r->own, r->gen);
     const cudaError_t e = cudaLaunchHostFunc(s, release_share, r);
     if (e != cudaSuccess) release_share(r);
     return (int)e;
+}
+
+// The copy-engine relay ring of this process for one (device, direction) (NEXT-4): S slots
+// of C bytes in this GPU's HBM and the dual relay pipeline's two streams. Slot s
+// is always used on stream s & 1, so stream order alone keeps a slot's next hop-1 DMA behind
+// its previous hop-2 DMA: the ring needs no flags, and a share of another process's transfer
+// moves through it with this process's copy engines only.
+struct ShareRing {
+    char* stage = nullptr;
+    uint64_t C = 0;
+    uint32_t S = 0;
+    cudaStream_t hop[2] = {};
+    cudaEvent_t fork = nullptr, done[2] = {};
+    uint64_t next = 0;   // chunks carried so far: the slot of the next one
+};
+ShareRing g_share_ring[MMA_MAX_GPUS][2];
+
+int share_ring(int device, int dir, uint64_t C, uint32_t S, ShareRing** out)
+{
+    ShareRing& r = g_share_ring[device][dir];
+    DeviceGuard g(device);
+    if (r.stage && (r.C < C || r.S != S)) {   // re-sized: drain, then make it afresh
+        for (cudaStream_t h : r.hop) CK(cudaStreamSynchronize(h));
+        CK(cudaFree(r.stage));
+        r.stage = nullptr;
+    }
+    if (!r.hop[0]) {
+        for (int k = 0; k < 2; k++) {
+            CK(cudaStreamCreateWithFlags(&r.hop[k], cudaStreamNonBlocking));
+            CK(cudaEventCreateWithFlags(&r.done[k], cudaEventDisableTiming));
+        }
+        CK(cudaEventCreateWithFlags(&r.fork, cudaEventDisableTiming));
+    }
+    if (!r.stage) {
+        CK(cudaMalloc(&r.stage, (size_t)S * C));
+        r.C = C;
+        r.S = S;
+        r.next = 0;
+    }
+    *out = &r;
+    return cudaSuccess;
 }
 
 }  // namespace
@@ -253,6 +295,71 @@ int mma_copy_share_segments(const mma_segment_t* segs, size_t nsegs, size_t chun
     }
     if (dtab) cudaFreeAsync(dtab, s);
     return rc;
+}
+
+int mma_copy_share_segments_ring(const mma_segment_t* segs, size_t nsegs, size_t chunk_bytes,
+                                 const uint8_t* path_of_chunk, size_t nchunks, int path, int device,
+                                 unsigned slots, mma_stream_t stream)
+{
+    CK((cudaError_t)ensure_init());
+    if (int se = sticky()) return se;
+    if (!nsegs) return cudaSuccess;
+    if (!segs || !path_of_chunk || chunk_bytes == 0 || path < 0 || slots < 1 || slots > 64) return cudaErrorInvalidValue;
+    Engine& e = E();
+    if (device < 0 || device >= e.ndev) return cudaErrorInvalidDevice;
+    std::vector<uint64_t> start(nsegs + 1, 0);
+    for (size_t k = 0; k < nsegs; k++) {
+        if (segs[k].bytes && (!segs[k].src || !segs[k].dst)) return cudaErrorInvalidValue;
+        start[k + 1] = start[k] + segs[k].bytes;
+    }
+    const uint64_t B = start[nsegs];
+    uint64_t C = chunk_bytes;
+    if ((B + C - 1) / C != nchunks && !(nchunks == 1 && B > 0)) return cudaErrorInvalidValue;
+    if (nchunks == 1) C = B;                   // a one-piece (fallback) plan
+    // direction from the memory kinds: a device source is an offload (D2H)
+    cudaPointerAttributes a;
+    int dir = MMA_H2D;
+    if (cudaPointerGetAttributes(&a, segs[0].src) == cudaSuccess && a.type == cudaMemoryTypeDevice) dir = MMA_D2H;
+    cudaGetLastError();
+    CK(make_device(device));
+    std::lock_guard<std::mutex> lk(g_mp_mu);
+    ShareRing* r = nullptr;
+    CK(share_ring(device, dir, C, slots, &r));
+    DeviceGuard g(device);
+    cudaStream_t user = (cudaStream_t)stream;
+    CK(cudaEventRecord(r->fork, user));
+    bool used[2] = {false, false};
+    uint64_t mine_bytes = 0;
+    for (size_t i = 0; i < nchunks; i++) {
+        if (path_of_chunk[i] != path) continue;
+        const uint64_t off = (uint64_t)i * C, len = std::min<uint64_t>(C, B - off);
+        const uint32_t slot = (uint32_t)(r->next++ % r->S);
+        const int k = slot & 1;
+        cudaStream_t hs = r->hop[k];
+        if (!used[k]) { CK(cudaStreamWaitEvent(hs, r->fork, 0)); used[k] = true; }
+        char* buf = r->stage + (uint64_t)slot * r->C;
+        DmaBatch in, out;
+        size_t q = std::upper_bound(start.begin(), start.end(), off) - start.begin() - 1;
+        for (; q < nsegs && start[q] < off + len; q++) {   // the chunk's pieces, packed in the slot
+            const uint64_t lo = std::max(start[q], off), hi = std::min(start[q + 1], off + len);
+            if (lo >= hi) continue;
+            const char* sp = (const char*)segs[q].src + (lo - start[q]);
+            char* dp = (char*)segs[q].dst + (lo - start[q]);
+            in.add(buf + (lo - off), sp, hi - lo);
+            out.add(dp, buf + (lo - off), hi - lo);
+        }
+        // hop 1 into the slot over this GPU's link (H2D) or from the source GPU (D2H, a peer
+        // copy over NVLink), hop 2 out of it: the same stream, so the slot is free again after
+        CK(in.issue(dir == MMA_H2D ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice, hs));
+        CK(out.issue(dir == MMA_H2D ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, hs));
+        mine_bytes += len;
+    }
+    for (int k = 0; k < 2; k++)   // join: the user stream waits for both relay streams
+        if (used[k]) {
+            CK(cudaEventRecord(r->done[k], r->hop[k]));
+            CK(cudaStreamWaitEvent(user, r->done[k], 0));
+        }
+    return ledger_share(segs, device, mine_bytes, path == 0, user);
 }
 
 int mma_copy_claim_segments(const mma_segment_t* segs, size_t nsegs, size_t claim_bytes,

@@ -537,7 +537,7 @@ void ledger_retire()
             e.ledger[f.dir][g] -= f.bytes[g];
             e.ledger_own[f.dir][g] -= f.own[g];
             if (f.shared && (f.bytes[g] || f.own[g]))
-                shm_ledger_add(f.dir, g, -(int64_t)f.bytes[g], -(int64_t)f.own[g]);
+                shm_ledger_add(f.dir, g, -(int64_t)f.bytes[g], -(int64_t)f.own[g], f.shared);
         }
         e.free_events.push_back({f.dev, f.done});
         e.inflight[i] = e.inflight.back();
@@ -567,10 +567,10 @@ static int ledger_add(int dir, int user_dev, cudaStream_t user, const uint64_t* 
         e.ledger_own[dir][k] += own[k];
     }
     // with a cross-process ledger attached, every process plans against every process's bytes
-    f.shared = shm_ledger_on();
+    f.shared = shm_ledger_gen();
     if (f.shared)
         for (int k = 0; k < MMA_MAX_GPUS; k++)
-            if (bytes[k] || own[k]) shm_ledger_add(dir, k, (int64_t)bytes[k], (int64_t)own[k]);
+            if (bytes[k] || own[k]) shm_ledger_add(dir, k, (int64_t)bytes[k], (int64_t)own[k], f.shared);
     e.inflight.push_back(f);
     return cudaSuccess;
 }

@@ -165,7 +165,7 @@ struct Engine {
         int dev, dir;
         uint64_t bytes[MMA_MAX_GPUS];
         uint64_t own[MMA_MAX_GPUS];
-        bool shared;                 // also entered in the cross-process ledger
+        uint64_t shared;             // attach generation of the cross-process ledger it entered (0 = none)
     };
     std::vector<InFlight> inflight;
     std::vector<std::pair<int, cudaEvent_t>> free_events;
@@ -362,10 +362,13 @@ int record_gates(int g, int dir);
 void ledger_retire();
 // ---- ledger_shm.cpp: the cross-process ledger (mma_ledger_attach)
 bool shm_ledger_on();
-void shm_ledger_add(int dir, int dev, int64_t bytes, int64_t own);
+uint64_t shm_ledger_gen();   // attach generation; 0 when detached
+// adds to this process's entry, if `gen` is still the current attach (else the bytes left
+// the ledger with the old attach)
+void shm_ledger_add(int dir, int dev, int64_t bytes, int64_t own, uint64_t gen);
 void shm_ledger_get(int dir, int dev, uint64_t* bytes, uint64_t* own);
 int shm_ledger_slot(int dev);   // -1 when detached; resolves the bus id (a CUDA call)
-void shm_ledger_add_slot(int dir, int slot, int64_t bytes, int64_t own);   // no CUDA calls
+void shm_ledger_add_slot(int dir, int slot, int64_t bytes, int64_t own, uint64_t gen);   // no CUDA calls
 int run_job(Job& j);
 int run_multi(std::vector<Job>& jobs);   // a joint plan of concurrent transfers (NEXT-1)
 int reserve_tables(const Job& j);

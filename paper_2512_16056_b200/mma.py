@@ -25,7 +25,7 @@ SYMBOLS = [
     "mma_memcpy_h2d_segments", "mma_memcpy_d2h_segments", "mma_get_paths", "mma_set_bandwidth",
     "mma_set_path_modes", "mma_calibrate", "mma_get_plan", "mma_plan_chunks",
     "mma_get_delivery_log", "mma_get_segment_order", "mma_plan_multi", "mma_memcpy_multi",
-    "mma_host_alloc_size", "mma_host_alloc", "mma_host_free", "mma_get_stats",
+    "mma_host_alloc_size", "mma_copy_share_segments_ring", "mma_ledger_process_add", "mma_host_alloc", "mma_host_free", "mma_get_stats",
     "mma_reset_stats", "mma_get_last_error", "mma_error_string", "mma_fill_pattern",
     "mma_verify_pattern", "mma_verify_segments", "mma_set_kernel_timing", "mma_kernel_times",
     "mma_tune_segments", "mma_get_segment_tuning", "mma_get_dynamic_counts", "mma_set_plan_mode",
@@ -125,6 +125,7 @@ def lib():
         L.mma_get_segment_order.argtypes = [C.c_int, vp, sz, C.POINTER(sz)]
         L.mma_memcpy_multi.argtypes = [C.POINTER(Transfer), sz]
         L.mma_host_alloc_size.argtypes = [vp, C.POINTER(sz)]
+        L.mma_copy_share_segments_ring.argtypes = [C.POINTER(Segment), sz, sz, vp, sz, C.c_int, C.c_int, C.c_uint, vp]
         L.mma_plan_multi.argtypes = [C.c_int, vp, vp, C.c_int, vp, vp, C.c_uint64, C.c_int, vp]
         L.mma_host_alloc.argtypes = [C.POINTER(vp), sz, C.c_uint]
         L.mma_host_free.argtypes = [vp]
@@ -145,6 +146,7 @@ def lib():
         L.mma_order_by_address.argtypes = [vp, sz, vp]
         L.mma_ledger_unlink.argtypes = [C.c_char_p]
         L.mma_ledger_shared_add.argtypes = [C.c_char_p, C.c_int, C.c_int64, C.c_int64]
+        L.mma_ledger_process_add.argtypes = [C.c_char_p, C.c_int, C.c_int64, C.c_int64]
         L.mma_ledger_shared_get.argtypes = [C.c_char_p, C.c_int, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]
         L.mma_tune_chunk.argtypes = [C.c_int, C.c_int, sz, C.POINTER(sz)]
         L.mma_tune_threshold.argtypes = [C.c_int, C.c_int, sz, C.POINTER(sz), C.POINTER(C.c_int)]
@@ -363,6 +365,10 @@ def ledger_shared_add(bus_id: str, direction: int, nbytes: int, own: int = 0) ->
     _check(lib().mma_ledger_shared_add(bus_id.encode(), direction, nbytes, own), "mma_ledger_shared_add")
 
 
+def ledger_process_add(bus_id: str, direction: int, nbytes: int, own: int = 0) -> None:
+    _check(lib().mma_ledger_process_add(bus_id.encode(), direction, nbytes, own), "mma_ledger_process_add")
+
+
 def ledger_shared_get(bus_id: str, direction: int):
     """(bytes, own) queued on the link of the GPU with this PCI bus id, all processes."""
     b, o = C.c_uint64(), C.c_uint64()
@@ -566,6 +572,14 @@ def copy_share_segments(segs, nsegs: int, chunk_bytes: int, path_of_chunk: bytes
     buf = (C.c_uint8 * max(len(path_of_chunk), 1)).from_buffer_copy(path_of_chunk or b"\0")
     _check(lib().mma_copy_share_segments(segs, nsegs, chunk_bytes, buf, len(path_of_chunk), path, device,
                                          _stream(stream, device)), "mma_copy_share_segments")
+
+
+def copy_share_segments_ring(segs, nsegs: int, chunk_bytes: int, path_of_chunk: bytes, path: int,
+                             device: int, slots: int = 4, stream=None) -> None:
+    """This process's share moved through its own copy-engine relay ring (NEXT-4)."""
+    buf = (C.c_uint8 * max(len(path_of_chunk), 1)).from_buffer_copy(path_of_chunk or b"\0")
+    _check(lib().mma_copy_share_segments_ring(segs, nsegs, chunk_bytes, buf, len(path_of_chunk), path, device,
+                                              slots, _stream(stream, device)), "mma_copy_share_segments_ring")
 
 
 def copy_claim_segments(segs, nsegs: int, claim_bytes: int, cursor_ptr: int, counts_ptr: int,

@@ -1,7 +1,7 @@
 #!/bin/bash
 mkdir -p gpurun_out/r02
 export MMA_SPIN_TIMEOUT_MS=8000
-timeout 1500 python -m pytest tests/test_gpu_multi.py tests/test_gpu_preload.py tests/test_gpu_hostmem.py tests/test_gpu_ledger.py -q > gpurun_out/r02/f_tests.log 2>&1; echo "rc=$?" >> gpurun_out/r02/f_tests.log
-timeout 900 python bench.py > gpurun_out/r02/f_bench.json 2> gpurun_out/r02/f_bench.err
-timeout 600 python bench.py --workload contention --steps 3 --warmup 1 > gpurun_out/r02/f_contention.json 2> gpurun_out/r02/f_contention.err
-tail -15 gpurun_out/r02/f_tests.log; tail -c 1500 gpurun_out/r02/f_bench.json; tail -3 gpurun_out/r02/f_bench.err; cat gpurun_out/r02/f_contention.json; tail -3 gpurun_out/r02/f_contention.err
+timeout 900 ncu --clock-control none --set full --import-source on --metrics nvlrx__bytes.sum,nvltx__bytes.sum,pcie__read_bytes.sum,pcie__write_bytes.sum \
+    -k regex:relay_pull -c 4 -f -o gpurun_out/prof_relay_proto_pull python scripts/ncu_relay_protocol.py > gpurun_out/ncu_relay_proto_pull.log 2>&1; echo "pull rc=$?"
+timeout 2400 python -m pytest tests -m gpu -q > gpurun_out/r02/g_all.log 2>&1; echo "rc=$?" >> gpurun_out/r02/g_all.log
+tail -15 gpurun_out/r02/g_all.log

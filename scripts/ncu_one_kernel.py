@@ -1,7 +1,8 @@
 #!/usr/bin/env python3
 """One zero-copy launch of the config-3 shape (for ncu): --dir h2d|d2h, --tokens N."""
-import argparse, sys
+import argparse, os, sys
 from pathlib import Path
+os.environ.setdefault("MMA_UPLOAD", "ce")   # tables by DMA: the only zc_copy_kernel launch is the copy
 sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
 import numpy as np, torch
 import paper_2512_16056_b200 as mma

@@ -122,6 +122,28 @@ def main():
             if e["gpu_time_ms"]:
                 e["payload_gbps"] = round(RELAY_BYTES / (e["gpu_time_ms"] * 1e-3) / 1e9, 1)
             summary["kernels"][name] = e
+    for rel, sfx in ((OUT / "prof_relay_proto.ncu-rep", ""), (OUT / "prof_relay_proto_pull.ncu-rep", "_pull")):
+        if not rel.exists():
+            continue
+        (PROF / f"{TAG}_ncu_relay_protocol{sfx}_details.csv").write_text(ncu_csv(rel, "details"))
+        (PROF / f"{TAG}_ncu_relay_protocol{sfx}_raw.csv").write_text(ncu_csv(rel, "raw"))
+        for k, d in enumerate(raw_rows(rel)):
+            name = d["Kernel Name"][0].split("(")[0].split("::")[-1]
+            grid = int(str(d.get("launch__grid_size", ("0",))[0]).replace(",", "") or 0)
+            # one wave: 3 rings x S = 4 chunks x 8 MiB (loopback form)
+            algo = 3 * 4 * (8 << 20)
+            e = kernel_entry(d, f"{name} in the engine's protocol (scripts/ncu_relay_protocol.py): one wave of "
+                                "3 rings x 4 chunks x 8 MiB, launched by mma_memcpy_* after (H2D) / before (D2H) "
+                                "the wave's hops; ncu serialises, so the wave's hop 1 is complete", algo,
+                             f"profiles/{TAG}_ncu_relay_protocol{sfx}_details.csv")
+            e["algorithmic_hbm_bytes_per_launch"] = 2 * algo
+            for m in ("nvlrx__bytes.sum", "nvltx__bytes.sum"):
+                if val(d, m) is not None:
+                    e[m.split(".")[0]] = int(val(d, m))
+            if e["gpu_time_ms"]:
+                e["payload_gbps"] = round(algo / (e["gpu_time_ms"] * 1e-3) / 1e9, 1)
+            e["launch"] = k
+            summary["kernels"][f"{name}/protocol/{k}"] = e
     lst = OUT / "launches_bench.csv"
     if lst.exists():
         shutil.copy(lst, PROF / f"{TAG}_launches_bench.csv")

@@ -8,6 +8,9 @@
 #      kernels return nan under kernel replay, so application replay with a metric list
 #   4. --set full of the relay pull / pack kernels alone (scripts/probe/probe_relay ncu:
 #      7 rings x 8 CTAs, hop 1 complete, slots in local HBM)
+#   5. --set full + NVLink counters of the relay pack and pull kernels in the engine's real
+#      protocol (scripts/ncu_relay_protocol.py: waves of S chunks through mma_memcpy_*;
+#      loopback rings on one GPU, peer rings with --peers on a multi-GPU box)
 mkdir -p gpurun_out
 NCU="ncu --clock-control none"
 timeout 900 $NCU --metrics gpu__time_duration.sum -c 400 --csv --log-file gpurun_out/launches_bench.csv \
@@ -26,3 +29,11 @@ echo "relay rc=$?"
 timeout 600 $NCU --set full --import-source on -k regex:relay -s 2 -c 2 -f -o gpurun_out/prof_relay_seg \
     ./scripts/probe/probe_relay ncu > gpurun_out/ncu_relay_seg.log 2>&1
 echo "relay seg rc=$?"
+[ -n "$PROFILE_ONLY_PROTO" ] && exit 0
+PEERS=""; [ "$(nvidia-smi -L | wc -l)" -gt 1 ] && PEERS="--peers"
+timeout 900 $NCU --set full --import-source on --metrics nvlrx__bytes.sum,nvltx__bytes.sum,pcie__read_bytes.sum,pcie__write_bytes.sum \
+    -k regex:relay_pack -c 4 -f -o gpurun_out/prof_relay_proto python scripts/ncu_relay_protocol.py $PEERS > gpurun_out/ncu_relay_proto.log 2>&1
+echo "relay protocol (pack) rc=$?"
+timeout 900 $NCU --set full --import-source on --metrics nvlrx__bytes.sum,nvltx__bytes.sum,pcie__read_bytes.sum,pcie__write_bytes.sum \
+    -k regex:relay_pull -c 4 -f -o gpurun_out/prof_relay_proto_pull python scripts/ncu_relay_protocol.py $PEERS > gpurun_out/ncu_relay_proto_pull.log 2>&1
+echo "relay protocol (pull) rc=$?"

@@ -96,3 +96,39 @@ def test_slots_by_bus_id_and_errors(name):
         m.ledger_attach(None)
     with pytest.raises(Exception):
         m.ledger_attach("bad/name")
+
+
+def _adder(name, bus, q_out):
+    m = _lib()
+    m.ledger_attach(name)
+    m.ledger_process_add(bus, H2D, 8 << 20, 0)        # a call of this process, in flight
+    q_out.put("added")
+    import time
+    time.sleep(600)                                   # killed before it completes
+
+
+def test_dead_process_bytes_leave_the_ledger(name):
+    """a process that dies with calls in flight must not pin its bytes in the
+    ledger: entries belong to processes, readers skip a dead owner's, and a later attacher
+    reclaims the entry"""
+    import signal
+    m = _lib()
+    m.ledger_attach(name)
+    bus = "0000:1b:00.0"
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    p = ctx.Process(target=_adder, args=(name, bus, q))
+    p.start()
+    try:
+        assert q.get(timeout=120) == "added"
+        assert m.ledger_shared_get(bus, H2D) == (8 << 20, 0)
+        m.ledger_process_add(bus, H2D, 1 << 20, 1 << 20)             # this process's own call
+        assert m.ledger_shared_get(bus, H2D) == (9 << 20, 1 << 20)
+    finally:
+        os.kill(p.pid, signal.SIGKILL)
+        p.join(timeout=60)
+    assert m.ledger_shared_get(bus, H2D) == (1 << 20, 1 << 20)       # the dead process's bytes are gone
+    m.ledger_process_add(bus, H2D, -(1 << 20), -(1 << 20))
+    m.ledger_attach(name)                                             # re-attach: a fresh entry
+    assert m.ledger_shared_get(bus, H2D) == (0, 0)
+    m.ledger_attach(None)
