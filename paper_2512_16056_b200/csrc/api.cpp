@@ -378,6 +378,7 @@ int mma_finalize(void)
             }
         cudaEventDestroy(r.fork);
         cudaEventDestroy(r.cap_fork);
+        for (cudaEvent_t ev : r.fork_pool) cudaEventDestroy(ev);
         for (auto& gd : r.gate_ev)
             for (cudaEvent_t ev : gd) cudaEventDestroy(ev);
         cudaEventDestroy(r.cap_ev);

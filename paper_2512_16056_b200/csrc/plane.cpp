@@ -747,10 +747,15 @@ public:
         return finish();
     }
 
-    ~Call() { close_range(); }
+    ~Call()
+    {
+        close_range();
+        // every stream wait on the fork event is enqueued by now: the event can be reused
+        if (pooled_fork_) eng_.dev[j_.user_dev].fork_pool.push_back(fork_);
+    }
 
 private:
-    bool done_ = false, forked_ = false, nvtx_open_ = false;
+    bool done_ = false, forked_ = false, nvtx_open_ = false, pooled_fork_ = false;
     std::vector<cudaEvent_t> gates_[MMA_MAX_GPUS];
     std::vector<cudaStream_t> gated_;   // streams already made to wait on their GPU's gates
 
@@ -1149,7 +1154,19 @@ private:
     {
         DeviceGuard g(j_.user_dev);
         CK(make_device(j_.user_dev));
-        fork_ = j_.capturing ? eng_.dev[j_.user_dev].cap_fork : eng_.dev[j_.user_dev].fork;
+        if (j_.capturing) {
+            fork_ = eng_.dev[j_.user_dev].cap_fork;
+        } else {   // an event of its own: calls of one joint plan fork before any of them forks a stream
+            auto& pool = eng_.dev[j_.user_dev].fork_pool;
+            if (pool.empty()) {
+                cudaEvent_t ev = nullptr;
+                CK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+                pool.push_back(ev);
+            }
+            fork_ = pool.back();
+            pool.pop_back();
+            pooled_fork_ = true;
+        }
         CK(cudaEventRecord(fork_, j_.user));
         return cudaSuccess;
     }

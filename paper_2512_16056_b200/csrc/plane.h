@@ -81,6 +81,7 @@ struct DevRes {
     Lanes cap_lane[2];
     cudaEvent_t fork = nullptr;      // recorded on a user stream of this device
     cudaEvent_t cap_fork = nullptr;  // idem, captured calls
+    std::vector<cudaEvent_t> fork_pool;   // fork events of live calls (one per call in flight of enqueue)
     // [dir][0 direct lane, 1 zero-copy lane]: recorded behind this GPU's own direct work when
     // a relay through this GPU must wait for it (direct path first, plane.cpp Call::gate)
     cudaEvent_t gate_ev[2][2] = {};

@@ -52,6 +52,7 @@ def test_two_fetches_one_queue(mma, orc, mode, hop):
     srcs = [pinned(torch, b, seed=40 + i) for i, b in enumerate(sizes)]
     dsts = [guarded_device(torch, b) for b in sizes]
     streams = [torch.cuda.Stream() for _ in sizes]
+    torch.cuda.synchronize()                      # the guard fill (default stream) is done
     xf = [(mma.H2D, 0, mma.make_segments([s.data_ptr()], [d.data_ptr() + G], [b]), st)
           for s, d, b, st in zip(srcs, dsts, sizes, streams)]
     mma.memcpy_multi(xf)
@@ -116,6 +117,7 @@ def test_each_stream_sees_its_transfer(mma):
     dsts = [torch.zeros(B, dtype=torch.uint8, device="cuda") for _ in range(3)]
     probes = [torch.zeros(B, dtype=torch.uint8, device="cuda") for _ in range(3)]
     st = [torch.cuda.Stream() for _ in range(3)]
+    torch.cuda.synchronize()
     mma.memcpy_multi([(mma.H2D, 0, mma.make_segments([s.data_ptr()], [d.data_ptr()], [B]), t)
                       for s, d, t in zip(srcs, dsts, st)])
     for d, p, t in zip(dsts, probes, st):

@@ -120,6 +120,7 @@ def test_repeated_calls_ring_reuse(mma, orc):
     stream = torch.cuda.Stream()
     srcs = [pinned(torch, B, seed=100 + k) for k in range(5)]
     dsts = [torch.zeros(B, dtype=torch.uint8, device="cuda") for _ in range(5)]
+    torch.cuda.synchronize()                  # the zero fills (default stream) precede the copies
     with torch.cuda.stream(stream):
         for k in range(5):
             mma.memcpy_h2d(dsts[k], srcs[k], B, stream=stream)

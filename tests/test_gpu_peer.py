@@ -167,6 +167,8 @@ def test_two_targets_relay_through_each_other(mma, orc):
     srcs = [pinned(torch, B, seed=90 + t) for t in (0, 1)]
     dsts = [guarded_device(torch, B, dev=t) for t in (0, 1)]
     streams = [torch.cuda.Stream(device=t) for t in (0, 1)]
+    for t in (0, 1):
+        torch.cuda.synchronize(t)                 # guard fills done before the copies' streams run
     for rep in range(3):
         for t in (0, 1):
             mma.memcpy_h2d(dsts[t][G:G + B], srcs[t], B, stream=streams[t])
@@ -221,6 +223,8 @@ def test_joint_plan_two_targets(mma, orc, mode, hop):
     srcs = [pinned(torch, b, seed=60 + i) for i, b in enumerate(sizes)]
     dsts = [guarded_device(torch, b, dev=t) for t, b in enumerate(sizes)]
     st = [torch.cuda.Stream(device=t) for t in (0, 1)]
+    for t in (0, 1):
+        torch.cuda.synchronize(t)
     mma.memcpy_multi([(0, t, mma.make_segments([srcs[t].data_ptr()], [dsts[t].data_ptr() + G], [sizes[t]]), st[t])
                       for t in (0, 1)])
     for t in (0, 1):

@@ -118,6 +118,7 @@ B = 24 * C
 src = pinned(torch, B, seed=0x4D4D41)
 dst = guarded_device(torch, B)
 s = torch.cuda.Stream()
+torch.cuda.synchronize()
 out = {{}}
 {direction_code}
 out["sticky"] = m.get_last_error()
@@ -133,6 +134,7 @@ except m.MMAError:
 s.synchronize()                                      # the partial call drains (no hang)
 for rep in range(2):                                 # the broken rings are remade
     dst.fill_(0xA5)
+    torch.cuda.synchronize()
     m.memcpy_h2d(dst[G:G + B], src, B, stream=s)
     s.synchronize()
     rc, path, _, fb = oracle.plan(bw, B, C, 0, oracle.INTERLEAVED)
@@ -145,6 +147,7 @@ for rep in range(2):                                 # the broken rings are rema
 D2H_CODE = r"""
 dsrc = dst[G:G + B]
 m.fill_pattern(dsrc, B, 0x99, 0)
+torch.cuda.synchronize()
 host = pinned(torch, B + 2 * G)
 try:
     m.memcpy_d2h(host[G:G + B], dsrc, B, stream=s)

@@ -49,6 +49,7 @@ def test_concurrent_threads(mma):
                     pool = torch.empty(hpool, dtype=torch.uint8).pin_memory()
                     mma_inputs.fill_pattern(pool.numpy(), 7 + tid)
                     cache = torch.zeros(dbytes, dtype=torch.uint8, device="cuda")
+                    torch.cuda.synchronize()   # the zero fill precedes the copy on s
                     lens = np.full(len(ho), sb, dtype=np.int64)
                     segs, n = mma.make_segments(pool.data_ptr() + ho, cache.data_ptr() + do, lens)
                     mma.memcpy_h2d_segments(segs, n, 0, stream=s)

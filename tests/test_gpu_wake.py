@@ -38,6 +38,7 @@ def test_wake_and_sleep_small_qwen(mma, orc):
     mma_inputs.fill_pattern(host.numpy(), 44)
     devbuf = torch.full((total,), 0xA5, dtype=torch.uint8, device="cuda")
     s = torch.cuda.Stream()
+    torch.cuda.synchronize()                  # the guard fill (default stream) precedes the copies
     hp, dp = host.data_ptr(), devbuf.data_ptr()
     for o, n in zip(offs, sizes):
         mma.memcpy_h2d(dp + o, hp + o, n, stream=s)
