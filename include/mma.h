@@ -67,7 +67,9 @@ typedef struct {
      * optima 2.81 MB H2D / 5.37 MB D2H on H20). Default 8 MiB (B200 DMA setup cost,
      * DESIGN.md §6). Multiple of 4096. */
     size_t chunk_bytes[2];
-    /* relay staging slots per ring (P:588-594 dual pipeline = 2). 0 = default (4). */
+    /* relay staging slots per ring, 1..64 (P:588-594 dual pipeline = 2). 0 = default: 32 MiB
+     * of staging per ring, i.e. S = 32 MiB / chunk_bytes clamped to 4..32 (S = 4 at the 8 MiB
+     * default chunk, 32 at 1 MiB chunks; reading R25). */
     unsigned ring_slots;
     /* fallback threshold per direction (§3.2, §5.1.3): a copy of B < thr
      * bytes takes the native single path. (size_t)-1 = always native; 0 = never. */

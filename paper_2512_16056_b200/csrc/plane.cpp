@@ -91,7 +91,7 @@ void defaults(mma_config_t* c)
 {
     memset(c, 0, sizeof(*c));
     c->chunk_bytes[0] = c->chunk_bytes[1] = kDefaultChunk;
-    c->ring_slots = kDefaultSlots;
+    c->ring_slots = 0;   // auto: ring_slots_for(C)
     // Fallback threshold: "between two and five chunks" (§5.1.3); 2 chunks until the
     // B200 break-even sweep replaces it.
     c->fallback_bytes[0] = c->fallback_bytes[1] = 2 * kDefaultChunk;
@@ -110,7 +110,7 @@ int validate_cfg(const mma_config_t& c)
 {
     for (int d = 0; d < 2; d++)
         if (c.chunk_bytes[d] == 0 || c.chunk_bytes[d] % 4096) return cudaErrorInvalidValue;
-    if (c.ring_slots < 1 || c.ring_slots > 64) return cudaErrorInvalidValue;
+    if (c.ring_slots > 64) return cudaErrorInvalidValue;
     if (c.npaths < 0 || c.npaths > MMA_MAX_PATHS) return cudaErrorInvalidValue;
     if (c.loopback_relays < 0 || c.loopback_relays > 8) return cudaErrorInvalidValue;
     if (c.plan_mode < PLAN_CONTIGUOUS || c.plan_mode > PLAN_DYNAMIC) return cudaErrorInvalidValue;
@@ -161,6 +161,19 @@ void order_by_key(const uint64_t* key, size_t n, std::vector<uint32_t>& perm)
             std::stable_sort(perm.begin() + a, perm.begin() + b, [&](uint32_t x, uint32_t y) { return key[x] < key[y]; });
         a = b;
     }
+}
+
+// Ring depth S: cfg.ring_slots, or (0, the default) a constant 32 MiB of staging per ring,
+// 4..32 slots. A ring pays per-wave and per-group costs (a kernel launch per wave of S chunks,
+// a DMA and a batched flag operation per group), so small chunks want deep rings: one loopback
+// kernel ring carries 0.79 / 0.85 / 0.89 of the native copy at C = 1 MiB and S = 8 / 16 / 32,
+// and 0.93 at 8 MiB with S = 4 (profiles/r02_sweep_ring_depth.jsonl).
+uint32_t ring_slots_for(uint64_t C)
+{
+    const Engine& e = E();
+    if (e.cfg.ring_slots) return e.cfg.ring_slots;
+    const uint64_t s = kRingBytes / std::max<uint64_t>(C, 1);
+    return (uint32_t)std::min<uint64_t>(32, std::max<uint64_t>(4, s));
 }
 
 uint64_t zc_grid(int d)
@@ -1318,7 +1331,7 @@ private:
             }
             if (!eng_.wait64 || !eng_.write64) return MMA_ERR_NO_MEMOPS;
             Ring* r = nullptr;   // enqueue_rings gets the same ring and base
-            CK((cudaError_t)get_ring(j_.d, j_.dir, p, j_.C, eng_.cfg.ring_slots, &r));
+            CK((cudaError_t)get_ring(j_.d, j_.dir, p, j_.C, ring_slots_for(j_.C), &r));
             for (size_t c = 0; c < lists_[p].size() && c < 2 * (size_t)r->S; c++) {
                 cudaStream_t hs = L.hop[((r->g_next + c) % r->S) & 1];
                 CK((cudaError_t)use(hs, g));
@@ -1482,7 +1495,7 @@ private:
             return cudaSuccess;
         }
         if (!eng_.wait64 || !eng_.write64) return MMA_ERR_NO_MEMOPS;
-        const uint32_t S = eng_.cfg.ring_slots;
+        const uint32_t S = ring_slots_for(j_.C);
         std::vector<Ring*> rings(P_, nullptr);
         std::vector<uint64_t> g0(P_, 0);
         for (int p : rp) {

@@ -37,6 +37,7 @@ using PFN_batch_memop = CUresult (*)(CUstream, unsigned int, CUstreamBatchMemOpP
 // 4 MiB 52.6, 16 MiB 54.8 of the link's 55.6 (scripts/probe/probe_chunks.cu)
 constexpr uint64_t kDefaultChunk = 8ull << 20;
 constexpr unsigned kDefaultSlots = 4;
+constexpr uint64_t kRingBytes = 32ull << 20;   // staging per ring when cfg.ring_slots = 0
 constexpr uint32_t kDefaultMbps = 50000;
 // Claim unit of the relay and zero-copy kernels: a CTA claims, checks the flag, copies and
 // releases per unit, so small units pay that bookkeeping often. Relay kernel alone, 8 CTAs,
@@ -349,6 +350,7 @@ int validate_cfg(const mma_config_t& c);
 int make_device(int d);
 // grid of a zero-copy path kernel on device d (cfg.zc_ctas, capped at 4 CTAs per SM)
 uint64_t zc_grid(int d);
+uint32_t ring_slots_for(uint64_t C);   // the ring depth for chunks of C bytes
 int do_init(const mma_config_t* cfg);
 int ensure_init();
 void make_paths(int d);

@@ -26,8 +26,8 @@ cfg = mma.default_config(); cfg.fallback_bytes[0] = cfg.fallback_bytes[1] = (1 <
 nat = {d: B / timed(f) / 1e6 for d, f in (("h2d", lambda: mma.memcpy_h2d(dev, host, B, stream=s)),
                                           ("d2h", lambda: mma.memcpy_d2h(host, dev, B, stream=s)))}
 for kind, hop in (("kernel", mma.HOP_CE), ("ce_p2p", mma.HOP_CE_P2P)):
-  for C in (1 << 20, 2 << 20, 4 << 20, 8 << 20):
-    for S in (4, 8):
+  for C in [int(x) for x in os.environ.get("SWEEP_C", "1048576,2097152,4194304,8388608").split(",")]:
+    for S in [int(x) for x in os.environ.get("SWEEP_S", "4,8").split(",")]:
         cfg = mma.default_config()
         cfg.chunk_bytes[0] = cfg.chunk_bytes[1] = C
         cfg.ring_slots = S
