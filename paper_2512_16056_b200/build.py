@@ -54,16 +54,22 @@ def build(force: bool = False, verbose: bool = False) -> Path:
         return LIB
     objdir = PKG / "build"
     objdir.mkdir(exist_ok=True)
-    objs = []
+    cmds = []
     for src in SOURCES:
         obj = objdir / (src.stem + ".o")
         cmd = [NVCC, *FLAGS, "-c", str(src), "-o", str(obj)]
         if src.suffix == ".cpp":
             cmd = [NVCC, *FLAGS, "-x", "cu", "-c", str(src), "-o", str(obj)]
+        cmds.append((cmd, str(obj)))
+    # the translation units compile independently: in parallel (nvcc is single-threaded)
+    from concurrent.futures import ThreadPoolExecutor
+    def run(c):
         if verbose:
-            print(" ".join(cmd))
-        subprocess.check_call(cmd)
-        objs.append(str(obj))
+            print(" ".join(c[0]))
+        subprocess.check_call(c[0])
+        return c[1]
+    with ThreadPoolExecutor(max_workers=min(len(cmds), os.cpu_count() or 1)) as ex:
+        objs = list(ex.map(run, cmds))
     tmp = LIB.with_suffix(".so.tmp")
     subprocess.check_call([NVCC, "-shared", "-gencode", "arch=compute_100a,code=sm_100a",
                            "-cudart", "static", "-o", str(tmp), *objs, "-ldl", "-lpthread", "-lrt"])
