@@ -88,7 +88,8 @@ static MemRange query_range(uintptr_t p, uintptr_t end, void*)
 static int capture_state(cudaStream_t stream, int d)
 {
     cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
-    if (cudaStreamIsCapturing(stream, &cap) != cudaSuccess) {
+    unsigned long long id = 0;
+    if (cudaStreamGetCaptureInfo(stream, &cap, &id) != cudaSuccess) {
         cudaGetLastError();
         return -1;
     }
@@ -102,15 +103,17 @@ static int capture_state(cudaStream_t stream, int d)
             const DevRes& r = e.dev[p.gpu];
             if (!r.made) return -1;
             // another capture still holds the capture lanes (its user has not ended it yet):
-            // joining them would tie the two graphs together
+            // joining them would tie the two graphs together. Lanes already in THIS capture
+            // (an earlier call of the same graph) are fine.
             for (const Lanes& l : r.cap_lane)
                 for (cudaStream_t s : {l.kern, l.hop[0], l.hop[1], l.direct, l.zc}) {
                     cudaStreamCaptureStatus st = cudaStreamCaptureStatusNone;
-                    if (cudaStreamIsCapturing(s, &st) != cudaSuccess) {
+                    unsigned long long lid = 0;
+                    if (cudaStreamGetCaptureInfo(s, &st, &lid) != cudaSuccess) {
                         cudaGetLastError();
                         return -1;
                     }
-                    if (st != cudaStreamCaptureStatusNone) return -1;
+                    if (st != cudaStreamCaptureStatusNone && lid != id) return -1;
                 }
         }
     return 1;

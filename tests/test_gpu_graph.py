@@ -283,3 +283,29 @@ def test_second_open_capture_records_native(mma):
         torch.cuda.synchronize()
         assert torch.equal(d1.cpu(), s1[:B]) and torch.equal(d2.cpu(), s2[:B]), seed
     assert mma.get_last_error() == 0
+
+
+def test_two_calls_in_one_capture(mma):
+    """two multipath calls recorded into ONE graph both stay multipath (the capture lanes are
+    already in this capture after the first), and the graph replays both"""
+    configure(mma, loopback=1, chunk=MiB, debug=0)
+    _two_paths(mma, mma.H2D)
+    B = 10 * MiB + 4096
+    s1, s2 = pinned(torch, B, seed=91), pinned(torch, B, seed=92)
+    d1 = torch.zeros(B, dtype=torch.uint8, device="cuda")
+    d2 = torch.zeros(B, dtype=torch.uint8, device="cuda")
+    mma.memcpy_h2d(d1, s1, B)
+    torch.cuda.synchronize()
+    k0 = mma.get_stats(0)["kernels"]
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        mma.memcpy_h2d(d1, s1, B)
+        mma.memcpy_h2d(d2, s2, B)
+    assert mma.get_stats(0)["kernels"] == k0 + 2        # both captured as multipath copies
+    for seed in (93, 94):
+        mma_inputs.fill_pattern(s1.numpy()[:B], seed)
+        mma_inputs.fill_pattern(s2.numpy()[:B], seed + 7)
+        g.replay()
+        torch.cuda.synchronize()
+        assert torch.equal(d1.cpu(), s1[:B]) and torch.equal(d2.cpu(), s2[:B]), seed
+    assert mma.get_last_error() == 0
