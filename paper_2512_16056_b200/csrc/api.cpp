@@ -344,6 +344,7 @@ int mma_finalize(void)
         DeviceGuard dg(d);
         cudaDeviceSynchronize();
     }
+    mp_finalize();
     for (int d = 0; d < e.ndev; d++) {
         Target& t = e.tgt[d];
         for (int dir = 0; dir < 2; dir++)

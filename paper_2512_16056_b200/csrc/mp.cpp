@@ -155,6 +155,24 @@ int share_ring(int device, int dir, uint64_t C, uint32_t S, ShareRing** out)
 
 }  // namespace
 
+// mma_finalize: the share rings die with the engine (every device was synchronised)
+void mp_finalize()
+{
+    std::lock_guard<std::mutex> lk(g_mp_mu);
+    for (int d = 0; d < MMA_MAX_GPUS; d++)
+        for (ShareRing& r : g_share_ring[d]) {
+            if (!r.hop[0] && !r.stage) continue;
+            DeviceGuard g(d);
+            if (r.stage) cudaFree(r.stage);
+            for (int k = 0; k < 2; k++) {
+                if (r.hop[k]) cudaStreamDestroy(r.hop[k]);
+                if (r.done[k]) cudaEventDestroy(r.done[k]);
+            }
+            if (r.fork) cudaEventDestroy(r.fork);
+            r = ShareRing();
+        }
+}
+
 }  // namespace mma
 
 using namespace mma;

@@ -374,6 +374,7 @@ int shm_ledger_slot(int dev);   // -1 when detached; resolves the bus id (a CUDA
 void shm_ledger_add_slot(int dir, int slot, int64_t bytes, int64_t own, uint64_t gen);   // no CUDA calls
 int run_job(Job& j);
 int run_multi(std::vector<Job>& jobs);   // a joint plan of concurrent transfers (NEXT-1)
+void mp_finalize();                      // mp.cpp: free the copy-engine share rings
 int reserve_tables(const Job& j);
 int sticky();
 extern bool g_ktime;
