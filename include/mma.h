@@ -100,9 +100,9 @@ typedef struct {
     int debug_log;
     /* backlog ledger: plan each call against the bytes other in-flight
      * calls still have queued on every link ("remaining tasks in the buffer provide an
-     * effective proxy for link congestion", §2.3), and never relay through a GPU
-     * whose own link still carries its own target's direct bytes ("direct path first",
-     * P:564-565 §3.4.2). 0 = off, 1 = on (default). */
+     * effective proxy for link congestion", §2.3); a relay GPU whose own target's
+     * direct bytes are still in flight takes relay work only behind them ("direct path
+     * first", §3.4.2; R27). 0 = off, 1 = on (default). */
     int ledger;
     /* dynamic pull (plan_mode 2): bytes one CTA claims at a time; the delivery log has one
      * entry per claim. Small claims keep every link's share proportional to its speed
@@ -135,6 +135,14 @@ typedef struct {
      * bytes on its own GPU's node. Bytes are unchanged; mma_get_stats reports local bytes.
      * 0 = off, 1 = auto (default; inert on a one-node host). */
     int numa_plan;
+    /* Contention with background traffic (§3.4.2), dynamic pull only: 0 = keep
+     * claiming as soon as a unit is done ("maximize link utilization", default); 1 = yield to
+     * background traffic: a CTA whose last unit took longer than yield_pct percent of the
+     * unit time the path's bandwidth predicts ("blocked") waits that long before it claims
+     * again, so a link shared with other traffic carries less of the transfer and the other
+     * links more. mma_get_dynamic_backoffs counts the waits. */
+    int background_policy;
+    unsigned yield_pct;   /* 0 = default (150) */
 } mma_config_t;
 
 typedef struct {
@@ -336,6 +344,9 @@ int mma_get_delivery_log(int device, uint8_t* path_of_chunk, size_t cap, size_t*
  * byte. *nsegs = 0 after a contiguous or native call. cap < *nsegs -> cudaErrorInvalidValue. */
 int mma_get_segment_order(int device, uint32_t* order, size_t cap, size_t* nsegs);
 
+/* Waits taken by yielding CTAs (background_policy = 1) in the last dynamic-pull call to
+ * `device` (synchronises). */
+int mma_get_dynamic_backoffs(int device, uint64_t* waits);
 /* Chunks each path took in the most recent dynamic-pull call to/from `device`
  * (synchronises; *npaths = 0 if none). */
 int mma_get_dynamic_counts(int device, uint64_t* chunks, int cap, int* npaths);

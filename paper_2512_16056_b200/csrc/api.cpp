@@ -808,6 +808,24 @@ int mma_get_dynamic_counts(int device, uint64_t* chunks, int cap, int* npaths)
     return cudaSuccess;
 }
 
+int mma_get_dynamic_backoffs(int device, uint64_t* waits)
+{
+    CK((cudaError_t)ensure_init());
+    Engine& e = E();
+    if (device < 0 || device >= e.ndev) return cudaErrorInvalidDevice;
+    if (!waits) return cudaErrorInvalidValue;
+    std::lock_guard<std::mutex> g(e.mu);
+    Target& t = e.tgt[device];
+    *waits = 0;
+    if (!t.last_dyn) return cudaSuccess;
+    DeviceGuard dg(device);
+    CK(cudaDeviceSynchronize());
+    unsigned long long w = 0;
+    CK(cudaMemcpy(&w, t.last_dyn + kDynBackoffWord, sizeof w, cudaMemcpyDeviceToHost));
+    *waits = w;
+    return cudaSuccess;
+}
+
 int mma_get_last_error(void)
 {
     if (!E().inited) return cudaSuccess;

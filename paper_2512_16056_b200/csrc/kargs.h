@@ -64,6 +64,12 @@ struct DynLaunchArg {
     unsigned long long* counts;   // [MMA_KMAX_RINGS] chunks taken per path (same slot)
     uint32_t path;
     uint8_t* log;
+    // contention with background traffic: yield_pct > 0 -> a CTA whose unit took more
+    // than yield_pct % of expect_ns waits that long again before its next claim
+    uint64_t expect_ns;
+    uint32_t yield_pct;
+    unsigned long long* backoffs;   // waits taken (same claim slot)
+    unsigned long long* pause;      // this path's "no claims before" time (%globaltimer ns)
 };
 
 struct ZcLaunchArg {

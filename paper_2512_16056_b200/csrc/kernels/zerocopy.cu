@@ -45,6 +45,14 @@ __global__ void __launch_bounds__(kThreads) zc_copy_kernel(const __grid_constant
 // cursor (a peer atomic over NVLink for relays), moves it, and claims again. The claim for
 // the next chunk is issued before the current chunk is copied, so the ~2 us NVLink
 // round trip of the atomic overlaps the copy.
+//
+// Contention with background traffic (§3.4.2, background_policy = 1): "if
+// prioritizing background traffic is desired, the outstanding queue can wait for a period
+// after being blocked before fetching micro-tasks". A unit that took longer than yield_pct %
+// of what the path's rate predicts means the link is blocked; the CTA then pushes the whole
+// path's pause time to now + that unit's duration, and every CTA of the path waits for it
+// before its next claim -- the path's link carries less of the transfer (the other links'
+// CTAs keep claiming), and the background flow gets the link meanwhile.
 __global__ void __launch_bounds__(kThreads) zc_dyn_kernel(const __grid_constant__ DynLaunchArg A)
 {
     __shared__ unsigned long long s_next;
@@ -52,19 +60,35 @@ __global__ void __launch_bounds__(kThreads) zc_dyn_kernel(const __grid_constant_
     if (threadIdx.x == 0) s_next = atomicAdd_system(A.cursor, 1ull);
     __syncthreads();
     uint64_t i = s_next;
-    unsigned long long taken = 0;
+    unsigned long long taken = 0, waits = 0;
     while (i < A.nchunks) {
         __syncthreads();                                   // everyone has read s_next
-        if (threadIdx.x == 0) s_next = atomicAdd_system(A.cursor, 1ull);
+        uint64_t t0 = 0;
+        if (threadIdx.x == 0) {
+            s_next = atomicAdd_system(A.cursor, 1ull);
+            if (A.yield_pct) t0 = globaltimer_ns();
+        }
         const uint64_t off = i * C;
         const uint64_t len = (B - off < C) ? B - off : C;
         v_copy<V_DIRECT>(A.v, off, off + len, nullptr);
         if (threadIdx.x == 0 && A.log) A.log[i] = (uint8_t)A.path;
         taken++;
         __syncthreads();
+        if (threadIdx.x == 0 && A.yield_pct) {
+            const uint64_t now = globaltimer_ns(), dt = now - t0;
+            if (dt * 100 > A.expect_ns * (uint64_t)A.yield_pct)   // blocked: pause the path
+                atomicMax_system(A.pause, now + (dt < 1000000 ? dt : 1000000));
+            const uint64_t until = *(volatile unsigned long long*)A.pause;
+            if (globaltimer_ns() < until) {
+                waits++;
+                while (globaltimer_ns() < until) __nanosleep(1000);
+            }
+        }
+        __syncthreads();
         i = s_next;
     }
     if (threadIdx.x == 0 && taken) atomicAdd_system(&A.counts[A.path], taken);
+    if (threadIdx.x == 0 && waits && A.backoffs) atomicAdd_system(A.backoffs, waits);
 }
 
 cudaError_t launch_zc_dyn(const DynLaunchArg& a, unsigned grid, cudaStream_t s)

@@ -75,6 +75,8 @@ void apply_env(mma_config_t* c)
     c->calib_rounds = env_int("MMA_CALIB_ROUNDS", c->calib_rounds);
     c->host_order = env_int("MMA_HOST_ORDER", c->host_order);
     c->numa_plan = env_int("MMA_NUMA_PLAN", c->numa_plan);
+    c->background_policy = env_int("MMA_BACKGROUND", c->background_policy);
+    c->yield_pct = (unsigned)env_int("MMA_YIELD_PCT", (int)c->yield_pct);
     if (const char* s = getenv("MMA_PATHS")) {   // comma-separated relay GPU ids
         c->npaths = 0;
         for (const char* p = s; *p && c->npaths < MMA_MAX_PATHS;) {
@@ -104,6 +106,8 @@ void defaults(mma_config_t* c)
     c->calib_rounds = 2;
     c->host_order = 1;
     c->numa_plan = 1;
+    c->background_policy = 0;
+    c->yield_pct = 150;
 }
 
 int validate_cfg(const mma_config_t& c)
@@ -122,6 +126,7 @@ int validate_cfg(const mma_config_t& c)
     if (c.calib_rounds < 0 || c.calib_rounds > 16) return cudaErrorInvalidValue;
     if (c.host_order < 0 || c.host_order > 2) return cudaErrorInvalidValue;
     if (c.numa_plan < 0 || c.numa_plan > 1) return cudaErrorInvalidValue;
+    if (c.background_policy < 0 || c.background_policy > 1 || c.yield_pct > 100000) return cudaErrorInvalidValue;
     return cudaSuccess;
 }
 
@@ -1374,6 +1379,14 @@ private:
             a.nchunks = n_log_;
             a.cursor = slot;
             a.counts = slot + 1;
+            a.backoffs = slot + kDynBackoffWord;
+            a.pause = slot + kDynPauseWord + p;
+            if (eng_.cfg.background_policy == 1 && pp_[p].mbps) {   // yield to background traffic
+                a.yield_pct = eng_.cfg.yield_pct ? eng_.cfg.yield_pct : 150;
+                const uint64_t ctas = std::min<uint64_t>(n_log_, zc_grid(g));
+                // ns one claim unit takes when the path's measured rate is split over its CTAs
+                a.expect_ns = claimC_ * ctas * 1000ull / pp_[p].mbps;
+            }
             a.path = (uint32_t)p;
             a.log = log_;
             const unsigned grid = (unsigned)std::min<uint64_t>(n_log_, zc_grid(g));

@@ -48,7 +48,9 @@ constexpr int kDefaultRelayCtas = 8;
 constexpr uint64_t kDefaultGroupBytes = 8ull << 20;   // MMA_GROUP_BYTES (profiles/r02_sweep_group_lanes.jsonl)
 constexpr int kDefaultZcCtas = 16;     // zero-copy kernel grid (mma_config_t::zc_ctas): the link saturates from 4-8
 constexpr unsigned kDynSlots = 64;        // per-call claim slots, rotating
-constexpr unsigned kDynSlotWords = 32;    // cursor + counts[MMA_KMAX_RINGS] (+ padding)
+constexpr unsigned kDynSlotWords = 64;    // cursor, counts[MMA_KMAX_RINGS], backoffs, pause[MMA_KMAX_RINGS]
+constexpr unsigned kDynBackoffWord = 1 + MMA_KMAX_RINGS;
+constexpr unsigned kDynPauseWord = 2 + MMA_KMAX_RINGS;
 
 struct DeviceGuard {
     int prev = -1;

@@ -25,7 +25,8 @@ SYMBOLS = [
     "mma_memcpy_h2d_segments", "mma_memcpy_d2h_segments", "mma_get_paths", "mma_set_bandwidth",
     "mma_set_path_modes", "mma_calibrate", "mma_get_plan", "mma_plan_chunks",
     "mma_get_delivery_log", "mma_get_segment_order", "mma_plan_multi", "mma_memcpy_multi",
-    "mma_host_alloc_size", "mma_copy_share_segments_ring", "mma_ledger_process_add", "mma_host_alloc", "mma_host_free", "mma_get_stats",
+    "mma_host_alloc_size", "mma_copy_share_segments_ring", "mma_ledger_process_add",
+    "mma_get_dynamic_backoffs", "mma_host_alloc", "mma_host_free", "mma_get_stats",
     "mma_reset_stats", "mma_get_last_error", "mma_error_string", "mma_fill_pattern",
     "mma_verify_pattern", "mma_verify_segments", "mma_set_kernel_timing", "mma_kernel_times",
     "mma_tune_segments", "mma_get_segment_tuning", "mma_get_dynamic_counts", "mma_set_plan_mode",
@@ -56,6 +57,8 @@ class Config(C.Structure):
         ("calib_rounds", C.c_int),
         ("host_order", C.c_int),
         ("numa_plan", C.c_int),
+        ("background_policy", C.c_int),
+        ("yield_pct", C.c_uint),
     ]
 
 
@@ -125,6 +128,7 @@ def lib():
         L.mma_get_segment_order.argtypes = [C.c_int, vp, sz, C.POINTER(sz)]
         L.mma_memcpy_multi.argtypes = [C.POINTER(Transfer), sz]
         L.mma_host_alloc_size.argtypes = [vp, C.POINTER(sz)]
+        L.mma_get_dynamic_backoffs.argtypes = [C.c_int, C.POINTER(C.c_uint64)]
         L.mma_copy_share_segments_ring.argtypes = [C.POINTER(Segment), sz, sz, vp, sz, C.c_int, C.c_int, C.c_uint, vp]
         L.mma_plan_multi.argtypes = [C.c_int, vp, vp, C.c_int, vp, vp, C.c_uint64, C.c_int, vp]
         L.mma_host_alloc.argtypes = [C.POINTER(vp), sz, C.c_uint]
@@ -485,6 +489,13 @@ def get_dynamic_counts(device: int):
     n = C.c_int()
     _check(lib().mma_get_dynamic_counts(device, buf, MAX_PATHS, C.byref(n)), "mma_get_dynamic_counts")
     return [int(buf[i]) for i in range(n.value)]
+
+
+def get_dynamic_backoffs(device: int) -> int:
+    """Waits yielding CTAs took in the last dynamic-pull call (background_policy = 1)."""
+    n = C.c_uint64()
+    _check(lib().mma_get_dynamic_backoffs(device, C.byref(n)), "mma_get_dynamic_backoffs")
+    return int(n.value)
 
 
 def reset_stats(device: int) -> None:

@@ -91,3 +91,27 @@ def test_dynamic_needs_all_zero_copy(mma):
     torch.cuda.synchronize()
     assert mma.get_stats(0)["dynamic_calls"] == 0
     assert torch.equal(dst.cpu(), src[:8 * MiB])
+
+
+@pytest.mark.parametrize("policy", [0, 1], ids=["maximize", "yield"])
+def test_background_policy_mechanism(mma, orc, policy):
+    """P:574 contention with background traffic: with background_policy = 1 a CTA whose unit
+    took longer than the path's bandwidth predicts waits before claiming again. Pinning an
+    absurdly high bandwidth makes every unit look "blocked": the yield policy must then wait
+    (and still move every byte exactly once); the default policy never waits."""
+    cfg = configure(mma, loopback=1, chunk=MiB, plan_mode=2, hop=(2, 2), claim=256 << 10)
+    cfg.background_policy = policy
+    mma.init(cfg)
+    mma.set_bandwidth(0, mma.H2D, [10_000_000, 10_000_000])
+    B = 32 * MiB + 99
+    src = pinned(torch, B, seed=17)
+    dst = guarded_device(torch, B)
+    mma.memcpy_h2d(dst[G:G + B], src, B)
+    torch.cuda.synchronize()
+    log = np.frombuffer(mma.get_delivery_log(0), dtype=np.uint8)
+    assert set(log.tolist()) <= {0, 1}
+    exp = guarded_host(B)
+    assert orc.move_contiguous(exp[G:G + B], src.numpy()[:B], 256 << 10, [1, 1], log.copy(), S=2) == 0
+    assert np.array_equal(dst.cpu().numpy(), exp)
+    waits = mma.get_dynamic_backoffs(0)
+    assert (waits > 0) if policy else (waits == 0), waits
