@@ -143,6 +143,10 @@ typedef struct {
      * links more. mma_get_dynamic_backoffs counts the waits. */
     int background_policy;
     unsigned yield_pct;   /* 0 = default (150) */
+    /* Relay task scheduling of joint plans (mma_memcpy_multi; §3.4.2): 0 = longest
+     * micro-task queue first (default); g + 1 = GPU g's queue first ("prioritize data
+     * transfer for a specific GPU"), then longest first. A link's own queue always first. */
+    int relay_prefer;
 } mma_config_t;
 
 typedef struct {
@@ -327,11 +331,14 @@ int mma_plan_chunks(const uint32_t* mbps, const int* kinds, const uint64_t* back
  *   target[t], nchunks[t]         transfers
  *   mode                          MMA plan mode: 0 contiguous (per transfer, own link's range
  *                                 first, then the other links by id), 1 interleaved (as pulled)
+ *   prefer                        -1, or an endpoint whose queue links relay first (P:569:
+ *                                 "tasks can be preferentially fetched from the corresponding
+ *                                 micro-task queue"; the own queue still comes first)
  *   link_of_chunk                 out: sum(nchunks) link ids, transfer after transfer
  * cudaErrorInvalidValue: bad arguments, or a transfer no link may carry. */
 int mma_plan_multi(int nlinks, const uint32_t* link_mbps, const uint8_t* carry, int ntransfers,
                    const int* target, const uint64_t* nchunks, uint64_t chunk_bytes, int mode,
-                   int32_t* link_of_chunk);
+                   int prefer, int32_t* link_of_chunk);
 
 /* Debug: the path that delivered each chunk of the most recent multipath copy to/from
  * `device`, as written on the GPU by the final hop (needs cfg.debug_log; synchronises). */

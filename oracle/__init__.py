@@ -65,7 +65,7 @@ def lib():
                                        C.c_uint32, C.c_void_p]
         L.orc_ring_explore.argtypes = [C.c_int, C.c_int, u64, C.c_int, p(u64), p(u64)]
         L.orc_plan_multi.argtypes = [C.c_int, C.c_void_p, C.c_void_p, C.c_int, C.c_void_p, C.c_void_p, u64,
-                                     C.c_int, C.c_void_p]
+                                     C.c_int, C.c_int, C.c_void_p]
         L.orc_numa_order.argtypes = [C.c_void_p, u64, p(Path_), C.c_void_p, C.c_int, C.c_void_p]
         _lib = L
     return _lib
@@ -81,7 +81,7 @@ def make_paths(bw, kinds=None, backlog=None):
     return arr
 
 
-def plan_multi(link_bw, relay_ok, targets, nchunks, C_, mode=INTERLEAVED):
+def plan_multi(link_bw, relay_ok, targets, nchunks, C_, mode=INTERLEAVED, prefer=-1):
     """Joint pull plan of concurrent transfers (NEXT-1). relay_ok: L x L 0/1
     (row = endpoint GPU, column = link). Returns (rc, list of per-transfer link arrays)."""
     L = len(link_bw)
@@ -91,7 +91,7 @@ def plan_multi(link_bw, relay_ok, targets, nchunks, C_, mode=INTERLEAVED):
     nc = np.ascontiguousarray(nchunks, dtype=np.uint64)
     out = np.full(max(1, int(nc.sum())), -1, dtype=np.int32)
     rc = lib().orc_plan_multi(L, bw.ctypes.data, ok.ctypes.data, len(tg), tg.ctypes.data, nc.ctypes.data,
-                              C_, mode, out.ctypes.data)
+                              C_, mode, prefer, out.ctypes.data)
     offs = np.concatenate([[0], np.cumsum(nc)]).astype(np.int64)
     return rc, [out[offs[t]:offs[t + 1]].copy() for t in range(len(tg))]
 

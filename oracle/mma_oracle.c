@@ -123,7 +123,7 @@ static int may_carry(int L, const uint8_t* relay_ok, int d, int l)
 
 int orc_plan_multi(int L, const uint32_t* link_bw, const uint8_t* relay_ok, int T,
                    const int32_t* target, const uint64_t* nchunks, uint64_t C, int mode,
-                   int32_t* link_of_chunk)
+                   int prefer, int32_t* link_of_chunk)
 {
     if (L < 1 || L > 128 || T < 0 || !link_bw || !relay_ok || (T && (!target || !nchunks)) || C == 0)
         return ORC_EINVAL;
@@ -171,6 +171,8 @@ int orc_plan_multi(int L, const uint32_t* link_bw, const uint8_t* relay_ok, int 
         /* what it takes: its own queue first, else the longest queue it may relay for */
         int q = -1;
         if (left[best] > 0) q = best;
+        else if (prefer >= 0 && prefer < L && prefer != best && left[prefer] > 0 && may_carry(L, relay_ok, prefer, best))
+            q = prefer;                                      /* the preferred GPU's queue */
         else
             for (int d = 0; d < L; d++)
                 if (d != best && left[d] > 0 && may_carry(L, relay_ok, d, best) && (q < 0 || left[d] > left[q])) q = d;

@@ -129,7 +129,9 @@ int orc_move(const orc_segment* segs, uint64_t nsegs, uint64_t C,
  *   corresponding to each GPU always has priority in fetching transfer tasks from the
  *   associated Mico-task Queue"), else
  *   the head of the longest queue it may relay for ("prioritizing tasks from the longest
- *   micro-task queue"; ties -> lower GPU id),
+ *   micro-task queue"; ties -> lower GPU id) -- or, with prefer >= 0,
+ *   GPU prefer's queue first when it is non-empty and the link may carry it ("tasks can be
+ *   preferentially fetched from the corresponding micro-task queue"; SPEC PreferGpu),
  * and a link with nothing it may take drops out (queues only shrink).
  *   L                  links (ids 0..L-1; a GPU's own link has the GPU's id), L <= 128
  *   link_bw[l]         MB/s; 0 = absent
@@ -143,7 +145,7 @@ int orc_move(const orc_segment* segs, uint64_t nsegs, uint64_t C,
  */
 int orc_plan_multi(int L, const uint32_t* link_bw, const uint8_t* relay_ok, int T,
                    const int32_t* target, const uint64_t* nchunks, uint64_t C, int mode,
-                   int32_t* link_of_chunk);
+                   int prefer, int32_t* link_of_chunk);
 
 /*
  * NUMA-affine order of a scattered transfer's segments (reading R23): the

@@ -645,7 +645,7 @@ int mma_plan_chunks(const uint32_t* mbps, const int* kinds, const uint64_t* back
 
 int mma_plan_multi(int nlinks, const uint32_t* link_mbps, const uint8_t* carry, int ntransfers,
                    const int* target, const uint64_t* nchunks, uint64_t chunk_bytes, int mode,
-                   int32_t* link_of_chunk)
+                   int prefer, int32_t* link_of_chunk)
 {
     if (nlinks < 1 || nlinks > 128 || ntransfers < 0 || !link_mbps || !carry ||
         (ntransfers && (!target || !nchunks || !link_of_chunk)))
@@ -658,7 +658,7 @@ int mma_plan_multi(int nlinks, const uint32_t* link_mbps, const uint8_t* carry, 
     std::vector<int> tg(target, target + ntransfers);
     std::vector<uint64_t> nc(nchunks, nchunks + ntransfers);
     std::vector<std::vector<int>> out;
-    if (make_plan_multi(links, ok, tg, nc, chunk_bytes, mode, out)) return cudaErrorInvalidValue;
+    if (make_plan_multi(links, ok, tg, nc, chunk_bytes, mode, out, prefer)) return cudaErrorInvalidValue;
     size_t i = 0;
     for (const auto& v : out)
         for (int l : v) link_of_chunk[i++] = l;

@@ -77,6 +77,7 @@ void apply_env(mma_config_t* c)
     c->numa_plan = env_int("MMA_NUMA_PLAN", c->numa_plan);
     c->background_policy = env_int("MMA_BACKGROUND", c->background_policy);
     c->yield_pct = (unsigned)env_int("MMA_YIELD_PCT", (int)c->yield_pct);
+    c->relay_prefer = env_int("MMA_RELAY_PREFER", c->relay_prefer);
     if (const char* s = getenv("MMA_PATHS")) {   // comma-separated relay GPU ids
         c->npaths = 0;
         for (const char* p = s; *p && c->npaths < MMA_MAX_PATHS;) {
@@ -127,6 +128,7 @@ int validate_cfg(const mma_config_t& c)
     if (c.host_order < 0 || c.host_order > 2) return cudaErrorInvalidValue;
     if (c.numa_plan < 0 || c.numa_plan > 1) return cudaErrorInvalidValue;
     if (c.background_policy < 0 || c.background_policy > 1 || c.yield_pct > 100000) return cudaErrorInvalidValue;
+    if (c.relay_prefer < 0 || c.relay_prefer > MMA_MAX_GPUS) return cudaErrorInvalidValue;
     return cudaSuccess;
 }
 
@@ -1910,7 +1912,8 @@ int run_multi(std::vector<Job>& jobs)
         if (idx.empty()) continue;
         const int mode = e.cfg.plan_mode == PLAN_INTERLEAVED ? PLAN_INTERLEAVED : PLAN_CONTIGUOUS;
         std::vector<std::vector<int>> lk;
-        if (make_plan_multi(links, carry, target, nchunks, jobs[idx[0]].C, mode, lk)) return cudaErrorInvalidValue;
+        const int prefer = e.cfg.relay_prefer > 0 ? e.cfg.relay_prefer - 1 : -1;
+        if (make_plan_multi(links, carry, target, nchunks, jobs[idx[0]].C, mode, lk, prefer)) return cudaErrorInvalidValue;
         for (size_t k = 0; k < idx.size(); k++) {
             Job& j = jobs[idx[k]];
             const auto& ps = e.tgt[j.d].paths[dir];

@@ -90,7 +90,7 @@ int make_plan(const PlanPath* paths, int npaths, uint64_t B, uint64_t C, uint64_
 // transfers. Queue lengths are few (<= the link count), so the longest is found by a scan.
 int make_plan_multi(const std::vector<MultiLink>& links, const std::vector<std::vector<uint8_t>>& carry,
                     const std::vector<int>& target, const std::vector<uint64_t>& nchunks, uint64_t C, int mode,
-                    std::vector<std::vector<int>>& link_of_chunk)
+                    std::vector<std::vector<int>>& link_of_chunk, int prefer)
 {
     const int L = (int)links.size(), T = (int)target.size();
     if (L < 1 || L > 128 || C == 0 || (int)nchunks.size() != T || (int)carry.size() != L) return -22;
@@ -128,6 +128,7 @@ int make_plan_multi(const std::vector<MultiLink>& links, const std::vector<std::
         const int l = k.idx;
         int d = -1;
         if (q[l].left) d = l;   // direct path first
+        else if (prefer >= 0 && prefer < L && prefer != l && q[prefer].left && may(prefer, l)) d = prefer;
         else
             for (int e = 0; e < L; e++)   // longest queue it may relay for; ties: lower id
                 if (e != l && q[e].left && may(e, l) && (d < 0 || q[e].left > q[d].left)) d = e;

@@ -32,13 +32,15 @@ int make_plan(const PlanPath* paths, int npaths, uint64_t B, uint64_t C, uint64_
 // to it; the link free first pulls its own endpoint's queue head ("direct path first",
 // P:564-565), else the head of the longest queue it may relay for (ties to the lower
 // id). links: rate per link id (0 = absent); carry(d, l): may link l carry chunks of endpoint d
-// (its own queue always). Output: for each transfer, the link id of each chunk; contiguous
+// (its own queue always). prefer >= 0: a link with an empty own queue takes endpoint
+// prefer's head first when it may ("tasks can be preferentially fetched from the
+// corresponding micro-task queue"). Output: for each transfer, the link id of each chunk; contiguous
 // mode lays each transfer's per-link counts out as ranges, own link first, then by link id.
 struct MultiLink {
     uint32_t mbps;
 };
 int make_plan_multi(const std::vector<MultiLink>& links, const std::vector<std::vector<uint8_t>>& carry,
                     const std::vector<int>& target, const std::vector<uint64_t>& nchunks, uint64_t C, int mode,
-                    std::vector<std::vector<int>>& link_of_chunk);
+                    std::vector<std::vector<int>>& link_of_chunk, int prefer = -1);
 
 }  // namespace mma

@@ -59,6 +59,7 @@ class Config(C.Structure):
         ("numa_plan", C.c_int),
         ("background_policy", C.c_int),
         ("yield_pct", C.c_uint),
+        ("relay_prefer", C.c_int),
     ]
 
 
@@ -130,7 +131,7 @@ def lib():
         L.mma_host_alloc_size.argtypes = [vp, C.POINTER(sz)]
         L.mma_get_dynamic_backoffs.argtypes = [C.c_int, C.POINTER(C.c_uint64)]
         L.mma_copy_share_segments_ring.argtypes = [C.POINTER(Segment), sz, sz, vp, sz, C.c_int, C.c_int, C.c_uint, vp]
-        L.mma_plan_multi.argtypes = [C.c_int, vp, vp, C.c_int, vp, vp, C.c_uint64, C.c_int, vp]
+        L.mma_plan_multi.argtypes = [C.c_int, vp, vp, C.c_int, vp, vp, C.c_uint64, C.c_int, C.c_int, vp]
         L.mma_host_alloc.argtypes = [C.POINTER(vp), sz, C.c_uint]
         L.mma_host_free.argtypes = [vp]
         L.mma_get_stats.argtypes = [C.c_int, C.POINTER(Stats)]
@@ -425,7 +426,7 @@ def get_delivery_log(device: int):
     return bytes(buf[: n.value])
 
 
-def plan_multi(link_mbps, carry, targets, nchunks, chunk: int, mode: int = 0):
+def plan_multi(link_mbps, carry, targets, nchunks, chunk: int, mode: int = 0, prefer: int = -1):
     """The joint planner alone (mma_plan_multi): per transfer, the link id of each chunk."""
     import numpy as np
     L = len(link_mbps)
@@ -435,7 +436,7 @@ def plan_multi(link_mbps, carry, targets, nchunks, chunk: int, mode: int = 0):
     nc = np.ascontiguousarray(nchunks, dtype=np.uint64)
     out = np.full(max(1, int(nc.sum())), -1, dtype=np.int32)
     rc = lib().mma_plan_multi(L, bw.ctypes.data, ok.ctypes.data, len(tg), tg.ctypes.data, nc.ctypes.data, chunk,
-                              mode, out.ctypes.data)
+                              mode, prefer, out.ctypes.data)
     offs = np.concatenate([[0], np.cumsum(nc)]).astype(np.int64)
     return rc, [out[offs[t]:offs[t + 1]].copy() for t in range(len(tg))]
 

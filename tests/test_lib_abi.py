@@ -125,8 +125,9 @@ def test_multi_planner_parity_random(orc, mode):
         targets = [int(x) for x in rng.integers(0, L, T)]
         nch = [int(x) for x in rng.integers(0, 300, T)]
         C = int(rng.choice([4096, 1 << 20, 8 << 20]))
-        orc_rc, orc_plans = orc.plan_multi(bw, ok, targets, nch, C, mode)
-        rc, plans = mma.plan_multi(bw, ok, targets, nch, C, mode)
+        prefer = int(rng.integers(-1, L)) if rng.random() < 0.3 else -1
+        orc_rc, orc_plans = orc.plan_multi(bw, ok, targets, nch, C, mode, prefer)
+        rc, plans = mma.plan_multi(bw, ok, targets, nch, C, mode, prefer)
         assert (rc == 0) == (orc_rc == 0), (case, bw, ok.tolist(), targets, nch)
         if rc == 0:
             for a, b in zip(plans, orc_plans):

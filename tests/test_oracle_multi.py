@@ -91,3 +91,19 @@ def test_valid_plan(L, data):
             order = own + [l for l in range(L) if l != d]
             ranks = [order.index(x) for x in cp.tolist()]
             assert ranks == sorted(ranks)                               # own link first, then by id
+
+
+def test_prefer_gpu():
+    """P:569 "tasks can be preferentially fetched from the corresponding micro-task queue"
+    (SPEC PreferGpu: the named queue when non-empty, then LongestQueueFirst). Same batch as
+    test_spec_longest_queue, GPU 0 preferred: link 2 drains GPU 0's queue (3 left after link
+    0's first pull) before it turns to the longer queue of GPU 1; the links' own queues still
+    come first."""
+    ok = [[0, 0, 1], [0, 0, 1], [0, 0, 0]]
+    rc, (a, b) = oracle.plan_multi([1, 1, 1000], ok, [0, 1], [4, 9], 1, I, prefer=0)
+    assert rc == 0
+    assert a.tolist() == [0, 2, 2, 2] and b.tolist() == [1] + [2] * 8
+    # preferring a GPU the link may not carry changes nothing
+    rc, (a2, b2) = oracle.plan_multi([1, 1, 1000], [[0, 0, 0], [0, 0, 1], [0, 0, 0]], [0, 1], [4, 9], 1, I, prefer=0)
+    rc3, (a3, b3) = oracle.plan_multi([1, 1, 1000], [[0, 0, 0], [0, 0, 1], [0, 0, 0]], [0, 1], [4, 9], 1, I)
+    assert a2.tolist() == a3.tolist() and b2.tolist() == b3.tolist()
