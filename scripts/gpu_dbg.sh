@@ -1,6 +1,10 @@
 #!/bin/bash
 mkdir -p gpurun_out/r02
-export MMA_SPIN_TIMEOUT_MS=8000
-timeout 900 python -m pytest tests/test_gpu_dynamic.py -q -x > gpurun_out/r02/l_dyn.log 2>&1; echo "rc=$?" >> gpurun_out/r02/l_dyn.log
-timeout 600 python scripts/probe_background.py > gpurun_out/r02/probe_background.jsonl 2>&1
-tail -5 gpurun_out/r02/l_dyn.log; cat gpurun_out/r02/probe_background.jsonl
+timeout 1200 python bench.py --workload wake --steps 3 --warmup 3 > gpurun_out/r02/m_wake.json 2> gpurun_out/r02/m_wake.err
+timeout 900 python bench.py --workload contention --steps 3 --warmup 3 > gpurun_out/r02/m_contention.json 2> gpurun_out/r02/m_contention.err
+timeout 1500 python scripts/sweep_sizes.py > gpurun_out/r02/m_sweep_sizes.jsonl 2> gpurun_out/r02/m_sweep_sizes.err
+for f in gpurun_out/r02/m_wake.json gpurun_out/r02/m_contention.json; do python -c "
+import json
+d=json.loads(open('$f').read().strip().splitlines()[-1])
+print('$f', d.get('value'), d.get('ms_per_step'), d.get('native'), d.get('per_call_ledger'), d.get('error'))"; done
+wc -l gpurun_out/r02/m_sweep_sizes.jsonl; tail -3 gpurun_out/r02/m_sweep_sizes.err
