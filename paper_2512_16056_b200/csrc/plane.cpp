@@ -679,7 +679,8 @@ public:
             ~CaptureFlag() { tl_capturing = false; }
         } cflag(j_.capturing);
         int rc = begin();
-        if (rc != cudaSuccess || done_) return rc;
+        if (rc != cudaSuccess) return forked_ ? end(rc) : rc;   // a failure after the fork still joins
+        if (done_) return rc;
         rc = enqueue_side(false);
         if (rc == cudaSuccess) rc = enqueue_side(true);
         return end(rc);
