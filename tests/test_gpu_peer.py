@@ -244,3 +244,40 @@ def test_joint_plan_two_targets(mma, orc, mode, hop):
         assert orc.move_contiguous(exp[G:G + sizes[t]], srcs[t].numpy()[:sizes[t]], MiB, [1, 1], path, S=3) == 0
         assert np.array_equal(dsts[t].cpu().numpy(), exp), t
         assert mma.get_delivery_log(t) == path.tobytes(), t
+
+
+def test_relay_behind_its_own_direct_work(mma, orc):
+    """R27: GPU 1 still has its own direct transfer in flight (held behind a
+    sleeping kernel on its stream). A call to GPU 0 plans its relay through GPU 1 behind that
+    backlog -- the oracle's earliest-finish plan with the ledger's bytes as backlog, not an
+    exclusion -- and its relay work waits for GPU 1's own work; all bytes exact."""
+    configure(mma, loopback=0, chunk=MiB, slots=4, plan_mode=1, hop=(CE, CE), paths=[0, 1])
+    for t in (0, 1):
+        mma.set_bandwidth(t, 0, [1, 1])
+    Bown = 32 * MiB
+    own_src = pinned(torch, Bown, seed=71)
+    own_dst = torch.zeros(Bown, dtype=torch.uint8, device="cuda:1")
+    s1 = torch.cuda.Stream(device=1)
+    torch.cuda.synchronize(1)
+    mma.reset_stats(1)
+    with torch.cuda.device(1), torch.cuda.stream(s1):
+        torch.cuda._sleep(1_000_000_000)                  # ~0.5 s: GPU 1's own call stays queued
+    mma.memcpy_h2d(own_dst, own_src, Bown, stream=s1)
+    B = 24 * MiB
+    st = mma.get_stats(1)
+    # the in-flight call's bytes per link: its direct share on GPU 1's link, its relay share
+    # (through GPU 0) on GPU 0's link
+    on_link1, on_link0 = st["path_bytes"][0][0], st["path_bytes"][0][1]
+    exp_plan = orc.plan([1, 1], B, MiB, 0, orc.INTERLEAVED, backlog=[on_link0, on_link1])[1]
+    assert mma.get_plan(0, 0, B)[0] == exp_plan.tobytes()
+    src = pinned(torch, B, seed=72)
+    dst = guarded_device(torch, B, dev=0)
+    torch.cuda.synchronize(0)
+    mma.memcpy_h2d(dst[G:G + B], src, B)
+    torch.cuda.synchronize(0)
+    torch.cuda.synchronize(1)
+    exp = guarded_host(B)
+    assert orc.move_contiguous(exp[G:G + B], src.numpy()[:B], MiB, [1, 1], exp_plan, S=4) == 0
+    assert np.array_equal(dst.cpu().numpy(), exp)
+    assert mma.get_delivery_log(0) == exp_plan.tobytes()
+    assert torch.equal(own_dst.cpu(), own_src[:Bown])
