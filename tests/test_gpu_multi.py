@@ -143,3 +143,56 @@ def test_invalid_transfer_enqueues_nothing(mma):
     assert bool((dst == 0xA5).all().item())
     with pytest.raises(mma.MMAError):
         mma.memcpy_multi([(mma.H2D, 7, mma.make_segments([src.data_ptr()], [dst.data_ptr()], [B]), 0)])
+
+
+def test_random_batches(mma, orc):
+    """randomised joint batches on one GPU: 1-4 transfers (mixed directions, contiguous or
+    scattered, ragged sizes), random path modes, bandwidths and plan modes; every byte
+    exact, and the last transfer's delivery log equal to the oracle's joint plan"""
+    import os
+    rng = np.random.default_rng(int(os.environ.get("MMA_RANDOM_SEED", "77")))
+    KiB = 1 << 10
+    pool_h = pinned(torch, 40 * MiB, seed=5)
+    pool_d = torch.empty(40 * MiB, dtype=torch.uint8, device="cuda")
+    pool_d.copy_(pool_h[:40 * MiB])
+    for case in range(int(os.environ.get("MMA_MULTI_CASES", "60"))):
+        lb = int(rng.integers(1, 4))
+        mode = int(rng.integers(0, 2))
+        configure(mma, loopback=lb, chunk=MiB, slots=int(rng.integers(1, 5)), plan_mode=mode, hop=(0, 0))
+        bw = [int(x) for x in rng.integers(1, 6, 1 + lb)]
+        for d in (mma.H2D, mma.D2H):
+            mma.set_path_modes(0, d, [int(x) for x in rng.choice([1, 2, 3], 1 + lb)])
+            mma.set_bandwidth(0, d, bw)
+        T = int(rng.integers(1, 5))
+        xf, checks = [], []
+        for t in range(T):
+            dirn = int(rng.integers(0, 2))
+            nseg = 1 if rng.random() < 0.5 else int(rng.integers(2, 60))
+            lens = rng.integers(1, 200 * KiB, nseg) if nseg > 1 else np.array([int(rng.integers(1, 12 * MiB))])
+            src_off = rng.integers(0, 20 * MiB, nseg)
+            span = int(lens.sum()) + 64 * nseg
+            dst_off = np.concatenate([[0], np.cumsum(lens[:-1] + 64)]).astype(np.int64)
+            if dirn == 0:
+                dst = torch.full((span,), 0xA5, dtype=torch.uint8, device="cuda")
+                segs = mma.make_segments(pool_h.data_ptr() + src_off, dst.data_ptr() + dst_off, lens)
+            else:
+                dst = torch.full((span,), 0xA5, dtype=torch.uint8).pin_memory()
+                segs = mma.make_segments(pool_d.data_ptr() + src_off, dst.data_ptr() + dst_off, lens)
+            xf.append((dirn, 0, segs, torch.cuda.Stream()))
+            checks.append((dirn, dst, src_off, dst_off, lens, span))
+        torch.cuda.synchronize()
+        mma.memcpy_multi(xf)
+        torch.cuda.synchronize()
+        assert mma.get_last_error() == 0, case
+        hn = pool_h.numpy()
+        for dirn, dst, src_off, dst_off, lens, span in checks:
+            got = dst.cpu().numpy() if dirn == 0 else dst.numpy()
+            exp = np.full(span, 0xA5, np.uint8)
+            for so, do_, ln in zip(src_off, dst_off, lens):
+                exp[do_:do_ + ln] = hn[so:so + ln]
+            assert np.array_equal(got, exp), (case, dirn, len(lens))
+        # the last transfer's executed route = its part of the oracle's joint plan
+        last_dir = checks[-1][0]
+        nch = [(int(c[4].sum()) + MiB - 1) // MiB for c in checks if c[0] == last_dir]
+        plans = _oracle_paths(orc, bw, nch, mode)
+        assert mma.get_delivery_log(0) == plans[-1].tobytes(), case
