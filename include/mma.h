@@ -344,6 +344,16 @@ int mma_plan_multi(int nlinks, const uint32_t* link_mbps, const uint8_t* carry, 
  * `device`, as written on the GPU by the final hop (needs cfg.debug_log; synchronises). */
 int mma_get_delivery_log(int device, uint8_t* path_of_chunk, size_t cap, size_t* nchunks);
 
+/* Debug (cfg.debug_log): what the relay kernels observed before moving each chunk of the
+ * most recent multipath copy to/from `device` -- the GPU-side evidence of the north_star
+ * invariant "a chunk is forwarded only after its staging write completes". For
+ * chunk i carried by a kernel-driven ring: H2D (pull) observed[i] = the seq value the kernel
+ * read before pulling the slot, expected[i] = g + 1 (they must be equal); D2H (pack)
+ * observed[i] = the credit value it read before overwriting the slot, expected[i] = g + 1,
+ * and observed[i] >= expected[i] - S must hold (0 when the slot had never been used).
+ * Chunks no relay kernel moved: both 0. Synchronises. */
+int mma_get_forward_log(int device, uint64_t* observed, uint64_t* expected, size_t cap, size_t* nchunks);
+
 /* Debug (cfg.debug_log): the order of the segments in the virtual stream v of the last
  * scattered call to `device` -- order[k] = table index of v's k-th segment. It is the table
  * order unless the call was regrouped by host NUMA node (reading R23, §5.1.1; the

@@ -17,7 +17,7 @@ from .mma import (  # noqa: F401
     ipc_close, copy_share_segments, copy_claim_segments, trace_begin, trace_end,
     save_calibration, load_calibration, host_alloc_for, host_page_node, get_calibration, tune_threshold,
     ledger_attach, ledger_unlink, ledger_shared_add, ledger_shared_get, device_bus_id, get_topology,
-    order_by_address, tune_chunk, get_segment_order, plan_multi, memcpy_multi, host_alloc_size, copy_share_segments_ring, ledger_process_add, get_dynamic_backoffs,
+    order_by_address, tune_chunk, get_segment_order, plan_multi, memcpy_multi, host_alloc_size, copy_share_segments_ring, ledger_process_add, get_dynamic_backoffs, get_forward_log,
 )
 
 try:

@@ -351,6 +351,7 @@ int mma_finalize(void)
             for (int p = 0; p < MMA_MAX_PATHS; p++) free_ring(t.rings[dir][p]);
         if (t.log) { DeviceGuard dg(d); cudaFree(t.log); }
         if (t.dyn) { DeviceGuard dg(d); cudaFree(t.dyn); }
+        if (t.fwd) { DeviceGuard dg(d); cudaFree(t.fwd); }
         for (auto& sc : t.scratch) {
             for (int g2 = 0; g2 < MMA_MAX_GPUS; g2++)
                 if (sc.dev[g2]) { DeviceGuard dg(g2); cudaFree(sc.dev[g2]); }
@@ -679,6 +680,28 @@ int mma_get_delivery_log(int device, uint8_t* path_of_chunk, size_t cap, size_t*
     DeviceGuard dg(device);
     CK(cudaDeviceSynchronize());
     CK(cudaMemcpy(path_of_chunk, t.log, t.log_n, cudaMemcpyDeviceToHost));
+    return cudaSuccess;
+}
+
+int mma_get_forward_log(int device, uint64_t* observed, uint64_t* expected, size_t cap, size_t* nchunks)
+{
+    CK((cudaError_t)ensure_init());
+    Engine& e = E();
+    if (device < 0 || device >= e.ndev) return cudaErrorInvalidDevice;
+    if (!nchunks) return cudaErrorInvalidValue;
+    std::lock_guard<std::mutex> g(e.mu);
+    Target& t = e.tgt[device];
+    *nchunks = t.fwd_n;
+    if (!t.fwd_n || (!observed && !expected)) return cudaSuccess;
+    if (cap < t.fwd_n) return cudaErrorInvalidValue;
+    DeviceGuard dg(device);
+    CK(cudaDeviceSynchronize());
+    std::vector<uint64_t> w(2 * t.fwd_n);
+    CK(cudaMemcpy(w.data(), t.fwd, w.size() * 8, cudaMemcpyDeviceToHost));
+    for (size_t i = 0; i < t.fwd_n; i++) {
+        if (observed) observed[i] = w[2 * i];
+        if (expected) expected[i] = w[2 * i + 1];
+    }
     return cudaSuccess;
 }
 

@@ -50,6 +50,11 @@ struct RelayLaunchArg {
     uint32_t nrings;
     uint32_t unit_bytes;         // bytes of one claimable unit (a chunk has ceil(C/U))
     uint8_t* log;                // delivery log [n] (device) or nullptr
+    // forward log (debug; SURVEY §8(c) "C1 logs the seq value it observed at forward start"):
+    // for chunk i of v, [2i] = the flag value this kernel saw satisfied before moving the chunk
+    // (pull: seq, must equal g + 1 -- the staging write completed; pack: credit, must be >=
+    // g - S + 1 -- the slot drained; 0 when no wait was needed), [2i + 1] = g + 1. nullptr = off.
+    uint64_t* fwd;
     int* err;                    // sticky error word (mapped host memory)
     uint64_t timeout_ns;         // bound on every spin
 };

@@ -46,13 +46,15 @@ __device__ __forceinline__ void ring_abort(const RelayLaunchArg& A, const RingAr
     }
 }
 
-// Spin (thread 0 only) until pred(*flag) holds; false on timeout or a peer's abort.
+// Spin (thread 0 only) until pred(*flag) holds; false on timeout or a peer's abort. *seen =
+// the last value read (the one that satisfied pred on success).
 template <typename Pred>
-__device__ __forceinline__ bool spin_until(const RelayLaunchArg& A, const uint64_t* flag, Pred pred)
+__device__ __forceinline__ bool spin_until(const RelayLaunchArg& A, const uint64_t* flag, Pred pred, uint64_t* seen)
 {
     uint64_t t0 = 0;
     for (uint32_t it = 0;; it++) {
         const uint64_t v = ld_acquire_sys(flag);
+        *seen = v;
         if (pred(v)) return true;
         if (v >= kReleaseAll) return false;              // ring aborted elsewhere
         if ((it & 255) == 0) {
@@ -99,9 +101,14 @@ __device__ __forceinline__ void relay_body(const RelayLaunchArg& A)
         char* slot = R.stage + (uint64_t)s * R.slot_bytes;
         if (threadIdx.x == 0) {
             bool ok;
+            uint64_t flag = 0;
             if (g == seen) ok = true;
-            else if (PULL) ok = spin_until(A, &R.seq[s], [g](uint64_t v) { return v == g + 1; });
-            else ok = (g < R.S) || spin_until(A, &R.credit[s], [g, &R](uint64_t v) { return v >= g - R.S + 1; });
+            else if (PULL) ok = spin_until(A, &R.seq[s], [g](uint64_t v) { return v == g + 1; }, &flag);
+            else ok = (g < R.S) || spin_until(A, &R.credit[s], [g, &R](uint64_t v) { return v >= g - R.S + 1; }, &flag);
+            if (g != seen && A.fwd) {   // the observation the forward (pack) of chunk i rests on
+                A.fwd[2 * i] = flag;
+                A.fwd[2 * i + 1] = g + 1;
+            }
             if (!ok) ring_abort(A, R);
             else seen = g;
             s_ok = ok;

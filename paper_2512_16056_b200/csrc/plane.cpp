@@ -823,6 +823,7 @@ private:
     cudaEvent_t fork_ = nullptr;
     std::vector<std::pair<cudaStream_t, int>> used_;   // engine streams this call enqueued on
     uint8_t* log_ = nullptr;
+    uint64_t* fwd_ = nullptr;   // forward log (debug_log), on the target
     // host-address order (config host_order): a zero-copy path of a scattered transfer gets a
     // private table of its own pieces sorted by host address, copy-engine batches are sorted
     bool host_order_ = false;
@@ -934,6 +935,7 @@ private:
             t_.stats.path_bytes[j_.dir][0] += j_.B;
             t_.stats.path_chunks[j_.dir][0] += 1;
             t_.log_n = 0;
+            t_.fwd_n = 0;
             if (eng_.cfg.ledger && !j_.capturing) {
                 uint64_t lb[MMA_MAX_GPUS] = {}, lo[MMA_MAX_GPUS] = {};
                 lb[j_.d] = lo[j_.d] = j_.B;
@@ -1306,6 +1308,7 @@ private:
         if (j_.no_log) return cudaSuccess;   // log_ stays null; the target's log is another call's
         if (!eng_.cfg.debug_log || j_.capturing) {
             t_.log_n = 0;
+            t_.fwd_n = 0;
             return cudaSuccess;
         }
         DeviceGuard g(j_.d);
@@ -1317,7 +1320,19 @@ private:
         log_ = t_.log;
         t_.log_n = n_log_;
         CK((cudaError_t)use(lanes(j_.d).direct, j_.d));
-        return (int)cudaMemsetAsync(log_, 0xff, n_log_, lanes(j_.d).direct);
+        CK(cudaMemsetAsync(log_, 0xff, n_log_, lanes(j_.d).direct));
+        if (dynamic_) {
+            t_.fwd_n = 0;
+            return cudaSuccess;
+        }
+        if (t_.fwd_cap < n_) {   // forward log: 0 = no relay kernel observed this chunk
+            if (t_.fwd) cudaFree(t_.fwd);
+            CK(cudaMalloc(&t_.fwd, n_ * 16));
+            t_.fwd_cap = n_;
+        }
+        fwd_ = t_.fwd;
+        t_.fwd_n = n_;
+        return (int)cudaMemsetAsync(fwd_, 0, n_ * 16, lanes(j_.d).direct);
     }
 
     // ---- measurement runs: every path's spans open at the fork, before any path's work is
@@ -1599,6 +1614,7 @@ private:
                 A.v = vstream_on(kd);
                 A.unit_bytes = eng_.unit_bytes;
                 A.log = log_;
+                A.fwd = fwd_;
                 A.err = eng_.err;
                 A.timeout_ns = eng_.timeout_ns;
                 grids[kd] = 0;

@@ -141,6 +141,8 @@ struct Target {
     mma_stats_t stats{};
     uint8_t* log = nullptr;
     size_t log_cap = 0, log_n = 0;
+    uint64_t* fwd = nullptr;         // forward log (debug_log): 2 words per chunk (kargs.h)
+    size_t fwd_cap = 0, fwd_n = 0;
     // debug_log: the table order of the last scattered call's virtual stream (R23 regrouping;
     // identity when not regrouped): last_order[k] = table index of v's k-th segment
     std::vector<uint32_t> last_order;

@@ -26,7 +26,7 @@ SYMBOLS = [
     "mma_set_path_modes", "mma_calibrate", "mma_get_plan", "mma_plan_chunks",
     "mma_get_delivery_log", "mma_get_segment_order", "mma_plan_multi", "mma_memcpy_multi",
     "mma_host_alloc_size", "mma_copy_share_segments_ring", "mma_ledger_process_add",
-    "mma_get_dynamic_backoffs", "mma_host_alloc", "mma_host_free", "mma_get_stats",
+    "mma_get_dynamic_backoffs", "mma_get_forward_log", "mma_host_alloc", "mma_host_free", "mma_get_stats",
     "mma_reset_stats", "mma_get_last_error", "mma_error_string", "mma_fill_pattern",
     "mma_verify_pattern", "mma_verify_segments", "mma_set_kernel_timing", "mma_kernel_times",
     "mma_tune_segments", "mma_get_segment_tuning", "mma_get_dynamic_counts", "mma_set_plan_mode",
@@ -130,6 +130,7 @@ def lib():
         L.mma_memcpy_multi.argtypes = [C.POINTER(Transfer), sz]
         L.mma_host_alloc_size.argtypes = [vp, C.POINTER(sz)]
         L.mma_get_dynamic_backoffs.argtypes = [C.c_int, C.POINTER(C.c_uint64)]
+        L.mma_get_forward_log.argtypes = [C.c_int, vp, vp, sz, C.POINTER(sz)]
         L.mma_copy_share_segments_ring.argtypes = [C.POINTER(Segment), sz, sz, vp, sz, C.c_int, C.c_int, C.c_uint, vp]
         L.mma_plan_multi.argtypes = [C.c_int, vp, vp, C.c_int, vp, vp, C.c_uint64, C.c_int, C.c_int, vp]
         L.mma_host_alloc.argtypes = [C.POINTER(vp), sz, C.c_uint]
@@ -439,6 +440,18 @@ def plan_multi(link_mbps, carry, targets, nchunks, chunk: int, mode: int = 0, pr
                               mode, prefer, out.ctypes.data)
     offs = np.concatenate([[0], np.cumsum(nc)]).astype(np.int64)
     return rc, [out[offs[t]:offs[t + 1]].copy() for t in range(len(tg))]
+
+
+def get_forward_log(device: int):
+    """Debug: (observed, expected) flag values per chunk of the last call (mma_get_forward_log)."""
+    import numpy as np
+    n = C.c_size_t()
+    _check(lib().mma_get_forward_log(device, None, None, 0, C.byref(n)), "mma_get_forward_log")
+    obs = np.zeros(max(1, n.value), dtype=np.uint64)
+    exp = np.zeros(max(1, n.value), dtype=np.uint64)
+    _check(lib().mma_get_forward_log(device, obs.ctypes.data, exp.ctypes.data, n.value, C.byref(n)),
+           "mma_get_forward_log")
+    return obs[: n.value], exp[: n.value]
 
 
 def get_segment_order(device: int):
