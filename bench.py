@@ -931,7 +931,7 @@ def main():
         check of the bench's own launch configuration (all outside the timed region)"""
         cfg = configure(relays)
         if args.modes:
-            m = {"ce": mma.HOP_CE, "zc": mma.HOP_ZC, "ce_p2p": mma.HOP_CE_P2P}
+            m = {"ce": mma.HOP_CE, "zc": mma.HOP_ZC, "ce_p2p": mma.HOP_CE_P2P, "push": mma.HOP_PUSH}
             h, d = (m[x] for x in args.modes.split(","))
             mma.set_path_modes(0, mma.H2D, [h] * len(mma.get_paths(0, mma.H2D)))
             mma.set_path_modes(0, mma.D2H, [d] * len(mma.get_paths(0, mma.D2H)))
@@ -1095,7 +1095,7 @@ def main():
             ms_list = [(h2d_ms if kdir == 0 else d2h_ms)] * args.steps
             peak = sum(pcie[g][dname] for g in path_gpus)
         elif kpath == 255:    # one relay kernel serves every copy-engine ring of the call
-            ring_paths = [i for i, pi in enumerate(pinfo) if pi["kind"] == 1 and eff_mode(pi) == 1]
+            ring_paths = [i for i, pi in enumerate(pinfo) if pi["kind"] == 1 and eff_mode(pi) in (1, 4)]
             moved = sum(st["path_bytes"][kdir][i] for i in ring_paths)
             peak = sum(pcie[pinfo[i]["gpu"]][dname] for i in ring_paths)
         else:
@@ -1326,7 +1326,7 @@ def main():
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u8",
         "data": "synthetic",
         "config": {"workload": w["desc"], "paths": k, "path_gpus": path_gpus, "target_gpu": 0,
-                   "chunk_bytes": int(cfg.chunk_bytes[0]), "claim_bytes": int(cfg.claim_bytes), "hop": {0: "auto", 1: "ce", 2: "zc", 3: "ce_p2p"}[args.hop],
+                   "chunk_bytes": int(cfg.chunk_bytes[0]), "claim_bytes": int(cfg.claim_bytes), "hop": {0: "auto", 1: "ce", 2: "zc", 3: "ce_p2p", 4: "push"}[args.hop],
                    "bytes_per_step": nbytes_step,
                    "fallback_bytes": thresholds or fallback_cfg,
                    "fallback_how": "measured break-even (mma_tune_threshold)" if thresholds else "default (2 chunks)", "l2": f"inputs ({w['bytes'] / GiB:.1f} GiB per direction) exceed the 126 MB L2; no flush",
@@ -1352,7 +1352,7 @@ def main():
         "per_path_count": per_k,
         "numa": numa_info(torch, sorted(set(path_gpus))),
         "topology": topology,
-        "modes": {d: [{"gpu": pi["gpu"], "mode": {0: "auto", 1: "ce", 2: "zc", 3: "ce_p2p"}.get(
+        "modes": {d: [{"gpu": pi["gpu"], "mode": {0: "auto", 1: "ce", 2: "zc", 3: "ce_p2p", 4: "push"}.get(
             pi["seg_mode"] if ("fetch" in w and pi["seg_mode"] >= 0) else pi["mode"], "?"),
             "mbps": pi["seg_mbps"] if ("fetch" in w and pi["seg_mbps"]) else pi["mbps"]} for pi in v]
             for d, v in tuned.items()},

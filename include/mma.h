@@ -46,6 +46,12 @@ typedef enum {
     MMA_HOP_CE = 1,    /* copy-engine DMA; a relay stages through its HBM ring */
     MMA_HOP_ZC = 2,    /* SM loads/stores of mapped pinned host memory; a relay writes the
                           target over NVLink directly (one hop, no staging) */
+    MMA_HOP_PUSH = 4,  /* relays only: the kernel ring with the relay kernel on the OTHER side of
+                          NVLink -- H2D on the relay GPU (it reads its own slot and writes the
+                          target over NVLink: posted writes), D2H on the target (it reads its own
+                          memory and writes the relay's slot). Same slots, flags and waves as
+                          MMA_HOP_CE; chosen against it by measurement (pull / push /
+                          copy engine) */
     MMA_HOP_CE_P2P = 3 /* relays only: the copy engine for both hops, the paper's own design
                           ("an H2D operation and a P2P operation"): host <-> the relay's
                           ring slot, then a peer DMA slot <-> the target, on the same relay

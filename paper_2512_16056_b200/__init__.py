@@ -8,7 +8,7 @@ makes every call raise (there is no CPU fallback); importing still works so that
 """
 from . import mma  # noqa: F401
 from .mma import (  # noqa: F401
-    H2D, D2H, HOP_AUTO, HOP_CE, HOP_ZC, HOP_CE_P2P, PATH_DIRECT, PATH_RELAY, Config, MMAError,
+    H2D, D2H, HOP_AUTO, HOP_CE, HOP_ZC, HOP_CE_P2P, HOP_PUSH, PATH_DIRECT, PATH_RELAY, Config, MMAError,
     calibrate, default_config, finalize, get_delivery_log, get_last_error, get_paths, get_plan,
     get_stats, host_alloc, host_array, host_free, init, make_segments, memcpy_d2h,
     memcpy_d2h_segments, memcpy_h2d, memcpy_h2d_segments, plan_chunks, reset_stats,

@@ -295,8 +295,8 @@ int load_calibration_locked(const char* path, int* applied)
         unsigned mbps, seg_mbps;
         if (sscanf(line, "%d %d %zu %d %d %u %d %u %d", &d, &dir, &p, &gpu, &kind, &mbps, &mode, &seg_mbps, &seg_mode) != 9)
             continue;
-        if (d < 0 || d >= e.ndev || dir < 0 || dir > 1 || mode < MMA_HOP_AUTO || mode > MMA_HOP_CE_P2P ||
-            seg_mode < -1 || seg_mode > MMA_HOP_CE_P2P)
+        if (d < 0 || d >= e.ndev || dir < 0 || dir > 1 || mode < MMA_HOP_AUTO || mode > MMA_HOP_PUSH ||
+            seg_mode < -1 || seg_mode > MMA_HOP_PUSH)
             continue;
         make_paths(d);
         auto& ps = e.tgt[d].paths[dir];
@@ -592,7 +592,7 @@ int mma_set_path_modes(int device, mma_dir_t dir, const int* modes, int npaths)
     auto& ps = e.tgt[device].paths[dir];
     if (npaths != (int)ps.size()) return cudaErrorInvalidValue;
     for (int i = 0; i < npaths; i++)
-        if (modes[i] < MMA_HOP_AUTO || modes[i] > MMA_HOP_CE_P2P) return cudaErrorInvalidValue;
+        if (modes[i] < MMA_HOP_AUTO || modes[i] > MMA_HOP_PUSH) return cudaErrorInvalidValue;
     for (int i = 0; i < npaths; i++) { ps[i].mode = modes[i]; ps[i].seg_mode = -1; }
     return cudaSuccess;
 }

@@ -120,7 +120,7 @@ int validate_cfg(const mma_config_t& c)
     if (c.loopback_relays < 0 || c.loopback_relays > 8) return cudaErrorInvalidValue;
     if (c.plan_mode < PLAN_CONTIGUOUS || c.plan_mode > PLAN_DYNAMIC) return cudaErrorInvalidValue;
     for (int d = 0; d < 2; d++)
-        if (c.hop_mode[d] < MMA_HOP_AUTO || c.hop_mode[d] > MMA_HOP_CE_P2P) return cudaErrorInvalidValue;
+        if (c.hop_mode[d] < MMA_HOP_AUTO || c.hop_mode[d] > MMA_HOP_PUSH) return cudaErrorInvalidValue;
     if (c.relay_ctas < 1 || c.relay_ctas > 64) return cudaErrorInvalidValue;
     if (c.claim_bytes % 16) return cudaErrorInvalidValue;
     if (c.zc_ctas < 0 || c.zc_ctas > 4096) return cudaErrorInvalidValue;
@@ -411,14 +411,23 @@ void free_ring(Ring& r)
     r = Ring();
 }
 
+// The GPU that runs a kernel ring's relay kernel: the pull form on the side that receives
+// over NVLink (H2D: the target; D2H: the relay), the push form (MMA_HOP_PUSH) on the side
+// that sends (H2D: the relay; D2H: the target).
+int ring_kdev(int d, int dir, int relay, int mode)
+{
+    const bool push = mode == MMA_HOP_PUSH;
+    return (dir == MMA_H2D) != push ? d : relay;
+}
+
 // Ring of path p of target d in direction dir: S slots of C bytes on the relay.
-int get_ring(int d, int dir, int p, uint64_t C, uint32_t S, Ring** out)
+int get_ring(int d, int dir, int p, uint64_t C, uint32_t S, bool push, Ring** out)
 {
     Engine& e = E();
     Ring& r = e.tgt[d].rings[dir][p];
     const int relay = e.tgt[d].paths[dir][p].gpu;
-    const int kdev = (dir == MMA_H2D) ? d : relay;
-    if (r.made && (r.broken || r.slot_bytes < C || r.S != S || r.relay != relay)) {
+    const int kdev = ring_kdev(d, dir, relay, push ? MMA_HOP_PUSH : MMA_HOP_CE);
+    if (r.made && (r.broken || r.slot_bytes < C || r.S != S || r.relay != relay || r.kdev != kdev)) {
         // tunables changed, or a failed call left the ring out of step: drain everything
         // that may still use the old ring
         { DeviceGuard g(r.relay); cudaDeviceSynchronize(); }
@@ -888,7 +897,7 @@ private:
             // out; zero-copy paths, the direct copy engine and all-copy-engine relays (on
             // staging of their own, enqueue_captured_p2p) replay as they are
             for (int p = 0; p < P_; p++)
-                if (path(p).kind == MMA_PATH_RELAY && resolve_mode(j_, pmode_[p]) == MMA_HOP_CE) pp_[p].mbps = 0;
+                if (path(p).kind == MMA_PATH_RELAY && kernel_ring(resolve_mode(j_, pmode_[p]))) pp_[p].mbps = 0;
         } else if (!j_.bw_override && !j_.plan_override) {
             std::vector<int> gate;
             ledger_inputs(j_.d, j_.dir, *ps_, pp_, &gate);
@@ -1049,7 +1058,8 @@ private:
         mode_.resize(P_);
         for (int p = 0; p < P_; p++) {
             mode_[p] = resolve_mode(j_, pmode_[p]);
-            if (mode_[p] == MMA_HOP_CE_P2P && path(p).kind == MMA_PATH_DIRECT) mode_[p] = MMA_HOP_CE;
+            if ((mode_[p] == MMA_HOP_CE_P2P || mode_[p] == MMA_HOP_PUSH) && path(p).kind == MMA_PATH_DIRECT)
+                mode_[p] = MMA_HOP_CE;
         }
         // GPU-driven dynamic pull when every usable path moves bytes with SMs:
         // the assignment is then observed (delivery log, per-path counts), not planned
@@ -1080,8 +1090,8 @@ private:
                 needs_tab_[path(p).gpu] = true;
                 if (host_order_ && !dynamic_) build_private(p);
                 else shared = true;
-            } else if (path(p).kind == MMA_PATH_RELAY && mode_[p] == MMA_HOP_CE) {   // the relay kernel
-                needs_tab_[j_.dir == MMA_H2D ? j_.d : path(p).gpu] = shared = true;
+            } else if (path(p).kind == MMA_PATH_RELAY && kernel_ring(mode_[p])) {   // the relay kernel
+                needs_tab_[ring_kdev(j_.d, j_.dir, path(p).gpu, mode_[p])] = shared = true;
             }
         }
         need_ctab_ = shared && e_plan_interleaved() && !dynamic_;
@@ -1354,7 +1364,7 @@ private:
             }
             if (!eng_.wait64 || !eng_.write64) return MMA_ERR_NO_MEMOPS;
             Ring* r = nullptr;   // enqueue_rings gets the same ring and base
-            CK((cudaError_t)get_ring(j_.d, j_.dir, p, j_.C, ring_slots_for(j_.C), &r));
+            CK((cudaError_t)get_ring(j_.d, j_.dir, p, j_.C, ring_slots_for(j_.C), mode_[p] == MMA_HOP_PUSH, &r));
             for (size_t c = 0; c < lists_[p].size() && c < 2 * (size_t)r->S; c++) {
                 cudaStream_t hs = L.hop[((r->g_next + c) % r->S) & 1];
                 CK((cudaError_t)use(hs, g));
@@ -1516,7 +1526,7 @@ private:
         std::vector<int> rp;   // relay paths using rings
         for (int p = 0; p < P_; p++)
             if (!lists_[p].empty() && path(p).kind == MMA_PATH_RELAY &&
-                (mode_[p] == MMA_HOP_CE || mode_[p] == MMA_HOP_CE_P2P))
+                (kernel_ring(mode_[p]) || mode_[p] == MMA_HOP_CE_P2P))
                 rp.push_back(p);
         if (rp.empty()) return cudaSuccess;
         if (eng_.fault_fail_rings) return cudaErrorUnknown;   // test hook (plane.h)
@@ -1530,7 +1540,7 @@ private:
         std::vector<Ring*> rings(P_, nullptr);
         std::vector<uint64_t> g0(P_, 0);
         for (int p : rp) {
-            CK((cudaError_t)get_ring(j_.d, j_.dir, p, j_.C, S, &rings[p]));
+            CK((cudaError_t)get_ring(j_.d, j_.dir, p, j_.C, S, mode_[p] == MMA_HOP_PUSH, &rings[p]));
             g0[p] = rings[p]->g_next;
         }
         size_t maxc = 0;

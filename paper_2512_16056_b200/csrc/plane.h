@@ -359,7 +359,9 @@ int do_init(const mma_config_t* cfg);
 int ensure_init();
 void make_paths(int d);
 void free_ring(Ring& r);
-int get_ring(int d, int dir, int p, uint64_t C, uint32_t S, Ring** out);
+int get_ring(int d, int dir, int p, uint64_t C, uint32_t S, bool push, Ring** out);
+int ring_kdev(int d, int dir, int relay, int mode);   // the GPU running a kernel ring's relay kernel
+inline bool kernel_ring(int mode) { return mode == MMA_HOP_CE || mode == MMA_HOP_PUSH; }
 // gate (optional): GPUs whose own direct work is in flight in this process; a relay through
 // one of them is planned behind that backlog and waits for it (direct path first)
 void ledger_inputs(int d, int dir, const std::vector<PathState>& ps, std::vector<PlanPath>& pp,

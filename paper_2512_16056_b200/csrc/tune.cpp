@@ -85,6 +85,7 @@ static int tune_paths(Job proto, int reps, std::vector<uint32_t>& mbps, std::vec
         std::vector<int> cands;
         if (relay) cands.push_back(MMA_HOP_CE_P2P);
         cands.push_back(MMA_HOP_CE);
+        if (relay) cands.push_back(MMA_HOP_PUSH);
         cands.push_back(MMA_HOP_ZC);
         for (int m : cands) {
             if (m == MMA_HOP_ZC && !proto.mapped) continue;

@@ -14,7 +14,7 @@ PKG = Path(__file__).resolve().parent
 LIB_PATH = PKG / "libmma.so"
 
 H2D, D2H = 0, 1
-HOP_AUTO, HOP_CE, HOP_ZC, HOP_CE_P2P = 0, 1, 2, 3
+HOP_AUTO, HOP_CE, HOP_ZC, HOP_CE_P2P, HOP_PUSH = 0, 1, 2, 3, 4
 PATH_DIRECT, PATH_RELAY = 0, 1
 MAX_PATHS = 16
 MAX_GPUS = 16

@@ -1,5 +1,5 @@
 #!/bin/bash
 mkdir -p gpurun_out/r02
 export MMA_SPIN_TIMEOUT_MS=8000
-timeout 1500 python -m pytest tests/test_gpu_forward_log.py tests/test_gpu_parity.py tests/test_gpu_serialized.py tests/test_gpu_fault.py -q -x > gpurun_out/r02/p_fwd.log 2>&1; echo "rc=$?" >> gpurun_out/r02/p_fwd.log
-tail -25 gpurun_out/r02/p_fwd.log
+timeout 2400 python -m pytest tests -m gpu -q > gpurun_out/r02/q_all.log 2>&1; echo "rc=$?" >> gpurun_out/r02/q_all.log
+tail -8 gpurun_out/r02/q_all.log

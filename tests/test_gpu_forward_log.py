@@ -34,10 +34,11 @@ def mma():
     m.finalize()
 
 
+@pytest.mark.parametrize("hop", [1, 4], ids=["pull", "push"])
 @pytest.mark.parametrize("S", [1, 2, 4])
 @pytest.mark.parametrize("scattered", [False, True], ids=["contig", "segments"])
-def test_forward_only_after_staging(mma, orc, S, scattered):
-    configure(mma, loopback=2, chunk=MiB, slots=S, plan_mode=1, hop=(1, 1))
+def test_forward_only_after_staging(mma, orc, S, scattered, hop):
+    configure(mma, loopback=2, chunk=MiB, slots=S, plan_mode=1, hop=(hop, hop))
     bw = [1, 2, 2]
     mma.set_bandwidth(0, mma.H2D, bw)
     mma.set_bandwidth(0, mma.D2H, bw)

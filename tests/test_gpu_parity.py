@@ -57,7 +57,7 @@ H2D_CASES = [
 
 
 @pytest.mark.parametrize("B,C,lb,S,mode", H2D_CASES)
-@pytest.mark.parametrize("hop", [1, 2, 3], ids=["ce", "zc", "ce_p2p"])
+@pytest.mark.parametrize("hop", [1, 2, 3, 4], ids=["ce", "zc", "ce_p2p", "push"])
 def test_h2d_contiguous(mma, orc, B, C, lb, S, mode, hop):
     configure(mma, loopback=lb, chunk=C, slots=S, plan_mode=mode, hop=(hop, hop))
     bw = [1] * (1 + lb)
@@ -76,7 +76,7 @@ def test_h2d_contiguous(mma, orc, B, C, lb, S, mode, hop):
 
 
 @pytest.mark.parametrize("B,C,lb,S,mode", H2D_CASES)
-@pytest.mark.parametrize("hop", [1, 2, 3], ids=["ce", "zc", "ce_p2p"])
+@pytest.mark.parametrize("hop", [1, 2, 3, 4], ids=["ce", "zc", "ce_p2p", "push"])
 def test_d2h_contiguous(mma, orc, B, C, lb, S, mode, hop):
     configure(mma, loopback=lb, chunk=C, slots=S, plan_mode=mode, hop=(hop, hop))
     bw = [1] * (1 + lb)

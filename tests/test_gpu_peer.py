@@ -42,7 +42,8 @@ def mma():
 
 
 CE, ZC, P2P = 1, 2, 3
-MODES = [(CE, "kernel_ring"), (P2P, "ce_p2p_ring"), (ZC, "zc_one_hop")]
+PUSH = 4
+MODES = [(CE, "kernel_ring"), (PUSH, "push_ring"), (P2P, "ce_p2p_ring"), (ZC, "zc_one_hop")]
 
 
 def _paths(mma, target, relay, dirn):

@@ -45,7 +45,7 @@ def test_random_transfers(mma, orc):
         C = int(rng.choice([4 * KiB, 64 * KiB, 256 * KiB, MiB, 3 * MiB]))
         S = int(rng.integers(1, 5))
         plan_mode = int(rng.choice([0, 1, 2]))
-        modes = [int(x) for x in rng.choice([1, 2, 3], P)]
+        modes = [int(x) for x in rng.choice([1, 2, 3, 4], P)]
         if plan_mode == 2 and rng.random() < 0.7:
             modes = [2] * P
         bw = [int(x) for x in rng.integers(1, 6, P)]

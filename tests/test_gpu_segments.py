@@ -49,6 +49,8 @@ CASES = [
     (2048, MiB, 1, 0, 2),        # 8192 segments: the radix path of the host-order sort
     (512, MiB, 2, 1, 3),         # all-copy-engine rings: batch into slots, peer batch out
     (272, 192 << 10, 1, 0, 3),
+    (512, MiB, 2, 1, 4),         # push-form kernel rings (relay kernel on the sending side)
+    (272, 192 << 10, 1, 0, 4),
 ]
 
 
