@@ -840,10 +840,14 @@ private:
         bool on = false;
         size_t off = 0;          // byte offset of its table in the upload
         uint64_t npieces = 0, B = 0;
-        std::vector<uint64_t> src, dst, len;
-        std::vector<uint32_t> chunk;   // chunk of v each piece belongs to (the kernel logs it)
+        uint64_t src0 = 0, dst0 = 0;   // the first piece (the stream's one-piece form)
     };
     std::vector<Priv> priv_;
+    struct HostSorted {   // the table's segments in host-address order (host_order_perm)
+        std::vector<uint64_t> src, dst, vs, ve;   // addresses and [start, end) in v
+    };
+    std::shared_ptr<const HostSorted> sorted_;
+    std::vector<uint8_t> owner_;   // path carrying each chunk (from the work lists)
     static constexpr int kArenaFull = -1000;
     struct CapturedAlloc {
         int dev;
@@ -1082,18 +1086,20 @@ private:
     // private host-ordered tables of zero-copy paths
     int build_tables()
     {
-        bool shared = false;
+        bool shared = false, any_priv = false;
         priv_.assign(P_, Priv());
         for (int p = 0; p < P_; p++) {
             if (!active_[p]) continue;
             if (mode_[p] == MMA_HOP_ZC) {
                 needs_tab_[path(p).gpu] = true;
-                if (host_order_ && !dynamic_) build_private(p);
+                if (host_order_ && !dynamic_) priv_[p].on = any_priv = true;
                 else shared = true;
             } else if (path(p).kind == MMA_PATH_RELAY && kernel_ring(mode_[p])) {   // the relay kernel
                 needs_tab_[ring_kdev(j_.d, j_.dir, path(p).gpu, mode_[p])] = shared = true;
             }
         }
+        if (any_priv) count_privates();
+        if (any_priv) tr_.mark("count");
         need_ctab_ = shared && e_plan_interleaved() && !dynamic_;
         const uint64_t seg_words = (shared && !j_.contiguous) ? (j_.nseg + 1) + 2 * j_.nseg : 0;
         size_t bytes = seg_words * 8 + (need_ctab_ ? n_ * 4 + (n_ & 1) * 4 : 0);
@@ -1130,15 +1136,8 @@ private:
                     memcpy(h + o, lists_[p].data(), lists_[p].size() * 4);
                     o += lists_[p].size() * 4;
                 }
-            for (auto& q : priv_) {
-                if (!q.on) continue;
-                uint64_t* w = (uint64_t*)(h + q.off);
-                w[0] = 0;
-                for (uint64_t k = 0; k < q.npieces; k++) w[k + 1] = w[k] + q.len[k];
-                memcpy(w + q.npieces + 1, q.src.data(), q.npieces * 8);
-                memcpy(w + 2 * q.npieces + 1, q.dst.data(), q.npieces * 8);
-                memcpy(w + 3 * q.npieces + 1, q.chunk.data(), q.npieces * 4);
-            }
+            tr_.mark("shared");
+            if (any_priv) fill_privates(h);
         }
         tr_.mark("tables");
         return cudaSuccess;
@@ -1146,40 +1145,101 @@ private:
 
     bool e_plan_interleaved() const { return eng_.cfg.plan_mode == PLAN_INTERLEAVED || j_.interleaved_plan; }
 
-    // path p's pieces (the parts of its chunks, chunk by chunk) reordered by host address: a
-    // private virtual stream of B_p bytes that the path's zero-copy kernel moves alone. Each
-    // piece keeps the index of its chunk in v, which the kernel writes to the delivery log.
-    void build_private(int p)
+    // the private streams of the zero-copy paths that get one (priv_[p].on): each path's
+    // pieces -- the parts of the chunks it carries -- in host-address order, a virtual stream
+    // of B_p bytes that the path's zero-copy kernel moves alone. One pass over the segments in
+    // host order (a single sort, cached for a table identical to the previous one) assigns
+    // every piece to the path carrying its chunk (the work lists, i.e. what is executed); each
+    // piece keeps the chunk's index, which the kernel logs. count_privates sizes the tables,
+    // fill_privates writes them straight into the pinned table buffer:
+    //   [npieces + 1] start offsets | [npieces] src | [npieces] dst | [npieces] u32 chunk
+    template <typename F>
+    void each_private_piece(F&& f)
     {
-        Priv& q = priv_[p];
-        std::vector<uint64_t> src, dst, len;
-        std::vector<uint32_t> chunk;
-        for (uint32_t i : lists_[p]) {
-            uint64_t o, l;
-            j_.extent(i, &o, &l);
-            j_.pieces(o, o + l, [&](const Piece& x) {
-                src.push_back((uint64_t)x.src);
-                dst.push_back((uint64_t)x.dst);
-                len.push_back(x.len);
-                chunk.push_back(i);
-            });
+        const uint64_t C = j_.C;
+        const HostSorted& hs = *sorted_;
+        for (size_t x = 0; x < hs.vs.size(); x++) {   // segments in host order, read in sequence
+            const uint64_t vk = hs.vs[x], vk1 = hs.ve[x];
+            for (uint64_t c = vk / C; c * C < vk1; c++) {
+                const int p = owner_[c];
+                if (!priv_[p].on) continue;
+                const uint64_t lo = std::max(vk, c * C), hi = std::min(vk1, (c + 1) * C);
+                f(p, x, c, lo - vk, hi - lo);
+            }
         }
+    }
+
+    void count_privates()
+    {
+        host_order_perm();
+        tr_.mark("host-order");
+        owner_.resize(n_);
+        for (int p = 0; p < P_; p++)
+            for (uint32_t i : lists_[p]) owner_[i] = (uint8_t)p;
+        for (auto& q : priv_) q.npieces = q.B = 0;
+        each_private_piece([&](int p, size_t, uint64_t, uint64_t, uint64_t len) {
+            priv_[p].npieces++;
+            priv_[p].B += len;
+        });
+    }
+
+    void fill_privates(char* h)
+    {
+        std::vector<uint64_t> at(P_, 0);
+        for (auto& q : priv_)
+            if (q.on) ((uint64_t*)(h + q.off))[0] = 0;
+        const HostSorted& hs = *sorted_;
+        each_private_piece([&](int p, size_t k, uint64_t c, uint64_t off, uint64_t len) {
+            Priv& q = priv_[p];
+            uint64_t* w = (uint64_t*)(h + q.off);
+            const uint64_t x = at[p]++, n = q.npieces;
+            w[x + 1] = w[x] + len;
+            w[n + 1 + x] = hs.src[k] + off;
+            w[2 * n + 1 + x] = hs.dst[k] + off;
+            ((uint32_t*)(w + 3 * n + 1))[x] = (uint32_t)c;
+            if (x == 0) {   // the one-piece form of the stream (private_stream_on)
+                q.src0 = w[n + 1];
+                q.dst0 = w[2 * n + 1];
+            }
+        });
+    }
+
+    // the segments in ascending host address (H2D: sources, D2H: destinations), as arrays
+    // read in sequence by the table passes; kept for the next call if its table is the same
+    // (a repeated offload of one block table pays one memcmp instead of a sort and a gather)
+    void host_order_perm()
+    {
+        static std::mutex mu;
+        static int dir = -1;
+        static std::vector<mma_segment_t> last;
+        static auto cached = std::make_shared<HostSorted>();
+        std::lock_guard<std::mutex> g(mu);   // (the engine mutex is held too)
+        const uint64_t n = j_.nseg;
+        if (dir == j_.dir && last.size() == n && !memcmp(last.data(), j_.segs, n * sizeof(mma_segment_t))) {
+            sorted_ = cached;
+            return;
+        }
+        std::vector<uint64_t> key(n);
+        for (uint64_t k = 0; k < n; k++)
+            key[k] = (uint64_t)(j_.dir == MMA_D2H ? (const void*)j_.segs[k].dst : j_.segs[k].src);
         std::vector<uint32_t> perm;
-        order_by_key(j_.dir == MMA_D2H ? dst.data() : src.data(), src.size(), perm);
-        q.on = true;
-        q.npieces = src.size();
-        q.src.resize(q.npieces);
-        q.dst.resize(q.npieces);
-        q.len.resize(q.npieces);
-        q.chunk.resize(q.npieces);
-        q.B = 0;
-        for (size_t k = 0; k < perm.size(); k++) {
-            q.src[k] = src[perm[k]];
-            q.dst[k] = dst[perm[k]];
-            q.len[k] = len[perm[k]];
-            q.chunk[k] = chunk[perm[k]];
-            q.B += q.len[k];
+        order_by_key(key.data(), n, perm);
+        auto hs = std::make_shared<HostSorted>();
+        hs->src.resize(n);
+        hs->dst.resize(n);
+        hs->vs.resize(n);
+        hs->ve.resize(n);
+        for (uint64_t x = 0; x < n; x++) {
+            const uint32_t k = perm[x];
+            hs->src[x] = (uint64_t)j_.segs[k].src;
+            hs->dst[x] = (uint64_t)j_.segs[k].dst;
+            hs->vs[x] = j_.vstart[k];
+            hs->ve[x] = j_.vstart[k + 1];
         }
+        dir = j_.dir;
+        last.assign(j_.segs, j_.segs + n);
+        cached = hs;
+        sorted_ = hs;
     }
 
     // ---- fork (a3): an event on the user stream gates every engine stream the call uses
@@ -1290,8 +1350,8 @@ private:
         v.C = j_.C;
         if (q.npieces == 1) {
             v.nseg = 1;
-            v.src0 = q.src[0];
-            v.dst0 = q.dst[0];
+            v.src0 = q.src0;
+            v.dst0 = q.dst0;
         } else {
             const uint64_t* w = (const uint64_t*)((const char*)dtab_[g] + q.off);
             v.nseg = q.npieces;
