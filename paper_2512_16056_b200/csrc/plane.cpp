@@ -990,17 +990,23 @@ private:
         seg_node_.resize(n);
         host_nodes(hp.data(), n, seg_node_.data());
         if (!eng_.cfg.numa_plan) return cudaSuccess;   // nodes kept for the statistics only
+        // group rank of each segment: the paths' nodes in path order, other known nodes by id,
+        // unknown last; a stable counting sort over the ranks (O(n), the table is large)
+        int maxnode = -1;
+        for (uint64_t k = 0; k < n; k++) maxnode = std::max(maxnode, seg_node_[k]);
+        const int R = (int)order.size() + std::max(0, maxnode + 1) + 1;   // last rank: unknown
+        std::vector<int> rank_of(std::max(0, maxnode + 1), -1);
+        for (size_t r = 0; r < order.size(); r++)
+            if (order[r] <= maxnode) rank_of[order[r]] = (int)r;
         auto rank = [&](int nd) -> int {
-            if (nd < 0) return 1 << 30;
-            for (size_t r = 0; r < order.size(); r++)
-                if (order[r] == nd) return (int)r;
-            return (int)order.size() + nd;
+            if (nd < 0) return R - 1;
+            return rank_of[nd] >= 0 ? rank_of[nd] : (int)order.size() + nd;
         };
+        std::vector<uint32_t> start(R + 1, 0);
+        for (uint64_t k = 0; k < n; k++) start[rank(seg_node_[k]) + 1]++;
+        for (int r = 0; r < R; r++) start[r + 1] += start[r];
         std::vector<uint32_t> idx(n);
-        for (uint64_t k = 0; k < n; k++) idx[k] = (uint32_t)k;
-        std::stable_sort(idx.begin(), idx.end(), [&](uint32_t a, uint32_t b) {
-            return rank(seg_node_[a]) < rank(seg_node_[b]);
-        });
+        for (uint64_t k = 0; k < n; k++) idx[start[rank(seg_node_[k])]++] = (uint32_t)k;
         if (eng_.cfg.debug_log) t_.last_order = idx;
         reseg_.resize(n);
         std::vector<int> nodes(n);
