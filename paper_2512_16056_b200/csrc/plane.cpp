@@ -270,9 +270,18 @@ int do_init(const mma_config_t* cfg)
         if (e.ndev > MMA_MAX_GPUS) e.ndev = MMA_MAX_GPUS;
         for (int a = 0; a < e.ndev; a++)
             for (int b = 0; b < e.ndev; b++) {
-                int ok = 0;
-                if (a != b) cudaDeviceCanAccessPeer(&ok, a, b);
+                int ok = 0, at = 0;
+                if (a != b) {
+                    cudaDeviceCanAccessPeer(&ok, a, b);
+                    if (cudaDeviceGetP2PAttribute(&at, cudaDevP2PAttrNativeAtomicSupported, a, b) != cudaSuccess) {
+                        cudaGetLastError();
+                        at = 0;
+                    }
+                }
                 e.p2p[a][b] = ok != 0;
+                // a kernel on a that updates flags / cursors in b's memory needs native atomics
+                // over the link (system-scope atomics to a peer); MMA_NO_P2P_ATOMICS: test hook
+                e.p2p_atomic[a][b] = a == b || (at != 0 && !getenv("MMA_NO_P2P_ATOMICS"));
             }
         cudaDriverEntryPointQueryResult q;
         void* fn = nullptr;
@@ -1070,6 +1079,13 @@ private:
             mode_[p] = resolve_mode(j_, pmode_[p]);
             if ((mode_[p] == MMA_HOP_CE_P2P || mode_[p] == MMA_HOP_PUSH) && path(p).kind == MMA_PATH_DIRECT)
                 mode_[p] = MMA_HOP_CE;
+            // a kernel ring whose relay kernel updates the ring's flags across the link needs
+            // native peer atomics (H2D pull: flags on the relay, kernel on the target; D2H
+            // push: the same); without them the ring's copy-engine form carries the chunks
+            if (kernel_ring(mode_[p]) && path(p).kind == MMA_PATH_RELAY) {
+                const int kd = ring_kdev(j_.d, j_.dir, path(p).gpu, mode_[p]);
+                if (!eng_.p2p_atomic[kd][path(p).gpu]) mode_[p] = MMA_HOP_CE_P2P;
+            }
         }
         // GPU-driven dynamic pull when every usable path moves bytes with SMs:
         // the assignment is then observed (delivery log, per-path counts), not planned
@@ -1078,6 +1094,8 @@ private:
         for (int p = 0; p < P_; p++) {
             active_[p] = !lists_[p].empty();
             if (dynamic_ && pp_[p].mbps && mode_[p] != MMA_HOP_ZC) dynamic_ = false;
+            // every path's kernel claims from a cursor in the target's memory
+            if (dynamic_ && pp_[p].mbps && !eng_.p2p_atomic[path(p).gpu][j_.d]) dynamic_ = false;
         }
         if (dynamic_)
             for (int p = 0; p < P_; p++) active_[p] = pp_[p].mbps > 0;

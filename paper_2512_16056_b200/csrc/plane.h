@@ -160,6 +160,7 @@ struct Engine {
     mma_config_t cfg{};
     int ndev = 0;
     bool p2p[MMA_MAX_GPUS][MMA_MAX_GPUS] = {};
+    bool p2p_atomic[MMA_MAX_GPUS][MMA_MAX_GPUS] = {};   // [a][b]: a kernel on a may atomically update b's memory
     DevRes dev[MMA_MAX_GPUS];
     Target tgt[MMA_MAX_GPUS];
     std::map<cudaStream_t, cudaEvent_t> join_ev;   // join event per engine stream

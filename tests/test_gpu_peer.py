@@ -282,3 +282,46 @@ def test_relay_behind_its_own_direct_work(mma, orc):
     assert np.array_equal(dst.cpu().numpy(), exp)
     assert mma.get_delivery_log(0) == exp_plan.tobytes()
     assert torch.equal(own_dst.cpu(), own_src[:Bown])
+
+
+ATOMICS_PROG = r"""
+import json, sys
+sys.path.insert(0, {root!r})
+sys.path.insert(0, {root!r} + "/tests")
+import torch
+import paper_2512_16056_b200 as m
+from gpu_util import configure, pinned
+configure(m, loopback=0, chunk=1 << 20, slots=3, plan_mode=1, hop=(1, 1), paths=[1])
+m.set_bandwidth(0, m.H2D, [1, 1])
+B = 24 << 20
+src = pinned(torch, B, seed=3)
+dst = torch.zeros(B, dtype=torch.uint8, device="cuda:0")
+torch.cuda.synchronize()
+m.reset_stats(0)
+m.memcpy_h2d(dst, src, B)
+torch.cuda.synchronize()
+st = m.get_stats(0)
+print(json.dumps(dict(ok=bool(torch.equal(dst.cpu(), src[:B])), kernels=st["kernels"], relay=st["relay_bytes"],
+                      err=m.get_last_error())))
+"""
+
+
+def test_no_peer_atomics_falls_back_to_copy_engine_ring(tmp_path):
+    """a pull ring's kernel updates the relay's credit flags across the link; without native
+    peer atomics (MMA_NO_P2P_ATOMICS makes the engine believe so) the relay's copy-engine ring
+    carries the chunks instead: no relay kernel, bytes exact"""
+    if not torch.cuda.is_available() or torch.cuda.device_count() < 2:
+        pytest.skip("peer relays need two GPUs; this box exposes one (gpurun is one GPU per call)")
+    import json
+    script = tmp_path / "at.py"
+    script.write_text(ATOMICS_PROG.format(root=str(ROOT)))
+    outs = {}
+    for flag in ("0", "1"):
+        env = dict(os.environ)
+        if flag == "1":
+            env["MMA_NO_P2P_ATOMICS"] = "1"
+        p = subprocess.run([sys.executable, str(script)], env=env, capture_output=True, text=True, timeout=240)
+        assert p.returncode == 0, p.stderr[-2000:]
+        outs[flag] = json.loads(p.stdout.strip().splitlines()[-1])
+    assert all(o["ok"] and o["err"] == 0 and o["relay"] > 0 for o in outs.values()), outs
+    assert outs["0"]["kernels"] > 0 and outs["1"]["kernels"] == 0, outs
