@@ -381,7 +381,6 @@ int mma_finalize(void)
                 cudaStreamDestroy(ls[k].direct);
                 cudaStreamDestroy(ls[k].zc);
             }
-        cudaEventDestroy(r.fork);
         cudaEventDestroy(r.cap_fork);
         for (cudaEvent_t ev : r.fork_pool) cudaEventDestroy(ev);
         for (auto& gd : r.gate_ev)

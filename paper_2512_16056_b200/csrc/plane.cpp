@@ -236,7 +236,6 @@ int make_device(int d)
         CK(cudaStreamCreateWithPriority(&l.direct, cudaStreamNonBlocking, hi));
         CK(cudaStreamCreateWithPriority(&l.zc, cudaStreamNonBlocking, hi));
     }
-    CK(cudaEventCreateWithFlags(&r.fork, cudaEventDisableTiming));
     CK(cudaEventCreateWithFlags(&r.cap_fork, cudaEventDisableTiming));
     CK(cudaEventCreateWithFlags(&r.cap_ev, cudaEventDisableTiming));
     for (auto& gd : r.gate_ev)

@@ -36,7 +36,6 @@ using PFN_batch_memop = CUresult (*)(CUstream, unsigned int, CUstreamBatchMemOpP
 // 8 MiB: a copy-engine DMA costs ~4 us of setup on B200, so 1 MiB chunks reach 46 GB/s,
 // 4 MiB 52.6, 16 MiB 54.8 of the link's 55.6 (scripts/probe/probe_chunks.cu)
 constexpr uint64_t kDefaultChunk = 8ull << 20;
-constexpr unsigned kDefaultSlots = 4;
 constexpr uint64_t kRingBytes = 32ull << 20;   // staging per ring when cfg.ring_slots = 0
 constexpr uint32_t kDefaultMbps = 50000;
 // Claim unit of the relay and zero-copy kernels: a CTA claims, checks the flag, copies and
@@ -82,7 +81,6 @@ struct DevRes {
     // live lanes (a live call on another stream may run in that window), and a second
     // capture while these are still capturing is recorded as the native copy (api.cpp)
     Lanes cap_lane[2];
-    cudaEvent_t fork = nullptr;      // recorded on a user stream of this device
     cudaEvent_t cap_fork = nullptr;  // idem, captured calls
     std::vector<cudaEvent_t> fork_pool;   // fork events of live calls (one per call in flight of enqueue)
     // [dir][0 direct lane, 1 zero-copy lane]: recorded behind this GPU's own direct work when
