@@ -81,7 +81,7 @@ struct DevRes {
     // live lanes (a live call on another stream may run in that window), and a second
     // capture while these are still capturing is recorded as the native copy (api.cpp)
     Lanes cap_lane[2];
-    cudaEvent_t cap_fork = nullptr;  // idem, captured calls
+    cudaEvent_t cap_fork = nullptr;  // fork event of captured calls (live calls take one from fork_pool)
     std::vector<cudaEvent_t> fork_pool;   // fork events of live calls (one per call in flight of enqueue)
     // [dir][0 direct lane, 1 zero-copy lane]: recorded behind this GPU's own direct work when
     // a relay through this GPU must wait for it (direct path first, plane.cpp Call::gate)
