@@ -12,7 +12,8 @@
 namespace mma {
 
 // kernels/relay.cu: H2D pull on the target (pull = true) or D2H pack on the relay
-cudaError_t launch_relay(const RelayLaunchArg& a, bool pull, unsigned grid, cudaStream_t s);
+// bulk: the cp.async.bulk (TMA) form of the copy (contiguous 16-byte-aligned units)
+cudaError_t launch_relay(const RelayLaunchArg& a, bool pull, unsigned grid, cudaStream_t s, bool bulk = false);
 // kernels/zerocopy.cu
 cudaError_t launch_zc(const ZcLaunchArg& a, unsigned grid, cudaStream_t s);
 cudaError_t launch_zc_dyn(const DynLaunchArg& a, unsigned grid, cudaStream_t s);

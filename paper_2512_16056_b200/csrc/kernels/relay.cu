@@ -67,7 +67,62 @@ __device__ __forceinline__ bool spin_until(const RelayLaunchArg& A, const uint64
     }
 }
 
-template <bool PULL>
+// ---- the bulk-copy (TMA) form of a unit's copy: one thread streams the unit through
+// shared memory with cp.async.bulk -- global -> shared completing on an mbarrier, then
+// shared -> global in a bulk group -- kBulkStages tiles of kBulkTile in flight. The vector
+// form keeps 64 KiB per CTA in flight in registers; this one 128 KiB in shared memory with a
+// single issuing thread ("or stage through shared memory / cp.async.bulk").
+// Used for contiguous transfers whose unit is 16-byte aligned (MMA_RELAY_BULK=1).
+constexpr uint32_t kBulkTile = 32u << 10;
+constexpr int kBulkStages = 4;
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void bulk_load(char* sbuf, const char* src, uint32_t n, uint64_t* bar)
+{
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(n) : "memory");
+    asm volatile("cp.async.bulk.shared::cta.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(smem_u32(sbuf)),
+                 "l"(src), "r"(n), "r"(smem_u32(bar))
+                 : "memory");
+}
+
+__device__ __forceinline__ void bulk_wait(uint64_t* bar, uint32_t parity)
+{
+    asm volatile("{ .reg .pred p; W: mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1; @!p bra W; }" ::"r"(smem_u32(bar)),
+                 "r"(parity)
+                 : "memory");
+}
+
+// thread 0 only: dst[0, len) = src[0, len); len % 16 == 0, both 16-byte aligned. *phase holds
+// one parity bit per stage (the barriers live as long as the CTA).
+__device__ __forceinline__ void bulk_copy(char* dst, const char* src, uint64_t len, char* smem, uint64_t* bar,
+                                          uint32_t* phase)
+{
+    const uint64_t ntiles = (len + kBulkTile - 1) / kBulkTile;
+    auto tile_bytes = [&](uint64_t t) { return (uint32_t)((len - t * kBulkTile) < kBulkTile ? len - t * kBulkTile : kBulkTile); };
+    asm volatile("fence.proxy.async;" ::: "memory");   // the flag's acquire before the async-proxy reads
+    for (uint64_t t = 0; t < ntiles && t < (uint64_t)kBulkStages; t++)
+        bulk_load(smem + t * kBulkTile, src + t * kBulkTile, tile_bytes(t), &bar[t]);
+    for (uint64_t t = 0; t < ntiles; t++) {
+        const int s = (int)(t % kBulkStages);
+        bulk_wait(&bar[s], (*phase >> s) & 1);
+        *phase ^= 1u << s;
+        asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst + t * kBulkTile),
+                     "r"(smem_u32(smem + s * kBulkTile)), "r"(tile_bytes(t))
+                     : "memory");
+        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        // the previous tile's stage is free once its store has read it: refill it
+        if (t >= 1 && t - 1 + kBulkStages < ntiles) {
+            asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+            const int sp = (int)((t - 1) % kBulkStages);
+            bulk_load(smem + sp * kBulkTile, src + (t - 1 + kBulkStages) * kBulkTile, tile_bytes(t - 1 + kBulkStages), &bar[sp]);
+        }
+    }
+    asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");   // every store performed
+    asm volatile("fence.proxy.async;" ::: "memory");             // ... before the generic-proxy release
+}
+
+template <bool PULL, bool BULK>
 __device__ __forceinline__ void relay_body(const RelayLaunchArg& A)
 {
     uint32_t r = 0;
@@ -79,6 +134,17 @@ __device__ __forceinline__ void relay_body(const RelayLaunchArg& A)
     const uint64_t nunits = R.chunks.count * upc;
     __shared__ unsigned long long s_u;
     __shared__ int s_ok;
+    extern __shared__ __align__(128) char s_bulk[];   // BULK: kBulkStages x kBulkTile
+    __shared__ __align__(8) uint64_t s_bar[kBulkStages];
+    uint32_t bulk_phase = 0;
+    if (BULK) {
+        if (threadIdx.x == 0) {
+            for (int k = 0; k < kBulkStages; k++)
+                asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&s_bar[k])));
+            asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        }
+        __syncthreads();
+    }
     // thread 0: the last chunk whose flag this CTA saw satisfied. Its flag cannot move on
     // while this CTA still holds one of its units (the slot is released only when every unit
     // of the chunk is done), so a later unit of the same chunk skips the poll.
@@ -115,8 +181,16 @@ __device__ __forceinline__ void relay_body(const RelayLaunchArg& A)
         }
         __syncthreads();
         if (!s_ok) return;
-        if (PULL) v_copy<V_UNPACK>(A.v, off + lo, off + hi, slot + lo);
-        else v_copy<V_PACK>(A.v, off + lo, off + hi, slot + lo);
+        // the bulk form for a contiguous, 16-byte-aligned unit; the vector form otherwise
+        const char* bsrc = PULL ? slot + lo : reinterpret_cast<const char*>(A.v.src0) + off + lo;
+        char* bdst = PULL ? reinterpret_cast<char*>(A.v.dst0) + off + lo : slot + lo;
+        if (BULK && A.v.nseg == 1 && !(((uintptr_t)bsrc | (uintptr_t)bdst | (hi - lo)) & 15)) {
+            if (threadIdx.x == 0) bulk_copy(bdst, bsrc, hi - lo, s_bulk, s_bar, &bulk_phase);
+        } else if (PULL) {
+            v_copy<V_UNPACK>(A.v, off + lo, off + hi, slot + lo);
+        } else {
+            v_copy<V_PACK>(A.v, off + lo, off + hi, slot + lo);
+        }
         __syncthreads();
         if (threadIdx.x == 0) {
             __threadfence();
@@ -134,17 +208,40 @@ __device__ __forceinline__ void relay_body(const RelayLaunchArg& A)
 
 __global__ void __launch_bounds__(kThreads) relay_pull_kernel(const __grid_constant__ RelayLaunchArg A)
 {
-    relay_body<true>(A);
+    relay_body<true, false>(A);
 }
 
 __global__ void __launch_bounds__(kThreads) relay_pack_kernel(const __grid_constant__ RelayLaunchArg A)
 {
-    relay_body<false>(A);
+    relay_body<false, false>(A);
 }
 
-cudaError_t launch_relay(const RelayLaunchArg& a, bool pull, unsigned grid, cudaStream_t s)
+__global__ void __launch_bounds__(kThreads) relay_pull_bulk_kernel(const __grid_constant__ RelayLaunchArg A)
+{
+    relay_body<true, true>(A);
+}
+
+__global__ void __launch_bounds__(kThreads) relay_pack_bulk_kernel(const __grid_constant__ RelayLaunchArg A)
+{
+    relay_body<false, true>(A);
+}
+
+cudaError_t launch_relay(const RelayLaunchArg& a, bool pull, unsigned grid, cudaStream_t s, bool bulk)
 {
     if (grid == 0) return cudaSuccess;
+    if (bulk) {
+        constexpr int smem = kBulkStages * kBulkTile;
+        static bool attr = [] {
+            return cudaFuncSetAttribute(relay_pull_bulk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) ==
+                       cudaSuccess &&
+                   cudaFuncSetAttribute(relay_pack_bulk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) ==
+                       cudaSuccess;
+        }();
+        if (!attr) return cudaErrorInvalidValue;
+        if (pull) relay_pull_bulk_kernel<<<grid, kThreads, smem, s>>>(a);
+        else relay_pack_bulk_kernel<<<grid, kThreads, smem, s>>>(a);
+        return cudaGetLastError();
+    }
     if (pull) relay_pull_kernel<<<grid, kThreads, 0, s>>>(a);
     else relay_pack_kernel<<<grid, kThreads, 0, s>>>(a);
     return cudaGetLastError();

@@ -304,6 +304,7 @@ int do_init(const mma_config_t* cfg)
         e.unit_bytes = (uint32_t)env_size("MMA_UNIT_BYTES", kDefaultUnit);
         e.group_bytes = env_size("MMA_GROUP_BYTES", kDefaultGroupBytes);
         e.hop_lanes = env_int("MMA_HOP_LANES", 2) == 1 ? 1 : 2;
+        e.relay_bulk = env_int("MMA_RELAY_BULK", 0) != 0;
         if (const char* u = getenv("MMA_UPLOAD")) e.upload_by_kernel = strcmp(u, "ce") != 0;
         const char* f = getenv("MMA_FAULT_DROP_PUBLISH");
         e.fault_drop_publish = f ? atoll(f) : -1;
@@ -1744,7 +1745,7 @@ private:
             DeviceGuard dg(kd);
             KTimer kt(kd, s, (j_.dir == MMA_H2D ? 1 : 2) | (j_.dir << 4) | (0xff << 8));
             TSpan ts(kd, s, j_.dir == MMA_H2D ? "relay pull kernel" : "relay pack kernel", -1, (long long)w0, 0);
-            CK(launch_relay(kv.second, j_.dir == MMA_H2D, grids[kd], s));
+            CK(launch_relay(kv.second, j_.dir == MMA_H2D, grids[kd], s, eng_.relay_bulk));
             t_.stats.kernels++;
         }
         return cudaSuccess;

@@ -187,6 +187,7 @@ struct Engine {
     uint32_t unit_bytes = kDefaultUnit;
     uint64_t group_bytes = kDefaultGroupBytes;   // ring hop groups (plane.cpp group_chunks)
     int hop_lanes = 2;                           // relay hop streams per direction used (1 or 2)
+    bool relay_bulk = false;                     // MMA_RELAY_BULK=1: the cp.async.bulk relay kernels
     bool upload_by_kernel = true;    // MMA_UPLOAD=ce: table uploads by the copy engine
     // fault injection (tests only, MMA_FAULT_DROP_PUBLISH=g): the hop-1 publish of global
     // ring chunk g is never issued, so the relay kernel must time out, record the sticky

@@ -23,6 +23,8 @@
 
 using namespace mma;
 
+static bool g_bulk = false;   // the cp.async.bulk form of the relay kernels
+
 struct RingMem {
     char* stage;
     uint64_t* flags;     // seq[64], credit[64]
@@ -32,6 +34,7 @@ struct RingMem {
 int main(int argc, char** argv)
 {
     const bool ncu = argc > 1 && !strcmp(argv[1], "ncu");
+
     const uint64_t C = 8ull << 20;          // engine default chunk
     const uint32_t S = 32;                  // slots = chunks per ring: 256 MiB per ring
     const uint64_t per_ring = S * C;
@@ -123,13 +126,36 @@ int main(int argc, char** argv)
         }
         A.nrings = rings;
         cudaEventRecord(a, st);
-        if (launch_relay(A, pull, rings * ctas, st) != cudaSuccess) return 1;
+        if (launch_relay(A, pull, rings * ctas, st, g_bulk) != cudaSuccess) return 1;
         cudaEventRecord(b, st);
         if (cudaEventSynchronize(b) != cudaSuccess) return 1;
         cudaEventElapsedTime(ms_out, a, b);
         return *(volatile int*)err;
     };
 
+    if (argc > 1 && !strcmp(argv[1], "bulk")) {   // vector vs bulk form, contiguous, 1 and 7 rings
+        printf("# relay kernels alone, vector form (16-byte loads in registers) vs bulk form (cp.async.bulk\n");
+        printf("# through shared memory, 4 x 32 KiB in flight per CTA), 512 KiB units; best of 5\n");
+        printf("%-5s %-6s %-6s %-5s %10s %10s\n", "kern", "form", "rings", "ctas", "GB/s", "GB/s/CTA");
+        for (int pull = 1; pull >= 0; pull--)
+            for (int bulk = 0; bulk < 2; bulk++)
+                for (int rings : {1, 7})
+                    for (int ctas : {1, 2, 4, 8, 16}) {
+                        g_bulk = bulk;
+                        float best = 1e30f;
+                        for (int rep = 0; rep < 6; rep++) {
+                            float ms = 0;
+                            int rc = run(rings, ctas, pull, 512u << 10, &ms);
+                            if (rc) { printf("ERR run rc=%d\n", rc); return 1; }
+                            if (rep) best = std::min(best, ms);
+                        }
+                        const double gbs = (double)per_ring * rings / (best * 1e-3) / 1e9;
+                        printf("%-5s %-6s %-6d %-5d %10.1f %10.1f\n", pull ? "pull" : "pack", bulk ? "bulk" : "vector",
+                               rings, ctas, gbs, gbs / (rings * ctas));
+                    }
+        g_bulk = false;
+        return 0;
+    }
     if (ncu) {     // one profiled launch per kernel: 7 rings x 8 CTAs (the engine default)
         float ms;
         CK((cudaError_t)run(7, 8, true, 128u << 10, &ms));
