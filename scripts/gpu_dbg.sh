@@ -1,9 +1,10 @@
 #!/bin/bash
 mkdir -p gpurun_out/r02
-for cfg in "MMA_ZC_CTAS=16" "MMA_ZC_CTAS=4" "MMA_ZC_CTAS=8" "MMA_ZC_CTAS=32" "MMA_UNIT_BYTES=2097152" "MMA_UNIT_BYTES=131072" "MMA_ZC_CTAS=4 MMA_UNIT_BYTES=4194304"; do
-  env $cfg timeout 600 python bench.py --quick --no-verify --steps 5 --warmup 3 > gpurun_out/r02/w.json 2>/dev/null
-  python -c "
-import json
-d=json.loads(open('gpurun_out/r02/w.json').read().strip().splitlines()[-1])
-print('$cfg', d.get('value'), d['per_direction'], (d.get('roofline') or {}).get('frac'))"
+export MMA_SPIN_TIMEOUT_MS=8000
+for seed in 1001 1002 1003 1004 1005; do
+  MMA_RANDOM_CASES=2000 MMA_RANDOM_SEED=$seed timeout 1200 python -m pytest tests/test_gpu_random.py -q -x > gpurun_out/r02/x_soak_$seed.log 2>&1; echo "seed $seed rc=$?"
 done
+for seed in 2001 2002; do
+  MMA_MULTI_CASES=1000 MMA_RANDOM_SEED=$seed timeout 1200 python -m pytest tests/test_gpu_multi.py -q -x -k random > gpurun_out/r02/x_multi_$seed.log 2>&1; echo "multi seed $seed rc=$?"
+done
+MMA_RELAY_BULK=1 MMA_RANDOM_CASES=1000 MMA_RANDOM_SEED=3001 timeout 1200 python -m pytest tests/test_gpu_random.py -q -x > gpurun_out/r02/x_soak_bulk.log 2>&1; echo "bulk soak rc=$?"

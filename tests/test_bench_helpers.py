@@ -54,6 +54,16 @@ def test_oracle_sample_bounded():
     assert "256 of 131072" in desc
 
 
+def test_cpu_baseline_legs(monkeypatch):
+    """cpu_baseline: the oracle at the bench's path threads and at ~nproc threads, with the
+    CPU model (SURVEY 8(d) "Oracle timing alongside")"""
+    monkeypatch.setattr(bench.os, "cpu_count", lambda: 5)
+    c = bench.cpu_baseline(1, nsegs_sample=128, seconds_per_leg=0.05)
+    assert [leg["threads"] for leg in c["legs"]] == [1, 5]      # 1 path; (5 + 1) // 2 = 3 paths -> 5 threads
+    assert c["value"] == c["legs"][0]["gbps"] and c["cores"] == 1 and c["nproc"] == 5
+    assert c["kind"] == "oracle" and "cpu_model" in c
+
+
 def test_reference_arm_line():
     p = subprocess.run([sys.executable, str(ROOT / "bench.py"), "--impl", "reference", "--steps", "1",
                         "--warmup", "0"], capture_output=True, text=True, timeout=300, cwd=str(ROOT))
@@ -98,7 +108,7 @@ def test_committed_bench_line_has_the_contract_keys():
     contract names, with the types it expects"""
     import json
     from pathlib import Path
-    d = json.loads((Path(__file__).resolve().parents[1] / "profiles" / "r01_bench.json").read_text())
+    d = json.loads((Path(__file__).resolve().parents[1] / "profiles" / "r02_bench.json").read_text())
     for k in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better",
               "scaling", "vs_baseline", "dtype", "data", "config", "roofline", "cpu_baseline", "e2e",
               "gpu_launches", "clocks"):
@@ -113,6 +123,7 @@ def test_committed_bench_line_has_the_contract_keys():
     for k in ("value", "unit", "cores", "kind", "sample"):
         assert k in c, k
     assert c["kind"] == "oracle" and c["cores"] >= 1
+    assert len(c["legs"]) >= 1 and c["nproc"] >= 1 and "cpu_model" in c     # round 2: both thread legs
     e = d["e2e"]
     for k in ("value", "unit", "h2d_bytes_per_step", "d2h_bytes_per_step"):
         assert k in e, k
