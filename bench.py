@@ -1053,13 +1053,23 @@ def main():
     time.sleep(0.3)
     t_start = torch.cuda.Event(enable_timing=True)
     t_end = torch.cuda.Event(enable_timing=True)
+    import resource
+    ru0, w0 = resource.getrusage(resource.RUSAGE_SELF), time.perf_counter()
     t_start.record(stream)
     for i in range(args.steps):
         run_step(mma, w, 0, stream, evs[i])
     t_end.record(stream)
     for g in path_gpus:
         torch.cuda.synchronize(g)
+    ru1, w1 = resource.getrusage(resource.RUSAGE_SELF), time.perf_counter()
     clk = clocks.stop()
+    # host CPU the engine used over the timed region (the paper's Fig 13 / P:934: two busy
+    # threads per GPU cost 822% CPU at 8 GPUs); ours has no thread in the per-chunk loop
+    cpu_s = (ru1.ru_utime - ru0.ru_utime) + (ru1.ru_stime - ru0.ru_stime)
+    host_cpu = {"cpu_percent": round(100 * cpu_s / max(1e-9, w1 - w0), 1), "cpu_s": round(cpu_s, 3),
+                "wall_s": round(w1 - w0, 3),
+                "what": "process user+system CPU time over the timed region (enqueue + waits; the clock "
+                        "sampler thread included) / wall time"}
     ktimes = mma.kernel_times()
     mma.set_kernel_timing(False)
     ms_total = t_start.elapsed_time(t_end)
@@ -1346,6 +1356,7 @@ def main():
         "gpu_launches": int(st["kernels"]),
         "kernel_kinds": kinds,
         "clocks": clk,
+        "host_cpu": host_cpu,
         "verify": verify,
         "plan": plan_choice,
         "mode_policy": policy or None,
