@@ -993,12 +993,25 @@ def main():
     multipath_error = None
     try:
         cfg, verify = prepare(list(range(1, k)))
-    except Exception as ex:  # noqa: BLE001 - report, then measure the direct path alone
+    except Exception as ex:  # noqa: BLE001 - report, then retry without relay kernels, then direct
         multipath_error = f"{type(ex).__name__}: {ex}"
-        print(f"multipath setup failed ({multipath_error}); falling back to the direct path", file=sys.stderr)
+        print(f"multipath setup failed ({multipath_error}); retrying with zero-copy paths only", file=sys.stderr)
         mma.finalize()
-        k = 1
-        cfg, verify = prepare([])
+        saved_modes = args.modes
+        try:
+            if k > 1 and "fetch" in w:   # the one-hop zero-copy relays need no ring and no flag
+                args.modes = "zc,zc"
+                cfg, verify = prepare(list(range(1, k)))
+                multipath_error += " (retried: every path zero-copy)"
+            else:
+                raise RuntimeError("no zero-copy retry for this workload")
+        except Exception as ex2:  # noqa: BLE001 - measure the direct path alone
+            args.modes = saved_modes
+            multipath_error += f"; retry failed ({type(ex2).__name__}: {ex2}); direct path only"
+            print(f"falling back to the direct path ({multipath_error})", file=sys.stderr)
+            mma.finalize()
+            k = 1
+            cfg, verify = prepare([])
     paths = mma.get_paths(0, mma.H2D)
     path_gpus = [p["gpu"] for p in paths]
     fallback_cfg = {"h2d": int(cfg.fallback_bytes[0]), "d2h": int(cfg.fallback_bytes[1])}
