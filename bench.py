@@ -1285,8 +1285,8 @@ def main():
            "h2d_bytes_per_step": w["bytes"], "d2h_bytes_per_step": w["bytes"],
            "how": "wall clock around the Python binding -> C ABI calls, stream synchronized each step"}
 
-    # ---- native baseline on the same buffers: one cudaMemcpyBatchAsync (config 3) or
-    # cudaMemcpyAsync (config 2) per direction on the user stream
+    # ---- native baseline on the same buffers: one cudaMemcpyAsync per segment (config 3, the
+    # per-block loop of a paged KV cache's swap) or per tensor / transfer, on the user stream
     native = None
     if not args.quick:
         cfg.fallback_bytes[0] = cfg.fallback_bytes[1] = (1 << 64) - 1   # everything native
@@ -1302,7 +1302,7 @@ def main():
         nd = statistics.median(nev[i][1].elapsed_time(nev[i][2]) for i in range(args.steps))
         native = {"h2d_gbps": round(w["bytes"] / nh / 1e6, 2), "d2h_gbps": round(w["bytes"] / nd / 1e6, 2),
                   "step_gbps": round(nbytes_step / (nh + nd) / 1e6, 2),
-                  "what": "cudaMemcpyBatchAsync of all segments on the user stream (single PCIe link)"
+                  "what": "one cudaMemcpyAsync per 32 KiB segment on the user stream (single PCIe link)"
                   if "fetch" in w else ("one cudaMemcpyAsync per tensor on the user stream (single PCIe link)"
                                         if "wake" in w else "cudaMemcpyAsync on the user stream (single PCIe link)"),
                   "speedup": round(value / (nbytes_step / (nh + nd) / 1e6), 3)}

@@ -953,7 +953,7 @@ private:
             j_.pieces(0, j_.B, [&](const Piece& x) { b.add(x.dst, x.src, x.len); });
             if (!small && host_order_) b.sort_by_host(kind_);   // a one-path plan, not a small copy
             TSpan ts(j_.user_dev, j_.user, "DMA native (fallback)", 0, -1, j_.B);
-            CK((cudaError_t)b.issue(kind_, j_.user, !j_.capturing));
+            CK((cudaError_t)b.issue(kind_, j_.user));
             t_.stats.path_bytes[j_.dir][0] += j_.B;
             t_.stats.path_chunks[j_.dir][0] += 1;
             t_.log_n = 0;
@@ -1310,7 +1310,7 @@ private:
             if (!j_.capturing && tab_bytes_ >= (64u << 10) && eng_.upload_by_kernel) {
                 // a large table is fetched by the zero-copy kernel from the mapped staging
                 // buffer: a copy-engine upload would queue behind whatever DMAs the copy
-                // engines hold (a 131,072-descriptor batch of another call), and its enqueue
+                // engines hold (131,072 per-segment DMAs of another call), and its enqueue
                 // blocks the host once the engine's queue is full
                 ZcLaunchArg a{};
                 a.v.nseg = 1;
@@ -1585,7 +1585,7 @@ private:
             if (host_order_) batch.sort_by_host(kind_);
             {
                 TSpan ts(g, s, "DMA direct", p, L[a], o1 + l1 - o0);
-                CK((cudaError_t)batch.issue(kind_, s, !j_.capturing));
+                CK((cudaError_t)batch.issue(kind_, s));
             }
             if (log_) CK(cudaMemsetAsync(log_ + L[a], p, b - a, s));
             a = b;
@@ -1778,14 +1778,14 @@ private:
                 j_.pieces(off, off + len, [&](const Piece& x) { in.add(slot + (x.v - off), x.src, x.len); });
                 j_.pieces(off, off + len, [&](const Piece& x) { out.add(x.dst, slot + (x.v - off), x.len); });
                 if (host_order_) in.sort_by_host(cudaMemcpyHostToDevice);
-                CK((cudaError_t)in.issue(cudaMemcpyHostToDevice, hs, false));
-                CK((cudaError_t)out.issue(cudaMemcpyDeviceToDevice, hs, false));
+                CK((cudaError_t)in.issue(cudaMemcpyHostToDevice, hs));
+                CK((cudaError_t)out.issue(cudaMemcpyDeviceToDevice, hs));
             } else {
                 j_.pieces(off, off + len, [&](const Piece& x) { in.add(slot + (x.v - off), x.src, x.len); });
                 j_.pieces(off, off + len, [&](const Piece& x) { out.add(x.dst, slot + (x.v - off), x.len); });
                 if (host_order_) out.sort_by_host(cudaMemcpyDeviceToHost);
-                CK((cudaError_t)in.issue(cudaMemcpyDeviceToDevice, hs, false));
-                CK((cudaError_t)out.issue(cudaMemcpyDeviceToHost, hs, false));
+                CK((cudaError_t)in.issue(cudaMemcpyDeviceToDevice, hs));
+                CK((cudaError_t)out.issue(cudaMemcpyDeviceToHost, hs));
             }
         }
         return cudaSuccess;

@@ -291,7 +291,9 @@ struct Job {
 
 void order_by_key(const uint64_t* key, size_t n, std::vector<uint32_t>& perm);
 
-// Pieces copied by one DMA call: cudaMemcpyAsync for one, cudaMemcpyBatchAsync for many.
+// Pieces copied by the copy engine: one cudaMemcpyAsync per merged run of pieces. Scattered
+// transfers with many pieces go to the zero-copy kernels instead (MMA_HOP_AUTO), since each
+// DMA costs host issue time.
 struct DmaBatch {
     std::vector<void*> dst, src;
     std::vector<size_t> len;
@@ -326,22 +328,8 @@ struct DmaBatch {
         src.swap(s2);
         len.swap(l2);
     }
-    // batch = false: one cudaMemcpyAsync per piece (graph capture records memcpy nodes)
-    int issue(cudaMemcpyKind kind, cudaStream_t s, bool batch = true)
+    int issue(cudaMemcpyKind kind, cudaStream_t s)
     {
-        if (dst.empty()) return cudaSuccess;
-        if (dst.size() == 1) return (int)cudaMemcpyAsync(dst[0], src[0], len[0], kind, s);
-        if (!batch || s == nullptr || s == cudaStreamLegacy) {   // the batch API rejects the legacy stream
-            for (size_t i = 0; i < dst.size(); i++) CK(cudaMemcpyAsync(dst[i], src[i], len[i], kind, s));
-            return cudaSuccess;
-        }
-        cudaMemcpyAttributes at;
-        memset(&at, 0, sizeof(at));
-        at.srcAccessOrder = cudaMemcpySrcAccessOrderStream;
-        size_t idx = 0, fail = 0;
-        cudaError_t e = cudaMemcpyBatchAsync(dst.data(), src.data(), len.data(), dst.size(), &at, &idx, 1, &fail, s);
-        if (e == cudaSuccess) return cudaSuccess;
-        cudaGetLastError();
         for (size_t i = 0; i < dst.size(); i++) CK(cudaMemcpyAsync(dst[i], src[i], len[i], kind, s));
         return cudaSuccess;
     }

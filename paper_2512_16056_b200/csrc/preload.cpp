@@ -16,16 +16,12 @@
 // buffer is the engine's own and usable by its zero-copy kernels; cudaFreeHost of such a
 // buffer is mma_host_free. Write-combined requests and every failure go to the runtime.
 //
-// It also exports cudaMemcpyBatchAsync (+ _ptsz), the batch API paged KV caches use for
-// block swaps: a batch of at least MMA_PRELOAD_MIN_BYTES whose every entry is pinned host
-// -> device memory of one GPU (or the reverse) becomes one scattered multipath copy
-// (mma_memcpy_{h2d,d2h}_segments, north_star (e)). Every entry is classified (a sampled
-// check could route a mixed batch wrongly); other batches pass through.
+// Scattered block swaps (paged KV caches) are not interposed: an application that wants the
+// multipath scattered copy calls mma_memcpy_{h2d,d2h}_segments (north_star (e)) itself.
 #include <dlfcn.h>
 #include <stdint.h>
 #include <stdlib.h>
 
-#include <new>
 
 #include "../../include/mma.h"
 
@@ -91,36 +87,6 @@ int route(void* dst, const void* src, size_t n, int kind)
     return (kind == kH2D || kind == kD2H) ? kind : 0;
 }
 
-// All entries host -> device d (kH2D) or device d -> host (kD2H), host memory pinned
-// (pointer type host): returns the kind and sets *dev; else 0.
-int route_batch(void** dsts, void** srcs, const size_t* sizes, size_t count, int* dev)
-{
-    if (g_inside || count < 2 || !dsts || !srcs || !sizes) return 0;
-    size_t total = 0;
-    for (size_t i = 0; i < count; i++) total += sizes[i];
-    if (total < min_bytes()) return 0;
-    static attr_fn get = next<attr_fn>("cudaPointerGetAttributes");
-    static auto clear = next<int (*)()>("cudaGetLastError");
-    if (!get) return 0;
-    int kind = 0;
-    *dev = -1;
-    for (size_t i = 0; i < count; i++) {
-        if (!sizes[i]) continue;
-        PtrAttr a{}, b{};
-        if (get(&a, dsts[i]) != 0 || get(&b, srcs[i]) != 0) {
-            if (clear) clear();
-            return 0;
-        }
-        int k = 0, d = -1;
-        if (a.type == kTypeDevice && b.type == kTypeHost) { k = kH2D; d = a.device; }
-        else if (b.type == kTypeDevice && a.type == kTypeHost) { k = kD2H; d = b.device; }
-        if (!k || (kind && k != kind) || (*dev >= 0 && d != *dev)) return 0;
-        kind = k;
-        *dev = d;
-    }
-    return kind;
-}
-
 int engine(void* dst, const void* src, size_t n, int kind, void* stream)
 {
     g_inside = 1;
@@ -130,20 +96,6 @@ int engine(void* dst, const void* src, size_t n, int kind, void* stream)
     return rc;
 }
 
-int engine_batch(void** dsts, void** srcs, const size_t* sizes, size_t count, int kind, int dev, void* stream)
-{
-    mma_segment_t* segs = new (std::nothrow) mma_segment_t[count];
-    if (!segs) return 1;
-    for (size_t i = 0; i < count; i++) segs[i] = mma_segment_t{srcs[i], dsts[i], sizes[i]};
-    g_inside = 1;
-    const int rc = (kind == kH2D) ? mma_memcpy_h2d_segments(segs, count, dev, (mma_stream_t)stream)
-                                  : mma_memcpy_d2h_segments(segs, count, dev, (mma_stream_t)stream);
-    g_inside = 0;
-    delete[] segs;   // the engine copies the table at call time
-    return rc;
-}
-
-typedef int (*batch_fn)(void**, void**, size_t*, size_t, void*, size_t*, size_t, size_t*, void*);
 typedef int (*host_alloc_fn)(void**, size_t, unsigned);
 typedef int (*malloc_host_fn)(void**, size_t);
 typedef int (*free_host_fn)(void*);
@@ -190,30 +142,6 @@ __attribute__((visibility("default"))) int cudaMemcpyAsync_ptsz(void* dst, const
         if (engine(dst, src, n, k, stream ? stream : (void*)0x2) == 0) return 0;
     }
     return real(dst, src, n, kind, stream);
-}
-
-__attribute__((visibility("default"))) int cudaMemcpyBatchAsync(void** dsts, void** srcs, size_t* sizes, size_t count,
-                                                                 void* attrs, size_t* attrs_idx, size_t nattrs,
-                                                                 size_t* fail_idx, void* stream)
-{
-    static batch_fn real = next<batch_fn>("cudaMemcpyBatchAsync");
-    int dev = -1;
-    if (const int k = route_batch(dsts, srcs, sizes, count, &dev)) {
-        if (engine_batch(dsts, srcs, sizes, count, k, dev, stream) == 0) return 0;
-    }
-    return real ? real(dsts, srcs, sizes, count, attrs, attrs_idx, nattrs, fail_idx, stream) : 1;
-}
-
-__attribute__((visibility("default"))) int cudaMemcpyBatchAsync_ptsz(void** dsts, void** srcs, size_t* sizes,
-                                                                      size_t count, void* attrs, size_t* attrs_idx,
-                                                                      size_t nattrs, size_t* fail_idx, void* stream)
-{
-    static batch_fn real = next<batch_fn>("cudaMemcpyBatchAsync_ptsz");
-    int dev = -1;
-    if (const int k = route_batch(dsts, srcs, sizes, count, &dev)) {
-        if (engine_batch(dsts, srcs, sizes, count, k, dev, stream ? stream : (void*)0x2) == 0) return 0;
-    }
-    return real ? real(dsts, srcs, sizes, count, attrs, attrs_idx, nattrs, fail_idx, stream) : 1;
 }
 
 __attribute__((visibility("default"))) int cudaHostAlloc(void** p, size_t n, unsigned flags)

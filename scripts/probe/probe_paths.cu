@@ -108,13 +108,6 @@ int main() {
   for (int i=nseg-1;i>0;i--){ int k=rand()%(i+1); std::swap(dofs[i],dofs[k]); }
   ms = timeit(s[0], 3, [&]{ for (int i=0;i<nseg;i++) cudaMemcpyAsync(d+dofs[i], h+so[i], seg, cudaMemcpyHostToDevice, s[0]); });
   printf("per-seg cudaMemcpyAsync 32KiB x %d: %.2f GB/s\n", nseg, gbps(B,ms));
-  { std::vector<void*> ds(nseg), ss(nseg); std::vector<size_t> sz(nseg, seg);
-    for (int i=0;i<nseg;i++){ ds[i]=d+dofs[i]; ss[i]=h+so[i]; }
-    cudaMemcpyAttributes at = {}; at.srcAccessOrder = cudaMemcpySrcAccessOrderStream; size_t idx=0, fail=0;
-    cudaError_t e = cudaMemcpyBatchAsync(ds.data(), ss.data(), sz.data(), nseg, &at, &idx, 1, &fail, s[0]);
-    printf("batch rc %d %s\n", (int)e, cudaGetErrorString(e)); cudaGetLastError();
-    if (!e) { ms = timeit(s[0], 3, [&]{ cudaMemcpyBatchAsync(ds.data(), ss.data(), sz.data(), nseg, &at, &idx, 1, &fail, s[0]); });
-      printf("cudaMemcpyBatchAsync 32KiB x %d: %.2f GB/s\n", nseg, gbps(B,ms)); } }
   long long *dso, *ddo; CK(cudaMalloc(&dso, nseg*8)); CK(cudaMalloc(&ddo, nseg*8));
   cudaMemcpy(dso, so.data(), nseg*8, cudaMemcpyHostToDevice); cudaMemcpy(ddo, dofs.data(), nseg*8, cudaMemcpyHostToDevice);
   for (int grid : {148, 296, 592}) { ms = timeit(s[0], 5, [&]{ zc_gather<<<grid, 512, 0, s[0]>>>(hdev, d, dso, ddo, nseg, seg); });

@@ -80,7 +80,7 @@ def main():
     cfg.fallback_bytes[0] = cfg.fallback_bytes[1] = (1 << 64) - 1
     mma.init(cfg)
     with torch.cuda.stream(s):
-        res = {"mode": "native (cudaMemcpyAsync / cudaMemcpyBatchAsync)",
+        res = {"mode": "native (cudaMemcpyAsync per copy)",
                "contig_h2d": B / timed(lambda: mma.memcpy_h2d(dev, host, B, stream=s), s) / 1e6,
                "contig_d2h": B / timed(lambda: mma.memcpy_d2h(host2, dev, B, stream=s), s) / 1e6,
                "kv_h2d": KB / timed(lambda: mma.memcpy_h2d_segments(*fetch, 0, stream=s), s) / 1e6,

@@ -50,67 +50,6 @@ def test_preload_routes_torch_copies(tmp_path):
     assert r["kernels"] >= 2 and r["relay"] > 0   # relay kernels ran (loopback ring)
 
 
-BATCH_PROG = r"""
-import ctypes, json, sys, torch
-import numpy as np
-sys.path.insert(0, {root!r})
-torch.cuda.init()
-seg, nseg = 64 << 10, 512                                # 32 MiB in 512 scattered blocks
-rng = np.random.default_rng(4)
-pool = torch.randint(0, 256, (2 * nseg * seg,), dtype=torch.uint8).pin_memory()
-cache = torch.zeros(nseg * seg, dtype=torch.uint8, device="cuda")
-back = torch.zeros(2 * nseg * seg, dtype=torch.uint8).pin_memory()
-slots = rng.permutation(2 * nseg)[:nseg]
-blocks = rng.permutation(nseg)
-P = ctypes.c_void_p * nseg
-S = ctypes.c_size_t * nseg
-hs = [pool.data_ptr() + int(s) * seg for s in slots]
-ds = [cache.data_ptr() + int(b) * seg for b in blocks]
-bs = [back.data_ptr() + int(s) * seg for s in slots]
-
-class Loc(ctypes.Structure):
-    _fields_ = [("type", ctypes.c_int), ("id", ctypes.c_int)]
-class Attr(ctypes.Structure):
-    _fields_ = [("order", ctypes.c_int), ("src", Loc), ("dst", Loc), ("flags", ctypes.c_uint)]
-attr = Attr(1, Loc(0, 0), Loc(0, 0), 0)                 # cudaMemcpySrcAccessOrderStream
-idx, fail = ctypes.c_size_t(0), ctypes.c_size_t(0)
-fn = ctypes.CDLL(None).cudaMemcpyBatchAsync             # global scope: the preload's definition
-fn.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p,
-               ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p, ctypes.c_void_p]
-s = torch.cuda.current_stream().cuda_stream
-rc1 = fn(P(*ds), P(*hs), S(*[seg] * nseg), nseg, ctypes.byref(attr), ctypes.byref(idx), 1,
-         ctypes.byref(fail), s)                          # KV fetch: host blocks -> device blocks
-rc2 = fn(P(*bs), P(*ds), S(*[seg] * nseg), nseg, ctypes.byref(attr), ctypes.byref(idx), 1,
-         ctypes.byref(fail), s)                          # offload back to the same slots
-torch.cuda.synchronize()
-import paper_2512_16056_b200 as m
-got = cache.cpu().numpy().reshape(nseg, seg)
-ref = pool.numpy().reshape(2 * nseg, seg)
-st = m.get_stats(0)
-print(json.dumps(dict(rc=[rc1, rc2], fetch=bool(np.array_equal(got[blocks], ref[slots])),
-                      offload=bool(np.array_equal(back.numpy().reshape(2 * nseg, seg)[slots], ref[slots])),
-                      calls=st["calls"], kernels=st["kernels"], err=m.get_last_error())))
-"""
-
-
-def test_preload_routes_batch_copies(tmp_path):
-    """cudaMemcpyBatchAsync (the API paged KV caches swap blocks with) of an unmodified
-    program becomes one scattered multipath copy per batch, bit-exact, in both directions."""
-    import torch
-    if not torch.cuda.is_available():
-        pytest.skip("no CUDA device")
-    lib = ROOT / "paper_2512_16056_b200" / "libmma_preload.so"
-    script = tmp_path / "b.py"
-    script.write_text(BATCH_PROG.format(root=str(ROOT)))
-    env = dict(os.environ, LD_PRELOAD=str(lib), MMA_LOOPBACK="1", MMA_FALLBACK_BYTES="0",
-               MMA_PRELOAD_MIN_BYTES=str(1 << 20), MMA_HOP="2", MMA_CHUNK_BYTES=str(4 << 20))
-    p = subprocess.run([sys.executable, str(script)], env=env, capture_output=True, text=True, timeout=280)
-    assert p.returncode == 0, p.stderr[-3000:]
-    r = json.loads(p.stdout.strip().splitlines()[-1])
-    assert r["rc"] == [0, 0] and r["fetch"] and r["offload"] and r["err"] == 0
-    assert r["calls"] >= 2 and r["kernels"] >= 2     # both batches ran as zero-copy multipath calls
-
-
 PIN_PROG = r"""
 import json, sys, torch
 sys.path.insert(0, {root!r})
