@@ -951,7 +951,7 @@ def main():
                 policy.update({"d2h_single_path": "SM zero-copy scatter (pinned for the line)",
                                "measured_choice": {1: "ce", 2: "zc"}.get(tuned_d2h[0]["seg_mode"], "?"),
                                "d2h_ce_host_order_gbps": ce, "d2h_zc_gbps": zc,
-                               "note": "copy-engine batches run in host-address order (cfg.host_order); "
+                               "note": "copy-engine DMAs (one cudaMemcpyAsync per block) run in host-address order (cfg.host_order); "
                                        "--engine-modes times the engine's own measured choice"})
             if len(mma.get_paths(0, mma.H2D)) > 1 and "fetch" not in w:
                 # the fallback threshold is the measured native/multipath break-even of
@@ -1187,8 +1187,8 @@ def main():
             torch.cuda.synchronize(0)
             a.record(stream)
             s2.wait_event(a)
-            # the cheaper enqueue first: a copy-engine batch of 131,072 descriptors holds the
-            # host for ~74 ms (DESIGN 5.3), a zero-copy launch for ~1 ms
+            # the cheaper enqueue first: a copy-engine path issues one DMA per block (~5 us of
+            # host time each, DESIGN 5.3), a zero-copy launch takes ~1 ms
             mma.memcpy_d2h_segments(*w["offload2"], 0, stream=s2)
             mma.memcpy_h2d_segments(*w["fetch"], 0, stream=stream)
             b1.record(stream)
@@ -1226,7 +1226,7 @@ def main():
                   "host_enqueue_ms_per_step": round(t_issue * 1e3 / nst, 3),
                   "what": "stream gated by a sleep kernel while the steps are enqueued; device time after the "
                           "gate. The enqueue time includes blocking once the GPU's command queue is full "
-                          "(a copy-engine batch of 131,072 descriptors does not fit while gated)"}
+                          "(131,072 per-block copy-engine DMAs do not fit while gated)"}
         assert mma.get_last_error() == 0
     except Exception as ex:  # noqa: BLE001 - evidence only
         preenq = {"error": f"{type(ex).__name__}: {ex}"}
