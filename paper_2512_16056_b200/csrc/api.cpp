@@ -217,7 +217,7 @@ int prepare_segments(int dir, const mma_segment_t* segs, size_t nsegs, int devic
         const void* hp = (dir == MMA_H2D) ? segs[k].src : segs[k].dst;
         int d = -1;
         bool m = false;
-        if (dc.kind((uintptr_t)dp, segs[k].bytes, &d, &m) != MK_DEVICE || d != device) return cudaErrorInvalidValue;
+        if (dc.kind((uintptr_t)dp, segs[k].bytes, &d, &m) != MK_DEVICE || d != phys_dev(device)) return cudaErrorInvalidValue;
         const int hk = hc.kind((uintptr_t)hp, segs[k].bytes, &d, &m);
         if (hk == MK_DEVICE || hk == MK_MIXED) return cudaErrorInvalidValue;
         if (hk == MK_PAGEABLE) {   // pageable or unregistered: the whole table goes native (R7)
@@ -414,9 +414,10 @@ int mma_get_topology(mma_topology_t* out)
     out->ngpu = e.ndev;
     for (int a = 0; a < e.ndev; a++) {
         for (int b = 0; b < e.ndev; b++) out->p2p[a][b] = e.p2p[a][b] ? 1 : 0;
-        CK(cudaDeviceGetAttribute(&out->copy_engines[a], cudaDevAttrAsyncEngineCount, a));
-        CK(cudaDeviceGetAttribute(&out->sms[a], cudaDevAttrMultiProcessorCount, a));
-        CK(cudaDeviceGetPCIBusId(out->bus_id[a], sizeof out->bus_id[a], a));
+        const int pa = phys_dev(a);   // a virtual GPU (MMA_VGPUS) reports its device's values
+        CK(cudaDeviceGetAttribute(&out->copy_engines[a], cudaDevAttrAsyncEngineCount, pa));
+        CK(cudaDeviceGetAttribute(&out->sms[a], cudaDevAttrMultiProcessorCount, pa));
+        CK(cudaDeviceGetPCIBusId(out->bus_id[a], sizeof out->bus_id[a], pa));
         out->numa_node[a] = gpu_numa_node(a);
     }
     for (int i = 0; i < 256; i++) {

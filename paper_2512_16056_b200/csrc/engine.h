@@ -37,5 +37,7 @@ void host_nodes(const void* const* p, size_t n, int* nodes);
 int host_numa_count();
 // NUMA node of a GPU's PCI device from sysfs (-1 = unknown)
 int gpu_numa_node(int dev);
+// plane.cpp: the CUDA device behind engine GPU index g (identity unless MMA_VGPUS)
+int phys_dev(int g);
 
 }  // namespace mma

@@ -223,7 +223,7 @@ void host_nodes(const void* const* p, size_t n, int* nodes)
 int gpu_numa_node(int dev)
 {
     char bus[32] = {0};
-    if (cudaDeviceGetPCIBusId(bus, sizeof bus - 1, dev) != cudaSuccess) {
+    if (cudaDeviceGetPCIBusId(bus, sizeof bus - 1, phys_dev(dev)) != cudaSuccess) {
         cudaGetLastError();
         return -1;
     }

@@ -87,7 +87,8 @@ int slot_of_device(int dev)
     if (dev < 0 || dev >= MMA_MAX_GPUS) return -1;
     if (g_slot_cache[dev] == -2) {
         char bus[32] = {0};
-        if (cudaDeviceGetPCIBusId(bus, sizeof bus - 1, dev) != cudaSuccess) {
+        // a virtual GPU (MMA_VGPUS) shares its device's entry
+        if (cudaDeviceGetPCIBusId(bus, sizeof bus - 1, phys_dev(dev)) != cudaSuccess) {
             cudaGetLastError();
             return -1;
         }
@@ -229,7 +230,7 @@ int mma_ledger_attach(const char* name)
 int mma_device_bus_id(int device, char* buf, int len)
 {
     if (!buf || len < 13) return cudaErrorInvalidValue;
-    return (int)cudaDeviceGetPCIBusId(buf, len, device);
+    return (int)cudaDeviceGetPCIBusId(buf, len, phys_dev(device));
 }
 
 int mma_ledger_unlink(const char* name)

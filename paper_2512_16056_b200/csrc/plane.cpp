@@ -34,6 +34,11 @@ Engine& E()
     return *e;
 }
 
+int phys_dev(int g)
+{
+    return (g >= 0 && g < MMA_MAX_GPUS) ? E().phys[g] : g;
+}
+
 size_t env_size(const char* name, size_t dflt)
 {
     const char* s = getenv(name);
@@ -246,10 +251,12 @@ int make_device(int d)
         for (int k = 0; k < 2; k++)
             for (cudaStream_t s : {ls[k].kern, ls[k].hop[0], ls[k].hop[1], ls[k].direct, ls[k].zc})
                 if (!join_event(s, d)) return cudaErrorMemoryAllocation;
-    CK(cudaDeviceGetAttribute(&r.sms, cudaDevAttrMultiProcessorCount, d));
+    CK(cudaDeviceGetAttribute(&r.sms, cudaDevAttrMultiProcessorCount, phys_dev(d)));
     for (int p = 0; p < e.ndev; p++) {
         if (p == d || !e.p2p[d][p]) continue;
-        cudaError_t pe = peer_denied(d, p) ? cudaErrorPeerAccessUnsupported : cudaDeviceEnablePeerAccess(p, 0);
+        cudaError_t pe = peer_denied(d, p)                  ? cudaErrorPeerAccessUnsupported
+                         : phys_dev(p) == phys_dev(d) ? cudaSuccess   // virtual GPUs of one device
+                                                      : cudaDeviceEnablePeerAccess(phys_dev(p), 0);
         if (pe == cudaErrorPeerAccessAlreadyEnabled) cudaGetLastError();
         else if (pe != cudaSuccess) { cudaGetLastError(); e.p2p[d][p] = false; }   // never a path
     }
@@ -267,12 +274,19 @@ int do_init(const mma_config_t* cfg)
     if (!e.inited) {
         CK(cudaGetDeviceCount(&e.ndev));
         if (e.ndev > MMA_MAX_GPUS) e.ndev = MMA_MAX_GPUS;
+        const int nphys = e.ndev;
+        const int nv = env_int("MMA_VGPUS", 0);
+        e.virt = nphys > 0 && nv > nphys;
+        if (e.virt) e.ndev = std::min(nv, MMA_MAX_GPUS);
+        for (int g = 0; g < MMA_MAX_GPUS; g++) e.phys[g] = (e.virt && g >= nphys) ? g % nphys : g;
         for (int a = 0; a < e.ndev; a++)
             for (int b = 0; b < e.ndev; b++) {
                 int ok = 0, at = 0;
-                if (a != b) {
-                    cudaDeviceCanAccessPeer(&ok, a, b);
-                    if (cudaDeviceGetP2PAttribute(&at, cudaDevP2PAttrNativeAtomicSupported, a, b) != cudaSuccess) {
+                const int pa = e.phys[a], pb = e.phys[b];
+                if (a != b && pa == pb) ok = at = 1;   // two indices of one device (MMA_VGPUS)
+                else if (a != b) {
+                    cudaDeviceCanAccessPeer(&ok, pa, pb);
+                    if (cudaDeviceGetP2PAttribute(&at, cudaDevP2PAttrNativeAtomicSupported, pa, pb) != cudaSuccess) {
                         cudaGetLastError();
                         at = 0;
                     }

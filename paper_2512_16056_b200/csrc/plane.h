@@ -51,12 +51,17 @@ constexpr unsigned kDynSlotWords = 64;    // cursor, counts[MMA_KMAX_RINGS], bac
 constexpr unsigned kDynBackoffWord = 1 + MMA_KMAX_RINGS;
 constexpr unsigned kDynPauseWord = 2 + MMA_KMAX_RINGS;
 
+// The CUDA device behind engine GPU index g: the identity, except under the MMA_VGPUS=k test
+// hook, where indices >= the physical device count are virtual GPUs g % count (plane.cpp).
+int phys_dev(int g);
+
 struct DeviceGuard {
     int prev = -1;
     explicit DeviceGuard(int d)
     {
         cudaGetDevice(&prev);
-        if (d != prev) cudaSetDevice(d);
+        const int p = phys_dev(d);
+        if (p != prev) cudaSetDevice(p);
     }
     ~DeviceGuard()
     {
@@ -157,6 +162,18 @@ struct Engine {
     std::atomic<bool> inited{false};   // read without the mutex by ensure_init's fast path
     mma_config_t cfg{};
     int ndev = 0;
+    // MMA_VGPUS=k (test hook, read at init): the engine sees k GPUs although the box has fewer;
+    // GPU index g >= the physical count is a virtual GPU on CUDA device phys[g] = g % count,
+    // with its own streams, rings, flags, ledger entries and path index. Relays through a
+    // virtual GPU therefore run every code path of a peer relay (relay index != target: the
+    // pack kernel on the relay, cross-index fork/join, gates, peer rings) except the NVLink
+    // transport itself, which a one-GPU box cannot provide.
+    int phys[MMA_MAX_GPUS];
+    bool virt = false;
+    Engine()
+    {
+        for (int g = 0; g < MMA_MAX_GPUS; g++) phys[g] = g;
+    }
     bool p2p[MMA_MAX_GPUS][MMA_MAX_GPUS] = {};
     bool p2p_atomic[MMA_MAX_GPUS][MMA_MAX_GPUS] = {};   // [a][b]: a kernel on a may atomically update b's memory
     DevRes dev[MMA_MAX_GPUS];

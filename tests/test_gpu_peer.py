@@ -11,7 +11,15 @@ claims on a peer's cursor, and cross-device fork/join events. Every case compare
 (with guard bands), the plan and the delivery log with the oracle, the scattered cases the
 path of every byte; two targets relaying through each other at once check that
 concurrent rings on both GPUs stay exact; MMA_DENY_PEER exercises the branch where
-cudaDeviceEnablePeerAccess fails (the pair must never become a path)."""
+cudaDeviceEnablePeerAccess fails (the pair must never become a path).
+
+On a one-GPU box the module runs in the engine's virtual-GPU mode (MMA_VGPUS=2, plane.h):
+GPU index 1 is a second engine GPU on the same device, with its own streams, rings, flags,
+ledger entries and path index, so every code path of a peer relay runs (relay index !=
+target: the pack kernel on the relay, polls and credits on the relay's flags, cross-index
+fork/join and gates, two targets relaying through each other, joint plans) -- everything
+but the NVLink transport. A virtual target's copies go through the segment API, whose
+explicit device names the target."""
 import os
 import subprocess
 import sys
@@ -29,16 +37,62 @@ MiB = 1 << 20
 ROOT = Path(__file__).resolve().parents[1]
 
 
+def _virtual():
+    return torch.cuda.is_available() and torch.cuda.device_count() < 2
+
+
+def _env():
+    """environment of the subprocess tests: the virtual-GPU mode on a one-GPU box"""
+    return dict(os.environ, MMA_VGPUS="2") if _virtual() else dict(os.environ)
+
+
 @pytest.fixture(scope="module")
 def mma():
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
-    if torch.cuda.device_count() < 2:
-        pytest.skip("peer relays need two GPUs; this box exposes one (gpurun is one GPU per call)")
     os.environ.setdefault("MMA_SPIN_TIMEOUT_MS", "8000")
     import paper_2512_16056_b200 as m
-    yield m
-    m.finalize()
+    virtual = _virtual()
+    if virtual:                        # read at init: start from a fresh engine
+        m.finalize()
+        os.environ["MMA_VGPUS"] = "2"
+    try:
+        yield m
+    finally:
+        m.finalize()
+        if virtual:
+            os.environ.pop("MMA_VGPUS", None)
+
+
+def cuda(g):
+    """torch device holding engine GPU g's memory (a virtual GPU's is its device's)"""
+    return f"cuda:{g % torch.cuda.device_count()}"
+
+
+def stream_of(g):
+    return torch.cuda.Stream(device=cuda(g))
+
+
+def sync(*gpus):
+    for d in sorted({g % torch.cuda.device_count() for g in gpus}):
+        torch.cuda.synchronize(d)
+
+
+def h2d(mma, dst, src, B, target, stream):
+    """contiguous H2D into engine GPU `target` (the segment API names a virtual target)"""
+    if target >= torch.cuda.device_count():
+        segs, n = mma.make_segments([src.data_ptr()], [dst.data_ptr()], [B])
+        mma.memcpy_h2d_segments(segs, n, target, stream=stream)
+    else:
+        mma.memcpy_h2d(dst, src, B, stream=stream)
+
+
+def d2h(mma, dst, src, B, target, stream):
+    if target >= torch.cuda.device_count():
+        segs, n = mma.make_segments([src.data_ptr()], [dst.data_ptr()], [B])
+        mma.memcpy_d2h_segments(segs, n, target, stream=stream)
+    else:
+        mma.memcpy_d2h(dst, src, B, stream=stream)
 
 
 CE, ZC, P2P = 1, 2, 3
@@ -64,22 +118,23 @@ def test_contiguous_peer_relay(mma, orc, target, relay, mode, name, dirn):
     B, C, S = 29 * MiB + 4321, MiB, 3
     rc, path, _, fb = orc.plan(bw, B, C, 0, orc.INTERLEAVED)
     assert mma.get_plan(target, dirn, B)[0] == path.tobytes()
+    st = stream_of(target)
     for rep in range(2):                                   # the second call starts mid-ring
         host = pinned(torch, B, seed=0x4D4D41 + rep)
         if dirn == 0:
-            dst = guarded_device(torch, B, dev=target)
-            mma.memcpy_h2d(dst[G:G + B], host, B)
-            torch.cuda.synchronize(target)
-            torch.cuda.synchronize(relay)
+            dst = torch.full((B + 2 * G,), 0xA5, dtype=torch.uint8, device=cuda(target))
+            sync(target)
+            h2d(mma, dst[G:G + B], host, B, target, st)
+            sync(target, relay)
             got = dst.cpu().numpy()
         else:
-            src = torch.empty(B, dtype=torch.uint8, device=f"cuda:{target}")
+            src = torch.empty(B, dtype=torch.uint8, device=cuda(target))
             src.copy_(host[:B])
             out = pinned(torch, B + 2 * G)
             out.fill_(0xA5)
-            mma.memcpy_d2h(out[G:G + B], src, B)
-            torch.cuda.synchronize(target)
-            torch.cuda.synchronize(relay)
+            sync(target)
+            d2h(mma, out[G:G + B], src, B, target, st)
+            sync(target, relay)
             got = out.numpy()
         exp = guarded_host(B)
         assert orc.move_contiguous(exp[G:G + B], host.numpy()[:B], C, bw, path, S=S) == 0
@@ -117,8 +172,7 @@ def test_scattered_peer_relay(mma, orc, mode, name, dirn):
         segs, n = mma.make_segments([base + k * sb for k in range(nseg)],
                                     [out.data_ptr() + int(s) * sb for s in slots], [sb] * nseg)
         mma.memcpy_d2h_segments(segs, n, target)
-    torch.cuda.synchronize(target)
-    torch.cuda.synchronize(relay)
+    sync(target, relay)
     rc, path, _, _ = orc.plan(bw, B, C, 0, orc.INTERLEAVED)
     assert mma.get_delivery_log(target) == path.tobytes()
     assert mma.get_segment_order(target).tolist() == list(range(nseg))   # one node: table order
@@ -144,8 +198,7 @@ def test_dynamic_pull_across_gpus(mma, orc):
     host = pinned(torch, B, seed=5)
     dst = guarded_device(torch, B, dev=target)
     mma.memcpy_h2d(dst[G:G + B], host, B)
-    torch.cuda.synchronize(target)
-    torch.cuda.synchronize(relay)
+    sync(target, relay)
     log = np.frombuffer(mma.get_delivery_log(target), dtype=np.uint8)
     assert log.size == (B + MiB - 1) // MiB and set(log.tolist()) <= {0, 1}
     counts = mma.get_dynamic_counts(target)
@@ -166,13 +219,12 @@ def test_two_targets_relay_through_each_other(mma, orc):
         mma.set_bandwidth(t, 0, [1, 1])
     B = 40 * MiB + 5
     srcs = [pinned(torch, B, seed=90 + t) for t in (0, 1)]
-    dsts = [guarded_device(torch, B, dev=t) for t in (0, 1)]
-    streams = [torch.cuda.Stream(device=t) for t in (0, 1)]
-    for t in (0, 1):
-        torch.cuda.synchronize(t)                 # guard fills done before the copies' streams run
+    dsts = [torch.full((B + 2 * G,), 0xA5, dtype=torch.uint8, device=cuda(t)) for t in (0, 1)]
+    streams = [stream_of(t) for t in (0, 1)]
+    sync(0, 1)                                    # guard fills done before the copies' streams run
     for rep in range(3):
         for t in (0, 1):
-            mma.memcpy_h2d(dsts[t][G:G + B], srcs[t], B, stream=streams[t])
+            h2d(mma, dsts[t][G:G + B], srcs[t], B, t, streams[t])
         for t in (0, 1):
             streams[t].synchronize()
         for t in (0, 1):
@@ -190,22 +242,22 @@ sys.path.insert(0, {root!r})
 import torch
 import paper_2512_16056_b200 as m
 m.init(m.default_config())
-print(json.dumps([[p["gpu"] for p in m.get_paths(t, 0)] for t in range(torch.cuda.device_count())]))
+print(json.dumps([[p["gpu"] for p in m.get_paths(t, 0)] for t in range(m.get_topology()["ngpu"])]))
 """
 
 
 def test_refused_peer_access_is_never_a_path(tmp_path):
-    if not torch.cuda.is_available() or torch.cuda.device_count() < 2:
-        pytest.skip("peer relays need two GPUs; this box exposes one (gpurun is one GPU per call)")
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
     script = tmp_path / "deny.py"
     script.write_text(PROG.format(root=str(ROOT)))
     import json
-    env = dict(os.environ, MMA_DENY_PEER="0,1")
+    env = dict(_env(), MMA_DENY_PEER="0,1")
     p = subprocess.run([sys.executable, str(script)], env=env, capture_output=True, text=True, timeout=240)
     assert p.returncode == 0, p.stderr[-2000:]
     paths = json.loads(p.stdout.strip().splitlines()[-1])
     assert 1 not in paths[0] and 0 not in paths[1], paths
-    p = subprocess.run([sys.executable, str(script)], env=dict(os.environ), capture_output=True, text=True,
+    p = subprocess.run([sys.executable, str(script)], env=_env(), capture_output=True, text=True,
                        timeout=240)
     allowed = json.loads(p.stdout.strip().splitlines()[-1])
     assert 1 in allowed[0] and 0 in allowed[1], allowed
@@ -222,14 +274,12 @@ def test_joint_plan_two_targets(mma, orc, mode, hop):
         mma.set_bandwidth(t, 0, [2, 3] if t == 0 else [3, 2])     # link 0: 2, link 1: 3
     sizes = [48 * MiB + 17, 6 * MiB]
     srcs = [pinned(torch, b, seed=60 + i) for i, b in enumerate(sizes)]
-    dsts = [guarded_device(torch, b, dev=t) for t, b in enumerate(sizes)]
-    st = [torch.cuda.Stream(device=t) for t in (0, 1)]
-    for t in (0, 1):
-        torch.cuda.synchronize(t)
+    dsts = [torch.full((b + 2 * G,), 0xA5, dtype=torch.uint8, device=cuda(t)) for t, b in enumerate(sizes)]
+    st = [stream_of(t) for t in (0, 1)]
+    sync(0, 1)
     mma.memcpy_multi([(0, t, mma.make_segments([srcs[t].data_ptr()], [dsts[t].data_ptr() + G], [sizes[t]]), st[t])
                       for t in (0, 1)])
-    for t in (0, 1):
-        torch.cuda.synchronize(t)
+    sync(0, 1)
     assert mma.get_last_error() == 0
     L = 16 + 8
     bw = [0] * L
@@ -257,13 +307,13 @@ def test_relay_behind_its_own_direct_work(mma, orc):
         mma.set_bandwidth(t, 0, [1, 1])
     Bown = 32 * MiB
     own_src = pinned(torch, Bown, seed=71)
-    own_dst = torch.zeros(Bown, dtype=torch.uint8, device="cuda:1")
-    s1 = torch.cuda.Stream(device=1)
-    torch.cuda.synchronize(1)
+    own_dst = torch.zeros(Bown, dtype=torch.uint8, device=cuda(1))
+    s1 = stream_of(1)
+    sync(1)
     mma.reset_stats(1)
-    with torch.cuda.device(1), torch.cuda.stream(s1):
+    with torch.cuda.device(cuda(1)), torch.cuda.stream(s1):
         torch.cuda._sleep(1_000_000_000)                  # ~0.5 s: GPU 1's own call stays queued
-    mma.memcpy_h2d(own_dst, own_src, Bown, stream=s1)
+    h2d(mma, own_dst, own_src, Bown, 1, s1)
     B = 24 * MiB
     st = mma.get_stats(1)
     # the in-flight call's bytes per link: its direct share on GPU 1's link, its relay share
@@ -275,8 +325,7 @@ def test_relay_behind_its_own_direct_work(mma, orc):
     dst = guarded_device(torch, B, dev=0)
     torch.cuda.synchronize(0)
     mma.memcpy_h2d(dst[G:G + B], src, B)
-    torch.cuda.synchronize(0)
-    torch.cuda.synchronize(1)
+    sync(0, 1)
     exp = guarded_host(B)
     assert orc.move_contiguous(exp[G:G + B], src.numpy()[:B], MiB, [1, 1], exp_plan, S=4) == 0
     assert np.array_equal(dst.cpu().numpy(), exp)
@@ -310,14 +359,14 @@ def test_no_peer_atomics_falls_back_to_copy_engine_ring(tmp_path):
     """a pull ring's kernel updates the relay's credit flags across the link; without native
     peer atomics (MMA_NO_P2P_ATOMICS makes the engine believe so) the relay's copy-engine ring
     carries the chunks instead: no relay kernel, bytes exact"""
-    if not torch.cuda.is_available() or torch.cuda.device_count() < 2:
-        pytest.skip("peer relays need two GPUs; this box exposes one (gpurun is one GPU per call)")
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
     import json
     script = tmp_path / "at.py"
     script.write_text(ATOMICS_PROG.format(root=str(ROOT)))
     outs = {}
     for flag in ("0", "1"):
-        env = dict(os.environ)
+        env = _env()
         if flag == "1":
             env["MMA_NO_P2P_ATOMICS"] = "1"
         p = subprocess.run([sys.executable, str(script)], env=env, capture_output=True, text=True, timeout=240)
