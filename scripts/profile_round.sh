@@ -13,8 +13,10 @@
 #      loopback rings on one GPU, peer rings with --peers on a multi-GPU box)
 mkdir -p gpurun_out
 NCU="ncu --clock-control none"
+[ -x scripts/probe/probe_relay ] || nvcc -O3 -std=c++17 -gencode arch=compute_100a,code=sm_100a -lineinfo \
+    -I include scripts/probe/probe_relay.cu -o scripts/probe/probe_relay
 timeout 900 $NCU --metrics gpu__time_duration.sum -c 400 --csv --log-file gpurun_out/launches_bench.csv \
-    python bench.py --steps 2 --warmup 1 --quick --no-verify --modes ce,zc > gpurun_out/ncu_launch_bench.log 2>&1
+    python bench.py --steps 2 --warmup 1 --quick --no-verify --modes zc,zc > gpurun_out/ncu_launch_bench.log 2>&1
 echo "launch list rc=$?"
 timeout 900 $NCU --set full --import-source on -k regex:zc_copy -c 1 -f -o gpurun_out/prof_zc_h2d \
     python scripts/ncu_one_kernel.py --dir h2d > gpurun_out/ncu_zc_h2d.log 2>&1
