@@ -119,6 +119,22 @@ class Dist:
             self.pg.destroy_process_group()
 
 
+def engine_gpus(torch):
+    """GPUs the engine drives: the visible devices, or more under its virtual-GPU test mode
+    (MMA_VGPUS=k: extra engine GPUs on the same devices -- a functional run of
+    the multi-path bench on one GPU; its rates are not link rates)"""
+    n = torch.cuda.device_count()
+    v = int(os.environ.get("MMA_VGPUS", "0") or 0)
+    return v if v > n > 0 else n
+
+
+def cdev(g):
+    """torch device of engine GPU g (g itself unless g is a virtual GPU, see engine_gpus)"""
+    import torch
+    n = torch.cuda.device_count()
+    return g % n if n and g >= n else g
+
+
 # ---------------------------------------------------------------------- clocks ---
 
 class Clocks:
@@ -134,7 +150,7 @@ class Clocks:
     def start(self):
         try:
             self.p = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
-                                       "-lms", "200", "-i", ",".join(str(g) for g in self.gpus)],
+                                       "-lms", "200", "-i", ",".join(str(g) for g in sorted({cdev(x) for x in self.gpus}))],
                                       stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
         except OSError:
             self.p = None
@@ -170,7 +186,7 @@ def numa_info(torch, gpus):
     gmap = {}
     for g in gpus:
         try:
-            pr = torch.cuda.get_device_properties(g)
+            pr = torch.cuda.get_device_properties(cdev(g))
             bdf = f"{pr.pci_domain_id:04x}:{pr.pci_bus_id:02x}:{pr.pci_device_id:02x}.0"
             gmap[str(g)] = int(Path(f"/sys/bus/pci/devices/{bdf}/numa_node").read_text().strip())
         except (OSError, ValueError, AttributeError):
@@ -277,7 +293,7 @@ class PcieCounters:
         self.N, self.gpus = N, list(gpus)
         self.h = []
         for g in self.gpus:
-            pr = torch.cuda.get_device_properties(g)
+            pr = torch.cuda.get_device_properties(cdev(g))
             bdf = f"{pr.pci_domain_id:08x}:{pr.pci_bus_id:02x}:{pr.pci_device_id:02x}.0"
             self.h.append(N.nvmlDeviceGetHandleByPciBusId(bdf))
         self.fields = [N.NVML_FI_DEV_PCIE_COUNT_RX_BYTES, N.NVML_FI_DEV_PCIE_COUNT_TX_BYTES]
@@ -336,7 +352,7 @@ def pcie_hw_check(torch, mma, w, stream, path_gpus, dynamic):
     cnt = PcieCounters(torch, gset)
     try:
         for g in gset:
-            torch.cuda.synchronize(g)
+            torch.cuda.synchronize(cdev(g))
         out = {"source": "NVML_FI_DEV_PCIE_COUNT_{RX,TX}_BYTES (32-bit, unwrapped by a sampler thread)",
                "note": "counters include TLP/DLLP protocol overhead (~8% H2D, ~9.5% D2H on one B200 link) "
                        "and idle background traffic (~16 KB/ms)"}
@@ -346,7 +362,7 @@ def pcie_hw_check(torch, mma, w, stream, path_gpus, dynamic):
             na = cnt.nvlink_kib()
             run_half(mma, w, 0, stream, half)
             for g in gset:
-                torch.cuda.synchronize(g)
+                torch.cuda.synchronize(cdev(g))
             b = cnt.mark()
             nb = cnt.nvlink_kib()
             st = mma.get_stats(0)
@@ -470,12 +486,12 @@ def pcie_rate(torch, g, nbytes=GiB, reps=8):
     """Solo native cudaMemcpyAsync GB/s of GPU g's PCIe link per direction (the roofline's
     PCIe term and R(1))."""
     h = torch.empty(nbytes, dtype=torch.uint8).pin_memory()
-    d = torch.empty(nbytes, dtype=torch.uint8, device=f"cuda:{g}")
-    s = torch.cuda.Stream(device=g)
+    d = torch.empty(nbytes, dtype=torch.uint8, device=f"cuda:{cdev(g)}")
+    s = torch.cuda.Stream(device=cdev(g))
     out = {}
     for name in ("h2d", "d2h"):
         best = 1e9
-        with torch.cuda.device(g), torch.cuda.stream(s):
+        with torch.cuda.device(cdev(g)), torch.cuda.stream(s):
             for _ in range(reps):
                 a = torch.cuda.Event(enable_timing=True)
                 b = torch.cuda.Event(enable_timing=True)
@@ -513,17 +529,17 @@ def conc_rate(torch, gpus, per_gpu=512 * MiB, reps=3):
     shared switch uplinks and the host-memory ceiling."""
     k = len(gpus)
     host = torch.empty(k * per_gpu, dtype=torch.uint8).pin_memory()
-    devs = [torch.empty(per_gpu, dtype=torch.uint8, device=f"cuda:{g}") for g in gpus]
-    streams = [torch.cuda.Stream(device=g) for g in gpus]
+    devs = [torch.empty(per_gpu, dtype=torch.uint8, device=f"cuda:{cdev(g)}") for g in gpus]
+    streams = [torch.cuda.Stream(device=cdev(g)) for g in gpus]
     out = {}
     for name in ("h2d", "d2h"):
         best = 1e9
         for _ in range(reps):
             for g in gpus:
-                torch.cuda.synchronize(g)
+                torch.cuda.synchronize(cdev(g))
             t0 = time.perf_counter()
             for i, g in enumerate(gpus):
-                with torch.cuda.device(g), torch.cuda.stream(streams[i]):
+                with torch.cuda.device(cdev(g)), torch.cuda.stream(streams[i]):
                     sl = host[i * per_gpu:(i + 1) * per_gpu]
                     if name == "h2d":
                         devs[i].copy_(sl, non_blocking=True)
@@ -543,18 +559,18 @@ def nvlink_rate(torch, target, relays, per_gpu=512 * MiB, reps=3):
     to (from) the target concurrently; wall time around the whole set, best of reps."""
     if not relays:
         return None
-    tgt = [torch.empty(per_gpu, dtype=torch.uint8, device=f"cuda:{target}") for _ in relays]
-    src = [torch.empty(per_gpu, dtype=torch.uint8, device=f"cuda:{g}") for g in relays]
-    streams = [torch.cuda.Stream(device=g) for g in relays]
+    tgt = [torch.empty(per_gpu, dtype=torch.uint8, device=f"cuda:{cdev(target)}") for _ in relays]
+    src = [torch.empty(per_gpu, dtype=torch.uint8, device=f"cuda:{cdev(g)}") for g in relays]
+    streams = [torch.cuda.Stream(device=cdev(g)) for g in relays]
     out = {}
     for name in ("ingress", "egress"):
         best = 1e9
         for _ in range(reps):
             for g in [target] + list(relays):
-                torch.cuda.synchronize(g)
+                torch.cuda.synchronize(cdev(g))
             t0 = time.perf_counter()
             for i, g in enumerate(relays):
-                with torch.cuda.device(g), torch.cuda.stream(streams[i]):
+                with torch.cuda.device(cdev(g)), torch.cuda.stream(streams[i]):
                     if name == "ingress":
                         tgt[i].copy_(src[i], non_blocking=True)
                     else:
@@ -763,43 +779,43 @@ def run_contention(args, dist, torch, mma, visible_sets):
         dist.barrier()
         return
     widen_visible(dist, visible_sets)
-    k = max(1, min(args.gpus, torch.cuda.device_count()))
+    k = max(1, min(args.gpus, engine_gpus(torch)))
     gpus = list(range(k))
     shard = int(17_640_734_720 * args.contention_scale) // 4096 * 4096
     hosts, devs, streams = [], [], []
     for g in gpus:
         p = mma.host_alloc(shard)
         hosts.append(p)
-        devs.append(torch.empty(shard, dtype=torch.uint8, device=f"cuda:{g}"))
-        streams.append(torch.cuda.Stream(device=g))
+        devs.append(torch.empty(shard, dtype=torch.uint8, device=f"cuda:{cdev(g)}"))
+        streams.append(torch.cuda.Stream(device=cdev(g)))
     tokens = max(256, int(32768 * args.contention_scale) // 16 * 16)
     kvs = []
     for g in gpus[:2]:
         shape = W.scaled_kv(tokens)
         ho, do, sb, hpool, dbytes = W.kv_segments(shape, SEED + g)
         pool = mma.host_alloc(hpool)
-        cache = torch.empty(dbytes, dtype=torch.uint8, device=f"cuda:{g}")
+        cache = torch.empty(dbytes, dtype=torch.uint8, device=f"cuda:{cdev(g)}")
         lens = np.full(len(ho), sb, dtype=np.int64)
         kvs.append((g, mma.make_segments(pool + ho, cache.data_ptr() + do, lens), int(lens.sum()), cache,
-                    torch.cuda.Stream(device=g)))
+                    torch.cuda.Stream(device=cdev(g))))
     total = shard * k + sum(x[2] for x in kvs)
 
     reload_segs = [mma.make_segments([hosts[i]], [devs[i].data_ptr()], [shard]) for i in range(k)]
 
     def batch(joint):
         for g in gpus:
-            torch.cuda.synchronize(g)
+            torch.cuda.synchronize(cdev(g))
         t0 = time.perf_counter()
         if joint:      # one joint plan for the whole batch (mma_memcpy_multi, NEXT-1)
             mma.memcpy_multi([(mma.H2D, g, reload_segs[i], streams[i]) for i, g in enumerate(gpus)] +
                              [(mma.H2D, g, segs, s) for g, segs, nb, cache, s in kvs])
         else:          # one call per transfer, each planned against the ledger's backlog
-            for i, g in enumerate(gpus):
-                mma.memcpy_h2d(devs[i], hosts[i], shard, stream=streams[i])
+            for i, g in enumerate(gpus):      # one segment = the contiguous copy into GPU g
+                mma.memcpy_h2d_segments(*reload_segs[i], g, stream=streams[i])
             for g, segs, nb, cache, s in kvs:
                 mma.memcpy_h2d_segments(*segs, g, stream=s)
         for g in gpus:
-            torch.cuda.synchronize(g)
+            torch.cuda.synchronize(cdev(g))
         return time.perf_counter() - t0
 
     def measure(native, joint=False):
@@ -871,7 +887,7 @@ def main():
         return
 
     vis_note = widen_visible(dist, visible_sets)
-    ngpu_vis = torch.cuda.device_count()
+    ngpu_vis = engine_gpus(torch)
     k = max(1, min(args.gpus, ngpu_vis))
     dev = torch.device("cuda:0")
     torch.cuda.set_device(0)
@@ -1061,7 +1077,7 @@ def main():
     dist.barrier()
     dist.barrier()
     for g in path_gpus:
-        torch.cuda.synchronize(g)
+        torch.cuda.synchronize(cdev(g))
     clocks.start()
     time.sleep(0.3)
     t_start = torch.cuda.Event(enable_timing=True)
@@ -1073,7 +1089,7 @@ def main():
         run_step(mma, w, 0, stream, evs[i])
     t_end.record(stream)
     for g in path_gpus:
-        torch.cuda.synchronize(g)
+        torch.cuda.synchronize(cdev(g))
     ru1, w1 = resource.getrusage(resource.RUSAGE_SELF), time.perf_counter()
     clk = clocks.stop()
     # host CPU the engine needs (the paper's Fig 13 / P:934: two busy threads per GPU cost
@@ -1354,7 +1370,8 @@ def main():
                    "fallback_bytes": thresholds or fallback_cfg,
                    "fallback_how": "measured break-even (mma_tune_threshold)" if thresholds else "default (2 chunks)", "l2": f"inputs ({w['bytes'] / GiB:.1f} GiB per direction) exceed the 126 MB L2; no flush",
                    "parallelism": f"1 process drives {k} path GPU(s); torchrun ranks>0 idle on gloo",
-                   "visible_devices": vis_note, "multipath_error": multipath_error},
+                   "visible_devices": vis_note, "multipath_error": multipath_error,
+                   "virtual_gpus": (ngpu_vis - torch.cuda.device_count()) or None},
         "per_direction": {"h2d_gbps": round(h2d_gbps, 2), "d2h_gbps": round(d2h_gbps, 2),
                           "h2d_ms": round(h2d_ms, 3), "d2h_ms": round(d2h_ms, 3)},
         "path_roofline": path_roof,

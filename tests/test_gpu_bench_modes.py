@@ -21,11 +21,11 @@ def _line(out):
     return json.loads(lines[-1])
 
 
-def _bench(args, torchrun=0, timeout=700):
+def _bench(args, torchrun=0, timeout=700, env_extra=None):
     import torch
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
-    env = dict(os.environ, MMA_SPIN_TIMEOUT_MS="8000")
+    env = dict(os.environ, MMA_SPIN_TIMEOUT_MS="8000", **(env_extra or {}))
     if torchrun:
         s = socket.socket(); s.bind(("127.0.0.1", 0)); port = s.getsockname()[1]; s.close()
         cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={torchrun}",
@@ -63,3 +63,20 @@ def test_mp_two_ranks():
 def test_torchrun_two_ranks_default_line():
     r = _bench(["--gpus", "2", "--tokens", "2048", "--steps", "2", "--warmup", "3", "--quick"], torchrun=2)
     assert r["n_gpus"] == 2 and r["verify"]["mismatched_bytes"] == 0
+
+
+def test_torchrun_four_ranks_virtual_gpus():
+    """the driver's N = 4 scaling launch with k = 4 paths into GPU 0 -- per-path tuning, the
+    concurrent calibration, the k = 1 / 2 re-runs (per_path_count), NVML counters and the
+    multi-path roofline -- end to end; on a one-GPU box through the engine's virtual GPUs
+    (MMA_VGPUS), where the four paths share one link"""
+    import torch
+    extra = {"MMA_VGPUS": "4"} if torch.cuda.is_available() and torch.cuda.device_count() < 4 else {}
+    r = _bench(["--gpus", "4", "--tokens", "2048", "--steps", "2", "--warmup", "3"], torchrun=4,
+               env_extra=extra)
+    assert r["n_gpus"] == 4 and r["config"]["paths"] == 4 and r["verify"]["mismatched_bytes"] == 0
+    assert r["config"]["multipath_error"] is None
+    # a planned step counts its relay bytes at enqueue; a dynamic-pull step's split is known
+    # only on the device (mma_get_dynamic_counts), so the stat stays 0 there
+    assert r["engine"]["relay_bytes"] > 0 or r["plan"]["chosen"] == "dynamic"
+    assert set(r["per_path_count"]) == {"1", "2", "4"}
