@@ -150,7 +150,7 @@ class Clocks:
     def start(self):
         try:
             self.p = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
-                                       "-lms", "200", "-i", ",".join(str(g) for g in sorted({cdev(x) for x in self.gpus}))],
+                                       "-lms", os.environ.get("MMA_BENCH_SMI_MS", "200"), "-i", ",".join(str(g) for g in sorted({cdev(x) for x in self.gpus}))],
                                       stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
         except OSError:
             self.p = None
