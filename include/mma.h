@@ -157,6 +157,9 @@ typedef struct {
 
 typedef struct {
     uint64_t calls, fallbacks, bytes;
+    /* path_bytes / path_chunks / relay_bytes count PLANNED work at enqueue; a dynamic-pull
+     * call (plan_mode 2) splits on the device, so it adds to none of them: its split is
+     * mma_get_dynamic_counts after completion (its bytes stay in `bytes`) */
     uint64_t path_bytes[2][MMA_MAX_PATHS];   /* [direction][path] of this target */
     uint64_t path_chunks[2][MMA_MAX_PATHS];
     uint64_t relay_bytes;                 /* bytes that crossed NVLink (relayed) */
