@@ -39,6 +39,31 @@ def mma():
 @pytest.mark.parametrize("scattered", [False, True], ids=["contig", "segments"])
 def test_forward_only_after_staging(mma, orc, S, scattered, hop):
     configure(mma, loopback=2, chunk=MiB, slots=S, plan_mode=1, hop=(hop, hop))
+    _forward_case(mma, orc, S, scattered)
+
+
+@pytest.mark.parametrize("hop", [1, 4], ids=["pull", "push"])
+@pytest.mark.parametrize("S", [1, 3])
+@pytest.mark.parametrize("scattered", [False, True], ids=["contig", "segments"])
+def test_forward_only_after_staging_relay_gpus(mma, orc, S, scattered, hop):
+    """the same with the rings on two other engine GPUs (real peers on a multi-GPU box,
+    virtual GPUs on one: MMA_VGPUS): the D2H pack kernel then runs on the relay
+    GPU, the H2D pull kernel polls the relay's flags"""
+    virtual = torch.cuda.device_count() < 3
+    if virtual:
+        mma.finalize()
+        os.environ["MMA_VGPUS"] = "3"
+    try:
+        configure(mma, loopback=0, chunk=MiB, slots=S, plan_mode=1, hop=(hop, hop), paths=[0, 1, 2])
+        assert [p["gpu"] for p in mma.get_paths(0, mma.H2D)] == [0, 1, 2]
+        _forward_case(mma, orc, S, scattered)
+    finally:
+        if virtual:
+            mma.finalize()
+            os.environ.pop("MMA_VGPUS", None)
+
+
+def _forward_case(mma, orc, S, scattered):
     bw = [1, 2, 2]
     mma.set_bandwidth(0, mma.H2D, bw)
     mma.set_bandwidth(0, mma.D2H, bw)
