@@ -20,7 +20,9 @@ import paper_2512_16056_b200 as m
 cfg = m.default_config()
 cfg.chunk_bytes[0] = cfg.chunk_bytes[1] = 1 << 20
 cfg.fallback_bytes[0] = cfg.fallback_bytes[1] = 0
-cfg.loopback_relays = 1
+cfg.loopback_relays = {loopback}
+if not cfg.loopback_relays:                    # the ring on engine GPU 1 (a peer or a virtual GPU)
+    cfg.npaths, cfg.path_gpus[0], cfg.path_gpus[1] = 2, 0, 1
 cfg.hop_mode[0] = cfg.hop_mode[1] = m.HOP_CE
 cfg.ring_slots = 2
 m.init(cfg)
@@ -49,13 +51,16 @@ print(json.dumps(dict(err=err, refused=refused, secs=time.time() - t0, ok=bool(t
 """
 
 
-def test_dropped_publish_times_out_cleanly(tmp_path):
+@pytest.mark.parametrize("relay", ["loopback", "relay_gpu"])
+def test_dropped_publish_times_out_cleanly(tmp_path, relay):
     import torch
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
     script = tmp_path / "f.py"
-    script.write_text(PROG.format(root=str(ROOT)))
+    script.write_text(PROG.format(root=str(ROOT), loopback=1 if relay == "loopback" else 0))
     env = dict(os.environ, MMA_FAULT_DROP_PUBLISH="3", MMA_SPIN_TIMEOUT_MS="1500")
+    if relay != "loopback" and torch.cuda.device_count() < 2:
+        env["MMA_VGPUS"] = "2"               # the engine's virtual GPU 1
     p = subprocess.run([sys.executable, str(script)], env=env, capture_output=True, text=True, timeout=240)
     assert p.returncode == 0, p.stderr[-3000:]
     r = json.loads(p.stdout.strip().splitlines()[-1])

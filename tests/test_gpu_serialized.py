@@ -36,7 +36,7 @@ from gpu_util import configure, pinned, guarded_device, guarded_host, G
 out = {{}}
 C = 1 << 20
 S = {slots}
-configure(m, loopback=2, chunk=C, slots=S, plan_mode=1, hop=(1, 1), ctas=4)
+configure(m, chunk=C, slots=S, plan_mode=1, hop=(1, 1), ctas=4, **{relays})
 bw = [2, 3, 3]
 m.set_bandwidth(0, m.H2D, bw)
 m.set_bandwidth(0, m.D2H, bw)
@@ -84,14 +84,27 @@ print(json.dumps(out))
 """
 
 
+def _relays(kind):
+    """two relay paths: loopback rings on GPU 0, or rings on engine GPUs 1 and 2 (real peers
+    when the box has three GPUs, else the engine's virtual GPUs): then the
+    D2H pack kernel runs on the relay GPU and the hops on the relay's own streams"""
+    import torch
+    if kind == "loopback":
+        return "dict(loopback=2)", {}
+    env = {"MMA_VGPUS": "3"} if torch.cuda.device_count() < 3 else {}
+    return "dict(loopback=0, paths=[0, 1, 2])", env
+
+
+@pytest.mark.parametrize("relays", ["loopback", "relay_gpus"])
 @pytest.mark.parametrize("slots", [1, 2, 4])
-def test_rings_complete_with_serialised_launches(tmp_path, slots):
+def test_rings_complete_with_serialised_launches(tmp_path, slots, relays):
     import torch
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
     script = tmp_path / "s.py"
-    script.write_text(PROG.format(root=str(ROOT), slots=slots))
-    env = dict(os.environ, CUDA_LAUNCH_BLOCKING="1", MMA_SPIN_TIMEOUT_MS="3000", PYTHONPATH=str(ROOT))
+    rel, renv = _relays(relays)
+    script.write_text(PROG.format(root=str(ROOT), slots=slots, relays=rel))
+    env = dict(os.environ, CUDA_LAUNCH_BLOCKING="1", MMA_SPIN_TIMEOUT_MS="3000", PYTHONPATH=str(ROOT), **renv)
     p = subprocess.run([sys.executable, str(script)], env=env, capture_output=True, text=True, timeout=500)
     assert p.returncode == 0, p.stderr[-3000:]
     r = json.loads(p.stdout.strip().splitlines()[-1])
@@ -110,7 +123,7 @@ from gpu_util import configure, pinned, guarded_device, guarded_host, G
 
 C = 1 << 20
 S = 2
-configure(m, loopback=2, chunk=C, slots=S, plan_mode=1, hop=({hop}, {hop}), ctas=4)
+configure(m, chunk=C, slots=S, plan_mode=1, hop=({hop}, {hop}), ctas=4, **{relays})
 bw = [1, 1, 1]
 m.set_bandwidth(0, m.H2D, bw)
 m.set_bandwidth(0, m.D2H, bw)
@@ -167,16 +180,18 @@ for rep in range(2):
 """
 
 
+@pytest.mark.parametrize("relays", ["loopback", "relay_gpus"])
 @pytest.mark.parametrize("direction", ["h2d", "d2h"])
 @pytest.mark.parametrize("hop", [1, 3], ids=["kernel_ring", "ce_p2p_ring"])
-def test_hop_failure_mid_call_poisons_and_remakes_rings(tmp_path, direction, hop):
+def test_hop_failure_mid_call_poisons_and_remakes_rings(tmp_path, direction, hop, relays):
     import torch
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
     script = tmp_path / "f.py"
     code = H2D_CODE if direction == "h2d" else D2H_CODE
-    script.write_text(FAULT_PROG.format(root=str(ROOT), hop=hop, direction_code=code))
-    env = dict(os.environ, MMA_FAULT_FAIL_HOP="5", MMA_SPIN_TIMEOUT_MS="5000", PYTHONPATH=str(ROOT))
+    rel, renv = _relays(relays)
+    script.write_text(FAULT_PROG.format(root=str(ROOT), hop=hop, direction_code=code, relays=rel))
+    env = dict(os.environ, MMA_FAULT_FAIL_HOP="5", MMA_SPIN_TIMEOUT_MS="5000", PYTHONPATH=str(ROOT), **renv)
     p = subprocess.run([sys.executable, str(script)], env=env, capture_output=True, text=True, timeout=300)
     assert p.returncode == 0, p.stderr[-3000:]
     r = json.loads(p.stdout.strip().splitlines()[-1])
