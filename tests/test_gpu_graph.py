@@ -309,3 +309,52 @@ def test_two_calls_in_one_capture(mma):
         torch.cuda.synchronize()
         assert torch.equal(d1.cpu(), s1[:B]) and torch.equal(d2.cpu(), s2[:B]), seed
     assert mma.get_last_error() == 0
+
+
+@pytest.mark.parametrize("dirn", [0, 1], ids=["h2d", "d2h"])
+@pytest.mark.parametrize("mode", ["zc", "ce_p2p"])
+def test_captured_relay_on_another_gpu(mma, dirn, mode):
+    """the relay path on engine GPU 1 (a peer on a multi-GPU box, else the engine's virtual GPU
+    on the same device): the capture joins the relay GPU's capture lanes, and
+    every replay moves the current bytes through it"""
+    virtual = torch.cuda.device_count() < 2
+    if virtual:
+        mma.finalize()
+        os.environ["MMA_VGPUS"] = "2"
+    try:
+        configure(mma, loopback=0, chunk=MiB, slots=4, debug=0, paths=[0, 1])
+        assert [p["gpu"] for p in mma.get_paths(0, dirn)] == [0, 1]
+        mma.set_path_modes(0, dirn, [mma.HOP_CE, mma.HOP_ZC if mode == "zc" else mma.HOP_CE_P2P])
+        mma.set_bandwidth(0, dirn, [1, 1])
+        B = 20 * MiB + 4096 + 48
+        host = pinned(torch, B, seed=5)
+        dev = torch.zeros(B, dtype=torch.uint8, device="cuda")
+
+        def copy():
+            if dirn == 0:
+                mma.memcpy_h2d(dev, host, B)
+            else:
+                mma.memcpy_d2h(host, dev, B)
+        copy()
+        torch.cuda.synchronize()
+        r0 = mma.get_stats(0)["relay_bytes"]
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            copy()
+        assert mma.get_stats(0)["relay_bytes"] > r0            # the relay took part in the capture
+        for seed in (71, 72, 73):
+            if dirn == 0:
+                mma_inputs.fill_pattern(host.numpy()[:B], seed)
+            else:
+                mma.fill_pattern(dev, B, seed, 0)
+                torch.cuda.synchronize()
+                host.numpy()[:] = 0
+            g.replay()
+            torch.cuda.synchronize()
+            assert torch.equal(dev.cpu(), host[:B]), seed
+        del g
+        assert mma.get_last_error() == 0
+    finally:
+        if virtual:
+            mma.finalize()
+            os.environ.pop("MMA_VGPUS", None)
