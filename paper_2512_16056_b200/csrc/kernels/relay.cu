@@ -47,23 +47,55 @@ __device__ __forceinline__ void ring_abort(const RelayLaunchArg& A, const RingAr
 }
 
 // Spin (thread 0 only) until pred(*flag) holds; false on timeout or a peer's abort. *seen =
-// the last value read (the one that satisfied pred on success).
+// the last value read (the one that satisfied pred on success). Polls are relaxed loads of
+// the (device-memory) flag with an exponential backoff (kSpinMinNs .. kSpinMaxNs); the
+// acquire fence is taken once, on success. The abort word lives in mapped HOST memory, and
+// reading host memory from waiting CTAs throttles the copy engines of the same GPU: 16 CTAs
+// reading a host word every ~0.5 us cut a concurrent 1 GiB H2D DMA from 55.6 to 30 GB/s, 56
+// CTAs to 8.9 (D2H: 13 and 2.8), while device-memory polls of any kind cost nothing
+// (scripts/probe/probe_spin_ce.cu, profiles/r02_probe_spin_ce.txt). Relay kernels wait
+// next to their own rings' DMAs, so the abort word is read only every kErrCheckNs (10 ms):
+// a peer's abort still ends the wait within 10 ms.
+#ifndef MMA_SPIN_MIN_NS
+#define MMA_SPIN_MIN_NS 32
+#endif
+#ifndef MMA_SPIN_MAX_NS
+#define MMA_SPIN_MAX_NS 512
+#endif
+#ifndef MMA_ERR_CHECK_NS
+#define MMA_ERR_CHECK_NS 10000000
+#endif
+constexpr unsigned kSpinMinNs = MMA_SPIN_MIN_NS, kSpinMaxNs = MMA_SPIN_MAX_NS;
+constexpr uint64_t kErrCheckNs = MMA_ERR_CHECK_NS;
+
 template <typename Pred>
 __device__ __forceinline__ bool spin_until(const RelayLaunchArg& A, const uint64_t* flag, Pred pred, uint64_t* seen)
 {
-    uint64_t t0 = 0;
-    for (uint32_t it = 0;; it++) {
+    const uint64_t t0 = globaltimer_ns();
+    uint64_t next_err = t0 + kErrCheckNs;
+    unsigned ns = kSpinMinNs;
+    for (;;) {
+#ifdef MMA_SPIN_ACQUIRE
         const uint64_t v = ld_acquire_sys(flag);
+#else
+        const uint64_t v = ld_relaxed_sys(flag);
+#endif
         *seen = v;
-        if (pred(v)) return true;
-        if (v >= kReleaseAll) return false;              // ring aborted elsewhere
-        if ((it & 255) == 0) {
-            const uint64_t t = globaltimer_ns();
-            if (it == 0) t0 = t;
-            else if (t - t0 > A.timeout_ns) return false;
-            if (A.err && *(volatile int*)A.err) return false;
+        if (pred(v)) {
+#ifndef MMA_SPIN_ACQUIRE
+            fence_acq_rel_sys();
+#endif
+            return true;
         }
-        __nanosleep(64);
+        if (v >= kReleaseAll) return false;              // ring aborted elsewhere
+        const uint64_t t = globaltimer_ns();
+        if (t - t0 > A.timeout_ns) return false;
+        if (t >= next_err) {
+            if (A.err && *(volatile int*)A.err) return false;
+            next_err = t + kErrCheckNs;
+        }
+        __nanosleep(ns);
+        if (ns < kSpinMaxNs) ns <<= 1;
     }
 }
 
