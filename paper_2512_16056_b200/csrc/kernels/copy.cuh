@@ -26,16 +26,13 @@ __device__ __forceinline__ uint64_t ld_acquire_sys(const uint64_t* p)
 }
 
 // a relaxed system-scope poll: no L1 invalidation per read (an acquire load is a load plus
-// CCTL.IVALL in SASS); a poll that succeeds is followed by fence_acq_rel_sys, the PTX
-// "acquire pattern" (relaxed read + fence) that orders everything after it
+// CCTL.IVALL in SASS); a poll that succeeds is confirmed by one ld_acquire_sys
 __device__ __forceinline__ uint64_t ld_relaxed_sys(const uint64_t* p)
 {
     uint64_t v;
     asm volatile("ld.relaxed.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
     return v;
 }
-
-__device__ __forceinline__ void fence_acq_rel_sys() { asm volatile("fence.acq_rel.sys;" ::: "memory"); }
 
 __device__ __forceinline__ void st_release_sys(uint64_t* p, uint64_t v)
 {

@@ -48,8 +48,8 @@ __device__ __forceinline__ void ring_abort(const RelayLaunchArg& A, const RingAr
 
 // Spin (thread 0 only) until pred(*flag) holds; false on timeout or a peer's abort. *seen =
 // the last value read (the one that satisfied pred on success). Polls are relaxed loads of
-// the (device-memory) flag with an exponential backoff (kSpinMinNs .. kSpinMaxNs); the
-// acquire fence is taken once, on success. The abort word lives in mapped HOST memory, and
+// the (device-memory) flag with an exponential backoff (kSpinMinNs .. kSpinMaxNs); one
+// acquire load is taken on success. The abort word lives in mapped HOST memory, and
 // reading host memory from waiting CTAs throttles the copy engines of the same GPU: 16 CTAs
 // reading a host word every ~0.5 us cut a concurrent 1 GiB H2D DMA from 55.6 to 30 GB/s, 56
 // CTAs to 8.9 (D2H: 13 and 2.8), while device-memory polls of any kind cost nothing
@@ -81,12 +81,14 @@ __device__ __forceinline__ bool spin_until(const RelayLaunchArg& A, const uint64
         const uint64_t v = ld_relaxed_sys(flag);
 #endif
         *seen = v;
-        if (pred(v)) {
-#ifndef MMA_SPIN_ACQUIRE
-            fence_acq_rel_sys();
+#ifdef MMA_SPIN_ACQUIRE
+        if (pred(v)) return true;
+#else
+        // the flag satisfied the wait: one acquire load of it (flags never move past a value
+        // a waiter still needs, so it satisfies pred again) orders the slot reads after it --
+        // cheaper than a fence.acq_rel.sys (a MEMBAR.SYS) and the same acquire
+        if (pred(v) && pred(*seen = ld_acquire_sys(flag))) return true;
 #endif
-            return true;
-        }
         if (v >= kReleaseAll) return false;              // ring aborted elsewhere
         const uint64_t t = globaltimer_ns();
         if (t - t0 > A.timeout_ns) return false;
