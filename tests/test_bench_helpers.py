@@ -131,3 +131,21 @@ def test_committed_bench_line_has_the_contract_keys():
     assert d["gpu_launches"] > 0
     for k in ("sm_mhz", "sm_max_mhz", "reasons"):
         assert k in d["clocks"], k
+
+
+def test_engine_gpu_indices_map_to_torch_devices(monkeypatch):
+    """virtual-GPU mode (MMA_VGPUS): the bench drives more engine GPUs than
+    torch sees and places a virtual GPU's buffers and streams on device g mod count; with
+    the variable unset (or not above the device count) every index is its own device"""
+    import torch
+    monkeypatch.setattr(torch.cuda, "device_count", lambda: 2)
+    monkeypatch.delenv("MMA_VGPUS", raising=False)
+    assert bench.engine_gpus(torch) == 2
+    assert [bench.cdev(g) for g in range(2)] == [0, 1]
+    monkeypatch.setenv("MMA_VGPUS", "2")
+    assert bench.engine_gpus(torch) == 2
+    monkeypatch.setenv("MMA_VGPUS", "8")
+    assert bench.engine_gpus(torch) == 8
+    assert [bench.cdev(g) for g in range(8)] == [0, 1, 0, 1, 0, 1, 0, 1]
+    monkeypatch.setattr(torch.cuda, "device_count", lambda: 0)     # no GPU: nothing to map
+    assert bench.engine_gpus(torch) == 0 and bench.cdev(3) == 3
