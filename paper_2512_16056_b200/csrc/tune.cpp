@@ -78,7 +78,6 @@ static int tune_paths(Job proto, int reps, std::vector<uint32_t>& mbps, std::vec
     }
     int rc = cudaSuccess;
     for (int p = 0; p < P && rc == cudaSuccess; p++) {
-        float best_rate = 0.f;
         // candidates in order of SM use: a relay's all-copy-engine ring uses none, the kernel
         // ring the relay kernel, zero-copy its own grid; a later candidate must win by 2%
         const bool relay = ps[p].kind == MMA_PATH_RELAY;
@@ -86,9 +85,21 @@ static int tune_paths(Job proto, int reps, std::vector<uint32_t>& mbps, std::vec
         if (relay) cands.push_back(MMA_HOP_CE_P2P);
         cands.push_back(MMA_HOP_CE);
         if (relay) cands.push_back(MMA_HOP_PUSH);
-        cands.push_back(MMA_HOP_ZC);
-        for (int m : cands) {
-            if (m == MMA_HOP_ZC && !proto.mapped) continue;
+        if (proto.mapped) cands.push_back(MMA_HOP_ZC);
+        // zero-copy is measured first: a copy-engine candidate whose warm-up run's host issue
+        // alone (x P, see above) bounds it below 0.8 of the zero-copy rate cannot be chosen,
+        // so its timed runs are skipped -- a scattered table costs the copy engine one DMA per
+        // piece (~5 us each since the batched API closed, DESIGN §5 item 11), i.e. seconds per
+        // candidate run at config-3 size. The choice itself is made below in SM-use order.
+        std::vector<float> rate_of(cands.size(), 0.f);
+        std::vector<size_t> order;
+        for (size_t c = 0; c < cands.size(); c++)
+            if (cands[c] == MMA_HOP_ZC) order.push_back(c);
+        for (size_t c = 0; c < cands.size(); c++)
+            if (cands[c] != MMA_HOP_ZC) order.push_back(c);
+        float zc_rate = 0.f;
+        for (size_t c : order) {
+            const int m = cands[c];
             for (int q = 0; q < P; q++) bw[q] = (q == p) ? 1 : 0;
             md[p] = m;
             float best = 1e30f, best_issue = 1e30f;
@@ -110,15 +121,23 @@ static int tune_paths(Job proto, int reps, std::vector<uint32_t>& mbps, std::vec
                     best = std::min(best, ms);
                     best_issue = std::min(best_issue, issue_ms);
                 }
+                if (rep == 0 && m != MMA_HOP_ZC && zc_rate > 0.f) {
+                    const double bound = (double)proto.B / ((double)issue_ms * P * 1e-3) / 1e6;
+                    if (bound < 0.8 * zc_rate) break;                // cannot win: skip the timed runs
+                }
             }
             const float eff_ms = std::max(best, best_issue * (float)P);
-            const float rate = best < 1e29f ? (float)((double)proto.B / (eff_ms * 1e-3) / 1e6) : 0.f;
+            rate_of[c] = best < 1e29f ? (float)((double)proto.B / (eff_ms * 1e-3) / 1e6) : 0.f;
+            if (m == MMA_HOP_ZC) zc_rate = rate_of[c];
+        }
+        float best_rate = 0.f;
+        for (size_t c = 0; c < cands.size(); c++) {
             // a candidate that uses more SMs must win by 2%: on a near-tie the path keeps its SMs
             // free (§3.4.3) and the run-to-run noise of one timed call cannot flip it
-            if (rate > best_rate * (best_rate > 0.f ? 1.02f : 1.0f)) {
-                best_rate = rate;
-                modes[p] = m;
-                mbps[p] = (uint32_t)llround(rate);
+            if (rate_of[c] > best_rate * (best_rate > 0.f ? 1.02f : 1.0f)) {
+                best_rate = rate_of[c];
+                modes[p] = cands[c];
+                mbps[p] = (uint32_t)llround(rate_of[c]);
             }
         }
     }
