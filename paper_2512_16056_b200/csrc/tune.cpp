@@ -121,7 +121,8 @@ static int tune_paths(Job proto, int reps, std::vector<uint32_t>& mbps, std::vec
                     best = std::min(best, ms);
                     best_issue = std::min(best_issue, issue_ms);
                 }
-                if (rep == 0 && m != MMA_HOP_ZC && zc_rate > 0.f) {
+                // (only a long issue counts: a first use may spend a few ms creating the ring)
+                if (rep == 0 && m != MMA_HOP_ZC && zc_rate > 0.f && issue_ms >= 50.f) {
                     const double bound = (double)proto.B / ((double)issue_ms * P * 1e-3) / 1e6;
                     if (bound < 0.8 * zc_rate) break;                // cannot win: skip the timed runs
                 }
