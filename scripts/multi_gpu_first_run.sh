@@ -25,5 +25,10 @@ timeout 900 $NCU --set full --metrics nvlrx__bytes.sum,nvltx__bytes.sum,pcie__re
     -k regex:relay -c 8 -f -o $out/prof_relay_peer python scripts/ncu_relay_protocol.py --peers > $out/ncu_relay_peer.log 2>&1
 echo "ncu relay (peer) rc=$?"
 ./scripts/probe/probe_relay bulk > $out/probe_relay_bulk.txt 2>&1
+# do waiting CTAs that poll a PEER's memory over NVLink slow the target's copy engine the way
+# host-memory polls do (DESIGN §5 item 12)? mode "peer flag" rows
+[ -x scripts/probe/probe_spin_ce ] || nvcc -O3 -std=c++17 -gencode arch=compute_100a,code=sm_100a \
+    -o scripts/probe/probe_spin_ce scripts/probe/probe_spin_ce.cu
+./scripts/probe/probe_spin_ce > $out/probe_spin_ce.txt 2>&1
 tail -3 $out/peer.log $out/gpu_all.log
 for k in 2 4 8; do [ -f $out/bench_n$k.json ] && tail -c 400 $out/bench_n$k.json; done

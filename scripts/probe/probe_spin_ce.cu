@@ -20,8 +20,8 @@ __device__ __forceinline__ uint64_t gtimer()
 
 // mode 0: nanosleep only (bounded by a timer), 1: ld.relaxed.sys of a device flag + sleep,
 // 2: ld.acquire.sys of a device flag + sleep, 3: volatile read of a mapped host flag + sleep,
-// 4: no thread-0 loop: every thread parked at a barrier behind a thread that sleeps in
-// one long nanosleep chain without memory reads
+// 4 (two or more GPUs): ld.relaxed.sys of a flag in GPU 1's memory over NVLink + sleep -- the
+// H2D pull kernel's seq polls in the peer form (to be measured on a multi-GPU box)
 __global__ void __launch_bounds__(512) waiter(int mode, const uint64_t* dflag, const volatile int* hflag, uint64_t ns_budget)
 {
     if (threadIdx.x == 0) {
@@ -31,6 +31,7 @@ __global__ void __launch_bounds__(512) waiter(int mode, const uint64_t* dflag, c
             if (mode == 1) asm volatile("ld.relaxed.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(dflag) : "memory");
             else if (mode == 2) asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(dflag) : "memory");
             else if (mode == 3) v = *hflag;
+            else if (mode == 4) asm volatile("ld.relaxed.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(dflag) : "memory");
             if (v) break;
             if (gtimer() - t0 > ns_budget) break;
             __nanosleep(500);
@@ -57,14 +58,30 @@ int main()
     cudaEvent_t a, b;
     CK(cudaEventCreate(&a));
     CK(cudaEventCreate(&b));
-    const char* names[] = {"nanosleep only", "ld.relaxed.sys dev flag", "ld.acquire.sys dev flag", "volatile host flag"};
+    const char* names[] = {"nanosleep only", "ld.relaxed.sys dev flag", "ld.acquire.sys dev flag", "volatile host flag",
+                           "ld.relaxed.sys peer flag"};
+    int ngpu = 0;
+    CK(cudaGetDeviceCount(&ngpu));
+    uint64_t* pflag = nullptr;                      // a flag in GPU 1's memory (peer form)
+    if (ngpu > 1) {
+        int ok = 0;
+        CK(cudaDeviceCanAccessPeer(&ok, 0, 1));
+        if (ok) {
+            CK(cudaDeviceEnablePeerAccess(1, 0));
+            CK(cudaSetDevice(1));
+            CK(cudaMalloc(&pflag, 64));
+            CK(cudaMemset(pflag, 0, 64));
+            CK(cudaDeviceSynchronize());
+            CK(cudaSetDevice(0));
+        }
+    }
     for (int dir = 0; dir < 2; dir++) {
-        for (int mode = 0; mode < 4; mode++) {
+        for (int mode = 0; mode < (pflag ? 5 : 4); mode++) {
             for (int n : {0, 16, 56, 112, 148}) {
                 if (n == 0 && mode > 0) continue;
                 float best = 1e9;
                 for (int rep = 0; rep < 3; rep++) {
-                    if (n) waiter<<<n, 512, 0, sk>>>(mode, dflag, hflag, 400000000ull);   // <= 0.4 s
+                    if (n) waiter<<<n, 512, 0, sk>>>(mode, mode == 4 ? pflag : dflag, hflag, 400000000ull);   // <= 0.4 s
                     CK(cudaEventRecord(a, sc));
                     CK(cudaMemcpyAsync(dir ? h : d, dir ? d : h, B, dir ? cudaMemcpyDeviceToHost : cudaMemcpyHostToDevice, sc));
                     CK(cudaEventRecord(b, sc));
