@@ -36,6 +36,10 @@ struct RingArg {
     uint64_t* credit;
     unsigned* cnt;               // [S] units finished of the slot's current chunk
     unsigned long long* cursor;  // monotone unit-claim cursor
+    // [S] on the kernel's GPU: the flag value the leader of the slot's current chunk (the CTA
+    // holding its first unit) saw satisfied; the other CTAs of the chunk wait on this LOCAL
+    // word instead of polling the flag, which may live in a peer's memory across NVLink
+    uint64_t* ready;
     uint64_t g0;                 // global ring index of this call's first chunk
     unsigned long long unit0;    // cursor value when this call's kernel starts
     ChunkListArg chunks;

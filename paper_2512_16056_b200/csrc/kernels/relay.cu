@@ -43,6 +43,7 @@ __device__ __forceinline__ void ring_abort(const RelayLaunchArg& A, const RingAr
     for (uint32_t s = 0; s < R.S; s++) {
         publish(&R.credit[s], kReleaseAll);
         publish(&R.seq[s], kReleaseAll);
+        if (R.ready) publish(&R.ready[s], kReleaseAll);   // releases the chunk's followers
     }
 }
 
@@ -202,9 +203,22 @@ __device__ __forceinline__ void relay_body(const RelayLaunchArg& A)
         if (threadIdx.x == 0) {
             bool ok;
             uint64_t flag = 0;
+            // the chunk's leader (the CTA holding its first unit) polls the ring flag, which may
+            // live in a peer's memory, and passes the value it saw to the local ready word; the
+            // chunk's other CTAs wait on that word. Both waits have acquire semantics, and the
+            // leader's fence + atomicMax is a release at GPU scope, so a follower's slot reads
+            // are ordered after the staging write the leader observed. ready[s] is monotone
+            // like the flags: it can pass this chunk's value only after every unit of the chunk
+            // is done (the slot must drain before chunk g + S is staged).
+            const bool leader = (k == 0) || !R.ready;
+            const uint64_t* wflag = leader ? (PULL ? &R.seq[s] : &R.credit[s]) : R.ready + s;
             if (g == seen) ok = true;
-            else if (PULL) ok = spin_until(A, &R.seq[s], [g](uint64_t v) { return v == g + 1; }, &flag);
-            else ok = (g < R.S) || spin_until(A, &R.credit[s], [g, &R](uint64_t v) { return v >= g - R.S + 1; }, &flag);
+            else if (PULL) ok = spin_until(A, wflag, [g](uint64_t v) { return v == g + 1; }, &flag);
+            else ok = (g < R.S) || spin_until(A, wflag, [g, &R](uint64_t v) { return v >= g - R.S + 1; }, &flag);
+            if (ok && g != seen && leader && R.ready && (PULL || g >= R.S)) {
+                __threadfence();
+                atomicMax(reinterpret_cast<unsigned long long*>(R.ready + s), (unsigned long long)flag);
+            }
             if (g != seen && A.fwd) {   // the observation the forward (pack) of chunk i rests on
                 A.fwd[2 * i] = flag;
                 A.fwd[2 * i + 1] = g + 1;

@@ -475,9 +475,12 @@ int get_ring(int d, int dir, int p, uint64_t C, uint32_t S, bool push, Ring** ou
         }
         {
             DeviceGuard g(kdev);
-            CK(cudaMalloc(&r.cnt, 64 * sizeof(unsigned) + 64));
-            CK(cudaMemsetAsync(r.cnt, 0, 64 * sizeof(unsigned) + 64, e.dev[kdev].setup));
+            // unit counters [64], the claim cursor, the leaders' observed flags [64]
+            const size_t bytes = 64 * sizeof(unsigned) + 64 + 64 * sizeof(uint64_t);
+            CK(cudaMalloc(&r.cnt, bytes));
+            CK(cudaMemsetAsync(r.cnt, 0, bytes, e.dev[kdev].setup));
             r.cursor = (unsigned long long*)((char*)r.cnt + 64 * sizeof(unsigned));
+            r.ready = (uint64_t*)((char*)r.cnt + 64 * sizeof(unsigned) + 64);
         }
         CK(cudaStreamSynchronize(e.dev[relay].setup));
         CK(cudaStreamSynchronize(e.dev[kdev].setup));
@@ -1735,6 +1738,7 @@ private:
             R.credit = r->credit;
             R.cnt = r->cnt;
             R.cursor = r->cursor;
+            R.ready = r->ready;
             R.g0 = g0[p] + w0;
             R.unit0 = r->unit_next;
             R.chunks = chunks_on(p, kd);

@@ -106,6 +106,7 @@ struct Ring {
     uint64_t* credit = nullptr;      // relay-local
     unsigned* cnt = nullptr;         // on kdev
     unsigned long long* cursor = nullptr;   // on kdev
+    uint64_t* ready = nullptr;              // on kdev: [64] leader-observed flag per slot
     uint64_t g_next = 0;             // chunks carried so far (reading R18)
     unsigned long long unit_next = 0;
     // a call failed part-way through this ring's enqueue: its flags and counters may be out

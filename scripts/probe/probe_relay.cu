@@ -111,6 +111,7 @@ int main(int argc, char** argv)
             R.credit = rm[r].flags + 64;
             R.cnt = rm[r].cnt;
             R.cursor = (unsigned long long*)((char*)rm[r].cnt + 64 * sizeof(unsigned));
+            R.ready = nullptr;   // every CTA polls the ring flag itself (flags are local here)
             R.g0 = 0;
             R.unit0 = 0;
             R.chunks.count = S;
