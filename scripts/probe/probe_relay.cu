@@ -28,7 +28,7 @@ static bool g_bulk = false;   // the cp.async.bulk form of the relay kernels
 struct RingMem {
     char* stage;
     uint64_t* flags;     // seq[64], credit[64]
-    unsigned* cnt;       // cnt[64] + cursor
+    unsigned* cnt;       // cnt[64] + cursor + ready[64] (the engine's layout, plane.cpp get_ring)
 };
 
 int main(int argc, char** argv)
@@ -46,7 +46,7 @@ int main(int argc, char** argv)
         CK(cudaMalloc(&r.stage, per_ring));
         CK(cudaMemset(r.stage, 0x5A, per_ring));
         CK(cudaMalloc(&r.flags, 128 * sizeof(uint64_t)));
-        CK(cudaMalloc(&r.cnt, 64 * sizeof(unsigned) + 64));
+        CK(cudaMalloc(&r.cnt, 64 * sizeof(unsigned) + 64 + 64 * sizeof(uint64_t)));
     }
     int* err;
     CK(cudaHostAlloc(&err, 64, cudaHostAllocMapped));
@@ -111,7 +111,7 @@ int main(int argc, char** argv)
             R.credit = rm[r].flags + 64;
             R.cnt = rm[r].cnt;
             R.cursor = (unsigned long long*)((char*)rm[r].cnt + 64 * sizeof(unsigned));
-            R.ready = nullptr;   // every CTA polls the ring flag itself (flags are local here)
+            R.ready = (uint64_t*)((char*)rm[r].cnt + 64 * sizeof(unsigned) + 64);   // leaders / followers
             R.g0 = 0;
             R.unit0 = 0;
             R.chunks.count = S;
@@ -123,7 +123,7 @@ int main(int argc, char** argv)
             // reset the ring: seq pre-published (pull) / all zero (pack), counters zero
             if (cudaMemcpy(rm[r].flags, pull ? seqs.data() : std::vector<uint64_t>(128, 0).data(),
                            128 * sizeof(uint64_t), cudaMemcpyHostToDevice)) return 1;
-            if (cudaMemset(rm[r].cnt, 0, 64 * sizeof(unsigned) + 64)) return 1;
+            if (cudaMemset(rm[r].cnt, 0, 64 * sizeof(unsigned) + 64 + 64 * sizeof(uint64_t))) return 1;
         }
         A.nrings = rings;
         cudaEventRecord(a, st);
