@@ -31,9 +31,19 @@ constexpr uint64_t kReleaseAll = 1ull << 62;
 // Flags the kernel publishes only ever grow (atomicMax after a system fence = a release
 // that cannot move a flag backwards), so once a ring is aborted every copy-engine wait on
 // it passes even if a CTA still finishing a chunk publishes afterwards.
+#ifndef MMA_PUBLISH_SC
+#define MMA_PUBLISH_SC 0
+#endif
 __device__ __forceinline__ void publish(uint64_t* flag, uint64_t v)
 {
+    // a release at system scope (the flag's readers include the copy engines' stream memory
+    // operations and other GPUs): fence.acq_rel.sys + the relaxed atomic is the PTX release
+    // pattern; MMA_PUBLISH_SC=1 builds the stronger fence.sc.sys (__threadfence_system)
+#if MMA_PUBLISH_SC
     __threadfence_system();
+#else
+    asm volatile("fence.acq_rel.sys;" ::: "memory");
+#endif
     atomicMax_system(reinterpret_cast<unsigned long long*>(flag), (unsigned long long)v);
 }
 
