@@ -17,13 +17,15 @@ import paper_2512_16056_b200 as mma  # noqa: E402
 K = int(os.environ.get("RINGS", "7"))
 CTAS = int(os.environ.get("CTAS", "16"))
 MiB = 1 << 20
+CHUNK = int(os.environ.get("CHUNK", str(8 * MiB)))
+RING_ONLY = os.environ.get("RING_ONLY") == "1"          # the direct path gets no chunk
 torch.cuda.set_device(0)
 s = torch.cuda.Stream()
 B = 1 << 30
 host = torch.empty(B, dtype=torch.uint8).pin_memory()
 dev = torch.empty(B, dtype=torch.uint8, device="cuda")
 cfg = mma.default_config()
-cfg.chunk_bytes[0] = cfg.chunk_bytes[1] = 8 * MiB
+cfg.chunk_bytes[0] = cfg.chunk_bytes[1] = CHUNK
 cfg.fallback_bytes[0] = cfg.fallback_bytes[1] = 0
 cfg.loopback_relays = K
 cfg.npaths, cfg.path_gpus[0] = 1, 0
@@ -32,7 +34,7 @@ cfg.debug_log = 0
 mma.init(cfg)
 for d in (mma.H2D, mma.D2H):
     mma.set_path_modes(0, d, [mma.HOP_CE] * (K + 1))
-    mma.set_bandwidth(0, d, [1] * (K + 1))
+    mma.set_bandwidth(0, d, [0 if RING_ONLY else 1] + [1] * K)
 mma.memcpy_h2d(dev, host, B, stream=s)
 mma.memcpy_d2h(host, dev, B, stream=s)
 s.synchronize()
@@ -43,7 +45,7 @@ for name, fn in (("h2d", lambda: mma.memcpy_h2d(dev, host, B, stream=s)),
     mma.trace_begin()
     fn()
     s.synchronize()
-    p = out / f"trace_rings_{name}_k{K}_c{CTAS}.json"
+    p = out / f"trace_rings_{name}_k{K}_c{CTAS}_C{CHUNK >> 20}M{'_ringonly' if RING_ONLY else ''}.json"
     n = mma.trace_end(str(p))
     ev = json.load(open(p))["traceEvents"]
     t0 = min(e["ts"] for e in ev)
@@ -55,7 +57,8 @@ for name, fn in (("h2d", lambda: mma.memcpy_h2d(dev, host, B, stream=s)),
         r[1] += 1
         if len(r[2]) < 6:
             r[2].append((e["name"][:28], round(e["ts"] - t0, 1), round(e["dur"], 1)))
-    print(json.dumps({"dir": name, "rings": K, "ctas": CTAS, "span_us": round(t1 - t0, 1), "spans": n,
+    print(json.dumps({"dir": name, "rings": K, "ctas": CTAS, "chunk": CHUNK, "ring_only": RING_ONLY,
+                      "gbps": round(B / (t1 - t0) / 1e3, 2), "span_us": round(t1 - t0, 1), "spans": n,
                       "rows": {k: {"busy_us": round(v[0], 1), "n": v[1], "first": v[2]} for k, v in rows.items()}}),
           flush=True)
 assert mma.get_last_error() == 0
