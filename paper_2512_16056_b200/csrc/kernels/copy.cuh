@@ -129,17 +129,74 @@ __device__ __forceinline__ void v_copy(const VStreamArg& v, uint64_t a, uint64_t
         else cta_copy(d, buf, b - a);
         return;
     }
-    for (uint64_t k = v_find(v, a); k < v.nseg; k++) {
+    // piece k of v clipped to [a, b): its source, destination and length for this MODE
+    auto piece = [&](uint64_t k, const char** s, char** d) -> uint64_t {
         const uint64_t vk = v.start[k], vk1 = v.start[k + 1];
-        if (vk >= b) break;
         const uint64_t lo = vk > a ? vk : a;
         const uint64_t hi = vk1 < b ? vk1 : b;
-        if (lo >= hi) continue;
-        const char* s = reinterpret_cast<const char*>(v.src[k]) + (lo - vk);
-        char* d = reinterpret_cast<char*>(v.dst[k]) + (lo - vk);
-        if (MODE == V_DIRECT) cta_copy(d, s, hi - lo);
-        else if (MODE == V_PACK) cta_copy(buf + (lo - a), s, hi - lo);
-        else cta_copy(d, buf + (lo - a), hi - lo);
+        *s = nullptr;
+        *d = nullptr;
+        if (lo >= hi) return 0;                      // an empty segment
+        *s = MODE == V_UNPACK ? buf + (lo - a) : reinterpret_cast<const char*>(v.src[k]) + (lo - vk);
+        *d = MODE == V_PACK ? buf + (lo - a) : reinterpret_cast<char*>(v.dst[k]) + (lo - vk);
+        return hi - lo;
+    };
+#ifdef MMA_NO_GROUP
+    constexpr bool kGroupPieces = false;   // probe builds: one piece per round (scripts/probe_duplex_grid.py)
+#else
+    constexpr bool kGroupPieces = true;
+#endif
+    constexpr uint64_t kRound = (uint64_t)kThreads * kUnroll * 16;   // bytes one round keeps in flight
+    uint64_t k = v_find(v, a);
+    while (k < v.nseg && v.start[k] < b) {
+        // Small pieces (a 32 KiB paged-KV segment fills half a round) are grouped: the group's
+        // loads all issue before any store, so a CTA keeps a full round in flight across piece
+        // boundaries instead of one piece (under full-duplex load a host read's round trip
+        // grows, and bytes in flight per SM bound the rate: scripts/probe_duplex_grid.py).
+        // A group is consecutive pieces, each 16-byte aligned at both ends with a length
+        // that is a multiple of 16, kMaxGroup at most, a round of bytes at most. Only the
+        // zero-copy kernels group (V_DIRECT: their loads cross PCIe); in the relay kernels the
+        // group's walk state spills at their 128-register bound, and their loads stay on-GPU.
+        constexpr uint64_t kMaxGroup = 16;
+        uint64_t k2 = k, tot = 0;
+        for (; MODE == V_DIRECT && kGroupPieces && k2 < v.nseg && k2 - k < kMaxGroup && v.start[k2] < b; k2++) {
+            const char* s;
+            char* d;
+            const uint64_t n = piece(k2, &s, &d);
+            if (tot + n > kRound || ((reinterpret_cast<uintptr_t>(s) | reinterpret_cast<uintptr_t>(d) | n) & 15)) break;
+            tot += n;
+        }
+        if (k2 - k >= 2) {
+            const uint64_t nv = tot >> 4;
+            uint4 r[kUnroll];
+            // each phase walks the group's pieces once (i grows with u); the store phase walks
+            // again rather than keeping kUnroll destination pointers live across the loads
+            for (int phase = 0; phase < 2; phase++) {
+                uint64_t p = k, pbase = 0;      // piece p holds group vectors [pbase, pbase + pn)
+                const char* ps;
+                char* pd;
+                uint64_t pn = piece(p, &ps, &pd) >> 4;
+#pragma unroll
+                for (int u = 0; u < kUnroll; u++) {
+                    const uint64_t i = (uint64_t)u * kThreads + threadIdx.x;
+                    if (i < nv) {
+                        while (i >= pbase + pn) {
+                            pbase += pn;
+                            pn = piece(++p, &ps, &pd) >> 4;
+                        }
+                        if (phase == 0) r[u] = __ldcg(reinterpret_cast<const uint4*>(ps) + (i - pbase));
+                        else __stcg(reinterpret_cast<uint4*>(pd) + (i - pbase), r[u]);
+                    }
+                }
+            }
+            k = k2;
+            continue;
+        }
+        const char* s;
+        char* d;
+        const uint64_t n = piece(k, &s, &d);
+        if (n) cta_copy(d, s, n);
+        k++;
     }
 }
 

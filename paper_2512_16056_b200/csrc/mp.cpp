@@ -97,13 +97,19 @@ void CUDART_CB release_share(void* p)
     delete r;
 }
 
+// direction of a segment table from the memory kinds: a device source is an offload (D2H)
+static int seg_dir(const mma_segment_t* segs)
+{
+    cudaPointerAttributes a;
+    if (cudaPointerGetAttributes(&a, segs[0].src) == cudaSuccess && a.type == cudaMemoryTypeDevice) return MMA_D2H;
+    return MMA_H2D;
+}
+
 int ledger_share(const mma_segment_t* segs, int device, uint64_t bytes, bool own, cudaStream_t s)
 {
     const int slot = shm_ledger_slot(device);
     if (slot < 0 || !bytes) return cudaSuccess;
-    cudaPointerAttributes a;
-    int dir = MMA_H2D;
-    if (cudaPointerGetAttributes(&a, segs[0].src) == cudaSuccess && a.type == cudaMemoryTypeDevice) dir = MMA_D2H;
+    const int dir = seg_dir(segs);
     cudaGetLastError();
     LedgerRelease* r = new LedgerRelease{dir, slot, (int64_t)bytes, own ? (int64_t)bytes : 0, shm_ledger_gen()};
     shm_ledger_add_slot(dir, slot, r->bytes, r->own, r->gen);
@@ -300,7 +306,7 @@ int mma_copy_share_segments(const mma_segment_t* segs, size_t nsegs, size_t chun
             a.unit_bytes = e.unit_bytes;
             a.path = (uint32_t)path;
             const uint64_t upc = (v.C + e.unit_bytes - 1) / e.unit_bytes;
-            const unsigned grid = (unsigned)std::min<uint64_t>(mine.size() * upc, zc_grid(device));
+            const unsigned grid = (unsigned)std::min<uint64_t>(mine.size() * upc, zc_grid(device, seg_dir(segs)));
             KTimer kt(device, s, 0 | (path << 8));
             rc = launch_zc(a, grid, s);
             cudaFreeAsync(dlist, s);
@@ -334,10 +340,7 @@ int mma_copy_share_segments_ring(const mma_segment_t* segs, size_t nsegs, size_t
     uint64_t C = chunk_bytes;
     if ((B + C - 1) / C != nchunks && !(nchunks == 1 && B > 0)) return cudaErrorInvalidValue;
     if (nchunks == 1) C = B;                   // a one-piece (fallback) plan
-    // direction from the memory kinds: a device source is an offload (D2H)
-    cudaPointerAttributes a;
-    int dir = MMA_H2D;
-    if (cudaPointerGetAttributes(&a, segs[0].src) == cudaSuccess && a.type == cudaMemoryTypeDevice) dir = MMA_D2H;
+    const int dir = seg_dir(segs);
     cudaGetLastError();
     CK(make_device(device));
     std::lock_guard<std::mutex> lk(g_mp_mu);
@@ -403,7 +406,7 @@ int mma_copy_claim_segments(const mma_segment_t* segs, size_t nsegs, size_t clai
     a.cursor = (unsigned long long*)cursor;
     a.counts = (unsigned long long*)counts;
     a.path = (uint32_t)path;
-    const unsigned grid = (unsigned)std::min<uint64_t>(a.nchunks, zc_grid(device));
+    const unsigned grid = (unsigned)std::min<uint64_t>(a.nchunks, zc_grid(device, seg_dir(segs)));
     int rc = cudaSuccess;
     if (a.nchunks) {
         KTimer kt(device, s, 3 | (path << 8));

@@ -188,11 +188,13 @@ uint32_t ring_slots_for(uint64_t C)
     return (uint32_t)std::min<uint64_t>(32, std::max<uint64_t>(4, s));
 }
 
-uint64_t zc_grid(int d)
+uint64_t zc_grid(int d, int dir)
 {
     const Engine& e = E();
     const uint64_t cap = (uint64_t)e.dev[d].sms * 4;
-    const uint64_t want = e.cfg.zc_ctas > 0 ? (uint64_t)e.cfg.zc_ctas : (uint64_t)kDefaultZcCtas;
+    const int per_dir = (dir == MMA_H2D || dir == MMA_D2H) ? e.zc_ctas_dir[dir] : 0;
+    const uint64_t want = per_dir > 0 ? (uint64_t)per_dir
+                        : e.cfg.zc_ctas > 0 ? (uint64_t)e.cfg.zc_ctas : (uint64_t)kDefaultZcCtas;
     return std::min(want, cap);
 }
 
@@ -319,6 +321,8 @@ int do_init(const mma_config_t* cfg)
         e.group_bytes = env_size("MMA_GROUP_BYTES", kDefaultGroupBytes);
         e.hop_lanes = env_int("MMA_HOP_LANES", 2) == 1 ? 1 : 2;
         e.relay_bulk = env_int("MMA_RELAY_BULK", 0) != 0;
+        e.zc_ctas_dir[MMA_H2D] = std::max(0, env_int("MMA_ZC_CTAS_H2D", 0));
+        e.zc_ctas_dir[MMA_D2H] = std::max(0, env_int("MMA_ZC_CTAS_D2H", 0));
         if (const char* u = getenv("MMA_UPLOAD")) e.upload_by_kernel = strcmp(u, "ce") != 0;
         const char* f = getenv("MMA_FAULT_DROP_PUBLISH");
         e.fault_drop_publish = f ? atoll(f) : -1;
@@ -1512,13 +1516,13 @@ private:
             a.pause = slot + kDynPauseWord + p;
             if (eng_.cfg.background_policy == 1 && pp_[p].mbps) {   // yield to background traffic
                 a.yield_pct = eng_.cfg.yield_pct ? eng_.cfg.yield_pct : 150;
-                const uint64_t ctas = std::min<uint64_t>(n_log_, zc_grid(g));
+                const uint64_t ctas = std::min<uint64_t>(n_log_, zc_grid(g, j_.dir));
                 // ns one claim unit takes when the path's measured rate is split over its CTAs
                 a.expect_ns = claimC_ * ctas * 1000ull / pp_[p].mbps;
             }
             a.path = (uint32_t)p;
             a.log = log_;
-            const unsigned grid = (unsigned)std::min<uint64_t>(n_log_, zc_grid(g));
+            const unsigned grid = (unsigned)std::min<uint64_t>(n_log_, zc_grid(g, j_.dir));
             KTimer kt(g, s, 3 | (j_.dir << 4) | (p << 8));
             TSpan ts(g, s, "zero-copy dynamic pull", p, -1, 0);
             CK(launch_zc_dyn(a, grid, s));
@@ -1572,7 +1576,7 @@ private:
         a.log = log_;
         if (own) a.piece_chunk = private_chunks_on(p, g);   // the kernel logs each piece's chunk
         const uint64_t upc = (j_.C + eng_.unit_bytes - 1) / eng_.unit_bytes;
-        const unsigned grid = (unsigned)std::min<uint64_t>(a.chunks.count * upc, zc_grid(g));
+        const unsigned grid = (unsigned)std::min<uint64_t>(a.chunks.count * upc, zc_grid(g, j_.dir));
         DeviceGuard dg(g);
         {
             KTimer kt(g, s, 0 | (j_.dir << 4) | (p << 8));

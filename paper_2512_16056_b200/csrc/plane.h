@@ -206,6 +206,7 @@ struct Engine {
     uint64_t group_bytes = kDefaultGroupBytes;   // ring hop groups (plane.cpp group_chunks)
     int hop_lanes = 2;                           // relay hop streams per direction used (1 or 2)
     bool relay_bulk = false;                     // MMA_RELAY_BULK=1: the cp.async.bulk relay kernels
+    int zc_ctas_dir[2] = {0, 0};                 // MMA_ZC_CTAS_{H2D,D2H}: per-direction zero-copy grid (0 = cfg.zc_ctas)
     bool upload_by_kernel = true;    // MMA_UPLOAD=ce: table uploads by the copy engine
     // fault injection (tests only, MMA_FAULT_DROP_PUBLISH=g): the hop-1 publish of global
     // ring chunk g is never issued, so the relay kernel must time out, record the sticky
@@ -358,8 +359,9 @@ void apply_env(mma_config_t* c);
 void defaults(mma_config_t* c);
 int validate_cfg(const mma_config_t& c);
 int make_device(int d);
-// grid of a zero-copy path kernel on device d (cfg.zc_ctas, capped at 4 CTAs per SM)
-uint64_t zc_grid(int d);
+// grid of a zero-copy path kernel on device d moving direction dir (cfg.zc_ctas, or the
+// engine's per-direction grid; capped at 4 CTAs per SM)
+uint64_t zc_grid(int d, int dir);
 uint32_t ring_slots_for(uint64_t C);   // the ring depth for chunks of C bytes
 int do_init(const mma_config_t* cfg);
 int ensure_init();
