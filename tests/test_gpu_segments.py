@@ -137,6 +137,49 @@ def test_irregular_segments(mma, orc):
         assert np.array_equal(dev.cpu().numpy(), exp), (hop, lb, mode)
 
 
+@pytest.mark.parametrize("dirn", [0, 1], ids=["h2d", "d2h"])
+@pytest.mark.parametrize("C,lb,mode", [(64 << 10, 0, 0), (MiB, 2, 1), (192 << 10, 1, 2)])
+def test_small_piece_groups(mma, orc, dirn, C, lb, mode):
+    """The zero-copy kernels move runs of small 16-byte-friendly pieces as one round of loads
+    (copy.cuh v_copy piece groups): mixed lengths (empty, 16 B, 4080 B, 32 KiB, 64 KiB + 16,
+    odd), mostly 16-byte-aligned ends with some unaligned pieces breaking the groups, chunk
+    and unit edges inside pieces; direct, one-hop relay and dynamic-pull zero-copy paths."""
+    rng = np.random.default_rng(31 + dirn)
+    nseg = 1500
+    lens = rng.choice([0, 16, 32, 48, 4080, 4096, 8192, 32768, 65552, 7, 100], nseg,
+                      p=[.03, .1, .1, .07, .1, .1, .1, .2, .1, .05, .05]).astype(np.int64)
+    span_s = int(lens.sum()) * 2 + (1 << 20)
+    s_off = (rng.integers(0, span_s - 70000, nseg) // 16) * 16
+    bad = rng.random(nseg) < 0.08
+    s_off[bad] += rng.integers(1, 16, int(bad.sum()))
+    d_off = np.zeros(nseg, np.int64)
+    pos = 0
+    for k in rng.permutation(nseg):
+        d_off[k] = pos + (int(rng.integers(1, 16)) if rng.random() < 0.05 else 0)
+        pos = ((d_off[k] + int(lens[k]) + 15) // 16) * 16 + 16 * int(rng.integers(0, 3))
+    span_d = pos + 4096
+    configure(mma, loopback=lb, chunk=C, slots=2, plan_mode=mode, hop=(2, 2))
+    bw = [2] + [1] * lb
+    mma.set_bandwidth(0, dirn, bw)
+    pat = mma_inputs.pattern_bytes(57, span_s)
+    if dirn == 0:
+        src = torch.from_numpy(pat.copy()).pin_memory()
+        dst = torch.full((span_d,), 0xA5, dtype=torch.uint8, device="cuda")
+    else:
+        src = torch.from_numpy(pat.copy()).to("cuda")
+        dst = torch.full((span_d,), 0xA5, dtype=torch.uint8).pin_memory()
+    segs, n = mma.make_segments(src.data_ptr() + s_off, dst.data_ptr() + d_off, lens)
+    (mma.memcpy_h2d_segments if dirn == 0 else mma.memcpy_d2h_segments)(segs, n, 0)
+    torch.cuda.synchronize()
+    assert mma.get_last_error() == 0
+    B = int(lens.sum())
+    rc, path, _, _ = orc.plan(bw, B, C, 0, min(mode, 1))    # bytes do not depend on the plan
+    exp = np.full(span_d, 0xA5, np.uint8)
+    _oracle_segments(orc, pat, exp, s_off, d_off, lens, C, bw, path)
+    got = dst.cpu().numpy() if dirn == 0 else dst.numpy()
+    assert np.array_equal(got, exp)
+
+
 def test_overlapping_destinations_rejected(mma):
     configure(mma, loopback=0, chunk=MiB)
     host = torch.empty(MiB, dtype=torch.uint8).pin_memory()
