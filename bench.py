@@ -40,7 +40,7 @@ def _hbm_peak():
 
 
 HBM_PEAK = _hbm_peak()
-KNAMES = {0: "zc_copy_kernel", 1: "relay_pull_kernel", 2: "relay_pack_kernel", 3: "zc_dyn_kernel"}
+KNAMES = {0: "zc_copy_kernel", 1: "relay_pull_kernel", 2: "relay_pack_kernel", 3: "zc_dyn_kernel", 4: "zc_bulk_kernel"}
 MiB, GiB = 1 << 20, 1 << 30
 # PCIe bytes per payload byte of a native copy-engine 4 GiB copy on one B200 link (NVML
 # counters, profiles/r01_probe_nvml.json): 256-byte TLPs + DLLPs
@@ -617,9 +617,10 @@ def ncu_traffic(direction, kernel):
     """dram bytes per launch of the dominant kernel from the committed ncu capture
     (profiles/ncu_summary.json), or None when that kernel was not captured."""
     p = ROOT / "profiles" / "ncu_summary.json"
-    if p.exists() and kernel == "zc_copy_kernel":
+    if p.exists() and kernel in ("zc_copy_kernel", "zc_bulk_kernel"):
         try:
-            return json.loads(p.read_text()).get("dram_bytes_per_launch", {}).get(direction)
+            e = json.loads(p.read_text()).get("kernels", {}).get(f"{kernel}/{direction}")
+            return e.get("dram_bytes_per_launch") if e else None
         except (ValueError, AttributeError):
             return None
     return None
@@ -1274,7 +1275,7 @@ def main():
     # measured overhead (SM writes / read completions travel as 128-byte TLPs; the copy engine's as
     # 256-byte ones). A second denominator beside the link peak, derived from two counters.
     try:
-        if roof and roof["kernel"] == "zc_copy_kernel" and roof["path"] == 0 and isinstance(pcie_hw, dict):
+        if roof and roof["kernel"] in ("zc_copy_kernel", "zc_bulk_kernel") and roof["path"] == 0 and isinstance(pcie_hw, dict):
             rows = pcie_hw.get(roof["direction"]) or []
             kern_ratio = next((r["ratio"] for r in rows if r["gpu"] == roof["device"] and r["ratio"]), None)
             ce_ratio = CE_PCIE_OVERHEAD[roof["direction"]]

@@ -15,7 +15,7 @@ namespace mma {
 // bulk: the cp.async.bulk (TMA) form of the copy (contiguous 16-byte-aligned units)
 cudaError_t launch_relay(const RelayLaunchArg& a, bool pull, unsigned grid, cudaStream_t s, bool bulk = false);
 // kernels/zerocopy.cu
-cudaError_t launch_zc(const ZcLaunchArg& a, unsigned grid, cudaStream_t s);
+cudaError_t launch_zc(const ZcLaunchArg& a, unsigned grid, cudaStream_t s, bool bulk = false);
 cudaError_t launch_zc_dyn(const DynLaunchArg& a, unsigned grid, cudaStream_t s);
 // kernels/verify.cu
 cudaError_t launch_fill(void* p, uint64_t bytes, uint64_t seed, uint64_t offset, cudaStream_t s);

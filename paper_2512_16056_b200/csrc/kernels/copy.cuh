@@ -6,6 +6,7 @@
 // NVLink (~2 us) and PCIe latency (all loads of an unrolled group issue before any store),
 // and L1 bypass (.cg) for data another agent rewrites during the kernel (staging slots).
 #pragma once
+#include <cuda_runtime.h>
 #include <stdint.h>
 
 #include "../kargs.h"
@@ -44,6 +45,38 @@ __device__ __forceinline__ uint64_t globaltimer_ns()
     uint64_t t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
     return t;
+}
+
+// the dynamic shared memory a bulk kernel needs, allowed once per device (the attribute is set
+// per function on the current device: a kernel first launched on GPU 0 is not yet allowed it
+// on GPU 1); one instantiation (and flag set) per kernel
+template <auto* FN>
+inline bool allow_dyn_smem(int bytes)
+{
+    static bool done[64] = {};
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return false;
+    if (!done[dev]) done[dev] = cudaFuncSetAttribute(FN, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes) == cudaSuccess;
+    return done[dev];
+}
+
+// cp.async.bulk (TMA) helpers: a shared-memory tile filled from global memory (completing on
+// an mbarrier with the tile's byte count) and its wait
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void bulk_load(char* sbuf, const char* src, uint32_t n, uint64_t* bar)
+{
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(n) : "memory");
+    asm volatile("cp.async.bulk.shared::cta.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(smem_u32(sbuf)),
+                 "l"(src), "r"(n), "r"(smem_u32(bar))
+                 : "memory");
+}
+
+__device__ __forceinline__ void bulk_wait(uint64_t* bar, uint32_t parity)
+{
+    asm volatile("{ .reg .pred p; W: mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1; @!p bra W; }" ::"r"(smem_u32(bar)),
+                 "r"(parity)
+                 : "memory");
 }
 
 // Cooperative copy of len bytes by the whole CTA. 16-byte vectors when src and dst share

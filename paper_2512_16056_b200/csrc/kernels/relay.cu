@@ -121,23 +121,6 @@ __device__ __forceinline__ bool spin_until(const RelayLaunchArg& A, const uint64
 constexpr uint32_t kBulkTile = 32u << 10;
 constexpr int kBulkStages = 4;
 
-__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
-
-__device__ __forceinline__ void bulk_load(char* sbuf, const char* src, uint32_t n, uint64_t* bar)
-{
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(n) : "memory");
-    asm volatile("cp.async.bulk.shared::cta.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(smem_u32(sbuf)),
-                 "l"(src), "r"(n), "r"(smem_u32(bar))
-                 : "memory");
-}
-
-__device__ __forceinline__ void bulk_wait(uint64_t* bar, uint32_t parity)
-{
-    asm volatile("{ .reg .pred p; W: mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1; @!p bra W; }" ::"r"(smem_u32(bar)),
-                 "r"(parity)
-                 : "memory");
-}
-
 // thread 0 only: dst[0, len) = src[0, len); len % 16 == 0, both 16-byte aligned. *phase holds
 // one parity bit per stage (the barriers live as long as the CTA).
 __device__ __forceinline__ void bulk_copy(char* dst, const char* src, uint64_t len, char* smem, uint64_t* bar,
@@ -289,13 +272,8 @@ cudaError_t launch_relay(const RelayLaunchArg& a, bool pull, unsigned grid, cuda
     if (grid == 0) return cudaSuccess;
     if (bulk) {
         constexpr int smem = kBulkStages * kBulkTile;
-        static bool attr = [] {
-            return cudaFuncSetAttribute(relay_pull_bulk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) ==
-                       cudaSuccess &&
-                   cudaFuncSetAttribute(relay_pack_bulk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) ==
-                       cudaSuccess;
-        }();
-        if (!attr) return cudaErrorInvalidValue;
+        if (!(pull ? allow_dyn_smem<relay_pull_bulk_kernel>(smem) : allow_dyn_smem<relay_pack_bulk_kernel>(smem)))
+            return cudaErrorInvalidValue;
         if (pull) relay_pull_bulk_kernel<<<grid, kThreads, smem, s>>>(a);
         else relay_pack_bulk_kernel<<<grid, kThreads, smem, s>>>(a);
         return cudaGetLastError();

@@ -98,9 +98,161 @@ cudaError_t launch_zc_dyn(const DynLaunchArg& a, unsigned grid, cudaStream_t s)
     return cudaGetLastError();
 }
 
-cudaError_t launch_zc(const ZcLaunchArg& a, unsigned grid, cudaStream_t s)
+// ---- the bulk-copy (TMA) form of the zero-copy kernel (MMA_ZC_BULK=1): one warp per CTA,
+// lane 0 streams the CTA's units through kZcStages shared-memory tiles with cp.async.bulk
+// (global -> shared completing on an mbarrier, shared -> global in bulk groups), so a CTA
+// keeps up to kZcStages x 32 KiB of host reads (H2D) in flight with one issuing thread and a
+// few registers, where the vector kernel holds one 64 KiB round in the registers of an
+// SM's whole register file. Tiles that are not 16-byte aligned at both ends or not a multiple
+// of 16 bytes long are copied by the warp directly. Every lane runs the same tile generator
+// over the same table (broadcast loads), so control flow is warp-uniform.
+constexpr uint32_t kZcTile = 32u << 10;
+constexpr int kZcStages = 6;
+constexpr int kZcBulkThreads = 32;
+
+struct ZcTileGen {
+    const ZcLaunchArg& A;
+    uint64_t upc, nunits, u, x, b, k;
+    bool in_unit = false;
+    __device__ ZcTileGen(const ZcLaunchArg& a) : A(a)
+    {
+        upc = (A.v.C + A.unit_bytes - 1) / A.unit_bytes;
+        nunits = A.chunks.count * upc;
+        u = blockIdx.x;
+    }
+    // the next unit's v range [x, b); logs the unit's chunk / pieces (lane 0 / the warp)
+    __device__ bool enter_unit()
+    {
+        const uint64_t U = A.unit_bytes, C = A.v.C, B = A.v.B;
+        for (; u < nunits; u += gridDim.x) {
+            const uint64_t j = u / upc, kk = u % upc;
+            const uint64_t i = chunk_index(A.chunks, j);
+            const uint64_t off = i * C;
+            const uint64_t len = (B - off < C) ? B - off : C;
+            const uint64_t lo = kk * U;
+            if (lo >= len) continue;
+            const uint64_t hi = (lo + U < len) ? lo + U : len;
+            x = off + lo;
+            b = off + hi;
+            k = A.v.nseg == 1 ? 0 : v_find(A.v, x);
+            if (A.log) {
+                if (!A.piece_chunk) {
+                    if (kk == 0 && threadIdx.x == 0) A.log[i] = (uint8_t)A.path;
+                } else if (A.v.nseg == 1) {
+                    if (threadIdx.x == 0) A.log[A.piece_chunk[0]] = (uint8_t)A.path;
+                } else {
+                    for (uint64_t q = k + threadIdx.x; q < A.v.nseg && A.v.start[q] < b; q += blockDim.x)
+                        A.log[A.piece_chunk[q]] = (uint8_t)A.path;
+                }
+            }
+            u += gridDim.x;
+            return true;
+        }
+        return false;
+    }
+    // next tile: src, dst, length (<= kZcTile); false when the CTA's units are done
+    __device__ bool next(const char** src, char** dst, uint32_t* n)
+    {
+        for (;;) {
+            if (!in_unit) {
+                if (!enter_unit()) return false;
+                in_unit = true;
+            }
+            if (x >= b) {
+                in_unit = false;
+                continue;
+            }
+            uint64_t vk = 0, end = b;
+            const char* s0;
+            char* d0;
+            if (A.v.nseg == 1) {
+                s0 = reinterpret_cast<const char*>(A.v.src0);
+                d0 = reinterpret_cast<char*>(A.v.dst0);
+            } else {
+                while (A.v.start[k + 1] <= x) k++;       // skip empty / finished pieces
+                vk = A.v.start[k];
+                if (A.v.start[k + 1] < end) end = A.v.start[k + 1];
+                s0 = reinterpret_cast<const char*>(A.v.src[k]);
+                d0 = reinterpret_cast<char*>(A.v.dst[k]);
+            }
+            const uint64_t m = (end - x < kZcTile) ? end - x : kZcTile;
+            *src = s0 + (x - vk);
+            *dst = d0 + (x - vk);
+            *n = (uint32_t)m;
+            x += m;
+            return true;
+        }
+    }
+};
+
+__global__ void __launch_bounds__(kZcBulkThreads) zc_bulk_kernel(const __grid_constant__ ZcLaunchArg A)
+{
+    extern __shared__ __align__(128) char s_tile[];
+    __shared__ __align__(8) uint64_t s_bar[kZcStages];
+    const bool lead = threadIdx.x == 0;
+    if (lead) {
+        for (int q = 0; q < kZcStages; q++)
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&s_bar[q])));
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncwarp();
+    ZcTileGen gen(A);
+    char* dst_of[kZcStages];          // lane 0: the destination and length of each stage's tile
+    uint32_t n_of[kZcStages];
+    uint32_t phase = 0;
+    uint64_t loaded = 0, stored = 0;   // bulk tiles whose load / store was issued
+    bool more = true;
+    // a tile for the next free stage: bulk tiles load into it, the others are copied now
+    auto fill = [&]() {
+        while (more) {
+            const char* s;
+            char* d;
+            uint32_t n;
+            if (!(more = gen.next(&s, &d, &n))) return;
+            if (((reinterpret_cast<uintptr_t>(s) | reinterpret_cast<uintptr_t>(d) | n) & 15) == 0) {
+                if (lead) {
+                    const int q = (int)(loaded % kZcStages);
+                    dst_of[q] = d;
+                    n_of[q] = n;
+                    bulk_load(s_tile + (uint64_t)q * kZcTile, s, n, &s_bar[q]);
+                }
+                loaded++;
+                return;
+            }
+            for (uint32_t t = threadIdx.x; t < n; t += kZcBulkThreads) d[t] = s[t];   // unaligned tile
+        }
+    };
+    for (int q = 0; q < kZcStages; q++) fill();
+    while (stored < loaded) {
+        if (lead) {
+            const int q = (int)(stored % kZcStages);
+            bulk_wait(&s_bar[q], (phase >> q) & 1);
+            phase ^= 1u << q;
+            asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst_of[q]),
+                         "r"(smem_u32(s_tile + (uint64_t)q * kZcTile)), "r"(n_of[q])
+                         : "memory");
+            asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        }
+        stored++;
+        // the previous tile's stage is free once its store has read it: refill it (after the
+        // first store no stage is free yet: the other K - 1 hold loads, this one the store)
+        if (more && stored >= 2) {
+            if (lead) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+            fill();
+        }
+    }
+    if (lead) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+
+cudaError_t launch_zc(const ZcLaunchArg& a, unsigned grid, cudaStream_t s, bool bulk)
 {
     if (grid == 0) return cudaSuccess;
+    if (bulk) {
+        constexpr int smem = kZcStages * kZcTile;
+        if (!allow_dyn_smem<zc_bulk_kernel>(smem)) return cudaErrorInvalidValue;
+        zc_bulk_kernel<<<grid, kZcBulkThreads, smem, s>>>(a);
+        return cudaGetLastError();
+    }
     zc_copy_kernel<<<grid, kThreads, 0, s>>>(a);
     return cudaGetLastError();
 }

@@ -308,7 +308,7 @@ int mma_copy_share_segments(const mma_segment_t* segs, size_t nsegs, size_t chun
             const uint64_t upc = (v.C + e.unit_bytes - 1) / e.unit_bytes;
             const unsigned grid = (unsigned)std::min<uint64_t>(mine.size() * upc, zc_grid(device, seg_dir(segs)));
             KTimer kt(device, s, 0 | (path << 8));
-            rc = launch_zc(a, grid, s);
+            rc = launch_zc(a, grid, s);   // the share's dst may be a peer's (IPC): vector form
             cudaFreeAsync(dlist, s);
         }
         if (rc == cudaSuccess) {   // this share's bytes, queued on this GPU's link

@@ -321,6 +321,7 @@ int do_init(const mma_config_t* cfg)
         e.group_bytes = env_size("MMA_GROUP_BYTES", kDefaultGroupBytes);
         e.hop_lanes = env_int("MMA_HOP_LANES", 2) == 1 ? 1 : 2;
         e.relay_bulk = env_int("MMA_RELAY_BULK", 0) != 0;
+        e.zc_bulk = env_int("MMA_ZC_BULK", 1) != 0;
         e.zc_ctas_dir[MMA_H2D] = std::max(0, env_int("MMA_ZC_CTAS_H2D", 0));
         e.zc_ctas_dir[MMA_D2H] = std::max(0, env_int("MMA_ZC_CTAS_D2H", 0));
         if (const char* u = getenv("MMA_UPLOAD")) e.upload_by_kernel = strcmp(u, "ce") != 0;
@@ -1579,9 +1580,10 @@ private:
         const unsigned grid = (unsigned)std::min<uint64_t>(a.chunks.count * upc, zc_grid(g, j_.dir));
         DeviceGuard dg(g);
         {
-            KTimer kt(g, s, 0 | (j_.dir << 4) | (p << 8));
+            const bool bulk = eng_.zc_bulk && !relay;   // the bulk kernel: direct paths (no peer addresses)
+            KTimer kt(g, s, (bulk ? 4 : 0) | (j_.dir << 4) | (p << 8));
             TSpan ts(g, s, relay ? "zero-copy one-hop relay kernel" : "zero-copy direct kernel", p, -1, bytes_p);
-            CK(launch_zc(a, grid, s));
+            CK(launch_zc(a, grid, s, bulk));
         }
         t_.stats.kernels++;
         if (j_.timing) j_.timing->end(p);

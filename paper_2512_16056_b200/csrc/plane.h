@@ -206,6 +206,7 @@ struct Engine {
     uint64_t group_bytes = kDefaultGroupBytes;   // ring hop groups (plane.cpp group_chunks)
     int hop_lanes = 2;                           // relay hop streams per direction used (1 or 2)
     bool relay_bulk = false;                     // MMA_RELAY_BULK=1: the cp.async.bulk relay kernels
+    bool zc_bulk = true;                         // MMA_ZC_BULK=0: direct zero-copy paths use the vector kernel
     int zc_ctas_dir[2] = {0, 0};                 // MMA_ZC_CTAS_{H2D,D2H}: per-direction zero-copy grid (0 = cfg.zc_ctas)
     bool upload_by_kernel = true;    // MMA_UPLOAD=ce: table uploads by the copy engine
     // fault injection (tests only, MMA_FAULT_DROP_PUBLISH=g): the hop-1 publish of global

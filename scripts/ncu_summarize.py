@@ -73,6 +73,13 @@ def kernel_entry(d, what, algo, source):
     return e
 
 
+def zc_name(d):
+    """zc_copy_kernel (vector form) or zc_bulk_kernel (cp.async.bulk form) from the row's kernel name"""
+    import re
+    m = re.search(r"(zc_\w+?_kernel)", d.get("Kernel Name", ("",))[0])
+    return m.group(1) if m else "zc_copy_kernel"
+
+
 def main():
     PROF.mkdir(exist_ok=True)
     summary = {"source": f"scripts/profile_round.sh on 1 x B200 (ncu --clock-control none), round {TAG}",
@@ -81,22 +88,22 @@ def main():
     if h2d.exists():
         (PROF / f"{TAG}_ncu_zc_h2d_details.csv").write_text(ncu_csv(h2d, "details"))
         d = raw_rows(h2d)[0]
-        e = kernel_entry(d, "SM zero-copy gather of the config-3 KV fetch (131072 x 32 KiB host segments -> "
+        e = kernel_entry(d, "SM zero-copy gather (" + zc_name(d) + ") of the config-3 KV fetch (131072 x 32 KiB host segments -> "
                             "paged device cache), one launch", KV_BYTES, f"profiles/{TAG}_ncu_zc_h2d_details.csv")
         e["note"] = ("HBM traffic ~= algorithmic (each payload byte written once; host reads cross PCIe, not "
                      "DRAM): no re-reads")
-        summary["kernels"]["zc_copy_kernel/h2d"] = e
+        summary["kernels"][f"{zc_name(d)}/h2d"] = e
         summary["dram_bytes_per_launch"]["h2d"] = e.get("dram_bytes_per_launch")
     d2h = OUT / "prof_zc_d2h.ncu-rep"
     if d2h.exists():
         (PROF / f"{TAG}_ncu_zc_d2h_metrics.csv").write_text(ncu_csv(d2h, "raw"))
         d = raw_rows(d2h)[0]
-        e = kernel_entry(d, "SM zero-copy scatter of the config-3 KV offload (paged device cache -> 131072 x "
+        e = kernel_entry(d, "SM zero-copy scatter (" + zc_name(d) + ") of the config-3 KV offload (paged device cache -> 131072 x "
                             "32 KiB host slots), one launch; application replay (host-writing kernels return nan "
                             "under kernel replay)", KV_BYTES, f"profiles/{TAG}_ncu_zc_d2h_metrics.csv")
         if e.get("pcie__write_bytes"):
             e["pcie_write_over_payload"] = round(e["pcie__write_bytes"] / KV_BYTES, 4)
-        summary["kernels"]["zc_copy_kernel/d2h"] = e
+        summary["kernels"][f"{zc_name(d)}/d2h"] = e
         summary["dram_bytes_per_launch"]["d2h"] = e.get("dram_bytes_per_launch")
     rel = OUT / "prof_relay.ncu-rep"
     if rel.exists():
