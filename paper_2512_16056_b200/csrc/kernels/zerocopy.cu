@@ -2,8 +2,9 @@
 // rows a7 and a10).
 //
 // The kernel runs on the path's GPU and moves the chunks that path carries directly
-// between mapped pinned host memory and device memory with 16-byte coalesced loads and
-// stores; nothing is staged. Launched on
+// between mapped pinned host memory and device memory -- zc_bulk_kernel (direct paths, the
+// default) through shared-memory tiles with cp.async.bulk, zc_copy_kernel with 16-byte
+// coalesced register loads and stores; no staging buffer in HBM. Launched on
 //   - the target GPU d: the direct path (H2D host->d HBM, D2H d HBM->host);
 //   - a relay GPU r: a one-hop relay (H2D: loads of host memory cross r's PCIe link,
 //     stores to d's HBM cross NVLink; D2H the reverse), which needs no ring and no flags.
