@@ -99,14 +99,16 @@ cudaError_t launch_zc_dyn(const DynLaunchArg& a, unsigned grid, cudaStream_t s)
     return cudaGetLastError();
 }
 
-// ---- the bulk-copy (TMA) form of the zero-copy kernel (MMA_ZC_BULK=1): one warp per CTA,
+// ---- the bulk-copy (TMA) form of the zero-copy kernel (direct paths; MMA_ZC_BULK=0: off): one warp per CTA,
 // lane 0 streams the CTA's units through kZcStages shared-memory tiles with cp.async.bulk
 // (global -> shared completing on an mbarrier, shared -> global in bulk groups), so a CTA
 // keeps up to kZcStages x 32 KiB of host reads (H2D) in flight with one issuing thread and a
 // few registers, where the vector kernel holds one 64 KiB round in the registers of an
 // SM's whole register file. Tiles that are not 16-byte aligned at both ends or not a multiple
-// of 16 bytes long are copied by the warp directly. Every lane runs the same tile generator
-// over the same table (broadcast loads), so control flow is warp-uniform.
+// of 16 bytes long keep their 16-byte-aligned middle on the bulk engine when source and
+// destination agree mod 16 (the warp copies the < 16-byte head and tail), else the warp copies
+// them. Every lane runs the same tile generator over the same table (broadcast loads), so
+// control flow is warp-uniform.
 constexpr uint32_t kZcTile = 32u << 10;
 constexpr int kZcStages = 6;
 constexpr int kZcBulkThreads = 32;
@@ -210,17 +212,63 @@ __global__ void __launch_bounds__(kZcBulkThreads) zc_bulk_kernel(const __grid_co
             char* d;
             uint32_t n;
             if (!(more = gen.next(&s, &d, &n))) return;
-            if (((reinterpret_cast<uintptr_t>(s) | reinterpret_cast<uintptr_t>(d) | n) & 15) == 0) {
+            const uintptr_t sa = reinterpret_cast<uintptr_t>(s), da = reinterpret_cast<uintptr_t>(d);
+            if (((sa ^ da) & 15) == 0) {
+                // same alignment mod 16: head and tail bytes (< 16 each) by the warp, the
+                // 16-byte-aligned middle by the bulk engine
+                const uint32_t head = min(n, (uint32_t)((16 - (sa & 15)) & 15));
+                const uint32_t mid = (n - head) & ~15u;
+                const uint32_t tail = n - head - mid;
+                if (threadIdx.x < head) d[threadIdx.x] = s[threadIdx.x];
+                if (threadIdx.x < tail) d[head + mid + threadIdx.x] = s[head + mid + threadIdx.x];
+                if (!mid) continue;
                 if (lead) {
                     const int q = (int)(loaded % kZcStages);
-                    dst_of[q] = d;
-                    n_of[q] = n;
-                    bulk_load(s_tile + (uint64_t)q * kZcTile, s, n, &s_bar[q]);
+                    dst_of[q] = d + head;
+                    n_of[q] = mid;
+                    bulk_load(s_tile + (uint64_t)q * kZcTile, s + head, mid, &s_bar[q]);
                 }
                 loaded++;
                 return;
             }
-            for (uint32_t t = threadIdx.x; t < n; t += kZcBulkThreads) d[t] = s[t];   // unaligned tile
+            // source and destination aligned differently mod 16: the warp copies the tile, with
+            // 4-byte words when they agree mod 4, kUnroll loads per lane in flight
+            if (((sa ^ da) & 3) == 0) {
+                const uint32_t head = min(n, (uint32_t)((4 - (sa & 3)) & 3));
+                if (threadIdx.x < head) d[threadIdx.x] = s[threadIdx.x];
+                const uint32_t nw = (n - head) >> 2;
+                const uint32_t* sw = reinterpret_cast<const uint32_t*>(s + head);
+                uint32_t* dw = reinterpret_cast<uint32_t*>(d + head);
+                for (uint32_t base = 0; base < nw; base += kZcBulkThreads * kUnroll) {
+                    uint32_t r[kUnroll];
+#pragma unroll
+                    for (int j = 0; j < kUnroll; j++) {
+                        const uint32_t i = base + j * kZcBulkThreads + threadIdx.x;
+                        if (i < nw) r[j] = __ldcg(sw + i);
+                    }
+#pragma unroll
+                    for (int j = 0; j < kUnroll; j++) {
+                        const uint32_t i = base + j * kZcBulkThreads + threadIdx.x;
+                        if (i < nw) __stcg(dw + i, r[j]);
+                    }
+                }
+                const uint32_t done = head + (nw << 2);
+                if (threadIdx.x < n - done) d[done + threadIdx.x] = s[done + threadIdx.x];
+            } else {
+                for (uint32_t base = 0; base < n; base += kZcBulkThreads * kUnroll) {
+                    char r[kUnroll];
+#pragma unroll
+                    for (int j = 0; j < kUnroll; j++) {
+                        const uint32_t i = base + j * kZcBulkThreads + threadIdx.x;
+                        if (i < n) r[j] = s[i];
+                    }
+#pragma unroll
+                    for (int j = 0; j < kUnroll; j++) {
+                        const uint32_t i = base + j * kZcBulkThreads + threadIdx.x;
+                        if (i < n) d[i] = r[j];
+                    }
+                }
+            }
         }
     };
     for (int q = 0; q < kZcStages; q++) fill();
