@@ -110,7 +110,10 @@ cudaError_t launch_zc_dyn(const DynLaunchArg& a, unsigned grid, cudaStream_t s)
 // them. Every lane runs the same tile generator over the same table (broadcast loads), so
 // control flow is warp-uniform.
 constexpr uint32_t kZcTile = 32u << 10;
-constexpr int kZcStages = 6;
+#ifndef MMA_ZC_STAGES
+#define MMA_ZC_STAGES 4
+#endif
+constexpr int kZcStages = MMA_ZC_STAGES;   // shared memory per CTA = kZcStages x kZcTile (4: 128 KiB; 3 loses 4% duplex, 6 gains nothing)
 constexpr int kZcBulkThreads = 32;
 
 struct ZcTileGen {
