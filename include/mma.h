@@ -114,10 +114,13 @@ typedef struct {
      * entry per claim. Small claims keep every link's share proportional to its speed
      * (the paper's outstanding-queue depth). 0 = default (256 KiB). */
     size_t claim_bytes;
-    /* CTAs (512 threads each) per zero-copy path kernel, planned or dynamic. A PCIe link
-     * saturates with 4 such CTAs (profiles/r01_probe_grid.txt), so a small grid leaves the
-     * relay GPU's other SMs to its own work (§3.4.3: relaying must not steal the
-     * peer's compute). 0 = default (16); at most 4 x the SM count. */
+    /* CTAs per zero-copy path kernel, planned or dynamic (the vector kernels: 512 threads;
+     * the cp.async.bulk kernel of direct paths: one warp and 128 KiB of shared memory). A
+     * PCIe link saturates with 4 vector CTAs (profiles/r01_probe_grid.txt), so a small grid
+     * leaves the relay GPU's other SMs to its own work (§3.4.3: relaying must not
+     * steal the peer's compute). 0 = default (16); at most 4 x the SM count. The environment
+     * variables MMA_ZC_CTAS_H2D / MMA_ZC_CTAS_D2H (read at the first init) override it per
+     * direction. */
     int zc_ctas;
     /* Concurrent calibration rounds (the bandwidth vector is "measured with
      * all paths of the set active"). After mma_calibrate / mma_tune_segments pick each
@@ -398,8 +401,9 @@ int mma_host_page_node(const void* ptr);
  * on the stream it is launched on. mma_kernel_times synchronises on the recorded launches,
  * returns their durations (ms) and tags in launch order (up to cap; *n = number recorded)
  * and clears the record. tag = kind | direction << 4 | path << 8 | device << 16, kind 0 =
- * zero-copy, 1 = relay pull (H2D), 2 = relay pack (D2H), 3 = dynamic-pull zero-copy;
- * path 255 = all rings of the launch. */
+ * zero-copy (vector kernel), 1 = relay pull (H2D), 2 = relay pack (D2H), 3 = dynamic-pull
+ * zero-copy, 4 = zero-copy (cp.async.bulk kernel, direct paths); path 255 = all rings of the
+ * launch. */
 int mma_set_kernel_timing(int on);
 int mma_kernel_times(float* ms, int* kinds, size_t cap, size_t* n);
 

@@ -547,7 +547,8 @@ def set_kernel_timing(on: bool) -> None:
 
 def kernel_times():
     """[(ms, kind)] of the kernel launches recorded since the last call (kind 0 zero-copy,
-    1 relay pull, 2 relay pack); synchronises on them."""
+    1 relay pull, 2 relay pack, 3 dynamic-pull zero-copy, 4 cp.async.bulk zero-copy);
+    synchronises on them."""
     n = C.c_size_t()
     cap = 1 << 16
     ms = (C.c_float * cap)()
