@@ -1,3 +1,7 @@
+#!/bin/bash
+# bench A/B of the current libmma.so against variants/libmma_prevbulk.so (the previous
+# commit's zerocopy.cu compiled against the current objects: nvcc -c <old zerocopy.cu>, then
+# link with paper_2512_16056_b200/build/*.o minus zerocopy.o, as in scripts/gpu_ab_group.sh)
 L=paper_2512_16056_b200/libmma.so
 cp $L /tmp/new.so
 for rep in 1 2; do for v in new prev; do
